@@ -1,0 +1,534 @@
+"""Parity checkers for the PQ / IVF hot path -- TEST INFRASTRUCTURE ONLY.
+
+Two CPU implementations live here, both built by ``oracle/Makefile``:
+
+* ``C``   -- ``oracle/pqii_oracle.c``, a plain-C restatement of the reference's
+  hot path (each function cites ``/root/reference/proj/<file>:<line>``).
+* ``REF`` -- ``oracle/_ref/libpqii_ref.so``, the reference's own sources
+  compiled as they lie plus ``oracle/ref_shim.cpp`` (extern "C" forwarding).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (cpu_baseline and
+``--impl reference``) may import this package.  The product package
+``paper_2604_21645_b200`` never does: it fails loudly without its CUDA library.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+C_LIB_PATH = os.path.join(HERE, "build", "liboracle.so")
+REF_LIB_PATH = os.path.join(HERE, "_ref", "libpqii_ref.so")
+
+_f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+_u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+_u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+_u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+_u64 = C.c_uint64
+_u32 = C.c_uint32
+
+
+def build() -> None:
+    """Compile the checkers (the C restatement always; _ref when the
+    reference sources are present)."""
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+def code_width(ks: int) -> int:
+    return 1 if ks <= 256 else 2
+
+
+class _Base:
+    def __init__(self, path: str, prefix: str):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} missing (run make -C oracle)")
+        self.lib = C.CDLL(path)
+        self.p = prefix
+
+    def fn(self, name, restype, argtypes):
+        f = getattr(self.lib, self.p + name)
+        f.restype = restype
+        f.argtypes = argtypes
+        return f
+
+
+class COracle(_Base):
+    """The C restatement (``pqii_oracle.c``)."""
+
+    def __init__(self, path: str = C_LIB_PATH):
+        super().__init__(path, "orc_")
+
+    def random_matrix(self, rows, dims, seed, lo=-1.0, hi=1.0):
+        out = np.empty((rows, dims), np.float32)
+        self.fn("random_matrix", None, [_u64, _u64, _u64, C.c_float, C.c_float, _f32p])(
+            rows, dims, seed, lo, hi, out)
+        return out
+
+    def uniform_indices(self, seed, n, k):
+        """The init index draws of kmeans_fit (kmeans.cpp:74-80)."""
+        out = np.empty(k, np.uint64)
+        self.fn("init_draws", None, [_u64, _u64, _u64, _u64p])(seed, n, k, out)
+        return out
+
+    def squared_l2(self, a, b):
+        a = np.ascontiguousarray(a, np.float32)
+        b = np.ascontiguousarray(b, np.float32)
+        return self.fn("squared_l2", C.c_double, [_f32p, _f32p, _u64])(a, b, a.size)
+
+    def nearest_batch(self, points, table):
+        points = np.ascontiguousarray(points, np.float32)
+        table = np.ascontiguousarray(table, np.float32)
+        n, d = points.shape
+        idx = np.empty(n, np.uint32)
+        dist = np.empty(n, np.float64)
+        self.fn("nearest_batch", None, [_f32p, _u64, _u64, _f32p, _u64, _u32p, _f64p])(
+            points, n, d, table, table.shape[0], idx, dist)
+        return idx, dist
+
+    def kmeans_fit(self, points, k, max_iters=20, seed=0, tol=1e-4):
+        points = np.ascontiguousarray(points, np.float32)
+        n, d = points.shape
+        cent = np.empty((k, d), np.float32)
+        assign = np.empty(n, np.uint32)
+        inertia = C.c_double()
+        iters = C.c_uint32()
+        per = np.zeros(max(1, max_iters), np.float64)
+        rc = self.fn("kmeans_fit", C.c_int,
+                     [_f32p, _u64, _u64, _u64, _u32, _u64, C.c_double, _f32p, _u32p,
+                      C.POINTER(C.c_double), C.POINTER(C.c_uint32), _f64p])(
+            points, n, d, k, max_iters, seed, tol, cent, assign, C.byref(inertia),
+            C.byref(iters), per)
+        if rc:
+            raise ValueError(f"kmeans_fit rc={rc}")
+        return dict(centroids=cent, assignments=assign, inertia=inertia.value,
+                    iterations_run=iters.value, inertia_per_iter=per[: iters.value].copy())
+
+    def pq_fit(self, data, M, ks, max_iters=20, seed=0):
+        data = np.ascontiguousarray(data, np.float32)
+        n, D = data.shape
+        if M == 0 or D % M:
+            raise ValueError("not divisible")
+        tables = np.empty((M, ks, D // M), np.float32)
+        iters = np.empty(M, np.uint32)
+        inert = np.empty(M, np.float64)
+        rc = self.fn("pq_fit", C.c_int, [_f32p, _u64, _u64, _u32, _u32, _u32, _u64, _f32p,
+                                         _u32p, _f64p])(
+            data, n, D, M, ks, max_iters, seed, tables, iters, inert)
+        if rc:
+            raise ValueError(f"pq_fit rc={rc}")
+        return tables, iters, inert
+
+    def pq_encode(self, data, tables):
+        data = np.ascontiguousarray(data, np.float32)
+        tables = np.ascontiguousarray(tables, np.float32)
+        M, ks, ds = tables.shape
+        n = data.shape[0]
+        codes = np.empty((n, M * code_width(ks)), np.uint8)
+        self.fn("pq_encode", None, [_f32p, _u64, _u32, _u32, _u32, _f32p, _u8p])(
+            data, n, M, ks, ds, tables, codes)
+        return codes
+
+    def pq_decode(self, codes, tables):
+        tables = np.ascontiguousarray(tables, np.float32)
+        codes = np.ascontiguousarray(codes, np.uint8)
+        M, ks, ds = tables.shape
+        n = codes.shape[0]
+        out = np.empty((n, M * ds), np.float32)
+        rc = self.fn("pq_decode", C.c_int, [_u8p, _u64, _u32, _u32, _u32, _f32p, _f32p])(
+            codes, n, M, ks, ds, tables, out)
+        if rc == -2:
+            raise IndexError("pq_decode: code out of range")
+        return out
+
+    def rmse(self, a, b):
+        a = np.ascontiguousarray(a, np.float32)
+        b = np.ascontiguousarray(b, np.float32)
+        return self.fn("rmse", C.c_double, [_f32p, _f32p, _u64, _u64])(a, b, a.shape[0], a.shape[1])
+
+    def adc_table(self, tables, query):
+        tables = np.ascontiguousarray(tables, np.float32)
+        M, ks, ds = tables.shape
+        out = np.empty((M, ks), np.float32)
+        self.fn("adc_table", None, [_f32p, _u32, _u32, _u32, _f32p, _f32p])(
+            tables, M, ks, ds, np.ascontiguousarray(query, np.float32), out)
+        return out
+
+    def adc_lookup_all(self, entries, codes):
+        entries = np.ascontiguousarray(entries, np.float32)
+        codes = np.ascontiguousarray(codes, np.uint8)
+        M, ks = entries.shape
+        f = self.fn("adc_lookup", C.c_int, [_f32p, _u32, _u32, _u8p, _u64, C.POINTER(C.c_double)])
+        out = np.empty(codes.shape[0], np.float64)
+        v = C.c_double()
+        for i in range(codes.shape[0]):
+            if f(entries, M, ks, codes, i, C.byref(v)):
+                raise IndexError("adc_lookup: code out of range")
+            out[i] = v.value
+        return out
+
+    def ivf_assign(self, codes, tables, coarse):
+        codes = np.ascontiguousarray(codes, np.uint8)
+        tables = np.ascontiguousarray(tables, np.float32)
+        coarse = np.ascontiguousarray(coarse, np.float32)
+        M, ks, ds = tables.shape
+        n = codes.shape[0]
+        out = np.empty(n, np.uint32)
+        rc = self.fn("ivf_assign", C.c_int,
+                     [_u8p, _u64, _u32, _u32, _u32, _f32p, _f32p, _u64, _u32p])(
+            codes, n, M, ks, ds, tables, coarse, coarse.shape[0], out)
+        if rc:
+            raise ValueError(f"ivf_assign rc={rc}")
+        return out
+
+    def ivf_csr(self, list_of, ids, codes, nlist):
+        codes = np.ascontiguousarray(codes, np.uint8)
+        n, rb = codes.shape
+        offsets = np.empty(nlist + 1, np.uint64)
+        out_ids = np.empty(n, np.uint64)
+        out_codes = np.empty_like(codes)
+        self.fn("ivf_csr", None, [_u32p, _u64p, _u8p, _u64, _u64, _u64, _u64p, _u64p, _u8p])(
+            np.ascontiguousarray(list_of, np.uint32), np.ascontiguousarray(ids, np.uint64),
+            codes, n, rb, nlist, offsets, out_ids, out_codes)
+        return offsets, out_ids, out_codes
+
+    def ivf_build_with_centroids(self, codes, ids, tables, coarse):
+        lists = self.ivf_assign(codes, tables, coarse)
+        return self.ivf_csr(lists, ids, codes, coarse.shape[0])
+
+    def probe_order(self, coarse, query, nprobe):
+        coarse = np.ascontiguousarray(coarse, np.float32)
+        out = np.empty(nprobe, np.uint32)
+        self.fn("probe_order", None, [_f32p, _u64, _u64, _f32p, _u64, _u32p])(
+            coarse, coarse.shape[0], coarse.shape[1], np.ascontiguousarray(query, np.float32),
+            nprobe, out)
+        return out
+
+    def ivf_query(self, tables, coarse, offsets, list_ids, list_codes, query, k, nprobe,
+                  max_sq_dist=None):
+        tables = np.ascontiguousarray(tables, np.float32)
+        M, ks, ds = tables.shape
+        ids = np.empty(k, np.uint64)
+        dist = np.empty(k, np.float64)
+        f = self.fn("ivf_query", C.c_int64,
+                    [_f32p, _u32, _u32, _u32, _f32p, _u64, _u64p, _u64p, _u8p, _f32p, _u64, _u64,
+                     C.c_int, C.c_double, _u64p, _f64p])
+        cnt = f(tables, M, ks, ds, np.ascontiguousarray(coarse, np.float32), coarse.shape[0],
+                np.ascontiguousarray(offsets, np.uint64), np.ascontiguousarray(list_ids, np.uint64),
+                np.ascontiguousarray(list_codes, np.uint8), np.ascontiguousarray(query, np.float32),
+                k, nprobe, int(max_sq_dist is not None),
+                0.0 if max_sq_dist is None else float(max_sq_dist), ids, dist)
+        if cnt < 0:
+            raise ValueError(f"ivf_query rc={cnt}")
+        return ids[:cnt], dist[:cnt]
+
+    def flat_scan(self, tables, codes, ids, query, k, max_sq_dist=None):
+        tables = np.ascontiguousarray(tables, np.float32)
+        M, ks, ds = tables.shape
+        out_ids = np.empty(k, np.uint64)
+        dist = np.empty(k, np.float64)
+        f = self.fn("flat_scan", C.c_int64,
+                    [_f32p, _u32, _u32, _u32, _u8p, _u64p, _u64, _f32p, _u64, C.c_int,
+                     C.c_double, _u64p, _f64p])
+        codes = np.ascontiguousarray(codes, np.uint8)
+        cnt = f(tables, M, ks, ds, codes, np.ascontiguousarray(ids, np.uint64), codes.shape[0],
+                np.ascontiguousarray(query, np.float32), k, int(max_sq_dist is not None),
+                0.0 if max_sq_dist is None else float(max_sq_dist), out_ids, dist)
+        if cnt < 0:
+            raise ValueError(f"flat_scan rc={cnt}")
+        return out_ids[:cnt], dist[:cnt]
+
+    def chunk_rows(self, n, c):
+        b = np.empty(c + 1, np.uint64)
+        if self.fn("chunk_rows", C.c_int, [_u64, _u64, _u64p])(n, c, b):
+            raise ValueError("chunk_rows")
+        return b
+
+
+class RefImpl(_Base):
+    """The reference compiled from its own sources (``oracle/_ref``)."""
+
+    def __init__(self, path: str = REF_LIB_PATH):
+        super().__init__(path, "ref_")
+        self.fn("ivf_build_with_centroids", C.c_void_p,
+                [_f32p, _u32, _u32, _u32, _u8p, _u64p, _u64, _f32p, _u64, C.POINTER(C.c_int)])
+        self.fn("ivf_build", C.c_void_p,
+                [_f32p, _u32, _u32, _u32, _u8p, _u64p, _u64, _u64, _u64, _u32, C.POINTER(C.c_int)])
+        self.fn("ivf_free", None, [C.c_void_p])
+        self.fn("ivf_nlist", _u64, [C.c_void_p])
+        self.fn("ivf_export", C.c_int, [C.c_void_p, _u64p, _u64p, _u8p, C.c_void_p])
+        self.fn("ivf_add", C.c_int, [C.c_void_p, _u8p, _u64p, _u64])
+        self.fn("ivf_merge", C.c_void_p, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int)])
+        self.fn("ivf_query_batch", C.c_int,
+                [C.c_void_p, _f32p, _u64, _u64, _u64, C.c_int, C.c_double, _u64p, _f64p, _u32p,
+                 C.c_int])
+        self.fn("ivf_query_subset", C.c_int,
+                [C.c_void_p, _f32p, _u64, _u64p, _u64, _u64, C.c_int, C.c_double, _u64p, _f64p,
+                 _u32p])
+        self.fn("hardware_concurrency", C.c_uint, [])
+
+    @staticmethod
+    def _check(rc, what):
+        if rc == -1:
+            raise ValueError(f"{what}: invalid_argument")
+        if rc == -2:
+            raise IndexError(f"{what}: out_of_range")
+        if rc:
+            raise RuntimeError(f"{what}: rc={rc}")
+
+    def random_matrix(self, rows, dims, seed, lo=-1.0, hi=1.0):
+        out = np.empty((rows, dims), np.float32)
+        self.fn("random_matrix", C.c_int, [_u64, _u64, _u64, C.c_float, C.c_float, _f32p])(
+            rows, dims, seed, lo, hi, out)
+        return out
+
+    def uniform_indices(self, seed, n, k):
+        out = np.empty(k, np.uint64)
+        self.fn("uniform_indices", C.c_int, [_u64, _u64, _u64, _u64p])(seed, n, k, out)
+        return out
+
+    def nearest_batch(self, points, table):
+        points = np.ascontiguousarray(points, np.float32)
+        table = np.ascontiguousarray(table, np.float32)
+        n, d = points.shape
+        idx = np.empty(n, np.uint32)
+        dist = np.empty(n, np.float64)
+        rc = self.fn("nearest_batch", C.c_int, [_f32p, _u64, _u64, _f32p, _u64, _u32p, _f64p])(
+            points, n, d, table, table.shape[0], idx, dist)
+        self._check(rc, "nearest")
+        return idx, dist
+
+    def kmeans_fit(self, points, k, max_iters=20, seed=0, tol=1e-4):
+        points = np.ascontiguousarray(points, np.float32)
+        n, d = points.shape
+        cent = np.empty((k, d), np.float32)
+        assign = np.empty(n, np.uint32)
+        inertia = C.c_double()
+        iters = C.c_uint32()
+        per = np.zeros(max(1, max_iters), np.float64)
+        rc = self.fn("kmeans_fit", C.c_int,
+                     [_f32p, _u64, _u64, _u64, _u32, _u64, C.c_double, _f32p, _u32p,
+                      C.POINTER(C.c_double), C.POINTER(C.c_uint32), _f64p])(
+            points, n, d, k, max_iters, seed, tol, cent, assign, C.byref(inertia),
+            C.byref(iters), per)
+        self._check(rc, "kmeans_fit")
+        return dict(centroids=cent, assignments=assign, inertia=inertia.value,
+                    iterations_run=iters.value, inertia_per_iter=per[: iters.value].copy())
+
+    def pq_fit(self, data, M, ks, max_iters=20, seed=0, threads=1):
+        data = np.ascontiguousarray(data, np.float32)
+        n, D = data.shape
+        tables = np.empty((M, ks, D // max(M, 1)), np.float32)
+        if threads > 1:
+            rc = self.fn("pq_fit_threads", C.c_int,
+                         [_f32p, _u64, _u64, _u32, _u32, _u32, _u64, _f32p, C.c_int])(
+                data, n, D, M, ks, max_iters, seed, tables, threads)
+        else:
+            rc = self.fn("pq_fit", C.c_int, [_f32p, _u64, _u64, _u32, _u32, _u32, _u64, _f32p])(
+                data, n, D, M, ks, max_iters, seed, tables)
+        self._check(rc, "pq_fit")
+        return tables
+
+    def pq_encode(self, data, tables, threads=1):
+        data = np.ascontiguousarray(data, np.float32)
+        tables = np.ascontiguousarray(tables, np.float32)
+        M, ks, ds = tables.shape
+        n = data.shape[0]
+        codes = np.empty((n, M * code_width(ks)), np.uint8)
+        if threads > 1:
+            rc = self.fn("pq_encode_threads", C.c_int,
+                         [_f32p, _u64, _u32, _u32, _u32, _f32p, _u8p, C.c_int])(
+                data, n, M, ks, ds, tables, codes, threads)
+        else:
+            rc = self.fn("pq_encode", C.c_int, [_f32p, _u64, _u32, _u32, _u32, _f32p, _u8p])(
+                data, n, M, ks, ds, tables, codes)
+        self._check(rc, "pq_encode")
+        return codes
+
+    def pq_decode(self, codes, tables):
+        tables = np.ascontiguousarray(tables, np.float32)
+        codes = np.ascontiguousarray(codes, np.uint8)
+        M, ks, ds = tables.shape
+        out = np.empty((codes.shape[0], M * ds), np.float32)
+        rc = self.fn("pq_decode", C.c_int, [_u8p, _u64, _u32, _u32, _u32, _f32p, _f32p])(
+            codes, codes.shape[0], M, ks, ds, tables, out)
+        self._check(rc, "pq_decode")
+        return out
+
+    def rmse(self, a, b):
+        a = np.ascontiguousarray(a, np.float32)
+        b = np.ascontiguousarray(b, np.float32)
+        out = C.c_double()
+        rc = self.fn("rmse", C.c_int, [_f32p, _f32p, _u64, _u64, C.POINTER(C.c_double)])(
+            a, b, a.shape[0], a.shape[1], C.byref(out))
+        self._check(rc, "rmse")
+        return out.value
+
+    def reconstruction_rmse(self, data, tables):
+        data = np.ascontiguousarray(data, np.float32)
+        tables = np.ascontiguousarray(tables, np.float32)
+        M, ks, ds = tables.shape
+        out = C.c_double()
+        rc = self.fn("reconstruction_rmse", C.c_int,
+                     [_f32p, _u64, _u32, _u32, _u32, _f32p, C.POINTER(C.c_double)])(
+            data, data.shape[0], M, ks, ds, tables, C.byref(out))
+        self._check(rc, "reconstruction_rmse")
+        return out.value
+
+    def adc_table(self, tables, query):
+        tables = np.ascontiguousarray(tables, np.float32)
+        M, ks, ds = tables.shape
+        out = np.empty((M, ks), np.float32)
+        rc = self.fn("adc_table", C.c_int, [_f32p, _u32, _u32, _u32, _f32p, _f32p])(
+            tables, M, ks, ds, np.ascontiguousarray(query, np.float32), out)
+        self._check(rc, "adc_table")
+        return out
+
+    def adc_lookup_all(self, entries, codes):
+        entries = np.ascontiguousarray(entries, np.float32)
+        codes = np.ascontiguousarray(codes, np.uint8)
+        M, ks = entries.shape
+        out = np.empty(codes.shape[0], np.float64)
+        rc = self.fn("adc_lookup_all", C.c_int, [_f32p, _u32, _u32, _u8p, _u64, _f64p])(
+            entries, M, ks, codes, codes.shape[0], out)
+        self._check(rc, "adc_lookup")
+        return out
+
+    # -- index handles ---------------------------------------------------
+    def ivf_build_with_centroids(self, codes, ids, tables, coarse):
+        tables = np.ascontiguousarray(tables, np.float32)
+        M, ks, ds = tables.shape
+        codes = np.ascontiguousarray(codes, np.uint8)
+        st = C.c_int()
+        h = self.lib.ref_ivf_build_with_centroids(
+            tables, M, ks, ds, codes, np.ascontiguousarray(ids, np.uint64), codes.shape[0],
+            np.ascontiguousarray(coarse, np.float32), coarse.shape[0], C.byref(st))
+        self._check(st.value, "ivf_build_with_centroids")
+        return RefIndexHandle(self, h, codes.shape[1], M * ds)
+
+    def ivf_build(self, codes, ids, tables, nlist, seed, iters=20):
+        tables = np.ascontiguousarray(tables, np.float32)
+        M, ks, ds = tables.shape
+        codes = np.ascontiguousarray(codes, np.uint8)
+        st = C.c_int()
+        h = self.lib.ref_ivf_build(tables, M, ks, ds, codes, np.ascontiguousarray(ids, np.uint64),
+                                   codes.shape[0], nlist, seed, iters, C.byref(st))
+        self._check(st.value, "ivf_build")
+        return RefIndexHandle(self, h, codes.shape[1], M * ds)
+
+    def flat_scan(self, tables, codes, ids, query, k, max_sq_dist=None):
+        tables = np.ascontiguousarray(tables, np.float32)
+        M, ks, ds = tables.shape
+        codes = np.ascontiguousarray(codes, np.uint8)
+        out_ids = np.empty(k, np.uint64)
+        dist = np.empty(k, np.float64)
+        cnt = np.zeros(1, np.uint32)
+        rc = self.fn("flat_scan", C.c_int,
+                     [_f32p, _u32, _u32, _u32, _u8p, _u64p, _u64, _f32p, _u64, C.c_int,
+                      C.c_double, _u64p, _f64p, _u32p])(
+            tables, M, ks, ds, codes, np.ascontiguousarray(ids, np.uint64), codes.shape[0],
+            np.ascontiguousarray(query, np.float32), k, int(max_sq_dist is not None),
+            0.0 if max_sq_dist is None else float(max_sq_dist), out_ids, dist, cnt)
+        self._check(rc, "flat_scan")
+        return out_ids[: cnt[0]], dist[: cnt[0]]
+
+    def default_nlist(self, n):
+        return self.fn("default_nlist", _u64, [_u64])(n)
+
+    def chunk_rows(self, n, c):
+        b = np.empty(c + 1, np.uint64)
+        self._check(self.fn("chunk_rows", C.c_int, [_u64, _u64, _u64p])(n, c, b), "chunk_rows")
+        return b
+
+    def hardware_concurrency(self):
+        return self.lib.ref_hardware_concurrency()
+
+
+class RefIndexHandle:
+    def __init__(self, ref: RefImpl, h, row_bytes: int, dims: int):
+        self.ref, self.h, self.row_bytes, self.dims = ref, h, row_bytes, dims
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.ref.lib.ref_ivf_free(self.h)
+            self.h = None
+
+    @property
+    def nlist(self):
+        return self.ref.lib.ref_ivf_nlist(self.h)
+
+    def export(self):
+        """(offsets[nlist+1], ids[n], codes[n, row_bytes], coarse[nlist, D])."""
+        nlist = self.nlist
+        f = self.ref.lib.ref_ivf_n_items
+        f.restype, f.argtypes = C.c_uint64, [C.c_void_p]
+        n = int(f(self.h))
+        offsets = np.empty(nlist + 1, np.uint64)
+        ids = np.empty(max(n, 1), np.uint64)
+        codes = np.empty((max(n, 1), self.row_bytes), np.uint8)
+        coarse = np.empty((nlist, self.dims), np.float32)
+        self.ref.lib.ref_ivf_export(self.h, offsets, ids, codes, coarse.ctypes.data)
+        return offsets, ids[:n], codes[:n], coarse
+
+    def add(self, codes, ids):
+        codes = np.ascontiguousarray(codes, np.uint8)
+        rc = self.ref.lib.ref_ivf_add(self.h, codes, np.ascontiguousarray(ids, np.uint64),
+                                      codes.shape[0])
+        self.ref._check(rc, "ivf_add")
+
+    def merge(self, other):
+        st = C.c_int()
+        h = self.ref.lib.ref_ivf_merge(self.h, other.h, C.byref(st))
+        self.ref._check(st.value, "ivf_merge")
+        return RefIndexHandle(self.ref, h, self.row_bytes, self.dims)
+
+    def query_batch(self, queries, k, nprobe, max_sq_dist=None, threads=1):
+        queries = np.ascontiguousarray(queries, np.float32).reshape(-1, self.dims)
+        nq = queries.shape[0]
+        ids = np.zeros((nq, k), np.uint64)
+        dist = np.zeros((nq, k), np.float64)
+        counts = np.zeros(nq, np.uint32)
+        rc = self.ref.lib.ref_ivf_query_batch(
+            self.h, queries, nq, k, nprobe, int(max_sq_dist is not None),
+            0.0 if max_sq_dist is None else float(max_sq_dist), ids, dist, counts, threads)
+        self.ref._check(rc, "ivf_query")
+        return ids, dist, counts
+
+    def query_subset(self, query, k, subset, nprobe, max_sq_dist=None):
+        ids = np.zeros(k, np.uint64)
+        dist = np.zeros(k, np.float64)
+        cnt = np.zeros(1, np.uint32)
+        subset = np.ascontiguousarray(subset, np.uint64)
+        rc = self.ref.lib.ref_ivf_query_subset(
+            self.h, np.ascontiguousarray(query, np.float32), k, subset, subset.size, nprobe,
+            int(max_sq_dist is not None), 0.0 if max_sq_dist is None else float(max_sq_dist),
+            ids, dist, cnt)
+        self.ref._check(rc, "ivf_query_subset")
+        return ids[: cnt[0]], dist[: cnt[0]]
+
+
+_C = None
+_R = None
+
+
+def c_oracle() -> COracle:
+    global _C
+    if _C is None:
+        if not os.path.exists(C_LIB_PATH):
+            build()
+        _C = COracle()
+    return _C
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_LIB_PATH)
+
+
+def ref_impl() -> RefImpl:
+    global _R
+    if _R is None:
+        _R = RefImpl()
+    return _R

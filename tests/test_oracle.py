@@ -1,0 +1,149 @@
+"""Pins the C restatement (oracle/pqii_oracle.c) before it is trusted as the
+checker: against the golden fixtures written by the compiled reference,
+against the compiled reference itself (oracle/_ref) and against the
+reference's own known-answer tests."""
+import numpy as np
+import pytest
+
+
+def bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint32 if a.dtype == np.float32 else np.uint64)
+
+
+def test_random_matrix_matches_libstdcxx(golden, orc):
+    # proj/tests/test_helpers.cpp:26-33
+    assert np.array_equal(bits(orc.random_matrix(120, 8, 57)), bits(golden["random_matrix/120x8_s57"]))
+
+
+def test_init_draws_match_libstdcxx(golden, orc):
+    # proj/src/kmeans.cpp:74-80 (uniform_int_distribution is implementation-defined)
+    assert np.array_equal(orc.uniform_indices(1234, 1000, 256), golden["init_draws/seed1234_n1000_k256"])
+
+
+@pytest.mark.parametrize("name", ["km_rand", "km_1d", "km_dup", "km_mix", "km_mix_tol0", "km_k1"])
+def test_kmeans_golden(golden, orc, name):
+    k, iters, seed = (int(v) for v in golden[f"{name}/params"])
+    tol = float(golden[f"{name}/tol"][0])
+    r = orc.kmeans_fit(golden[f"{name}/points"], k, iters, seed, tol)
+    assert np.array_equal(bits(r["centroids"]), bits(golden[f"{name}/centroids"]))
+    assert np.array_equal(r["assignments"], golden[f"{name}/assignments"])
+    assert np.array_equal(bits(r["inertia_per_iter"]), bits(golden[f"{name}/inertia_per_iter"]))
+    assert r["iterations_run"] == int(golden[f"{name}/iterations_run"][0])
+
+
+def test_kmeans_known_answers(orc):
+    # proj/tests/test_kmeans.cpp:80-96: {0,1,9,10} -> {0.5, 9.5}, inertia 1.0
+    pts = np.array([[0], [1], [9], [10]], np.float32)
+    for seed in range(6):
+        r = orc.kmeans_fit(pts, 2, 20, seed)
+        assert abs(r["inertia"] - 1.0) < 1e-9
+        assert sorted(r["centroids"].ravel().tolist()) == [0.5, 9.5]
+    # :66-78 two separated points -> inertia 0
+    r = orc.kmeans_fit(np.array([[0, 0], [10, 10]], np.float32), 2, 20, 5)
+    assert r["inertia"] == 0.0
+    # :174-179 duplicates never give non-finite centroids
+    r = orc.kmeans_fit(np.full((6, 2), 1.5, np.float32), 3, 10, 0)
+    assert r["inertia"] == 0.0 and np.isfinite(r["centroids"]).all()
+
+
+def test_nearest_known_answers(orc):
+    # proj/tests/test_kmeans.cpp:98-112
+    table = orc.random_matrix(16, 8, 31)
+    idx, dist = orc.nearest_batch(table[3:4], table)
+    assert idx[0] == 3 and dist[0] == 0.0
+    idx, _ = orc.nearest_batch(np.array([[2.0]], np.float32), np.array([[1.0], [3.0]], np.float32))
+    assert idx[0] == 0  # equidistant -> lowest index
+
+
+def test_pq_golden(golden, orc):
+    M, ks, iters, seed = (int(v) for v in golden["pq/params"])
+    tables, _, _ = orc.pq_fit(golden["pq/data"], M, ks, iters, seed)
+    assert np.array_equal(bits(tables), bits(golden["pq/tables"]))
+    codes = orc.pq_encode(golden["pq/data"], tables)
+    assert np.array_equal(codes, golden["pq/codes"])
+    dec = orc.pq_decode(codes, tables)
+    assert np.array_equal(bits(dec), bits(golden["pq/decoded"]))
+    assert orc.rmse(golden["pq/data"], dec) == float(golden["pq/rmse"][0])
+    # M=1 degenerates to kmeans_fit(seed) bit-for-bit (test_pq.cpp:47-51)
+    t1, _, _ = orc.pq_fit(golden["pq_m1/data"], 1, 8, 10, 42)
+    assert np.array_equal(bits(t1), bits(golden["pq_m1/tables"]))
+    t2, _, _ = orc.pq_fit(golden["pq_m1/data"], 2, 8, 10, 1)
+    assert np.array_equal(bits(t2), bits(golden["pq_ds2/tables"]))
+
+
+def test_pq_wide_codes_golden(golden, orc):
+    codes = orc.pq_encode(golden["pq_wide/data"], golden["pq_wide/tables"])
+    assert codes.shape[1] == 4  # 2 subspaces x 2 bytes
+    assert np.array_equal(codes, golden["pq_wide/codes"])
+
+
+def test_adc_golden(golden, orc):
+    for i, q in enumerate(golden["adc/queries"]):
+        t = orc.adc_table(golden["pq/tables"], q)
+        assert np.array_equal(bits(t), bits(golden["adc/tables"][i]))
+        lk = orc.adc_lookup_all(t, golden["pq/codes"])
+        assert np.array_equal(bits(lk), bits(golden["adc/lookup"][i]))
+
+
+def test_adc_known_answers(orc):
+    # proj/tests/test_pq.cpp:163-214: (1-3)^2 == 4.0f
+    tables = np.array([[[3.0]], [[0.0]]], np.float32).reshape(2, 1, 1)
+    t = orc.adc_table(tables, np.array([1.0, 0.0], np.float32))
+    assert t[0, 0] == 4.0 and t[1, 0] == 0.0
+
+
+def test_ivf_golden(golden, orc):
+    off, lid, lcodes = orc.ivf_build_with_centroids(golden["pq/codes"], golden["ivf/ids"],
+                                                    golden["pq/tables"], golden["ivf/coarse"])
+    assert np.array_equal(off, golden["ivf/offsets"])
+    assert np.array_equal(lid, golden["ivf/list_ids"])
+    assert np.array_equal(lcodes, golden["ivf/list_codes"])
+    for nprobe in (1, 4, 40):
+        for qi, q in enumerate(golden["ivf/queries"]):
+            ids, dist = orc.ivf_query(golden["pq/tables"], golden["ivf/coarse"], off, lid, lcodes,
+                                      q, 10, nprobe)
+            c = int(golden[f"ivf/q_np{nprobe}_count"][qi])
+            assert len(ids) == c
+            assert np.array_equal(ids, golden[f"ivf/q_np{nprobe}_ids"][qi, :c])
+            assert np.array_equal(bits(dist), bits(golden[f"ivf/q_np{nprobe}_dist"][qi, :c]))
+    for qi, q in enumerate(golden["ivf/queries"]):
+        ids, dist = orc.ivf_query(golden["pq/tables"], golden["ivf/coarse"], off, lid, lcodes,
+                                  q, 10, 4, max_sq_dist=60.0)
+        c = int(golden["ivf/q_max_count"][qi])
+        assert np.array_equal(ids, golden["ivf/q_max_ids"][qi, :c])
+        fi, fd = orc.flat_scan(golden["pq/tables"], golden["pq/codes"], golden["ivf/ids"], q, 10)
+        assert np.array_equal(fi, golden["ivf/flat_ids"][qi])
+        assert np.array_equal(bits(fd), bits(golden["ivf/flat_dist"][qi]))
+
+
+def test_chunk_rows_golden(golden, orc):
+    assert np.array_equal(orc.chunk_rows(10, 3), golden["chunk_rows/10_3"])
+
+
+# --- live comparison against the compiled reference (oracle/_ref) -----------
+
+@pytest.mark.parametrize("seed", [0, 3, 77])
+def test_oracle_vs_ref_kmeans_random(orc, ref, seed):
+    rng = np.random.default_rng(seed)
+    n, d = int(rng.integers(50, 400)), int(rng.integers(1, 9))
+    k = int(rng.integers(1, min(40, n)))
+    pts = orc.random_matrix(n, d, seed + 100)
+    a = orc.kmeans_fit(pts, k, 25, seed, 0.0)
+    b = ref.kmeans_fit(pts, k, 25, seed, 0.0)
+    assert np.array_equal(bits(a["centroids"]), bits(b["centroids"]))
+    assert np.array_equal(a["assignments"], b["assignments"])
+    assert np.array_equal(bits(a["inertia_per_iter"]), bits(b["inertia_per_iter"]))
+
+
+def test_oracle_vs_ref_ivf_query(orc, ref, golden):
+    h = ref.ivf_build_with_centroids(golden["pq/codes"], golden["ivf/ids"], golden["pq/tables"],
+                                     golden["ivf/coarse"])
+    off, lid, lcodes, _ = h.export()
+    qs = golden["ivf/queries"]
+    ri, rd, rc = h.query_batch(qs, 7, 9)
+    for qi, q in enumerate(qs):
+        ids, dist = orc.ivf_query(golden["pq/tables"], golden["ivf/coarse"], off, lid, lcodes,
+                                  q, 7, 9)
+        assert np.array_equal(ids, ri[qi, : rc[qi]])
+        assert np.array_equal(bits(dist), bits(rd[qi, : rc[qi]]))
