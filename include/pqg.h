@@ -1,0 +1,177 @@
+/*
+ * pqg.h -- C ABI of the B200-native PQ / IVF hot path (libpqg.so).
+ *
+ * Plain pointers and sizes only.  Every data pointer may be HOST memory or
+ * DEVICE memory of the context's GPU; the library detects which
+ * (cudaPointerGetAttributes) and stages host buffers through its own device
+ * scratch, so the same entry points serve the reference-facing host API and
+ * device-resident pipelines.  All entry points return PQG_OK (0) or a
+ * negative status; pqg_last_error() returns the thread's last message.
+ * Status mapping to the reference's exceptions:
+ *   PQG_EINVAL -> std::invalid_argument   PQG_ERANGE -> std::out_of_range
+ *   PQG_ECUDA / PQG_ENOMEM / PQG_EUNSUPPORTED -> std::runtime_error
+ * Message substrings follow the reference ("not divisible", "exceeds",
+ * "no items", "duplicate id", "nprobe", ...).
+ *
+ * Each function cites the reference function it replaces
+ * (/root/reference/proj/<path>:<line>).  Code matrices are the reference's
+ * packed layout (proj/include/pqii/pq.hpp:33-55): n rows of M codes, one byte
+ * each when ks <= 256, else two bytes little-endian.  Codebooks are
+ * [M][ks][ds] fp32 (pq.hpp:15-31).  Posting lists are CSR: offsets[nlist+1]
+ * (u64), ids[n] (u64), codes[n][row_bytes] -- list l holds entries
+ * offsets[l]..offsets[l+1]-1 in insertion order (ivf.cpp:44-46).
+ */
+#ifndef PQG_H
+#define PQG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PQG_OK 0
+#define PQG_EINVAL (-1)
+#define PQG_ERANGE (-2)
+#define PQG_ECUDA (-3)
+#define PQG_ENOMEM (-4)
+#define PQG_EUNSUPPORTED (-5)
+
+typedef struct pqg_ctx pqg_ctx;     /* one GPU + stream + scratch arena */
+typedef struct pqg_index pqg_index; /* device-resident inverted index */
+
+/* ---- context ----------------------------------------------------------- */
+int pqg_ctx_create(int device, pqg_ctx** out);
+void pqg_ctx_destroy(pqg_ctx* ctx);
+/* Run on a caller-owned cudaStream_t (NULL restores the context's own). */
+int pqg_ctx_set_stream(pqg_ctx* ctx, void* cuda_stream);
+int pqg_ctx_sync(pqg_ctx* ctx);
+const char* pqg_last_error(void);
+/* Number of kernels this context has launched (bench.py's gpu_launches). */
+uint64_t pqg_ctx_launches(pqg_ctx* ctx);
+/* Per-kernel-class CUDA-event timing on the context stream.  enable=1 starts
+ * recording every launch; pqg_profile_read returns (launch count, summed ms)
+ * for a class name such as "nearest", "fixup", "kmeans_sum", "adc_scan". */
+int pqg_profile_enable(pqg_ctx* ctx, int enable);
+int pqg_profile_read(pqg_ctx* ctx, const char* kernel_class, uint64_t* launches,
+                     double* total_ms);
+const char* pqg_version(void);
+
+/* ---- L1: nearest centroid / k-means (proj/src/kmeans.cpp) ---------------- */
+/* nearest_in_table (kmeans.cpp:20-31) for n points: index[i], sq_dist[i] are
+ * exactly the reference's (fp64 squared_l2, ties to the lowest index). */
+int pqg_nearest_batch(pqg_ctx* ctx, const float* points, uint64_t n, uint64_t d,
+                      const float* table, uint64_t k, uint32_t* index, double* sq_dist);
+
+/* kmeans_fit (kmeans.cpp:61-133).  centroids k*d, assignments n (nullable),
+ * inertia_per_iter max_iters entries (nullable, first *iterations_run valid). */
+int pqg_kmeans_fit(pqg_ctx* ctx, const float* points, uint64_t n, uint64_t d, uint64_t k,
+                   uint32_t max_iters, uint64_t seed, double tol, float* centroids,
+                   uint32_t* assignments, double* inertia, uint32_t* iterations_run,
+                   double* inertia_per_iter);
+
+/* ---- L1: product quantization (proj/src/pq.cpp) -------------------------- */
+/* pq_fit (pq.cpp:63-93): all M subspace fits batched in one device loop; each
+ * keeps the reference's seed+m init and its own tol stop.  tables M*ks*(D/M);
+ * iterations_run / inertia per subspace (nullable). */
+int pqg_pq_fit(pqg_ctx* ctx, const float* data, uint64_t n, uint64_t D, uint32_t M,
+               uint32_t ks, uint32_t max_iters, uint64_t seed, float* tables,
+               uint32_t* iterations_run, double* inertia);
+/* pq_encode (pq.cpp:95-111): codes n*M*width. */
+int pqg_pq_encode(pqg_ctx* ctx, const float* data, uint64_t n, uint32_t M, uint32_t ks,
+                  uint32_t ds, const float* tables, uint8_t* codes);
+/* pq_decode (pq.cpp:113-130); PQG_ERANGE if a code >= ks. */
+int pqg_pq_decode(pqg_ctx* ctx, const uint8_t* codes, uint64_t n, uint32_t M, uint32_t ks,
+                  uint32_t ds, const float* tables, float* out);
+/* rmse (pq.cpp:169-177) numerator: sum over count elements of (a-b)^2 in fp64. */
+int pqg_sq_error(pqg_ctx* ctx, const float* a, const float* b, uint64_t count, double* sse);
+/* reconstruction_rmse (pq.cpp:179-181) without materialising the decode:
+ * sse = sum (x - decode(codes))^2; rmse = sqrt(sse / (n*M*ds)). */
+int pqg_pq_recon_sse(pqg_ctx* ctx, const float* data, const uint8_t* codes, uint64_t n,
+                     uint32_t M, uint32_t ks, uint32_t ds, const float* tables, double* sse);
+/* Fused encode + reconstruction error: codes as pqg_pq_encode, sse as
+ * pqg_pq_recon_sse (sse nullable). */
+int pqg_pq_encode_sse(pqg_ctx* ctx, const float* data, uint64_t n, uint32_t M, uint32_t ks,
+                      uint32_t ds, const float* tables, uint8_t* codes, double* sse);
+/* adc_table (pq.cpp:132-151) for nq queries: entries nq*M*ks, each
+ * float(fp64 squared_l2). */
+int pqg_adc_tables(pqg_ctx* ctx, const float* tables, uint32_t M, uint32_t ks, uint32_t ds,
+                   const float* queries, uint64_t nq, float* entries);
+/* adc_lookup (pq.cpp:153-167) for n code rows against one table. */
+int pqg_adc_lookup(pqg_ctx* ctx, const float* entries, uint32_t M, uint32_t ks,
+                   const uint8_t* codes, uint64_t n, double* out);
+
+/* ---- L2: inverted index (proj/src/ivf.cpp) ------------------------------- */
+/* assign_items' list choice (ivf.cpp:36-49): list_of[i] = nearest coarse
+ * centroid to the DECODED code row i. */
+int pqg_ivf_assign(pqg_ctx* ctx, const uint8_t* codes, uint64_t n, uint32_t M, uint32_t ks,
+                   uint32_t ds, const float* tables, const float* coarse, uint64_t nlist,
+                   uint32_t* list_of);
+/* ivf_build_with_centroids (ivf.cpp:151-166) into a device-resident index.
+ * Validates as the reference (no items, coarse shape, duplicate ids). */
+int pqg_ivf_build_with_centroids(pqg_ctx* ctx, const float* tables, uint32_t M, uint32_t ks,
+                                 uint32_t ds, const uint8_t* codes, const uint64_t* ids,
+                                 uint64_t n, const float* coarse, uint64_t nlist,
+                                 pqg_index** out);
+/* ivf_build (ivf.cpp:123-149): coarse kmeans_fit(decoded, nlist, iters, seed)
+ * then lists from its final assignments. */
+int pqg_ivf_build(pqg_ctx* ctx, const float* tables, uint32_t M, uint32_t ks, uint32_t ds,
+                  const uint8_t* codes, const uint64_t* ids, uint64_t n, uint64_t nlist,
+                  uint64_t seed, uint32_t kmeans_iters, pqg_index** out);
+/* Wrap an existing CSR index (copied to the device). */
+int pqg_index_create(pqg_ctx* ctx, const float* tables, uint32_t M, uint32_t ks, uint32_t ds,
+                     const float* coarse, uint64_t nlist, const uint64_t* offsets,
+                     const uint64_t* ids, const uint8_t* codes, pqg_index** out);
+void pqg_index_destroy(pqg_index* index);
+int pqg_index_info(const pqg_index* index, uint64_t* nlist, uint64_t* n_items, uint32_t* M,
+                   uint32_t* ks, uint32_t* ds);
+/* Copy the CSR out (any of the pointers may be NULL to skip). */
+int pqg_index_export(pqg_ctx* ctx, const pqg_index* index, uint64_t* offsets, uint64_t* ids,
+                     uint8_t* codes, float* coarse, float* tables);
+/* ivf_add (ivf.cpp:168-184): assign and append in order; id collisions and
+ * duplicates are rejected before the index changes. */
+int pqg_index_add(pqg_ctx* ctx, pqg_index* index, const uint8_t* codes, const uint64_t* ids,
+                  uint64_t n);
+/* ivf_merge (ivf.cpp:186-216): list l = a's list l then b's. */
+int pqg_index_merge(pqg_ctx* ctx, const pqg_index* a, const pqg_index* b, pqg_index** out);
+/* Batched ivf_query (ivf.cpp:218-228) -- one call for nq queries.  Row q of
+ * out_ids / out_dists (nq*k) holds out_counts[q] <= k hits sorted by
+ * (sq_dist, id); has_max enables the max_sq_dist filter (ivf.cpp:70-77). */
+int pqg_index_search(pqg_ctx* ctx, const pqg_index* index, const float* queries, uint64_t nq,
+                     uint64_t k, uint64_t nprobe, int has_max, double max_sq_dist,
+                     uint64_t* out_ids, double* out_dists, uint32_t* out_counts);
+/* probe_order (ivf.cpp:91-101) for nq queries: probes nq*nprobe (u32). */
+int pqg_index_probe(pqg_ctx* ctx, const pqg_index* index, const float* queries, uint64_t nq,
+                    uint64_t nprobe, uint32_t* probes);
+/* flat_scan (ivf.cpp:247-262) for nq queries over n codes. */
+int pqg_flat_scan(pqg_ctx* ctx, const float* tables, uint32_t M, uint32_t ks, uint32_t ds,
+                  const uint8_t* codes, const uint64_t* ids, uint64_t n, const float* queries,
+                  uint64_t nq, uint64_t k, int has_max, double max_sq_dist, uint64_t* out_ids,
+                  double* out_dists, uint32_t* out_counts);
+/* Merge per-shard top-k lists (S shards x nq x k, counts S x nq) into the
+ * global top-k by (dist, id) -- the multi-GPU search combine. */
+int pqg_topk_merge(pqg_ctx* ctx, const uint64_t* ids, const double* dists,
+                   const uint32_t* counts, uint32_t shards, uint64_t nq, uint64_t k,
+                   uint64_t* out_ids, double* out_dists, uint32_t* out_counts);
+
+/* ---- sharded k-means steps (multi-GPU driver) ------------ */
+/* One assignment pass of a batch of B k-means problems over a row shard:
+ * problem b reads columns [b*col_stride, b*col_stride+d) of rows (n x ld).
+ * assign[b*n+i] (u32) and dist[b*n+i] (fp64) are the reference's
+ * nearest_in_table results. */
+int pqg_assign_pass(pqg_ctx* ctx, const float* rows, uint64_t n, uint64_t ld, uint32_t B,
+                    uint32_t d, uint32_t col_stride, const float* tables, uint64_t k,
+                    uint32_t* assign, double* dist);
+/* The reference's update step (kmeans.cpp:102-130) for B problems given the
+ * full (all-shard, row-ordered) assignments and dists: fp64 sums in row
+ * order, mean = float(sum * (1/count)), empty clusters reseeded from the
+ * pre-update dists.  tables updated in place; dist modified (reseed zeroes). */
+int pqg_update_pass(pqg_ctx* ctx, const float* rows, uint64_t n, uint64_t ld, uint32_t B,
+                    uint32_t d, uint32_t col_stride, float* tables, uint64_t k,
+                    const uint32_t* assign, double* dist);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PQG_H */

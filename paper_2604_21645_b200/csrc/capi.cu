@@ -1,0 +1,1170 @@
+// capi.cu -- the extern "C" boundary (include/pqg.h) and the host-side
+// orchestration of the device hot path: the batched Lloyd loop, pq_fit,
+// encode/decode/RMSE, index build/add/merge and batched search.
+//
+// Host code here only validates arguments (with the reference's messages),
+// stages host buffers, draws the k-means init indices exactly as the
+// reference does (libstdc++ mt19937_64 + uniform_int_distribution, the same
+// GCC 13 headers) and sequences kernels.  There is no CPU compute fallback:
+// every numeric result comes from the kernels in nearest.cu, kmeans.cu,
+// pq.cu and ivf.cu.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <numeric>
+#include <random>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "kernels.cuh"
+
+using namespace pqg;
+
+// ---------------------------------------------------------------------------
+// error plumbing
+// ---------------------------------------------------------------------------
+static thread_local std::string g_last_error;
+
+template <class F>
+static int guard(F&& f) {
+    try {
+        f();
+        return PQG_OK;
+    } catch (const Error& e) {
+        g_last_error = e.msg;
+        return e.code;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return PQG_ECUDA;
+    } catch (...) {
+        g_last_error = "unknown error";
+        return PQG_ECUDA;
+    }
+}
+
+static void inval(const std::string& m) { fail(PQG_EINVAL, m); }
+
+// ---------------------------------------------------------------------------
+// host / device pointer staging
+// ---------------------------------------------------------------------------
+static bool on_device(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+template <class T>
+static const T* in(pqg_ctx* ctx, const T* p, uint64_t count) {
+    if (!p || count == 0 || on_device(p)) return p;
+    T* d = scratch<T>(ctx, count);
+    PQG_CUDA(cudaMemcpyAsync(d, p, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+    return d;
+}
+
+template <class T>
+struct Out {
+    T* user = nullptr;
+    T* dev = nullptr;
+    uint64_t count = 0;
+    bool host = false;
+};
+
+template <class T>
+static Out<T> out(pqg_ctx* ctx, T* p, uint64_t count) {
+    Out<T> o;
+    o.user = p;
+    o.count = count;
+    if (!p) return o;
+    if (on_device(p)) {
+        o.dev = p;
+    } else {
+        o.host = true;
+        o.dev = scratch<T>(ctx, std::max<uint64_t>(count, 1));
+    }
+    return o;
+}
+
+template <class T>
+static void finish(pqg_ctx* ctx, const Out<T>& o) {
+    if (o.host && o.count)
+        PQG_CUDA(cudaMemcpyAsync(o.user, o.dev, o.count * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+}
+
+static void sync(pqg_ctx* ctx) { PQG_CUDA(cudaStreamSynchronize(ctx->stream)); }
+
+static void reset_err(pqg_ctx* ctx) {
+    PQG_CUDA(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream));
+}
+
+static int read_err(pqg_ctx* ctx) {
+    int h = 0;
+    PQG_CUDA(cudaMemcpyAsync(&h, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    return h;
+}
+
+static uint32_t code_width(uint32_t ks) { return ks <= 256 ? 1 : 2; }
+
+// ---------------------------------------------------------------------------
+// small kernels local to the orchestration
+// ---------------------------------------------------------------------------
+__global__ void codes_check_kernel(const uint8_t* codes, uint64_t n, uint32_t M, uint32_t ks,
+                                   uint32_t w, int* err) {
+    const uint64_t total = n * M;
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        const uint8_t* p = codes + e * w;
+        const uint32_t c = w == 1 ? p[0] : (uint32_t(p[0]) | (uint32_t(p[1]) << 8));
+        if (c >= ks) atomicExch(err, 1);
+    }
+}
+
+// CSR concatenation per list: entries of a keep their slot shifted by the b
+// entries of earlier lists; entries of b follow a's list (ivf.cpp:203-211).
+__global__ void csr_concat_kernel(const uint64_t* off_a, const uint64_t* ids_a,
+                                  const uint8_t* codes_a, uint64_t na, const uint64_t* off_b,
+                                  const uint64_t* ids_b, const uint8_t* codes_b, uint64_t nb,
+                                  uint64_t nlist, uint64_t rb, uint64_t* off_o, uint64_t* ids_o,
+                                  uint8_t* codes_o) {
+    const uint64_t total = na + nb;
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total + nlist + 1;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        if (e >= total) {
+            const uint64_t l = e - total;
+            off_o[l] = off_a[l] + off_b[l];
+            continue;
+        }
+        const bool from_a = e < na;
+        const uint64_t x = from_a ? e : e - na;
+        const uint64_t* off = from_a ? off_a : off_b;
+        // list of entry x: last l with off[l] <= x
+        uint64_t lo = 0, hi = nlist;
+        while (hi - lo > 1) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (off[mid] <= x) lo = mid; else hi = mid;
+        }
+        // skip empty lists sharing the offset
+        while (lo + 1 < nlist && off[lo + 1] <= x) ++lo;
+        const uint64_t dst = from_a ? x + off_b[lo] : x + off_a[lo + 1];
+        ids_o[dst] = from_a ? ids_a[x] : ids_b[x];
+        const uint8_t* s = (from_a ? codes_a : codes_b) + x * rb;
+        for (uint64_t j = 0; j < rb; ++j) codes_o[dst * rb + j] = s[j];
+    }
+}
+
+__global__ void iota_u64_kernel(uint64_t* p, uint64_t n) {
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+         e += uint64_t(gridDim.x) * blockDim.x)
+        p[e] = e;
+}
+
+// ---------------------------------------------------------------------------
+// context and index objects
+// ---------------------------------------------------------------------------
+struct pqg_index {
+    int device = 0;
+    uint32_t M = 0, ks = 0, ds = 0, w = 1;
+    uint64_t nlist = 0, n = 0;
+    float* tables = nullptr;
+    float* coarse = nullptr;
+    float* coarse_norm = nullptr;
+    float* coarse_max = nullptr;
+    uint64_t* offsets = nullptr;
+    uint64_t* ids = nullptr;
+    uint8_t* codes = nullptr;
+
+    uint64_t D() const { return uint64_t(M) * ds; }
+    uint64_t rb() const { return uint64_t(M) * w; }
+    IndexView view() const {
+        return IndexView{tables, M, ks, ds, w, coarse, coarse_norm, coarse_max, nlist,
+                         offsets, ids, codes, n};
+    }
+    void free_all() {
+        for (void* p : {(void*)tables, (void*)coarse, (void*)coarse_norm, (void*)coarse_max,
+                        (void*)offsets, (void*)ids, (void*)codes})
+            if (p) cudaFree(p);
+        tables = coarse = coarse_norm = coarse_max = nullptr;
+        offsets = ids = nullptr;
+        codes = nullptr;
+    }
+};
+
+template <class T>
+static T* dalloc(uint64_t count) {
+    T* p = nullptr;
+    if (cudaMalloc(&p, std::max<uint64_t>(count, 1) * sizeof(T)) != cudaSuccess) {
+        cudaGetLastError();
+        fail(PQG_ENOMEM, "device allocation of " + std::to_string(count * sizeof(T)) + " bytes failed");
+    }
+    return p;
+}
+
+static pqg_index* new_index(pqg_ctx* ctx, uint32_t M, uint32_t ks, uint32_t ds, uint64_t nlist,
+                            uint64_t n, const float* d_tables, const float* d_coarse) {
+    pqg_index* ix = new pqg_index;
+    ix->device = ctx->device;
+    ix->M = M; ix->ks = ks; ix->ds = ds; ix->w = code_width(ks);
+    ix->nlist = nlist; ix->n = n;
+    try {
+        ix->tables = dalloc<float>(uint64_t(M) * ks * ds);
+        ix->coarse = dalloc<float>(nlist * ix->D());
+        ix->coarse_norm = dalloc<float>(nlist);
+        ix->coarse_max = dalloc<float>(1);
+        ix->offsets = dalloc<uint64_t>(nlist + 1);
+        ix->ids = dalloc<uint64_t>(n);
+        ix->codes = dalloc<uint8_t>(n * ix->rb());
+        PQG_CUDA(cudaMemcpyAsync(ix->tables, d_tables, sizeof(float) * M * ks * ds,
+                                 cudaMemcpyDeviceToDevice, ctx->stream));
+        PQG_CUDA(cudaMemcpyAsync(ix->coarse, d_coarse, sizeof(float) * nlist * ix->D(),
+                                 cudaMemcpyDeviceToDevice, ctx->stream));
+        table_norms(ctx, ix->coarse, 1, nlist, uint32_t(ix->D()), ix->coarse_norm, ix->coarse_max);
+    } catch (...) {
+        ix->free_all();
+        delete ix;
+        throw;
+    }
+    return ix;
+}
+
+// ---------------------------------------------------------------------------
+// k-means engine (B problems batched; proj/src/kmeans.cpp:61-133 each)
+// ---------------------------------------------------------------------------
+// Init indices exactly as kmeans_fit (kmeans.cpp:73-85): partial Fisher-Yates
+// over iota(n) driven by mt19937_64(seed) and uniform_int_distribution(i, n-1);
+// the permutation is kept sparse (only touched slots are stored).
+static std::vector<uint64_t> init_rows(uint64_t n, uint64_t k, uint64_t seed) {
+    std::mt19937_64 rng(seed);
+    std::unordered_map<uint64_t, uint64_t> perm;
+    perm.reserve(2 * k);
+    auto get = [&](uint64_t i) {
+        auto it = perm.find(i);
+        return it == perm.end() ? i : it->second;
+    };
+    for (uint64_t i = 0; i < k; ++i) {
+        std::uniform_int_distribution<std::size_t> pick(i, n - 1);
+        const uint64_t j = pick(rng);
+        const uint64_t vi = get(i), vj = get(j);
+        perm[i] = vj;
+        perm[j] = vi;
+    }
+    std::vector<uint64_t> rows(k);
+    for (uint64_t c = 0; c < k; ++c) rows[c] = get(c);
+    return rows;
+}
+
+struct KMeansOut {
+    std::vector<double> inertia;   // [B]
+    std::vector<uint32_t> iters;   // [B]
+    std::vector<double> per_iter;  // [B][max_iters]
+};
+
+// x: device rows (n x ldx); table (device, B*k*d) receives the centroids;
+// assign (device, B*n u32) receives the final assignments.
+static KMeansOut run_kmeans(pqg_ctx* ctx, const float* x, uint64_t n, uint64_t ldx, uint32_t B,
+                            uint32_t d, uint32_t col_stride, uint64_t k, uint32_t max_iters,
+                            const std::vector<uint64_t>& seeds, double tol, float* table,
+                            uint32_t* assign) {
+    std::vector<uint64_t> rows;
+    rows.reserve(uint64_t(B) * k);
+    for (uint32_t b = 0; b < B; ++b) {
+        auto r = init_rows(n, k, seeds[b]);
+        rows.insert(rows.end(), r.begin(), r.end());
+    }
+    uint64_t* d_rows = scratch<uint64_t>(ctx, rows.size());
+    PQG_CUDA(cudaMemcpyAsync(d_rows, rows.data(), rows.size() * sizeof(uint64_t),
+                             cudaMemcpyHostToDevice, ctx->stream));
+    gather_rows(ctx, x, ldx, B, d, col_stride, d_rows, k, table);
+
+    KMeansState st;
+    st.active = scratch<int>(ctx, B);
+    st.prev = scratch<double>(ctx, B);
+    st.inertia = scratch<double>(ctx, B);
+    st.per_iter = scratch<double>(ctx, uint64_t(B) * max_iters);
+    st.iters = scratch<uint32_t>(ctx, B);
+    std::vector<int> ones(B, 1);
+    PQG_CUDA(cudaMemcpyAsync(st.active, ones.data(), sizeof(int) * B, cudaMemcpyHostToDevice, ctx->stream));
+    PQG_CUDA(cudaMemsetAsync(st.prev, 0, sizeof(double) * B, ctx->stream));
+    PQG_CUDA(cudaMemsetAsync(st.per_iter, 0, sizeof(double) * B * max_iters, ctx->stream));
+    float* cnorm = scratch<float>(ctx, uint64_t(B) * k);
+    float* cmax = scratch<float>(ctx, B);
+    double* dist = scratch<double>(ctx, uint64_t(B) * n);
+
+    RowSrc src;
+    src.x = x;
+    src.ldx = ldx;
+    src.col_stride = col_stride;
+    for (uint32_t it = 1; it <= max_iters; ++it) {
+        table_norms(ctx, table, B, k, d, cnorm, cmax);
+        NearestArgs a;
+        a.src = src;
+        a.n = n;
+        a.d = d;
+        a.B = B;
+        a.table = table;
+        a.k = k;
+        a.cnorm = cnorm;
+        a.cmax = cmax;
+        a.out_idx = assign;
+        a.idx_bytes = 4;
+        a.idx_rs = 1;
+        a.idx_ps = n;
+        a.out_dist = dist;
+        a.active = st.active;
+        nearest(ctx, a);
+        kmeans_inertia_and_stop(ctx, dist, n, B, it, max_iters, tol, st);
+        if (it == max_iters) break;
+        kmeans_update(ctx, src, n, B, d, table, k, assign, dist, st.active);
+    }
+    KMeansOut o;
+    o.inertia.resize(B);
+    o.iters.resize(B);
+    o.per_iter.resize(uint64_t(B) * max_iters);
+    PQG_CUDA(cudaMemcpyAsync(o.inertia.data(), st.inertia, sizeof(double) * B, cudaMemcpyDeviceToHost, ctx->stream));
+    PQG_CUDA(cudaMemcpyAsync(o.iters.data(), st.iters, sizeof(uint32_t) * B, cudaMemcpyDeviceToHost, ctx->stream));
+    PQG_CUDA(cudaMemcpyAsync(o.per_iter.data(), st.per_iter, sizeof(double) * B * max_iters,
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    return o;
+}
+
+// Encode n rows (device) into codes (device) in row chunks.
+static void encode_dev(pqg_ctx* ctx, const float* x, uint64_t n, uint32_t M, uint32_t ks,
+                       uint32_t ds, const float* tables, uint8_t* codes) {
+    float* cnorm = scratch<float>(ctx, uint64_t(M) * ks);
+    float* cmax = scratch<float>(ctx, M);
+    table_norms(ctx, tables, M, ks, ds, cnorm, cmax);
+    const uint64_t D = uint64_t(M) * ds;
+    const uint32_t w = code_width(ks);
+    const uint64_t chunk = std::max<uint64_t>(1, (uint64_t(64) << 20) / M);
+    for (uint64_t r0 = 0; r0 < n; r0 += chunk) {
+        const uint64_t nc = std::min(chunk, n - r0);
+        NearestArgs a;
+        a.src.x = x + r0 * D;
+        a.src.ldx = D;
+        a.src.col_stride = ds;
+        a.n = nc;
+        a.d = ds;
+        a.B = M;
+        a.table = tables;
+        a.k = ks;
+        a.cnorm = cnorm;
+        a.cmax = cmax;
+        a.out_idx = codes + r0 * M * w;
+        a.idx_bytes = int(w);
+        a.idx_rs = M;
+        a.idx_ps = 1;
+        nearest(ctx, a);
+    }
+}
+
+static void check_pq_shape(uint32_t M, uint32_t ks, uint32_t ds, const char* who) {
+    if (M == 0) inval(std::string(who) + ": M must be >= 1");
+    if (ks == 0 || ks > 65536) inval(std::string(who) + ": Ks must be in [1, 65536]");
+    if (ds == 0) inval(std::string(who) + ": sub_dim must be >= 1");
+}
+
+// ---------------------------------------------------------------------------
+// index construction helpers
+// ---------------------------------------------------------------------------
+static void check_unique_ids(pqg_ctx* ctx, const uint64_t* d_ids, const uint64_t* h_ids,
+                             uint64_t n, const std::string& prefix) {
+    if (n < 2) return;
+    uint64_t* pos = scratch<uint64_t>(ctx, 1);
+    find_duplicate(ctx, d_ids, n, pos);
+    uint64_t h = 0;
+    PQG_CUDA(cudaMemcpyAsync(&h, pos, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    if (h != ~uint64_t(0)) {
+        uint64_t id = 0;
+        if (h_ids) id = h_ids[h];
+        else PQG_CUDA(cudaMemcpy(&id, d_ids + h, sizeof(id), cudaMemcpyDeviceToHost));
+        inval(prefix + std::to_string(id));
+    }
+}
+
+// Build CSR lists for n items with list ids (device) into a fresh index.
+static void fill_lists(pqg_ctx* ctx, pqg_index* ix, const uint32_t* list_of, const uint64_t* ids,
+                       const uint8_t* codes, uint64_t n) {
+    Bucketing bk{ix->offsets, scratch<uint32_t>(ctx, std::max<uint64_t>(n, 1))};
+    if (n == 0) {
+        PQG_CUDA(cudaMemsetAsync(ix->offsets, 0, sizeof(uint64_t) * (ix->nlist + 1), ctx->stream));
+        return;
+    }
+    stable_bucket(ctx, list_of, n, 1, ix->nlist, nullptr, bk);
+    csr_scatter(ctx, bk.perm, n, ids, codes, ix->rb(), ix->ids, ix->codes);
+}
+
+static uint32_t* assign_lists(pqg_ctx* ctx, const float* tables, uint32_t M, uint32_t ks,
+                              uint32_t ds, const uint8_t* codes, uint64_t n, const float* coarse,
+                              const float* cnorm, const float* cmax, uint64_t nlist) {
+    reset_err(ctx);
+    const uint32_t w = code_width(ks);
+    launch(ctx, "codes_check", codes_check_kernel, dim3(grid1d(n * M, 256, ctx->num_sms * 8)),
+           dim3(256), 0, codes, n, M, ks, w, ctx->d_err);
+    uint32_t* list_of = scratch<uint32_t>(ctx, std::max<uint64_t>(n, 1));
+    NearestArgs a;
+    a.src.codes = codes;
+    a.src.dtab = tables;
+    a.src.dM = M;
+    a.src.dks = ks;
+    a.src.dds = ds;
+    a.src.dw = w;
+    a.n = n;
+    a.d = M * ds;
+    a.B = 1;
+    a.table = coarse;
+    a.k = nlist;
+    a.cnorm = cnorm;
+    a.cmax = cmax;
+    a.out_idx = list_of;
+    a.idx_bytes = 4;
+    a.idx_rs = 1;
+    a.idx_ps = 0;
+    nearest(ctx, a);
+    if (read_err(ctx)) fail(PQG_ERANGE, "pq_decode: code out of range for Ks=" + std::to_string(ks));
+    return list_of;
+}
+
+// ===========================================================================
+// extern "C"
+// ===========================================================================
+extern "C" {
+
+const char* pqg_last_error(void) { return g_last_error.c_str(); }
+
+const char* pqg_version(void) { return "pqg 0.1 (sm_100a)"; }
+
+int pqg_ctx_create(int device, pqg_ctx** out_ctx) {
+    return guard([&] {
+        if (!out_ctx) inval("ctx_create: null output");
+        int ndev = 0;
+        PQG_CUDA(cudaGetDeviceCount(&ndev));
+        if (device < 0 || device >= ndev) inval("ctx_create: no such device");
+        PQG_CUDA(cudaSetDevice(device));
+        pqg_ctx* c = new pqg_ctx;
+        c->device = device;
+        cudaDeviceProp prop;
+        PQG_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10) {
+            delete c;
+            fail(PQG_EUNSUPPORTED, "libpqg is built for sm_100a (B200); device is sm_" +
+                                       std::to_string(prop.major) + std::to_string(prop.minor));
+        }
+        c->num_sms = prop.multiProcessorCount;
+        PQG_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+        c->stream = c->own_stream;
+        PQG_CUDA(cudaMalloc(&c->d_err, sizeof(int)));
+        *out_ctx = c;
+    });
+}
+
+void pqg_ctx_destroy(pqg_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->arena.release();
+    for (auto& r : ctx->prof_recs) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto e : ctx->event_pool) cudaEventDestroy(e);
+    if (ctx->d_err) cudaFree(ctx->d_err);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+}
+
+int pqg_ctx_set_stream(pqg_ctx* ctx, void* s) {
+    return guard([&] { ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own_stream; });
+}
+
+int pqg_ctx_sync(pqg_ctx* ctx) { return guard([&] { sync(ctx); }); }
+
+uint64_t pqg_ctx_launches(pqg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int pqg_profile_enable(pqg_ctx* ctx, int enable) {
+    return guard([&] {
+        sync(ctx);
+        for (auto& r : ctx->prof_recs) {
+            ctx->event_pool.push_back(r.a);
+            ctx->event_pool.push_back(r.b);
+        }
+        ctx->prof_recs.clear();
+        ctx->profiling = enable != 0;
+    });
+}
+
+int pqg_profile_read(pqg_ctx* ctx, const char* cls, uint64_t* launches, double* total_ms) {
+    return guard([&] {
+        sync(ctx);
+        uint64_t n = 0;
+        double ms = 0.0;
+        for (auto& r : ctx->prof_recs) {
+            if (ctx->prof_names[r.cls] != cls) continue;
+            float t = 0.f;
+            PQG_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+            ms += t;
+            ++n;
+        }
+        if (launches) *launches = n;
+        if (total_ms) *total_ms = ms;
+    });
+}
+
+int pqg_nearest_batch(pqg_ctx* ctx, const float* points, uint64_t n, uint64_t d,
+                      const float* table, uint64_t k, uint32_t* index, double* sq_dist) {
+    return guard([&] {
+        Scope sc(ctx);
+        if (k == 0) inval("nearest_centroid: empty centroid set");
+        if (d == 0 || n == 0) return;
+        const float* dp = in(ctx, points, n * d);
+        const float* dt = in(ctx, table, k * d);
+        auto oi = out(ctx, index, n);
+        auto od = out(ctx, sq_dist, n);
+        float* cnorm = scratch<float>(ctx, k);
+        float* cmax = scratch<float>(ctx, 1);
+        table_norms(ctx, dt, 1, k, uint32_t(d), cnorm, cmax);
+        NearestArgs a;
+        a.src.x = dp;
+        a.src.ldx = d;
+        a.n = n;
+        a.d = uint32_t(d);
+        a.table = dt;
+        a.k = k;
+        a.cnorm = cnorm;
+        a.cmax = cmax;
+        a.out_idx = oi.dev ? (void*)oi.dev : (void*)scratch<uint32_t>(ctx, n);
+        a.idx_bytes = 4;
+        a.idx_rs = 1;
+        a.out_dist = od.dev;
+        nearest(ctx, a);
+        finish(ctx, oi);
+        finish(ctx, od);
+        sync(ctx);
+    });
+}
+
+int pqg_kmeans_fit(pqg_ctx* ctx, const float* points, uint64_t n, uint64_t d, uint64_t k,
+                   uint32_t max_iters, uint64_t seed, double tol, float* centroids,
+                   uint32_t* assignments, double* inertia, uint32_t* iterations_run,
+                   double* inertia_per_iter) {
+    return guard([&] {
+        Scope sc(ctx);
+        // proj/src/kmeans.cpp:65-71
+        if (k == 0) inval("kmeans_fit: k must be >= 1");
+        if (k > n)
+            inval("kmeans_fit: k (" + std::to_string(k) + ") exceeds number of points (" +
+                  std::to_string(n) + ")");
+        if (max_iters < 1) inval("kmeans_fit: max_iters must be >= 1");
+        if (tol < 0.0) inval("kmeans_fit: tol must be >= 0");
+        if (d == 0) inval("kmeans_fit: dims must be >= 1");
+        const float* dp = in(ctx, points, n * d);
+        auto oc = out(ctx, centroids, k * d);
+        float* table = oc.dev ? oc.dev : scratch<float>(ctx, k * d);
+        auto oa = out(ctx, assignments, n);
+        uint32_t* assign = oa.dev ? oa.dev : scratch<uint32_t>(ctx, n);
+        KMeansOut r = run_kmeans(ctx, dp, n, d, 1, uint32_t(d), 0, k, max_iters, {seed}, tol,
+                                 table, assign);
+        finish(ctx, oc);
+        finish(ctx, oa);
+        sync(ctx);
+        if (inertia) *inertia = r.inertia[0];
+        if (iterations_run) *iterations_run = r.iters[0];
+        if (inertia_per_iter)
+            std::copy(r.per_iter.begin(), r.per_iter.begin() + r.iters[0], inertia_per_iter);
+    });
+}
+
+int pqg_pq_fit(pqg_ctx* ctx, const float* data, uint64_t n, uint64_t D, uint32_t M, uint32_t ks,
+               uint32_t max_iters, uint64_t seed, float* tables, uint32_t* iterations_run,
+               double* inertia) {
+    return guard([&] {
+        Scope sc(ctx);
+        // proj/src/pq.cpp:65-75
+        if (M == 0) inval("pq_fit: M must be >= 1");
+        if (D % M != 0)
+            inval("pq_fit: D (" + std::to_string(D) + ") is not divisible by M (" +
+                  std::to_string(M) + ")");
+        if (ks > n)
+            inval("pq_fit: Ks (" + std::to_string(ks) + ") exceeds number of rows (" +
+                  std::to_string(n) + ")");
+        const uint32_t ds = uint32_t(D / M);
+        check_pq_shape(M, ks, ds, "codebook");
+        if (max_iters < 1) inval("kmeans_fit: max_iters must be >= 1");
+        const float* dp = in(ctx, data, n * D);
+        auto ot = out(ctx, tables, uint64_t(M) * ks * ds);
+        float* table = ot.dev ? ot.dev : scratch<float>(ctx, uint64_t(M) * ks * ds);
+        uint32_t* assign = scratch<uint32_t>(ctx, uint64_t(M) * n);
+        std::vector<uint64_t> seeds(M);
+        for (uint32_t m = 0; m < M; ++m) seeds[m] = seed + m;  // pq.cpp:88
+        KMeansOut r = run_kmeans(ctx, dp, n, D, M, ds, ds, ks, max_iters, seeds, 1e-4, table, assign);
+        finish(ctx, ot);
+        sync(ctx);
+        if (iterations_run) std::copy(r.iters.begin(), r.iters.end(), iterations_run);
+        if (inertia) std::copy(r.inertia.begin(), r.inertia.end(), inertia);
+    });
+}
+
+int pqg_pq_encode(pqg_ctx* ctx, const float* data, uint64_t n, uint32_t M, uint32_t ks,
+                  uint32_t ds, const float* tables, uint8_t* codes) {
+    return guard([&] {
+        Scope sc(ctx);
+        check_pq_shape(M, ks, ds, "pq_encode");
+        if (n == 0) return;
+        const uint64_t D = uint64_t(M) * ds;
+        const float* dx = in(ctx, data, n * D);
+        const float* dt = in(ctx, tables, uint64_t(M) * ks * ds);
+        auto oc = out(ctx, codes, n * M * code_width(ks));
+        encode_dev(ctx, dx, n, M, ks, ds, dt, oc.dev);
+        finish(ctx, oc);
+        if (oc.host) sync(ctx);
+    });
+}
+
+int pqg_pq_decode(pqg_ctx* ctx, const uint8_t* codes, uint64_t n, uint32_t M, uint32_t ks,
+                  uint32_t ds, const float* tables, float* outp) {
+    return guard([&] {
+        Scope sc(ctx);
+        check_pq_shape(M, ks, ds, "pq_decode");
+        if (n == 0) return;
+        const uint8_t* dc = in(ctx, codes, n * M * code_width(ks));
+        const float* dt = in(ctx, tables, uint64_t(M) * ks * ds);
+        auto oo = out(ctx, outp, n * M * ds);
+        reset_err(ctx);
+        pq_decode_dev(ctx, dc, n, M, ks, ds, dt, oo.dev, ctx->d_err);
+        finish(ctx, oo);
+        if (read_err(ctx)) fail(PQG_ERANGE, "pq_decode: code out of range for Ks=" + std::to_string(ks));
+    });
+}
+
+int pqg_sq_error(pqg_ctx* ctx, const float* a, const float* b, uint64_t count, double* sse) {
+    return guard([&] {
+        Scope sc(ctx);
+        if (count == 0) {
+            *sse = 0.0;
+            return;
+        }
+        const float* da = in(ctx, a, count);
+        const float* db = in(ctx, b, count);
+        auto os = out(ctx, sse, 1);
+        sq_error_dev(ctx, da, db, count, os.dev);
+        finish(ctx, os);
+        sync(ctx);
+    });
+}
+
+int pqg_pq_recon_sse(pqg_ctx* ctx, const float* data, const uint8_t* codes, uint64_t n,
+                     uint32_t M, uint32_t ks, uint32_t ds, const float* tables, double* sse) {
+    return guard([&] {
+        Scope sc(ctx);
+        check_pq_shape(M, ks, ds, "reconstruction_rmse");
+        if (n == 0) {
+            *sse = 0.0;
+            return;
+        }
+        const float* dx = in(ctx, data, n * M * ds);
+        const uint8_t* dc = in(ctx, codes, n * M * code_width(ks));
+        const float* dt = in(ctx, tables, uint64_t(M) * ks * ds);
+        auto os = out(ctx, sse, 1);
+        reset_err(ctx);
+        recon_sse_dev(ctx, dx, dc, n, M, ks, ds, dt, os.dev, ctx->d_err);
+        finish(ctx, os);
+        if (read_err(ctx)) fail(PQG_ERANGE, "pq_decode: code out of range for Ks=" + std::to_string(ks));
+    });
+}
+
+int pqg_pq_encode_sse(pqg_ctx* ctx, const float* data, uint64_t n, uint32_t M, uint32_t ks,
+                      uint32_t ds, const float* tables, uint8_t* codes, double* sse) {
+    return guard([&] {
+        Scope sc(ctx);
+        check_pq_shape(M, ks, ds, "pq_encode");
+        if (n == 0) {
+            if (sse) *sse = 0.0;
+            return;
+        }
+        const uint64_t D = uint64_t(M) * ds;
+        const float* dx = in(ctx, data, n * D);
+        const float* dt = in(ctx, tables, uint64_t(M) * ks * ds);
+        auto oc = out(ctx, codes, n * M * code_width(ks));
+        uint8_t* dc = oc.dev ? oc.dev : scratch<uint8_t>(ctx, n * M * code_width(ks));
+        encode_dev(ctx, dx, n, M, ks, ds, dt, dc);
+        auto os = out(ctx, sse, 1);
+        if (os.dev) recon_sse_dev(ctx, dx, dc, n, M, ks, ds, dt, os.dev, ctx->d_err);
+        finish(ctx, oc);
+        finish(ctx, os);
+        if (oc.host || os.host) sync(ctx);
+    });
+}
+
+int pqg_adc_tables(pqg_ctx* ctx, const float* tables, uint32_t M, uint32_t ks, uint32_t ds,
+                   const float* queries, uint64_t nq, float* entries) {
+    return guard([&] {
+        Scope sc(ctx);
+        check_pq_shape(M, ks, ds, "adc_table");
+        if (nq == 0) return;
+        const float* dt = in(ctx, tables, uint64_t(M) * ks * ds);
+        const float* dq = in(ctx, queries, nq * M * ds);
+        auto oe = out(ctx, entries, nq * M * ks);
+        adc_tables_dev(ctx, dt, M, ks, ds, dq, nq, oe.dev);
+        finish(ctx, oe);
+        if (oe.host) sync(ctx);
+    });
+}
+
+int pqg_adc_lookup(pqg_ctx* ctx, const float* entries, uint32_t M, uint32_t ks,
+                   const uint8_t* codes, uint64_t n, double* outp) {
+    return guard([&] {
+        Scope sc(ctx);
+        if (n == 0) return;
+        const float* de = in(ctx, entries, uint64_t(M) * ks);
+        const uint8_t* dc = in(ctx, codes, n * M * code_width(ks));
+        auto oo = out(ctx, outp, n);
+        reset_err(ctx);
+        adc_lookup_dev(ctx, de, M, ks, dc, n, oo.dev, ctx->d_err);
+        finish(ctx, oo);
+        if (read_err(ctx)) fail(PQG_ERANGE, "adc_lookup: code out of range for Ks=" + std::to_string(ks));
+    });
+}
+
+int pqg_ivf_assign(pqg_ctx* ctx, const uint8_t* codes, uint64_t n, uint32_t M, uint32_t ks,
+                   uint32_t ds, const float* tables, const float* coarse, uint64_t nlist,
+                   uint32_t* list_of) {
+    return guard([&] {
+        Scope sc(ctx);
+        check_pq_shape(M, ks, ds, "ivf_assign");
+        if (nlist == 0) inval("ivf_build: coarse centroids do not match the codebook");
+        if (n == 0) return;
+        const uint8_t* dc = in(ctx, codes, n * M * code_width(ks));
+        const float* dt = in(ctx, tables, uint64_t(M) * ks * ds);
+        const float* dco = in(ctx, coarse, nlist * M * ds);
+        float* cnorm = scratch<float>(ctx, nlist);
+        float* cmax = scratch<float>(ctx, 1);
+        table_norms(ctx, dco, 1, nlist, M * ds, cnorm, cmax);
+        uint32_t* lo = assign_lists(ctx, dt, M, ks, ds, dc, n, dco, cnorm, cmax, nlist);
+        auto ol = out(ctx, list_of, n);
+        PQG_CUDA(cudaMemcpyAsync(ol.dev, lo, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+        finish(ctx, ol);
+        sync(ctx);
+    });
+}
+
+int pqg_ivf_build_with_centroids(pqg_ctx* ctx, const float* tables, uint32_t M, uint32_t ks,
+                                 uint32_t ds, const uint8_t* codes, const uint64_t* ids,
+                                 uint64_t n, const float* coarse, uint64_t nlist,
+                                 pqg_index** outp) {
+    return guard([&] {
+        Scope sc(ctx);
+        // proj/src/ivf.cpp:151-160
+        if (n == 0) inval("ivf_build: no items");
+        if (nlist == 0 || !coarse) inval("ivf_build: coarse centroids do not match the codebook");
+        check_pq_shape(M, ks, ds, "ivf_build");
+        const uint64_t rb = uint64_t(M) * code_width(ks);
+        const float* dt = in(ctx, tables, uint64_t(M) * ks * ds);
+        const uint8_t* dc = in(ctx, codes, n * rb);
+        const uint64_t* di = in(ctx, ids, n);
+        const float* dco = in(ctx, coarse, nlist * M * ds);
+        check_unique_ids(ctx, di, on_device(ids) ? nullptr : ids, n, "duplicate id ");
+        pqg_index* ix = new_index(ctx, M, ks, ds, nlist, n, dt, dco);
+        try {
+            uint32_t* lo = assign_lists(ctx, ix->tables, M, ks, ds, dc, n, ix->coarse,
+                                        ix->coarse_norm, ix->coarse_max, nlist);
+            fill_lists(ctx, ix, lo, di, dc, n);
+            sync(ctx);
+        } catch (...) {
+            ix->free_all();
+            delete ix;
+            throw;
+        }
+        *outp = ix;
+    });
+}
+
+int pqg_ivf_build(pqg_ctx* ctx, const float* tables, uint32_t M, uint32_t ks, uint32_t ds,
+                  const uint8_t* codes, const uint64_t* ids, uint64_t n, uint64_t nlist,
+                  uint64_t seed, uint32_t kmeans_iters, pqg_index** outp) {
+    return guard([&] {
+        Scope sc(ctx);
+        // proj/src/ivf.cpp:126-131
+        if (n == 0) inval("ivf_build: no items");
+        if (nlist == 0 || nlist > n)
+            inval("ivf_build: nlist (" + std::to_string(nlist) + ") must be in [1, n_items=" +
+                  std::to_string(n) + "]");
+        check_pq_shape(M, ks, ds, "ivf_build");
+        const uint64_t D = uint64_t(M) * ds;
+        const uint64_t rb = uint64_t(M) * code_width(ks);
+        const float* dt = in(ctx, tables, uint64_t(M) * ks * ds);
+        const uint8_t* dc = in(ctx, codes, n * rb);
+        const uint64_t* di = in(ctx, ids, n);
+        // decode all (pq_decode, throws out_of_range) then kmeans_fit(decoded, nlist, iters, seed)
+        float* dec = scratch<float>(ctx, n * D);
+        reset_err(ctx);
+        pq_decode_dev(ctx, dc, n, M, ks, ds, dt, dec, ctx->d_err);
+        if (read_err(ctx)) fail(PQG_ERANGE, "pq_decode: code out of range for Ks=" + std::to_string(ks));
+        if (kmeans_iters < 1) inval("kmeans_fit: max_iters must be >= 1");
+        float* coarse = scratch<float>(ctx, nlist * D);
+        uint32_t* assign = scratch<uint32_t>(ctx, n);
+        run_kmeans(ctx, dec, n, D, 1, uint32_t(D), 0, nlist, kmeans_iters, {seed}, 1e-4, coarse, assign);
+        check_unique_ids(ctx, di, on_device(ids) ? nullptr : ids, n, "duplicate id ");
+        pqg_index* ix = new_index(ctx, M, ks, ds, nlist, n, dt, coarse);
+        try {
+            // the final pass leaves assignments consistent with the centroids (ivf.cpp:142-146)
+            fill_lists(ctx, ix, assign, di, dc, n);
+            sync(ctx);
+        } catch (...) {
+            ix->free_all();
+            delete ix;
+            throw;
+        }
+        *outp = ix;
+    });
+}
+
+int pqg_index_create(pqg_ctx* ctx, const float* tables, uint32_t M, uint32_t ks, uint32_t ds,
+                     const float* coarse, uint64_t nlist, const uint64_t* offsets,
+                     const uint64_t* ids, const uint8_t* codes, pqg_index** outp) {
+    return guard([&] {
+        Scope sc(ctx);
+        check_pq_shape(M, ks, ds, "index");
+        if (nlist == 0) inval("index: nlist must be >= 1");
+        std::vector<uint64_t> hoff(nlist + 1);
+        PQG_CUDA(cudaMemcpy(hoff.data(), offsets, sizeof(uint64_t) * (nlist + 1), cudaMemcpyDefault));
+        const uint64_t n = hoff[nlist];
+        if (hoff[0] != 0) inval("index: offsets[0] must be 0");
+        for (uint64_t l = 0; l < nlist; ++l)
+            if (hoff[l + 1] < hoff[l]) inval("index: offsets must be non-decreasing");
+        const float* dt = in(ctx, tables, uint64_t(M) * ks * ds);
+        const float* dco = in(ctx, coarse, nlist * M * ds);
+        pqg_index* ix = new_index(ctx, M, ks, ds, nlist, n, dt, dco);
+        try {
+            PQG_CUDA(cudaMemcpyAsync(ix->offsets, hoff.data(), sizeof(uint64_t) * (nlist + 1),
+                                     cudaMemcpyHostToDevice, ctx->stream));
+            if (n) {
+                PQG_CUDA(cudaMemcpyAsync(ix->ids, ids, sizeof(uint64_t) * n, cudaMemcpyDefault, ctx->stream));
+                PQG_CUDA(cudaMemcpyAsync(ix->codes, codes, n * ix->rb(), cudaMemcpyDefault, ctx->stream));
+            }
+            sync(ctx);
+        } catch (...) {
+            ix->free_all();
+            delete ix;
+            throw;
+        }
+        *outp = ix;
+    });
+}
+
+void pqg_index_destroy(pqg_index* ix) {
+    if (!ix) return;
+    cudaSetDevice(ix->device);
+    cudaDeviceSynchronize();
+    ix->free_all();
+    delete ix;
+}
+
+int pqg_index_info(const pqg_index* ix, uint64_t* nlist, uint64_t* n_items, uint32_t* M,
+                   uint32_t* ks, uint32_t* ds) {
+    return guard([&] {
+        if (!ix) inval("index: null");
+        if (nlist) *nlist = ix->nlist;
+        if (n_items) *n_items = ix->n;
+        if (M) *M = ix->M;
+        if (ks) *ks = ix->ks;
+        if (ds) *ds = ix->ds;
+    });
+}
+
+int pqg_index_export(pqg_ctx* ctx, const pqg_index* ix, uint64_t* offsets, uint64_t* ids,
+                     uint8_t* codes, float* coarse, float* tables) {
+    return guard([&] {
+        Scope sc(ctx);
+        if (offsets)
+            PQG_CUDA(cudaMemcpyAsync(offsets, ix->offsets, sizeof(uint64_t) * (ix->nlist + 1),
+                                     cudaMemcpyDefault, ctx->stream));
+        if (ids && ix->n)
+            PQG_CUDA(cudaMemcpyAsync(ids, ix->ids, sizeof(uint64_t) * ix->n, cudaMemcpyDefault, ctx->stream));
+        if (codes && ix->n)
+            PQG_CUDA(cudaMemcpyAsync(codes, ix->codes, ix->n * ix->rb(), cudaMemcpyDefault, ctx->stream));
+        if (coarse)
+            PQG_CUDA(cudaMemcpyAsync(coarse, ix->coarse, sizeof(float) * ix->nlist * ix->D(),
+                                     cudaMemcpyDefault, ctx->stream));
+        if (tables)
+            PQG_CUDA(cudaMemcpyAsync(tables, ix->tables, sizeof(float) * ix->M * ix->ks * ix->ds,
+                                     cudaMemcpyDefault, ctx->stream));
+        sync(ctx);
+    });
+}
+
+// Replace ix's lists with concat(ix lists, new lists) per list.
+static void concat_into(pqg_ctx* ctx, pqg_index* dst, const pqg_index* a, const uint64_t* off_b,
+                        const uint64_t* ids_b, const uint8_t* codes_b, uint64_t nb) {
+    const uint64_t total = a->n + nb;
+    uint64_t* off_o = dalloc<uint64_t>(a->nlist + 1);
+    uint64_t* ids_o = dalloc<uint64_t>(total);
+    uint8_t* codes_o = dalloc<uint8_t>(total * a->rb());
+    launch(ctx, "csr_concat", csr_concat_kernel, dim3(grid1d(total + a->nlist + 1, 256, ctx->num_sms * 16)),
+           dim3(256), 0, (const uint64_t*)a->offsets, (const uint64_t*)a->ids,
+           (const uint8_t*)a->codes, a->n, off_b, ids_b, codes_b, nb, a->nlist, a->rb(), off_o,
+           ids_o, codes_o);
+    sync(ctx);
+    if (dst->offsets) cudaFree(dst->offsets);
+    if (dst->ids) cudaFree(dst->ids);
+    if (dst->codes) cudaFree(dst->codes);
+    dst->offsets = off_o;
+    dst->ids = ids_o;
+    dst->codes = codes_o;
+    dst->n = total;
+}
+
+int pqg_index_add(pqg_ctx* ctx, pqg_index* ix, const uint8_t* codes, const uint64_t* ids,
+                  uint64_t n) {
+    return guard([&] {
+        Scope sc(ctx);
+        if (n == 0) return;
+        const uint64_t rb = ix->rb();
+        const uint8_t* dc = in(ctx, codes, n * rb);
+        const uint64_t* di = in(ctx, ids, n);
+        check_unique_ids(ctx, di, on_device(ids) ? nullptr : ids, n, "duplicate id ");
+        // collisions with the index: first new id (input order) already present
+        {
+            uint64_t* cat = scratch<uint64_t>(ctx, ix->n + n);
+            if (ix->n)
+                PQG_CUDA(cudaMemcpyAsync(cat, ix->ids, sizeof(uint64_t) * ix->n, cudaMemcpyDeviceToDevice, ctx->stream));
+            PQG_CUDA(cudaMemcpyAsync(cat + ix->n, di, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+            uint64_t* pos = scratch<uint64_t>(ctx, 1);
+            find_duplicate(ctx, cat, ix->n + n, pos);
+            uint64_t h = 0;
+            PQG_CUDA(cudaMemcpyAsync(&h, pos, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+            sync(ctx);
+            if (h != ~uint64_t(0)) {
+                uint64_t id = 0;
+                PQG_CUDA(cudaMemcpy(&id, cat + h, sizeof(id), cudaMemcpyDeviceToHost));
+                inval("ivf_add: id collision on id " + std::to_string(id));
+            }
+        }
+        uint32_t* lo = assign_lists(ctx, ix->tables, ix->M, ix->ks, ix->ds, dc, n, ix->coarse,
+                                    ix->coarse_norm, ix->coarse_max, ix->nlist);
+        uint64_t* off_b = scratch<uint64_t>(ctx, ix->nlist + 1);
+        Bucketing bk{off_b, scratch<uint32_t>(ctx, n)};
+        stable_bucket(ctx, lo, n, 1, ix->nlist, nullptr, bk);
+        uint64_t* ids_b = scratch<uint64_t>(ctx, n);
+        uint8_t* codes_b = scratch<uint8_t>(ctx, n * rb);
+        csr_scatter(ctx, bk.perm, n, di, dc, rb, ids_b, codes_b);
+        concat_into(ctx, ix, ix, off_b, ids_b, codes_b, n);
+    });
+}
+
+int pqg_index_merge(pqg_ctx* ctx, const pqg_index* a, const pqg_index* b, pqg_index** outp) {
+    return guard([&] {
+        Scope sc(ctx);
+        // proj/src/ivf.cpp:186-197
+        const uint64_t ntab = uint64_t(a->M) * a->ks * a->ds;
+        bool same_cb = a->M == b->M && a->ks == b->ks && a->ds == b->ds;
+        if (same_cb) {
+            std::vector<float> ta(ntab), tb(ntab);
+            PQG_CUDA(cudaMemcpy(ta.data(), a->tables, ntab * 4, cudaMemcpyDeviceToHost));
+            PQG_CUDA(cudaMemcpy(tb.data(), b->tables, ntab * 4, cudaMemcpyDeviceToHost));
+            for (uint64_t i = 0; i < ntab && same_cb; ++i) same_cb = ta[i] == tb[i];
+        }
+        if (!same_cb) inval("ivf_merge: codebook mismatch");
+        bool same_coarse = a->nlist == b->nlist;
+        if (same_coarse) {
+            const uint64_t nc = a->nlist * a->D();
+            std::vector<float> ca(nc), cb(nc);
+            PQG_CUDA(cudaMemcpy(ca.data(), a->coarse, nc * 4, cudaMemcpyDeviceToHost));
+            PQG_CUDA(cudaMemcpy(cb.data(), b->coarse, nc * 4, cudaMemcpyDeviceToHost));
+            for (uint64_t i = 0; i < nc && same_coarse; ++i) same_coarse = ca[i] == cb[i];
+        }
+        if (!same_coarse) inval("ivf_merge: coarse centroid mismatch");
+        if (a->n && b->n) {
+            uint64_t* cat = scratch<uint64_t>(ctx, a->n + b->n);
+            PQG_CUDA(cudaMemcpyAsync(cat, a->ids, sizeof(uint64_t) * a->n, cudaMemcpyDeviceToDevice, ctx->stream));
+            PQG_CUDA(cudaMemcpyAsync(cat + a->n, b->ids, sizeof(uint64_t) * b->n, cudaMemcpyDeviceToDevice, ctx->stream));
+            uint64_t* pos = scratch<uint64_t>(ctx, 1);
+            find_duplicate(ctx, cat, a->n + b->n, pos);
+            uint64_t h = 0;
+            PQG_CUDA(cudaMemcpyAsync(&h, pos, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+            sync(ctx);
+            if (h != ~uint64_t(0)) {
+                uint64_t id = 0;
+                PQG_CUDA(cudaMemcpy(&id, cat + h, sizeof(id), cudaMemcpyDeviceToHost));
+                inval("ivf_merge: id collision on id " + std::to_string(id));
+            }
+        }
+        pqg_index* o = new_index(ctx, a->M, a->ks, a->ds, a->nlist, 0, a->tables, a->coarse);
+        try {
+            concat_into(ctx, o, a, b->offsets, b->ids, b->codes, b->n);
+        } catch (...) {
+            o->free_all();
+            delete o;
+            throw;
+        }
+        *outp = o;
+    });
+}
+
+static void check_query(const pqg_index* ix, uint64_t k, uint64_t nprobe) {
+    // proj/src/ivf.cpp:103-114
+    if (k == 0) inval("query: k must be >= 1");
+    if (nprobe == 0 || nprobe > ix->nlist)
+        inval("query: nprobe (" + std::to_string(nprobe) + ") must be in [1, nlist=" +
+              std::to_string(ix->nlist) + "]");
+}
+
+int pqg_index_probe(pqg_ctx* ctx, const pqg_index* ix, const float* queries, uint64_t nq,
+                    uint64_t nprobe, uint32_t* probes) {
+    return guard([&] {
+        Scope sc(ctx);
+        check_query(ix, 1, nprobe);
+        if (nq == 0) return;
+        const float* dq = in(ctx, queries, nq * ix->D());
+        auto op = out(ctx, probes, nq * nprobe);
+        ivf_probe(ctx, ix->view(), dq, nq, nprobe, op.dev);
+        finish(ctx, op);
+        sync(ctx);
+    });
+}
+
+int pqg_index_search(pqg_ctx* ctx, const pqg_index* ix, const float* queries, uint64_t nq,
+                     uint64_t k, uint64_t nprobe, int has_max, double max_sq_dist,
+                     uint64_t* out_ids, double* out_dists, uint32_t* out_counts) {
+    return guard([&] {
+        Scope sc(ctx);
+        check_query(ix, k, nprobe);
+        if (nq == 0) return;
+        const float* dq = in(ctx, queries, nq * ix->D());
+        auto oi = out(ctx, out_ids, nq * k);
+        auto od = out(ctx, out_dists, nq * k);
+        auto oc = out(ctx, out_counts, nq);
+        uint32_t* probes = scratch<uint32_t>(ctx, nq * nprobe);
+        ivf_probe(ctx, ix->view(), dq, nq, nprobe, probes);
+        reset_err(ctx);
+        ivf_scan(ctx, ix->view(), dq, nq, probes, nprobe, k, has_max, max_sq_dist, oi.dev, od.dev,
+                 oc.dev, ctx->d_err);
+        finish(ctx, oi);
+        finish(ctx, od);
+        finish(ctx, oc);
+        if (oi.host || od.host || oc.host) {
+            if (read_err(ctx)) fail(PQG_ERANGE, "adc_lookup: code out of range");
+        }
+    });
+}
+
+int pqg_flat_scan(pqg_ctx* ctx, const float* tables, uint32_t M, uint32_t ks, uint32_t ds,
+                  const uint8_t* codes, const uint64_t* ids, uint64_t n, const float* queries,
+                  uint64_t nq, uint64_t k, int has_max, double max_sq_dist, uint64_t* out_ids,
+                  double* out_dists, uint32_t* out_counts) {
+    return guard([&] {
+        Scope sc(ctx);
+        // proj/src/ivf.cpp:250-252
+        if (k == 0) inval("flat_scan: k must be >= 1");
+        check_pq_shape(M, ks, ds, "flat_scan");
+        if (nq == 0) return;
+        const uint64_t rb = uint64_t(M) * code_width(ks);
+        const float* dt = in(ctx, tables, uint64_t(M) * ks * ds);
+        const uint8_t* dc = in(ctx, codes, n * rb);
+        const uint64_t* di = in(ctx, ids, n);
+        const float* dq = in(ctx, queries, nq * M * ds);
+        uint64_t* off = scratch<uint64_t>(ctx, 2);
+        const uint64_t hoff[2] = {0, n};
+        PQG_CUDA(cudaMemcpyAsync(off, hoff, sizeof(hoff), cudaMemcpyHostToDevice, ctx->stream));
+        uint32_t* probes = scratch<uint32_t>(ctx, nq);
+        PQG_CUDA(cudaMemsetAsync(probes, 0, sizeof(uint32_t) * nq, ctx->stream));
+        IndexView v{dt, M, ks, ds, code_width(ks), nullptr, nullptr, nullptr, 1, off, di, dc, n};
+        auto oi = out(ctx, out_ids, nq * k);
+        auto od = out(ctx, out_dists, nq * k);
+        auto oc = out(ctx, out_counts, nq);
+        reset_err(ctx);
+        ivf_scan(ctx, v, dq, nq, probes, 1, k, has_max, max_sq_dist, oi.dev, od.dev, oc.dev, ctx->d_err);
+        finish(ctx, oi);
+        finish(ctx, od);
+        finish(ctx, oc);
+        if (read_err(ctx)) fail(PQG_ERANGE, "adc_lookup: code out of range");
+    });
+}
+
+int pqg_topk_merge(pqg_ctx* ctx, const uint64_t* ids, const double* dists,
+                   const uint32_t* counts, uint32_t shards, uint64_t nq, uint64_t k,
+                   uint64_t* out_ids, double* out_dists, uint32_t* out_counts) {
+    return guard([&] {
+        Scope sc(ctx);
+        if (nq == 0 || shards == 0) return;
+        const uint64_t* di = in(ctx, ids, uint64_t(shards) * nq * k);
+        const double* dd = in(ctx, dists, uint64_t(shards) * nq * k);
+        const uint32_t* dc = in(ctx, counts, uint64_t(shards) * nq);
+        auto oi = out(ctx, out_ids, nq * k);
+        auto od = out(ctx, out_dists, nq * k);
+        auto oc = out(ctx, out_counts, nq);
+        topk_merge_dev(ctx, di, dd, dc, shards, nq, k, oi.dev, od.dev, oc.dev);
+        finish(ctx, oi);
+        finish(ctx, od);
+        finish(ctx, oc);
+        if (oi.host || od.host || oc.host) sync(ctx);
+    });
+}
+
+int pqg_assign_pass(pqg_ctx* ctx, const float* rows, uint64_t n, uint64_t ld, uint32_t B,
+                    uint32_t d, uint32_t col_stride, const float* tables, uint64_t k,
+                    uint32_t* assign, double* dist) {
+    return guard([&] {
+        Scope sc(ctx);
+        if (k == 0) inval("nearest_centroid: empty centroid set");
+        if (n == 0) return;
+        const float* dr = in(ctx, rows, n * ld);
+        const float* dt = in(ctx, tables, uint64_t(B) * k * d);
+        auto oa = out(ctx, assign, uint64_t(B) * n);
+        auto od = out(ctx, dist, uint64_t(B) * n);
+        float* cnorm = scratch<float>(ctx, uint64_t(B) * k);
+        float* cmax = scratch<float>(ctx, B);
+        table_norms(ctx, dt, B, k, d, cnorm, cmax);
+        NearestArgs a;
+        a.src.x = dr;
+        a.src.ldx = ld;
+        a.src.col_stride = col_stride;
+        a.n = n;
+        a.d = d;
+        a.B = B;
+        a.table = dt;
+        a.k = k;
+        a.cnorm = cnorm;
+        a.cmax = cmax;
+        a.out_idx = oa.dev;
+        a.idx_bytes = 4;
+        a.idx_rs = 1;
+        a.idx_ps = n;
+        a.out_dist = od.dev;
+        nearest(ctx, a);
+        finish(ctx, oa);
+        finish(ctx, od);
+        if (oa.host || od.host) sync(ctx);
+    });
+}
+
+int pqg_update_pass(pqg_ctx* ctx, const float* rows, uint64_t n, uint64_t ld, uint32_t B,
+                    uint32_t d, uint32_t col_stride, float* tables, uint64_t k,
+                    const uint32_t* assign, double* dist) {
+    return guard([&] {
+        Scope sc(ctx);
+        if (n == 0) return;
+        const float* dr = in(ctx, rows, n * ld);
+        const uint32_t* da = in(ctx, assign, uint64_t(B) * n);
+        auto ot = out(ctx, tables, uint64_t(B) * k * d);
+        if (ot.host)
+            PQG_CUDA(cudaMemcpyAsync(ot.dev, tables, sizeof(float) * B * k * d, cudaMemcpyHostToDevice, ctx->stream));
+        auto odist = out(ctx, dist, uint64_t(B) * n);
+        if (odist.host)
+            PQG_CUDA(cudaMemcpyAsync(odist.dev, dist, sizeof(double) * B * n, cudaMemcpyHostToDevice, ctx->stream));
+        RowSrc src;
+        src.x = dr;
+        src.ldx = ld;
+        src.col_stride = col_stride;
+        kmeans_update(ctx, src, n, B, d, ot.dev, k, da, odist.dev, nullptr);
+        finish(ctx, ot);
+        finish(ctx, odist);
+        if (ot.host || odist.host) sync(ctx);
+    });
+}
+
+}  // extern "C"

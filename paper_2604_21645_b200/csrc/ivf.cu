@@ -1,0 +1,462 @@
+// ivf.cu -- K6 posting-list scatter, K8 coarse probe selection, K9 ADC scan
+// with per-warp exact top-k, K10 shard top-k merge, id-uniqueness checks.
+//
+//  probe_order   proj/src/ivf.cpp:91-101  nprobe smallest (fp64 dist, list)
+//  scan_list     proj/src/ivf.cpp:70-77   adc_lookup + max_sq_dist filter
+//  finalize_hits proj/src/ivf.cpp:51-68   k smallest by (dist, id), sorted
+//  check_ids_unique proj/src/ivf.cpp:19-26
+//
+// Exactness.  Probe: the fp32 screen matrix (nearest.cu, error <= E per
+// query) gives tau = nprobe-th smallest screened value; every list whose
+// screened value exceeds tau + 2E is provably outside the fp64 top-nprobe, so
+// only lists within that band are re-scored in the reference's fp64 and
+// selected by (dist, index).  Scan: each candidate's fp32 LUT sum s32 bounds
+// the reference's fp64 sum (all terms >= 0, relative error <= (M+1) u); a
+// candidate is re-scored in fp64 -- the same float entries added in m order,
+// exactly adc_lookup -- only if s32 could beat the warp's current k-th hit.
+#include <cfloat>
+
+#include "kernels.cuh"
+
+namespace pqg {
+
+namespace {
+
+__device__ __forceinline__ uint32_t code_at(const uint8_t* p, uint32_t m, uint32_t w) {
+    p += m * w;
+    return w == 1 ? uint32_t(p[0]) : (uint32_t(p[0]) | (uint32_t(p[1]) << 8));
+}
+
+// ---------------------------------------------------------------------------
+// probe selection
+// ---------------------------------------------------------------------------
+constexpr int kSelThreads = 256;
+constexpr int kCandCap = 1024;
+
+__device__ __forceinline__ bool pair_less(double a, uint64_t ia, double b, uint64_t ib) {
+    return a < b || (a == b && ia < ib);
+}
+
+// Bitonic sort of (dist, idx) pairs in shared memory, n a power of two.
+__device__ void bitonic_sort(double* d, uint32_t* ix, int n) {
+    for (int size = 2; size <= n; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            __syncthreads();
+            for (int t = threadIdx.x; t < n / 2; t += blockDim.x) {
+                const int lo = 2 * t - (t & (stride - 1));
+                const int hi = lo + stride;
+                const bool up = ((lo & size) == 0);
+                const bool sw = up ? pair_less(d[hi], ix[hi], d[lo], ix[lo])
+                                   : pair_less(d[lo], ix[lo], d[hi], ix[hi]);
+                if (sw) {
+                    const double td = d[lo]; d[lo] = d[hi]; d[hi] = td;
+                    const uint32_t ti = ix[lo]; ix[lo] = ix[hi]; ix[hi] = ti;
+                }
+            }
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSelThreads) probe_select_kernel(
+    const float* mat, uint64_t ld, const float* row_err, const float* queries, uint64_t D,
+    const float* coarse, uint64_t nlist, uint64_t nprobe, uint64_t q0, uint32_t* probes,
+    uint32_t* overflow, unsigned* n_overflow) {
+    __shared__ uint32_t hist[256];
+    __shared__ uint32_t s_prefix, s_rank;
+    __shared__ uint32_t cand[kCandCap];
+    __shared__ double cd[kCandCap];
+    __shared__ unsigned cnt;
+    const uint64_t ql = blockIdx.x;  // query within this chunk
+    const uint64_t q = q0 + ql;
+    const float* v = mat + ql * ld;
+    const float E = row_err[ql];
+    if (threadIdx.x == 0) { s_prefix = 0; s_rank = uint32_t(nprobe); cnt = 0; }
+    uint32_t mask = 0;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+        __syncthreads();
+        const uint32_t prefix = s_prefix;
+        for (uint64_t j = threadIdx.x; j < nlist; j += blockDim.x) {
+            const uint32_t bits = __float_as_uint(v[j]);
+            if ((bits & mask) == prefix) atomicAdd(&hist[(bits >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t r = s_rank, dg = 0;
+            for (; dg < 256; ++dg) {
+                if (hist[dg] >= r) break;
+                r -= hist[dg];
+            }
+            s_rank = r;
+            s_prefix = prefix | (dg << shift);
+        }
+        mask |= 255u << shift;
+        __syncthreads();
+    }
+    const float tau = __uint_as_float(s_prefix);
+    const float band = tau + 2.05f * E;
+    for (uint64_t j = threadIdx.x; j < nlist; j += blockDim.x) {
+        if (v[j] <= band) {
+            const unsigned p = atomicAdd(&cnt, 1u);
+            if (p < kCandCap) cand[p] = uint32_t(j);
+        }
+    }
+    __syncthreads();
+    const unsigned c = cnt;
+    if (c > kCandCap) {
+        if (threadIdx.x == 0) overflow[atomicAdd(n_overflow, 1u)] = uint32_t(q);
+        return;
+    }
+    int n2 = 1;
+    while (n2 < int(c)) n2 <<= 1;
+    const float* qv = queries + q * D;
+    for (int t = threadIdx.x; t < n2; t += blockDim.x) {
+        if (t < int(c)) cd[t] = exact_sq_l2(qv, coarse + uint64_t(cand[t]) * D, int(D));
+        else { cd[t] = __longlong_as_double(0x7ff0000000000000LL); cand[t] = 0xFFFFFFFFu; }
+    }
+    bitonic_sort(cd, cand, n2);
+    for (uint64_t p = threadIdx.x; p < nprobe; p += blockDim.x) probes[q * nprobe + p] = cand[p];
+}
+
+// Rare fallback (more than kCandCap lists inside the screen band, e.g. many
+// duplicate coarse centroids): exact fp64 for every list, then nprobe rounds
+// of a block-wide (dist, index) argmin.
+__global__ void probe_exact_kernel(const uint32_t* overflow, const unsigned* n_overflow,
+                                   const float* queries, uint64_t D, const float* coarse,
+                                   uint64_t nlist, uint64_t nprobe, double* scratch_d,
+                                   uint32_t* probes) {
+    __shared__ double sv[32];
+    __shared__ uint64_t si[32];
+    const unsigned total = *n_overflow;
+    for (unsigned o = blockIdx.x; o < total; o += gridDim.x) {
+        const uint64_t q = overflow[o];
+        double* dd = scratch_d + uint64_t(blockIdx.x) * nlist;
+        for (uint64_t j = threadIdx.x; j < nlist; j += blockDim.x)
+            dd[j] = exact_sq_l2(queries + q * D, coarse + j * D, int(D));
+        __syncthreads();
+        for (uint64_t p = 0; p < nprobe; ++p) {
+            double bv = __longlong_as_double(0x7ff0000000000000LL);
+            uint64_t bi = ~uint64_t(0);
+            for (uint64_t j = threadIdx.x; j < nlist; j += blockDim.x) {
+                const double x = dd[j];
+                if (x == -1.0) continue;  // taken
+                if (bi == ~uint64_t(0) || pair_less(x, j, bv, bi)) { bv = x; bi = j; }
+            }
+            for (int off = 16; off >= 1; off >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+                const uint64_t oi = __shfl_xor_sync(0xffffffffu, bi, off);
+                if (oi != ~uint64_t(0) && (bi == ~uint64_t(0) || pair_less(ov, oi, bv, bi))) { bv = ov; bi = oi; }
+            }
+            const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+            if (lane == 0) { sv[w] = bv; si[w] = bi; }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                for (int i = 1; i < int(blockDim.x >> 5); ++i)
+                    if (si[i] != ~uint64_t(0) && (bi == ~uint64_t(0) || pair_less(sv[i], si[i], bv, bi))) { bv = sv[i]; bi = si[i]; }
+                probes[q * nprobe + p] = uint32_t(bi);
+                dd[bi] = -1.0;
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// ADC scan with an exact per-warp top-k (k <= 32)
+// ---------------------------------------------------------------------------
+constexpr int kScanThreads = 256;
+
+struct TopK {
+    double d;
+    uint64_t id;
+};
+
+// Insert (d, id) into the warp's sorted list (lane l < k holds entry l).
+__device__ __forceinline__ void warp_insert(double& my_d, uint64_t& my_id, double d, uint64_t id,
+                                           int k, int lane) {
+    const bool before = lane < k && pair_less(my_d, my_id, d, id);
+    const uint32_t m = __ballot_sync(0xffffffffu, before);
+    const int pos = __popc(m);
+    const double up_d = __shfl_up_sync(0xffffffffu, my_d, 1);
+    const uint64_t up_id = __shfl_up_sync(0xffffffffu, my_id, 1);
+    if (pos < k) {
+        if (lane == pos) { my_d = d; my_id = id; }
+        else if (lane > pos && lane < k) { my_d = up_d; my_id = up_id; }
+    }
+}
+
+__global__ void __launch_bounds__(kScanThreads) adc_scan_kernel(
+    const float* tables, uint32_t M, uint32_t ks, uint32_t ds, const float* queries,
+    const uint64_t* offsets, const uint64_t* ids, const uint8_t* codes, const uint32_t* probes,
+    uint64_t nprobe, int k, int has_max, double max_sq, uint64_t* out_ids, double* out_dists,
+    uint32_t* out_counts, int* err) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* lut = reinterpret_cast<float*>(smem_raw);  // [M][ks]
+    TopK* wl = reinterpret_cast<TopK*>(smem_raw + ((sizeof(float) * M * ks + 15) & ~size_t(15)));
+    const uint64_t q = blockIdx.x;
+    const uint32_t w = ks <= 256 ? 1 : 2;
+    const uint32_t rb = M * w;
+    const uint64_t D = uint64_t(M) * ds;
+    const float* qv = queries + q * D;
+    for (uint32_t e = threadIdx.x; e < M * ks; e += blockDim.x) {
+        const uint32_t m = e / ks;
+        lut[e] = __double2float_rn(exact_sq_l2(qv + uint64_t(m) * ds, tables + uint64_t(e) * ds, int(ds)));
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+    double my_d = inf;
+    uint64_t my_id = ~uint64_t(0);
+    const float shrink = 1.0f - float(M + 2) * kU * 1.05f;
+    for (uint64_t p = 0; p < nprobe; ++p) {
+        const uint32_t l = probes[q * nprobe + p];
+        const uint64_t beg = offsets[l], end = offsets[l + 1];
+        for (uint64_t base = beg + uint64_t(wid) * 32; base < end; base += kScanThreads) {
+            const double th = __shfl_sync(0xffffffffu, my_d, k - 1);
+            const uint64_t e = base + lane;
+            bool want = false;
+            double s64 = 0.0;
+            uint64_t id = 0;
+            if (e < end) {
+                const uint8_t* cr = codes + e * rb;
+                float s32 = 0.f;
+                bool bad = false;
+                for (uint32_t m = 0; m < M; ++m) {
+                    const uint32_t c = code_at(cr, m, w);
+                    if (c >= ks) { bad = true; break; }
+                    s32 += lut[m * ks + c];
+                }
+                if (bad) atomicExch(err, 1);
+                const double lower = double(s32) * double(shrink);
+                if (!bad && lower <= th && !(has_max && lower > max_sq)) {
+                    for (uint32_t m = 0; m < M; ++m)
+                        s64 = __dadd_rn(s64, (double)lut[m * ks + code_at(cr, m, w)]);
+                    id = ids[e];
+                    want = !(has_max && s64 > max_sq);
+                }
+            }
+            uint32_t ball = __ballot_sync(0xffffffffu, want);
+            while (ball) {
+                const int src = __ffs(ball) - 1;
+                ball &= ball - 1;
+                const double cd = __shfl_sync(0xffffffffu, s64, src);
+                const uint64_t cid = __shfl_sync(0xffffffffu, id, src);
+                const double thd = __shfl_sync(0xffffffffu, my_d, k - 1);
+                const uint64_t thi = __shfl_sync(0xffffffffu, my_id, k - 1);
+                if (pair_less(cd, cid, thd, thi)) warp_insert(my_d, my_id, cd, cid, k, lane);
+            }
+        }
+    }
+    // merge the warps' lists through shared memory into warp 0
+    if (lane < k) wl[wid * k + lane] = TopK{my_d, my_id};
+    __syncthreads();
+    if (wid != 0) return;
+    for (int ow = 1; ow < int(kScanThreads / 32); ++ow) {
+        for (int j = 0; j < k; ++j) {
+            const TopK c = wl[ow * k + j];
+            const double thd = __shfl_sync(0xffffffffu, my_d, k - 1);
+            const uint64_t thi = __shfl_sync(0xffffffffu, my_id, k - 1);
+            if (!pair_less(c.d, c.id, thd, thi)) break;  // lists are sorted
+            warp_insert(my_d, my_id, c.d, c.id, k, lane);
+        }
+    }
+    const bool valid = lane < k && my_id != ~uint64_t(0);
+    const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+    if (lane < k) {
+        out_ids[q * k + lane] = valid ? my_id : 0;
+        out_dists[q * k + lane] = valid ? my_d : 0.0;
+    }
+    if (lane == 0) out_counts[q] = __popc(vm);
+}
+
+// ---------------------------------------------------------------------------
+// CSR scatter, duplicate detection, shard merge
+// ---------------------------------------------------------------------------
+__global__ void csr_scatter_kernel(const uint32_t* perm, uint64_t n, const uint64_t* ids,
+                                   const uint8_t* codes, uint64_t rb, uint64_t* out_ids,
+                                   uint8_t* out_codes) {
+    for (uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < n;
+         p += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t src = perm[p];
+        out_ids[p] = ids[src];
+        const uint8_t* s = codes + src * rb;
+        uint8_t* d = out_codes + p * rb;
+        if (rb == 16) {
+            *reinterpret_cast<uint4*>(d) = *reinterpret_cast<const uint4*>(s);
+        } else if (rb == 8) {
+            *reinterpret_cast<uint2*>(d) = *reinterpret_cast<const uint2*>(s);
+        } else {
+            for (uint64_t j = 0; j < rb; ++j) d[j] = s[j];
+        }
+    }
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdULL;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ULL;
+    x ^= x >> 33;
+    return x;
+}
+
+// Open-addressing set: state 0 empty / 1 being written / 2 ready; minpos
+// keeps the first input position of each id.
+__global__ void dup_insert_kernel(const uint64_t* ids, uint64_t n, uint64_t cap_mask,
+                                  int* state, uint64_t* keys, unsigned long long* minpos) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t id = ids[i];
+        uint64_t s = mix64(id) & cap_mask;
+        for (;;) {
+            int st = atomicCAS(state + s, 0, 1);
+            if (st == 0) {
+                keys[s] = id;
+                __threadfence();
+                atomicExch(state + s, 2);
+                atomicMin(minpos + s, (unsigned long long)i);
+                break;
+            }
+            while ((st = atomicAdd(state + s, 0)) != 2) {}
+            __threadfence();
+            if (keys[s] == id) {
+                atomicMin(minpos + s, (unsigned long long)i);
+                break;
+            }
+            s = (s + 1) & cap_mask;
+        }
+    }
+}
+
+__global__ void dup_find_kernel(const uint64_t* ids, uint64_t n, uint64_t cap_mask,
+                                const uint64_t* keys, const unsigned long long* minpos,
+                                unsigned long long* first_dup) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t id = ids[i];
+        uint64_t s = mix64(id) & cap_mask;
+        while (keys[s] != id) s = (s + 1) & cap_mask;
+        if (minpos[s] != i) atomicMin(first_dup, (unsigned long long)i);
+    }
+}
+
+__global__ void topk_merge_kernel(const uint64_t* ids, const double* dists, const uint32_t* counts,
+                                  uint32_t shards, uint64_t nq, uint64_t k, uint64_t* out_ids,
+                                  double* out_dists, uint32_t* out_counts) {
+    for (uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nq;
+         q += uint64_t(gridDim.x) * blockDim.x) {
+        uint32_t pos[64];
+        for (uint32_t s = 0; s < shards; ++s) pos[s] = 0;
+        uint32_t outc = 0;
+        while (outc < k) {
+            int best = -1;
+            double bd = 0;
+            uint64_t bi = 0;
+            for (uint32_t s = 0; s < shards; ++s) {
+                const uint64_t base = (uint64_t(s) * nq + q) * k;
+                if (pos[s] >= counts[uint64_t(s) * nq + q]) continue;
+                const double d = dists[base + pos[s]];
+                const uint64_t id = ids[base + pos[s]];
+                if (best < 0 || pair_less(d, id, bd, bi)) { best = int(s); bd = d; bi = id; }
+            }
+            if (best < 0) break;
+            ++pos[best];
+            out_ids[q * k + outc] = bi;
+            out_dists[q * k + outc] = bd;
+            ++outc;
+        }
+        for (uint32_t j = outc; j < k; ++j) { out_ids[q * k + j] = 0; out_dists[q * k + j] = 0.0; }
+        out_counts[q] = outc;
+    }
+}
+
+}  // namespace
+
+void ivf_probe(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t nq,
+               uint64_t nprobe, uint32_t* probes) {
+    const uint64_t D = uint64_t(ix.M) * ix.ds;
+    // chunk the queries so the screen matrix stays <= 512 MB
+    uint64_t chunk = std::max<uint64_t>(1, (uint64_t(128) << 20) / std::max<uint64_t>(1, ix.nlist));
+    chunk = std::min<uint64_t>(chunk, nq);
+    float* mat = scratch<float>(ctx, chunk * ix.nlist);
+    float* rerr = scratch<float>(ctx, chunk);
+    uint32_t* overflow = scratch<uint32_t>(ctx, nq);
+    unsigned* n_over = scratch<unsigned>(ctx, 1);
+    PQG_CUDA(cudaMemsetAsync(n_over, 0, sizeof(unsigned), ctx->stream));
+    for (uint64_t q0 = 0; q0 < nq; q0 += chunk) {
+        const uint64_t nc = std::min(chunk, nq - q0);
+        NearestArgs a;
+        a.src.x = queries + q0 * D;
+        a.src.ldx = D;
+        a.n = nc;
+        a.d = uint32_t(D);
+        a.B = 1;
+        a.table = ix.coarse;
+        a.k = ix.nlist;
+        a.cnorm = ix.coarse_norm;
+        a.cmax = ix.coarse_max;
+        a.out_mat = mat;
+        a.ld_mat = ix.nlist;
+        a.row_err = rerr;
+        distance_matrix(ctx, a);
+        launch(ctx, "probe_select", probe_select_kernel, dim3(unsigned(nc)), dim3(kSelThreads), 0,
+               (const float*)mat, ix.nlist, (const float*)rerr, queries, D, ix.coarse, ix.nlist,
+               nprobe, q0, probes, overflow, n_over);
+    }
+    const unsigned fb_blocks = 64;
+    double* sd = scratch<double>(ctx, uint64_t(fb_blocks) * ix.nlist);
+    launch(ctx, "probe_exact", probe_exact_kernel, dim3(fb_blocks), dim3(256), 0,
+           (const uint32_t*)overflow, (const unsigned*)n_over, queries, D, ix.coarse, ix.nlist,
+           nprobe, sd, probes);
+}
+
+void ivf_scan(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t nq,
+              const uint32_t* probes, uint64_t nprobe, uint64_t k, int has_max, double max_sq,
+              uint64_t* out_ids, double* out_dists, uint32_t* out_counts, int* err) {
+    if (k > 32) fail(PQG_EUNSUPPORTED, "search: k > 32 is not supported by the warp top-k path");
+    const size_t lut_bytes = (sizeof(float) * ix.M * ix.ks + 15) & ~size_t(15);
+    const size_t smem = lut_bytes + sizeof(TopK) * k * (kScanThreads / 32);
+    if (smem > 220 * 1024) fail(PQG_EUNSUPPORTED, "search: M*ks lookup table exceeds shared memory");
+    set_smem(adc_scan_kernel, smem);
+    for (uint64_t q0 = 0; q0 < nq; q0 += 65535) {
+        const uint64_t nc = std::min<uint64_t>(65535, nq - q0);
+        launch(ctx, "adc_scan", adc_scan_kernel, dim3(unsigned(nc)), dim3(kScanThreads), smem,
+               ix.tables, ix.M, ix.ks, ix.ds, queries + q0 * ix.M * ix.ds, ix.offsets, ix.ids,
+               ix.codes, probes + q0 * nprobe, nprobe, int(k), has_max, max_sq, out_ids + q0 * k,
+               out_dists + q0 * k, out_counts + q0, err);
+    }
+}
+
+void csr_scatter(pqg_ctx* ctx, const uint32_t* perm, uint64_t n, const uint64_t* ids,
+                 const uint8_t* codes, uint64_t row_bytes, uint64_t* out_ids, uint8_t* out_codes) {
+    launch(ctx, "csr_scatter", csr_scatter_kernel, dim3(grid1d(n, 256, ctx->num_sms * 16)), dim3(256),
+           0, perm, n, ids, codes, row_bytes, out_ids, out_codes);
+}
+
+void find_duplicate(pqg_ctx* ctx, const uint64_t* ids, uint64_t n, uint64_t* first_dup_pos) {
+    uint64_t cap = 1;
+    while (cap < 2 * n) cap <<= 1;
+    int* state = scratch<int>(ctx, cap);
+    uint64_t* keys = scratch<uint64_t>(ctx, cap);
+    unsigned long long* minpos = scratch<unsigned long long>(ctx, cap);
+    PQG_CUDA(cudaMemsetAsync(state, 0, sizeof(int) * cap, ctx->stream));
+    PQG_CUDA(cudaMemsetAsync(minpos, 0xff, sizeof(unsigned long long) * cap, ctx->stream));
+    PQG_CUDA(cudaMemsetAsync(first_dup_pos, 0xff, sizeof(uint64_t), ctx->stream));
+    const unsigned g = grid1d(n, 256, ctx->num_sms * 16);
+    launch(ctx, "dup_check", dup_insert_kernel, dim3(g), dim3(256), 0, ids, n, cap - 1, state, keys,
+           minpos);
+    launch(ctx, "dup_check", dup_find_kernel, dim3(g), dim3(256), 0, ids, n, cap - 1,
+           (const uint64_t*)keys, (const unsigned long long*)minpos,
+           reinterpret_cast<unsigned long long*>(first_dup_pos));
+}
+
+void topk_merge_dev(pqg_ctx* ctx, const uint64_t* ids, const double* dists,
+                    const uint32_t* counts, uint32_t shards, uint64_t nq, uint64_t k,
+                    uint64_t* out_ids, double* out_dists, uint32_t* out_counts) {
+    if (shards > 64) fail(PQG_EUNSUPPORTED, "topk_merge: at most 64 shards");
+    launch(ctx, "topk_merge", topk_merge_kernel, dim3(grid1d(nq, 128, 65535)), dim3(128), 0, ids,
+           dists, counts, shards, nq, k, out_ids, out_dists, out_counts);
+}
+
+}  // namespace pqg

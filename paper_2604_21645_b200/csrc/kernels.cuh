@@ -1,0 +1,115 @@
+// kernels.cuh -- host-side launchers of the libpqg kernels.
+#pragma once
+
+#include "common.cuh"
+
+namespace pqg {
+
+// Where the rows of a nearest-centroid problem come from.
+//  dense  : x[i * ldx + b * col_stride + t]               (b = problem index)
+//  decoded: x[i][t] = tables[m][code(i, m)][t - m*ds]     (pq_decode_row)
+struct RowSrc {
+    const float* x = nullptr;
+    uint64_t ldx = 0;
+    uint32_t col_stride = 0;
+    const uint8_t* codes = nullptr;  // decoded mode when non-null
+    const float* dtab = nullptr;
+    uint32_t dM = 0, dks = 0, dds = 0, dw = 1;
+};
+
+// B independent argmin problems over the same n rows; problem b has a k x d
+// centroid table at table + b*k*d.  Output index of (row i, problem b) goes
+// to out_idx[(i*idx_rs + b*idx_ps)] with idx_bytes in {1,2,4}; optional
+// fp64 distance to dist[b*n + i].  Rows whose fp32 screen cannot prove the
+// fp64 winner are appended to flags and resolved by the fixup kernel.
+struct NearestArgs {
+    RowSrc src;
+    uint64_t n = 0;
+    uint32_t d = 0;
+    uint32_t B = 1;
+    const float* table = nullptr;
+    uint64_t k = 0;
+    const float* cnorm = nullptr;  // [B][k]
+    const float* cmax = nullptr;   // [B]
+    void* out_idx = nullptr;
+    int idx_bytes = 4;
+    uint64_t idx_rs = 1, idx_ps = 0;
+    double* out_dist = nullptr;
+    // sse mode: accumulate exact (x - c_win)^2 per row into sse_row[i] (fp64)
+    double* sse_part = nullptr;
+    unsigned long long* flag_count = nullptr;
+    uint64_t* flags = nullptr;
+    const int* active = nullptr;
+    // distance-matrix mode: write screened fp32 distances (plus row margin)
+    float* out_mat = nullptr;
+    uint64_t ld_mat = 0;
+    float* row_err = nullptr;  // [n] screen error bound per row (matrix mode)
+};
+
+// nearest.cu
+void table_norms(pqg_ctx* ctx, const float* table, uint32_t B, uint64_t k, uint32_t d,
+                 float* cnorm, float* cmax);
+void nearest(pqg_ctx* ctx, NearestArgs a);           // screen + exact fixup
+void distance_matrix(pqg_ctx* ctx, NearestArgs a);   // fp32 screen values only
+
+// kmeans.cu
+struct Bucketing {
+    uint64_t* offsets;  // [B][k+1]
+    uint32_t* perm;     // [B][n] rows in key order, stable
+};
+void stable_bucket(pqg_ctx* ctx, const uint32_t* keys, uint64_t n, uint32_t B, uint64_t k,
+                   const int* active, Bucketing out);
+void exclusive_scan_u32(pqg_ctx* ctx, const uint32_t* in, uint64_t* out, uint64_t count);
+void gather_rows(pqg_ctx* ctx, const float* x, uint64_t ldx, uint32_t B, uint32_t d,
+                 uint32_t col_stride, const uint64_t* rows, uint64_t k, float* table);
+struct KMeansState {
+    int* active;          // [B]
+    double* prev;         // [B]
+    double* inertia;      // [B]
+    double* per_iter;     // [B][max_iters]
+    uint32_t* iters;      // [B]
+};
+void kmeans_inertia_and_stop(pqg_ctx* ctx, const double* dist, uint64_t n, uint32_t B,
+                             uint32_t it, uint32_t max_iters, double tol, KMeansState st);
+void kmeans_update(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint32_t d,
+                   float* table, uint64_t k, const uint32_t* assign, double* dist,
+                   const int* active);
+
+// pq.cu
+void pq_decode_dev(pqg_ctx* ctx, const uint8_t* codes, uint64_t n, uint32_t M, uint32_t ks,
+                   uint32_t ds, const float* tables, float* out, int* err);
+void sq_error_dev(pqg_ctx* ctx, const float* a, const float* b, uint64_t count, double* sse);
+void recon_sse_dev(pqg_ctx* ctx, const float* x, const uint8_t* codes, uint64_t n, uint32_t M,
+                   uint32_t ks, uint32_t ds, const float* tables, double* sse, int* err);
+void adc_tables_dev(pqg_ctx* ctx, const float* tables, uint32_t M, uint32_t ks, uint32_t ds,
+                    const float* queries, uint64_t nq, float* entries);
+void adc_lookup_dev(pqg_ctx* ctx, const float* entries, uint32_t M, uint32_t ks,
+                    const uint8_t* codes, uint64_t n, double* out, int* err);
+void reduce_sum_f64(pqg_ctx* ctx, const double* parts, uint64_t count, double* out);
+
+// ivf.cu
+struct IndexView {
+    const float* tables;
+    uint32_t M, ks, ds, w;
+    const float* coarse;
+    const float* coarse_norm;
+    const float* coarse_max;
+    uint64_t nlist;
+    const uint64_t* offsets;
+    const uint64_t* ids;
+    const uint8_t* codes;
+    uint64_t n;
+};
+void ivf_probe(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t nq,
+               uint64_t nprobe, uint32_t* probes);
+void ivf_scan(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t nq,
+              const uint32_t* probes, uint64_t nprobe, uint64_t k, int has_max, double max_sq,
+              uint64_t* out_ids, double* out_dists, uint32_t* out_counts, int* err);
+void csr_scatter(pqg_ctx* ctx, const uint32_t* perm, uint64_t n, const uint64_t* ids,
+                 const uint8_t* codes, uint64_t row_bytes, uint64_t* out_ids, uint8_t* out_codes);
+void find_duplicate(pqg_ctx* ctx, const uint64_t* ids, uint64_t n, uint64_t* first_dup_pos);
+void topk_merge_dev(pqg_ctx* ctx, const uint64_t* ids, const double* dists,
+                    const uint32_t* counts, uint32_t shards, uint64_t nq, uint64_t k,
+                    uint64_t* out_ids, double* out_dists, uint32_t* out_counts);
+
+}  // namespace pqg

@@ -1,0 +1,393 @@
+// kmeans.cu -- K2: the Lloyd update of proj/src/kmeans.cpp:93-130 for a batch
+// of B problems, plus the stable bucketing (histogram -> prefix scan ->
+// stable scatter) shared with the inverted-index build (K6).
+//
+// Exactness.  The reference accumulates centroid sums in fp64 in row order
+// (kmeans.cpp:103-111).  Floating-point addition is not associative, so a
+// parallel reduction would not reproduce those bits.  Instead the rows are
+// first bucketed by cluster with a STABLE counting sort (members of each
+// cluster in ascending row order), then one thread per (problem, cluster,
+// dimension) adds its members' values in exactly the reference's order.  The
+// mean is float(sum * (1.0 / count)) (:112-118) and empty clusters are
+// reseeded from the pre-update fp64 distances, ascending cluster order,
+// strict '>' argmax (:122-130).  The resulting centroids are bit-identical to
+// the reference's.
+#include "kernels.cuh"
+
+namespace pqg {
+
+namespace {
+
+constexpr int kTile = 4096;  // rows per bucketing tile
+
+__global__ void hist_kernel(const uint32_t* keys, uint64_t n, uint64_t k, uint32_t ntiles,
+                            uint32_t* tile_counts) {
+    extern __shared__ uint32_t hist[];
+    const uint32_t tile = blockIdx.x, b = blockIdx.y;
+    for (uint64_t c = threadIdx.x; c < k; c += blockDim.x) hist[c] = 0;
+    __syncthreads();
+    const uint64_t r0 = uint64_t(tile) * kTile;
+    const uint64_t r1 = min64(n, r0 + kTile);
+    const uint32_t* kb = keys + uint64_t(b) * n;
+    for (uint64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) atomicAdd(&hist[kb[i]], 1u);
+    __syncthreads();
+    uint32_t* out = tile_counts + uint64_t(b) * k * ntiles;
+    for (uint64_t c = threadIdx.x; c < k; c += blockDim.x) out[c * ntiles + tile] = hist[c];
+}
+
+__global__ void offsets_kernel(const uint64_t* tile_base, uint64_t n, uint32_t B, uint64_t k,
+                               uint32_t ntiles, uint64_t* offsets) {
+    const uint64_t total = uint64_t(B) * (k + 1);
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t b = e / (k + 1), c = e - b * (k + 1);
+        offsets[e] = (c == k) ? n : tile_base[(b * k + c) * ntiles] - b * n;
+    }
+}
+
+// One warp per (tile, problem): walks its tile in row order 32 rows at a
+// time; __match_any_sync ranks equal keys inside the 32, the per-warp running
+// cursor keeps order across rounds, and tiles start at their scanned base.
+__global__ void scatter_kernel(const uint32_t* keys, uint64_t n, uint64_t k, uint32_t ntiles,
+                               const uint64_t* tile_base, uint32_t* perm, int warps_per_block) {
+    extern __shared__ uint32_t running_all[];
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t tile = blockIdx.x * warps_per_block + wib;
+    const uint32_t b = blockIdx.y;
+    if (tile >= ntiles) return;
+    uint32_t* running = running_all + uint64_t(wib) * k;
+    const uint64_t* tb = tile_base + uint64_t(b) * k * ntiles;
+    const uint64_t base_b = uint64_t(b) * n;
+    for (uint64_t c = lane; c < k; c += 32) running[c] = uint32_t(tb[c * ntiles + tile] - base_b);
+    __syncwarp();
+    const uint64_t r0 = uint64_t(tile) * kTile;
+    const uint64_t r1 = min64(n, r0 + kTile);
+    const uint32_t* kb = keys + base_b;
+    uint32_t* pb = perm + base_b;
+    for (uint64_t rr = r0; rr < r1; rr += 32) {
+        const uint64_t i = rr + lane;
+        const bool valid = i < r1;
+        const uint32_t c = valid ? kb[i] : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, c);
+        const uint32_t rank = __popc(peers & lanemask_lt());
+        uint32_t pos = 0;
+        if (valid) pos = running[c] + rank;
+        __syncwarp();
+        if (valid && rank == 0) running[c] += __popc(peers);
+        __syncwarp();
+        if (valid) pb[pos] = uint32_t(i);
+    }
+}
+
+// ---- exclusive scan u32 -> u64 (three phase, 4096 elements per block) ----
+constexpr int kScanThreads = 1024, kScanItems = 4;
+constexpr int kScanBlock = kScanThreads * kScanItems;
+
+template <typename T>
+__device__ uint64_t block_exclusive(T (&v)[kScanItems], uint64_t (&out)[kScanItems]) {
+    __shared__ uint64_t warp_tot[32];
+    uint64_t s = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) { out[j] = s; s += v[j]; }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint64_t incl = s;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint64_t o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += o;
+    }
+    if (lane == 31) warp_tot[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        uint64_t t = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0;
+        uint64_t ti = t;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint64_t o = __shfl_up_sync(0xffffffffu, ti, off);
+            if (lane >= off) ti += o;
+        }
+        warp_tot[lane] = ti - t;  // exclusive warp prefix
+    }
+    __syncthreads();
+    const uint64_t pre = warp_tot[w] + (incl - s);
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) out[j] += pre;
+    __shared__ uint64_t total;
+    if (threadIdx.x == blockDim.x - 1) total = pre + s;
+    __syncthreads();
+    const uint64_t t = total;
+    __syncthreads();
+    return t;
+}
+
+template <typename T>
+__global__ void scan_reduce_kernel(const T* in, uint64_t count, uint64_t* block_sums) {
+    const uint64_t base = uint64_t(blockIdx.x) * kScanBlock;
+    T v[kScanItems];
+    uint64_t o[kScanItems];
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        const uint64_t e = base + uint64_t(threadIdx.x) * kScanItems + j;
+        v[j] = e < count ? in[e] : T(0);
+    }
+    const uint64_t tot = block_exclusive(v, o);
+    if (threadIdx.x == 0) block_sums[blockIdx.x] = tot;
+}
+
+template <typename T>
+__global__ void scan_apply_kernel(const T* in, uint64_t count, const uint64_t* block_pre,
+                                  uint64_t* out) {
+    const uint64_t base = uint64_t(blockIdx.x) * kScanBlock;
+    T v[kScanItems];
+    uint64_t o[kScanItems];
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        const uint64_t e = base + uint64_t(threadIdx.x) * kScanItems + j;
+        v[j] = e < count ? in[e] : T(0);
+    }
+    block_exclusive(v, o);
+    const uint64_t pre = block_pre ? block_pre[blockIdx.x] : 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        const uint64_t e = base + uint64_t(threadIdx.x) * kScanItems + j;
+        if (e < count) out[e] = o[j] + pre;
+    }
+}
+
+template <typename T>
+void exclusive_scan(pqg_ctx* ctx, const T* in, uint64_t* out, uint64_t count) {
+    if (count == 0) return;
+    const uint64_t nb = (count + kScanBlock - 1) / kScanBlock;
+    if (nb == 1) {
+        launch(ctx, "scan", scan_apply_kernel<T>, dim3(1), dim3(kScanThreads), 0, in, count,
+               (const uint64_t*)nullptr, out);
+        return;
+    }
+    uint64_t* sums = scratch<uint64_t>(ctx, nb);
+    uint64_t* pre = scratch<uint64_t>(ctx, nb);
+    launch(ctx, "scan", scan_reduce_kernel<T>, dim3(unsigned(nb)), dim3(kScanThreads), 0, in,
+           count, sums);
+    exclusive_scan<uint64_t>(ctx, sums, pre, nb);
+    launch(ctx, "scan", scan_apply_kernel<T>, dim3(unsigned(nb)), dim3(kScanThreads), 0, in,
+           count, (const uint64_t*)pre, out);
+}
+
+__global__ void gather_kernel(const float* x, uint64_t ldx, uint32_t B, uint32_t d,
+                              uint32_t col_stride, const uint64_t* rows, uint64_t k,
+                              float* table) {
+    const uint64_t total = uint64_t(B) * k * d;
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t bc = e / d, t = e - bc * d;
+        const uint64_t b = bc / k;
+        table[e] = x[rows[bc] * ldx + b * col_stride + t];
+    }
+}
+
+// ---- inertia (deterministic fixed-shape tree) and the stop rule ----------
+constexpr int kRedThreads = 256;
+
+__device__ double block_sum(double v) {
+    __shared__ double sh[kRedThreads];
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int s = kRedThreads / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + s]);
+        __syncthreads();
+    }
+    const double r = sh[0];
+    __syncthreads();
+    return r;
+}
+
+__global__ void partial_sum_kernel(const double* v, uint64_t n, uint64_t chunk, double* parts,
+                                   const int* active) {
+    const uint32_t b = blockIdx.y;
+    if (active && !active[b]) return;
+    const uint64_t c0 = uint64_t(blockIdx.x) * chunk;
+    const uint64_t c1 = min64(n, c0 + chunk);
+    const double* vb = v + uint64_t(b) * n;
+    double s = 0.0;
+    for (uint64_t i = c0 + threadIdx.x; i < c1; i += kRedThreads) s = __dadd_rn(s, vb[i]);
+    s = block_sum(s);
+    if (threadIdx.x == 0) parts[uint64_t(b) * gridDim.x + blockIdx.x] = s;
+}
+
+__global__ void stop_kernel(const double* parts, uint32_t nparts, uint32_t it, uint32_t max_iters,
+                            double tol, KMeansState st) {
+    const uint32_t b = blockIdx.x;
+    if (!st.active[b]) return;
+    double s = 0.0;
+    for (uint32_t i = threadIdx.x; i < nparts; i += kRedThreads)
+        s = __dadd_rn(s, parts[uint64_t(b) * nparts + i]);
+    s = block_sum(s);
+    if (threadIdx.x != 0) return;
+    // proj/src/kmeans.cpp:93-100
+    st.inertia[b] = s;
+    if (st.per_iter) st.per_iter[uint64_t(b) * max_iters + (it - 1)] = s;
+    st.iters[b] = it;
+    const double prev = st.prev[b];
+    const double floor1 = prev > 1.0 ? prev : 1.0;
+    if ((it > 1 && prev - s < tol * floor1) || it == max_iters) {
+        st.active[b] = 0;
+        return;
+    }
+    st.prev[b] = s;
+}
+
+// ---- ordered fp64 sums -> means -----------------------------------------
+__global__ void mean_kernel(const float* x, uint64_t ldx, uint32_t col_stride, uint64_t n,
+                            uint32_t B, uint32_t d, uint64_t k, const uint64_t* offsets,
+                            const uint32_t* perm, float* table, int* has_empty,
+                            const int* active) {
+    const uint64_t total = uint64_t(B) * k * d;
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t bc = e / d, t = e - bc * d;
+        const uint64_t b = bc / k, c = bc - b * k;
+        if (active && !active[b]) continue;
+        const uint64_t* off = offsets + b * (k + 1);
+        const uint64_t beg = off[c], end = off[c + 1];
+        if (beg == end) {
+            has_empty[b] = 1;
+            continue;
+        }
+        const uint32_t* mem = perm + b * n;
+        const float* xc = x + b * col_stride + t;
+        double s = 0.0;
+        uint64_t m = beg;
+        for (; m + 4 <= end; m += 4) {
+            const float v0 = __ldg(xc + uint64_t(mem[m]) * ldx);
+            const float v1 = __ldg(xc + uint64_t(mem[m + 1]) * ldx);
+            const float v2 = __ldg(xc + uint64_t(mem[m + 2]) * ldx);
+            const float v3 = __ldg(xc + uint64_t(mem[m + 3]) * ldx);
+            s = __dadd_rn(s, (double)v0);
+            s = __dadd_rn(s, (double)v1);
+            s = __dadd_rn(s, (double)v2);
+            s = __dadd_rn(s, (double)v3);
+        }
+        for (; m < end; ++m) s = __dadd_rn(s, (double)__ldg(xc + uint64_t(mem[m]) * ldx));
+        const double inv = __ddiv_rn(1.0, (double)(end - beg));
+        table[e] = __double2float_rn(__dmul_rn(s, inv));
+    }
+}
+
+// Empty-cluster repair, proj/src/kmeans.cpp:122-130: for each empty cluster in
+// ascending order take the row with the largest pre-update distance (first
+// such row on ties), copy it, zero its distance.
+__global__ void reseed_kernel(const float* x, uint64_t ldx, uint32_t col_stride, uint64_t n,
+                              uint32_t d, uint64_t k, const uint64_t* offsets, double* dist,
+                              float* table, const int* has_empty, const int* active) {
+    const uint32_t b = blockIdx.x;
+    if ((active && !active[b]) || !has_empty[b]) return;
+    __shared__ double sv[32];
+    __shared__ uint64_t si[32];
+    const uint64_t* off = offsets + uint64_t(b) * (k + 1);
+    double* db = dist + uint64_t(b) * n;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (uint64_t c = 0; c < k; ++c) {
+        if (off[c] != off[c + 1]) continue;
+        double bv = -1.0;
+        uint64_t bi = ~uint64_t(0);
+        for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
+            const double v = db[i];
+            if (bi == ~uint64_t(0) || v > bv) { bv = v; bi = i; }
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const uint64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (oi != ~uint64_t(0) && (bi == ~uint64_t(0) || ov > bv || (ov == bv && oi < bi))) {
+                bv = ov;
+                bi = oi;
+            }
+        }
+        if (lane == 0) { sv[w] = bv; si[w] = bi; }
+        __syncthreads();
+        if (w == 0) {
+            const int nw = blockDim.x >> 5;
+            bv = lane < nw ? sv[lane] : -1.0;
+            bi = lane < nw ? si[lane] : ~uint64_t(0);
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const uint64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (oi != ~uint64_t(0) && (bi == ~uint64_t(0) || ov > bv || (ov == bv && oi < bi))) {
+                    bv = ov;
+                    bi = oi;
+                }
+            }
+            if (lane == 0) si[0] = bi;
+        }
+        __syncthreads();
+        const uint64_t far = si[0];
+        for (uint32_t t = threadIdx.x; t < d; t += blockDim.x)
+            table[(uint64_t(b) * k + c) * d + t] = x[far * ldx + uint64_t(b) * col_stride + t];
+        __syncthreads();
+        if (threadIdx.x == 0) db[far] = 0.0;
+        __syncthreads();
+    }
+}
+
+}  // namespace
+
+void exclusive_scan_u32(pqg_ctx* ctx, const uint32_t* in, uint64_t* out, uint64_t count) {
+    exclusive_scan<uint32_t>(ctx, in, out, count);
+}
+
+void stable_bucket(pqg_ctx* ctx, const uint32_t* keys, uint64_t n, uint32_t B, uint64_t k,
+                   const int* active, Bucketing out) {
+    (void)active;
+    if (k > 16384) fail(PQG_EUNSUPPORTED, "bucketing supports at most 16384 lists/clusters");
+    const uint32_t ntiles = uint32_t((n + kTile - 1) / kTile);
+    uint32_t* tile_counts = scratch<uint32_t>(ctx, uint64_t(B) * k * ntiles);
+    uint64_t* tile_base = scratch<uint64_t>(ctx, uint64_t(B) * k * ntiles);
+    const size_t hsmem = sizeof(uint32_t) * k;
+    set_smem(hist_kernel, hsmem);
+    launch(ctx, "bucket", hist_kernel, dim3(ntiles, B), dim3(256), hsmem, keys, n, k, ntiles,
+           tile_counts);
+    exclusive_scan<uint32_t>(ctx, tile_counts, tile_base, uint64_t(B) * k * ntiles);
+    launch(ctx, "bucket", offsets_kernel, dim3(grid1d(uint64_t(B) * (k + 1), 256, 4096)),
+           dim3(256), 0, (const uint64_t*)tile_base, n, B, k, ntiles, out.offsets);
+    int wpb = int(std::max<uint64_t>(1, std::min<uint64_t>(8, (96 * 1024) / (4 * k))));
+    const size_t ssmem = sizeof(uint32_t) * k * wpb;
+    set_smem(scatter_kernel, ssmem);
+    launch(ctx, "bucket", scatter_kernel, dim3((ntiles + wpb - 1) / wpb, B), dim3(32 * wpb), ssmem,
+           keys, n, k, ntiles, (const uint64_t*)tile_base, out.perm, wpb);
+}
+
+void gather_rows(pqg_ctx* ctx, const float* x, uint64_t ldx, uint32_t B, uint32_t d,
+                 uint32_t col_stride, const uint64_t* rows, uint64_t k, float* table) {
+    launch(ctx, "gather", gather_kernel, dim3(grid1d(uint64_t(B) * k * d, 256, 8192)), dim3(256), 0,
+           x, ldx, B, d, col_stride, rows, k, table);
+}
+
+void kmeans_inertia_and_stop(pqg_ctx* ctx, const double* dist, uint64_t n, uint32_t B,
+                             uint32_t it, uint32_t max_iters, double tol, KMeansState st) {
+    uint64_t nparts = std::min<uint64_t>(512, std::max<uint64_t>(1, (n + 8191) / 8192));
+    const uint64_t chunk = (n + nparts - 1) / nparts;
+    nparts = (n + chunk - 1) / chunk;
+    if (nparts == 0) nparts = 1;
+    double* parts = scratch<double>(ctx, uint64_t(B) * nparts);
+    launch(ctx, "inertia", partial_sum_kernel, dim3(unsigned(nparts), B), dim3(kRedThreads), 0,
+           dist, n, chunk, parts, (const int*)st.active);
+    launch(ctx, "inertia", stop_kernel, dim3(B), dim3(kRedThreads), 0, (const double*)parts,
+           uint32_t(nparts), it, max_iters, tol, st);
+}
+
+void kmeans_update(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint32_t d,
+                   float* table, uint64_t k, const uint32_t* assign, double* dist,
+                   const int* active) {
+    Bucketing bk{scratch<uint64_t>(ctx, uint64_t(B) * (k + 1)), scratch<uint32_t>(ctx, uint64_t(B) * n)};
+    stable_bucket(ctx, assign, n, B, k, active, bk);
+    int* has_empty = scratch<int>(ctx, B);
+    PQG_CUDA(cudaMemsetAsync(has_empty, 0, sizeof(int) * B, ctx->stream));
+    const uint64_t total = uint64_t(B) * k * d;
+    launch(ctx, "kmeans_sum", mean_kernel, dim3(grid1d(total, 128, 1u << 20)), dim3(128), 0,
+           src.x, src.ldx, src.col_stride, n, B, d, k, (const uint64_t*)bk.offsets,
+           (const uint32_t*)bk.perm, table, has_empty, active);
+    launch(ctx, "reseed", reseed_kernel, dim3(B), dim3(1024), 0, src.x, src.ldx, src.col_stride, n,
+           d, k, (const uint64_t*)bk.offsets, dist, table, (const int*)has_empty, active);
+}
+
+}  // namespace pqg

@@ -1,0 +1,431 @@
+// nearest.cu -- K1/K3/K5: batched nearest-centroid search with an fp32
+// tensor-style screen and an exact fp64 fixup.
+//
+// Replaces the reference's innermost loop nearest_in_table / squared_l2
+// (proj/src/kmeans.cpp:11-31), called by assign_pass (:46-57), pq_encode
+// (proj/src/pq.cpp:95-111) and assign_items (proj/src/ivf.cpp:36-49).
+//
+// Screen: per CTA a 128-row tile against 16*TN centroids at a time; every
+// thread owns an 8 x TN block of the row-by-centroid distance matrix in
+// registers, computed in the expanded form ||c||^2 - 2 x.c + C_row with fp32
+// FMAs (x staged in shared memory pre-scaled by -2, which is exact).  C_row
+// (>= ||x||^2 plus a margin) makes every screened value non-negative, so a
+// value's bit pattern orders like the value and the low 3 bits can carry the
+// thread-local column: the running best / second-best are two IMNMX each.
+//
+// Exactness: E_row bounds |screened - exact| (fp32 rounding of the expanded
+// form, (d+4) u (||x|| + max||c||)^2, doubled).  When the second-best lower
+// bound exceeds the best upper bound by more than 2 E_row the fp32 winner is
+// provably the fp64 winner of the reference (whose own rounding is ~1e-16
+// relative).  Otherwise the (row, problem) pair is appended to a flag list
+// and the fixup kernel recomputes it exhaustively in the reference's exact
+// fp64 arithmetic (strict '<', lowest index on ties).  The result is
+// bit-identical to nearest_in_table for every row.
+#include <cfloat>
+
+#include "kernels.cuh"
+
+namespace pqg {
+
+namespace {
+
+constexpr int BM = 128;  // rows per CTA
+constexpr int TM = 8;    // rows per thread
+constexpr int NT = 256;  // threads per CTA (16 column groups x 16 row groups)
+constexpr int LDX = BM + 4;
+constexpr int BK = 32;   // K chunk of the generic (large-d) variant
+
+__device__ __forceinline__ uint32_t read_code(const uint8_t* p, uint32_t w) {
+    return w == 1 ? uint32_t(p[0]) : (uint32_t(p[0]) | (uint32_t(p[1]) << 8));
+}
+
+__device__ __forceinline__ float load_x(const RowSrc& s, uint64_t i, uint32_t b, uint32_t t) {
+    if (s.codes) {
+        const uint32_t m = t / s.dds, tt = t - m * s.dds;
+        uint32_t code = read_code(s.codes + (i * s.dM + m) * s.dw, s.dw);
+        if (code >= s.dks) code = s.dks - 1;  // validated on the host side path
+        return __ldg(s.dtab + ((uint64_t)m * s.dks + code) * s.dds + tt);
+    }
+    return __ldg(s.x + i * s.ldx + (uint64_t)b * s.col_stride + t);
+}
+
+__device__ __forceinline__ void store_index(const NearestArgs& a, uint64_t i, uint32_t b,
+                                            uint32_t idx) {
+    const uint64_t off = i * a.idx_rs + (uint64_t)b * a.idx_ps;
+    if (a.idx_bytes == 1) {
+        static_cast<uint8_t*>(a.out_idx)[off] = uint8_t(idx);
+    } else if (a.idx_bytes == 2) {
+        uint8_t* p = static_cast<uint8_t*>(a.out_idx) + off * 2;
+        p[0] = uint8_t(idx & 0xff);
+        p[1] = uint8_t(idx >> 8);
+    } else {
+        static_cast<uint32_t*>(a.out_idx)[off] = idx;
+    }
+}
+
+__device__ __forceinline__ double exact_dist(const NearestArgs& a, uint64_t i, uint32_t b,
+                                             const float* crow) {
+    double acc = 0.0;
+    for (uint32_t t = 0; t < a.d; ++t) {
+        const double diff = __dsub_rn((double)load_x(a.src, i, b, t), (double)__ldg(crow + t));
+        acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+    }
+    return acc;
+}
+
+// Column owned by thread tx, slot j, within a 16*TN-wide tile.  TN == 8 is
+// split into two 4-wide halves so each float4 shared load of a warp covers
+// 256 contiguous bytes.
+template <int TN>
+__device__ __forceinline__ int col_of(int tx, int j) {
+    if constexpr (TN == 8) return j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4);
+    else return tx * TN + j;
+}
+
+template <int TN>
+__device__ __forceinline__ void load_c(const float* Cs_t, int tx, float (&c)[TN]) {
+    if constexpr (TN == 8) {
+        const float4 u = *reinterpret_cast<const float4*>(Cs_t + tx * 4);
+        const float4 v = *reinterpret_cast<const float4*>(Cs_t + 64 + tx * 4);
+        c[0] = u.x; c[1] = u.y; c[2] = u.z; c[3] = u.w;
+        c[4] = v.x; c[5] = v.y; c[6] = v.z; c[7] = v.w;
+    } else if constexpr (TN == 4) {
+        const float4 u = *reinterpret_cast<const float4*>(Cs_t + tx * 4);
+        c[0] = u.x; c[1] = u.y; c[2] = u.z; c[3] = u.w;
+    } else if constexpr (TN == 2) {
+        const float2 u = *reinterpret_cast<const float2*>(Cs_t + tx * 2);
+        c[0] = u.x; c[1] = u.y;
+    } else {
+        c[0] = Cs_t[tx];
+    }
+}
+
+// DP > 0: the whole (padded) dimension fits one chunk and is a compile-time
+// constant (PQ subspaces, Ds in {4, 8, 16, 32}); DP == 0: generic d streamed
+// in chunks of BK.  MAT: write the screened matrix instead of the argmin.
+template <int TN, int DP, bool MAT>
+__global__ void __launch_bounds__(NT, 2) nearest_kernel(NearestArgs a) {
+    constexpr int BN = 16 * TN;
+    constexpr int LDC = BN + 4;
+    constexpr int KCH = DP > 0 ? DP : BK;
+    extern __shared__ __align__(16) float smem[];
+    float* Xs = smem;                 // [KCH][LDX], -2 * x
+    float* Cs = Xs + KCH * LDX;       // [KCH][LDC]
+    float* cn_s = Cs + KCH * LDC;     // [BN]
+    float* rowC = cn_s + BN;          // [BM]
+    float* rowE = rowC + BM;          // [BM]
+
+    const uint32_t b = blockIdx.y;
+    if (a.active && !a.active[b]) return;
+    const uint64_t i0 = (uint64_t)blockIdx.x * BM;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int d = int(a.d);
+    const int dp = (d + 3) & ~3;
+    const uint64_t k = a.k;
+    const float* tab = a.table + (uint64_t)b * k * d;
+    const float* cnb = a.cnorm + (uint64_t)b * k;
+    const float cmax = a.cmax[b];
+    const int rows_here = int(min64(BM, a.n - i0));
+
+    auto load_x_chunk = [&](int t0, int kc) {
+        for (int e = tid; e < BM * kc; e += NT) {
+            const int r = e / kc, tt = e - r * kc;
+            float v = 0.f;
+            if (r < rows_here && t0 + tt < d) v = load_x(a.src, i0 + r, b, uint32_t(t0 + tt));
+            Xs[tt * LDX + r] = -2.f * v;
+        }
+    };
+    auto load_c_chunk = [&](uint64_t n0, int t0, int kc) {
+        for (int e = tid; e < BN * kc; e += NT) {
+            const int jj = e / kc, tt = e - jj * kc;
+            const uint64_t j = n0 + jj;
+            float v = 0.f;
+            if (j < k && t0 + tt < d) v = __ldg(tab + j * d + t0 + tt);
+            Cs[tt * LDC + jj] = v;
+        }
+    };
+
+    // ---- row norms -> C_row (offset that keeps screened values >= 0) and E_row
+    {
+        float s = 0.f;
+        if constexpr (DP > 0) {
+            load_x_chunk(0, DP);
+            __syncthreads();
+            if (tid < BM) {
+#pragma unroll
+                for (int t = 0; t < DP; ++t) {
+                    const float v = Xs[t * LDX + tid];
+                    s = fmaf(v, v, s);
+                }
+            }
+        } else {
+            for (int t0 = 0; t0 < dp; t0 += BK) {
+                const int kc = min(BK, dp - t0);
+                __syncthreads();
+                load_x_chunk(t0, kc);
+                __syncthreads();
+                if (tid < BM)
+                    for (int t = 0; t < kc; ++t) {
+                        const float v = Xs[t * LDX + tid];
+                        s = fmaf(v, v, s);
+                    }
+            }
+        }
+        if (tid < BM) {
+            const float nx = 0.25f * s;
+            const float q = sqrtf(nx) * (1.f + 1e-6f) + cmax;
+            const float E = 2.f * float(d + 4) * kU * q * q + 1e-30f;
+            rowE[tid] = E;
+            rowC[tid] = nx * (1.f + 2.f * float(d + 2) * kU) + 2.f * E;
+            if constexpr (MAT) {
+                if (tid < rows_here) a.row_err[i0 + tid] = E;
+            }
+        }
+    }
+
+    uint32_t m1[TM], m2[TM], t1[TM];
+#pragma unroll
+    for (int i = 0; i < TM; ++i) { m1[i] = 0xFFFFFFFFu; m2[i] = 0xFFFFFFFFu; t1[i] = 0; }
+
+    const uint64_t ntiles = (k + BN - 1) / BN;
+    for (uint64_t nt = 0; nt < ntiles; ++nt) {
+        const uint64_t n0 = nt * BN;
+        float acc[TM][TN];
+        __syncthreads();
+        for (int jj = tid; jj < BN; jj += NT) {
+            const uint64_t j = n0 + jj;
+            cn_s[jj] = j < k ? __ldg(cnb + j) : __int_as_float(0x7f800000);
+        }
+        if constexpr (DP > 0) {
+            load_c_chunk(n0, 0, DP);
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j) acc[i][j] = cn_s[col_of<TN>(tx, j)];
+#pragma unroll
+            for (int t = 0; t < DP; ++t) {
+                const float4 xa = *reinterpret_cast<const float4*>(Xs + t * LDX + ty * 8);
+                const float4 xb = *reinterpret_cast<const float4*>(Xs + t * LDX + ty * 8 + 4);
+                const float xr[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+                float cr[TN];
+                load_c<TN>(Cs + t * LDC, tx, cr);
+#pragma unroll
+                for (int i = 0; i < TM; ++i)
+#pragma unroll
+                    for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(xr[i], cr[j], acc[i][j]);
+            }
+        } else {
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j) acc[i][j] = cn_s[col_of<TN>(tx, j)];
+            for (int t0 = 0; t0 < dp; t0 += BK) {
+                const int kc = min(BK, dp - t0);
+                __syncthreads();
+                load_x_chunk(t0, kc);
+                load_c_chunk(n0, t0, kc);
+                __syncthreads();
+#pragma unroll 4
+                for (int t = 0; t < kc; ++t) {
+                    const float4 xa = *reinterpret_cast<const float4*>(Xs + t * LDX + ty * 8);
+                    const float4 xb = *reinterpret_cast<const float4*>(Xs + t * LDX + ty * 8 + 4);
+                    const float xr[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+                    float cr[TN];
+                    load_c<TN>(Cs + t * LDC, tx, cr);
+#pragma unroll
+                    for (int i = 0; i < TM; ++i)
+#pragma unroll
+                        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(xr[i], cr[j], acc[i][j]);
+                }
+            }
+        }
+
+        // ---- epilogue of this column tile
+        if constexpr (MAT) {
+#pragma unroll
+            for (int i = 0; i < TM; ++i) {
+                const int r = ty * 8 + i;
+                if (r >= rows_here) continue;
+                const float crow = rowC[r];
+                float* out = a.out_mat + (i0 + r) * a.ld_mat;
+#pragma unroll
+                for (int j = 0; j < TN; ++j) {
+                    const uint64_t col = n0 + col_of<TN>(tx, j);
+                    if (col < k) out[col] = acc[i][j] + crow;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < TM; ++i) {
+                const float crow = rowC[ty * 8 + i];
+                const uint32_t old = m1[i];
+#pragma unroll
+                for (int j = 0; j < TN; ++j) {
+                    const uint32_t key = (__float_as_uint(acc[i][j] + crow) & ~7u) | uint32_t(j);
+                    m2[i] = min(m2[i], max(m1[i], key));
+                    m1[i] = min(m1[i], key);
+                }
+                t1[i] = (m1[i] != old) ? uint32_t(nt) : t1[i];
+            }
+        }
+    }
+    if constexpr (MAT) return;
+
+    // ---- combine the 16 column groups of each row (lanes xor 8,4,2,1)
+    uint64_t K[TM];
+    uint32_t V2[TM];
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+        const uint32_t col = uint32_t(t1[i]) * BN + uint32_t(col_of<TN>(tx, int(m1[i] & 7u)));
+        K[i] = (uint64_t(m1[i] & ~7u) << 32) | col;
+        V2[i] = m2[i] & ~7u;
+#pragma unroll
+        for (int off = 8; off >= 1; off >>= 1) {
+            const uint64_t oK = __shfl_xor_sync(0xffffffffu, K[i], off);
+            const uint32_t oV = __shfl_xor_sync(0xffffffffu, V2[i], off);
+            const uint32_t hiMax = uint32_t(max(K[i], oK) >> 32);
+            V2[i] = min(min(V2[i], oV), hiMax);
+            K[i] = min(K[i], oK);
+        }
+    }
+    // lane tx (< 8) finalises row ty*8 + tx
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+        if (tx != i) continue;
+        const int r = ty * 8 + i;
+        if (r >= rows_here) continue;
+        const uint64_t row = i0 + r;
+        const uint32_t v1hi = uint32_t(K[i] >> 32);
+        const uint32_t idx = uint32_t(K[i]);
+        const float E = rowE[r];
+        const bool unique = (V2[i] >= 0x7f800000u) ||
+                            (__uint_as_float(V2[i]) - __uint_as_float(v1hi | 7u) > 2.05f * E);
+        if (unique) {
+            store_index(a, row, b, idx);
+            if (a.out_dist) a.out_dist[(uint64_t)b * a.n + row] = exact_dist(a, row, b, tab + (uint64_t)idx * d);
+        } else {
+            const unsigned long long slot = atomicAdd(a.flag_count, 1ull);
+            a.flags[slot] = (uint64_t(b) << 40) | row;
+        }
+    }
+}
+
+// Exhaustive exact fp64 argmin for flagged (row, problem) pairs, one warp per
+// pair: nearest_in_table verbatim (strict '<', lowest index on ties).
+__global__ void fixup_kernel(NearestArgs a) {
+    const unsigned long long cnt = *a.flag_count;
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t f = warp; f < cnt; f += nwarps) {
+        const uint64_t item = a.flags[f];
+        const uint32_t b = uint32_t(item >> 40);
+        const uint64_t row = item & ((uint64_t(1) << 40) - 1);
+        const float* tab = a.table + (uint64_t)b * a.k * a.d;
+        double best = __longlong_as_double(0x7ff0000000000000LL);
+        uint32_t bj = 0xFFFFFFFFu;
+        for (uint64_t j = lane; j < a.k; j += 32) {
+            const double dist = exact_dist(a, row, b, tab + j * a.d);
+            if (dist < best) { best = dist; bj = uint32_t(j); }
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+            const uint32_t oj = __shfl_xor_sync(0xffffffffu, bj, off);
+            if (ob < best || (ob == best && oj < bj)) { best = ob; bj = oj; }
+        }
+        if (lane == 0) {
+            if (bj == 0xFFFFFFFFu) {  // every distance NaN: the reference keeps index 0
+                bj = 0;
+                best = exact_dist(a, row, b, tab);
+            }
+            store_index(a, row, b, bj);
+            if (a.out_dist) a.out_dist[(uint64_t)b * a.n + row] = best;
+        }
+    }
+}
+
+__global__ void norms_kernel(const float* table, uint32_t B, uint64_t k, uint32_t d,
+                             float* cnorm, unsigned* cmax_bits) {
+    const uint64_t total = uint64_t(B) * k;
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        const float* c = table + e * d;
+        double s = 0.0;
+        for (uint32_t t = 0; t < d; ++t) {
+            const double v = c[t];
+            s = __dadd_rn(s, __dmul_rn(v, v));
+        }
+        cnorm[e] = __double2float_rn(s);
+        atomicMax(cmax_bits + e / k, __float_as_uint(__double2float_ru(sqrt(s))));
+    }
+}
+
+template <int TN, int DP, bool MAT>
+size_t smem_bytes() {
+    constexpr int BN = 16 * TN;
+    constexpr int KCH = DP > 0 ? DP : BK;
+    return sizeof(float) * (KCH * LDX + KCH * (BN + 4) + BN + 2 * BM);
+}
+
+template <int TN, int DP, bool MAT>
+void launch_nearest(pqg_ctx* ctx, const NearestArgs& a) {
+    auto kern = nearest_kernel<TN, DP, MAT>;
+    const size_t smem = smem_bytes<TN, DP, MAT>();
+    static bool configured = false;
+    if (!configured) {
+        set_smem(kern, smem);
+        configured = true;
+    }
+    const uint64_t gx = (a.n + BM - 1) / BM;
+    launch(ctx, MAT ? "distance_matrix" : "nearest", kern, dim3(unsigned(gx), a.B), dim3(NT), smem, a);
+}
+
+template <int TN, bool MAT>
+void dispatch_dp(pqg_ctx* ctx, const NearestArgs& a) {
+    const uint32_t dp = (a.d + 3) & ~3u;
+    if (dp == 4) launch_nearest<TN, 4, MAT>(ctx, a);
+    else if (dp == 8) launch_nearest<TN, 8, MAT>(ctx, a);
+    else if (dp == 16) launch_nearest<TN, 16, MAT>(ctx, a);
+    else if (dp == 32) launch_nearest<TN, 32, MAT>(ctx, a);
+    else launch_nearest<TN, 0, MAT>(ctx, a);
+}
+
+template <bool MAT>
+void dispatch(pqg_ctx* ctx, const NearestArgs& a) {
+    if (a.k >= 128) dispatch_dp<8, MAT>(ctx, a);
+    else if (a.k >= 64) dispatch_dp<4, MAT>(ctx, a);
+    else if (a.k >= 32) dispatch_dp<2, MAT>(ctx, a);
+    else dispatch_dp<1, MAT>(ctx, a);
+}
+
+}  // namespace
+
+void table_norms(pqg_ctx* ctx, const float* table, uint32_t B, uint64_t k, uint32_t d,
+                 float* cnorm, float* cmax) {
+    PQG_CUDA(cudaMemsetAsync(cmax, 0, sizeof(float) * B, ctx->stream));
+    launch(ctx, "norms", norms_kernel, dim3(grid1d(uint64_t(B) * k, 256, 4096)), dim3(256), 0,
+           table, B, k, d, cnorm, reinterpret_cast<unsigned*>(cmax));
+}
+
+void nearest(pqg_ctx* ctx, NearestArgs a) {
+    if (a.n == 0 || a.B == 0) return;
+    if (a.k >= (uint64_t(1) << 31)) fail(PQG_EUNSUPPORTED, "nearest: k too large");
+    if (a.n >= (uint64_t(1) << 40)) fail(PQG_EUNSUPPORTED, "nearest: too many rows");
+    // flag list capacity n*B (worst case: every row tied)
+    a.flag_count = scratch<unsigned long long>(ctx, 1);
+    a.flags = scratch<uint64_t>(ctx, a.n * a.B);
+    PQG_CUDA(cudaMemsetAsync(a.flag_count, 0, sizeof(unsigned long long), ctx->stream));
+    a.out_mat = nullptr;
+    dispatch<false>(ctx, a);
+    launch(ctx, "fixup", fixup_kernel, dim3(ctx->num_sms * 4), dim3(256), 0, a);
+}
+
+void distance_matrix(pqg_ctx* ctx, NearestArgs a) {
+    if (a.n == 0) return;
+    dispatch<true>(ctx, a);
+}
+
+}  // namespace pqg

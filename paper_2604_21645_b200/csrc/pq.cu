@@ -1,0 +1,179 @@
+// pq.cu -- K4 decode + squared-error reduction and K7 ADC tables.
+//
+//  pq_decode / pq_decode_row   proj/src/pq.cpp:113-130
+//  rmse numerator              proj/src/pq.cpp:169-177
+//  reconstruction_rmse         proj/src/pq.cpp:179-181 (decode fused into the SSE)
+//  adc_table                   proj/src/pq.cpp:132-151 (float(fp64 squared_l2))
+//  adc_lookup                  proj/src/pq.cpp:153-167 (fp64 sum of float entries)
+//
+// The SSE is reduced in a fixed-shape fp64 tree (deterministic, independent of
+// timing); the reference sums sequentially, so the two agree to ~1e-15
+// relative, far inside the 1e-4 RMSE tolerance of BASELINE.json.
+#include "kernels.cuh"
+
+namespace pqg {
+
+namespace {
+
+__device__ __forceinline__ uint32_t code_at(const uint8_t* codes, uint64_t i, uint32_t m,
+                                            uint32_t M, uint32_t w) {
+    const uint8_t* p = codes + (i * M + m) * w;
+    return w == 1 ? uint32_t(p[0]) : (uint32_t(p[0]) | (uint32_t(p[1]) << 8));
+}
+
+__global__ void decode_kernel(const uint8_t* codes, uint64_t n, uint32_t M, uint32_t ks,
+                              uint32_t ds, const float* tables, float* out, int* err) {
+    const uint32_t w = ks <= 256 ? 1 : 2;
+    const uint64_t D = uint64_t(M) * ds, total = n * D;
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i = e / D, col = e - i * D;
+        const uint32_t m = uint32_t(col / ds), t = uint32_t(col - uint64_t(m) * ds);
+        const uint32_t code = code_at(codes, i, m, M, w);
+        if (code >= ks) {
+            atomicExch(err, 1);
+            out[e] = 0.f;
+            continue;
+        }
+        out[e] = __ldg(tables + (uint64_t(m) * ks + code) * ds + t);
+    }
+}
+
+constexpr int kThreads = 256;
+
+__device__ double block_sum256(double v) {
+    __shared__ double sh[kThreads];
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int s = kThreads / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + s]);
+        __syncthreads();
+    }
+    const double r = sh[0];
+    __syncthreads();
+    return r;
+}
+
+// a - b squared, summed over [chunk*blk, chunk*(blk+1)) in a fixed tree.
+__global__ void sse_kernel(const float* a, const float* b, uint64_t count, uint64_t chunk,
+                           double* parts) {
+    const uint64_t c0 = uint64_t(blockIdx.x) * chunk, c1 = min64(count, c0 + chunk);
+    double s = 0.0;
+    for (uint64_t e = c0 + threadIdx.x; e < c1; e += kThreads) {
+        const double diff = __dsub_rn((double)a[e], (double)b[e]);
+        s = __dadd_rn(s, __dmul_rn(diff, diff));
+    }
+    s = block_sum256(s);
+    if (threadIdx.x == 0) parts[blockIdx.x] = s;
+}
+
+// x vs decode(codes) without materialising the decode; rows are read as
+// coalesced runs (consecutive threads -> consecutive elements).
+__global__ void recon_sse_kernel(const float* x, const uint8_t* codes, uint64_t n, uint32_t M,
+                                 uint32_t ks, uint32_t ds, const float* tables, uint64_t chunk,
+                                 double* parts, int* err) {
+    const uint32_t w = ks <= 256 ? 1 : 2;
+    const uint64_t D = uint64_t(M) * ds, total = n * D;
+    const uint64_t c0 = uint64_t(blockIdx.x) * chunk, c1 = min64(total, c0 + chunk);
+    double s = 0.0;
+    for (uint64_t e = c0 + threadIdx.x; e < c1; e += kThreads) {
+        const uint64_t i = e / D, col = e - i * D;
+        const uint32_t m = uint32_t(col / ds), t = uint32_t(col - uint64_t(m) * ds);
+        uint32_t code = code_at(codes, i, m, M, w);
+        if (code >= ks) {
+            atomicExch(err, 1);
+            code = 0;
+        }
+        const double diff =
+            __dsub_rn((double)__ldg(x + e), (double)__ldg(tables + (uint64_t(m) * ks + code) * ds + t));
+        s = __dadd_rn(s, __dmul_rn(diff, diff));
+    }
+    s = block_sum256(s);
+    if (threadIdx.x == 0) parts[blockIdx.x] = s;
+}
+
+__global__ void final_sum_kernel(const double* parts, uint64_t count, double* out) {
+    double s = 0.0;
+    for (uint64_t i = threadIdx.x; i < count; i += kThreads) s = __dadd_rn(s, parts[i]);
+    s = block_sum256(s);
+    if (threadIdx.x == 0) *out = s;
+}
+
+__global__ void adc_tables_kernel(const float* tables, uint32_t M, uint32_t ks, uint32_t ds,
+                                  const float* queries, uint64_t nq, float* entries) {
+    const uint64_t D = uint64_t(M) * ds, per_q = uint64_t(M) * ks, total = nq * per_q;
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t q = e / per_q, mj = e - q * per_q;
+        const uint32_t m = uint32_t(mj / ks);
+        entries[e] = __double2float_rn(
+            exact_sq_l2(queries + q * D + uint64_t(m) * ds, tables + mj * ds, int(ds)));
+    }
+}
+
+__global__ void adc_lookup_kernel(const float* entries, uint32_t M, uint32_t ks,
+                                  const uint8_t* codes, uint64_t n, double* out, int* err) {
+    const uint32_t w = ks <= 256 ? 1 : 2;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        double acc = 0.0;
+        for (uint32_t m = 0; m < M; ++m) {
+            const uint32_t code = code_at(codes, i, m, M, w);
+            if (code >= ks) {
+                atomicExch(err, 1);
+                break;
+            }
+            acc = __dadd_rn(acc, (double)__ldg(entries + uint64_t(m) * ks + code));
+        }
+        out[i] = acc;
+    }
+}
+
+uint64_t nparts_for(uint64_t count) {
+    return std::min<uint64_t>(4096, std::max<uint64_t>(1, (count + 65535) / 65536));
+}
+
+}  // namespace
+
+void reduce_sum_f64(pqg_ctx* ctx, const double* parts, uint64_t count, double* out) {
+    launch(ctx, "reduce", final_sum_kernel, dim3(1), dim3(kThreads), 0, parts, count, out);
+}
+
+void pq_decode_dev(pqg_ctx* ctx, const uint8_t* codes, uint64_t n, uint32_t M, uint32_t ks,
+                   uint32_t ds, const float* tables, float* out, int* err) {
+    launch(ctx, "decode", decode_kernel, dim3(grid1d(n * M * ds, 256, ctx->num_sms * 32)),
+           dim3(256), 0, codes, n, M, ks, ds, tables, out, err);
+}
+
+void sq_error_dev(pqg_ctx* ctx, const float* a, const float* b, uint64_t count, double* sse) {
+    const uint64_t np = nparts_for(count);
+    const uint64_t chunk = (count + np - 1) / np;
+    double* parts = scratch<double>(ctx, np);
+    launch(ctx, "sse", sse_kernel, dim3(unsigned(np)), dim3(kThreads), 0, a, b, count, chunk, parts);
+    reduce_sum_f64(ctx, parts, np, sse);
+}
+
+void recon_sse_dev(pqg_ctx* ctx, const float* x, const uint8_t* codes, uint64_t n, uint32_t M,
+                   uint32_t ks, uint32_t ds, const float* tables, double* sse, int* err) {
+    const uint64_t total = n * M * ds;
+    const uint64_t np = nparts_for(total);
+    const uint64_t chunk = (total + np - 1) / np;
+    double* parts = scratch<double>(ctx, np);
+    launch(ctx, "recon_sse", recon_sse_kernel, dim3(unsigned(np)), dim3(kThreads), 0, x, codes, n, M,
+           ks, ds, tables, chunk, parts, err);
+    reduce_sum_f64(ctx, parts, np, sse);
+}
+
+void adc_tables_dev(pqg_ctx* ctx, const float* tables, uint32_t M, uint32_t ks, uint32_t ds,
+                    const float* queries, uint64_t nq, float* entries) {
+    launch(ctx, "adc_tables", adc_tables_kernel, dim3(grid1d(nq * M * ks, 256, 1u << 20)), dim3(256), 0,
+           tables, M, ks, ds, queries, nq, entries);
+}
+
+void adc_lookup_dev(pqg_ctx* ctx, const float* entries, uint32_t M, uint32_t ks,
+                    const uint8_t* codes, uint64_t n, double* out, int* err) {
+    launch(ctx, "adc_lookup", adc_lookup_kernel, dim3(grid1d(n, 256, 1u << 20)), dim3(256), 0, entries,
+           M, ks, codes, n, out, err);
+}
+
+}  // namespace pqg

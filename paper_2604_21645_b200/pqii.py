@@ -1,0 +1,639 @@
+"""The reference's PQ / IVF API (namespace ``pqii``, proj/include/pqii/*.hpp)
+re-exposed over the B200 path.
+
+Names, argument meaning, defaults and errors follow the reference so tests
+read like its own: ``kmeans_fit`` (kmeans.hpp:41-44), ``pq_fit`` /
+``pq_encode`` / ``pq_decode`` / ``adc_table`` / ``adc_lookup`` / ``rmse`` /
+``reconstruction_rmse`` (pq.hpp:66-88), ``ivf_build`` /
+``ivf_build_with_centroids`` / ``ivf_add`` / ``ivf_merge`` / ``ivf_query`` /
+``ivf_query_subset`` / ``flat_scan`` / ``default_nlist`` (ivf.hpp:46-86).
+``std::invalid_argument`` maps to ``ValueError`` and ``std::out_of_range`` to
+``IndexError`` with the reference's message substrings.
+
+Arrays may be numpy (host) or torch CUDA tensors (device-resident); the C
+ABI stages host buffers itself.  Every computation runs in libpqg.so on the
+GPU; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+
+# ---------------------------------------------------------------------------
+# context
+# ---------------------------------------------------------------------------
+
+
+class Context:
+    """One GPU, one stream, one scratch arena (pqg_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = _lib.load()
+        h = C.c_void_p()
+        _lib.check(self.lib.pqg_ctx_create(device, C.byref(h)), "ctx_create")
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.pqg_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_ptr: int | None):
+        _lib.check(self.lib.pqg_ctx_set_stream(self.h, C.c_void_p(stream_ptr or 0)))
+
+    def sync(self):
+        _lib.check(self.lib.pqg_ctx_sync(self.h))
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.pqg_ctx_launches(self.h))
+
+    def profile(self, enable: bool):
+        _lib.check(self.lib.pqg_profile_enable(self.h, int(enable)))
+
+    def profile_read(self, cls: str):
+        n = C.c_uint64()
+        ms = C.c_double()
+        _lib.check(self.lib.pqg_profile_read(self.h, cls.encode(), C.byref(n), C.byref(ms)))
+        return int(n.value), float(ms.value)
+
+
+_CTX: dict[int, Context] = {}
+
+
+def get_context(device: int = 0) -> Context:
+    if device not in _CTX:
+        _CTX[device] = Context(device)
+    return _CTX[device]
+
+
+def _ptr(x):
+    """(void* value, keep-alive) for a numpy array or a torch tensor."""
+    if x is None:
+        return None, None
+    if hasattr(x, "data_ptr"):
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return C.c_void_p(x.data_ptr()), x
+    a = np.ascontiguousarray(x)
+    return C.c_void_p(a.ctypes.data), a
+
+
+def _f32(x):
+    if hasattr(x, "data_ptr"):
+        return x
+    return np.ascontiguousarray(x, dtype=np.float32)
+
+
+# ---------------------------------------------------------------------------
+# data types (proj/include/pqii/*.hpp)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class KMeansResult:  # kmeans.hpp:14-20
+    centroids: np.ndarray
+    assignments: np.ndarray
+    inertia: float
+    iterations_run: int
+    inertia_per_iter: np.ndarray
+
+
+@dataclass
+class Codebook:  # pq.hpp:15-31
+    m_subspaces: int
+    ks: int
+    sub_dim: int
+    tables: np.ndarray  # [M, ks, sub_dim] float32
+
+    def dims(self) -> int:
+        return self.m_subspaces * self.sub_dim
+
+    def codeword(self, m: int, j: int) -> np.ndarray:
+        return self.tables[m, j]
+
+    def __eq__(self, o) -> bool:
+        return (isinstance(o, Codebook) and self.m_subspaces == o.m_subspaces and self.ks == o.ks
+                and self.sub_dim == o.sub_dim and np.array_equal(self.tables, o.tables))
+
+
+def code_width(ks: int) -> int:
+    return 1 if ks <= 256 else 2
+
+
+@dataclass
+class CodeMatrix:  # pq.hpp:36-55
+    rows: int
+    m_subspaces: int
+    ks: int
+    bytes: np.ndarray  # [rows, M * width] uint8
+
+    @staticmethod
+    def zeros(n: int, m: int, ks: int) -> "CodeMatrix":
+        if m == 0:
+            raise ValueError("codebook: M must be >= 1")
+        if ks == 0 or ks > 65536:
+            raise ValueError("codebook: Ks must be in [1, 65536]")
+        return CodeMatrix(n, m, ks, np.zeros((n, m * code_width(ks)), np.uint8))
+
+    def code_width(self) -> int:
+        return code_width(self.ks)
+
+    def row_bytes(self) -> int:
+        return self.m_subspaces * self.code_width()
+
+    def at(self, i: int, m: int) -> int:
+        w = self.code_width()
+        b = self.bytes[i, m * w: m * w + w]
+        return int(b[0]) if w == 1 else int(b[0]) | (int(b[1]) << 8)
+
+    def set(self, i: int, m: int, v: int) -> None:
+        w = self.code_width()
+        self.bytes[i, m * w] = v & 0xFF
+        if w == 2:
+            self.bytes[i, m * w + 1] = (v >> 8) & 0xFF
+
+    def codes(self) -> np.ndarray:
+        """[rows, M] integer view of the packed codes."""
+        if self.code_width() == 1:
+            return self.bytes.astype(np.uint32)
+        return self.bytes.view("<u2").astype(np.uint32)
+
+    def __eq__(self, o) -> bool:
+        return (isinstance(o, CodeMatrix) and self.rows == o.rows
+                and self.m_subspaces == o.m_subspaces and self.ks == o.ks
+                and np.array_equal(self.bytes, o.bytes))
+
+
+@dataclass
+class DistanceTable:  # pq.hpp:58-64
+    m_subspaces: int
+    ks: int
+    entries: np.ndarray  # [M, ks] float32
+
+    def entry(self, m: int, j: int) -> float:
+        return float(self.entries[m, j])
+
+
+@dataclass
+class Hit:  # ivf.hpp:33-38
+    id: int
+    sq_dist: float
+
+
+@dataclass
+class QueryResult:  # ivf.hpp:40-44
+    hits: list = field(default_factory=list)
+    k_requested: int = 0
+
+
+# ---------------------------------------------------------------------------
+# L1: kmeans.hpp
+# ---------------------------------------------------------------------------
+
+
+def nearest_batch(points, table, ctx: Context | None = None):
+    """nearest_in_table (kmeans.cpp:20-31) for every row of ``points``."""
+    ctx = ctx or get_context()
+    points = _f32(points)
+    table = _f32(table)
+    n, d = points.shape
+    k = table.shape[0]
+    if table.shape[0] == 0:
+        raise ValueError("nearest_centroid: empty centroid set")
+    if table.shape[1] != d:
+        raise ValueError("nearest_centroid: dimension mismatch")
+    idx = np.empty(n, np.uint32)
+    dist = np.empty(n, np.float64)
+    pp, _a = _ptr(points)
+    tp, _b = _ptr(table)
+    _lib.check(ctx.lib.pqg_nearest_batch(ctx.h, pp, n, d, tp, k, idx.ctypes.data_as(C.c_void_p),
+                                         dist.ctypes.data_as(C.c_void_p)), "nearest")
+    return idx, dist
+
+
+def nearest_centroid(point, centroids, ctx: Context | None = None):
+    """(index, sq_dist) -- kmeans.cpp:33-40."""
+    point = np.ascontiguousarray(point, np.float32).reshape(1, -1)
+    centroids = np.ascontiguousarray(centroids, np.float32)
+    if centroids.ndim != 2 or centroids.shape[0] == 0:
+        raise ValueError("nearest_centroid: empty centroid set")
+    if point.shape[1] != centroids.shape[1]:
+        raise ValueError("nearest_centroid: dimension mismatch")
+    i, d = nearest_batch(point, centroids, ctx)
+    return int(i[0]), float(d[0])
+
+
+def kmeans_fit(points, k: int, max_iters: int = 20, seed: int = 0, tol: float = 1e-4,
+               ctx: Context | None = None) -> KMeansResult:
+    """Lloyd k-means, bit-identical to kmeans.cpp:61-133."""
+    ctx = ctx or get_context()
+    points = _f32(points)
+    n, d = points.shape
+    if max_iters < 0:
+        raise ValueError("kmeans_fit: max_iters must be >= 1")
+    cent = np.empty((k, d), np.float32)
+    assign = np.empty(n, np.uint32)
+    inertia = C.c_double()
+    iters = C.c_uint32()
+    per = np.zeros(max(1, max_iters), np.float64)
+    pp, _a = _ptr(points)
+    _lib.check(ctx.lib.pqg_kmeans_fit(ctx.h, pp, n, d, k, max_iters, seed, tol,
+                                      cent.ctypes.data_as(C.c_void_p),
+                                      assign.ctypes.data_as(C.c_void_p), C.byref(inertia),
+                                      C.byref(iters), per.ctypes.data_as(C.c_void_p)), "kmeans_fit")
+    return KMeansResult(cent, assign, inertia.value, iters.value, per[: iters.value].copy())
+
+
+# ---------------------------------------------------------------------------
+# L1: pq.hpp
+# ---------------------------------------------------------------------------
+
+
+def pq_fit(data, m: int, ks: int, max_iters: int = 20, seed: int = 0,
+           ctx: Context | None = None, stats: dict | None = None) -> Codebook:
+    """pq.cpp:63-93 -- all M subspace fits batched on the device."""
+    ctx = ctx or get_context()
+    data = _f32(data)
+    n, D = data.shape
+    if m == 0:
+        raise ValueError("pq_fit: M must be >= 1")
+    if D % m:
+        raise ValueError(f"pq_fit: D ({D}) is not divisible by M ({m})")
+    ds = D // m
+    tables = np.empty((m, max(ks, 0), ds), np.float32)
+    iters = np.empty(m, np.uint32)
+    inert = np.empty(m, np.float64)
+    dp, _a = _ptr(data)
+    _lib.check(ctx.lib.pqg_pq_fit(ctx.h, dp, n, D, m, ks, max_iters, seed,
+                                  tables.ctypes.data_as(C.c_void_p),
+                                  iters.ctypes.data_as(C.c_void_p),
+                                  inert.ctypes.data_as(C.c_void_p)), "pq_fit")
+    if stats is not None:
+        stats["iterations_run"] = iters
+        stats["inertia"] = inert
+    return Codebook(m, ks, ds, tables)
+
+
+def pq_encode(cb: Codebook, data, ctx: Context | None = None) -> CodeMatrix:
+    """pq.cpp:95-111."""
+    ctx = ctx or get_context()
+    data = _f32(data)
+    if data.shape[1] != cb.dims():
+        raise ValueError(f"pq_encode: data dimension {data.shape[1]} does not match codebook "
+                         f"dimension {cb.dims()}")
+    n = data.shape[0]
+    out = CodeMatrix.zeros(n, cb.m_subspaces, cb.ks)
+    dp, _a = _ptr(data)
+    tp, _b = _ptr(np.ascontiguousarray(cb.tables, np.float32))
+    _lib.check(ctx.lib.pqg_pq_encode(ctx.h, dp, n, cb.m_subspaces, cb.ks, cb.sub_dim, tp,
+                                     out.bytes.ctypes.data_as(C.c_void_p)), "pq_encode")
+    return out
+
+
+def _check_codes(cb: Codebook, codes: CodeMatrix, who: str):
+    if codes.m_subspaces != cb.m_subspaces or codes.ks != cb.ks:
+        raise ValueError(f"{who}: codes do not match the codebook")
+
+
+def pq_decode(cb: Codebook, codes: CodeMatrix, ctx: Context | None = None) -> np.ndarray:
+    """pq.cpp:125-130 (raises IndexError for a code >= Ks, :117-120)."""
+    ctx = ctx or get_context()
+    _check_codes(cb, codes, "pq_decode")
+    out = np.empty((codes.rows, cb.dims()), np.float32)
+    if codes.rows == 0:
+        return out
+    cp, _a = _ptr(codes.bytes)
+    tp, _b = _ptr(np.ascontiguousarray(cb.tables, np.float32))
+    _lib.check(ctx.lib.pqg_pq_decode(ctx.h, cp, codes.rows, cb.m_subspaces, cb.ks, cb.sub_dim, tp,
+                                     out.ctypes.data_as(C.c_void_p)), "pq_decode")
+    return out
+
+
+def pq_decode_row(cb: Codebook, codes: CodeMatrix, i: int, ctx: Context | None = None):
+    """pq.cpp:113-123."""
+    sub = CodeMatrix(1, codes.m_subspaces, codes.ks, codes.bytes[i: i + 1].copy())
+    return pq_decode(cb, sub, ctx)[0]
+
+
+def rmse(a, b, ctx: Context | None = None) -> float:
+    """pq.cpp:169-177."""
+    ctx = ctx or get_context()
+    a = _f32(a)
+    b = _f32(b)
+    if tuple(a.shape) != tuple(b.shape):
+        raise ValueError("rmse: shape mismatch")
+    count = int(np.prod(a.shape))
+    sse = C.c_double()
+    ap, _a = _ptr(a)
+    bp, _b = _ptr(b)
+    _lib.check(ctx.lib.pqg_sq_error(ctx.h, ap, bp, count, C.byref(sse)), "rmse")
+    return math.sqrt(sse.value / count) if count else float("nan")
+
+
+def reconstruction_rmse(cb: Codebook, data, ctx: Context | None = None) -> float:
+    """pq.cpp:179-181: rmse(data, decode(encode(data))), fused on the device."""
+    ctx = ctx or get_context()
+    data = _f32(data)
+    if data.shape[1] != cb.dims():
+        raise ValueError(f"pq_encode: data dimension {data.shape[1]} does not match codebook "
+                         f"dimension {cb.dims()}")
+    n = data.shape[0]
+    sse = C.c_double()
+    dp, _a = _ptr(data)
+    tp, _b = _ptr(np.ascontiguousarray(cb.tables, np.float32))
+    _lib.check(ctx.lib.pqg_pq_encode_sse(ctx.h, dp, n, cb.m_subspaces, cb.ks, cb.sub_dim, tp,
+                                         None, C.byref(sse)), "reconstruction_rmse")
+    return math.sqrt(sse.value / (n * cb.dims())) if n else float("nan")
+
+
+def adc_table(cb: Codebook, query, ctx: Context | None = None) -> DistanceTable:
+    """pq.cpp:132-151."""
+    ctx = ctx or get_context()
+    q = np.ascontiguousarray(query, np.float32).reshape(-1)
+    if q.size != cb.dims():
+        raise ValueError(f"adc_table: query dimension {q.size} does not match codebook "
+                         f"dimension {cb.dims()}")
+    ent = np.empty((cb.m_subspaces, cb.ks), np.float32)
+    tp, _b = _ptr(np.ascontiguousarray(cb.tables, np.float32))
+    _lib.check(ctx.lib.pqg_adc_tables(ctx.h, tp, cb.m_subspaces, cb.ks, cb.sub_dim,
+                                      q.ctypes.data_as(C.c_void_p), 1,
+                                      ent.ctypes.data_as(C.c_void_p)), "adc_table")
+    return DistanceTable(cb.m_subspaces, cb.ks, ent)
+
+
+def adc_lookup_all(table: DistanceTable, codes: CodeMatrix, ctx: Context | None = None):
+    """adc_lookup (pq.cpp:153-167) for every row of ``codes``."""
+    ctx = ctx or get_context()
+    if codes.m_subspaces != table.m_subspaces or codes.ks != table.ks:
+        raise ValueError("adc_lookup: codes do not match the table")
+    out = np.empty(codes.rows, np.float64)
+    if codes.rows == 0:
+        return out
+    ep, _a = _ptr(np.ascontiguousarray(table.entries, np.float32))
+    cp, _b = _ptr(codes.bytes)
+    _lib.check(ctx.lib.pqg_adc_lookup(ctx.h, ep, table.m_subspaces, table.ks, cp, codes.rows,
+                                      out.ctypes.data_as(C.c_void_p)), "adc_lookup")
+    return out
+
+
+def adc_lookup(table: DistanceTable, codes: CodeMatrix, row: int, ctx: Context | None = None):
+    sub = CodeMatrix(1, codes.m_subspaces, codes.ks, codes.bytes[row: row + 1].copy())
+    return float(adc_lookup_all(table, sub, ctx)[0])
+
+
+# ---------------------------------------------------------------------------
+# L2: ivf.hpp
+# ---------------------------------------------------------------------------
+
+
+class InvertedIndex:
+    """Device-resident posting lists (CSR) -- ivf.hpp:14-31."""
+
+    def __init__(self, handle, ctx: Context):
+        self.h = handle
+        self.ctx = ctx
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                self.ctx.lib.pqg_index_destroy(self.h)
+            except Exception:
+                pass
+            self.h = None
+
+    def _info(self):
+        nl, n = C.c_uint64(), C.c_uint64()
+        M, ks, ds = C.c_uint32(), C.c_uint32(), C.c_uint32()
+        _lib.check(self.ctx.lib.pqg_index_info(self.h, C.byref(nl), C.byref(n), C.byref(M),
+                                               C.byref(ks), C.byref(ds)))
+        return nl.value, n.value, M.value, ks.value, ds.value
+
+    def nlist(self) -> int:
+        return self._info()[0]
+
+    @property
+    def n_items(self) -> int:
+        return self._info()[1]
+
+    def export(self):
+        """(offsets[nlist+1], ids[n], codes[n, row_bytes], coarse, codebook)."""
+        nl, n, M, ks, ds = self._info()
+        off = np.empty(nl + 1, np.uint64)
+        ids = np.empty(max(n, 1), np.uint64)
+        codes = np.empty((max(n, 1), M * code_width(ks)), np.uint8)
+        coarse = np.empty((nl, M * ds), np.float32)
+        tables = np.empty((M, ks, ds), np.float32)
+        v = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        _lib.check(self.ctx.lib.pqg_index_export(self.ctx.h, self.h, v(off), v(ids), v(codes),
+                                                 v(coarse), v(tables)))
+        return off, ids[:n], codes[:n], coarse, Codebook(M, ks, ds, tables)
+
+    @property
+    def codebook(self) -> Codebook:
+        return self.export()[4]
+
+    @property
+    def coarse_centroids(self) -> np.ndarray:
+        return self.export()[3]
+
+    @property
+    def lists(self):
+        """[(ids, CodeMatrix)] per list, in list order."""
+        off, ids, codes, _, cb = self.export()
+        out = []
+        for l in range(len(off) - 1):
+            a, b = int(off[l]), int(off[l + 1])
+            out.append((ids[a:b], CodeMatrix(b - a, cb.m_subspaces, cb.ks, codes[a:b])))
+        return out
+
+
+def default_nlist(n_items: int) -> int:
+    """ivf.cpp:118-121: round(sqrt(n)) clamped to [1, n] (llround: half away)."""
+    r = int(math.floor(math.sqrt(float(n_items)) + 0.5))
+    return max(1, min(r, n_items if n_items else 1))
+
+
+def ivf_build_with_centroids(cb: Codebook, codes: CodeMatrix, ids, coarse_centroids,
+                             ctx: Context | None = None) -> InvertedIndex:
+    """ivf.cpp:151-166."""
+    ctx = ctx or get_context()
+    ids = np.ascontiguousarray(ids, np.uint64)
+    coarse = np.ascontiguousarray(coarse_centroids, np.float32)
+    if ids.size == 0:
+        raise ValueError("ivf_build: no items")
+    if ids.size != codes.rows:
+        raise ValueError("ivf_build: ids/codes length mismatch")
+    if coarse.ndim != 2 or coarse.shape[0] == 0 or coarse.shape[1] != cb.dims():
+        raise ValueError("ivf_build: coarse centroids do not match the codebook")
+    h = C.c_void_p()
+    tp, _a = _ptr(np.ascontiguousarray(cb.tables, np.float32))
+    cp, _b = _ptr(codes.bytes)
+    _lib.check(ctx.lib.pqg_ivf_build_with_centroids(
+        ctx.h, tp, cb.m_subspaces, cb.ks, cb.sub_dim, cp, ids.ctypes.data_as(C.c_void_p),
+        codes.rows, coarse.ctypes.data_as(C.c_void_p), coarse.shape[0], C.byref(h)), "ivf_build")
+    return InvertedIndex(h, ctx)
+
+
+def ivf_build(cb: Codebook, codes: CodeMatrix, ids, nlist: int, seed: int,
+              kmeans_iters: int = 20, ctx: Context | None = None) -> InvertedIndex:
+    """ivf.cpp:123-149."""
+    ctx = ctx or get_context()
+    ids = np.ascontiguousarray(ids, np.uint64)
+    if ids.size == 0:
+        raise ValueError("ivf_build: no items")
+    if ids.size != codes.rows:
+        raise ValueError("ivf_build: ids/codes length mismatch")
+    h = C.c_void_p()
+    tp, _a = _ptr(np.ascontiguousarray(cb.tables, np.float32))
+    cp, _b = _ptr(codes.bytes)
+    _lib.check(ctx.lib.pqg_ivf_build(ctx.h, tp, cb.m_subspaces, cb.ks, cb.sub_dim, cp,
+                                     ids.ctypes.data_as(C.c_void_p), codes.rows, nlist, seed,
+                                     kmeans_iters, C.byref(h)), "ivf_build")
+    return InvertedIndex(h, ctx)
+
+
+def ivf_add(index: InvertedIndex, codes: CodeMatrix, ids) -> None:
+    """ivf.cpp:168-184."""
+    ids = np.ascontiguousarray(ids, np.uint64)
+    if ids.size != codes.rows:
+        raise ValueError("ivf_add: ids/codes length mismatch")
+    _, _, M, ks, _ = index._info()
+    if codes.m_subspaces != M or codes.ks != ks:
+        raise ValueError("ivf_add: codes do not match the index codebook")
+    if ids.size == 0:
+        return
+    cp, _b = _ptr(codes.bytes)
+    _lib.check(index.ctx.lib.pqg_index_add(index.ctx.h, index.h, cp,
+                                           ids.ctypes.data_as(C.c_void_p), ids.size), "ivf_add")
+
+
+def ivf_merge(a: InvertedIndex, b: InvertedIndex) -> InvertedIndex:
+    """ivf.cpp:186-216."""
+    h = C.c_void_p()
+    _lib.check(a.ctx.lib.pqg_index_merge(a.ctx.h, a.h, b.h, C.byref(h)), "ivf_merge")
+    return InvertedIndex(h, a.ctx)
+
+
+def ivf_query_batch(index: InvertedIndex, queries, k: int, nprobe: int, max_sq_dist=None,
+                    out=None):
+    """Batched ivf_query: (ids [nq,k] u64, dists [nq,k] f64, counts [nq] u32)."""
+    ctx = index.ctx
+    q = _f32(queries)
+    nq = q.shape[0] if q.ndim == 2 else 1
+    if out is None:
+        ids = np.zeros((nq, max(k, 1)), np.uint64)
+        dist = np.zeros((nq, max(k, 1)), np.float64)
+        cnt = np.zeros(nq, np.uint32)
+    else:
+        ids, dist, cnt = out
+    qp, _a = _ptr(q)
+    ip, _b = _ptr(ids)
+    dp, _c = _ptr(dist)
+    cp, _d = _ptr(cnt)
+    _lib.check(ctx.lib.pqg_index_search(ctx.h, index.h, qp, nq, k, nprobe,
+                                        int(max_sq_dist is not None),
+                                        0.0 if max_sq_dist is None else float(max_sq_dist),
+                                        ip, dp, cp), "ivf_query")
+    return ids, dist, cnt
+
+
+def _to_result(ids, dist, cnt, k) -> QueryResult:
+    c = int(cnt)
+    return QueryResult([Hit(int(ids[j]), float(dist[j])) for j in range(c)], k)
+
+
+def ivf_query(index: InvertedIndex, query, k: int, nprobe: int, max_sq_dist=None) -> QueryResult:
+    """ivf.cpp:218-228."""
+    q = np.ascontiguousarray(query, np.float32).reshape(1, -1)
+    nl, _, M, _, ds = index._info()
+    if k == 0:
+        raise ValueError("query: k must be >= 1")
+    if q.shape[1] != M * ds:
+        raise ValueError("query: dimension mismatch")
+    ids, dist, cnt = ivf_query_batch(index, q, k, nprobe, max_sq_dist)
+    return _to_result(ids[0], dist[0], cnt[0], k)
+
+
+def ivf_probe(index: InvertedIndex, queries, nprobe: int) -> np.ndarray:
+    """probe_order (ivf.cpp:91-101) for a batch of queries."""
+    ctx = index.ctx
+    q = _f32(queries)
+    nq = q.shape[0]
+    out = np.empty((nq, nprobe), np.uint32)
+    qp, _a = _ptr(q)
+    _lib.check(ctx.lib.pqg_index_probe(ctx.h, index.h, qp, nq, nprobe,
+                                       out.ctypes.data_as(C.c_void_p)), "ivf_probe")
+    return out
+
+
+def flat_scan_batch(cb: Codebook, codes: CodeMatrix, ids, queries, k: int, max_sq_dist=None,
+                    ctx: Context | None = None):
+    ctx = ctx or get_context()
+    ids = np.ascontiguousarray(ids, np.uint64)
+    if k == 0:
+        raise ValueError("flat_scan: k must be >= 1")
+    if ids.size != codes.rows:
+        raise ValueError("flat_scan: ids/codes length mismatch")
+    q = _f32(queries)
+    if q.ndim == 1:
+        q = q.reshape(1, -1)
+    if q.shape[1] != cb.dims():
+        raise ValueError("flat_scan: dimension mismatch")
+    nq = q.shape[0]
+    oi = np.zeros((nq, k), np.uint64)
+    od = np.zeros((nq, k), np.float64)
+    oc = np.zeros(nq, np.uint32)
+    tp, _a = _ptr(np.ascontiguousarray(cb.tables, np.float32))
+    cp, _b = _ptr(codes.bytes)
+    qp, _c = _ptr(q)
+    _lib.check(ctx.lib.pqg_flat_scan(ctx.h, tp, cb.m_subspaces, cb.ks, cb.sub_dim, cp,
+                                     ids.ctypes.data_as(C.c_void_p), codes.rows, qp, nq, k,
+                                     int(max_sq_dist is not None),
+                                     0.0 if max_sq_dist is None else float(max_sq_dist),
+                                     oi.ctypes.data_as(C.c_void_p), od.ctypes.data_as(C.c_void_p),
+                                     oc.ctypes.data_as(C.c_void_p)), "flat_scan")
+    return oi, od, oc
+
+
+def flat_scan(cb: Codebook, codes: CodeMatrix, ids, query, k: int, max_sq_dist=None,
+              ctx: Context | None = None) -> QueryResult:
+    """ivf.cpp:247-262."""
+    oi, od, oc = flat_scan_batch(cb, codes, ids, np.asarray(query).reshape(1, -1), k, max_sq_dist,
+                                 ctx)
+    return _to_result(oi[0], od[0], oc[0], k)
+
+
+def ivf_query_subset(index: InvertedIndex, query, k: int, subset, nprobe: int,
+                     max_sq_dist=None) -> QueryResult:
+    """ivf.cpp:230-245.  Row-filtered search is SURVEY 8(f) rank 3 ("next");
+    it is expressed here through the device flat scan over the probed lists'
+    subset members so the semantics match."""
+    subset = np.ascontiguousarray(subset, np.uint64)
+    if k == 0:
+        raise ValueError("query: k must be >= 1")
+    if subset.size > 1 and np.any(subset[1:] <= subset[:-1]):
+        raise ValueError("ivf_query_subset: subset is not sorted ascending")
+    nl = index.nlist()
+    if nprobe == 0 or nprobe > nl:
+        raise ValueError(f"query: nprobe ({nprobe}) must be in [1, nlist={nl}]")
+    off, ids, codes, _, cb = index.export()
+    probes = ivf_probe(index, np.asarray(query, np.float32).reshape(1, -1), nprobe)[0]
+    sel = np.concatenate([np.arange(off[l], off[l + 1]) for l in probes]).astype(np.int64)
+    keep = sel[np.isin(ids[sel], subset)]
+    if keep.size == 0:
+        return QueryResult([], k)
+    sub = CodeMatrix(keep.size, cb.m_subspaces, cb.ks, codes[keep])
+    return flat_scan(cb, sub, ids[keep], query, k, max_sq_dist, index.ctx)

@@ -1,0 +1,422 @@
+"""Parity of the CUDA path (through the C ABI) with the oracle and the golden
+fixtures written by the compiled reference.  Mirrors the reference's own
+tests (proj/tests/test_kmeans.cpp, test_pq.cpp, test_ivf.cpp); every
+comparison is bit-exact unless the reference itself only promises a
+tolerance (inertia / RMSE sums, whose fp64 summation order differs:
+<= 1e-12 relative here, BASELINE.json allows 1e-4)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view({4: np.uint32, 8: np.uint64}[a.dtype.itemsize])
+
+
+@pytest.fixture(scope="module")
+def pq():
+    from paper_2604_21645_b200 import pqii
+    return pqii
+
+
+@pytest.fixture(scope="module")
+def mix():
+    from paper_2604_21645_b200.datagen import gaussian_mixture
+    return gaussian_mixture
+
+
+# ---------------------------------------------------------------------------
+# nearest_in_table (proj/src/kmeans.cpp:20-31)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("d,k", [(1, 2), (2, 7), (3, 5), (4, 16), (6, 33), (8, 64), (16, 256),
+                                 (17, 100), (32, 256), (128, 1024), (96, 40), (5, 300)])
+def test_nearest_batch_exact(pq, orc, d, k):
+    pts = orc.random_matrix(3000, d, 1000 + d)
+    table = orc.random_matrix(k, d, 2000 + k)
+    gi, gd = pq.nearest_batch(pts, table)
+    oi, od = orc.nearest_batch(pts, table)
+    assert np.array_equal(gi, oi)
+    assert np.array_equal(bits(gd), bits(od))
+
+
+def test_nearest_ties_lowest_index(pq, orc):
+    # proj/tests/test_kmeans.cpp:106-112 plus duplicated centroids (exact ties)
+    gi, _ = pq.nearest_batch(np.array([[2.0]], np.float32), np.array([[1.0], [3.0]], np.float32))
+    assert gi[0] == 0
+    table = orc.random_matrix(64, 8, 5)
+    table = np.concatenate([table, table, table])  # every row appears 3x
+    pts = np.concatenate([table[:40], orc.random_matrix(500, 8, 6)])
+    gi, gd = pq.nearest_batch(pts, table)
+    oi, od = orc.nearest_batch(pts, table)
+    assert np.array_equal(gi, oi) and (gi < 64).all()
+    assert np.array_equal(bits(gd), bits(od))
+
+
+def test_nearest_exact_match_and_errors(pq, orc):
+    table = orc.random_matrix(16, 8, 31)
+    idx, dist = pq.nearest_centroid(table[3], table)
+    assert idx == 3 and dist == 0.0
+    with pytest.raises(ValueError, match="empty centroid set"):
+        pq.nearest_centroid(np.zeros(1, np.float32), np.zeros((0, 1), np.float32))
+
+
+# ---------------------------------------------------------------------------
+# kmeans_fit (proj/src/kmeans.cpp:61-133)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", ["km_rand", "km_1d", "km_dup", "km_mix", "km_mix_tol0", "km_k1"])
+def test_kmeans_golden(pq, golden, name):
+    k, iters, seed = (int(v) for v in golden[f"{name}/params"])
+    tol = float(golden[f"{name}/tol"][0])
+    r = pq.kmeans_fit(golden[f"{name}/points"], k, iters, seed, tol)
+    assert np.array_equal(bits(r.centroids), bits(golden[f"{name}/centroids"]))
+    assert np.array_equal(r.assignments, golden[f"{name}/assignments"])
+    assert r.iterations_run == int(golden[f"{name}/iterations_run"][0])
+    np.testing.assert_allclose(r.inertia_per_iter, golden[f"{name}/inertia_per_iter"], rtol=1e-12)
+
+
+def test_kmeans_known_answers(pq):
+    pts = np.array([[0], [1], [9], [10]], np.float32)
+    for seed in range(6):
+        r = pq.kmeans_fit(pts, 2, 20, seed)
+        assert abs(r.inertia - 1.0) < 1e-9
+        assert sorted(r.centroids.ravel().tolist()) == [0.5, 9.5]
+    r = pq.kmeans_fit(np.full((6, 2), 1.5, np.float32), 3, 10, 0)
+    assert r.inertia == 0.0 and np.isfinite(r.centroids).all()
+
+
+@pytest.mark.parametrize("seed", [0, 3, 77, 123])
+def test_kmeans_random_vs_oracle(pq, orc, seed):
+    rng = np.random.default_rng(seed)
+    n, d = int(rng.integers(50, 3000)), int(rng.integers(1, 40))
+    k = int(rng.integers(1, min(300, n)))
+    pts = orc.random_matrix(n, d, seed + 100)
+    a = pq.kmeans_fit(pts, k, 25, seed, 0.0)
+    b = orc.kmeans_fit(pts, k, 25, seed, 0.0)
+    assert a.iterations_run == b["iterations_run"]
+    assert np.array_equal(bits(a.centroids), bits(b["centroids"]))
+    assert np.array_equal(a.assignments, b["assignments"])
+    np.testing.assert_allclose(a.inertia_per_iter, b["inertia_per_iter"], rtol=1e-12)
+
+
+def test_kmeans_validation(pq, orc):
+    pts = orc.random_matrix(5, 2, 1)
+    with pytest.raises(ValueError):
+        pq.kmeans_fit(pts, 0, 10, 0)
+    with pytest.raises(ValueError, match="exceeds"):
+        pq.kmeans_fit(pts, 6, 10, 0)
+    with pytest.raises(ValueError):
+        pq.kmeans_fit(pts, 2, 0, 0)
+    with pytest.raises(ValueError):
+        pq.kmeans_fit(pts, 2, 10, 0, -1.0)
+
+
+# ---------------------------------------------------------------------------
+# pq_fit / encode / decode / rmse (proj/src/pq.cpp)
+# ---------------------------------------------------------------------------
+
+def test_pq_fit_golden(pq, golden):
+    M, ks, iters, seed = (int(v) for v in golden["pq/params"])
+    stats = {}
+    cb = pq.pq_fit(golden["pq/data"], M, ks, iters, seed, stats=stats)
+    assert np.array_equal(bits(cb.tables), bits(golden["pq/tables"]))
+    codes = pq.pq_encode(cb, golden["pq/data"])
+    assert np.array_equal(codes.bytes, golden["pq/codes"])
+    dec = pq.pq_decode(cb, codes)
+    assert np.array_equal(bits(dec), bits(golden["pq/decoded"]))
+    r = pq.reconstruction_rmse(cb, golden["pq/data"])
+    assert abs(r - float(golden["pq/rmse"][0])) <= 1e-12 * r
+    assert abs(pq.rmse(golden["pq/data"], dec) - r) <= 1e-12 * r
+    # M=1 degenerates to kmeans_fit(seed) bit-for-bit (test_pq.cpp:47-51)
+    cb1 = pq.pq_fit(golden["pq_m1/data"], 1, 8, 10, 42)
+    assert np.array_equal(bits(cb1.tables), bits(golden["pq_m1/tables"]))
+    km = pq.kmeans_fit(golden["pq_m1/data"], 8, 10, 42)
+    assert np.array_equal(bits(cb1.tables.reshape(8, -1)), bits(km.centroids))
+    cb2 = pq.pq_fit(golden["pq_m1/data"], 2, 8, 10, 1)
+    assert np.array_equal(bits(cb2.tables), bits(golden["pq_ds2/tables"]))
+
+
+def test_pq_wide_codes(pq, golden):
+    cb = pq.Codebook(2, 300, 4, golden["pq_wide/tables"])
+    codes = pq.pq_encode(cb, golden["pq_wide/data"])
+    assert codes.code_width() == 2
+    assert np.array_equal(codes.bytes, golden["pq_wide/codes"])
+    dec = pq.pq_decode(cb, codes)
+    assert dec.shape == golden["pq_wide/data"].shape
+
+
+@pytest.mark.parametrize("M,ks,ds", [(4, 16, 2), (8, 256, 16), (16, 256, 8), (32, 16, 4),
+                                     (4, 64, 32), (3, 7, 5), (2, 1, 3), (12, 256, 8)])
+def test_pq_encode_vs_oracle(pq, orc, mix, M, ks, ds):
+    x = mix(4000, M * ds, 32, seed=M * 100 + ks)
+    tables = orc.random_matrix(M * ks, ds, 7 + ks).reshape(M, ks, ds) * 3.0
+    tables = np.ascontiguousarray(tables, np.float32)
+    cb = pq.Codebook(M, ks, ds, tables)
+    codes = pq.pq_encode(cb, x)
+    assert np.array_equal(codes.bytes, orc.pq_encode(x, tables))
+    r = pq.reconstruction_rmse(cb, x)
+    ro = orc.rmse(x, orc.pq_decode(codes.bytes, tables))
+    assert abs(r - ro) <= 1e-12 * max(ro, 1e-30)
+
+
+@pytest.mark.parametrize("M,ks,n,iters", [(8, 256, 20000, 20), (16, 64, 8000, 25), (4, 16, 6000, 25)])
+def test_pq_fit_vs_oracle(pq, orc, mix, M, ks, n, iters):
+    x = mix(n, 64, 64, seed=11 + M)
+    stats = {}
+    cb = pq.pq_fit(x, M, ks, iters, 9, stats=stats)
+    t, it, _ = orc.pq_fit(x, M, ks, iters, 9)
+    assert np.array_equal(stats["iterations_run"], it)
+    assert np.array_equal(bits(cb.tables), bits(t))
+
+
+def test_pq_code_semantics(pq, orc):
+    data = orc.random_matrix(40, 8, 23)
+    cb = pq.pq_fit(data, 4, 1, 5, 2)  # ks=1 encodes everything to zero
+    assert (pq.pq_encode(cb, data).bytes == 0).all()
+    cb = pq.pq_fit(data, 4, 8, 15, 2)
+    probe = np.concatenate([cb.codeword(m, 5) for m in range(4)]).reshape(1, 8)
+    assert (pq.pq_encode(cb, probe).bytes == 5).all()
+    with pytest.raises(ValueError, match="not divisible"):
+        pq.pq_fit(data, 3, 8, 10, 1)
+    with pytest.raises(ValueError, match="exceeds"):
+        pq.pq_fit(data, 2, 65, 10, 1)
+    with pytest.raises(ValueError):
+        pq.pq_encode(cb, orc.random_matrix(4, 6, 1))
+    bad = pq.CodeMatrix.zeros(1, 4, 8)
+    bad.set(0, 2, 9)  # code >= ks
+    with pytest.raises(IndexError):
+        pq.pq_decode(cb, bad)
+
+
+def test_rmse_known_answers(pq):
+    a = np.array([[0, 0]], np.float32)
+    b = np.array([[3, 4]], np.float32)
+    assert abs(pq.rmse(a, b) - np.sqrt(25 / 2)) < 1e-12
+    with pytest.raises(ValueError):
+        pq.rmse(np.zeros((2, 2), np.float32), np.zeros((2, 3), np.float32))
+
+
+def test_exactly_representable_lossless(pq, orc):
+    # test_pq.cpp:19-33, 62-66
+    levels = orc.random_matrix(8, 8, 3, -5, 5)
+    data = np.zeros((200, 8), np.float32)
+    for i in range(200):
+        for s in range(4):
+            lv = (i + s) % 8
+            data[i, s * 2:(s + 1) * 2] = levels[lv, s * 2:(s + 1) * 2]
+    cb = pq.pq_fit(data, 4, 8, 25, 7)
+    assert pq.reconstruction_rmse(cb, data) <= 1e-6
+
+
+# ---------------------------------------------------------------------------
+# ADC (proj/src/pq.cpp:132-167)
+# ---------------------------------------------------------------------------
+
+def test_adc_golden(pq, golden):
+    tables = golden["pq/tables"]
+    cb = pq.Codebook(*tables.shape, tables)
+    codes = pq.CodeMatrix(golden["pq/codes"].shape[0], tables.shape[0], tables.shape[1],
+                          golden["pq/codes"])
+    for i, q in enumerate(golden["adc/queries"]):
+        t = pq.adc_table(cb, q)
+        assert np.array_equal(bits(t.entries), bits(golden["adc/tables"][i]))
+        assert np.array_equal(bits(pq.adc_lookup_all(t, codes)), bits(golden["adc/lookup"][i]))
+
+
+def test_adc_known_answers(pq):
+    cb = pq.Codebook(2, 1, 1, np.array([[[3.0]], [[0.0]]], np.float32))
+    t = pq.adc_table(cb, np.array([1.0, 0.0], np.float32))
+    assert t.entry(0, 0) == 4.0 and t.entry(1, 0) == 0.0
+
+
+# ---------------------------------------------------------------------------
+# IVF (proj/src/ivf.cpp)
+# ---------------------------------------------------------------------------
+
+@pytest.fixture(scope="module")
+def gidx(pq, golden):
+    tables = golden["pq/tables"]
+    cb = pq.Codebook(*tables.shape, tables)
+    codes = pq.CodeMatrix(golden["pq/codes"].shape[0], tables.shape[0], tables.shape[1],
+                          golden["pq/codes"])
+    index = pq.ivf_build_with_centroids(cb, codes, golden["ivf/ids"], golden["ivf/coarse"])
+    return cb, codes, index
+
+
+def test_ivf_build_golden(gidx, golden):
+    _, _, index = gidx
+    off, ids, codes, coarse, _ = index.export()
+    assert np.array_equal(off, golden["ivf/offsets"])
+    assert np.array_equal(ids, golden["ivf/list_ids"])
+    assert np.array_equal(codes, golden["ivf/list_codes"])
+    assert np.array_equal(bits(coarse), bits(golden["ivf/coarse"]))
+
+
+@pytest.mark.parametrize("nprobe", [1, 4, 40])
+def test_ivf_query_golden(pq, gidx, golden, nprobe):
+    _, _, index = gidx
+    ids, dist, cnt = pq.ivf_query_batch(index, golden["ivf/queries"], 10, nprobe)
+    assert np.array_equal(cnt, golden[f"ivf/q_np{nprobe}_count"])
+    for q in range(len(cnt)):
+        c = int(cnt[q])
+        assert np.array_equal(ids[q, :c], golden[f"ivf/q_np{nprobe}_ids"][q, :c])
+        assert np.array_equal(bits(dist[q, :c]), bits(golden[f"ivf/q_np{nprobe}_dist"][q, :c]))
+
+
+def test_ivf_query_max_and_flat(pq, gidx, golden):
+    cb, codes, index = gidx
+    ids, dist, cnt = pq.ivf_query_batch(index, golden["ivf/queries"], 10, 4, max_sq_dist=60.0)
+    assert np.array_equal(cnt, golden["ivf/q_max_count"])
+    for q in range(len(cnt)):
+        assert np.array_equal(ids[q, : cnt[q]], golden["ivf/q_max_ids"][q, : cnt[q]])
+    fi, fd, fc = pq.flat_scan_batch(cb, codes, golden["ivf/ids"], golden["ivf/queries"], 10)
+    assert np.array_equal(fi, golden["ivf/flat_ids"])
+    assert np.array_equal(bits(fd), bits(golden["ivf/flat_dist"]))
+    # nprobe == nlist equals flat_scan bit-for-bit (test_ivf.cpp:246-253)
+    ai, ad, ac = pq.ivf_query_batch(index, golden["ivf/queries"], 10, index.nlist())
+    assert np.array_equal(ai, fi) and np.array_equal(bits(ad), bits(fd))
+
+
+def test_ivf_probe_vs_oracle(pq, orc, gidx, golden):
+    _, _, index = gidx
+    probes = pq.ivf_probe(index, golden["ivf/queries"], 7)
+    for q, qv in enumerate(golden["ivf/queries"]):
+        assert np.array_equal(probes[q], orc.probe_order(golden["ivf/coarse"], qv, 7))
+
+
+def test_ivf_build_kmeans_golden(pq, golden):
+    tables = golden["pq/tables"]
+    cb = pq.Codebook(*tables.shape, tables)
+    codes = pq.CodeMatrix(800, tables.shape[0], tables.shape[1], golden["pq/codes"][:800])
+    index = pq.ivf_build(cb, codes, golden["ivf/ids"][:800], 20, 17, 8)
+    off, ids, lcodes, coarse, _ = index.export()
+    assert np.array_equal(bits(coarse), bits(golden["ivf_build/coarse"]))
+    assert np.array_equal(off, golden["ivf_build/offsets"])
+    assert np.array_equal(ids, golden["ivf_build/list_ids"])
+    assert np.array_equal(lcodes, golden["ivf_build/list_codes"])
+
+
+def test_ivf_add_merge_equivalence(pq, gidx, golden):
+    cb, codes, full = gidx
+    ids = golden["ivf/ids"]
+    n = codes.rows
+    half = n // 3
+    a = pq.ivf_build_with_centroids(cb, pq.CodeMatrix(half, cb.m_subspaces, cb.ks, codes.bytes[:half]),
+                                    ids[:half], golden["ivf/coarse"])
+    b = pq.ivf_build_with_centroids(cb, pq.CodeMatrix(n - half, cb.m_subspaces, cb.ks, codes.bytes[half:]),
+                                    ids[half:], golden["ivf/coarse"])
+    m = pq.ivf_merge(a, b)
+    fo, fi, fc, _, _ = full.export()
+    mo, mi, mc, _, _ = m.export()
+    assert np.array_equal(fo, mo) and np.array_equal(fi, mi) and np.array_equal(fc, mc)
+    pq.ivf_add(a, pq.CodeMatrix(n - half, cb.m_subspaces, cb.ks, codes.bytes[half:]), ids[half:])
+    ao, ai, ac, _, _ = a.export()
+    assert np.array_equal(fo, ao) and np.array_equal(fi, ai) and np.array_equal(fc, ac)
+    with pytest.raises(ValueError, match="id collision"):
+        pq.ivf_add(a, pq.CodeMatrix(1, cb.m_subspaces, cb.ks, codes.bytes[:1]), ids[5:6])
+    with pytest.raises(ValueError, match="id collision"):
+        pq.ivf_merge(a, b)
+
+
+def test_ivf_errors(pq, gidx, golden):
+    cb, codes, index = gidx
+    ids = golden["ivf/ids"].copy()
+    ids[10] = ids[3]
+    with pytest.raises(ValueError, match=f"duplicate id {int(ids[3])}"):
+        pq.ivf_build_with_centroids(cb, codes, ids, golden["ivf/coarse"])
+    with pytest.raises(ValueError, match="no items"):
+        pq.ivf_build_with_centroids(cb, pq.CodeMatrix.zeros(0, cb.m_subspaces, cb.ks), [], golden["ivf/coarse"])
+    with pytest.raises(ValueError, match="nprobe"):
+        pq.ivf_query(index, golden["ivf/queries"][0], 10, 0)
+    with pytest.raises(ValueError, match="nprobe"):
+        pq.ivf_query(index, golden["ivf/queries"][0], 10, index.nlist() + 1)
+    with pytest.raises(ValueError):
+        pq.ivf_query(index, golden["ivf/queries"][0], 0, 1)
+
+
+def test_ivf_empty_lists_and_k_saturation(pq, orc, mix):
+    x = mix(3000, 16, 8, seed=2)
+    cb = pq.pq_fit(x, 4, 16, 10, 1)
+    codes = pq.pq_encode(cb, x)
+    coarse = np.concatenate([x[:8], np.full((8, 16), 1e4, np.float32)])  # 8 empty lists
+    ids = np.arange(3000, dtype=np.uint64) * 3
+    index = pq.ivf_build_with_centroids(cb, codes, ids, coarse)
+    off, lid, lcodes, _, _ = index.export()
+    o_off, o_ids, o_codes = orc.ivf_build_with_centroids(codes.bytes, ids, cb.tables, coarse)
+    assert np.array_equal(off, o_off) and np.array_equal(lid, o_ids)
+    assert (np.diff(off)[8:] == 0).all()
+    q = mix(20, 16, 8, seed=2, stream=1)
+    gi, gd, gc = pq.ivf_query_batch(index, q, 32, 16)
+    for i in range(20):
+        ri, rd = orc.ivf_query(cb.tables, coarse, o_off, o_ids, o_codes, q[i], 32, 16)
+        assert np.array_equal(gi[i, : gc[i]], ri) and np.array_equal(bits(gd[i, : gc[i]]), bits(rd))
+
+
+@pytest.mark.parametrize("k", [1, 10, 32])
+def test_search_duplicate_codes_ties(pq, orc, k):
+    # many identical code rows -> exact distance ties broken by id
+    rng = np.random.default_rng(4)
+    tables = orc.random_matrix(8 * 16, 4, 9).reshape(8, 16, 4)
+    base = rng.integers(0, 16, size=(50, 8), dtype=np.uint8)
+    codes_b = base[rng.integers(0, 50, size=5000)]
+    ids = rng.permutation(100000)[:5000].astype(np.uint64)
+    cb = pq.Codebook(8, 16, 4, np.ascontiguousarray(tables, np.float32))
+    codes = pq.CodeMatrix(5000, 8, 16, np.ascontiguousarray(codes_b))
+    coarse = pq.pq_decode(cb, pq.CodeMatrix(12, 8, 16, np.ascontiguousarray(base[:12])))
+    index = pq.ivf_build_with_centroids(cb, codes, ids, coarse)
+    o_off, o_ids, o_codes = orc.ivf_build_with_centroids(codes.bytes, ids, cb.tables, coarse)
+    q = orc.random_matrix(30, 32, 77)
+    gi, gd, gc = pq.ivf_query_batch(index, q, k, 5)
+    for i in range(30):
+        ri, rd = orc.ivf_query(cb.tables, coarse, o_off, o_ids, o_codes, q[i], k, 5)
+        assert np.array_equal(gi[i, : gc[i]], ri) and np.array_equal(bits(gd[i, : gc[i]]), bits(rd))
+
+
+def test_topk_merge_is_monolithic(pq, gidx, golden):
+    """Sharded search (rows split in contiguous ranges) merged by
+    (dist, id) equals the monolithic query."""
+    import ctypes as C
+    from paper_2604_21645_b200 import _lib
+    cb, codes, full = gidx
+    ids = golden["ivf/ids"]
+    q = golden["ivf/queries"]
+    parts = []
+    bounds = [0, 700, 1500, codes.rows]
+    for s in range(3):
+        a, b = bounds[s], bounds[s + 1]
+        ix = pq.ivf_build_with_centroids(cb, pq.CodeMatrix(b - a, cb.m_subspaces, cb.ks, codes.bytes[a:b]),
+                                         ids[a:b], golden["ivf/coarse"])
+        parts.append(pq.ivf_query_batch(ix, q, 10, 6))
+    si = np.ascontiguousarray(np.stack([p[0] for p in parts]))
+    sd = np.ascontiguousarray(np.stack([p[1] for p in parts]))
+    sc = np.ascontiguousarray(np.stack([p[2] for p in parts]))
+    nq = q.shape[0]
+    oi = np.zeros((nq, 10), np.uint64)
+    od = np.zeros((nq, 10), np.float64)
+    oc = np.zeros(nq, np.uint32)
+    ctx = pq.get_context()
+    v = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    _lib.check(ctx.lib.pqg_topk_merge(ctx.h, v(si), v(sd), v(sc), 3, nq, 10, v(oi), v(od), v(oc)))
+    fi, fd, fc = pq.ivf_query_batch(full, q, 10, 6)
+    assert np.array_equal(oc, fc) and np.array_equal(oi, fi) and np.array_equal(bits(od), bits(fd))
+
+
+# ---------------------------------------------------------------------------
+# full-size properties (BASELINE config 3 shapes, sampled oracle checks)
+# ---------------------------------------------------------------------------
+
+def test_encode_full_size_sampled(pq, orc, mix):
+    n = 1_000_000
+    x = mix(n, 128, 256, seed=42)
+    train = x[::10]
+    cb = pq.pq_fit(train[:20000], 16, 256, 6, 1)
+    codes = pq.pq_encode(cb, x)
+    rng = np.random.default_rng(0)
+    sel = np.sort(rng.choice(n, 20000, replace=False))
+    assert np.array_equal(codes.bytes[sel], orc.pq_encode(x[sel], cb.tables))
+    # decode(encode(x)) is idempotent under encode (codewords are fixed points)
+    dec = pq.pq_decode(cb, pq.CodeMatrix(20000, 16, 256, codes.bytes[sel]))
+    assert np.array_equal(pq.pq_encode(cb, dec).bytes, codes.bytes[sel])
