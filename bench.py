@@ -1,0 +1,496 @@
+"""Benchmark of the PQ / IVF hot path on B200 (contract: one JSON line).
+
+Workload (N=1): BASELINE.json configs[1] -- N=1,000,000 x D=128 fp32 rows of a
+seeded 256-component Gaussian mixture; PQ k-means (25 iterations on a seeded
+100k-row sample) then encode of all 1M rows.  The headline `value` is PQ
+encode vectors/s at M=8, Ks=256 (the reference's own config-1 codebook shape);
+the sweep over M in {4,8,16,32} x Ks in {16,64,256}, the k-means iterations/s
+and the config-3 ADC search queries/s (1M items, nlist 1024, 10k queries,
+nprobe 16, k 10) ride along in the same line.
+
+A step = one pq_encode of the 1M device-resident rows (512 MB > the 126 MB
+L2, so no flush is needed between steps).  `e2e` is the same metric through
+the C ABI with pinned HOST buffers (H2D of the rows and D2H of the codes in
+the timed region).  `--impl reference` times the reference's own pq_encode
+(oracle/_ref, compiled from its sources) on the host cores.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PQ encode vectors/s and k-means iters/s at M,Ks; ADC queries/s; % of roofline"
+N_ROWS = 1_000_000
+DIMS = 128
+COMPONENTS = 256
+SAMPLE = 100_000
+FIT_ITERS = 25
+HEAD_M, HEAD_KS = 8, 256
+SEED = 2604
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing (torch.distributed over NCCL, one process per GPU)
+# ---------------------------------------------------------------------------
+def dist_setup():
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def ncu_traffic(kernel_key: str):
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    v = d.get(kernel_key, {})
+    return v.get("dram_bytes_per_launch")
+
+
+# ---------------------------------------------------------------------------
+# reference arm (the reference's own CPU code, all host threads)
+# ---------------------------------------------------------------------------
+def reference_encode_rate(x: np.ndarray, tables: np.ndarray, threads: int, rows: int):
+    import oracle
+    R = oracle.ref_impl()
+    sample = np.ascontiguousarray(x[:rows])
+    t0 = time.perf_counter()
+    R.pq_encode(sample, tables, threads=threads)
+    dt = time.perf_counter() - t0
+    return rows / dt, dt
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import oracle
+    from paper_2604_21645_b200.datagen import gaussian_mixture
+    if not oracle.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libpqii_ref.so not built"}))
+        return
+    R = oracle.ref_impl()
+    threads = max(1, R.hardware_concurrency())
+    x = gaussian_mixture(N_ROWS, DIMS, COMPONENTS, SEED)
+    tables = reference_codebook(x)
+    rows = min(N_ROWS, 2500 * threads)  # ~0.1-0.2 s per step at ~20k vec/s/thread
+    for _ in range(args.warmup):
+        reference_encode_rate(x, tables, threads, rows)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        reference_encode_rate(x, tables, threads, rows)
+    dt = (time.perf_counter() - t0) / args.steps
+    v = rows / dt
+    print(json.dumps({
+        "metric": METRIC, "value": v, "unit": "vectors/s", "impl": "reference", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_block(world),
+        "cpu_baseline": {"value": v, "unit": "vectors/s", "cores": threads, "kind": "reference",
+                         "sample": f"pq_encode of {rows} of the 1M rows per step, M={HEAD_M} Ks={HEAD_KS}, "
+                                   f"chunk_rows over {threads} threads (proj/src/pipeline.cpp:226-231)"},
+        "e2e": {"value": v, "unit": "vectors/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def reference_codebook(x):
+    """A fixed M=8, Ks=256 codebook for the reference arm: rows of the sample
+    (fitting it on the CPU would take minutes; encode cost does not depend on
+    the codebook values)."""
+    from paper_2604_21645_b200.datagen import strided_sample
+    s = strided_sample(N_ROWS, SAMPLE, SEED)
+    ds = DIMS // HEAD_M
+    t = np.empty((HEAD_M, HEAD_KS, ds), np.float32)
+    for m in range(HEAD_M):
+        t[m] = x[s[m * HEAD_KS:(m + 1) * HEAD_KS], m * ds:(m + 1) * ds]
+    return t
+
+
+def config_block(world):
+    return {"workload": "BASELINE configs[1]: 1M x 128 fp32, 256-comp Gaussian mixture; "
+                        f"PQ fit {FIT_ITERS} iters on seeded 100k sample + encode all rows "
+                        f"(headline M={HEAD_M}, Ks={HEAD_KS}); ADC per configs[2]",
+            "rows_per_gpu": N_ROWS, "dims": DIMS, "M": HEAD_M, "Ks": HEAD_KS,
+            "global_rows": N_ROWS * world, "parallelism": f"row shards x{world}",
+            "l2": "inputs (512 MB/GPU) exceed the 126 MB L2; no flush needed",
+            "seed": SEED}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world, local):
+    import torch
+
+    import paper_2604_21645_b200._lib as L
+    from paper_2604_21645_b200 import pqii
+    from paper_2604_21645_b200.datagen import gaussian_mixture, strided_sample
+
+    torch.cuda.set_device(local)
+    ctx = pqii.Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    lib = ctx.lib
+    vp = C.c_void_p
+
+    # per-rank shard of rows (weak scaling: 1M rows per GPU), generated per shard
+    x_host = gaussian_mixture(N_ROWS, DIMS, COMPONENTS, SEED, stream=2 + rank)
+    x = torch.from_numpy(x_host).cuda()
+    sample_idx = torch.from_numpy(strided_sample(N_ROWS, SAMPLE, SEED)).cuda()
+    train = x.index_select(0, sample_idx).contiguous()
+
+    def fit(M, ks, iters=FIT_ITERS):
+        ds = DIMS // M
+        tables = torch.empty((M, ks, ds), dtype=torch.float32, device="cuda")
+        it = np.zeros(M, np.uint32)
+        L.check(lib.pqg_pq_fit(ctx.h, vp(train.data_ptr()), SAMPLE, DIMS, M, ks, iters, SEED,
+                               vp(tables.data_ptr()), it.ctypes.data_as(vp), None), "pq_fit")
+        return tables, int(it.max())
+
+    def encode(tables, M, ks, codes):
+        L.check(lib.pqg_pq_encode(ctx.h, vp(x.data_ptr()), N_ROWS, M, ks, DIMS // M,
+                                  vp(tables.data_ptr()), vp(codes.data_ptr())), "encode")
+
+    def rmse_of(tables, M, ks, codes):
+        sse = C.c_double()
+        L.check(lib.pqg_pq_recon_sse(ctx.h, vp(x.data_ptr()), vp(codes.data_ptr()), N_ROWS, M, ks,
+                                     DIMS // M, vp(tables.data_ptr()), C.byref(sse)), "sse")
+        return (sse.value / (N_ROWS * DIMS)) ** 0.5
+
+    def timed(fn, steps, warmup):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        barrier(world)
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(steps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        return max_over_ranks(a.elapsed_time(b) / steps, world)
+
+    # ---- k-means fit at the headline point (iters/s)
+    fit(HEAD_M, HEAD_KS)  # warm-up (also JIT of module-level state)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    tables, iters_run = fit(HEAD_M, HEAD_KS)
+    torch.cuda.synchronize()
+    fit_s = max_over_ranks(time.perf_counter() - t0, world)
+    kmeans_ips = iters_run / fit_s
+
+    # ---- headline encode, timed with profiling of the dominant kernel
+    codes = torch.empty((N_ROWS, HEAD_M), dtype=torch.uint8, device="cuda")
+    encode(tables, HEAD_M, HEAD_KS, codes)
+    l0 = ctx.launches
+    with ClockSampler(local) as clk:
+        ctx.profile(True)
+        ms = timed(lambda: encode(tables, HEAD_M, HEAD_KS, codes), args.steps, args.warmup)
+        n_near, near_ms = ctx.profile_read("nearest")
+        n_fix, fix_ms = ctx.profile_read("fixup")
+        n_norm, norm_ms = ctx.profile_read("norms")
+        ctx.profile(False)
+    launches_per_step = (ctx.launches - l0) / (args.steps + args.warmup)
+    value = N_ROWS * world / (ms / 1e3)
+    head_rmse = rmse_of(tables, HEAD_M, HEAD_KS, codes)
+
+    # roofline of the dominant kernel (fp32 screen; 2*Ks*D flops per vector)
+    peaks, src = measured_peaks()
+    near_avg_ms = near_ms / max(n_near, 1)
+    flops_per_launch = float(N_ROWS) * 2 * HEAD_KS * DIMS
+    achieved_tflops = flops_per_launch / (near_avg_ms / 1e3) / 1e12
+    props = torch.cuda.get_device_properties(local)
+    fp32_peak = props.multi_processor_count * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+    traffic = ncu_traffic("nearest_encode_M8_Ks256")
+
+    # ---- e2e through the C ABI with pinned host buffers
+    xh = torch.from_numpy(x_host).pin_memory()
+    ch = torch.empty((N_ROWS, HEAD_M), dtype=torch.uint8).pin_memory()
+    tables_h = tables.cpu().contiguous()
+
+    def e2e_step():
+        L.check(lib.pqg_pq_encode(ctx.h, vp(xh.data_ptr()), N_ROWS, HEAD_M, HEAD_KS, DIMS // HEAD_M,
+                                  vp(tables_h.data_ptr()), vp(ch.data_ptr())), "encode_e2e")
+
+    for _ in range(args.warmup):
+        e2e_step()
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / args.steps, world)
+    assert torch.equal(ch, codes.cpu()), "e2e codes differ from the device-resident run"
+
+    # ---- sweep over M x Ks (configs[1]) -- encode vec/s and RMSE per point
+    sweep = []
+    if not args.quick:
+        for M in (4, 8, 16, 32):
+            for ks in (16, 64, 256):
+                t, itr = fit(M, ks)
+                cds = torch.empty((N_ROWS, M), dtype=torch.uint8, device="cuda")
+                ms_pt = timed(lambda: encode(t, M, ks, cds), max(2, args.steps // 2), 1)
+                vps = N_ROWS * world / (ms_pt / 1e3)
+                fl = 2.0 * ks * DIMS
+                by = 4.0 * DIMS + M
+                bound_s = max(fl / (fp32_peak * 1e12), by / (peaks["hbm_gbs"] * 1e9))
+                sweep.append({"M": M, "Ks": ks, "encode_vectors_per_s": vps,
+                              "rmse": rmse_of(t, M, ks, cds), "fit_iters_run": itr,
+                              "roofline_vectors_per_s": 1.0 / bound_s,
+                              "frac": vps / world * bound_s})
+                del cds
+
+    # ---- configs[2]: ADC search queries/s
+    adc = None
+    if not args.quick:
+        adc = adc_bench(ctx, lib, L, x, train, args, world, stream, timed)
+
+    # ---- CPU baseline: the compiled reference on this host (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            import oracle
+            if oracle.ref_available():
+                R = oracle.ref_impl()
+                thr = max(1, R.hardware_concurrency())
+                rows = min(N_ROWS, 4000 * thr)
+                v_cpu, dt = reference_encode_rate(x_host, tables_h.numpy(), thr, rows)
+                reps = max(1, int(10.0 / max(dt, 1e-3)))
+                reps = min(reps, 20)
+                tot = 0.0
+                for _ in range(reps):
+                    _, d1 = reference_encode_rate(x_host, tables_h.numpy(), thr, rows)
+                    tot += d1
+                v_cpu = rows * reps / tot
+                cpu = {"value": v_cpu, "unit": "vectors/s", "cores": thr, "kind": "reference",
+                       "sample": f"{reps} x pq_encode of {rows} rows (M={HEAD_M}, Ks={HEAD_KS}) "
+                                 f"with chunk_rows over {thr} threads; reference compiled -O3"}
+        except Exception as e:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": "vectors/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank != 0:
+        return
+    out = {
+        "metric": METRIC, "value": value, "unit": "vectors/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded Gaussian mixture, BASELINE configs[1]/[2] shapes)",
+        "config": config_block(world),
+        "rmse": head_rmse,
+        "kmeans_iters_per_s": kmeans_ips,
+        "kmeans_fit": {"M": HEAD_M, "Ks": HEAD_KS, "sample_rows": SAMPLE, "iters_run": iters_run,
+                       "seconds": fit_s},
+        "adc": adc,
+        "sweep": sweep,
+        "roofline": {"bound": "fp32", "achieved": achieved_tflops, "peak": fp32_peak,
+                     "unit": "TFLOP/s", "frac": achieved_tflops / fp32_peak, "traffic": traffic,
+                     "kernel": "nearest_kernel<TN=8,DP=16> (encode screen)",
+                     "algorithmic": "2*Ks*D = 65536 flop per vector x 1M vectors per launch",
+                     "peak_source": f"148 SMs x 128 FP32 lanes x 2 x sm_max_mhz ({src} MEASURED_PEAKS.json clock)",
+                     "kernel_ms": near_avg_ms, "launches": n_near,
+                     "share_of_step": near_ms / max(ms * args.steps, 1e-9),
+                     "fixup_ms_per_step": fix_ms / max(args.steps, 1),
+                     "norms_ms_per_step": norm_ms / max(args.steps, 1)},
+        "cpu_baseline": cpu,
+        "e2e": {"value": N_ROWS * world / e2e_s, "unit": "vectors/s",
+                "h2d_bytes_per_step": N_ROWS * DIMS * 4 + HEAD_M * HEAD_KS * (DIMS // HEAD_M) * 4,
+                "d2h_bytes_per_step": N_ROWS * HEAD_M,
+                "path": "pqg_pq_encode with pinned host input/output (C ABI)"},
+        "gpu_launches": int(round(launches_per_step * args.steps)),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(out))
+
+
+def adc_bench(ctx, lib, L, x, train, args, world, stream, timed):
+    """configs[2]: M=16, Ks=256, nlist=1024 coarse centroids fitted on the 100k
+    sample, coarse-assign + CSR of all rows, 10k queries, nprobe 16, k 10."""
+    import torch
+    from paper_2604_21645_b200.datagen import gaussian_mixture
+    vp = C.c_void_p
+    M, ks, nlist, nq, nprobe, k = 16, 256, 1024, 10_000, 16, 10
+    tables = torch.empty((M, ks, DIMS // M), dtype=torch.float32, device="cuda")
+    L.check(lib.pqg_pq_fit(ctx.h, vp(train.data_ptr()), SAMPLE, DIMS, M, ks, 20, SEED,
+                           vp(tables.data_ptr()), None, None))
+    coarse = torch.empty((nlist, DIMS), dtype=torch.float32, device="cuda")
+    inertia = C.c_double()
+    it = C.c_uint32()
+    t0 = time.perf_counter()
+    L.check(lib.pqg_kmeans_fit(ctx.h, vp(train.data_ptr()), SAMPLE, DIMS, nlist, 20, SEED + M,
+                               1e-4, vp(coarse.data_ptr()), None, C.byref(inertia), C.byref(it),
+                               None))
+    torch.cuda.synchronize()
+    coarse_s = time.perf_counter() - t0
+    codes = torch.empty((N_ROWS, M), dtype=torch.uint8, device="cuda")
+    L.check(lib.pqg_pq_encode(ctx.h, vp(x.data_ptr()), N_ROWS, M, ks, DIMS // M,
+                              vp(tables.data_ptr()), vp(codes.data_ptr())))
+    ids = torch.arange(N_ROWS, dtype=torch.int64, device="cuda")
+    h = C.c_void_p()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    L.check(lib.pqg_ivf_build_with_centroids(ctx.h, vp(tables.data_ptr()), M, ks, DIMS // M,
+                                             vp(codes.data_ptr()), vp(ids.data_ptr()), N_ROWS,
+                                             vp(coarse.data_ptr()), nlist, C.byref(h)))
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    q = torch.from_numpy(gaussian_mixture(nq, DIMS, COMPONENTS, SEED, stream=1)).cuda()
+    oi = torch.empty((nq, k), dtype=torch.int64, device="cuda")
+    od = torch.empty((nq, k), dtype=torch.float64, device="cuda")
+    oc = torch.empty((nq,), dtype=torch.int32, device="cuda")
+
+    def search():
+        L.check(lib.pqg_index_search(ctx.h, h, vp(q.data_ptr()), nq, k, nprobe, 0, 0.0,
+                                     vp(oi.data_ptr()), vp(od.data_ptr()), vp(oc.data_ptr())))
+
+    ctx.profile(True)
+    ms = timed(search, max(3, args.steps // 2), 2)
+    n_scan, scan_ms = ctx.profile_read("adc_scan")
+    n_sel, sel_ms = ctx.profile_read("probe_select")
+    n_mat, mat_ms = ctx.profile_read("distance_matrix")
+    ctx.profile(False)
+    off = torch.empty(nlist + 1, dtype=torch.int64)
+    L.check(lib.pqg_index_export(ctx.h, h, vp(off.data_ptr()), None, None, None, None))
+    lib.pqg_index_destroy(h)
+    return {"queries_per_s": nq * world / (ms / 1e3), "ms_per_batch": ms, "nq": nq,
+            "nprobe": nprobe, "k": k, "nlist": nlist, "M": M, "Ks": ks,
+            "coarse_kmeans_seconds": coarse_s, "coarse_iters_run": it.value,
+            "ivf_build_seconds": build_s,
+            "scan_ms": scan_ms / max(n_scan, 1) * max(1, n_scan // max(1, (max(3, args.steps // 2)))),
+            "kernel_ms_per_batch": {"adc_scan": scan_ms / max(3, args.steps // 2),
+                                    "probe_select": sel_ms / max(3, args.steps // 2),
+                                    "distance_matrix": mat_ms / max(3, args.steps // 2)},
+            "max_list": int((off[1:] - off[:-1]).max())}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--quick", action="store_true", help="headline only (no sweep / ADC)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        run_reference(args, rank, world)
+        return
+    rank, world, local = dist_setup()
+    run_ours(args, rank, world, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
