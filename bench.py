@@ -233,7 +233,11 @@ def run_ours(args, rank, world, local):
 
     torch.cuda.set_device(local)
     ctx = pqii.Context(local)
-    stream = torch.cuda.current_stream()
+    # a dedicated stream shared by torch (events, copies) and libpqg (kernels);
+    # torch's legacy default stream has handle 0, which the C ABI reads as
+    # "use the context's own stream", so it cannot be used here
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     lib = ctx.lib
     vp = C.c_void_p
@@ -308,7 +312,10 @@ def run_ours(args, rank, world, local):
     flops_per_launch = float(N_ROWS) * 2 * HEAD_KS * DIMS
     achieved_tflops = flops_per_launch / (near_avg_ms / 1e3) / 1e12
     props = torch.cuda.get_device_properties(local)
-    fp32_peak = props.multi_processor_count * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+    fp32_nominal = props.multi_processor_count * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+    probe = C.c_double()
+    L.check(lib.pqg_fp32_probe(ctx.h, C.byref(probe)), "fp32_probe")
+    fp32_peak = float(probe.value)
     traffic = ncu_traffic("nearest_encode_M8_Ks256")
 
     # ---- e2e through the C ABI with pinned host buffers
@@ -394,7 +401,8 @@ def run_ours(args, rank, world, local):
                      "unit": "TFLOP/s", "frac": achieved_tflops / fp32_peak, "traffic": traffic,
                      "kernel": "nearest_kernel<TN=8,DP=16> (encode screen)",
                      "algorithmic": "2*Ks*D = 65536 flop per vector x 1M vectors per launch",
-                     "peak_source": f"148 SMs x 128 FP32 lanes x 2 x sm_max_mhz ({src} MEASURED_PEAKS.json clock)",
+                     "peak_source": "measured: register-operand FFMA probe (pqg_fp32_probe) on this GPU",
+                     "fp32_nominal_tflops": fp32_nominal,
                      "kernel_ms": near_avg_ms, "launches": n_near,
                      "share_of_step": near_ms / max(ms * args.steps, 1e-9),
                      "fixup_ms_per_step": fix_ms / max(args.steps, 1),

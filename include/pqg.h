@@ -57,6 +57,9 @@ int pqg_profile_enable(pqg_ctx* ctx, int enable);
 int pqg_profile_read(pqg_ctx* ctx, const char* kernel_class, uint64_t* launches,
                      double* total_ms);
 const char* pqg_version(void);
+/* Measured FP32 FFMA throughput of this GPU (TFLOP/s): the denominator of the
+ * fp32-bound kernels' roofline fraction. */
+int pqg_fp32_probe(pqg_ctx* ctx, double* tflops);
 
 /* ---- L1: nearest centroid / k-means (proj/src/kmeans.cpp) ---------------- */
 /* nearest_in_table (kmeans.cpp:20-31) for n points: index[i], sq_dist[i] are

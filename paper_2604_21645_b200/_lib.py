@@ -36,6 +36,7 @@ _SIGS = {
     "pqg_profile_enable": (_i32, [_vp, _i32]),
     "pqg_profile_read": (_i32, [_vp, C.c_char_p, C.POINTER(_u64), C.POINTER(_f64)]),
     "pqg_version": (C.c_char_p, []),
+    "pqg_fp32_probe": (_i32, [_vp, C.POINTER(_f64)]),
     "pqg_nearest_batch": (_i32, [_vp, _vp, _u64, _u64, _vp, _u64, _vp, _vp]),
     "pqg_kmeans_fit": (_i32, [_vp, _vp, _u64, _u64, _u64, _u32, _u64, _f64, _vp, _vp,
                               C.POINTER(_f64), C.POINTER(_u32), _vp]),
