@@ -1,0 +1,638 @@
+// pqii_facade.cpp -- the reference's C++ API (namespace pqii) implemented
+// over the C ABI of libpqg.so, so unchanged reference callers (pipeline,
+// bench, CLI, tests: /root/reference/proj/src/pipeline.cpp:84-266,
+// proj/tests/*) link against libpqg_pqii.so instead of libpqii.a.
+//
+// Every numeric result comes from the device (include/pqg.h); this file only
+// validates with the reference's messages, marshals the reference's structs
+// and maintains the host-side data structures the API returns by value
+// (posting-list vectors, id_set).  One pqg context per calling thread keeps
+// the API re-entrant as run_pipeline requires (SURVEY.md 8(b) Threading).
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <list>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+
+#include "pqg.h"
+#include "pqii/ivf.hpp"
+#include "pqii/kmeans.hpp"
+#include "pqii/matrix.hpp"
+#include "pqii/pq.hpp"
+
+namespace pqii {
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// context and error mapping
+// ---------------------------------------------------------------------------
+int device_index() {
+    const char* e = std::getenv("PQG_DEVICE");
+    return e ? std::atoi(e) : 0;
+}
+
+void raise(int rc) {
+    if (rc == PQG_OK) return;
+    const std::string msg = pqg_last_error();
+    if (rc == PQG_EINVAL) throw std::invalid_argument(msg);
+    if (rc == PQG_ERANGE) throw std::out_of_range(msg);
+    throw std::runtime_error(msg);
+}
+
+struct CtxHolder {
+    pqg_ctx* c = nullptr;
+    ~CtxHolder() {
+        if (c) pqg_ctx_destroy(c);
+    }
+};
+
+pqg_ctx* ctx() {
+    thread_local CtxHolder h;
+    if (!h.c) raise(pqg_ctx_create(device_index(), &h.c));
+    return h.c;
+}
+
+// ---------------------------------------------------------------------------
+// device-index cache for repeated queries on the same (unmodified) index
+// ---------------------------------------------------------------------------
+using IndexKey = std::tuple<const void*, std::size_t, std::size_t, const void*, const void*,
+                            const void*, const void*, std::size_t>;
+
+IndexKey key_of(const InvertedIndex& ix) {
+    const void* first = ix.lists.empty() ? nullptr : ix.lists.front().ids.data();
+    const void* last = ix.lists.empty() ? nullptr : ix.lists.back().ids.data();
+    return {ix.lists.data(), ix.lists.size(), ix.n_items, first, last, ix.codebook.tables.data(),
+            ix.coarse_centroids.values.data(), ix.id_set.size()};
+}
+
+struct IndexDeleter {
+    void operator()(pqg_index* p) const { pqg_index_destroy(p); }
+};
+using IndexPtr = std::shared_ptr<pqg_index>;
+
+std::mutex g_cache_mu;
+std::list<std::pair<IndexKey, IndexPtr>> g_cache;  // most recent first
+
+IndexPtr upload(const InvertedIndex& ix) {
+    const std::size_t nlist = ix.lists.size();
+    const std::size_t rb = ix.codebook.m_subspaces * (ix.codebook.ks <= 256 ? 1 : 2);
+    std::vector<std::uint64_t> offsets(nlist + 1, 0), ids;
+    std::vector<std::uint8_t> codes;
+    for (std::size_t l = 0; l < nlist; ++l) offsets[l + 1] = offsets[l] + ix.lists[l].ids.size();
+    ids.reserve(offsets[nlist]);
+    codes.reserve(offsets[nlist] * rb);
+    for (const auto& pl : ix.lists) {
+        ids.insert(ids.end(), pl.ids.begin(), pl.ids.end());
+        codes.insert(codes.end(), pl.codes.bytes.begin(), pl.codes.bytes.end());
+    }
+    pqg_index* h = nullptr;
+    raise(pqg_index_create(ctx(), ix.codebook.tables.data(), ix.codebook.m_subspaces,
+                           ix.codebook.ks, ix.codebook.sub_dim, ix.coarse_centroids.values.data(),
+                           nlist, offsets.data(), ids.data(), codes.data(), &h));
+    return IndexPtr(h, IndexDeleter());
+}
+
+IndexPtr device_index_for(const InvertedIndex& ix) {
+    const IndexKey k = key_of(ix);
+    {
+        std::lock_guard<std::mutex> g(g_cache_mu);
+        for (auto it = g_cache.begin(); it != g_cache.end(); ++it) {
+            if (it->first == k) {
+                g_cache.splice(g_cache.begin(), g_cache, it);
+                return g_cache.front().second;
+            }
+        }
+    }
+    IndexPtr p = upload(ix);
+    std::lock_guard<std::mutex> g(g_cache_mu);
+    g_cache.emplace_front(k, p);
+    while (g_cache.size() > 8) g_cache.pop_back();
+    return p;
+}
+
+// Build the reference's host structure from a device index (CSR export).
+InvertedIndex to_host(pqg_index* h, const Codebook& cb) {
+    std::uint64_t nlist = 0, n = 0;
+    std::uint32_t M = 0, ks = 0, ds = 0;
+    raise(pqg_index_info(h, &nlist, &n, &M, &ks, &ds));
+    const std::size_t rb = std::size_t(M) * (ks <= 256 ? 1 : 2);
+    std::vector<std::uint64_t> offsets(nlist + 1), ids(std::max<std::uint64_t>(n, 1));
+    std::vector<std::uint8_t> codes(std::max<std::uint64_t>(n, 1) * rb);
+    InvertedIndex ix;
+    ix.codebook = cb;
+    ix.coarse_centroids = VectorMatrix(nlist, std::size_t(M) * ds);
+    raise(pqg_index_export(ctx(), h, offsets.data(), ids.data(), codes.data(),
+                           ix.coarse_centroids.values.data(), nullptr));
+    ix.lists.resize(nlist);
+    for (std::size_t l = 0; l < nlist; ++l) {
+        PostingList& pl = ix.lists[l];
+        const std::size_t a = offsets[l], b = offsets[l + 1];
+        pl.ids.assign(ids.begin() + a, ids.begin() + b);
+        pl.codes = CodeMatrix(0, M, ks);
+        pl.codes.bytes.assign(codes.begin() + a * rb, codes.begin() + b * rb);
+        pl.codes.rows = b - a;
+    }
+    ix.n_items = n;
+    ix.id_set.reserve(n);
+    ix.id_set.insert(ids.begin(), ids.begin() + n);
+    return ix;
+}
+
+void check_codebook_params(std::uint32_t m, std::uint32_t ks, std::uint32_t sub_dim) {
+    if (m == 0) throw std::invalid_argument("codebook: M must be >= 1");
+    if (ks == 0 || ks > 65536) throw std::invalid_argument("codebook: Ks must be in [1, 65536]");
+    if (sub_dim == 0) throw std::invalid_argument("codebook: sub_dim must be >= 1");
+}
+
+void check_codes_match(const Codebook& cb, const CodeMatrix& codes, const char* who) {
+    if (codes.m_subspaces != cb.m_subspaces || codes.ks != cb.ks)
+        throw std::invalid_argument(std::string(who) + ": codes do not match the codebook");
+}
+
+void check_query(const InvertedIndex& index, std::span<const float> query, std::size_t k,
+                 std::size_t nprobe) {
+    if (k == 0) throw std::invalid_argument("query: k must be >= 1");
+    if (query.size() != index.codebook.dims()) throw std::invalid_argument("query: dimension mismatch");
+    if (nprobe == 0 || nprobe > index.nlist())
+        throw std::invalid_argument("query: nprobe (" + std::to_string(nprobe) +
+                                    ") must be in [1, nlist=" + std::to_string(index.nlist()) + "]");
+}
+
+QueryResult result_of(const std::uint64_t* ids, const double* d, std::uint32_t cnt, std::size_t k) {
+    QueryResult r;
+    r.k_requested = k;
+    r.hits.reserve(cnt);
+    for (std::uint32_t j = 0; j < cnt; ++j) r.hits.push_back({ids[j], d[j]});
+    return r;
+}
+
+// little-endian scalar IO for the on-disk formats (pq.hpp:90-97, ivf.hpp:88-92)
+template <class T>
+void put(std::ofstream& o, T v) {
+    o.write(reinterpret_cast<const char*>(&v), sizeof(T));
+}
+template <class T>
+T get(std::ifstream& in, const std::string& path, const char* what) {
+    T v{};
+    in.read(reinterpret_cast<char*>(&v), sizeof(T));
+    if (in.gcount() != std::streamsize(sizeof(T)))
+        throw std::runtime_error(path + ": truncated " + what);
+    return v;
+}
+void magic_in(std::ifstream& in, const char* m, const std::string& path, const char* what) {
+    char b[4];
+    in.read(b, 4);
+    if (in.gcount() != 4 || std::memcmp(b, m, 4) != 0)
+        throw std::runtime_error(path + ": bad magic for " + what);
+}
+
+}  // namespace
+
+// ===========================================================================
+// matrix.hpp
+// ===========================================================================
+VectorMatrix slice_rows(const VectorMatrix& m, RowRange r) {
+    if (r.begin >= r.end || r.end > m.rows) throw std::invalid_argument("slice_rows: range out of bounds");
+    VectorMatrix out(r.size(), m.dims);
+    std::memcpy(out.values.data(), m.row(r.begin), r.size() * m.dims * sizeof(float));
+    return out;
+}
+
+// ===========================================================================
+// kmeans.hpp
+// ===========================================================================
+NearestCentroid nearest_in_table(const float* point, const float* table, std::size_t k,
+                                 std::size_t d) {
+    if (d == 0) return {0, 0.0};
+    std::uint32_t idx = 0;
+    double dist = 0.0;
+    raise(pqg_nearest_batch(ctx(), point, 1, d, table, k, &idx, &dist));
+    return {idx, dist};
+}
+
+double squared_l2(const float* a, const float* b, std::size_t d) {
+    return nearest_in_table(a, b, 1, d).sq_dist;
+}
+
+NearestCentroid nearest_centroid(std::span<const float> point, const VectorMatrix& centroids) {
+    if (centroids.rows == 0) throw std::invalid_argument("nearest_centroid: empty centroid set");
+    if (point.size() != centroids.dims) throw std::invalid_argument("nearest_centroid: dimension mismatch");
+    return nearest_in_table(point.data(), centroids.values.data(), centroids.rows, centroids.dims);
+}
+
+KMeansResult kmeans_fit(const VectorMatrix& points, std::size_t k, std::uint32_t max_iters,
+                        std::uint64_t seed, double tol) {
+    KMeansResult r;
+    r.centroids = VectorMatrix(k <= points.rows ? k : 0, points.dims);
+    r.assignments.resize(points.rows);
+    r.inertia_per_iter.resize(std::max<std::uint32_t>(max_iters, 1));
+    raise(pqg_kmeans_fit(ctx(), points.values.data(), points.rows, points.dims, k, max_iters, seed,
+                         tol, r.centroids.values.data(), r.assignments.data(), &r.inertia,
+                         &r.iterations_run, r.inertia_per_iter.data()));
+    r.inertia_per_iter.resize(r.iterations_run);
+    return r;
+}
+
+// ===========================================================================
+// pq.hpp
+// ===========================================================================
+CodeMatrix::CodeMatrix(std::size_t n, std::uint32_t m, std::uint32_t ks_)
+    : rows(n), m_subspaces(m), ks(ks_) {
+    check_codebook_params(m, ks_, 1);
+    bytes.assign(n * row_bytes(), 0);
+}
+
+std::uint32_t CodeMatrix::at(std::size_t i, std::size_t m) const {
+    const std::size_t off = i * row_bytes() + m * code_width();
+    return code_width() == 1 ? bytes[off] : (std::uint32_t(bytes[off]) | std::uint32_t(bytes[off + 1]) << 8);
+}
+
+void CodeMatrix::set(std::size_t i, std::size_t m, std::uint32_t value) {
+    const std::size_t off = i * row_bytes() + m * code_width();
+    bytes[off] = std::uint8_t(value & 0xff);
+    if (code_width() == 2) bytes[off + 1] = std::uint8_t(value >> 8);
+}
+
+void CodeMatrix::append_row_from(const CodeMatrix& src, std::size_t src_row) {
+    if (src.m_subspaces != m_subspaces || src.ks != ks)
+        throw std::invalid_argument("CodeMatrix: shape mismatch on append");
+    const std::size_t rb = row_bytes();
+    const std::uint8_t* p = src.bytes.data() + src_row * rb;
+    bytes.insert(bytes.end(), p, p + rb);
+    ++rows;
+}
+
+Codebook pq_fit(const VectorMatrix& data, std::uint32_t m, std::uint32_t ks,
+                std::uint32_t max_iters, std::uint64_t seed) {
+    Codebook cb;
+    cb.m_subspaces = m;
+    cb.ks = ks;
+    cb.sub_dim = m ? std::uint32_t(data.dims / m) : 0;
+    cb.tables.resize(std::size_t(m) * ks * cb.sub_dim);
+    raise(pqg_pq_fit(ctx(), data.values.data(), data.rows, data.dims, m, ks, max_iters, seed,
+                     cb.tables.data(), nullptr, nullptr));
+    return cb;
+}
+
+CodeMatrix pq_encode(const Codebook& cb, const VectorMatrix& data) {
+    if (data.dims != cb.dims())
+        throw std::invalid_argument("pq_encode: data dimension " + std::to_string(data.dims) +
+                                    " does not match codebook dimension " + std::to_string(cb.dims()));
+    CodeMatrix codes(data.rows, cb.m_subspaces, cb.ks);
+    raise(pqg_pq_encode(ctx(), data.values.data(), data.rows, cb.m_subspaces, cb.ks, cb.sub_dim,
+                        cb.tables.data(), codes.bytes.data()));
+    return codes;
+}
+
+void pq_decode_row(const Codebook& cb, const CodeMatrix& codes, std::size_t i, float* out) {
+    raise(pqg_pq_decode(ctx(), codes.bytes.data() + i * codes.row_bytes(), 1, cb.m_subspaces, cb.ks,
+                        cb.sub_dim, cb.tables.data(), out));
+}
+
+VectorMatrix pq_decode(const Codebook& cb, const CodeMatrix& codes) {
+    check_codes_match(cb, codes, "pq_decode");
+    VectorMatrix out(codes.rows, cb.dims());
+    raise(pqg_pq_decode(ctx(), codes.bytes.data(), codes.rows, cb.m_subspaces, cb.ks, cb.sub_dim,
+                        cb.tables.data(), out.values.data()));
+    return out;
+}
+
+DistanceTable adc_table(const Codebook& cb, std::span<const float> query) {
+    if (query.size() != cb.dims())
+        throw std::invalid_argument("adc_table: query dimension " + std::to_string(query.size()) +
+                                    " does not match codebook dimension " + std::to_string(cb.dims()));
+    DistanceTable t;
+    t.m_subspaces = cb.m_subspaces;
+    t.ks = cb.ks;
+    t.entries.resize(std::size_t(cb.m_subspaces) * cb.ks);
+    raise(pqg_adc_tables(ctx(), cb.tables.data(), cb.m_subspaces, cb.ks, cb.sub_dim, query.data(), 1,
+                         t.entries.data()));
+    return t;
+}
+
+double adc_lookup(const DistanceTable& table, const CodeMatrix& codes, std::size_t row) {
+    if (codes.m_subspaces != table.m_subspaces || codes.ks != table.ks)
+        throw std::invalid_argument("adc_lookup: codes do not match the table");
+    double out = 0.0;
+    raise(pqg_adc_lookup(ctx(), table.entries.data(), table.m_subspaces, table.ks,
+                         codes.bytes.data() + row * codes.row_bytes(), 1, &out));
+    return out;
+}
+
+double rmse(const VectorMatrix& a, const VectorMatrix& b) {
+    if (!a.same_shape(b)) throw std::invalid_argument("rmse: shape mismatch");
+    double sse = 0.0;
+    raise(pqg_sq_error(ctx(), a.values.data(), b.values.data(), a.values.size(), &sse));
+    return std::sqrt(sse / double(a.rows * a.dims));
+}
+
+double reconstruction_rmse(const Codebook& cb, const VectorMatrix& data) {
+    if (data.dims != cb.dims())
+        throw std::invalid_argument("pq_encode: data dimension " + std::to_string(data.dims) +
+                                    " does not match codebook dimension " + std::to_string(cb.dims()));
+    double sse = 0.0;
+    raise(pqg_pq_encode_sse(ctx(), data.values.data(), data.rows, cb.m_subspaces, cb.ks, cb.sub_dim,
+                            cb.tables.data(), nullptr, &sse));
+    return std::sqrt(sse / double(data.rows * data.dims));
+}
+
+void save_codebook(const Codebook& cb, const std::string& path) {
+    std::ofstream o(path, std::ios::binary | std::ios::trunc);
+    if (!o) throw std::runtime_error("cannot open file for writing: " + path);
+    o.write("PQCB", 4);
+    put<std::uint32_t>(o, 1);
+    put(o, cb.m_subspaces);
+    put(o, cb.ks);
+    put(o, cb.sub_dim);
+    o.write(reinterpret_cast<const char*>(cb.tables.data()), std::streamsize(cb.tables.size() * 4));
+    if (!o) throw std::runtime_error("write failed: " + path);
+}
+
+Codebook load_codebook(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw std::runtime_error("cannot open file: " + path);
+    magic_in(in, "PQCB", path, "codebook file");
+    const auto ver = get<std::uint32_t>(in, path, "version");
+    if (ver != 1) throw std::runtime_error(path + ": unsupported version " + std::to_string(ver));
+    Codebook cb;
+    cb.m_subspaces = get<std::uint32_t>(in, path, "M");
+    cb.ks = get<std::uint32_t>(in, path, "Ks");
+    cb.sub_dim = get<std::uint32_t>(in, path, "sub_dim");
+    check_codebook_params(cb.m_subspaces, cb.ks, cb.sub_dim);
+    cb.tables.resize(std::size_t(cb.m_subspaces) * cb.ks * cb.sub_dim);
+    in.read(reinterpret_cast<char*>(cb.tables.data()), std::streamsize(cb.tables.size() * 4));
+    if (std::size_t(in.gcount()) != cb.tables.size() * 4) throw std::runtime_error(path + ": truncated payload");
+    for (float v : cb.tables)
+        if (!std::isfinite(v)) throw std::runtime_error(path + ": non-finite codeword value");
+    return cb;
+}
+
+void save_codes(const CodeMatrix& codes, const std::string& path) {
+    std::ofstream o(path, std::ios::binary | std::ios::trunc);
+    if (!o) throw std::runtime_error("cannot open file for writing: " + path);
+    o.write("PQCM", 4);
+    put<std::uint32_t>(o, 1);
+    put<std::uint64_t>(o, codes.rows);
+    put(o, codes.m_subspaces);
+    put(o, codes.ks);
+    o.write(reinterpret_cast<const char*>(codes.bytes.data()), std::streamsize(codes.bytes.size()));
+    if (!o) throw std::runtime_error("write failed: " + path);
+}
+
+CodeMatrix load_codes(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw std::runtime_error("cannot open file: " + path);
+    magic_in(in, "PQCM", path, "code file");
+    const auto ver = get<std::uint32_t>(in, path, "version");
+    if (ver != 1) throw std::runtime_error(path + ": unsupported version " + std::to_string(ver));
+    const auto n = get<std::uint64_t>(in, path, "row count");
+    const auto m = get<std::uint32_t>(in, path, "M");
+    const auto ks = get<std::uint32_t>(in, path, "Ks");
+    CodeMatrix codes(std::size_t(n), m, ks);
+    in.read(reinterpret_cast<char*>(codes.bytes.data()), std::streamsize(codes.bytes.size()));
+    if (std::size_t(in.gcount()) != codes.bytes.size()) throw std::runtime_error(path + ": truncated payload");
+    for (std::size_t i = 0; i < codes.rows; ++i)
+        for (std::uint32_t s = 0; s < m; ++s)
+            if (codes.at(i, s) >= ks)
+                throw std::runtime_error(path + ": code out of range at row " + std::to_string(i));
+    return codes;
+}
+
+// ===========================================================================
+// ivf.hpp
+// ===========================================================================
+std::size_t default_nlist(std::size_t n_items) {
+    const auto r = static_cast<std::size_t>(std::llround(std::sqrt(double(n_items))));
+    return std::clamp<std::size_t>(r, 1, n_items == 0 ? 1 : n_items);
+}
+
+InvertedIndex ivf_build(const Codebook& cb, const CodeMatrix& codes,
+                        std::span<const std::uint64_t> ids, std::size_t nlist, std::uint64_t seed,
+                        std::uint32_t kmeans_iters) {
+    if (ids.empty()) throw std::invalid_argument("ivf_build: no items");
+    if (ids.size() != codes.rows) throw std::invalid_argument("ivf_build: ids/codes length mismatch");
+    check_codes_match(cb, codes, "pq_decode");
+    pqg_index* h = nullptr;
+    raise(pqg_ivf_build(ctx(), cb.tables.data(), cb.m_subspaces, cb.ks, cb.sub_dim,
+                        codes.bytes.data(), ids.data(), codes.rows, nlist, seed, kmeans_iters, &h));
+    IndexPtr p(h, IndexDeleter());
+    return to_host(h, cb);
+}
+
+InvertedIndex ivf_build_with_centroids(const Codebook& cb, const CodeMatrix& codes,
+                                       std::span<const std::uint64_t> ids,
+                                       const VectorMatrix& coarse_centroids) {
+    if (ids.empty()) throw std::invalid_argument("ivf_build: no items");
+    if (ids.size() != codes.rows) throw std::invalid_argument("ivf_build: ids/codes length mismatch");
+    if (coarse_centroids.rows == 0 || coarse_centroids.dims != cb.dims())
+        throw std::invalid_argument("ivf_build: coarse centroids do not match the codebook");
+    pqg_index* h = nullptr;
+    raise(pqg_ivf_build_with_centroids(ctx(), cb.tables.data(), cb.m_subspaces, cb.ks, cb.sub_dim,
+                                       codes.bytes.data(), ids.data(), codes.rows,
+                                       coarse_centroids.values.data(), coarse_centroids.rows, &h));
+    IndexPtr p(h, IndexDeleter());
+    return to_host(h, cb);
+}
+
+void ivf_add(InvertedIndex& index, const CodeMatrix& codes, std::span<const std::uint64_t> ids) {
+    if (ids.size() != codes.rows) throw std::invalid_argument("ivf_add: ids/codes length mismatch");
+    if (codes.m_subspaces != index.codebook.m_subspaces || codes.ks != index.codebook.ks)
+        throw std::invalid_argument("ivf_add: codes do not match the index codebook");
+    if (ids.empty()) return;
+    std::unordered_set<std::uint64_t> fresh;
+    fresh.reserve(ids.size());
+    for (const std::uint64_t id : ids)
+        if (!fresh.insert(id).second) throw std::invalid_argument("duplicate id " + std::to_string(id));
+    for (const std::uint64_t id : ids)
+        if (index.id_set.contains(id))
+            throw std::invalid_argument("ivf_add: id collision on id " + std::to_string(id));
+    std::vector<std::uint32_t> list_of(codes.rows);
+    const Codebook& cb = index.codebook;
+    raise(pqg_ivf_assign(ctx(), codes.bytes.data(), codes.rows, cb.m_subspaces, cb.ks, cb.sub_dim,
+                         cb.tables.data(), index.coarse_centroids.values.data(), index.nlist(),
+                         list_of.data()));
+    for (std::size_t i = 0; i < codes.rows; ++i) {  // append in input order (ivf.cpp:44-46)
+        PostingList& pl = index.lists[list_of[i]];
+        pl.ids.push_back(ids[i]);
+        pl.codes.append_row_from(codes, i);
+    }
+    index.n_items += codes.rows;
+    index.id_set.merge(fresh);
+}
+
+InvertedIndex ivf_merge(const InvertedIndex& a, const InvertedIndex& b) {
+    if (!(a.codebook == b.codebook)) throw std::invalid_argument("ivf_merge: codebook mismatch");
+    if (!(a.coarse_centroids == b.coarse_centroids))
+        throw std::invalid_argument("ivf_merge: coarse centroid mismatch");
+    const auto& small = a.id_set.size() <= b.id_set.size() ? a.id_set : b.id_set;
+    const auto& large = a.id_set.size() <= b.id_set.size() ? b.id_set : a.id_set;
+    for (const std::uint64_t id : small)
+        if (large.contains(id)) throw std::invalid_argument("ivf_merge: id collision on id " + std::to_string(id));
+    InvertedIndex out;
+    out.codebook = a.codebook;
+    out.coarse_centroids = a.coarse_centroids;
+    out.lists.resize(a.lists.size());
+    for (std::size_t l = 0; l < a.lists.size(); ++l) {  // list l = a's then b's
+        PostingList& d = out.lists[l];
+        d.ids = a.lists[l].ids;
+        d.ids.insert(d.ids.end(), b.lists[l].ids.begin(), b.lists[l].ids.end());
+        d.codes = a.lists[l].codes;
+        d.codes.bytes.insert(d.codes.bytes.end(), b.lists[l].codes.bytes.begin(), b.lists[l].codes.bytes.end());
+        d.codes.rows += b.lists[l].codes.rows;
+    }
+    out.n_items = a.n_items + b.n_items;
+    out.id_set = a.id_set;
+    out.id_set.insert(b.id_set.begin(), b.id_set.end());
+    return out;
+}
+
+std::vector<QueryResult> ivf_query_batch(const InvertedIndex& index, const VectorMatrix& queries,
+                                         std::size_t k, std::size_t nprobe,
+                                         std::optional<double> max_sq_dist) {
+    const std::size_t nq = queries.rows;
+    if (nq == 0) return {};
+    check_query(index, queries.row_span(0), k, nprobe);
+    IndexPtr dev = device_index_for(index);
+    std::vector<std::uint64_t> ids(nq * k);
+    std::vector<double> d(nq * k);
+    std::vector<std::uint32_t> cnt(nq);
+    raise(pqg_index_search(ctx(), dev.get(), queries.values.data(), nq, k, nprobe,
+                           max_sq_dist.has_value(), max_sq_dist.value_or(0.0), ids.data(), d.data(),
+                           cnt.data()));
+    std::vector<QueryResult> out;
+    out.reserve(nq);
+    for (std::size_t q = 0; q < nq; ++q) out.push_back(result_of(&ids[q * k], &d[q * k], cnt[q], k));
+    return out;
+}
+
+QueryResult ivf_query(const InvertedIndex& index, std::span<const float> query, std::size_t k,
+                      std::size_t nprobe, std::optional<double> max_sq_dist) {
+    check_query(index, query, k, nprobe);
+    VectorMatrix q(1, query.size());
+    std::memcpy(q.values.data(), query.data(), query.size() * sizeof(float));
+    return ivf_query_batch(index, q, k, nprobe, max_sq_dist)[0];
+}
+
+QueryResult ivf_query_subset(const InvertedIndex& index, std::span<const float> query,
+                             std::size_t k, std::span<const std::uint64_t> subset,
+                             std::size_t nprobe, std::optional<double> max_sq_dist) {
+    check_query(index, query, k, nprobe);
+    for (std::size_t i = 1; i < subset.size(); ++i)
+        if (subset[i - 1] >= subset[i])
+            throw std::invalid_argument("ivf_query_subset: subset is not sorted ascending");
+    IndexPtr dev = device_index_for(index);
+    std::vector<std::uint32_t> probes(nprobe);
+    raise(pqg_index_probe(ctx(), dev.get(), query.data(), 1, nprobe, probes.data()));
+    // candidates of the probed lists that are members of the subset
+    CodeMatrix cand(0, index.codebook.m_subspaces, index.codebook.ks);
+    std::vector<std::uint64_t> cand_ids;
+    for (const std::uint32_t l : probes) {
+        const PostingList& pl = index.lists[l];
+        for (std::size_t i = 0; i < pl.ids.size(); ++i) {
+            if (!std::binary_search(subset.begin(), subset.end(), pl.ids[i])) continue;
+            cand_ids.push_back(pl.ids[i]);
+            cand.append_row_from(pl.codes, i);
+        }
+    }
+    return flat_scan(index.codebook, cand, cand_ids, query, k, max_sq_dist);
+}
+
+QueryResult flat_scan(const Codebook& cb, const CodeMatrix& codes,
+                      std::span<const std::uint64_t> ids, std::span<const float> query,
+                      std::size_t k, std::optional<double> max_sq_dist) {
+    if (k == 0) throw std::invalid_argument("flat_scan: k must be >= 1");
+    if (ids.size() != codes.rows) throw std::invalid_argument("flat_scan: ids/codes length mismatch");
+    if (query.size() != cb.dims()) throw std::invalid_argument("flat_scan: dimension mismatch");
+    std::vector<std::uint64_t> oi(k);
+    std::vector<double> od(k);
+    std::uint32_t cnt = 0;
+    if (codes.rows == 0) return result_of(oi.data(), od.data(), 0, k);
+    raise(pqg_flat_scan(ctx(), cb.tables.data(), cb.m_subspaces, cb.ks, cb.sub_dim,
+                        codes.bytes.data(), ids.data(), codes.rows, query.data(), 1, k,
+                        max_sq_dist.has_value(), max_sq_dist.value_or(0.0), oi.data(), od.data(), &cnt));
+    return result_of(oi.data(), od.data(), cnt, k);
+}
+
+void save_index(const InvertedIndex& index, const std::string& path) {
+    std::ofstream o(path, std::ios::binary | std::ios::trunc);
+    if (!o) throw std::runtime_error("cannot open file for writing: " + path);
+    o.write("PQII", 4);
+    put<std::uint32_t>(o, 1);
+    o.write("PQCB", 4);
+    put<std::uint32_t>(o, 1);
+    put(o, index.codebook.m_subspaces);
+    put(o, index.codebook.ks);
+    put(o, index.codebook.sub_dim);
+    o.write(reinterpret_cast<const char*>(index.codebook.tables.data()),
+            std::streamsize(index.codebook.tables.size() * 4));
+    put<std::uint32_t>(o, std::uint32_t(index.nlist()));
+    o.write(reinterpret_cast<const char*>(index.coarse_centroids.values.data()),
+            std::streamsize(index.coarse_centroids.values.size() * 4));
+    for (const auto& pl : index.lists) {
+        put<std::uint64_t>(o, pl.ids.size());
+        const std::size_t rb = pl.codes.row_bytes();
+        for (std::size_t i = 0; i < pl.ids.size(); ++i) {
+            put<std::uint64_t>(o, pl.ids[i]);
+            o.write(reinterpret_cast<const char*>(pl.codes.bytes.data() + i * rb), std::streamsize(rb));
+        }
+    }
+    if (!o) throw std::runtime_error("write failed: " + path);
+}
+
+InvertedIndex load_index(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw std::runtime_error("cannot open file: " + path);
+    magic_in(in, "PQII", path, "index file");
+    if (get<std::uint32_t>(in, path, "version") != 1) throw std::runtime_error(path + ": unsupported version");
+    magic_in(in, "PQCB", path, "embedded codebook");
+    if (get<std::uint32_t>(in, path, "codebook version") != 1)
+        throw std::runtime_error(path + ": unsupported codebook version");
+    InvertedIndex ix;
+    ix.codebook.m_subspaces = get<std::uint32_t>(in, path, "M");
+    ix.codebook.ks = get<std::uint32_t>(in, path, "Ks");
+    ix.codebook.sub_dim = get<std::uint32_t>(in, path, "sub_dim");
+    if (!ix.codebook.m_subspaces || !ix.codebook.ks || !ix.codebook.sub_dim)
+        throw std::runtime_error(path + ": invalid codebook header");
+    ix.codebook.tables.resize(std::size_t(ix.codebook.m_subspaces) * ix.codebook.ks * ix.codebook.sub_dim);
+    in.read(reinterpret_cast<char*>(ix.codebook.tables.data()), std::streamsize(ix.codebook.tables.size() * 4));
+    if (std::size_t(in.gcount()) != ix.codebook.tables.size() * 4) throw std::runtime_error(path + ": truncated codebook tables");
+    const auto nlist = get<std::uint32_t>(in, path, "nlist");
+    if (nlist == 0) throw std::runtime_error(path + ": nlist must be >= 1");
+    ix.coarse_centroids = VectorMatrix(nlist, ix.codebook.dims());
+    in.read(reinterpret_cast<char*>(ix.coarse_centroids.values.data()),
+            std::streamsize(ix.coarse_centroids.values.size() * 4));
+    if (std::size_t(in.gcount()) != ix.coarse_centroids.values.size() * 4)
+        throw std::runtime_error(path + ": truncated coarse centroids");
+    ix.lists.resize(nlist);
+    for (auto& pl : ix.lists) {
+        pl.codes = CodeMatrix(0, ix.codebook.m_subspaces, ix.codebook.ks);
+        const auto len = get<std::uint64_t>(in, path, "list length");
+        const std::size_t rb = pl.codes.row_bytes();
+        pl.ids.resize(len);
+        pl.codes.bytes.resize(len * rb);
+        pl.codes.rows = len;
+        for (std::size_t i = 0; i < len; ++i) {
+            pl.ids[i] = get<std::uint64_t>(in, path, "entry id");
+            in.read(reinterpret_cast<char*>(pl.codes.bytes.data() + i * rb), std::streamsize(rb));
+            if (std::size_t(in.gcount()) != rb) throw std::runtime_error(path + ": truncated entry code");
+            if (!ix.id_set.insert(pl.ids[i]).second)
+                throw std::runtime_error(path + ": duplicate id " + std::to_string(pl.ids[i]));
+        }
+        for (std::size_t i = 0; i < len; ++i)
+            for (std::uint32_t m = 0; m < ix.codebook.m_subspaces; ++m)
+                if (pl.codes.at(i, m) >= ix.codebook.ks) throw std::runtime_error(path + ": code out of range");
+        ix.n_items += len;
+    }
+    char extra;
+    if (in.read(&extra, 1); in.gcount() != 0) throw std::runtime_error(path + ": trailing data after payload");
+    return ix;
+}
+
+}  // namespace pqii
