@@ -172,7 +172,12 @@ int pqg_assign_pass(pqg_ctx* ctx, const float* rows, uint64_t n, uint64_t ld, ui
  * pre-update dists.  tables updated in place; dist modified (reseed zeroes). */
 int pqg_update_pass(pqg_ctx* ctx, const float* rows, uint64_t n, uint64_t ld, uint32_t B,
                     uint32_t d, uint32_t col_stride, float* tables, uint64_t k,
-                    const uint32_t* assign, double* dist);
+                    const uint32_t* assign, double* dist, const int* active);
+/* Per-problem inertia of B x n fp64 distances with the same fixed-shape tree
+ * the single-process fit uses (so sharded and single fits stop identically). */
+int pqg_rows_sum_f64(pqg_ctx* ctx, const double* v, uint64_t n, uint32_t B, double* out);
+/* The k init rows kmeans_fit draws (proj/src/kmeans.cpp:73-85), host-side. */
+int pqg_kmeans_init_rows(uint64_t n, uint64_t k, uint64_t seed, uint64_t* rows);
 
 #ifdef __cplusplus
 }

@@ -67,7 +67,9 @@ _SIGS = {
                              _f64, _vp, _vp, _vp]),
     "pqg_topk_merge": (_i32, [_vp, _vp, _vp, _vp, _u32, _u64, _u64, _vp, _vp, _vp]),
     "pqg_assign_pass": (_i32, [_vp, _vp, _u64, _u64, _u32, _u32, _u32, _vp, _u64, _vp, _vp]),
-    "pqg_update_pass": (_i32, [_vp, _vp, _u64, _u64, _u32, _u32, _u32, _vp, _u64, _vp, _vp]),
+    "pqg_update_pass": (_i32, [_vp, _vp, _u64, _u64, _u32, _u32, _u32, _vp, _u64, _vp, _vp, _vp]),
+    "pqg_rows_sum_f64": (_i32, [_vp, _vp, _u64, _u32, _vp]),
+    "pqg_kmeans_init_rows": (_i32, [_u64, _u64, _u64, _vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -1144,7 +1144,7 @@ int pqg_assign_pass(pqg_ctx* ctx, const float* rows, uint64_t n, uint64_t ld, ui
 
 int pqg_update_pass(pqg_ctx* ctx, const float* rows, uint64_t n, uint64_t ld, uint32_t B,
                     uint32_t d, uint32_t col_stride, float* tables, uint64_t k,
-                    const uint32_t* assign, double* dist) {
+                    const uint32_t* assign, double* dist, const int* active) {
     return guard([&] {
         Scope sc(ctx);
         if (n == 0) return;
@@ -1160,10 +1160,34 @@ int pqg_update_pass(pqg_ctx* ctx, const float* rows, uint64_t n, uint64_t ld, ui
         src.x = dr;
         src.ldx = ld;
         src.col_stride = col_stride;
-        kmeans_update(ctx, src, n, B, d, ot.dev, k, da, odist.dev, nullptr);
+        const int* dact = in(ctx, active, B);
+        kmeans_update(ctx, src, n, B, d, ot.dev, k, da, odist.dev, dact);
         finish(ctx, ot);
         finish(ctx, odist);
         if (ot.host || odist.host) sync(ctx);
+    });
+}
+
+int pqg_rows_sum_f64(pqg_ctx* ctx, const double* v, uint64_t n, uint32_t B, double* outp) {
+    return guard([&] {
+        Scope sc(ctx);
+        if (n == 0 || B == 0) {
+            for (uint32_t b = 0; b < B; ++b) outp[b] = 0.0;
+            return;
+        }
+        const double* dv = in(ctx, v, uint64_t(B) * n);
+        auto oo = out(ctx, outp, B);
+        rows_sum_f64(ctx, dv, n, B, oo.dev);
+        finish(ctx, oo);
+        sync(ctx);
+    });
+}
+
+int pqg_kmeans_init_rows(uint64_t n, uint64_t k, uint64_t seed, uint64_t* rows) {
+    return guard([&] {
+        if (k == 0 || k > n) inval("kmeans_fit: k (" + std::to_string(k) + ") exceeds number of points (" + std::to_string(n) + ")");
+        const auto r = init_rows(n, k, seed);
+        std::copy(r.begin(), r.end(), rows);
     });
 }
 

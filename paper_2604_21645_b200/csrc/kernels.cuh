@@ -69,6 +69,7 @@ struct KMeansState {
     double* per_iter;     // [B][max_iters]
     uint32_t* iters;      // [B]
 };
+void rows_sum_f64(pqg_ctx* ctx, const double* v, uint64_t n, uint32_t B, double* out);
 void kmeans_inertia_and_stop(pqg_ctx* ctx, const double* dist, uint64_t n, uint32_t B,
                              uint32_t it, uint32_t max_iters, double tol, KMeansState st);
 void kmeans_update(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint32_t d,

@@ -235,6 +235,15 @@ __global__ void stop_kernel(const double* parts, uint32_t nparts, uint32_t it, u
     st.prev[b] = s;
 }
 
+__global__ void final_parts_kernel(const double* parts, uint32_t nparts, double* out) {
+    const uint32_t b = blockIdx.x;
+    double s = 0.0;
+    for (uint32_t i = threadIdx.x; i < nparts; i += kRedThreads)
+        s = __dadd_rn(s, parts[uint64_t(b) * nparts + i]);
+    s = block_sum(s);
+    if (threadIdx.x == 0) out[b] = s;
+}
+
 // ---- ordered fp64 sums -> means -----------------------------------------
 __global__ void mean_kernel(const float* x, uint64_t ldx, uint32_t col_stride, uint64_t n,
                             uint32_t B, uint32_t d, uint64_t k, const uint64_t* offsets,
@@ -362,17 +371,34 @@ void gather_rows(pqg_ctx* ctx, const float* x, uint64_t ldx, uint32_t B, uint32_
            x, ldx, B, d, col_stride, rows, k, table);
 }
 
-void kmeans_inertia_and_stop(pqg_ctx* ctx, const double* dist, uint64_t n, uint32_t B,
-                             uint32_t it, uint32_t max_iters, double tol, KMeansState st) {
-    uint64_t nparts = std::min<uint64_t>(512, std::max<uint64_t>(1, (n + 8191) / 8192));
-    const uint64_t chunk = (n + nparts - 1) / nparts;
+// The fixed reduction shape (chunking of n) shared by the in-loop inertia and
+// pqg_rows_sum_f64, so sharded and single-process fits see identical sums.
+static void inertia_parts(uint64_t n, uint64_t& nparts, uint64_t& chunk) {
+    nparts = std::min<uint64_t>(512, std::max<uint64_t>(1, (n + 8191) / 8192));
+    chunk = (n + nparts - 1) / nparts;
     nparts = (n + chunk - 1) / chunk;
     if (nparts == 0) nparts = 1;
+}
+
+void kmeans_inertia_and_stop(pqg_ctx* ctx, const double* dist, uint64_t n, uint32_t B,
+                             uint32_t it, uint32_t max_iters, double tol, KMeansState st) {
+    uint64_t nparts, chunk;
+    inertia_parts(n, nparts, chunk);
     double* parts = scratch<double>(ctx, uint64_t(B) * nparts);
     launch(ctx, "inertia", partial_sum_kernel, dim3(unsigned(nparts), B), dim3(kRedThreads), 0,
            dist, n, chunk, parts, (const int*)st.active);
     launch(ctx, "inertia", stop_kernel, dim3(B), dim3(kRedThreads), 0, (const double*)parts,
            uint32_t(nparts), it, max_iters, tol, st);
+}
+
+void rows_sum_f64(pqg_ctx* ctx, const double* v, uint64_t n, uint32_t B, double* out) {
+    uint64_t nparts, chunk;
+    inertia_parts(n, nparts, chunk);
+    double* parts = scratch<double>(ctx, uint64_t(B) * nparts);
+    launch(ctx, "inertia", partial_sum_kernel, dim3(unsigned(nparts), B), dim3(kRedThreads), 0,
+           v, n, chunk, parts, (const int*)nullptr);
+    launch(ctx, "inertia", final_parts_kernel, dim3(B), dim3(kRedThreads), 0, (const double*)parts,
+           uint32_t(nparts), out);
 }
 
 void kmeans_update(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint32_t d,

@@ -1,0 +1,41 @@
+"""Rank bodies for tests/test_dist_gloo.py (importable by spawned workers)."""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+for p in (ROOT, os.path.join(ROOT, "tests")):
+    if p not in sys.path:
+        sys.path.insert(0, p)
+
+
+def run_rank(rank, world, port, outdir):
+    import torch.distributed as dist
+
+    from cpu_backend import OracleBackend
+    from paper_2604_21645_b200 import dist as D
+    from paper_2604_21645_b200.datagen import gaussian_mixture
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comm = D.Comm()
+    be = OracleBackend()
+    x = gaussian_mixture(1203, 16, 12, seed=9)  # odd size: uneven shards
+    lo, hi = D.chunk_rows(x.shape[0], world)[rank]
+    local = x[lo:hi]
+    res = {}
+    fit = D.kmeans_fit_sharded(comm, be, local, 1, 16, 0, 24, 12, [5], 1e-4)
+    res["km_tables"], res["km_assign"], res["km_iters"] = fit.tables, fit.assignments, fit.iterations_run
+    res["pq_tables"] = D.pq_fit_sharded(comm, be, local, 4, 16, 10, 3)
+    codes, rmse = D.encode_sharded(comm, be, local, res["pq_tables"])
+    res["codes"], res["rmse"] = codes, np.array([rmse])
+    coarse = x[::100][:12].copy()
+    ids = np.arange(lo, hi, dtype=np.uint64) * 3 + 1
+    q = gaussian_mixture(9, 16, 12, seed=9, stream=1)
+    oi, od, oc = D.search_sharded(comm, be, res["pq_tables"], codes, ids, coarse, q, 7, 4)
+    res["s_ids"], res["s_d"], res["s_c"] = oi, od, oc
+    np.savez(os.path.join(outdir, f"rank{rank}.npz"), **res)
+    dist.barrier()
+    dist.destroy_process_group()
