@@ -18,7 +18,7 @@ namespace pqg {
 
 namespace {
 
-constexpr int kTile = 4096;  // rows per bucketing tile
+constexpr int kTile = 2048;  // rows per bucketing tile (one warp walks a tile)
 
 __global__ void hist_kernel(const uint32_t* keys, uint64_t n, uint64_t k, uint32_t ntiles,
                             uint32_t* tile_counts) {
@@ -64,18 +64,28 @@ __global__ void scatter_kernel(const uint32_t* keys, uint64_t n, uint64_t k, uin
     const uint64_t r1 = min64(n, r0 + kTile);
     const uint32_t* kb = keys + base_b;
     uint32_t* pb = perm + base_b;
-    for (uint64_t rr = r0; rr < r1; rr += 32) {
-        const uint64_t i = rr + lane;
-        const bool valid = i < r1;
-        const uint32_t c = valid ? kb[i] : 0xFFFFFFFFu;
-        const uint32_t peers = __match_any_sync(0xffffffffu, c);
-        const uint32_t rank = __popc(peers & lanemask_lt());
-        uint32_t pos = 0;
-        if (valid) pos = running[c] + rank;
-        __syncwarp();
-        if (valid && rank == 0) running[c] += __popc(peers);
-        __syncwarp();
-        if (valid) pb[pos] = uint32_t(i);
+    // keys of the tile prefetched 32 rounds at a time (one register per round)
+    for (uint64_t c0 = r0; c0 < r1; c0 += 32 * 32) {
+        uint32_t key[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+            const uint64_t i = c0 + uint64_t(q) * 32 + lane;
+            key[q] = i < r1 ? __ldg(kb + i) : 0xFFFFFFFFu;
+        }
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+            const uint64_t i = c0 + uint64_t(q) * 32 + lane;
+            const bool valid = i < r1;
+            const uint32_t c = key[q];
+            const uint32_t peers = __match_any_sync(0xffffffffu, c);
+            const uint32_t rank = __popc(peers & lanemask_lt());
+            uint32_t pos = 0;
+            if (valid) pos = running[c] + rank;
+            __syncwarp();
+            if (valid && rank == 0) running[c] += __popc(peers);
+            __syncwarp();
+            if (valid) pb[pos] = uint32_t(i);
+        }
     }
 }
 
@@ -263,19 +273,21 @@ __global__ void mean_kernel(const float* x, uint64_t ldx, uint32_t col_stride, u
         }
         const uint32_t* mem = perm + b * n;
         const float* xc = x + b * col_stride + t;
+        // members in ascending row order; 16 independent gathers in flight,
+        // then the adds in the reference's order
         double s = 0.0;
-        uint64_t m = beg;
-        for (; m + 4 <= end; m += 4) {
-            const float v0 = __ldg(xc + uint64_t(mem[m]) * ldx);
-            const float v1 = __ldg(xc + uint64_t(mem[m + 1]) * ldx);
-            const float v2 = __ldg(xc + uint64_t(mem[m + 2]) * ldx);
-            const float v3 = __ldg(xc + uint64_t(mem[m + 3]) * ldx);
-            s = __dadd_rn(s, (double)v0);
-            s = __dadd_rn(s, (double)v1);
-            s = __dadd_rn(s, (double)v2);
-            s = __dadd_rn(s, (double)v3);
+        for (uint64_t m = beg; m < end; m += 16) {
+            const uint64_t cnt = min64(16, end - m);
+            uint32_t idx[16];
+            float v[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) idx[j] = j < int(cnt) ? __ldg(mem + m + j) : 0u;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = j < int(cnt) ? __ldg(xc + uint64_t(idx[j]) * ldx) : 0.f;
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (j < int(cnt)) s = __dadd_rn(s, (double)v[j]);
         }
-        for (; m < end; ++m) s = __dadd_rn(s, (double)__ldg(xc + uint64_t(mem[m]) * ldx));
         const double inv = __ddiv_rn(1.0, (double)(end - beg));
         table[e] = __double2float_rn(__dmul_rn(s, inv));
     }

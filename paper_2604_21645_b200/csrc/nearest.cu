@@ -109,15 +109,17 @@ __global__ void __launch_bounds__(NT, 2) nearest_kernel(NearestArgs a) {
     constexpr int LDC = BN + 4;
     constexpr int KCH = DP > 0 ? DP : BK;
     extern __shared__ __align__(16) float smem[];
-    float* Xs = smem;                 // [KCH][LDX], -2 * x
+    float* rowC = smem;               // [BM]
+    float* rowE = rowC + BM;          // [BM]
+    float* Xs = rowE + BM;            // [KCH][LDX], -2 * x
     float* Cs = Xs + KCH * LDX;       // [KCH][LDC]
     float* cn_s = Cs + KCH * LDC;     // [BN]
-    float* rowC = cn_s + BN;          // [BM]
-    float* rowE = rowC + BM;          // [BM]
 
-    const uint32_t b = blockIdx.y;
+    // problem index fastest: the B CTAs that read the same rows run together,
+    // so each row is fetched from HBM once and served to the others by L2
+    const uint32_t b = blockIdx.x % a.B;
     if (a.active && !a.active[b]) return;
-    const uint64_t i0 = (uint64_t)blockIdx.x * BM;
+    const uint64_t i0 = (uint64_t)(blockIdx.x / a.B) * BM;
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const int d = int(a.d);
     const int dp = (d + 3) & ~3;
@@ -202,7 +204,7 @@ __global__ void __launch_bounds__(NT, 2) nearest_kernel(NearestArgs a) {
 #pragma unroll
             for (int i = 0; i < TM; ++i)
 #pragma unroll
-                for (int j = 0; j < TN; ++j) acc[i][j] = cn_s[col_of<TN>(tx, j)];
+                for (int j = 0; j < TN; ++j) acc[i][j] = cn_s[col_of<TN>(tx, j)] + rowC[ty * 8 + i];
 #pragma unroll
             for (int t = 0; t < DP; ++t) {
                 const float4 xa = *reinterpret_cast<const float4*>(Xs + t * LDX + ty * 8);
@@ -220,7 +222,7 @@ __global__ void __launch_bounds__(NT, 2) nearest_kernel(NearestArgs a) {
 #pragma unroll
             for (int i = 0; i < TM; ++i)
 #pragma unroll
-                for (int j = 0; j < TN; ++j) acc[i][j] = cn_s[col_of<TN>(tx, j)];
+                for (int j = 0; j < TN; ++j) acc[i][j] = cn_s[col_of<TN>(tx, j)] + rowC[ty * 8 + i];
             for (int t0 = 0; t0 < dp; t0 += BK) {
                 const int kc = min(BK, dp - t0);
                 __syncthreads();
@@ -248,22 +250,20 @@ __global__ void __launch_bounds__(NT, 2) nearest_kernel(NearestArgs a) {
             for (int i = 0; i < TM; ++i) {
                 const int r = ty * 8 + i;
                 if (r >= rows_here) continue;
-                const float crow = rowC[r];
                 float* out = a.out_mat + (i0 + r) * a.ld_mat;
 #pragma unroll
                 for (int j = 0; j < TN; ++j) {
                     const uint64_t col = n0 + col_of<TN>(tx, j);
-                    if (col < k) out[col] = acc[i][j] + crow;
+                    if (col < k) out[col] = acc[i][j];
                 }
             }
         } else {
 #pragma unroll
             for (int i = 0; i < TM; ++i) {
-                const float crow = rowC[ty * 8 + i];
                 const uint32_t old = m1[i];
 #pragma unroll
                 for (int j = 0; j < TN; ++j) {
-                    const uint32_t key = (__float_as_uint(acc[i][j] + crow) & ~7u) | uint32_t(j);
+                    const uint32_t key = (__float_as_uint(acc[i][j]) & ~7u) | uint32_t(j);
                     m2[i] = min(m2[i], max(m1[i], key));
                     m1[i] = min(m1[i], key);
                 }
@@ -273,62 +273,103 @@ __global__ void __launch_bounds__(NT, 2) nearest_kernel(NearestArgs a) {
     }
     if constexpr (MAT) return;
 
-    // ---- combine the 16 column groups of each row (lanes xor 8,4,2,1)
-    uint64_t K[TM];
-    uint32_t V2[TM];
+    // ---- combine the 16 column groups of each row through shared memory:
+    // every thread parks (best key|column, second-best value) of its 8 rows,
+    // then one thread per row folds the 16 entries.
+    __syncthreads();
+    uint64_t* redK = reinterpret_cast<uint64_t*>(smem + 2 * BM);  // [BM][16] (reuses Xs/Cs)
+    uint32_t* redV = reinterpret_cast<uint32_t*>(redK + BM * 16);  // [BM][16]
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
         const uint32_t col = uint32_t(t1[i]) * BN + uint32_t(col_of<TN>(tx, int(m1[i] & 7u)));
-        K[i] = (uint64_t(m1[i] & ~7u) << 32) | col;
-        V2[i] = m2[i] & ~7u;
-#pragma unroll
-        for (int off = 8; off >= 1; off >>= 1) {
-            const uint64_t oK = __shfl_xor_sync(0xffffffffu, K[i], off);
-            const uint32_t oV = __shfl_xor_sync(0xffffffffu, V2[i], off);
-            const uint32_t hiMax = uint32_t(max(K[i], oK) >> 32);
-            V2[i] = min(min(V2[i], oV), hiMax);
-            K[i] = min(K[i], oK);
-        }
+        redK[(ty * 8 + i) * 16 + tx] = (uint64_t(m1[i] & ~7u) << 32) | col;
+        redV[(ty * 8 + i) * 16 + tx] = m2[i] & ~7u;
     }
-    // lane tx (< 8) finalises row ty*8 + tx
+    __syncthreads();
+    if (tid >= rows_here) return;
+    uint64_t K = redK[tid * 16];
+    uint32_t V2 = redV[tid * 16];
 #pragma unroll
-    for (int i = 0; i < TM; ++i) {
-        if (tx != i) continue;
-        const int r = ty * 8 + i;
-        if (r >= rows_here) continue;
-        const uint64_t row = i0 + r;
-        const uint32_t v1hi = uint32_t(K[i] >> 32);
-        const uint32_t idx = uint32_t(K[i]);
-        const float E = rowE[r];
-        const bool unique = (V2[i] >= 0x7f800000u) ||
-                            (__uint_as_float(V2[i]) - __uint_as_float(v1hi | 7u) > 2.05f * E);
-        if (unique) {
-            store_index(a, row, b, idx);
-            if (a.out_dist) a.out_dist[(uint64_t)b * a.n + row] = exact_dist(a, row, b, tab + (uint64_t)idx * d);
-        } else {
-            const unsigned long long slot = atomicAdd(a.flag_count, 1ull);
-            a.flags[slot] = (uint64_t(b) << 40) | row;
-        }
+    for (int g = 1; g < 16; ++g) {
+        const uint64_t oK = redK[tid * 16 + g];
+        const uint32_t oV = redV[tid * 16 + g];
+        V2 = min(min(V2, oV), uint32_t(max(K, oK) >> 32));
+        K = min(K, oK);
+    }
+    const uint64_t row = i0 + tid;
+    const uint32_t v1hi = uint32_t(K >> 32);
+    const uint32_t idx = uint32_t(K);
+    const float E = rowE[tid];
+    const bool unique = (V2 >= 0x7f800000u) ||
+                        (__uint_as_float(V2) - __uint_as_float(v1hi | 7u) > 2.05f * E);
+    if (unique) {
+        store_index(a, row, b, idx);
+        if (a.out_dist) a.out_dist[(uint64_t)b * a.n + row] = exact_dist(a, row, b, tab + (uint64_t)idx * d);
+    } else {
+        const unsigned long long slot = atomicAdd(a.flag_count, 1ull);
+        a.flags[slot] = (uint64_t(b) << 40) | row;
     }
 }
 
-// Exhaustive exact fp64 argmin for flagged (row, problem) pairs, one warp per
-// pair: nearest_in_table verbatim (strict '<', lowest index on ties).
-__global__ void fixup_kernel(NearestArgs a) {
+// Exact argmin for flagged (row, problem) pairs, one warp per pair.
+// Pass 1: fp32 direct-form distances (relative error <= eps = (d+2)u), warp
+// minimum vmin.  A candidate can tie or beat the fp64 winner only if its fp32
+// value is <= vmin (1+eps)/(1-eps); pass 2 re-scores exactly those in the
+// reference's fp64 arithmetic and takes the (dist, index) minimum -- the
+// result of nearest_in_table (strict '<', lowest index on ties).
+constexpr int kFixWarps = 8;
+constexpr int kFixMaxD = 512;
+
+__global__ void __launch_bounds__(32 * kFixWarps) fixup_kernel(NearestArgs a) {
+    __shared__ float xs_all[kFixWarps][kFixMaxD];
     const unsigned long long cnt = *a.flag_count;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    const uint32_t d = a.d;
+    const bool staged = d <= kFixMaxD;
+    float* xs = xs_all[wib];
+    const float eps = float(d + 2) * kU * 1.01f;
     for (uint64_t f = warp; f < cnt; f += nwarps) {
         const uint64_t item = a.flags[f];
         const uint32_t b = uint32_t(item >> 40);
         const uint64_t row = item & ((uint64_t(1) << 40) - 1);
-        const float* tab = a.table + (uint64_t)b * a.k * a.d;
+        const float* tab = a.table + (uint64_t)b * a.k * d;
+        if (staged) {
+            __syncwarp();
+            for (uint32_t t = lane; t < d; t += 32) xs[t] = load_x(a.src, row, b, t);
+            __syncwarp();
+        }
+        auto xval = [&](uint32_t t) { return staged ? xs[t] : load_x(a.src, row, b, t); };
+        float vmin = __int_as_float(0x7f800000);
+        for (uint64_t j = lane; j < a.k; j += 32) {
+            const float* c = tab + j * d;
+            float v = 0.f;
+            for (uint32_t t = 0; t < d; ++t) {
+                const float df = xval(t) - __ldg(c + t);
+                v = fmaf(df, df, v);
+            }
+            vmin = fminf(vmin, v);
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, off));
+        const float thr = vmin * ((1.f + eps) / (1.f - eps)) * (1.f + 4.f * kU) + 1e-37f;
         double best = __longlong_as_double(0x7ff0000000000000LL);
         uint32_t bj = 0xFFFFFFFFu;
         for (uint64_t j = lane; j < a.k; j += 32) {
-            const double dist = exact_dist(a, row, b, tab + j * a.d);
-            if (dist < best) { best = dist; bj = uint32_t(j); }
+            const float* c = tab + j * d;
+            float v = 0.f;
+            for (uint32_t t = 0; t < d; ++t) {
+                const float df = xval(t) - __ldg(c + t);
+                v = fmaf(df, df, v);
+            }
+            if (!(v <= thr) && !(v != v)) continue;  // NaN candidates go to the exact path
+            double acc = 0.0;
+            for (uint32_t t = 0; t < d; ++t) {
+                const double diff = __dsub_rn((double)xval(t), (double)__ldg(c + t));
+                acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+            }
+            if (acc < best) { best = acc; bj = uint32_t(j); }
         }
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) {
@@ -367,7 +408,9 @@ template <int TN, int DP, bool MAT>
 size_t smem_bytes() {
     constexpr int BN = 16 * TN;
     constexpr int KCH = DP > 0 ? DP : BK;
-    return sizeof(float) * (KCH * LDX + KCH * (BN + 4) + BN + 2 * BM);
+    const size_t main = sizeof(float) * (KCH * LDX + KCH * (BN + 4) + BN + 2 * BM);
+    const size_t red = size_t(BM) * 16 * (sizeof(uint64_t) + sizeof(uint32_t));
+    return main > red + sizeof(float) * 2 * BM ? main : red + sizeof(float) * 2 * BM;
 }
 
 template <int TN, int DP, bool MAT>
@@ -380,7 +423,7 @@ void launch_nearest(pqg_ctx* ctx, const NearestArgs& a) {
         configured = true;
     }
     const uint64_t gx = (a.n + BM - 1) / BM;
-    launch(ctx, MAT ? "distance_matrix" : "nearest", kern, dim3(unsigned(gx), a.B), dim3(NT), smem, a);
+    launch(ctx, MAT ? "distance_matrix" : "nearest", kern, dim3(unsigned(gx * a.B)), dim3(NT), smem, a);
 }
 
 template <int TN, bool MAT>
@@ -420,7 +463,7 @@ void nearest(pqg_ctx* ctx, NearestArgs a) {
     PQG_CUDA(cudaMemsetAsync(a.flag_count, 0, sizeof(unsigned long long), ctx->stream));
     a.out_mat = nullptr;
     dispatch<false>(ctx, a);
-    launch(ctx, "fixup", fixup_kernel, dim3(ctx->num_sms * 4), dim3(256), 0, a);
+    launch(ctx, "fixup", fixup_kernel, dim3(ctx->num_sms * 4), dim3(32 * kFixWarps), 0, a);
 }
 
 void distance_matrix(pqg_ctx* ctx, NearestArgs a) {
