@@ -52,6 +52,10 @@ void table_norms(pqg_ctx* ctx, const float* table, uint32_t B, uint64_t k, uint3
 void nearest(pqg_ctx* ctx, NearestArgs a);           // screen + exact fixup
 void distance_matrix(pqg_ctx* ctx, NearestArgs a);   // fp32 screen values only
 
+// umma.cu (tcgen05 3xTF32 screen for PQ subspaces)
+bool umma_screen_supported(const NearestArgs& a);
+void umma_screen(pqg_ctx* ctx, const NearestArgs& a);
+
 // kmeans.cu
 struct Bucketing {
     uint64_t* offsets;  // [B][k+1]

@@ -22,6 +22,8 @@
 // fp64 arithmetic (strict '<', lowest index on ties).  The result is
 // bit-identical to nearest_in_table for every row.
 #include <cfloat>
+#include <cstdlib>
+#include <cstring>
 
 #include "kernels.cuh"
 
@@ -462,7 +464,11 @@ void nearest(pqg_ctx* ctx, NearestArgs a) {
     a.flags = scratch<uint64_t>(ctx, a.n * a.B);
     PQG_CUDA(cudaMemsetAsync(a.flag_count, 0, sizeof(unsigned long long), ctx->stream));
     a.out_mat = nullptr;
-    dispatch<false>(ctx, a);
+    // screen selection: tcgen05 for PQ subspaces unless PQG_SCREEN=fp32
+    const char* mode = std::getenv("PQG_SCREEN");
+    const bool force_fp32 = mode && std::strcmp(mode, "fp32") == 0;
+    if (!force_fp32 && umma_screen_supported(a)) umma_screen(ctx, a);
+    else dispatch<false>(ctx, a);
     launch(ctx, "fixup", fixup_kernel, dim3(ctx->num_sms * 4), dim3(32 * kFixWarps), 0, a);
 }
 

@@ -1,0 +1,345 @@
+// umma.cu -- tcgen05 (5th-gen tensor core) screen for the PQ subspace argmin
+// (pq_encode, proj/src/pq.cpp:95-111; assign_pass of pq_fit,
+// proj/src/kmeans.cpp:46-57), the B200 replacement of the FP32 screen in
+// nearest.cu for Ds + 2 <= 40 and Ks a multiple of 16 up to 256.
+//
+// One CTA = 4 warps = 128 rows of a tile; TMEM lane r <-> row r <-> thread r.
+// Augmented operands make the MMA produce the screened value directly:
+//   A_r = [ x_r (Ds) , 1 , C_r ]          (C_r >= ||x_r||^2 + 2E_r)
+//   B_j = [ -2 c_j (Ds), ||c_j||^2 , 1 ]
+//   (A B^T)_rj = ||x_r - c_j||^2 + (C_r - ||x_r||^2)   >= E_r > 0.
+// fp32 accuracy from TF32 inputs by the 3xTF32 split (A_hi B_hi + A_hi B_lo +
+// A_lo B_hi, hi = tf32-rounded, lo = residual).  The accumulator (128 x N fp32)
+// lives in TMEM; each thread tcgen05.ld's its row (32 columns per load) and
+// keeps the best and second-best (value|column) keys with integer min/max --
+// no cross-thread reduction.  The flag rule and the exact fp64 fixup are the
+// ones of nearest.cu, with the error bound E widened for the split and the
+// tensor core's accumulation (see tc_error_bound).
+//
+// Operands are staged in shared memory in the canonical K-major
+// SWIZZLE_NONE ("interleaved") layout: 8-row x 16-byte core matrices; core
+// matrices adjacent in K are LBO = 128 B apart, adjacent 8-row groups
+// SBO = (K/4)*128 B apart.  Descriptor / instruction-descriptor bit layouts
+// follow the sm_100 UMMA definitions (CUTLASS cute/arch/mma_sm100_desc.hpp).
+#include "kernels.cuh"
+
+namespace pqg {
+
+namespace {
+
+constexpr int kRows = 128;  // M of the MMA, rows per tile, threads per CTA
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= uint64_t((saddr >> 4) & 0x3FFF);
+    d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
+    d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
+    d |= uint64_t(1) << 46;  // version 1 (sm_100)
+    // base_offset 0, lbo_mode 0, layout_type 0 = SWIZZLE_NONE
+    return d;
+}
+
+__host__ __device__ constexpr uint32_t make_idesc_tf32(uint32_t M, uint32_t N) {
+    return (1u << 4)            // D format F32
+           | (2u << 7)          // A format TF32
+           | (2u << 10)         // B format TF32
+           | ((N >> 3) << 17)   // N / 8
+           | ((M >> 4) << 24);  // M / 16
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                         uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
+        :: "r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 :: "r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred done;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+        "@!done bra WAIT_%=;\n\t}\n"
+        :: "r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+          "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+          "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// tf32 hi part: round to nearest at 10 mantissa bits (cvt.rna.tf32.f32)
+__device__ __forceinline__ float tf32_hi(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+// byte offset of element (row, k) of a K-major interleaved operand
+__device__ __forceinline__ uint32_t il_off(uint32_t row, uint32_t k, uint32_t sbo) {
+    return (row >> 3) * sbo + (k >> 2) * 128u + (row & 7u) * 16u + (k & 3u) * 4u;
+}
+
+__device__ __forceinline__ void store_index(const NearestArgs& a, uint64_t i, uint32_t b, uint32_t idx) {
+    const uint64_t off = i * a.idx_rs + (uint64_t)b * a.idx_ps;
+    if (a.idx_bytes == 1) {
+        static_cast<uint8_t*>(a.out_idx)[off] = uint8_t(idx);
+    } else if (a.idx_bytes == 2) {
+        uint8_t* p = static_cast<uint8_t*>(a.out_idx) + off * 2;
+        p[0] = uint8_t(idx & 0xff);
+        p[1] = uint8_t(idx >> 8);
+    } else {
+        static_cast<uint32_t*>(a.out_idx)[off] = idx;
+    }
+}
+
+// |screened - exact| bound for the 3xTF32 tensor-core screen: every product
+// of tf32 operands is exact in fp32; each of the 3*K accumulation steps may
+// lose one fp32 ulp of the running magnitude (truncating adder assumed);
+// the dropped lo*lo term and the tf32 rounding of lo parts are <= 2^-21 of
+// |x||c| per coordinate.  Doubled for safety.
+__device__ __forceinline__ float tc_error_bound(float S, int K) {
+    return 2.f * (2.f * float(3 * K + 4) + 16.f) * kU * S + 1e-30f;
+}
+
+template <int DS, int KA>
+__global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, uint32_t n_pad,
+                                                               uint32_t tmem_cols, uint32_t tiles_per_cta) {
+    static_assert(KA % 8 == 0 && KA >= DS + 2, "augmented K");
+    constexpr uint32_t SBO = (KA / 4) * 128;  // bytes between 8-row groups
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* Bh = smem;                         // [n_pad][KA]
+    uint8_t* Bl = Bh + size_t(n_pad) * KA * 4;  // [n_pad][KA]
+    uint8_t* Ah = Bl + size_t(n_pad) * KA * 4;  // [128][KA]
+    uint8_t* Al = Ah + size_t(kRows) * KA * 4;
+    __shared__ uint64_t mbar;
+    __shared__ uint32_t tmem_base;
+
+    const uint32_t tid = threadIdx.x, warp = tid >> 5;
+    const uint32_t B = a.B;
+    const uint32_t b = blockIdx.x % B;
+    const uint32_t cta = blockIdx.x / B, ncta = gridDim.x / B;
+    if (a.active && !a.active[b]) return;
+    const uint64_t k = a.k;
+    const float* tab = a.table + uint64_t(b) * k * DS;
+    const float cmax = a.cmax[b];
+
+    // ---- TMEM allocation (warp 0) and the mbarrier
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"(smem_u32(&tmem_base)), "r"(tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        mbar_init(&mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+
+    // ---- B operand: [-2c, ||c||^2, 1, 0...] split hi/lo, rows j >= k padded
+    for (uint32_t e = tid; e < n_pad * KA; e += kRows) {
+        const uint32_t j = e / KA, t = e - j * KA;
+        float v = 0.f;
+        if (j < k) {
+            if (t < DS) v = -2.f * __ldg(tab + uint64_t(j) * DS + t);
+            else if (t == DS) v = __ldg(a.cnorm + uint64_t(b) * k + j);
+            else if (t == DS + 1) v = 1.f;
+        } else if (t == DS) {
+            v = 3.0e38f;  // padded codeword: never the minimum
+        }
+        const float h = tf32_hi(v);
+        *reinterpret_cast<float*>(Bh + il_off(j, t, SBO)) = h;
+        *reinterpret_cast<float*>(Bl + il_off(j, t, SBO)) = tf32_hi(v - h);
+    }
+    fence_async_smem();
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = tmem_base;
+    const uint32_t idesc = make_idesc_tf32(kRows, n_pad);
+    const uint32_t a_hi = smem_u32(Ah), a_lo = smem_u32(Al);
+    const uint32_t b_hi = smem_u32(Bh), b_lo = smem_u32(Bl);
+    uint32_t phase = 0;
+
+    const bool vec4 = ((a.src.ldx | a.src.col_stride) & 3u) == 0 &&
+                      (reinterpret_cast<uintptr_t>(a.src.x) & 15u) == 0;
+    const uint64_t ntiles = (a.n + kRows - 1) / kRows;
+    for (uint64_t tile = cta; tile < ntiles; tile += ncta) {
+        const uint64_t row = tile * kRows + tid;
+        const bool valid = row < a.n;
+        // ---- stage A: this thread's row [x, 1, C]
+        float x[DS];
+        float nx = 0.f;
+        if (valid) {
+            const float* xp = a.src.x + row * a.src.ldx + uint64_t(b) * a.src.col_stride;
+            if (vec4) {
+#pragma unroll
+                for (int t = 0; t < DS; t += 4) {
+                    const float4 v = __ldg(reinterpret_cast<const float4*>(xp + t));
+                    x[t] = v.x; x[t + 1] = v.y; x[t + 2] = v.z; x[t + 3] = v.w;
+                }
+            } else {
+#pragma unroll
+                for (int t = 0; t < DS; ++t) x[t] = __ldg(xp + t);
+            }
+#pragma unroll
+            for (int t = 0; t < DS; ++t) nx = fmaf(x[t], x[t], nx);
+        } else {
+#pragma unroll
+            for (int t = 0; t < DS; ++t) x[t] = 0.f;
+        }
+        const float q = sqrtf(nx) * (1.f + 1e-6f) + cmax;
+        const float S = 3.f * q * q + 1.f;  // bounds sum |terms| incl. C and ||c||^2
+        const float E = tc_error_bound(S, KA);
+        const float C = nx * (1.f + 2.f * float(DS + 2) * kU) + 2.f * E;
+#pragma unroll
+        for (int t = 0; t < KA; t += 4) {
+            float h[4], l[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int tt = t + u;
+                const float v = tt < DS ? x[tt] : (tt == DS ? 1.f : (tt == DS + 1 ? C : 0.f));
+                h[u] = tf32_hi(v);
+                l[u] = tf32_hi(v - h[u]);
+            }
+            *reinterpret_cast<float4*>(Ah + il_off(tid, t, SBO)) = make_float4(h[0], h[1], h[2], h[3]);
+            *reinterpret_cast<float4*>(Al + il_off(tid, t, SBO)) = make_float4(l[0], l[1], l[2], l[3]);
+        }
+        fence_async_smem();
+        fence_before();
+        __syncthreads();
+        // ---- MMA: D = Ah Bh^T + Ah Bl^T + Al Bh^T over KA/8 k-steps
+        if (tid == 0) {
+            fence_after();
+#pragma unroll
+            for (int s = 0; s < KA / 8; ++s) {
+                const uint32_t ko = s * 256;  // two 16-byte K chunks per k-step
+                const uint64_t dah = make_desc(a_hi + ko, 128, SBO);
+                const uint64_t dal = make_desc(a_lo + ko, 128, SBO);
+                const uint64_t dbh = make_desc(b_hi + ko, 128, SBO);
+                const uint64_t dbl = make_desc(b_lo + ko, 128, SBO);
+                mma_tf32(tmem, dah, dbh, idesc, s > 0);
+                mma_tf32(tmem, dah, dbl, idesc, 1);
+                mma_tf32(tmem, dal, dbh, idesc, 1);
+            }
+            mma_commit(&mbar);
+        }
+        mbar_wait(&mbar, phase);
+        phase ^= 1;
+        fence_after();
+        // ---- epilogue: this thread's row, all n_pad columns
+        uint32_t m1 = 0xFFFFFFFFu, m2 = 0xFFFFFFFFu;
+        const uint32_t lane_base = (warp * 32u) << 16;
+        for (uint32_t c0 = 0; c0 < n_pad; c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(tmem + lane_base + c0, r);
+            tmem_wait_ld();
+            if (n_pad - c0 < 32) {  // columns past N are not written by the MMA
+#pragma unroll
+                for (int j = 16; j < 32; ++j) r[j] = 0x7f800000u;
+            }
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+                const uint32_t ka = (r[j] & ~0xFFu) | (c0 + j);
+                const uint32_t kb = (r[j + 1] & ~0xFFu) | (c0 + j + 1);
+                const uint32_t lo = min(ka, kb), hi = max(ka, kb);
+                m2 = min(min(m2, max(m1, lo)), hi);
+                m1 = min(m1, lo);
+            }
+        }
+        fence_before();
+        if (valid) {
+            const uint32_t idx = m1 & 0xFFu;
+            const bool unique = (m2 >= 0x7f800000u) ||
+                                (__uint_as_float(m2 & ~0xFFu) - __uint_as_float(m1 | 0xFFu) > 2.05f * E);
+            if (unique && idx < k) {
+                store_index(a, row, b, idx);
+                if (a.out_dist) {
+                    const float* c = tab + uint64_t(idx) * DS;
+                    double acc = 0.0;
+#pragma unroll
+                    for (int t = 0; t < DS; ++t) {
+                        const double diff = __dsub_rn((double)x[t], (double)__ldg(c + t));
+                        acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+                    }
+                    a.out_dist[uint64_t(b) * a.n + row] = acc;
+                }
+            } else {
+                const unsigned long long slot = atomicAdd(a.flag_count, 1ull);
+                a.flags[slot] = (uint64_t(b) << 40) | row;
+            }
+        }
+        __syncthreads();  // TMEM and the A stage are reused by the next tile
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(tmem_cols));
+    }
+    (void)tiles_per_cta;
+}
+
+template <int DS, int KA>
+void launch_umma(pqg_ctx* ctx, const NearestArgs& a) {
+    const uint32_t n_pad = uint32_t((a.k + 15) / 16 * 16);
+    uint32_t cols = 32;
+    while (cols < n_pad) cols <<= 1;
+    const size_t smem = size_t(2) * n_pad * KA * 4 + size_t(2) * kRows * KA * 4;
+    auto kern = umma_screen_kernel<DS, KA>;
+    set_smem(kern, smem);
+    const uint64_t ntiles = (a.n + kRows - 1) / kRows;
+    // persistent: ~2 CTAs per SM in total, each problem gets its share
+    uint64_t per_b = std::max<uint64_t>(1, (uint64_t(ctx->num_sms) * 2 + a.B - 1) / a.B);
+    per_b = std::min<uint64_t>(per_b, ntiles);
+    launch(ctx, "nearest_tc", kern, dim3(unsigned(per_b * a.B)), dim3(kRows), smem, a, n_pad, cols,
+           uint32_t((ntiles + per_b - 1) / per_b));
+}
+
+}  // namespace
+
+bool umma_screen_supported(const NearestArgs& a) {
+    if (a.src.codes || a.out_mat) return false;
+    if (a.k < 16 || a.k > 256 || a.k % 16 != 0) return false;
+    return a.d == 4 || a.d == 8 || a.d == 16 || a.d == 32;
+}
+
+void umma_screen(pqg_ctx* ctx, const NearestArgs& a) {
+    switch (a.d) {
+        case 4: launch_umma<4, 8>(ctx, a); break;
+        case 8: launch_umma<8, 16>(ctx, a); break;
+        case 16: launch_umma<16, 24>(ctx, a); break;
+        case 32: launch_umma<32, 40>(ctx, a); break;
+        default: fail(PQG_EUNSUPPORTED, "umma_screen: unsupported sub-dimension");
+    }
+}
+
+}  // namespace pqg
