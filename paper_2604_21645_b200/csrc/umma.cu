@@ -122,13 +122,17 @@ __device__ __forceinline__ void store_index(const NearestArgs& a, uint64_t i, ui
     }
 }
 
-// |screened - exact| bound for the 3xTF32 tensor-core screen: every product
-// of tf32 operands is exact in fp32; each of the 3*K accumulation steps may
-// lose one fp32 ulp of the running magnitude (truncating adder assumed);
-// the dropped lo*lo term and the tf32 rounding of lo parts are <= 2^-21 of
-// |x||c| per coordinate.  Doubled for safety.
+// |screened - exact| bound for the 3xTF32 tensor-core screen.  S bounds the
+// sum of |terms| (2|x.c| + ||c||^2 + C <= (||x|| + max||c||)^2 + small).
+// Products of tf32 operands are exact in fp32; each MMA instruction may
+// lose up to one fp32 ulp (2u) of the accumulator, whose magnitude is <= S
+// (3 splits x K/8 k-steps instructions); the dropped lo*lo term and the tf32
+// rounding of the lo parts are <= 2^-21 |x_t c_t| per coordinate (<= 4u S).
+// Doubled for safety.  Empirically (tools/screen_bench.py) the TC and FP32
+// screens return identical codes on all 1M x M rows tested.
 __device__ __forceinline__ float tc_error_bound(float S, int K) {
-    return 2.f * (2.f * float(3 * K + 4) + 16.f) * kU * S + 1e-30f;
+    const float n_mma = float(3 * (K / 8));
+    return 2.f * (2.f * n_mma + 8.f) * kU * S + 1e-30f;
 }
 
 template <int DS, int KA>
@@ -217,7 +221,7 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
             for (int t = 0; t < DS; ++t) x[t] = 0.f;
         }
         const float q = sqrtf(nx) * (1.f + 1e-6f) + cmax;
-        const float S = 3.f * q * q + 1.f;  // bounds sum |terms| incl. C and ||c||^2
+        const float S = q * q * 1.01f + 1e-6f;  // >= 2|x.c| + ||c||^2 + C
         const float E = tc_error_bound(S, KA);
         const float C = nx * (1.f + 2.f * float(DS + 2) * kU) + 2.f * E;
 #pragma unroll
@@ -256,7 +260,9 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
         phase ^= 1;
         fence_after();
         // ---- epilogue: this thread's row, all n_pad columns
-        uint32_t m1 = 0xFFFFFFFFu, m2 = 0xFFFFFFFFu;
+        // keys carry the column within a 32-column chunk in 5 low bits (value
+        // quantum 32 ulp); the chunk of the running best is tracked on change
+        uint32_t m1 = 0xFFFFFFFFu, m2 = 0xFFFFFFFFu, chunk1 = 0;
         const uint32_t lane_base = (warp * 32u) << 16;
         for (uint32_t c0 = 0; c0 < n_pad; c0 += 32) {
             uint32_t r[32];
@@ -266,20 +272,22 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
 #pragma unroll
                 for (int j = 16; j < 32; ++j) r[j] = 0x7f800000u;
             }
+            const uint32_t old = m1;
 #pragma unroll
             for (int j = 0; j < 32; j += 2) {
-                const uint32_t ka = (r[j] & ~0xFFu) | (c0 + j);
-                const uint32_t kb = (r[j + 1] & ~0xFFu) | (c0 + j + 1);
+                const uint32_t ka = (r[j] & ~31u) | uint32_t(j);
+                const uint32_t kb = (r[j + 1] & ~31u) | uint32_t(j + 1);
                 const uint32_t lo = min(ka, kb), hi = max(ka, kb);
                 m2 = min(min(m2, max(m1, lo)), hi);
                 m1 = min(m1, lo);
             }
+            chunk1 = (m1 != old) ? c0 : chunk1;
         }
         fence_before();
         if (valid) {
-            const uint32_t idx = m1 & 0xFFu;
+            const uint32_t idx = chunk1 + (m1 & 31u);
             const bool unique = (m2 >= 0x7f800000u) ||
-                                (__uint_as_float(m2 & ~0xFFu) - __uint_as_float(m1 | 0xFFu) > 2.05f * E);
+                                (__uint_as_float(m2 & ~31u) - __uint_as_float(m1 | 31u) > 2.05f * E);
             if (unique && idx < k) {
                 store_index(a, row, b, idx);
                 if (a.out_dist) {
@@ -315,7 +323,7 @@ void launch_umma(pqg_ctx* ctx, const NearestArgs& a) {
     while (cols < n_pad) cols <<= 1;
     const size_t smem = size_t(2) * n_pad * KA * 4 + size_t(2) * kRows * KA * 4;
     auto kern = umma_screen_kernel<DS, KA>;
-    set_smem(kern, smem);
+    PQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     const uint64_t ntiles = (a.n + kRows - 1) / kRows;
     // persistent: ~2 CTAs per SM in total, each problem gets its share
     uint64_t per_b = std::max<uint64_t>(1, (uint64_t(ctx->num_sms) * 2 + a.B - 1) / a.B);
