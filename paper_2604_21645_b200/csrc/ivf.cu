@@ -186,6 +186,34 @@ __device__ __forceinline__ void warp_insert(double& my_d, uint64_t& my_id, doubl
     }
 }
 
+// A code row of RB bytes (RB in {4, 8, 16, 32}) read with vector loads; the
+// codes are extracted from registers (RB == 0: generic byte path).
+template <int RB>
+struct CodeRow {
+    uint32_t w[RB > 0 ? RB / 4 : 1];
+    __device__ __forceinline__ void load(const uint8_t* p) {
+        if constexpr (RB == 4) {
+            w[0] = __ldg(reinterpret_cast<const uint32_t*>(p));
+        } else if constexpr (RB == 8) {
+            const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+            w[0] = v.x; w[1] = v.y;
+        } else if constexpr (RB == 16 || RB == 32) {
+#pragma unroll
+            for (int q = 0; q < RB / 16; ++q) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(p) + q);
+                w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+            }
+        }
+    }
+    // code of subspace m for code width W
+    template <int W>
+    __device__ __forceinline__ uint32_t get(int m) const {
+        if constexpr (W == 1) return (w[m >> 2] >> ((m & 3) * 8)) & 0xFFu;
+        else return (w[m >> 1] >> ((m & 1) * 16)) & 0xFFFFu;
+    }
+};
+
+template <int RB, int W>
 __global__ void __launch_bounds__(kScanThreads) adc_scan_kernel(
     const float* tables, uint32_t M, uint32_t ks, uint32_t ds, const float* queries,
     const uint64_t* offsets, const uint64_t* ids, const uint8_t* codes, const uint32_t* probes,
@@ -222,19 +250,44 @@ __global__ void __launch_bounds__(kScanThreads) adc_scan_kernel(
                 const uint8_t* cr = codes + e * rb;
                 float s32 = 0.f;
                 bool bad = false;
-                for (uint32_t m = 0; m < M; ++m) {
-                    const uint32_t c = code_at(cr, m, w);
-                    if (c >= ks) { bad = true; break; }
-                    s32 += lut[m * ks + c];
+                if constexpr (RB > 0) {
+                    const bool check = W == 2 || ks < 256;
+                    CodeRow<RB> row;
+                    row.load(cr);
+                    constexpr int MM = RB / W;
+#pragma unroll
+                    for (int m = 0; m < MM; ++m) {
+                        const uint32_t c = row.template get<W>(m);
+                        if (check && c >= ks) bad = true;
+                        s32 += lut[m * ks + min(c, ks - 1)];
+                    }
+                    if (!bad) {
+                        const double lower = double(s32) * double(shrink);
+                        if (lower <= th && !(has_max && lower > max_sq)) {
+#pragma unroll
+                            for (int m = 0; m < MM; ++m)
+                                s64 = __dadd_rn(s64, (double)lut[m * ks + row.template get<W>(m)]);
+                            id = ids[e];
+                            want = !(has_max && s64 > max_sq);
+                        }
+                    }
+                } else {
+                    for (uint32_t m = 0; m < M; ++m) {
+                        const uint32_t c = code_at(cr, m, w);
+                        if (c >= ks) { bad = true; break; }
+                        s32 += lut[m * ks + c];
+                    }
+                    if (!bad) {
+                        const double lower = double(s32) * double(shrink);
+                        if (lower <= th && !(has_max && lower > max_sq)) {
+                            for (uint32_t m = 0; m < M; ++m)
+                                s64 = __dadd_rn(s64, (double)lut[m * ks + code_at(cr, m, w)]);
+                            id = ids[e];
+                            want = !(has_max && s64 > max_sq);
+                        }
+                    }
                 }
                 if (bad) atomicExch(err, 1);
-                const double lower = double(s32) * double(shrink);
-                if (!bad && lower <= th && !(has_max && lower > max_sq)) {
-                    for (uint32_t m = 0; m < M; ++m)
-                        s64 = __dadd_rn(s64, (double)lut[m * ks + code_at(cr, m, w)]);
-                    id = ids[e];
-                    want = !(has_max && s64 > max_sq);
-                }
             }
             uint32_t ball = __ballot_sync(0xffffffffu, want);
             while (ball) {
@@ -418,14 +471,26 @@ void ivf_scan(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t 
     const size_t lut_bytes = (sizeof(float) * ix.M * ix.ks + 15) & ~size_t(15);
     const size_t smem = lut_bytes + sizeof(TopK) * k * (kScanThreads / 32);
     if (smem > 220 * 1024) fail(PQG_EUNSUPPORTED, "search: M*ks lookup table exceeds shared memory");
-    set_smem(adc_scan_kernel, smem);
-    for (uint64_t q0 = 0; q0 < nq; q0 += 65535) {
-        const uint64_t nc = std::min<uint64_t>(65535, nq - q0);
-        launch(ctx, "adc_scan", adc_scan_kernel, dim3(unsigned(nc)), dim3(kScanThreads), smem,
-               ix.tables, ix.M, ix.ks, ix.ds, queries + q0 * ix.M * ix.ds, ix.offsets, ix.ids,
-               ix.codes, probes + q0 * nprobe, nprobe, int(k), has_max, max_sq, out_ids + q0 * k,
-               out_dists + q0 * k, out_counts + q0, err);
-    }
+    const uint32_t rb = ix.M * ix.w;
+    auto run = [&](auto kern) {
+        set_smem(kern, smem);
+        for (uint64_t q0 = 0; q0 < nq; q0 += 65535) {
+            const uint64_t nc = std::min<uint64_t>(65535, nq - q0);
+            launch(ctx, "adc_scan", kern, dim3(unsigned(nc)), dim3(kScanThreads), smem, ix.tables,
+                   ix.M, ix.ks, ix.ds, queries + q0 * ix.M * ix.ds, ix.offsets, ix.ids, ix.codes,
+                   probes + q0 * nprobe, nprobe, int(k), has_max, max_sq, out_ids + q0 * k,
+                   out_dists + q0 * k, out_counts + q0, err);
+        }
+    };
+    // vector code loads need rb-aligned rows (CSR rows are rb apart from an aligned base)
+    const bool aligned = (reinterpret_cast<uintptr_t>(ix.codes) % (rb >= 16 ? 16 : rb)) == 0;
+    if (aligned && ix.w == 1 && rb == 16) run(adc_scan_kernel<16, 1>);
+    else if (aligned && ix.w == 1 && rb == 8) run(adc_scan_kernel<8, 1>);
+    else if (aligned && ix.w == 1 && rb == 32) run(adc_scan_kernel<32, 1>);
+    else if (aligned && ix.w == 1 && rb == 4) run(adc_scan_kernel<4, 1>);
+    else if (aligned && ix.w == 2 && rb == 16) run(adc_scan_kernel<16, 2>);
+    else if (aligned && ix.w == 2 && rb == 8) run(adc_scan_kernel<8, 2>);
+    else run(adc_scan_kernel<0, 1>);
 }
 
 void csr_scatter(pqg_ctx* ctx, const uint32_t* perm, uint64_t n, const uint64_t* ids,

@@ -261,8 +261,12 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
         fence_after();
         // ---- epilogue: this thread's row, all n_pad columns
         // keys carry the column within a 32-column chunk in 5 low bits (value
-        // quantum 32 ulp); the chunk of the running best is tracked on change
-        uint32_t m1 = 0xFFFFFFFFu, m2 = 0xFFFFFFFFu, chunk1 = 0;
+        // quantum 32 ulp); the chunk of each running best is tracked on
+        // change.  Four independent (best, second) states per thread break the
+        // min/max dependency chain; they are merged at the end.
+        uint32_t m1[4], m2[4], ch[4];
+#pragma unroll
+        for (int s4 = 0; s4 < 4; ++s4) { m1[s4] = 0xFFFFFFFFu; m2[s4] = 0xFFFFFFFFu; ch[s4] = 0; }
         const uint32_t lane_base = (warp * 32u) << 16;
         for (uint32_t c0 = 0; c0 < n_pad; c0 += 32) {
             uint32_t r[32];
@@ -272,22 +276,40 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
 #pragma unroll
                 for (int j = 16; j < 32; ++j) r[j] = 0x7f800000u;
             }
-            const uint32_t old = m1;
+            uint32_t old[4];
 #pragma unroll
-            for (int j = 0; j < 32; j += 2) {
-                const uint32_t ka = (r[j] & ~31u) | uint32_t(j);
-                const uint32_t kb = (r[j + 1] & ~31u) | uint32_t(j + 1);
-                const uint32_t lo = min(ka, kb), hi = max(ka, kb);
-                m2 = min(min(m2, max(m1, lo)), hi);
-                m1 = min(m1, lo);
+            for (int s4 = 0; s4 < 4; ++s4) old[s4] = m1[s4];
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+#pragma unroll
+                for (int s4 = 0; s4 < 4; ++s4) {
+                    const int jj = j + 2 * s4;
+                    const uint32_t ka = (r[jj] & ~31u) | uint32_t(jj);
+                    const uint32_t kb = (r[jj + 1] & ~31u) | uint32_t(jj + 1);
+                    const uint32_t lo = min(ka, kb), hi = max(ka, kb);
+                    m2[s4] = min(min(m2[s4], max(m1[s4], lo)), hi);
+                    m1[s4] = min(m1[s4], lo);
+                }
             }
-            chunk1 = (m1 != old) ? c0 : chunk1;
+#pragma unroll
+            for (int s4 = 0; s4 < 4; ++s4) ch[s4] = (m1[s4] != old[s4]) ? c0 : ch[s4];
+        }
+        // merge the four states: full keys (value bits | global column) for the
+        // best, value bits (low 5 cleared) for the runner-up
+        uint64_t K1 = (uint64_t(m1[0] & ~31u) << 32) | (ch[0] + (m1[0] & 31u));
+        uint32_t V2 = m2[0] & ~31u;
+#pragma unroll
+        for (int s4 = 1; s4 < 4; ++s4) {
+            const uint64_t o = (uint64_t(m1[s4] & ~31u) << 32) | (ch[s4] + (m1[s4] & 31u));
+            V2 = min(min(V2, m2[s4] & ~31u), uint32_t(max(K1, o) >> 32));
+            K1 = min(K1, o);
         }
         fence_before();
         if (valid) {
-            const uint32_t idx = chunk1 + (m1 & 31u);
-            const bool unique = (m2 >= 0x7f800000u) ||
-                                (__uint_as_float(m2 & ~31u) - __uint_as_float(m1 | 31u) > 2.05f * E);
+            const uint32_t idx = uint32_t(K1);
+            const uint32_t v1 = uint32_t(K1 >> 32);
+            const bool unique = (V2 >= 0x7f800000u) ||
+                                (__uint_as_float(V2) - __uint_as_float(v1 | 31u) > 2.05f * E);
             if (unique && idx < k) {
                 store_index(a, row, b, idx);
                 if (a.out_dist) {
