@@ -21,6 +21,8 @@
 // matrices adjacent in K are LBO = 128 B apart, adjacent 8-row groups
 // SBO = (K/4)*128 B apart.  Descriptor / instruction-descriptor bit layouts
 // follow the sm_100 UMMA definitions (CUTLASS cute/arch/mma_sm100_desc.hpp).
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace pqg {
@@ -338,8 +340,287 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
     (void)tiles_per_cta;
 }
 
+// ---------------------------------------------------------------------------
+// Pipelined version: one CTA per SM, 8 warps, persistent over the row tiles
+// of one subspace.  TMEM holds two 128 x n_pad fp32 accumulators and the A
+// stage is double-buffered, so the MMAs of tile i+1 run while the CUDA cores
+// reduce tile i; the rows of tile i+2 are already in flight from HBM.  Warp w
+// reads TMEM lanes 32(w%4).. and the column half w/4; the halves meet in
+// shared memory.
+// ---------------------------------------------------------------------------
+template <int DS>
+struct RowRegs {
+    float x[DS];
+};
+
+template <int DS>
+__device__ __forceinline__ void load_row(const NearestArgs& a, uint64_t row, uint32_t b, bool vec4,
+                                         RowRegs<DS>& r) {
+    if (row < a.n) {
+        const float* xp = a.src.x + row * a.src.ldx + uint64_t(b) * a.src.col_stride;
+        if (vec4) {
+#pragma unroll
+            for (int t = 0; t < DS; t += 4) {
+                const float4 v = __ldg(reinterpret_cast<const float4*>(xp + t));
+                r.x[t] = v.x; r.x[t + 1] = v.y; r.x[t + 2] = v.z; r.x[t + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int t = 0; t < DS; ++t) r.x[t] = __ldg(xp + t);
+        }
+    } else {
+#pragma unroll
+        for (int t = 0; t < DS; ++t) r.x[t] = 0.f;
+    }
+}
+
+template <int DS, int KA>
+__global__ void __launch_bounds__(256, 1) umma_screen2_kernel(NearestArgs a, uint32_t n_pad) {
+    constexpr uint32_t SBO = (KA / 4) * 128;
+    constexpr uint32_t ASTAGE = kRows * KA * 4;  // bytes of one A (hi or lo) stage
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* Bh = smem;
+    uint8_t* Bl = Bh + size_t(n_pad) * KA * 4;
+    uint8_t* A0 = Bl + size_t(n_pad) * KA * 4;  // [stage][hi|lo][128 x KA]
+    __shared__ uint64_t mbar[2];
+    __shared__ uint32_t tmem_base;
+    __shared__ float ebuf[2][kRows];
+    __shared__ uint64_t mK[kRows];
+    __shared__ uint32_t mV[kRows];
+
+    const uint32_t tid = threadIdx.x, warp = tid >> 5;
+    const uint32_t B = a.B;
+    const uint32_t b = blockIdx.x % B;
+    const uint32_t cta = blockIdx.x / B, ncta = gridDim.x / B;
+    if (a.active && !a.active[b]) return;
+    const uint64_t k = a.k;
+    const float* tab = a.table + uint64_t(b) * k * DS;
+    const float cmax = a.cmax[b];
+    const uint32_t row_l = tid & (kRows - 1);  // row of the tile this thread stages / reads
+    const uint32_t half = tid >> 7;             // K half it stages, column half it reduces
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"(smem_u32(&tmem_base)), "r"(512u));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (uint32_t e = tid; e < n_pad * KA; e += blockDim.x) {
+        const uint32_t j = e / KA, t = e - j * KA;
+        float v = 0.f;
+        if (j < k) {
+            if (t < DS) v = -2.f * __ldg(tab + uint64_t(j) * DS + t);
+            else if (t == DS) v = __ldg(a.cnorm + uint64_t(b) * k + j);
+            else if (t == DS + 1) v = 1.f;
+        } else if (t == DS) {
+            v = 3.0e38f;
+        }
+        const float h = tf32_hi(v);
+        *reinterpret_cast<float*>(Bh + il_off(j, t, SBO)) = h;
+        *reinterpret_cast<float*>(Bl + il_off(j, t, SBO)) = tf32_hi(v - h);
+    }
+    fence_async_smem();
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = tmem_base;
+    const uint32_t idesc = make_idesc_tf32(kRows, n_pad);
+    const uint32_t b_hi = smem_u32(Bh), b_lo = smem_u32(Bl);
+    const bool vec4 = ((a.src.ldx | a.src.col_stride) & 3u) == 0 &&
+                      (reinterpret_cast<uintptr_t>(a.src.x) & 15u) == 0;
+    const uint64_t ntiles = (a.n + kRows - 1) / kRows;
+    const uint64_t my_tiles = cta < ntiles ? (ntiles - cta + ncta - 1) / ncta : 0;
+
+    // stage the A operand of tile number `it` (local index) from registers
+    auto stage = [&](uint64_t it, const RowRegs<DS>& r) {
+        float nx = 0.f;
+#pragma unroll
+        for (int t = 0; t < DS; ++t) nx = fmaf(r.x[t], r.x[t], nx);
+        const float q = sqrtf(nx) * (1.f + 1e-6f) + cmax;
+        const float S = q * q * 1.01f + 1e-6f;
+        const float E = tc_error_bound(S, KA);
+        const float C = nx * (1.f + 2.f * float(DS + 2) * kU) + 2.f * E;
+        if (half == 0) ebuf[it & 1][row_l] = E;
+        uint8_t* Ah = A0 + (it & 1) * 2 * ASTAGE;
+        uint8_t* Al = Ah + ASTAGE;
+        constexpr int NCH = KA / 4;               // 16-byte chunks per row
+        constexpr int C0 = 0, C1 = (NCH + 1) / 2;  // this half's chunk range
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            if ((half == 0) != (c < C1)) continue;
+            float h[4], l[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int tt = 4 * c + u;
+                const float v = tt < DS ? r.x[tt] : (tt == DS ? 1.f : (tt == DS + 1 ? C : 0.f));
+                h[u] = tf32_hi(v);
+                l[u] = tf32_hi(v - h[u]);
+            }
+            *reinterpret_cast<float4*>(Ah + il_off(row_l, 4 * c, SBO)) = make_float4(h[0], h[1], h[2], h[3]);
+            *reinterpret_cast<float4*>(Al + il_off(row_l, 4 * c, SBO)) = make_float4(l[0], l[1], l[2], l[3]);
+        }
+        (void)C0;
+    };
+    auto issue = [&](uint64_t it) {
+        const uint32_t ah = smem_u32(A0 + (it & 1) * 2 * ASTAGE), al = ah + ASTAGE;
+        const uint32_t d_tmem = tmem + uint32_t(it & 1) * 256u;
+#pragma unroll
+        for (int s2 = 0; s2 < KA / 8; ++s2) {
+            const uint32_t ko = s2 * 256;
+            const uint64_t dah = make_desc(ah + ko, 128, SBO);
+            const uint64_t dal = make_desc(al + ko, 128, SBO);
+            const uint64_t dbh = make_desc(b_hi + ko, 128, SBO);
+            const uint64_t dbl = make_desc(b_lo + ko, 128, SBO);
+            mma_tf32(d_tmem, dah, dbh, idesc, s2 > 0);
+            mma_tf32(d_tmem, dah, dbl, idesc, 1);
+            mma_tf32(d_tmem, dal, dbh, idesc, 1);
+        }
+        mma_commit(&mbar[it & 1]);
+    };
+    auto tile_of = [&](uint64_t it) { return uint64_t(cta) + it * ncta; };
+
+    RowRegs<DS> xr;
+    if (my_tiles > 0) {
+        load_row<DS>(a, tile_of(0) * kRows + row_l, b, vec4, xr);
+        stage(0, xr);
+        if (my_tiles > 1) load_row<DS>(a, tile_of(1) * kRows + row_l, b, vec4, xr);
+        fence_async_smem();
+        fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            fence_after();
+            issue(0);
+        }
+    }
+    uint32_t phases = 0;  // bit s: parity of mbar[s]
+    for (uint64_t it = 0; it < my_tiles; ++it) {
+        // stage tile it+1 (rows already in registers), prefetch tile it+2
+        if (it + 1 < my_tiles) {
+            stage(it + 1, xr);
+            if (it + 2 < my_tiles) load_row<DS>(a, tile_of(it + 2) * kRows + row_l, b, vec4, xr);
+        }
+        fence_async_smem();
+        fence_before();
+        __syncthreads();
+        if (tid == 0 && it + 1 < my_tiles) {
+            fence_after();
+            issue(it + 1);
+        }
+        mbar_wait(&mbar[it & 1], (phases >> (it & 1)) & 1u);
+        phases ^= 1u << (it & 1);
+        fence_after();
+        // ---- epilogue of tile it: this thread's row, its column half
+        uint32_t m1[4], m2[4], ch[4];
+#pragma unroll
+        for (int s4 = 0; s4 < 4; ++s4) { m1[s4] = 0xFFFFFFFFu; m2[s4] = 0xFFFFFFFFu; ch[s4] = 0; }
+        const uint32_t lane_base = ((warp & 3u) * 32u) << 16;
+        const uint32_t ncols_half = (n_pad + 31) / 64 * 32;  // 32-column chunks per half
+        const uint32_t cbeg = half * ncols_half;
+        const uint32_t cend = min(n_pad, cbeg + ncols_half);
+        const uint32_t tb = tmem + uint32_t(it & 1) * 256u;
+        for (uint32_t c0 = cbeg; c0 < cend; c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(tb + lane_base + c0, r);
+            tmem_wait_ld();
+            if (n_pad - c0 < 32) {
+#pragma unroll
+                for (int j = 16; j < 32; ++j) r[j] = 0x7f800000u;
+            }
+            uint32_t old[4];
+#pragma unroll
+            for (int s4 = 0; s4 < 4; ++s4) old[s4] = m1[s4];
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+#pragma unroll
+                for (int s4 = 0; s4 < 4; ++s4) {
+                    const int jj = j + 2 * s4;
+                    const uint32_t ka = (r[jj] & ~31u) | uint32_t(jj);
+                    const uint32_t kb = (r[jj + 1] & ~31u) | uint32_t(jj + 1);
+                    const uint32_t lo = min(ka, kb), hi = max(ka, kb);
+                    m2[s4] = min(min(m2[s4], max(m1[s4], lo)), hi);
+                    m1[s4] = min(m1[s4], lo);
+                }
+            }
+#pragma unroll
+            for (int s4 = 0; s4 < 4; ++s4) ch[s4] = (m1[s4] != old[s4]) ? c0 : ch[s4];
+        }
+        fence_before();
+        uint64_t K1 = (uint64_t(m1[0] & ~31u) << 32) | (ch[0] + (m1[0] & 31u));
+        uint32_t V2 = m2[0] & ~31u;
+#pragma unroll
+        for (int s4 = 1; s4 < 4; ++s4) {
+            const uint64_t o = (uint64_t(m1[s4] & ~31u) << 32) | (ch[s4] + (m1[s4] & 31u));
+            V2 = min(min(V2, m2[s4] & ~31u), uint32_t(max(K1, o) >> 32));
+            K1 = min(K1, o);
+        }
+        if (half == 1) {
+            mK[row_l] = K1;
+            mV[row_l] = V2;
+        }
+        __syncthreads();
+        if (half == 0) {
+            const uint64_t oK = mK[row_l];
+            V2 = min(min(V2, mV[row_l]), uint32_t(max(K1, oK) >> 32));
+            K1 = min(K1, oK);
+            const uint64_t row = tile_of(it) * kRows + row_l;
+            if (row < a.n) {
+                const uint32_t idx = uint32_t(K1);
+                const uint32_t v1 = uint32_t(K1 >> 32);
+                const float E = ebuf[it & 1][row_l];
+                const bool unique = (V2 >= 0x7f800000u) ||
+                                    (__uint_as_float(V2) - __uint_as_float(v1 | 31u) > 2.05f * E);
+                if (unique && idx < k) {
+                    store_index(a, row, b, idx);
+                    if (a.out_dist) {
+                        const float* xp = a.src.x + row * a.src.ldx + uint64_t(b) * a.src.col_stride;
+                        const float* c = tab + uint64_t(idx) * DS;
+                        double acc = 0.0;
+#pragma unroll
+                        for (int t = 0; t < DS; ++t) {
+                            const double diff = __dsub_rn((double)__ldg(xp + t), (double)__ldg(c + t));
+                            acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+                        }
+                        a.out_dist[uint64_t(b) * a.n + row] = acc;
+                    }
+                } else {
+                    const unsigned long long slot = atomicAdd(a.flag_count, 1ull);
+                    a.flags[slot] = (uint64_t(b) << 40) | row;
+                }
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(512u));
+    }
+}
+
+template <int DS, int KA>
+void launch_umma2(pqg_ctx* ctx, const NearestArgs& a) {
+    const uint32_t n_pad = uint32_t((a.k + 15) / 16 * 16);
+    const size_t smem = size_t(2) * n_pad * KA * 4 + size_t(4) * kRows * KA * 4;
+    auto kern = umma_screen2_kernel<DS, KA>;
+    PQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    const uint64_t ntiles = (a.n + kRows - 1) / kRows;
+    // one CTA per SM; each subspace gets floor(SMs / B) CTAs (at least 1)
+    uint64_t per_b = std::max<uint64_t>(1, uint64_t(ctx->num_sms) / a.B);
+    per_b = std::min<uint64_t>(per_b, ntiles);
+    launch(ctx, "nearest_tc", kern, dim3(unsigned(per_b * a.B)), dim3(256), smem, a, n_pad);
+}
+
 template <int DS, int KA>
 void launch_umma(pqg_ctx* ctx, const NearestArgs& a) {
+    static const bool v1 = std::getenv("PQG_UMMA") && std::getenv("PQG_UMMA")[0] == '1';
+    if (!v1) {
+        launch_umma2<DS, KA>(ctx, a);
+        return;
+    }
     const uint32_t n_pad = uint32_t((a.k + 15) / 16 * 16);
     uint32_t cols = 32;
     while (cols < n_pad) cols <<= 1;
