@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(256, 1) umma_screen2_kernel(NearestArgs a, uin
 #pragma unroll
         for (int s4 = 0; s4 < 4; ++s4) { m1[s4] = 0xFFFFFFFFu; m2[s4] = 0xFFFFFFFFu; ch[s4] = 0; }
         const uint32_t lane_base = ((warp & 3u) * 32u) << 16;
-        const uint32_t ncols_half = (n_pad + 31) / 64 * 32;  // 32-column chunks per half
+        const uint32_t ncols_half = (n_pad + 63) / 64 * 32;  // columns per half, whole 32-chunks
         const uint32_t cbeg = half * ncols_half;
         const uint32_t cend = min(n_pad, cbeg + ncols_half);
         const uint32_t tb = tmem + uint32_t(it & 1) * 256u;
