@@ -106,6 +106,15 @@ __device__ __forceinline__ float tf32_hi(float x) {
     return __uint_as_float(r);
 }
 
+// (value bits with the low 5 bits replaced by j): one shift on the ALU pipe
+// and one integer multiply-add on the FMA pipe (m32 == 32 is passed at run
+// time so the compiler cannot fold the pair back into two ALU LOP3s).
+__device__ __forceinline__ uint32_t chunk_key(uint32_t r, uint32_t j, uint32_t m32) {
+    uint32_t k;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(k) : "r"(r >> 5), "r"(m32), "r"(j));
+    return k;
+}
+
 // byte offset of element (row, k) of a K-major interleaved operand
 __device__ __forceinline__ uint32_t il_off(uint32_t row, uint32_t k, uint32_t sbo) {
     return (row >> 3) * sbo + (k >> 2) * 128u + (row & 7u) * 16u + (k & 3u) * 4u;
@@ -374,8 +383,10 @@ __device__ __forceinline__ void load_row(const NearestArgs& a, uint64_t row, uin
     }
 }
 
-template <int DS, int KA>
-__global__ void __launch_bounds__(256, 1) umma_screen2_kernel(NearestArgs a, uint32_t n_pad) {
+template <int DS, int KA, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) umma_screen2_kernel(NearestArgs a, uint32_t n_pad,
+                                                                  uint32_t m32) {
+    constexpr int NPART = NW / 4;  // column parts (warp quads) per tile
     constexpr uint32_t SBO = (KA / 4) * 128;
     constexpr uint32_t ASTAGE = kRows * KA * 4;  // bytes of one A (hi or lo) stage
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -385,8 +396,8 @@ __global__ void __launch_bounds__(256, 1) umma_screen2_kernel(NearestArgs a, uin
     __shared__ uint64_t mbar[2];
     __shared__ uint32_t tmem_base;
     __shared__ float ebuf[2][kRows];
-    __shared__ uint64_t mK[kRows];
-    __shared__ uint32_t mV[kRows];
+    __shared__ uint64_t mK[NPART > 1 ? NPART - 1 : 1][kRows];
+    __shared__ uint32_t mV[NPART > 1 ? NPART - 1 : 1][kRows];
 
     const uint32_t tid = threadIdx.x, warp = tid >> 5;
     const uint32_t B = a.B;
@@ -397,7 +408,7 @@ __global__ void __launch_bounds__(256, 1) umma_screen2_kernel(NearestArgs a, uin
     const float* tab = a.table + uint64_t(b) * k * DS;
     const float cmax = a.cmax[b];
     const uint32_t row_l = tid & (kRows - 1);  // row of the tile this thread stages / reads
-    const uint32_t half = tid >> 7;             // K half it stages, column half it reduces
+    const uint32_t half = tid >> 7;             // K part it stages, column part it reduces
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
@@ -447,11 +458,10 @@ __global__ void __launch_bounds__(256, 1) umma_screen2_kernel(NearestArgs a, uin
         if (half == 0) ebuf[it & 1][row_l] = E;
         uint8_t* Ah = A0 + (it & 1) * 2 * ASTAGE;
         uint8_t* Al = Ah + ASTAGE;
-        constexpr int NCH = KA / 4;               // 16-byte chunks per row
-        constexpr int C0 = 0, C1 = (NCH + 1) / 2;  // this half's chunk range
+        constexpr int NCH = KA / 4;  // 16-byte chunks per row, dealt round-robin to the parts
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
-            if ((half == 0) != (c < C1)) continue;
+            if (uint32_t(c % NPART) != half) continue;
             float h[4], l[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -463,7 +473,6 @@ __global__ void __launch_bounds__(256, 1) umma_screen2_kernel(NearestArgs a, uin
             *reinterpret_cast<float4*>(Ah + il_off(row_l, 4 * c, SBO)) = make_float4(h[0], h[1], h[2], h[3]);
             *reinterpret_cast<float4*>(Al + il_off(row_l, 4 * c, SBO)) = make_float4(l[0], l[1], l[2], l[3]);
         }
-        (void)C0;
     };
     auto issue = [&](uint64_t it) {
         const uint32_t ah = smem_u32(A0 + (it & 1) * 2 * ASTAGE), al = ah + ASTAGE;
@@ -518,9 +527,10 @@ __global__ void __launch_bounds__(256, 1) umma_screen2_kernel(NearestArgs a, uin
 #pragma unroll
         for (int s4 = 0; s4 < 4; ++s4) { m1[s4] = 0xFFFFFFFFu; m2[s4] = 0xFFFFFFFFu; ch[s4] = 0; }
         const uint32_t lane_base = ((warp & 3u) * 32u) << 16;
-        const uint32_t ncols_half = (n_pad + 63) / 64 * 32;  // columns per half, whole 32-chunks
-        const uint32_t cbeg = half * ncols_half;
-        const uint32_t cend = min(n_pad, cbeg + ncols_half);
+        const uint32_t nchunks = (n_pad + 31) / 32;
+        const uint32_t per = (nchunks + NPART - 1) / NPART;  // 32-column chunks per part
+        const uint32_t cbeg = half * per * 32;
+        const uint32_t cend = min(n_pad, cbeg + per * 32);
         const uint32_t tb = tmem + uint32_t(it & 1) * 256u;
         for (uint32_t c0 = cbeg; c0 < cend; c0 += 32) {
             uint32_t r[32];
@@ -538,8 +548,8 @@ __global__ void __launch_bounds__(256, 1) umma_screen2_kernel(NearestArgs a, uin
 #pragma unroll
                 for (int s4 = 0; s4 < 4; ++s4) {
                     const int jj = j + 2 * s4;
-                    const uint32_t ka = (r[jj] & ~31u) | uint32_t(jj);
-                    const uint32_t kb = (r[jj + 1] & ~31u) | uint32_t(jj + 1);
+                    const uint32_t ka = chunk_key(r[jj], uint32_t(jj), m32);
+                    const uint32_t kb = chunk_key(r[jj + 1], uint32_t(jj + 1), m32);
                     const uint32_t lo = min(ka, kb), hi = max(ka, kb);
                     m2[s4] = min(min(m2[s4], max(m1[s4], lo)), hi);
                     m1[s4] = min(m1[s4], lo);
@@ -557,15 +567,18 @@ __global__ void __launch_bounds__(256, 1) umma_screen2_kernel(NearestArgs a, uin
             V2 = min(min(V2, m2[s4] & ~31u), uint32_t(max(K1, o) >> 32));
             K1 = min(K1, o);
         }
-        if (half == 1) {
-            mK[row_l] = K1;
-            mV[row_l] = V2;
+        if (half > 0) {
+            mK[half - 1][row_l] = K1;
+            mV[half - 1][row_l] = V2;
         }
         __syncthreads();
         if (half == 0) {
-            const uint64_t oK = mK[row_l];
-            V2 = min(min(V2, mV[row_l]), uint32_t(max(K1, oK) >> 32));
-            K1 = min(K1, oK);
+#pragma unroll
+            for (int p2 = 0; p2 < NPART - 1; ++p2) {
+                const uint64_t oK = mK[p2][row_l];
+                V2 = min(min(V2, mV[p2][row_l]), uint32_t(max(K1, oK) >> 32));
+                K1 = min(K1, oK);
+            }
             const uint64_t row = tile_of(it) * kRows + row_l;
             if (row < a.n) {
                 const uint32_t idx = uint32_t(K1);
@@ -605,18 +618,22 @@ template <int DS, int KA>
 void launch_umma2(pqg_ctx* ctx, const NearestArgs& a) {
     const uint32_t n_pad = uint32_t((a.k + 15) / 16 * 16);
     const size_t smem = size_t(2) * n_pad * KA * 4 + size_t(4) * kRows * KA * 4;
-    auto kern = umma_screen2_kernel<DS, KA>;
-    PQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    const int nw_env = std::getenv("PQG_UMMA_WARPS") ? std::atoi(std::getenv("PQG_UMMA_WARPS")) : 16;
     const uint64_t ntiles = (a.n + kRows - 1) / kRows;
     // one CTA per SM; each subspace gets floor(SMs / B) CTAs (at least 1)
     uint64_t per_b = std::max<uint64_t>(1, uint64_t(ctx->num_sms) / a.B);
     per_b = std::min<uint64_t>(per_b, ntiles);
-    launch(ctx, "nearest_tc", kern, dim3(unsigned(per_b * a.B)), dim3(256), smem, a, n_pad);
+    auto go = [&](auto kern, int nthreads) {
+        PQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        launch(ctx, "nearest_tc", kern, dim3(unsigned(per_b * a.B)), dim3(nthreads), smem, a, n_pad, 32u);
+    };
+    if (nw_env == 8) go(umma_screen2_kernel<DS, KA, 8>, 256);
+    else go(umma_screen2_kernel<DS, KA, 16>, 512);
 }
 
 template <int DS, int KA>
 void launch_umma(pqg_ctx* ctx, const NearestArgs& a) {
-    static const bool v1 = std::getenv("PQG_UMMA") && std::getenv("PQG_UMMA")[0] == '1';
+    const bool v1 = std::getenv("PQG_UMMA") && std::getenv("PQG_UMMA")[0] == '1';
     if (!v1) {
         launch_umma2<DS, KA>(ctx, a);
         return;

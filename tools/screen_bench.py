@@ -35,8 +35,10 @@ def main():
         os.environ["PQG_SCREEN"] = "fp32"
         L.check(lib.pqg_pq_fit(ctx.h, vp(train.data_ptr()), 100_000, D, M, ks, 3, 7, vp(t.data_ptr()), None, None))
         res = {}
-        for mode in ("fp32", "tc"):
-            os.environ["PQG_SCREEN"] = mode
+        for mode in ("fp32", "tc1", "tc8", "tc16"):
+            os.environ["PQG_SCREEN"] = "fp32" if mode == "fp32" else "tc"
+            os.environ["PQG_UMMA"] = "1" if mode == "tc1" else "0"
+            os.environ["PQG_UMMA_WARPS"] = "8" if mode == "tc8" else "16"
             codes = torch.empty((N, M), dtype=torch.uint8, device="cuda")
             enc = lambda: L.check(lib.pqg_pq_encode(ctx.h, vp(x.data_ptr()), N, M, ks, D // M,
                                                      vp(t.data_ptr()), vp(codes.data_ptr())))
@@ -51,19 +53,19 @@ def main():
             b.record(s)
             torch.cuda.synchronize()
             ms = a.elapsed_time(b) / 10
-            kname = "nearest_tc" if mode == "tc" else "nearest"
+            kname = "nearest" if mode == "fp32" else "nearest_tc"
             n1, k1 = ctx.profile_read(kname)
             n2, k2 = ctx.profile_read("fixup")
             ctx.profile(False)
             res[mode] = codes.cpu().numpy()
             print(f"M={M:2d} Ks={ks:3d} {mode:4s}: {ms:7.3f} ms/encode  {N/ms/1e6:8.2f} Mvec/s  "
                   f"screen {k1/max(n1,1):.3f} ms  fixup {k2/max(n2,1):.3f} ms", flush=True)
-        same = np.array_equal(res["fp32"], res["tc"])
+        same = all(np.array_equal(res["fp32"], res[m]) for m in ("tc1", "tc8", "tc16"))
         ref = orc.pq_encode(xh[sel], t.cpu().numpy())
-        ok = np.array_equal(res["tc"][sel], ref)
+        ok = np.array_equal(res["tc16"][sel], ref)
         print(f"   codes tc==fp32: {same}  tc==oracle(sample): {ok}", flush=True)
         if not same:
-            diff = np.argwhere(res["fp32"] != res["tc"])
+            diff = np.argwhere(res["fp32"] != res["tc16"])
             print("   first diffs", diff[:5].tolist(), flush=True)
 
 
