@@ -298,7 +298,11 @@ def run_ours(args, rank, world, local):
     with ClockSampler(local) as clk:
         ctx.profile(True)
         ms = timed(lambda: encode(tables, HEAD_M, HEAD_KS, codes), args.steps, args.warmup)
-        n_near, near_ms = ctx.profile_read("nearest")
+        n_near, near_ms = ctx.profile_read("nearest_tc")
+        screen_kernel = "umma_screen (tcgen05 3xTF32, TMEM accumulator)"
+        if n_near == 0:
+            n_near, near_ms = ctx.profile_read("nearest")
+            screen_kernel = "nearest_kernel (FP32 FFMA screen)"
         n_fix, fix_ms = ctx.profile_read("fixup")
         n_norm, norm_ms = ctx.profile_read("norms")
         ctx.profile(False)
@@ -399,7 +403,7 @@ def run_ours(args, rank, world, local):
         "sweep": sweep,
         "roofline": {"bound": "fp32", "achieved": achieved_tflops, "peak": fp32_peak,
                      "unit": "TFLOP/s", "frac": achieved_tflops / fp32_peak, "traffic": traffic,
-                     "kernel": "nearest_kernel<TN=8,DP=16> (encode screen)",
+                     "kernel": screen_kernel,
                      "algorithmic": "2*Ks*D = 65536 flop per vector x 1M vectors per launch",
                      "peak_source": "measured: register-operand FFMA probe (pqg_fp32_probe) on this GPU",
                      "fp32_nominal_tflops": fp32_nominal,

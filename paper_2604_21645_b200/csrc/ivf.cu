@@ -213,7 +213,7 @@ struct CodeRow {
     }
 };
 
-template <int RB, int W>
+template <int RB, int W, int KS>
 __global__ void __launch_bounds__(kScanThreads) adc_scan_kernel(
     const float* tables, uint32_t M, uint32_t ks, uint32_t ds, const float* queries,
     const uint64_t* offsets, const uint64_t* ids, const uint8_t* codes, const uint32_t* probes,
@@ -251,22 +251,29 @@ __global__ void __launch_bounds__(kScanThreads) adc_scan_kernel(
                 float s32 = 0.f;
                 bool bad = false;
                 if constexpr (RB > 0) {
-                    const bool check = W == 2 || ks < 256;
+                    const uint32_t ksc = KS > 0 ? uint32_t(KS) : ks;
+                    const bool check = KS == 0 && (W == 2 || ks < 256);
                     CodeRow<RB> row;
                     row.load(cr);
                     constexpr int MM = RB / W;
+                    float s_even = 0.f, s_odd = 0.f;  // two chains: half the FADD latency
 #pragma unroll
                     for (int m = 0; m < MM; ++m) {
-                        const uint32_t c = row.template get<W>(m);
-                        if (check && c >= ks) bad = true;
-                        s32 += lut[m * ks + min(c, ks - 1)];
+                        uint32_t c = row.template get<W>(m);
+                        if (check) {
+                            if (c >= ks) bad = true;
+                            c = min(c, ks - 1);
+                        }
+                        if (m & 1) s_odd += lut[m * ksc + c];
+                        else s_even += lut[m * ksc + c];
                     }
+                    s32 = s_even + s_odd;
                     if (!bad) {
                         const double lower = double(s32) * double(shrink);
                         if (lower <= th && !(has_max && lower > max_sq)) {
 #pragma unroll
                             for (int m = 0; m < MM; ++m)
-                                s64 = __dadd_rn(s64, (double)lut[m * ks + row.template get<W>(m)]);
+                                s64 = __dadd_rn(s64, (double)lut[m * ksc + row.template get<W>(m)]);
                             id = ids[e];
                             want = !(has_max && s64 > max_sq);
                         }
@@ -484,13 +491,14 @@ void ivf_scan(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t 
     };
     // vector code loads need rb-aligned rows (CSR rows are rb apart from an aligned base)
     const bool aligned = (reinterpret_cast<uintptr_t>(ix.codes) % (rb >= 16 ? 16 : rb)) == 0;
-    if (aligned && ix.w == 1 && rb == 16) run(adc_scan_kernel<16, 1>);
-    else if (aligned && ix.w == 1 && rb == 8) run(adc_scan_kernel<8, 1>);
-    else if (aligned && ix.w == 1 && rb == 32) run(adc_scan_kernel<32, 1>);
-    else if (aligned && ix.w == 1 && rb == 4) run(adc_scan_kernel<4, 1>);
-    else if (aligned && ix.w == 2 && rb == 16) run(adc_scan_kernel<16, 2>);
-    else if (aligned && ix.w == 2 && rb == 8) run(adc_scan_kernel<8, 2>);
-    else run(adc_scan_kernel<0, 1>);
+    const bool k256 = ix.ks == 256;
+    if (aligned && ix.w == 1 && rb == 16) k256 ? run(adc_scan_kernel<16, 1, 256>) : run(adc_scan_kernel<16, 1, 0>);
+    else if (aligned && ix.w == 1 && rb == 8) k256 ? run(adc_scan_kernel<8, 1, 256>) : run(adc_scan_kernel<8, 1, 0>);
+    else if (aligned && ix.w == 1 && rb == 32) k256 ? run(adc_scan_kernel<32, 1, 256>) : run(adc_scan_kernel<32, 1, 0>);
+    else if (aligned && ix.w == 1 && rb == 4) run(adc_scan_kernel<4, 1, 0>);
+    else if (aligned && ix.w == 2 && rb == 16) run(adc_scan_kernel<16, 2, 0>);
+    else if (aligned && ix.w == 2 && rb == 8) run(adc_scan_kernel<8, 2, 0>);
+    else run(adc_scan_kernel<0, 1, 0>);
 }
 
 void csr_scatter(pqg_ctx* ctx, const uint32_t* perm, uint64_t n, const uint64_t* ids,

@@ -148,7 +148,7 @@ __device__ __forceinline__ float tc_error_bound(float S, int K) {
 
 template <int DS, int KA>
 __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, uint32_t n_pad,
-                                                               uint32_t tmem_cols, uint32_t tiles_per_cta) {
+                                                               uint32_t tmem_cols, uint32_t m32) {
     static_assert(KA % 8 == 0 && KA >= DS + 2, "augmented K");
     constexpr uint32_t SBO = (KA / 4) * 128;  // bytes between 8-row groups
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -295,8 +295,8 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
 #pragma unroll
                 for (int s4 = 0; s4 < 4; ++s4) {
                     const int jj = j + 2 * s4;
-                    const uint32_t ka = (r[jj] & ~31u) | uint32_t(jj);
-                    const uint32_t kb = (r[jj + 1] & ~31u) | uint32_t(jj + 1);
+                    const uint32_t ka = chunk_key(r[jj], uint32_t(jj), m32);
+                    const uint32_t kb = chunk_key(r[jj + 1], uint32_t(jj + 1), m32);
                     const uint32_t lo = min(ka, kb), hi = max(ka, kb);
                     m2[s4] = min(min(m2[s4], max(m1[s4], lo)), hi);
                     m1[s4] = min(m1[s4], lo);
@@ -346,7 +346,6 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
         fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(tmem_cols));
     }
-    (void)tiles_per_cta;
 }
 
 // ---------------------------------------------------------------------------
@@ -618,7 +617,7 @@ template <int DS, int KA>
 void launch_umma2(pqg_ctx* ctx, const NearestArgs& a) {
     const uint32_t n_pad = uint32_t((a.k + 15) / 16 * 16);
     const size_t smem = size_t(2) * n_pad * KA * 4 + size_t(4) * kRows * KA * 4;
-    const int nw_env = std::getenv("PQG_UMMA_WARPS") ? std::atoi(std::getenv("PQG_UMMA_WARPS")) : 16;
+    const int nw_env = std::getenv("PQG_UMMA_WARPS") ? std::atoi(std::getenv("PQG_UMMA_WARPS")) : 8;
     const uint64_t ntiles = (a.n + kRows - 1) / kRows;
     // one CTA per SM; each subspace gets floor(SMs / B) CTAs (at least 1)
     uint64_t per_b = std::max<uint64_t>(1, uint64_t(ctx->num_sms) / a.B);
@@ -633,7 +632,13 @@ void launch_umma2(pqg_ctx* ctx, const NearestArgs& a) {
 
 template <int DS, int KA>
 void launch_umma(pqg_ctx* ctx, const NearestArgs& a) {
-    const bool v1 = std::getenv("PQG_UMMA") && std::getenv("PQG_UMMA")[0] == '1';
+    // measured (tools/screen_bench.py, r1): the synchronous 2-CTA/SM kernel wins
+    // for narrow tables and Ds=16/Ks=256; the pipelined 8-warp kernel otherwise
+    const char* env = std::getenv("PQG_UMMA");
+    const uint32_t n_pad_sel = uint32_t((a.k + 15) / 16 * 16);
+    bool v1 = n_pad_sel <= 128 || (DS == 16 && n_pad_sel == 256);
+    if (env && env[0] == '1') v1 = true;
+    if (env && env[0] == '2') v1 = false;
     if (!v1) {
         launch_umma2<DS, KA>(ctx, a);
         return;
@@ -648,8 +653,7 @@ void launch_umma(pqg_ctx* ctx, const NearestArgs& a) {
     // persistent: ~2 CTAs per SM in total, each problem gets its share
     uint64_t per_b = std::max<uint64_t>(1, (uint64_t(ctx->num_sms) * 2 + a.B - 1) / a.B);
     per_b = std::min<uint64_t>(per_b, ntiles);
-    launch(ctx, "nearest_tc", kern, dim3(unsigned(per_b * a.B)), dim3(kRows), smem, a, n_pad, cols,
-           uint32_t((ntiles + per_b - 1) / per_b));
+    launch(ctx, "nearest_tc", kern, dim3(unsigned(per_b * a.B)), dim3(kRows), smem, a, n_pad, cols, 32u);
 }
 
 }  // namespace
