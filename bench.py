@@ -320,7 +320,7 @@ def run_ours(args, rank, world, local):
     probe = C.c_double()
     L.check(lib.pqg_fp32_probe(ctx.h, C.byref(probe)), "fp32_probe")
     fp32_peak = float(probe.value)
-    traffic = ncu_traffic("prof_nearest")
+    traffic = ncu_traffic("prof_umma")
 
     # ---- e2e through the C ABI with pinned host buffers
     xh = torch.from_numpy(x_host).pin_memory()
