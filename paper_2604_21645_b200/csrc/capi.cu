@@ -298,7 +298,9 @@ static KMeansOut run_kmeans(pqg_ctx* ctx, const float* x, uint64_t n, uint64_t l
     src.x = x;
     src.ldx = ldx;
     src.col_stride = col_stride;
+    const auto iter_mark = ctx->arena.mark();
     for (uint32_t it = 1; it <= max_iters; ++it) {
+        ctx->arena.reset_to(iter_mark);  // per-iteration scratch is reused
         table_norms(ctx, table, B, k, d, cnorm, cmax);
         NearestArgs a;
         a.src = src;
@@ -341,7 +343,9 @@ static void encode_dev(pqg_ctx* ctx, const float* x, uint64_t n, uint32_t M, uin
     const uint64_t D = uint64_t(M) * ds;
     const uint32_t w = code_width(ks);
     const uint64_t chunk = std::max<uint64_t>(1, (uint64_t(64) << 20) / M);
+    const auto chunk_mark = ctx->arena.mark();
     for (uint64_t r0 = 0; r0 < n; r0 += chunk) {
+        ctx->arena.reset_to(chunk_mark);
         const uint64_t nc = std::min(chunk, n - r0);
         NearestArgs a;
         a.src.x = x + r0 * D;

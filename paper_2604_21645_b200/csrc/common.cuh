@@ -93,6 +93,14 @@ struct Arena {
         if (used_total > peak_total) peak_total = used_total;
         return p;
     }
+    // Stream-ordered reuse inside one call: everything allocated after mark()
+    // is handed out again after reset_to(mark) (later kernels on the same
+    // stream run after the earlier ones finished with it).
+    std::pair<size_t, size_t> mark() const { return {cur_block, cur_off}; }
+    void reset_to(std::pair<size_t, size_t> m) {
+        cur_block = m.first;
+        cur_off = m.second;
+    }
     // Called when the outermost scope closes: rewind; consolidate fragments.
     void rewind() {
         cur_block = 0;

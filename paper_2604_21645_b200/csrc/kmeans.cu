@@ -254,11 +254,28 @@ __global__ void final_parts_kernel(const double* parts, uint32_t nparts, double*
     if (threadIdx.x == 0) out[b] = s;
 }
 
-// ---- ordered fp64 sums -> means -----------------------------------------
-__global__ void mean_kernel(const float* x, uint64_t ldx, uint32_t col_stride, uint64_t n,
-                            uint32_t B, uint32_t d, uint64_t k, const uint64_t* offsets,
-                            const uint32_t* perm, float* table, int* has_empty,
-                            const int* active) {
+// ---- ordered fp64 sums -> means (rows gathered into member order first)
+// Rows gathered into member order (problem b's column block only), so the
+// ordered sums below stream contiguous memory instead of chasing indices.
+__global__ void gather_sorted_kernel(const float* x, uint64_t ldx, uint32_t col_stride, uint64_t n,
+                                     uint32_t B, uint32_t d, const uint32_t* perm, float* sorted,
+                                     const int* active) {
+    const uint64_t total = uint64_t(B) * n * d;
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t bp = e / d, t = e - bp * d;
+        const uint64_t b = bp / n;
+        if (active && !active[b]) continue;
+        sorted[e] = __ldg(x + uint64_t(__ldg(perm + bp)) * ldx + b * col_stride + t);
+    }
+}
+
+// One thread per (problem, cluster, dim): sequential fp64 sum over the
+// cluster's members (ascending row order, contiguous in `sorted`), then
+// float(sum * (1/count)).  Loads are issued 16 ahead of the dependent adds.
+__global__ void mean_sorted_kernel(const float* sorted, uint64_t n, uint32_t B, uint32_t d,
+                                   uint64_t k, const uint64_t* offsets, float* table,
+                                   int* has_empty, const int* active) {
     const uint64_t total = uint64_t(B) * k * d;
     for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
          e += uint64_t(gridDim.x) * blockDim.x) {
@@ -271,25 +288,18 @@ __global__ void mean_kernel(const float* x, uint64_t ldx, uint32_t col_stride, u
             has_empty[b] = 1;
             continue;
         }
-        const uint32_t* mem = perm + b * n;
-        const float* xc = x + b * col_stride + t;
-        // members in ascending row order; 16 independent gathers in flight,
-        // then the adds in the reference's order
+        const float* src = sorted + (b * n) * d + t;
         double s = 0.0;
-        for (uint64_t m = beg; m < end; m += 16) {
-            const uint64_t cnt = min64(16, end - m);
-            uint32_t idx[16];
+        uint64_t m = beg;
+        for (; m + 16 <= end; m += 16) {
             float v[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) idx[j] = j < int(cnt) ? __ldg(mem + m + j) : 0u;
+            for (int j = 0; j < 16; ++j) v[j] = __ldg(src + (m + j) * d);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = j < int(cnt) ? __ldg(xc + uint64_t(idx[j]) * ldx) : 0.f;
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (j < int(cnt)) s = __dadd_rn(s, (double)v[j]);
+            for (int j = 0; j < 16; ++j) s = __dadd_rn(s, (double)v[j]);
         }
-        const double inv = __ddiv_rn(1.0, (double)(end - beg));
-        table[e] = __double2float_rn(__dmul_rn(s, inv));
+        for (; m < end; ++m) s = __dadd_rn(s, (double)__ldg(src + m * d));
+        table[e] = __double2float_rn(__dmul_rn(s, __ddiv_rn(1.0, (double)(end - beg))));
     }
 }
 
@@ -421,9 +431,12 @@ void kmeans_update(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint
     int* has_empty = scratch<int>(ctx, B);
     PQG_CUDA(cudaMemsetAsync(has_empty, 0, sizeof(int) * B, ctx->stream));
     const uint64_t total = uint64_t(B) * k * d;
-    launch(ctx, "kmeans_sum", mean_kernel, dim3(grid1d(total, 128, 1u << 20)), dim3(128), 0,
-           src.x, src.ldx, src.col_stride, n, B, d, k, (const uint64_t*)bk.offsets,
-           (const uint32_t*)bk.perm, table, has_empty, active);
+    float* sorted = scratch<float>(ctx, uint64_t(B) * n * d);
+    launch(ctx, "kmeans_sum", gather_sorted_kernel, dim3(grid1d(uint64_t(B) * n * d, 256, ctx->num_sms * 64)),
+           dim3(256), 0, src.x, src.ldx, src.col_stride, n, B, d, (const uint32_t*)bk.perm, sorted,
+           active);
+    launch(ctx, "kmeans_sum", mean_sorted_kernel, dim3(grid1d(total, 128, 1u << 20)), dim3(128), 0,
+           (const float*)sorted, n, B, d, k, (const uint64_t*)bk.offsets, table, has_empty, active);
     launch(ctx, "reseed", reseed_kernel, dim3(B), dim3(1024), 0, src.x, src.ldx, src.col_stride, n,
            d, k, (const uint64_t*)bk.offsets, dist, table, (const int*)has_empty, active);
 }
