@@ -55,6 +55,9 @@ void distance_matrix(pqg_ctx* ctx, NearestArgs a);   // fp32 screen values only
 // umma.cu (tcgen05 3xTF32 screen for PQ subspaces)
 bool umma_screen_supported(const NearestArgs& a);
 void umma_screen(pqg_ctx* ctx, const NearestArgs& a);
+// umma_big.cu (tcgen05 GEMM-argmin / screen matrix for the coarse quantizer)
+bool umma_big_supported(const NearestArgs& a);
+void umma_big(pqg_ctx* ctx, const NearestArgs& a);
 
 // kmeans.cu
 struct Bucketing {

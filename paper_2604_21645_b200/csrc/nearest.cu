@@ -468,12 +468,19 @@ void nearest(pqg_ctx* ctx, NearestArgs a) {
     const char* mode = std::getenv("PQG_SCREEN");
     const bool force_fp32 = mode && std::strcmp(mode, "fp32") == 0;
     if (!force_fp32 && umma_screen_supported(a)) umma_screen(ctx, a);
+    else if (!force_fp32 && umma_big_supported(a)) umma_big(ctx, a);
     else dispatch<false>(ctx, a);
     launch(ctx, "fixup", fixup_kernel, dim3(ctx->num_sms * 4), dim3(32 * kFixWarps), 0, a);
 }
 
 void distance_matrix(pqg_ctx* ctx, NearestArgs a) {
     if (a.n == 0) return;
+    const char* mode = std::getenv("PQG_SCREEN");
+    const bool force_fp32 = mode && std::strcmp(mode, "fp32") == 0;
+    if (!force_fp32 && umma_big_supported(a)) {
+        umma_big(ctx, a);
+        return;
+    }
     dispatch<true>(ctx, a);
 }
 

@@ -1,0 +1,442 @@
+// umma_big.cu -- tcgen05 GEMM-argmin for the coarse quantizer: many rows
+// against many centroids in full dimension (assign_items / probe_order /
+// coarse kmeans_fit: proj/src/ivf.cpp:36-49, :91-101, proj/src/kmeans.cpp:46-57),
+// e.g. 1M x 128 rows against nlist = 1024..16384 centroids.
+//
+// Operands are prepared once per call in global memory, already split into
+// TF32 hi/lo halves and laid out in the canonical K-major no-swizzle UMMA
+// layout, so the main kernel only moves bytes:
+//   A (rows)      : [row tile of 128][K chunk of 32][hi|lo][16 KB]
+//   B (centroids) : [N block of 256][K chunk of 32][hi|lo][32 KB]
+// with the augmented rows A_r = [x_r, 1, C_r, 0..], B_j = [-2c_j, ||c_j||^2, 1, 0..]
+// (see umma.cu), so the MMA accumulates the screened value directly.
+//
+// Main kernel: persistent, one CTA per SM, 6 warps.
+//   warp 0     producer: cp.async.bulk of the A and B chunks of each
+//              (row tile, N block, K chunk) into a 2-stage smem ring
+//              (mbarrier complete_tx)
+//   warp 1     MMA issuer: 4 k-steps x 3 (3xTF32) tcgen05.mma per chunk into
+//              one of two TMEM accumulators (128 x 256 fp32 each)
+//   warps 2-5  epilogue: thread = row = TMEM lane; tcgen05.ld 32 columns at a
+//              time; keep the 4 smallest (value, column) per row across all N
+//              blocks; at the end of the row tile resolve the winner:
+//              every centroid within 2E of the best is among the top 4 unless
+//              the 4th is itself inside the band, so <= 3 candidates are
+//              re-scored in the reference's exact fp64 arithmetic in-kernel
+//              and only rows with >= 4 candidates in the band go to the
+//              global fixup.  MAT mode instead writes the screened matrix.
+#include <cstdlib>
+
+#include "kernels.cuh"
+
+namespace pqg {
+
+namespace {
+
+constexpr int kR = 128;             // rows per tile (MMA M)
+constexpr int kN = 256;             // centroids per N block (MMA N)
+constexpr int kKC = 32;             // K elements per chunk
+constexpr uint32_t kSBO = (kKC / 4) * 128;  // 1024 B between 8-row groups
+constexpr uint32_t kAChunk = kR * kKC * 4;   // 16 KB per half
+constexpr uint32_t kBChunk = kN * kKC * 4;   // 32 KB per half
+constexpr uint32_t kStage = 2 * kAChunk + 2 * kBChunk;  // 96 KB
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
+           (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46);
+}
+__host__ __device__ constexpr uint32_t idesc_tf32(uint32_t M, uint32_t N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
+                 :: "r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 :: "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bar_init(uint64_t* bar, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile("{\n\t.reg .pred done;\nW_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+                 "@!done bra W_%=;\n\t}\n" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+          "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+          "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ float tf32_hi(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+__device__ __forceinline__ uint32_t il_off(uint32_t row, uint32_t k) {  // within one K chunk
+    return (row >> 3) * kSBO + (k >> 2) * 128u + (row & 7u) * 16u + (k & 3u) * 4u;
+}
+
+__device__ __forceinline__ float row_x(const RowSrc& s, uint64_t i, uint32_t t) {
+    if (s.codes) {
+        const uint32_t m = t / s.dds, tt = t - m * s.dds;
+        const uint8_t* p = s.codes + (i * s.dM + m) * s.dw;
+        uint32_t code = s.dw == 1 ? uint32_t(p[0]) : (uint32_t(p[0]) | (uint32_t(p[1]) << 8));
+        if (code >= s.dks) code = s.dks - 1;
+        return __ldg(s.dtab + ((uint64_t)m * s.dks + code) * s.dds + tt);
+    }
+    return __ldg(s.x + i * s.ldx + t);
+}
+
+// E bound of the 3xTF32 screen (see umma.cu tc_error_bound): 2 ulps of the
+// accumulator magnitude per MMA instruction plus split residuals, doubled.
+__device__ __forceinline__ float big_error_bound(float S, uint32_t kchunks) {
+    const float n_mma = float(3 * 4 * kchunks);
+    return 2.f * (2.f * n_mma + 8.f) * kU * S + 1e-30f;
+}
+
+// ---- operand preparation ---------------------------------------------------
+// One thread per row: A_r = [x_r, 1, C_r, 0...], split hi/lo, interleaved.
+__global__ void split_rows_kernel(RowSrc src, uint64_t n, uint32_t d, uint32_t kchunks,
+                                  const float* cmax_p, uint8_t* A, float* Erow) {
+    const float cmax = *cmax_p;
+    for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < (n + kR - 1) / kR * kR;
+         r += uint64_t(gridDim.x) * blockDim.x) {
+        const bool valid = r < n;
+        float nx = 0.f;
+        if (valid)
+            for (uint32_t t = 0; t < d; ++t) {
+                const float v = row_x(src, r, t);
+                nx = fmaf(v, v, nx);
+            }
+        const float q = sqrtf(nx) * (1.f + 1e-6f) + cmax;
+        const float S = q * q * 1.01f + 1e-6f;
+        const float E = big_error_bound(S, kchunks);
+        const float C = nx * (1.f + 2.f * float(d + 2) * kU) + 2.f * E;
+        if (valid) Erow[r] = E;
+        const uint64_t tile = r / kR;
+        const uint32_t rl = uint32_t(r % kR);
+        for (uint32_t kc = 0; kc < kchunks; ++kc) {
+            uint8_t* blk = A + (tile * kchunks + kc) * (2 * kAChunk);
+            for (uint32_t k4 = 0; k4 < kKC; k4 += 4) {
+                float h[4], l[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t t = kc * kKC + k4 + u;
+                    float v = 0.f;
+                    if (valid) v = t < d ? row_x(src, r, t) : (t == d ? 1.f : (t == d + 1 ? C : 0.f));
+                    h[u] = tf32_hi(v);
+                    l[u] = tf32_hi(v - h[u]);
+                }
+                *reinterpret_cast<float4*>(blk + il_off(rl, k4)) = make_float4(h[0], h[1], h[2], h[3]);
+                *reinterpret_cast<float4*>(blk + kAChunk + il_off(rl, k4)) = make_float4(l[0], l[1], l[2], l[3]);
+            }
+        }
+    }
+}
+
+// One thread per centroid: B_j = [-2c_j, ||c_j||^2, 1, 0...]; padded rows never win.
+__global__ void split_table_kernel(const float* table, const float* cnorm, uint64_t k, uint32_t d,
+                                   uint32_t kchunks, uint64_t k_pad, uint8_t* Bm) {
+    for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < k_pad;
+         j += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t nb = j / kN;
+        const uint32_t jl = uint32_t(j % kN);
+        for (uint32_t kc = 0; kc < kchunks; ++kc) {
+            uint8_t* blk = Bm + (nb * kchunks + kc) * (2 * kBChunk);
+            for (uint32_t k4 = 0; k4 < kKC; k4 += 4) {
+                float h[4], l[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t t = kc * kKC + k4 + u;
+                    float v = 0.f;
+                    if (j < k) {
+                        if (t < d) v = -2.f * __ldg(table + j * d + t);
+                        else if (t == d) v = __ldg(cnorm + j);
+                        else if (t == d + 1) v = 1.f;
+                    } else if (t == d) {
+                        v = 3.0e38f;
+                    }
+                    h[u] = tf32_hi(v);
+                    l[u] = tf32_hi(v - h[u]);
+                }
+                *reinterpret_cast<float4*>(blk + il_off(jl, k4)) = make_float4(h[0], h[1], h[2], h[3]);
+                *reinterpret_cast<float4*>(blk + kBChunk + il_off(jl, k4)) = make_float4(l[0], l[1], l[2], l[3]);
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void store_index(const NearestArgs& a, uint64_t i, uint32_t idx) {
+    const uint64_t off = i * a.idx_rs;
+    if (a.idx_bytes == 1) static_cast<uint8_t*>(a.out_idx)[off] = uint8_t(idx);
+    else if (a.idx_bytes == 2) {
+        uint8_t* p = static_cast<uint8_t*>(a.out_idx) + off * 2;
+        p[0] = uint8_t(idx & 0xff);
+        p[1] = uint8_t(idx >> 8);
+    } else static_cast<uint32_t*>(a.out_idx)[off] = idx;
+}
+
+__device__ __forceinline__ double exact_row_dist(const NearestArgs& a, uint64_t row, uint32_t j) {
+    const float* c = a.table + uint64_t(j) * a.d;
+    double acc = 0.0;
+    for (uint32_t t = 0; t < a.d; ++t) {
+        const double diff = __dsub_rn((double)row_x(a.src, row, t), (double)__ldg(c + t));
+        acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+    }
+    return acc;
+}
+
+// ---- main kernel -----------------------------------------------------------
+template <bool MAT>
+__global__ void __launch_bounds__(192, 1) big_kernel(NearestArgs a, const uint8_t* __restrict__ A,
+                                                     const uint8_t* __restrict__ Bm,
+                                                     const float* __restrict__ Erow,
+                                                     uint32_t kchunks, uint32_t nblocks,
+                                                     uint64_t row_base) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t full[2], empty[2], tfull[2], tempty[2];
+    __shared__ uint32_t tmem_base;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t ntiles = (a.n + kR - 1) / kR;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"(smem_u32(&tmem_base)), "r"(512u));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (threadIdx.x == 32) {
+        for (int s = 0; s < 2; ++s) {
+            bar_init(&full[s], 1);
+            bar_init(&empty[s], 1);
+            bar_init(&tfull[s], 1);
+            bar_init(&tempty[s], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = tmem_base;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            uint32_t q = 0;
+            for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                for (uint32_t nb = 0; nb < nblocks; ++nb) {
+                    for (uint32_t kc = 0; kc < kchunks; ++kc, ++q) {
+                        const uint32_t s = q & 1, ph = (q >> 1) & 1;
+                        bar_wait(&empty[s], ph ^ 1);
+                        uint8_t* st = smem + s * kStage;
+                        bar_expect_tx(&full[s], kStage);
+                        bulk_g2s(st, A + (tile * kchunks + kc) * (2 * kAChunk), 2 * kAChunk, &full[s]);
+                        bulk_g2s(st + 2 * kAChunk, Bm + (uint64_t(nb) * kchunks + kc) * (2 * kBChunk),
+                                 2 * kBChunk, &full[s]);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            const uint32_t idesc = idesc_tf32(kR, kN);
+            uint32_t q = 0, u = 0;
+            for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                for (uint32_t nb = 0; nb < nblocks; ++nb, ++u) {
+                    const uint32_t buf = u & 1, tph = (u >> 1) & 1;
+                    bar_wait(&tempty[buf], tph ^ 1);
+                    fence_after();
+                    const uint32_t d_tmem = tmem + buf * 256u;
+                    for (uint32_t kc = 0; kc < kchunks; ++kc, ++q) {
+                        const uint32_t s = q & 1, ph = (q >> 1) & 1;
+                        bar_wait(&full[s], ph);
+                        fence_after();
+                        const uint32_t base = smem_u32(smem + s * kStage);
+                        const uint32_t ah = base, al = base + kAChunk;
+                        const uint32_t bh = base + 2 * kAChunk, bl = bh + kBChunk;
+#pragma unroll
+                        for (int k4 = 0; k4 < kKC / 8; ++k4) {
+                            const uint32_t ko = k4 * 256;
+                            const uint64_t dah = make_desc(ah + ko, 128, kSBO);
+                            const uint64_t dal = make_desc(al + ko, 128, kSBO);
+                            const uint64_t dbh = make_desc(bh + ko, 128, kSBO);
+                            const uint64_t dbl = make_desc(bl + ko, 128, kSBO);
+                            mma_tf32(d_tmem, dah, dbh, idesc, (kc | k4) != 0);
+                            mma_tf32(d_tmem, dah, dbl, idesc, 1);
+                            mma_tf32(d_tmem, dal, dbh, idesc, 1);
+                        }
+                        commit(&empty[s]);  // smem stage free once these MMAs are done
+                    }
+                    commit(&tfull[buf]);  // accumulator ready for the epilogue
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue
+        const uint32_t quarter = warp & 3u;  // TMEM lane quarter of this warp
+        const uint32_t rl = quarter * 32 + lane;
+        const uint32_t lane_base = (quarter * 32u) << 16;
+        uint32_t u = 0;
+        for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const uint64_t row = tile * kR + rl;
+            float tv[4];
+            uint32_t ti[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) { tv[i] = __int_as_float(0x7f800000); ti[i] = 0xFFFFFFFFu; }
+            for (uint32_t nb = 0; nb < nblocks; ++nb, ++u) {
+                const uint32_t buf = u & 1, tph = (u >> 1) & 1;
+                bar_wait(&tfull[buf], tph);
+                fence_after();
+                const uint32_t tb = tmem + buf * 256u + lane_base;
+                for (uint32_t c0 = 0; c0 < uint32_t(kN); c0 += 32) {
+                    uint32_t r[32];
+                    tmem_ld32(tb + c0, r);
+                    tmem_wait_ld();
+                    const uint32_t col0 = nb * kN + c0;
+                    if constexpr (MAT) {
+                        if (row < a.n) {
+                            float* o = a.out_mat + row * a.ld_mat + col0;
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                if (col0 + j < a.k) o[j] = __uint_as_float(r[j]);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const float v = __uint_as_float(r[j]);
+                            if (v < tv[3]) {  // rare after the first columns
+                                const uint32_t c = col0 + j;
+                                if (v < tv[2]) {
+                                    tv[3] = tv[2]; ti[3] = ti[2];
+                                    if (v < tv[1]) {
+                                        tv[2] = tv[1]; ti[2] = ti[1];
+                                        if (v < tv[0]) {
+                                            tv[1] = tv[0]; ti[1] = ti[0];
+                                            tv[0] = v; ti[0] = c;
+                                        } else { tv[1] = v; ti[1] = c; }
+                                    } else { tv[2] = v; ti[2] = c; }
+                                } else { tv[3] = v; ti[3] = c; }
+                            }
+                        }
+                    }
+                }
+                fence_before();
+                __syncwarp();
+                if (lane == 0) bar_arrive(&tempty[buf]);
+            }
+            if constexpr (!MAT) {
+                if (row < a.n) {
+                    const float E = Erow[row];
+                    const float band = tv[0] + 2.05f * E;
+                    if (tv[3] > band * (1.f + 4.f * kU)) {
+                        // all possible fp64 winners are among the top 3: re-score exactly
+                        double best = __longlong_as_double(0x7ff0000000000000LL);
+                        uint32_t bj = 0xFFFFFFFFu;
+                        for (int i = 0; i < 3; ++i) {
+                            if (ti[i] == 0xFFFFFFFFu || !(tv[i] <= band * (1.f + 4.f * kU))) continue;
+                            const double dd = exact_row_dist(a, row, ti[i]);
+                            if (dd < best || (dd == best && ti[i] < bj)) { best = dd; bj = ti[i]; }
+                        }
+                        if (bj != 0xFFFFFFFFu) {
+                            store_index(a, row, bj);
+                            if (a.out_dist) a.out_dist[row] = best;
+                        } else {
+                            const unsigned long long slot = atomicAdd(a.flag_count, 1ull);
+                            a.flags[slot] = row_base + row;
+                        }
+                    } else {
+                        const unsigned long long slot = atomicAdd(a.flag_count, 1ull);
+                        a.flags[slot] = row_base + row;
+                    }
+                }
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(512u));
+    }
+}
+
+bool umma_big_supported_impl(const NearestArgs& a) {
+    if (a.B != 1 || a.active) return false;  // single problem (coarse) only
+    if (a.d < 24) return false;              // small d: the PQ kernels
+    if (a.k < 64) return false;
+    return true;
+}
+
+}  // namespace
+
+bool umma_big_supported(const NearestArgs& a) { return umma_big_supported_impl(a); }
+
+void umma_big(pqg_ctx* ctx, const NearestArgs& a0) {
+    const uint32_t kchunks = (a0.d + 2 + kKC - 1) / kKC;
+    const uint32_t nblocks = uint32_t((a0.k + kN - 1) / kN);
+    const uint64_t k_pad = uint64_t(nblocks) * kN;
+    uint8_t* Bm = scratch<uint8_t>(ctx, uint64_t(nblocks) * kchunks * 2 * kBChunk);
+    launch(ctx, "big_split", split_table_kernel, dim3(grid1d(k_pad, 128, 4096)), dim3(128), 0,
+           a0.table, a0.cnorm, a0.k, a0.d, kchunks, k_pad, Bm);
+    const size_t smem = 2 * size_t(kStage);
+    PQG_CUDA(cudaFuncSetAttribute(big_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    PQG_CUDA(cudaFuncSetAttribute(big_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    // rows in chunks so the split operand stays <= ~2.5 GB of scratch
+    const uint64_t chunk_rows = uint64_t(2) << 20;
+    const auto mark = ctx->arena.mark();
+    for (uint64_t r0 = 0; r0 < a0.n; r0 += chunk_rows) {
+        ctx->arena.reset_to(mark);
+        NearestArgs a = a0;
+        a.n = std::min<uint64_t>(chunk_rows, a0.n - r0);
+        if (a.src.codes) a.src.codes += r0 * a.src.dM * a.src.dw;
+        else a.src.x += r0 * a.src.ldx;
+        const uint64_t ntiles = (a.n + kR - 1) / kR;
+        uint8_t* Am = scratch<uint8_t>(ctx, ntiles * kchunks * 2 * kAChunk);
+        float* Erow = scratch<float>(ctx, a.n);
+        launch(ctx, "big_split", split_rows_kernel, dim3(grid1d(ntiles * kR, 128, 1u << 20)), dim3(128), 0,
+               a.src, a.n, a.d, kchunks, a.cmax, Am, Erow);
+        const unsigned grid = unsigned(std::min<uint64_t>(ntiles, uint64_t(ctx->num_sms)));
+        if (a.out_mat) {
+            a.out_mat += r0 * a.ld_mat;
+            launch(ctx, "distance_matrix_tc", big_kernel<true>, dim3(grid), dim3(192), smem, a,
+                   (const uint8_t*)Am, (const uint8_t*)Bm, (const float*)Erow, kchunks, nblocks, r0);
+            if (a.row_err)
+                PQG_CUDA(cudaMemcpyAsync(a.row_err + r0, Erow, sizeof(float) * a.n, cudaMemcpyDeviceToDevice,
+                                         ctx->stream));
+        } else {
+            a.out_idx = static_cast<uint8_t*>(a.out_idx) + r0 * a.idx_rs * uint64_t(a.idx_bytes);
+            if (a.out_dist) a.out_dist += r0;
+            launch(ctx, "nearest_big_tc", big_kernel<false>, dim3(grid), dim3(192), smem, a,
+                   (const uint8_t*)Am, (const uint8_t*)Bm, (const float*)Erow, kchunks, nblocks, r0);
+        }
+    }
+}
+
+}  // namespace pqg
