@@ -298,6 +298,16 @@ static KMeansOut run_kmeans(pqg_ctx* ctx, const float* x, uint64_t n, uint64_t l
     src.x = x;
     src.ldx = ldx;
     src.col_stride = col_stride;
+    // coarse fits (one problem, large d and k): split the row operand for the
+    // tensor-core screen once; every assignment pass reuses it
+    NearestArgs prep;
+    prep.src = src;
+    prep.n = n;
+    prep.d = d;
+    prep.B = B;
+    prep.k = k;
+    prep.cmax = cmax;
+    const bool big = B == 1 && umma_big_prepare_rows(ctx, prep);
     const auto iter_mark = ctx->arena.mark();
     for (uint32_t it = 1; it <= max_iters; ++it) {
         ctx->arena.reset_to(iter_mark);  // per-iteration scratch is reused
@@ -317,6 +327,10 @@ static KMeansOut run_kmeans(pqg_ctx* ctx, const float* x, uint64_t n, uint64_t l
         a.idx_ps = n;
         a.out_dist = dist;
         a.active = st.active;
+        if (big) {
+            a.big_rows = prep.big_rows;
+            a.big_nx = prep.big_nx;
+        }
         nearest(ctx, a);
         kmeans_inertia_and_stop(ctx, dist, n, B, it, max_iters, tol, st);
         if (it == max_iters) break;

@@ -44,6 +44,9 @@ struct NearestArgs {
     float* out_mat = nullptr;
     uint64_t ld_mat = 0;
     float* row_err = nullptr;  // [n] screen error bound per row (matrix mode)
+    // umma_big: row operand already split (k-means reuses it every iteration)
+    const uint8_t* big_rows = nullptr;
+    const float* big_nx = nullptr;
 };
 
 // nearest.cu
@@ -58,6 +61,9 @@ void umma_screen(pqg_ctx* ctx, const NearestArgs& a);
 // umma_big.cu (tcgen05 GEMM-argmin / screen matrix for the coarse quantizer)
 bool umma_big_supported(const NearestArgs& a);
 void umma_big(pqg_ctx* ctx, const NearestArgs& a);
+// Split the row operand once (C_r = ||x_r||^2, no margin) for repeated argmin
+// calls over the same rows; returns false if the big kernel does not apply.
+bool umma_big_prepare_rows(pqg_ctx* ctx, NearestArgs& a);
 
 // kmeans.cu
 struct Bucketing {

@@ -26,6 +26,7 @@
 //              and only rows with >= 4 candidates in the band go to the
 //              global fixup.  MAT mode instead writes the screened matrix.
 #include <cstdlib>
+#include <cstring>
 
 #include "kernels.cuh"
 
@@ -123,8 +124,11 @@ __device__ __forceinline__ float big_error_bound(float S, uint32_t kchunks) {
 
 // ---- operand preparation ---------------------------------------------------
 // One thread per row: A_r = [x_r, 1, C_r, 0...], split hi/lo, interleaved.
+// C_r = ||x_r||^2 (+ 2E margin in matrix mode, whose consumer orders values as
+// unsigned bits); the argmin epilogue compares floats and recomputes E from
+// the stored ||x_r||^2 and the current max ||c||.
 __global__ void split_rows_kernel(RowSrc src, uint64_t n, uint32_t d, uint32_t kchunks,
-                                  const float* cmax_p, uint8_t* A, float* Erow) {
+                                  const float* cmax_p, int margin, uint8_t* A, float* nxrow) {
     const float cmax = *cmax_p;
     for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < (n + kR - 1) / kR * kR;
          r += uint64_t(gridDim.x) * blockDim.x) {
@@ -138,8 +142,8 @@ __global__ void split_rows_kernel(RowSrc src, uint64_t n, uint32_t d, uint32_t k
         const float q = sqrtf(nx) * (1.f + 1e-6f) + cmax;
         const float S = q * q * 1.01f + 1e-6f;
         const float E = big_error_bound(S, kchunks);
-        const float C = nx * (1.f + 2.f * float(d + 2) * kU) + 2.f * E;
-        if (valid) Erow[r] = E;
+        const float C = margin ? nx * (1.f + 2.f * float(d + 2) * kU) + 2.f * E : nx;
+        if (valid) nxrow[r] = nx;
         const uint64_t tile = r / kR;
         const uint32_t rl = uint32_t(r % kR);
         for (uint32_t kc = 0; kc < kchunks; ++kc) {
@@ -217,9 +221,10 @@ __device__ __forceinline__ double exact_row_dist(const NearestArgs& a, uint64_t 
 template <bool MAT>
 __global__ void __launch_bounds__(192, 1) big_kernel(NearestArgs a, const uint8_t* __restrict__ A,
                                                      const uint8_t* __restrict__ Bm,
-                                                     const float* __restrict__ Erow,
+                                                     const float* __restrict__ nxrow,
                                                      uint32_t kchunks, uint32_t nblocks,
                                                      uint64_t row_base) {
+    if (a.active && !a.active[0]) return;
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t full[2], empty[2], tfull[2], tempty[2];
     __shared__ uint32_t tmem_base;
@@ -351,16 +356,20 @@ __global__ void __launch_bounds__(192, 1) big_kernel(NearestArgs a, const uint8_
                 __syncwarp();
                 if (lane == 0) bar_arrive(&tempty[buf]);
             }
-            if constexpr (!MAT) {
-                if (row < a.n) {
-                    const float E = Erow[row];
-                    const float band = tv[0] + 2.05f * E;
-                    if (tv[3] > band * (1.f + 4.f * kU)) {
+            if (row < a.n) {
+                const float q = sqrtf(nxrow[row]) * (1.f + 1e-6f) + *a.cmax;
+                const float E = big_error_bound(q * q * 1.01f + 1e-6f, kchunks);
+                if constexpr (MAT) {
+                    if (a.row_err) a.row_err[row] = E;
+                } else {
+                    const float band0 = tv[0] + 2.05f * E;
+                    const float band = band0 + 4.f * kU * fabsf(band0);
+                    if (tv[3] > band) {
                         // all possible fp64 winners are among the top 3: re-score exactly
                         double best = __longlong_as_double(0x7ff0000000000000LL);
                         uint32_t bj = 0xFFFFFFFFu;
                         for (int i = 0; i < 3; ++i) {
-                            if (ti[i] == 0xFFFFFFFFu || !(tv[i] <= band * (1.f + 4.f * kU))) continue;
+                            if (ti[i] == 0xFFFFFFFFu || !(tv[i] <= band)) continue;
                             const double dd = exact_row_dist(a, row, ti[i]);
                             if (dd < best || (dd == best && ti[i] < bj)) { best = dd; bj = ti[i]; }
                         }
@@ -388,7 +397,7 @@ __global__ void __launch_bounds__(192, 1) big_kernel(NearestArgs a, const uint8_
 }
 
 bool umma_big_supported_impl(const NearestArgs& a) {
-    if (a.B != 1 || a.active) return false;  // single problem (coarse) only
+    if (a.B != 1) return false;  // single problem (coarse) only
     if (a.d < 24) return false;              // small d: the PQ kernels
     if (a.k < 64) return false;
     return true;
@@ -397,6 +406,23 @@ bool umma_big_supported_impl(const NearestArgs& a) {
 }  // namespace
 
 bool umma_big_supported(const NearestArgs& a) { return umma_big_supported_impl(a); }
+
+bool umma_big_prepare_rows(pqg_ctx* ctx, NearestArgs& a) {
+    const char* mode = std::getenv("PQG_SCREEN");
+    if (mode && std::strcmp(mode, "fp32") == 0) return false;
+    NearestArgs probe = a;
+    probe.active = nullptr;
+    if (!umma_big_supported_impl(probe) || a.n > (uint64_t(2) << 20)) return false;
+    const uint32_t kchunks = (a.d + 2 + kKC - 1) / kKC;
+    const uint64_t ntiles = (a.n + kR - 1) / kR;
+    uint8_t* Am = scratch<uint8_t>(ctx, ntiles * kchunks * 2 * kAChunk);
+    float* nx = scratch<float>(ctx, a.n);
+    launch(ctx, "big_split", split_rows_kernel, dim3(grid1d(ntiles * kR, 128, 1u << 20)), dim3(128), 0,
+           a.src, a.n, a.d, kchunks, a.cmax, 0, Am, nx);
+    a.big_rows = Am;
+    a.big_nx = nx;
+    return true;
+}
 
 void umma_big(pqg_ctx* ctx, const NearestArgs& a0) {
     const uint32_t kchunks = (a0.d + 2 + kKC - 1) / kKC;
@@ -408,6 +434,13 @@ void umma_big(pqg_ctx* ctx, const NearestArgs& a0) {
     const size_t smem = 2 * size_t(kStage);
     PQG_CUDA(cudaFuncSetAttribute(big_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     PQG_CUDA(cudaFuncSetAttribute(big_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    if (a0.big_rows) {  // rows prepared by umma_big_prepare_rows (single chunk)
+        const uint64_t ntiles = (a0.n + kR - 1) / kR;
+        const unsigned grid = unsigned(std::min<uint64_t>(ntiles, uint64_t(ctx->num_sms)));
+        launch(ctx, "nearest_big_tc", big_kernel<false>, dim3(grid), dim3(192), smem, a0, a0.big_rows,
+               (const uint8_t*)Bm, a0.big_nx, kchunks, nblocks, uint64_t(0));
+        return;
+    }
     // rows in chunks so the split operand stays <= ~2.5 GB of scratch
     const uint64_t chunk_rows = uint64_t(2) << 20;
     const auto mark = ctx->arena.mark();
@@ -419,22 +452,20 @@ void umma_big(pqg_ctx* ctx, const NearestArgs& a0) {
         else a.src.x += r0 * a.src.ldx;
         const uint64_t ntiles = (a.n + kR - 1) / kR;
         uint8_t* Am = scratch<uint8_t>(ctx, ntiles * kchunks * 2 * kAChunk);
-        float* Erow = scratch<float>(ctx, a.n);
+        float* nx = scratch<float>(ctx, a.n);
         launch(ctx, "big_split", split_rows_kernel, dim3(grid1d(ntiles * kR, 128, 1u << 20)), dim3(128), 0,
-               a.src, a.n, a.d, kchunks, a.cmax, Am, Erow);
+               a.src, a.n, a.d, kchunks, a.cmax, a.out_mat ? 1 : 0, Am, nx);
         const unsigned grid = unsigned(std::min<uint64_t>(ntiles, uint64_t(ctx->num_sms)));
         if (a.out_mat) {
             a.out_mat += r0 * a.ld_mat;
+            if (a.row_err) a.row_err += r0;
             launch(ctx, "distance_matrix_tc", big_kernel<true>, dim3(grid), dim3(192), smem, a,
-                   (const uint8_t*)Am, (const uint8_t*)Bm, (const float*)Erow, kchunks, nblocks, r0);
-            if (a.row_err)
-                PQG_CUDA(cudaMemcpyAsync(a.row_err + r0, Erow, sizeof(float) * a.n, cudaMemcpyDeviceToDevice,
-                                         ctx->stream));
+                   (const uint8_t*)Am, (const uint8_t*)Bm, (const float*)nx, kchunks, nblocks, r0);
         } else {
             a.out_idx = static_cast<uint8_t*>(a.out_idx) + r0 * a.idx_rs * uint64_t(a.idx_bytes);
             if (a.out_dist) a.out_dist += r0;
             launch(ctx, "nearest_big_tc", big_kernel<false>, dim3(grid), dim3(192), smem, a,
-                   (const uint8_t*)Am, (const uint8_t*)Bm, (const float*)Erow, kchunks, nblocks, r0);
+                   (const uint8_t*)Am, (const uint8_t*)Bm, (const float*)nx, kchunks, nblocks, r0);
         }
     }
 }
