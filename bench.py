@@ -467,6 +467,8 @@ def adc_bench(ctx, lib, L, x, train, args, world, stream, timed):
     n_scan, scan_ms = ctx.profile_read("adc_scan")
     n_sel, sel_ms = ctx.profile_read("probe_select")
     n_mat, mat_ms = ctx.profile_read("distance_matrix")
+    n_mtc, mtc_ms = ctx.profile_read("distance_matrix_tc")
+    n_spl, spl_ms = ctx.profile_read("big_split")
     ctx.profile(False)
     off = torch.empty(nlist + 1, dtype=torch.int64)
     L.check(lib.pqg_index_export(ctx.h, h, vp(off.data_ptr()), None, None, None, None))
@@ -475,10 +477,10 @@ def adc_bench(ctx, lib, L, x, train, args, world, stream, timed):
             "nprobe": nprobe, "k": k, "nlist": nlist, "M": M, "Ks": ks,
             "coarse_kmeans_seconds": coarse_s, "coarse_iters_run": it.value,
             "ivf_build_seconds": build_s,
-            "scan_ms": scan_ms / max(n_scan, 1) * max(1, n_scan // max(1, (max(3, args.steps // 2)))),
-            "kernel_ms_per_batch": {"adc_scan": scan_ms / max(3, args.steps // 2),
-                                    "probe_select": sel_ms / max(3, args.steps // 2),
-                                    "distance_matrix": mat_ms / max(3, args.steps // 2)},
+            "kernel_ms_per_batch": {k_: v_ / (max(3, args.steps // 2) + 2) for k_, v_ in
+                                    (("adc_scan", scan_ms), ("probe_select", sel_ms),
+                                     ("distance_matrix_fp32", mat_ms),
+                                     ("distance_matrix_tc", mtc_ms), ("operand_split", spl_ms))},
             "max_list": int((off[1:] - off[:-1]).max())}
 
 
