@@ -44,7 +44,8 @@ typedef struct pqg_index pqg_index; /* device-resident inverted index */
 /* ---- context ----------------------------------------------------------- */
 int pqg_ctx_create(int device, pqg_ctx** out);
 void pqg_ctx_destroy(pqg_ctx* ctx);
-/* Run on a caller-owned cudaStream_t (NULL restores the context's own). */
+/* Run on a caller-owned cudaStream_t (NULL restores the context's own;
+ * (void*)1 is cudaStreamLegacy, the default stream of other libraries). */
 int pqg_ctx_set_stream(pqg_ctx* ctx, void* cuda_stream);
 int pqg_ctx_sync(pqg_ctx* ctx);
 const char* pqg_last_error(void);

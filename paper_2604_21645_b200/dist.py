@@ -3,10 +3,12 @@
 GPU g owns the contiguous global rows ``chunk_rows(N, P)[g]``
 (proj/src/dataset_io.cpp:322-339), the B200 replacement of the paper's CPU
 row chunking.  ``torch.distributed`` carries the exchanges
-(NCCL on GPUs, gloo in the CPU tests); the per-shard compute goes through a
-*backend* -- ``CudaBackend`` (libpqg.so via the C ABI) in production.  The
-exchange logic is backend-independent so it is tested on CPU with gloo and
-an oracle-backed backend (tests/test_dist_gloo.py).
+(NCCL on GPUs, gloo in the CPU tests) on torch tensors that stay on the
+device; the per-shard compute goes through a *backend* -- ``CudaBackend``
+(libpqg.so via the C ABI, device pointers) in production.  The exchange
+logic is backend-independent, so it is tested on CPU with gloo and an
+oracle-backed backend (tests/test_dist_gloo.py) and on a GPU with NCCL
+(tests/test_dist_gpu.py).
 
 * ``kmeans_fit_sharded`` -- exact: each rank runs the assignment pass on its
   shard of the training sample, assignments + fp64 distances are
@@ -17,6 +19,9 @@ an oracle-backed backend (tests/test_dist_gloo.py).
 * ``search_sharded`` -- shard-local index + search, all-gather of the
   per-shard top-k lists, merge by (dist, id): equal to the monolithic
   ``ivf_query`` because shards are ascending id ranges and lists are stable.
+
+Unsigned 32/64-bit values travel as same-width signed tensors (int32/int64
+bit patterns): gloo and parts of torch have no unsigned types.
 """
 from __future__ import annotations
 
@@ -49,7 +54,7 @@ def kmeans_stop(it: int, max_iters: int, prev: float, inertia: float, tol: float
 
 
 # ---------------------------------------------------------------------------
-# collectives (torch.distributed); arrays travel as torch tensors
+# collectives on torch tensors
 # ---------------------------------------------------------------------------
 class Comm:
     def __init__(self, group=None):
@@ -58,131 +63,129 @@ class Comm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
-        self.device = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
 
-    _SIGNED = {np.dtype(np.uint32): np.int32, np.dtype(np.uint64): np.int64,
-               np.dtype(np.uint16): np.int16}
-
-    def _t(self, a):
-        """numpy -> torch on the collective's device; unsigned dtypes travel as
-        same-width signed views (gloo has no unsigned 32/64-bit types)."""
-        import torch
-        a = np.ascontiguousarray(a)
-        if a.dtype in self._SIGNED:
-            a = a.view(self._SIGNED[a.dtype])
-        return torch.from_numpy(a).to(self.device)
-
-    @staticmethod
-    def _back(t, dtype):
-        return t.cpu().numpy().view(dtype)
-
-    def allgather_rows(self, a: np.ndarray, counts: list[int]) -> np.ndarray:
-        """Concatenate per-rank arrays (first axis sizes ``counts``) in rank order."""
+    def allgather_rows(self, t, counts: list[int]):
+        """Concatenate per-rank tensors (first-axis sizes ``counts``) in rank order."""
         import torch
         mx = max(counts)
-        pad = np.zeros((mx,) + a.shape[1:], a.dtype)
-        pad[: a.shape[0]] = a
-        t = self._t(pad)
-        outs = [torch.empty_like(t) for _ in range(self.world)]
-        self.dist.all_gather(outs, t, group=self.group)
-        return np.concatenate([self._back(o, a.dtype)[:c] for o, c in zip(outs, counts)])
+        pad = torch.zeros((mx,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        pad[: t.shape[0]] = t
+        outs = [torch.empty_like(pad) for _ in range(self.world)]
+        self.dist.all_gather(outs, pad, group=self.group)
+        return torch.cat([o[:c] for o, c in zip(outs, counts)])
 
-    def allgather_cols(self, a: np.ndarray, counts: list[int]) -> np.ndarray:
-        """a is [B, n_local]; returns [B, sum(counts)] in rank order."""
-        g = self.allgather_rows(np.ascontiguousarray(a.T), counts)
-        return np.ascontiguousarray(g.T)
+    def allgather_cols(self, t, counts: list[int]):
+        """t is [B, n_local]; returns [B, sum(counts)] in rank order."""
+        return self.allgather_rows(t.t().contiguous(), counts).t().contiguous()
 
-    def allreduce_sum(self, x: float) -> float:
+    def allreduce_sum(self, x: float, device) -> float:
         import torch
-        t = self._t(np.array([x], np.float64))
+        t = torch.tensor([x], dtype=torch.float64, device=device)
         self.dist.all_reduce(t, group=self.group)
-        return float(t.cpu().numpy()[0])
+        return float(t.item())
 
-    def allgather_equal(self, a: np.ndarray) -> np.ndarray:
+    def allgather_equal(self, t):
         import torch
-        a = np.ascontiguousarray(a)
-        t = self._t(a)
         outs = [torch.empty_like(t) for _ in range(self.world)]
-        self.dist.all_gather(outs, t, group=self.group)
-        return np.stack([self._back(o, a.dtype) for o in outs])
+        self.dist.all_gather(outs, t.contiguous(), group=self.group)
+        return torch.stack(outs)
 
 
 # ---------------------------------------------------------------------------
-# production backend: libpqg.so
+# production backend: libpqg.so on device tensors
 # ---------------------------------------------------------------------------
 class CudaBackend:
-    """Shard-local compute through the C ABI (include/pqg.h)."""
+    """Shard-local compute through the C ABI (include/pqg.h) on CUDA tensors."""
 
     def __init__(self, device: int = 0):
+        import torch
+
         from . import _lib, pqii
+        self.torch = torch
         self.L = _lib
         self.pqii = pqii
+        self.device = torch.device("cuda", device)
         self.ctx = pqii.get_context(device)
         self.lib = self.ctx.lib
+        # libpqg runs on torch's current stream so collectives and kernels order;
+        # torch's default stream is the legacy stream (handle 0 -> cudaStreamLegacy)
+        self.ctx.set_stream(torch.cuda.current_stream(self.device).cuda_stream or 1)
 
-    def _v(self, a):
-        return a.ctypes.data_as(C.c_void_p)
+    @staticmethod
+    def _p(t):
+        return C.c_void_p(t.data_ptr())
 
     def init_rows(self, n, k, seed):
         out = np.empty(k, np.uint64)
-        self.L.check(self.lib.pqg_kmeans_init_rows(n, k, seed, self._v(out)), "init")
+        self.L.check(self.lib.pqg_kmeans_init_rows(n, k, seed, out.ctypes.data_as(C.c_void_p)), "init")
         return out
 
     def assign_pass(self, rows, B, d, col_stride, tables):
-        rows = np.ascontiguousarray(rows, np.float32)
+        torch = self.torch
         n, ld = rows.shape
         k = tables.shape[1]
-        a = np.empty((B, n), np.uint32)
-        dist = np.empty((B, n), np.float64)
-        self.L.check(self.lib.pqg_assign_pass(self.ctx.h, self._v(rows), n, ld, B, d, col_stride,
-                                              self._v(np.ascontiguousarray(tables)), k, self._v(a),
-                                              self._v(dist)), "assign_pass")
+        a = torch.empty((B, n), dtype=torch.int32, device=rows.device)
+        dist = torch.empty((B, n), dtype=torch.float64, device=rows.device)
+        self.L.check(self.lib.pqg_assign_pass(self.ctx.h, self._p(rows), n, ld, B, d, col_stride,
+                                              self._p(tables), k, self._p(a), self._p(dist)),
+                     "assign_pass")
         return a, dist
 
     def rows_sum(self, v):
-        v = np.ascontiguousarray(v, np.float64)
         B, n = v.shape
         out = np.empty(B, np.float64)
-        self.L.check(self.lib.pqg_rows_sum_f64(self.ctx.h, self._v(v), n, B, self._v(out)), "sum")
+        self.L.check(self.lib.pqg_rows_sum_f64(self.ctx.h, self._p(v), n, B,
+                                               out.ctypes.data_as(C.c_void_p)), "sum")
         return out
 
     def update_pass(self, rows, B, d, col_stride, tables, assign, dist, active):
-        rows = np.ascontiguousarray(rows, np.float32)
         n, ld = rows.shape
         k = tables.shape[1]
-        act = np.ascontiguousarray(active, np.int32)
-        self.L.check(self.lib.pqg_update_pass(self.ctx.h, self._v(rows), n, ld, B, d, col_stride,
-                                              self._v(tables), k, self._v(np.ascontiguousarray(assign)),
-                                              self._v(dist), self._v(act)), "update_pass")
+        act = self.torch.as_tensor(np.ascontiguousarray(active, np.int32), device=rows.device)
+        self.L.check(self.lib.pqg_update_pass(self.ctx.h, self._p(rows), n, ld, B, d, col_stride,
+                                              self._p(tables), k, self._p(assign), self._p(dist),
+                                              self._p(act)), "update_pass")
 
     def encode_sse(self, rows, tables):
-        rows = np.ascontiguousarray(rows, np.float32)
+        torch = self.torch
         M, ks, ds = tables.shape
-        codes = np.empty((rows.shape[0], M * (1 if ks <= 256 else 2)), np.uint8)
+        codes = torch.empty((rows.shape[0], M * (1 if ks <= 256 else 2)), dtype=torch.uint8,
+                            device=rows.device)
         sse = C.c_double()
-        self.L.check(self.lib.pqg_pq_encode_sse(self.ctx.h, self._v(rows), rows.shape[0], M, ks, ds,
-                                                self._v(np.ascontiguousarray(tables)),
-                                                self._v(codes), C.byref(sse)), "encode")
+        self.L.check(self.lib.pqg_pq_encode_sse(self.ctx.h, self._p(rows), rows.shape[0], M, ks, ds,
+                                                self._p(tables), self._p(codes), C.byref(sse)),
+                     "encode")
         return codes, sse.value
 
     def search_local(self, tables, codes, ids, coarse, queries, k, nprobe):
-        pq = self.pqii
+        torch = self.torch
         M, ks, ds = tables.shape
-        cb = pq.Codebook(M, ks, ds, np.ascontiguousarray(tables))
-        cm = pq.CodeMatrix(codes.shape[0], M, ks, np.ascontiguousarray(codes))
-        index = pq.ivf_build_with_centroids(cb, cm, ids, coarse)
-        return pq.ivf_query_batch(index, queries, k, nprobe)
+        h = C.c_void_p()
+        self.L.check(self.lib.pqg_ivf_build_with_centroids(
+            self.ctx.h, self._p(tables), M, ks, ds, self._p(codes), self._p(ids), codes.shape[0],
+            self._p(coarse), coarse.shape[0], C.byref(h)), "ivf_build")
+        nq = queries.shape[0]
+        oi = torch.zeros((nq, k), dtype=torch.int64, device=queries.device)
+        od = torch.zeros((nq, k), dtype=torch.float64, device=queries.device)
+        oc = torch.zeros(nq, dtype=torch.int32, device=queries.device)
+        try:
+            self.L.check(self.lib.pqg_index_search(self.ctx.h, h, self._p(queries), nq, k, nprobe,
+                                                   0, 0.0, self._p(oi), self._p(od), self._p(oc)),
+                         "search")
+        finally:
+            self.lib.pqg_index_destroy(h)
+        return oi, od, oc
 
     def topk_merge(self, ids, dists, counts, k):
+        torch = self.torch
         S, nq, _ = ids.shape
-        oi = np.zeros((nq, k), np.uint64)
-        od = np.zeros((nq, k), np.float64)
-        oc = np.zeros(nq, np.uint32)
-        self.L.check(self.lib.pqg_topk_merge(
-            self.ctx.h, self._v(np.ascontiguousarray(ids, np.uint64)),
-            self._v(np.ascontiguousarray(dists, np.float64)),
-            self._v(np.ascontiguousarray(counts, np.uint32)), S, nq, k, self._v(oi), self._v(od),
-            self._v(oc)), "topk_merge")
+        oi = torch.zeros((nq, k), dtype=torch.int64, device=ids.device)
+        od = torch.zeros((nq, k), dtype=torch.float64, device=ids.device)
+        oc = torch.zeros(nq, dtype=torch.int32, device=ids.device)
+        self.L.check(self.lib.pqg_topk_merge(self.ctx.h, self._p(ids.contiguous()),
+                                             self._p(dists.contiguous()), self._p(counts.contiguous()),
+                                             S, nq, k, self._p(oi), self._p(od), self._p(oc)),
+                     "topk_merge")
         return oi, od, oc
 
 
@@ -191,19 +194,22 @@ class CudaBackend:
 # ---------------------------------------------------------------------------
 @dataclass
 class ShardedFit:
-    tables: np.ndarray          # [B, k, d]
-    assignments: np.ndarray     # [B, N] (global row order)
+    tables: object              # [B, k, d] float32 tensor
+    assignments: object         # [B, N] int32 tensor (u32 bit patterns), global row order
     inertia: np.ndarray         # [B]
     iterations_run: np.ndarray  # [B]
     inertia_per_iter: list
 
 
-def kmeans_fit_sharded(comm: Comm, backend, local_rows: np.ndarray, B: int, d: int,
-                       col_stride: int, k: int, max_iters: int, seeds, tol: float = 1e-4) -> ShardedFit:
+def kmeans_fit_sharded(comm: Comm, backend, local_rows, B: int, d: int, col_stride: int, k: int,
+                       max_iters: int, seeds, tol: float = 1e-4) -> ShardedFit:
     """B batched k-means problems (B = M subspaces for pq_fit, B = 1 for the
     coarse quantizer) over rows sharded by rank; bit-identical to the
     single-process fit (see module docstring)."""
-    counts = [int(c) for c in comm.allgather_equal(np.array([local_rows.shape[0]], np.int64))[:, 0]]
+    import torch
+    dev = local_rows.device
+    counts = [int(c) for c in comm.allgather_equal(
+        torch.tensor([local_rows.shape[0]], dtype=torch.int64, device=dev)).view(-1).tolist()]
     n = sum(counts)
     if k == 0:
         raise ValueError("kmeans_fit: k must be >= 1")
@@ -211,18 +217,17 @@ def kmeans_fit_sharded(comm: Comm, backend, local_rows: np.ndarray, B: int, d: i
         raise ValueError(f"kmeans_fit: k ({k}) exceeds number of points ({n})")
     if max_iters < 1:
         raise ValueError("kmeans_fit: max_iters must be >= 1")
-    full = comm.allgather_rows(np.ascontiguousarray(local_rows, np.float32), counts)
-    offset = sum(counts[: comm.rank])
-    tables = np.empty((B, k, d), np.float32)
+    full = comm.allgather_rows(local_rows.contiguous(), counts)
+    tables = torch.empty((B, k, d), dtype=torch.float32, device=dev)
     for b in range(B):  # init rows: the reference's draws, identical on every rank
-        rows = backend.init_rows(n, k, int(seeds[b])).astype(np.int64)
-        tables[b] = full[rows, b * col_stride: b * col_stride + d]
+        rows = torch.as_tensor(backend.init_rows(n, k, int(seeds[b])).astype(np.int64), device=dev)
+        tables[b] = full.index_select(0, rows)[:, b * col_stride: b * col_stride + d]
     active = np.ones(B, np.int32)
     prev = np.zeros(B)
     inertia = np.zeros(B)
     iters = np.zeros(B, np.uint32)
     per_iter = [[] for _ in range(B)]
-    assign_full = np.zeros((B, n), np.uint32)
+    assign_full = torch.zeros((B, n), dtype=torch.int32, device=dev)
     for it in range(1, max_iters + 1):
         a_loc, d_loc = backend.assign_pass(local_rows, B, d, col_stride, tables)
         a_full = comm.allgather_cols(a_loc, counts)
@@ -242,12 +247,11 @@ def kmeans_fit_sharded(comm: Comm, backend, local_rows: np.ndarray, B: int, d: i
         if not active.any():
             break
         backend.update_pass(full, B, d, col_stride, tables, a_full, d_full, active)
-    del offset
     return ShardedFit(tables, assign_full, inertia, iters, per_iter)
 
 
-def pq_fit_sharded(comm: Comm, backend, local_rows: np.ndarray, M: int, ks: int,
-                   max_iters: int = 20, seed: int = 0) -> np.ndarray:
+def pq_fit_sharded(comm: Comm, backend, local_rows, M: int, ks: int, max_iters: int = 20,
+                   seed: int = 0):
     """pq_fit (proj/src/pq.cpp:63-93) over row shards: subspace m uses seed + m."""
     D = local_rows.shape[1]
     if M == 0 or D % M:
@@ -258,11 +262,11 @@ def pq_fit_sharded(comm: Comm, backend, local_rows: np.ndarray, M: int, ks: int,
     return fit.tables
 
 
-def encode_sharded(comm: Comm, backend, local_rows: np.ndarray, tables: np.ndarray):
+def encode_sharded(comm: Comm, backend, local_rows, tables):
     """Shard-local codes and the GLOBAL reconstruction RMSE (one all-reduce)."""
     codes, sse = backend.encode_sse(local_rows, tables)
-    n = comm.allreduce_sum(float(local_rows.shape[0]))
-    total = comm.allreduce_sum(sse)
+    n = comm.allreduce_sum(float(local_rows.shape[0]), local_rows.device)
+    total = comm.allreduce_sum(sse, local_rows.device)
     return codes, float(np.sqrt(total / (n * local_rows.shape[1])))
 
 
@@ -271,7 +275,5 @@ def search_sharded(comm: Comm, backend, tables, local_codes, local_ids, coarse, 
     """Shard-local index + search, then all-gather and (dist, id) merge."""
     ids, dists, counts = backend.search_local(tables, local_codes, local_ids, coarse, queries, k,
                                               nprobe)
-    all_ids = comm.allgather_equal(np.ascontiguousarray(ids, np.uint64))
-    all_d = comm.allgather_equal(np.ascontiguousarray(dists, np.float64))
-    all_c = comm.allgather_equal(np.ascontiguousarray(counts, np.uint32))
-    return backend.topk_merge(all_ids, all_d, all_c, k)
+    return backend.topk_merge(comm.allgather_equal(ids), comm.allgather_equal(dists),
+                              comm.allgather_equal(counts), k)

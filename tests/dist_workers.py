@@ -22,20 +22,24 @@ def run_rank(rank, world, port, outdir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     comm = D.Comm()
     be = OracleBackend()
+    import torch
     x = gaussian_mixture(1203, 16, 12, seed=9)  # odd size: uneven shards
     lo, hi = D.chunk_rows(x.shape[0], world)[rank]
-    local = x[lo:hi]
+    local = torch.from_numpy(np.ascontiguousarray(x[lo:hi]))
     res = {}
     fit = D.kmeans_fit_sharded(comm, be, local, 1, 16, 0, 24, 12, [5], 1e-4)
-    res["km_tables"], res["km_assign"], res["km_iters"] = fit.tables, fit.assignments, fit.iterations_run
-    res["pq_tables"] = D.pq_fit_sharded(comm, be, local, 4, 16, 10, 3)
-    codes, rmse = D.encode_sharded(comm, be, local, res["pq_tables"])
-    res["codes"], res["rmse"] = codes, np.array([rmse])
-    coarse = x[::100][:12].copy()
-    ids = np.arange(lo, hi, dtype=np.uint64) * 3 + 1
-    q = gaussian_mixture(9, 16, 12, seed=9, stream=1)
-    oi, od, oc = D.search_sharded(comm, be, res["pq_tables"], codes, ids, coarse, q, 7, 4)
-    res["s_ids"], res["s_d"], res["s_c"] = oi, od, oc
+    res["km_tables"] = fit.tables.numpy()
+    res["km_assign"] = fit.assignments.numpy().view(np.uint32)
+    res["km_iters"] = fit.iterations_run
+    tables = D.pq_fit_sharded(comm, be, local, 4, 16, 10, 3)
+    res["pq_tables"] = tables.numpy()
+    codes, rmse = D.encode_sharded(comm, be, local, tables)
+    res["codes"], res["rmse"] = codes.numpy(), np.array([rmse])
+    coarse = torch.from_numpy(x[::100][:12].copy())
+    ids = torch.from_numpy((np.arange(lo, hi, dtype=np.uint64) * 3 + 1).view(np.int64))
+    q = torch.from_numpy(gaussian_mixture(9, 16, 12, seed=9, stream=1))
+    oi, od, oc = D.search_sharded(comm, be, tables, codes, ids, coarse, q, 7, 4)
+    res["s_ids"], res["s_d"], res["s_c"] = oi.numpy().view(np.uint64), od.numpy(), oc.numpy().view(np.uint32)
     np.savez(os.path.join(outdir, f"rank{rank}.npz"), **res)
     dist.barrier()
     dist.destroy_process_group()
