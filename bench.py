@@ -54,21 +54,26 @@ def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if "RANK" in os.environ:  # launched by torchrun (any world size): NCCL process group
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
 
 
+def distributed():
+    import torch.distributed as dist
+    return dist.is_available() and dist.is_initialized()
+
+
 def barrier(world):
-    if world > 1:
+    if distributed():
         import torch.distributed as dist
         dist.barrier()
 
 
 def max_over_ranks(x: float, world: int) -> float:
-    if world == 1:
+    if not distributed():
         return x
     import torch
     import torch.distributed as dist
@@ -291,6 +296,23 @@ def run_ours(args, rank, world, local):
     fit_s = max_over_ranks(time.perf_counter() - t0, world)
     kmeans_ips = iters_run / fit_s
 
+    # ---- exact sharded PQ fit over the ranks' samples (torchrun only):
+    # assignment pass per shard, all-gather, replicated ordered update
+    sharded_fit = None
+    if distributed():
+        from paper_2604_21645_b200 import dist as D
+        comm, be = D.Comm(), D.CudaBackend(local)
+        be.ctx.set_stream(stream.cuda_stream)
+        D.pq_fit_sharded(comm, be, train, HEAD_M, HEAD_KS, 2, SEED)  # warm-up
+        torch.cuda.synchronize()
+        barrier(world)
+        t0 = time.perf_counter()
+        D.pq_fit_sharded(comm, be, train, HEAD_M, HEAD_KS, FIT_ITERS, SEED)
+        torch.cuda.synchronize()
+        sf_s = max_over_ranks(time.perf_counter() - t0, world)
+        sharded_fit = {"global_sample_rows": SAMPLE * world, "iters": FIT_ITERS, "seconds": sf_s,
+                       "iters_per_s": FIT_ITERS / sf_s}
+
     # ---- headline encode, timed with profiling of the dominant kernel
     codes = torch.empty((N_ROWS, HEAD_M), dtype=torch.uint8, device="cuda")
     encode(tables, HEAD_M, HEAD_KS, codes)
@@ -399,6 +421,7 @@ def run_ours(args, rank, world, local):
         "kmeans_iters_per_s": kmeans_ips,
         "kmeans_fit": {"M": HEAD_M, "Ks": HEAD_KS, "sample_rows": SAMPLE, "iters_run": iters_run,
                        "seconds": fit_s},
+        "sharded_pq_fit": sharded_fit,
         "adc": adc,
         "sweep": sweep,
         "roofline": {"bound": "fp32", "achieved": achieved_tflops, "peak": fp32_peak,
@@ -444,7 +467,7 @@ def adc_bench(ctx, lib, L, x, train, args, world, stream, timed):
     codes = torch.empty((N_ROWS, M), dtype=torch.uint8, device="cuda")
     L.check(lib.pqg_pq_encode(ctx.h, vp(x.data_ptr()), N_ROWS, M, ks, DIMS // M,
                               vp(tables.data_ptr()), vp(codes.data_ptr())))
-    ids = torch.arange(N_ROWS, dtype=torch.int64, device="cuda")
+    ids = torch.arange(N_ROWS, dtype=torch.int64, device="cuda") + int(os.environ.get("RANK", "0")) * N_ROWS
     h = C.c_void_p()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -458,9 +481,26 @@ def adc_bench(ctx, lib, L, x, train, args, world, stream, timed):
     od = torch.empty((nq, k), dtype=torch.float64, device="cuda")
     oc = torch.empty((nq,), dtype=torch.int32, device="cuda")
 
+    if distributed():
+        # every rank searches its shard (global ids rank*N + i), then the
+        # per-shard top-k lists are all-gathered and merged by (dist, id)
+        import torch.distributed as dist
+        gi = torch.empty((world, nq, k), dtype=torch.int64, device="cuda")
+        gd = torch.empty((world, nq, k), dtype=torch.float64, device="cuda")
+        gc = torch.empty((world, nq), dtype=torch.int32, device="cuda")
+        mi = torch.empty((nq, k), dtype=torch.int64, device="cuda")
+        md = torch.empty((nq, k), dtype=torch.float64, device="cuda")
+        mc = torch.empty((nq,), dtype=torch.int32, device="cuda")
+
     def search():
         L.check(lib.pqg_index_search(ctx.h, h, vp(q.data_ptr()), nq, k, nprobe, 0, 0.0,
                                      vp(oi.data_ptr()), vp(od.data_ptr()), vp(oc.data_ptr())))
+        if distributed():
+            dist.all_gather_into_tensor(gi, oi)
+            dist.all_gather_into_tensor(gd, od)
+            dist.all_gather_into_tensor(gc, oc)
+            L.check(lib.pqg_topk_merge(ctx.h, vp(gi.data_ptr()), vp(gd.data_ptr()), vp(gc.data_ptr()),
+                                       world, nq, k, vp(mi.data_ptr()), vp(md.data_ptr()), vp(mc.data_ptr())))
 
     ctx.profile(True)
     ms = timed(search, max(3, args.steps // 2), 2)
@@ -473,7 +513,8 @@ def adc_bench(ctx, lib, L, x, train, args, world, stream, timed):
     off = torch.empty(nlist + 1, dtype=torch.int64)
     L.check(lib.pqg_index_export(ctx.h, h, vp(off.data_ptr()), None, None, None, None))
     lib.pqg_index_destroy(h)
-    return {"queries_per_s": nq * world / (ms / 1e3), "ms_per_batch": ms, "nq": nq,
+    return {"queries_per_s": nq / (ms / 1e3), "ms_per_batch": ms, "nq": nq,
+            "index_rows": N_ROWS * world, "shards": world,
             "nprobe": nprobe, "k": k, "nlist": nlist, "M": M, "Ks": ks,
             "coarse_kmeans_seconds": coarse_s, "coarse_iters_run": it.value,
             "ivf_build_seconds": build_s,
@@ -501,7 +542,7 @@ def main():
         return
     rank, world, local = dist_setup()
     run_ours(args, rank, world, local)
-    if world > 1:
+    if distributed():
         import torch.distributed as dist
         dist.destroy_process_group()
 
