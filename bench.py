@@ -55,6 +55,9 @@ def dist_setup():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if "RANK" in os.environ:  # launched by torchrun (any world size): NCCL process group
+        # keep stdout to the one JSON line (NCCL prints its version banner otherwise)
+        if not os.environ.get("PQG_KEEP_NCCL_DEBUG"):
+            os.environ["NCCL_DEBUG"] = "WARN"
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))

@@ -420,3 +420,63 @@ def test_encode_full_size_sampled(pq, orc, mix):
     # decode(encode(x)) is idempotent under encode (codewords are fixed points)
     dec = pq.pq_decode(cb, pq.CodeMatrix(20000, 16, 256, codes.bytes[sel]))
     assert np.array_equal(pq.pq_encode(cb, dec).bytes, codes.bytes[sel])
+
+
+# ---------------------------------------------------------------------------
+# both screens (tcgen05 default and the FP32 FFMA screen) on the coarse and
+# PQ shapes that route to each kernel
+# ---------------------------------------------------------------------------
+
+@pytest.fixture(params=["tc", "fp32"])
+def screen(request, monkeypatch):
+    monkeypatch.setenv("PQG_SCREEN", request.param)
+    return request.param
+
+
+@pytest.mark.parametrize("n,d,k", [(5000, 32, 300), (3000, 128, 1024), (4000, 96, 520), (2500, 40, 64)])
+def test_coarse_nearest_both_screens(pq, orc, mix, screen, n, d, k):
+    x = mix(n, d, 64, seed=d + k)
+    table = mix(k, d, 64, seed=d + k + 1)
+    gi, gd = pq.nearest_batch(x, table)
+    oi, od = orc.nearest_batch(x, table)
+    assert np.array_equal(gi, oi)
+    assert np.array_equal(bits(gd), bits(od))
+
+
+def test_coarse_kmeans_both_screens(pq, orc, mix, screen):
+    x = mix(6000, 32, 40, seed=77)
+    a = pq.kmeans_fit(x, 150, 12, 4)
+    b = orc.kmeans_fit(x, 150, 12, 4)
+    assert a.iterations_run == b["iterations_run"]
+    assert np.array_equal(bits(a.centroids), bits(b["centroids"]))
+    assert np.array_equal(a.assignments, b["assignments"])
+
+
+def test_ivf_large_nlist_both_screens(pq, orc, mix, screen):
+    x = mix(8000, 32, 64, seed=5)
+    cb = pq.pq_fit(x, 8, 64, 8, 2)
+    codes = pq.pq_encode(cb, x)
+    assert np.array_equal(codes.bytes, orc.pq_encode(x, cb.tables))
+    coarse = pq.kmeans_fit(x, 300, 6, 9).centroids
+    ids = np.arange(8000, dtype=np.uint64) + 10
+    index = pq.ivf_build_with_centroids(cb, codes, ids, coarse)
+    off, lid, lcodes, _, _ = index.export()
+    o_off, o_ids, o_codes = orc.ivf_build_with_centroids(codes.bytes, ids, cb.tables, coarse)
+    assert np.array_equal(off, o_off) and np.array_equal(lid, o_ids) and np.array_equal(lcodes, o_codes)
+    q = mix(40, 32, 64, seed=5, stream=1)
+    probes = pq.ivf_probe(index, q, 20)
+    gi, gd, gc = pq.ivf_query_batch(index, q, 10, 20)
+    for i in range(40):
+        assert np.array_equal(probes[i], orc.probe_order(coarse, q[i], 20))
+        ri, rd = orc.ivf_query(cb.tables, coarse, o_off, o_ids, o_codes, q[i], 10, 20)
+        assert np.array_equal(gi[i, : gc[i]], ri) and np.array_equal(bits(gd[i, : gc[i]]), bits(rd))
+
+
+@pytest.mark.parametrize("M,ks", [(8, 256), (16, 64), (4, 16)])
+def test_pq_fit_both_screens(pq, orc, mix, screen, M, ks):
+    x = mix(5000, 64, 32, seed=M * ks)
+    t, it, _ = orc.pq_fit(x, M, ks, 10, 3)
+    stats = {}
+    cb = pq.pq_fit(x, M, ks, 10, 3, stats=stats)
+    assert np.array_equal(stats["iterations_run"], it)
+    assert np.array_equal(bits(cb.tables), bits(t))
