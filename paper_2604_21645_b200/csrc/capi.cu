@@ -492,6 +492,9 @@ void pqg_ctx_destroy(pqg_ctx* ctx) {
     }
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
     if (ctx->d_err) cudaFree(ctx->d_err);
+    for (auto e : ctx->pipe_ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
 }
@@ -627,6 +630,46 @@ int pqg_pq_fit(pqg_ctx* ctx, const float* data, uint64_t n, uint64_t D, uint32_t
     });
 }
 
+// Host rows: overlap the H2D copy of chunk c+1 (copy stream) with the encode
+// of chunk c (context stream) through two staging buffers; codes go back per
+// chunk on the copy stream.  PCIe is the bound for host inputs (~50 GB/s vs
+// the ~500 GB/s the encode consumes), so this hides the encode entirely.
+static void encode_host_pipelined(pqg_ctx* ctx, const float* data, uint64_t n, uint32_t M,
+                                  uint32_t ks, uint32_t ds, const float* dt, uint8_t* codes_host) {
+    const uint64_t D = uint64_t(M) * ds;
+    const uint32_t w = code_width(ks);
+    if (!ctx->copy_stream) {
+        PQG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+        for (auto& e : ctx->pipe_ev) PQG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const uint64_t chunk = std::max<uint64_t>(4096, std::min<uint64_t>(n / 8 + 1, (uint64_t(64) << 20) / (D * 4)));
+    float* stage[2] = {scratch<float>(ctx, chunk * D), scratch<float>(ctx, chunk * D)};
+    uint8_t* dcodes = scratch<uint8_t>(ctx, n * M * w);
+    cudaEvent_t* copied = ctx->pipe_ev;      // [2]: chunk landed in stage[b]
+    cudaEvent_t* consumed = ctx->pipe_ev + 2;  // [2]: encode of stage[b] done
+    PQG_CUDA(cudaEventRecord(consumed[0], ctx->stream));
+    PQG_CUDA(cudaEventRecord(consumed[1], ctx->stream));
+    const auto mark = ctx->arena.mark();
+    uint64_t c = 0;
+    for (uint64_t r0 = 0; r0 < n; r0 += chunk, ++c) {
+        const uint64_t nc = std::min(chunk, n - r0);
+        const int b = int(c & 1);
+        PQG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, consumed[b], 0));
+        PQG_CUDA(cudaMemcpyAsync(stage[b], data + r0 * D, nc * D * sizeof(float), cudaMemcpyHostToDevice,
+                                 ctx->copy_stream));
+        PQG_CUDA(cudaEventRecord(copied[b], ctx->copy_stream));
+        PQG_CUDA(cudaStreamWaitEvent(ctx->stream, copied[b], 0));
+        ctx->arena.reset_to(mark);
+        encode_dev(ctx, stage[b], nc, M, ks, ds, dt, dcodes + r0 * M * w);
+        PQG_CUDA(cudaEventRecord(consumed[b], ctx->stream));
+        PQG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, consumed[b], 0));
+        PQG_CUDA(cudaMemcpyAsync(codes_host + r0 * M * w, dcodes + r0 * M * w, nc * M * w,
+                                 cudaMemcpyDeviceToHost, ctx->copy_stream));
+    }
+    PQG_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+    PQG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
 int pqg_pq_encode(pqg_ctx* ctx, const float* data, uint64_t n, uint32_t M, uint32_t ks,
                   uint32_t ds, const float* tables, uint8_t* codes) {
     return guard([&] {
@@ -634,6 +677,11 @@ int pqg_pq_encode(pqg_ctx* ctx, const float* data, uint64_t n, uint32_t M, uint3
         check_pq_shape(M, ks, ds, "pq_encode");
         if (n == 0) return;
         const uint64_t D = uint64_t(M) * ds;
+        if (n >= 65536 && !on_device(data) && codes && !on_device(codes)) {
+            const float* dt0 = in(ctx, tables, uint64_t(M) * ks * ds);
+            encode_host_pipelined(ctx, data, n, M, ks, ds, dt0, codes);
+            return;
+        }
         const float* dx = in(ctx, data, n * D);
         const float* dt = in(ctx, tables, uint64_t(M) * ks * ds);
         auto oc = out(ctx, codes, n * M * code_width(ks));

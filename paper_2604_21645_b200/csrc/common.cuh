@@ -147,6 +147,9 @@ struct pqg_ctx {
     std::vector<cudaEvent_t> event_pool;
     // device flag word for kernel-side error reports (range errors)
     int* d_err = nullptr;
+    // copy stream + events for host-input pipelines (created on first use)
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t pipe_ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 
 namespace pqg {
