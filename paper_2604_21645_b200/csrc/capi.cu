@@ -650,21 +650,28 @@ static void encode_host_pipelined(pqg_ctx* ctx, const float* data, uint64_t n, u
     PQG_CUDA(cudaEventRecord(consumed[0], ctx->stream));
     PQG_CUDA(cudaEventRecord(consumed[1], ctx->stream));
     const auto mark = ctx->arena.mark();
-    uint64_t c = 0;
-    for (uint64_t r0 = 0; r0 < n; r0 += chunk, ++c) {
-        const uint64_t nc = std::min(chunk, n - r0);
+    const uint64_t nchunks = (n + chunk - 1) / chunk;
+    auto h2d = [&](uint64_t c) {  // copy stream: chunk c -> stage[c & 1]
+        const uint64_t r0 = c * chunk, nc = std::min(chunk, n - r0);
         const int b = int(c & 1);
         PQG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, consumed[b], 0));
         PQG_CUDA(cudaMemcpyAsync(stage[b], data + r0 * D, nc * D * sizeof(float), cudaMemcpyHostToDevice,
                                  ctx->copy_stream));
         PQG_CUDA(cudaEventRecord(copied[b], ctx->copy_stream));
+    };
+    h2d(0);
+    for (uint64_t c = 0; c < nchunks; ++c) {
+        // the next chunk's copy is queued before this chunk's results go back,
+        // so the copy engine streams rows while the SMs encode
+        if (c + 1 < nchunks) h2d(c + 1);
+        const uint64_t r0 = c * chunk, nc = std::min(chunk, n - r0);
+        const int b = int(c & 1);
         PQG_CUDA(cudaStreamWaitEvent(ctx->stream, copied[b], 0));
         ctx->arena.reset_to(mark);
         encode_dev(ctx, stage[b], nc, M, ks, ds, dt, dcodes + r0 * M * w);
         PQG_CUDA(cudaEventRecord(consumed[b], ctx->stream));
-        PQG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, consumed[b], 0));
         PQG_CUDA(cudaMemcpyAsync(codes_host + r0 * M * w, dcodes + r0 * M * w, nc * M * w,
-                                 cudaMemcpyDeviceToHost, ctx->copy_stream));
+                                 cudaMemcpyDeviceToHost, ctx->stream));
     }
     PQG_CUDA(cudaStreamSynchronize(ctx->copy_stream));
     PQG_CUDA(cudaStreamSynchronize(ctx->stream));
