@@ -145,6 +145,13 @@ int pqg_index_merge(pqg_ctx* ctx, const pqg_index* a, const pqg_index* b, pqg_in
 int pqg_index_search(pqg_ctx* ctx, const pqg_index* index, const float* queries, uint64_t nq,
                      uint64_t k, uint64_t nprobe, int has_max, double max_sq_dist,
                      uint64_t* out_ids, double* out_dists, uint32_t* out_counts);
+/* ivf_query_subset (ivf.cpp:230-245) for nq queries sharing one subset of
+ * ids (sorted ascending, unique; PQG_EINVAL "not sorted" otherwise): hits are
+ * restricted to the subset before the top-k. */
+int pqg_index_search_subset(pqg_ctx* ctx, const pqg_index* index, const float* queries,
+                            uint64_t nq, uint64_t k, const uint64_t* subset, uint64_t nsub,
+                            uint64_t nprobe, int has_max, double max_sq_dist, uint64_t* out_ids,
+                            double* out_dists, uint32_t* out_counts);
 /* probe_order (ivf.cpp:91-101) for nq queries: probes nq*nprobe (u32). */
 int pqg_index_probe(pqg_ctx* ctx, const pqg_index* index, const float* queries, uint64_t nq,
                     uint64_t nprobe, uint32_t* probes);

@@ -225,6 +225,26 @@ class COracle(_Base):
             raise ValueError(f"ivf_query rc={cnt}")
         return ids[:cnt], dist[:cnt]
 
+    def ivf_query_subset(self, tables, coarse, offsets, list_ids, list_codes, query, k, subset,
+                         nprobe, max_sq_dist=None):
+        tables = np.ascontiguousarray(tables, np.float32)
+        M, ks, ds = tables.shape
+        subset = np.ascontiguousarray(subset, np.uint64)
+        ids = np.empty(k, np.uint64)
+        dist = np.empty(k, np.float64)
+        f = self.fn("ivf_query_subset", C.c_int64,
+                    [_f32p, _u32, _u32, _u32, _f32p, _u64, _u64p, _u64p, _u8p, _f32p, _u64,
+                     C.c_void_p, _u64, _u64, C.c_int, C.c_double, _u64p, _f64p])
+        cnt = f(tables, M, ks, ds, np.ascontiguousarray(coarse, np.float32), coarse.shape[0],
+                np.ascontiguousarray(offsets, np.uint64), np.ascontiguousarray(list_ids, np.uint64),
+                np.ascontiguousarray(list_codes, np.uint8), np.ascontiguousarray(query, np.float32),
+                k, subset.ctypes.data if subset.size else None, subset.size, nprobe,
+                int(max_sq_dist is not None), 0.0 if max_sq_dist is None else float(max_sq_dist),
+                ids, dist)
+        if cnt < 0:
+            raise ValueError(f"ivf_query_subset rc={cnt}")
+        return ids[:cnt], dist[:cnt]
+
     def flat_scan(self, tables, codes, ids, query, k, max_sq_dist=None):
         tables = np.ascontiguousarray(tables, np.float32)
         M, ks, ds = tables.shape

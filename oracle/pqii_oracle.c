@@ -518,3 +518,55 @@ void orc_init_draws(uint64_t seed, uint64_t n, uint64_t k, uint64_t* out) {
     orc_mt_seed(&g, seed);
     for (uint64_t i = 0; i < k; ++i) out[i] = orc_uniform_index(&g, i, n - 1);
 }
+
+static int in_sorted(const uint64_t* s, uint64_t n, uint64_t v) { /* std::binary_search */
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) / 2;
+        if (s[mid] < v) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo < n && s[lo] == v;
+}
+
+/* proj/src/ivf.cpp:230-245 (ivf_query_subset) with scan_list_subset (:79-88):
+ * candidates whose id is not in the sorted subset are skipped before the
+ * distance test.  Returns the hit count or a negative status. */
+int64_t orc_ivf_query_subset(const float* tables, uint32_t M, uint32_t ks, uint32_t ds,
+                             const float* coarse, uint64_t nlist, const uint64_t* offsets,
+                             const uint64_t* list_ids, const uint8_t* list_codes, const float* query,
+                             uint64_t k, const uint64_t* subset, uint64_t nsub, uint64_t nprobe,
+                             int has_max, double max_sq_dist, uint64_t* out_ids, double* out_d) {
+    if (k == 0 || nprobe == 0 || nprobe > nlist) return ORC_EINVAL;
+    for (uint64_t i = 1; i < nsub; ++i)
+        if (subset[i - 1] >= subset[i]) return ORC_EINVAL;
+    const uint64_t D = (uint64_t)M * ds;
+    float* table = (float*)malloc((uint64_t)M * ks * sizeof(float));
+    uint32_t* probes = (uint32_t*)malloc(nprobe * sizeof(uint32_t));
+    orc_adc_table(tables, M, ks, ds, query, table);
+    orc_probe_order(coarse, nlist, D, query, nprobe, probes);
+    uint64_t cap = 0;
+    for (uint64_t p = 0; p < nprobe; ++p) cap += offsets[probes[p] + 1] - offsets[probes[p]];
+    orc_hit* hits = (orc_hit*)malloc((cap ? cap : 1) * sizeof(orc_hit));
+    uint64_t nh = 0;
+    const uint64_t rb = (uint64_t)M * code_width(ks);
+    int rc = 0;
+    for (uint64_t p = 0; p < nprobe && !rc; ++p) {
+        const uint64_t l = probes[p];
+        for (uint64_t e = offsets[l]; e < offsets[l + 1]; ++e) {
+            if (!in_sorted(subset, nsub, list_ids[e])) continue;
+            double dist;
+            rc = orc_adc_lookup(table, M, ks, list_codes + e * rb, 0, &dist);
+            if (rc) break;
+            if (has_max && dist > max_sq_dist) continue;
+            hits[nh].id = list_ids[e];
+            hits[nh].d = dist;
+            ++nh;
+        }
+    }
+    int64_t cnt = rc ? rc : (int64_t)finalize(hits, nh, k, out_ids, out_d);
+    free(hits);
+    free(table);
+    free(probes);
+    return cnt;
+}

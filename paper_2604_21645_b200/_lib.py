@@ -63,6 +63,8 @@ _SIGS = {
     "pqg_index_merge": (_i32, [_vp, _vp, _vp, C.POINTER(_vp)]),
     "pqg_index_search": (_i32, [_vp, _vp, _vp, _u64, _u64, _u64, _i32, _f64, _vp, _vp, _vp]),
     "pqg_index_probe": (_i32, [_vp, _vp, _vp, _u64, _u64, _vp]),
+    "pqg_index_search_subset": (_i32, [_vp, _vp, _vp, _u64, _u64, _vp, _u64, _u64, _i32, _f64, _vp,
+                                       _vp, _vp]),
     "pqg_flat_scan": (_i32, [_vp, _vp, _u32, _u32, _u32, _vp, _vp, _u64, _vp, _u64, _u64, _i32,
                              _f64, _vp, _vp, _vp]),
     "pqg_topk_merge": (_i32, [_vp, _vp, _vp, _vp, _u32, _u64, _u64, _vp, _vp, _vp]),

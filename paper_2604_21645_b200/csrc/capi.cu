@@ -1125,6 +1125,45 @@ int pqg_index_search(pqg_ctx* ctx, const pqg_index* ix, const float* queries, ui
     });
 }
 
+int pqg_index_search_subset(pqg_ctx* ctx, const pqg_index* ix, const float* queries, uint64_t nq,
+                            uint64_t k, const uint64_t* subset, uint64_t nsub, uint64_t nprobe,
+                            int has_max, double max_sq_dist, uint64_t* out_ids, double* out_dists,
+                            uint32_t* out_counts) {
+    return guard([&] {
+        Scope sc(ctx);
+        check_query(ix, k, nprobe);
+        // proj/src/ivf.cpp:234-238
+        if (nsub > 1) {
+            std::vector<uint64_t> hs(nsub);
+            PQG_CUDA(cudaMemcpy(hs.data(), subset, sizeof(uint64_t) * nsub, cudaMemcpyDefault));
+            for (uint64_t i = 1; i < nsub; ++i)
+                if (hs[i - 1] >= hs[i]) inval("ivf_query_subset: subset is not sorted ascending");
+        }
+        if (nq == 0) return;
+        const float* dq = in(ctx, queries, nq * ix->D());
+        const uint64_t* dsub = in(ctx, subset, std::max<uint64_t>(nsub, 1));
+        uint64_t* empty_sub = nullptr;
+        if (nsub == 0) {  // an empty subset admits nothing
+            empty_sub = scratch<uint64_t>(ctx, 1);
+            dsub = empty_sub;
+        }
+        auto oi = out(ctx, out_ids, nq * k);
+        auto od = out(ctx, out_dists, nq * k);
+        auto oc = out(ctx, out_counts, nq);
+        uint32_t* probes = scratch<uint32_t>(ctx, nq * nprobe);
+        ivf_probe(ctx, ix->view(), dq, nq, nprobe, probes);
+        reset_err(ctx);
+        ivf_scan(ctx, ix->view(), dq, nq, probes, nprobe, k, has_max, max_sq_dist, oi.dev, od.dev,
+                 oc.dev, ctx->d_err, dsub, nsub);
+        finish(ctx, oi);
+        finish(ctx, od);
+        finish(ctx, oc);
+        if (oi.host || od.host || oc.host) {
+            if (read_err(ctx)) fail(PQG_ERANGE, "adc_lookup: code out of range");
+        }
+    });
+}
+
 int pqg_flat_scan(pqg_ctx* ctx, const float* tables, uint32_t M, uint32_t ks, uint32_t ds,
                   const uint8_t* codes, const uint64_t* ids, uint64_t n, const float* queries,
                   uint64_t nq, uint64_t k, int has_max, double max_sq_dist, uint64_t* out_ids,

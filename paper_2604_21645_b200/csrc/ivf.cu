@@ -217,13 +217,26 @@ template <int RB, int W, int KS>
 __global__ void __launch_bounds__(kScanThreads) adc_scan_kernel(
     const float* tables, uint32_t M, uint32_t ks, uint32_t ds, const float* queries,
     const uint64_t* offsets, const uint64_t* ids, const uint8_t* codes, const uint32_t* probes,
-    uint64_t nprobe, int k, int has_max, double max_sq, uint64_t* out_ids, double* out_dists,
-    uint32_t* out_counts, int* err) {
+    uint64_t nprobe, int k, int has_max, double max_sq, const uint64_t* subset, uint64_t nsub,
+    uint64_t* out_ids, double* out_dists, uint32_t* out_counts, int* err) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* lut = reinterpret_cast<float*>(smem_raw);  // [M][ks]
     TopK* wl = reinterpret_cast<TopK*>(smem_raw + ((sizeof(float) * M * ks + 15) & ~size_t(15)));
     const uint64_t q = blockIdx.x;
     const uint32_t w = ks <= 256 ? 1 : 2;
+    // ivf_query_subset (proj/src/ivf.cpp:79-88): candidates outside the sorted
+    // subset are skipped before they can enter the top-k
+    auto member = [&](uint64_t id) {
+        if (!subset) return true;
+        uint64_t lo = 0, hi = nsub;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            const uint64_t v = __ldg(subset + mid);
+            if (v == id) return true;
+            if (v < id) lo = mid + 1; else hi = mid;
+        }
+        return false;
+    };
     const uint32_t rb = M * w;
     const uint64_t D = uint64_t(M) * ds;
     const float* qv = queries + q * D;
@@ -275,7 +288,7 @@ __global__ void __launch_bounds__(kScanThreads) adc_scan_kernel(
                             for (int m = 0; m < MM; ++m)
                                 s64 = __dadd_rn(s64, (double)lut[m * ksc + row.template get<W>(m)]);
                             id = ids[e];
-                            want = !(has_max && s64 > max_sq);
+                            want = !(has_max && s64 > max_sq) && member(id);
                         }
                     }
                 } else {
@@ -290,7 +303,7 @@ __global__ void __launch_bounds__(kScanThreads) adc_scan_kernel(
                             for (uint32_t m = 0; m < M; ++m)
                                 s64 = __dadd_rn(s64, (double)lut[m * ks + code_at(cr, m, w)]);
                             id = ids[e];
-                            want = !(has_max && s64 > max_sq);
+                            want = !(has_max && s64 > max_sq) && member(id);
                         }
                     }
                 }
@@ -473,7 +486,8 @@ void ivf_probe(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t
 
 void ivf_scan(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t nq,
               const uint32_t* probes, uint64_t nprobe, uint64_t k, int has_max, double max_sq,
-              uint64_t* out_ids, double* out_dists, uint32_t* out_counts, int* err) {
+              uint64_t* out_ids, double* out_dists, uint32_t* out_counts, int* err,
+              const uint64_t* subset, uint64_t nsub) {
     if (k > 32) fail(PQG_EUNSUPPORTED, "search: k > 32 is not supported by the warp top-k path");
     const size_t lut_bytes = (sizeof(float) * ix.M * ix.ks + 15) & ~size_t(15);
     const size_t smem = lut_bytes + sizeof(TopK) * k * (kScanThreads / 32);
@@ -485,8 +499,8 @@ void ivf_scan(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t 
             const uint64_t nc = std::min<uint64_t>(65535, nq - q0);
             launch(ctx, "adc_scan", kern, dim3(unsigned(nc)), dim3(kScanThreads), smem, ix.tables,
                    ix.M, ix.ks, ix.ds, queries + q0 * ix.M * ix.ds, ix.offsets, ix.ids, ix.codes,
-                   probes + q0 * nprobe, nprobe, int(k), has_max, max_sq, out_ids + q0 * k,
-                   out_dists + q0 * k, out_counts + q0, err);
+                   probes + q0 * nprobe, nprobe, int(k), has_max, max_sq, subset, nsub,
+                   out_ids + q0 * k, out_dists + q0 * k, out_counts + q0, err);
         }
     };
     // vector code loads need rb-aligned rows (CSR rows are rb apart from an aligned base)

@@ -118,7 +118,8 @@ void ivf_probe(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t
                uint64_t nprobe, uint32_t* probes);
 void ivf_scan(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t nq,
               const uint32_t* probes, uint64_t nprobe, uint64_t k, int has_max, double max_sq,
-              uint64_t* out_ids, double* out_dists, uint32_t* out_counts, int* err);
+              uint64_t* out_ids, double* out_dists, uint32_t* out_counts, int* err,
+              const uint64_t* subset = nullptr, uint64_t nsub = 0);
 void csr_scatter(pqg_ctx* ctx, const uint32_t* perm, uint64_t n, const uint64_t* ids,
                  const uint8_t* codes, uint64_t row_bytes, uint64_t* out_ids, uint8_t* out_codes);
 void find_duplicate(pqg_ctx* ctx, const uint64_t* ids, uint64_t n, uint64_t* first_dup_pos);

@@ -524,24 +524,14 @@ QueryResult ivf_query_subset(const InvertedIndex& index, std::span<const float> 
                              std::size_t k, std::span<const std::uint64_t> subset,
                              std::size_t nprobe, std::optional<double> max_sq_dist) {
     check_query(index, query, k, nprobe);
-    for (std::size_t i = 1; i < subset.size(); ++i)
-        if (subset[i - 1] >= subset[i])
-            throw std::invalid_argument("ivf_query_subset: subset is not sorted ascending");
     IndexPtr dev = device_index_for(index);
-    std::vector<std::uint32_t> probes(nprobe);
-    raise(pqg_index_probe(ctx(), dev.get(), query.data(), 1, nprobe, probes.data()));
-    // candidates of the probed lists that are members of the subset
-    CodeMatrix cand(0, index.codebook.m_subspaces, index.codebook.ks);
-    std::vector<std::uint64_t> cand_ids;
-    for (const std::uint32_t l : probes) {
-        const PostingList& pl = index.lists[l];
-        for (std::size_t i = 0; i < pl.ids.size(); ++i) {
-            if (!std::binary_search(subset.begin(), subset.end(), pl.ids[i])) continue;
-            cand_ids.push_back(pl.ids[i]);
-            cand.append_row_from(pl.codes, i);
-        }
-    }
-    return flat_scan(index.codebook, cand, cand_ids, query, k, max_sq_dist);
+    std::vector<std::uint64_t> ids(k);
+    std::vector<double> d(k);
+    std::uint32_t cnt = 0;
+    raise(pqg_index_search_subset(ctx(), dev.get(), query.data(), 1, k, subset.data(), subset.size(),
+                                  nprobe, max_sq_dist.has_value(), max_sq_dist.value_or(0.0),
+                                  ids.data(), d.data(), &cnt));
+    return result_of(ids.data(), d.data(), cnt, k);
 }
 
 QueryResult flat_scan(const Codebook& cb, const CodeMatrix& codes,

@@ -618,22 +618,22 @@ def flat_scan(cb: Codebook, codes: CodeMatrix, ids, query, k: int, max_sq_dist=N
 
 def ivf_query_subset(index: InvertedIndex, query, k: int, subset, nprobe: int,
                      max_sq_dist=None) -> QueryResult:
-    """ivf.cpp:230-245.  Row-filtered search is SURVEY 8(f) rank 3 ("next");
-    it is expressed here through the device flat scan over the probed lists'
-    subset members so the semantics match."""
+    """ivf.cpp:230-245: ivf_query restricted to ids in ``subset`` (sorted
+    ascending, unique); the membership test runs inside the device scan."""
     subset = np.ascontiguousarray(subset, np.uint64)
+    q = np.ascontiguousarray(query, np.float32).reshape(1, -1)
+    _, _, M, _, ds = index._info()
     if k == 0:
         raise ValueError("query: k must be >= 1")
-    if subset.size > 1 and np.any(subset[1:] <= subset[:-1]):
-        raise ValueError("ivf_query_subset: subset is not sorted ascending")
-    nl = index.nlist()
-    if nprobe == 0 or nprobe > nl:
-        raise ValueError(f"query: nprobe ({nprobe}) must be in [1, nlist={nl}]")
-    off, ids, codes, _, cb = index.export()
-    probes = ivf_probe(index, np.asarray(query, np.float32).reshape(1, -1), nprobe)[0]
-    sel = np.concatenate([np.arange(off[l], off[l + 1]) for l in probes]).astype(np.int64)
-    keep = sel[np.isin(ids[sel], subset)]
-    if keep.size == 0:
-        return QueryResult([], k)
-    sub = CodeMatrix(keep.size, cb.m_subspaces, cb.ks, codes[keep])
-    return flat_scan(cb, sub, ids[keep], query, k, max_sq_dist, index.ctx)
+    if q.shape[1] != M * ds:
+        raise ValueError("query: dimension mismatch")
+    ctx = index.ctx
+    ids = np.zeros((1, k), np.uint64)
+    dist = np.zeros((1, k), np.float64)
+    cnt = np.zeros(1, np.uint32)
+    v = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    _lib.check(ctx.lib.pqg_index_search_subset(
+        ctx.h, index.h, v(q), 1, k, v(subset) if subset.size else None, subset.size, nprobe,
+        int(max_sq_dist is not None), 0.0 if max_sq_dist is None else float(max_sq_dist), v(ids),
+        v(dist), v(cnt)), "ivf_query_subset")
+    return _to_result(ids[0], dist[0], cnt[0], k)

@@ -102,6 +102,12 @@ def main() -> None:
         g[f"ivf/q_np{nprobe}_count"] = oc
     oi, od, oc = h.query_batch(qs, 10, 4, max_sq_dist=60.0)
     g["ivf/q_max_ids"], g["ivf/q_max_dist"], g["ivf/q_max_count"] = oi, od, oc
+    subset = ids[::3].copy()  # every third item (sorted ascending)
+    sub = [h.query_subset(qi, 10, subset, 6) for qi in qs]
+    g["ivf/subset"] = subset
+    g["ivf/q_sub_ids"] = np.stack([np.pad(s_[0], (0, 10 - len(s_[0]))) for s_ in sub])
+    g["ivf/q_sub_count"] = np.array([len(s_[0]) for s_ in sub], np.uint32)
+    g["ivf/q_sub_dist"] = np.stack([np.pad(s_[1], (0, 10 - len(s_[1]))) for s_ in sub])
     fl = [R.flat_scan(tables, codes, ids, qi, 10) for qi in qs]
     g["ivf/flat_ids"] = np.stack([f[0] for f in fl])
     g["ivf/flat_dist"] = np.stack([f[1] for f in fl])

@@ -480,3 +480,16 @@ def test_pq_fit_both_screens(pq, orc, mix, screen, M, ks):
     cb = pq.pq_fit(x, M, ks, 10, 3, stats=stats)
     assert np.array_equal(stats["iterations_run"], it)
     assert np.array_equal(bits(cb.tables), bits(t))
+
+
+def test_ivf_query_subset_golden_gpu(pq, gidx, golden):
+    _, _, index = gidx
+    for qi, q in enumerate(golden["ivf/queries"]):
+        r = pq.ivf_query_subset(index, q, 10, golden["ivf/subset"], 6)
+        c = int(golden["ivf/q_sub_count"][qi])
+        assert [h.id for h in r.hits] == golden["ivf/q_sub_ids"][qi, :c].tolist()
+        assert np.array_equal(bits(np.array([h.sq_dist for h in r.hits], np.float64)),
+                              bits(golden["ivf/q_sub_dist"][qi, :c]))
+    with pytest.raises(ValueError, match="not sorted"):
+        pq.ivf_query_subset(index, golden["ivf/queries"][0], 10, golden["ivf/subset"][::-1], 6)
+    assert pq.ivf_query_subset(index, golden["ivf/queries"][0], 10, [], 6).hits == []

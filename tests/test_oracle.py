@@ -147,3 +147,13 @@ def test_oracle_vs_ref_ivf_query(orc, ref, golden):
                                   q, 7, 9)
         assert np.array_equal(ids, ri[qi, : rc[qi]])
         assert np.array_equal(bits(dist), bits(rd[qi, : rc[qi]]))
+
+
+def test_ivf_query_subset_golden(golden, orc):
+    off, lid, lcodes = golden["ivf/offsets"], golden["ivf/list_ids"], golden["ivf/list_codes"]
+    for qi, q in enumerate(golden["ivf/queries"]):
+        ids, dist = orc.ivf_query_subset(golden["pq/tables"], golden["ivf/coarse"], off, lid, lcodes,
+                                         q, 10, golden["ivf/subset"], 6)
+        c = int(golden["ivf/q_sub_count"][qi])
+        assert np.array_equal(ids, golden["ivf/q_sub_ids"][qi, :c])
+        assert np.array_equal(bits(dist), bits(golden["ivf/q_sub_dist"][qi, :c]))
