@@ -9,7 +9,7 @@
  * negative status; pqg_last_error() returns the thread's last message.
  * Status mapping to the reference's exceptions:
  *   PQG_EINVAL -> std::invalid_argument   PQG_ERANGE -> std::out_of_range
- *   PQG_ECUDA / PQG_ENOMEM / PQG_EUNSUPPORTED -> std::runtime_error
+ *   PQG_ECUDA / PQG_ENOMEM / PQG_EUNSUPPORTED / PQG_ECHUNK -> std::runtime_error
  * Message substrings follow the reference ("not divisible", "exceeds",
  * "no items", "duplicate id", "nprobe", ...).
  *
@@ -37,6 +37,7 @@ extern "C" {
 #define PQG_ECUDA (-3)
 #define PQG_ENOMEM (-4)
 #define PQG_EUNSUPPORTED (-5)
+#define PQG_ECHUNK (-6) /* a pipeline chunk task failed: std::runtime_error("chunk <id>: ...") */
 
 typedef struct pqg_ctx pqg_ctx;     /* one GPU + stream + scratch arena */
 typedef struct pqg_index pqg_index; /* device-resident inverted index */
@@ -165,6 +166,44 @@ int pqg_flat_scan(pqg_ctx* ctx, const float* tables, uint32_t M, uint32_t ks, ui
 int pqg_topk_merge(pqg_ctx* ctx, const uint64_t* ids, const double* dists,
                    const uint32_t* counts, uint32_t shards, uint64_t nq, uint64_t k,
                    uint64_t* out_ids, double* out_dists, uint32_t* out_counts);
+
+/* ---- L3: the paper's chunked pipeline (proj/src/pipeline.cpp) ----------- */
+#define PQG_MODE_SINGLE 0            /* PipelineMode::kSingle */
+#define PQG_MODE_PARALLEL_PQ 1       /* PipelineMode::kParallelPq */
+#define PQG_MODE_PARALLEL_PQ_INDEX 2 /* PipelineMode::kParallelPqIndex */
+/* phase_seconds[] slots (the reference's phase_seconds keys); -1 = not run */
+#define PQG_PHASE_FIT 0
+#define PQG_PHASE_CHUNKING 1
+#define PQG_PHASE_LOCAL_FIT 2
+#define PQG_PHASE_GLOBAL_FIT 3
+#define PQG_PHASE_COARSE_FIT 4
+#define PQG_PHASE_ENCODE 5
+#define PQG_PHASE_INDEX_BUILD 6
+#define PQG_PHASE_MERGE 7
+#define PQG_PHASE_COUNT 8
+/* train_chunk (pipeline.cpp:84-106) for all chunk_rows(n, n_chunks) chunks
+ * in one batched k-means (n_chunks*M problems; chunk c seeds seed+c).
+ * representatives (n_chunks*ks) x D (the decoded local codewords, in chunk
+ * order = aggregate_representatives, :108-135), local_rmse n_chunks,
+ * iterations_run n_chunks*M -- all nullable.  Errors as run_chunk_tasks
+ * (pipeline.cpp:30-62): PQG_ECHUNK "chunk <id>: ..." for the lowest failing
+ * chunk. */
+int pqg_train_chunks(pqg_ctx* ctx, const float* data, uint64_t n, uint64_t D, uint64_t n_chunks,
+                     uint32_t M, uint32_t ks, uint32_t max_iters, uint64_t seed,
+                     float* representatives, double* local_rmse, uint32_t* iterations_run);
+/* run_pipeline (pipeline.cpp:142-266) with the data resident on the device
+ * between phases.  nlist 0 = default_nlist(n) (capped at n_chunks*ks in
+ * PARALLEL_PQ_INDEX mode); nlist_used receives the resolved value.
+ * global_tables M*ks*(D/M); representatives (n_chunks*ks) x D and
+ * local_rmse[n_chunks] (parallel modes, nullable); merged_index (index mode,
+ * nullable; the caller destroys it); phase_seconds[PQG_PHASE_COUNT]
+ * (nullable).  The thread count of the reference is not a parameter: the
+ * result never depended on it (pipeline.hpp:74-78). */
+int pqg_pipeline_run(pqg_ctx* ctx, const float* data, uint64_t n, uint64_t D, uint64_t n_chunks,
+                     uint32_t M, uint32_t ks, uint64_t nlist, uint32_t max_iters, uint64_t seed,
+                     int mode, float* global_tables, double* global_rmse, float* representatives,
+                     double* local_rmse, uint64_t* nlist_used, pqg_index** merged_index,
+                     double* phase_seconds);
 
 /* ---- sharded k-means steps (multi-GPU driver) ------------ */
 /* One assignment pass of a batch of B k-means problems over a row shard:

@@ -268,6 +268,71 @@ class COracle(_Base):
         return b
 
 
+    # -- the chunked pipeline (proj/src/pipeline.cpp) -------------------------
+    def train_chunk(self, chunk, M, ks, max_iters, chunk_seed):
+        """train_chunk (pipeline.cpp:84-106): (representatives ks x D, local rmse)."""
+        chunk = np.ascontiguousarray(chunk, np.float32)
+        n, D = chunk.shape
+        reps = np.empty((ks, D), np.float32)
+        r = C.c_double()
+        rc = self.fn("train_chunk", C.c_int, [_f32p, _u64, _u64, _u32, _u32, _u32, _u64, _f32p,
+                                              C.POINTER(C.c_double)])(
+            chunk, n, D, M, ks, max_iters, chunk_seed, reps, C.byref(r))
+        if rc:
+            raise ValueError(f"train_chunk rc={rc}")
+        return reps, r.value
+
+    def run_pipeline(self, data, n_chunks, M, ks, nlist=0, max_iters=20, seed=0, mode="single"):
+        """run_pipeline (pipeline.cpp:142-266) composed from the restated pieces:
+        chunk_rows -> train_chunk(seed + c) per chunk -> concatenation in chunk
+        order (aggregate_representatives, :108-135) -> pq_fit(reps, seed)
+        (fit_global, :137-140) -> reconstruction rmse on the data; index mode
+        adds kmeans_fit(reps, nlist, iters, seed + M) for the shared coarse
+        centroids, per-chunk ivf_build_with_centroids with ids [begin, end) and
+        the per-list a-then-b merge (ivf.cpp:186-216)."""
+        data = np.ascontiguousarray(data, np.float32)
+        n, D = data.shape
+        out = {}
+        if nlist == 0:
+            nlist = max(1, min(n, int(np.floor(np.sqrt(float(n)) + 0.5))))
+            if mode == "parallel_pq_index":
+                nlist = min(nlist, n_chunks * ks)
+        out["nlist"] = nlist
+        if mode == "single":
+            tables, _, _ = self.pq_fit(data, M, ks, max_iters, seed)
+            out["tables"] = tables
+            out["rmse"] = self.rmse(data, self.pq_decode(self.pq_encode(data, tables), tables))
+            return out
+        bounds = self.chunk_rows(n, n_chunks)
+        reps, local = [], []
+        for c in range(n_chunks):
+            r, lr = self.train_chunk(data[bounds[c]:bounds[c + 1]], M, ks, max_iters, seed + c)
+            reps.append(r)
+            local.append(lr)
+        reps = np.concatenate(reps)
+        tables, _, _ = self.pq_fit(reps, M, ks, max_iters, seed)
+        codes = self.pq_encode(data, tables)
+        out.update(tables=tables, representatives=reps, local_rmse=np.array(local),
+                   rmse=self.rmse(data, self.pq_decode(codes, tables)))
+        if mode == "parallel_pq_index":
+            coarse = self.kmeans_fit(reps, nlist, max_iters, seed + M)["centroids"]
+            lists_ids = [[] for _ in range(nlist)]
+            lists_codes = [[] for _ in range(nlist)]
+            for c in range(n_chunks):
+                b0, b1 = int(bounds[c]), int(bounds[c + 1])
+                ids = np.arange(b0, b1, dtype=np.uint64)
+                off, lid, lcodes = self.ivf_build_with_centroids(codes[b0:b1], ids, tables, coarse)
+                for l in range(nlist):
+                    lists_ids[l].append(lid[off[l]:off[l + 1]])
+                    lists_codes[l].append(lcodes[off[l]:off[l + 1]])
+            sizes = [sum(len(a) for a in li) for li in lists_ids]
+            out["coarse"] = coarse
+            out["offsets"] = np.concatenate([[0], np.cumsum(sizes)]).astype(np.uint64)
+            out["list_ids"] = np.concatenate([np.concatenate(li) for li in lists_ids])
+            out["list_codes"] = np.concatenate([np.concatenate(li) for li in lists_codes])
+        return out
+
+
 class RefImpl(_Base):
     """The reference compiled from its own sources (``oracle/_ref``)."""
 
@@ -465,6 +530,54 @@ class RefImpl(_Base):
 
     def hardware_concurrency(self):
         return self.lib.ref_hardware_concurrency()
+
+    def train_chunk(self, chunk, M, ks, max_iters, chunk_seed):
+        chunk = np.ascontiguousarray(chunk, np.float32)
+        n, D = chunk.shape
+        reps = np.empty((ks, D), np.float32)
+        r = C.c_double()
+        rc = self.fn("train_chunk", C.c_int, [_f32p, _u64, _u64, _u32, _u32, _u32, _u64, _f32p,
+                                              C.POINTER(C.c_double)])(
+            chunk, n, D, M, ks, max_iters, chunk_seed, reps, C.byref(r))
+        self._check(rc, "train_chunk")
+        return reps, r.value
+
+    def run_pipeline(self, data, n_chunks, M, ks, nlist=0, max_iters=20, seed=0,
+                     mode="single", threads=1):
+        """The reference's own run_pipeline; returns a dict like
+        COracle.run_pipeline plus "phases" (name -> seconds) and "total"."""
+        data = np.ascontiguousarray(data, np.float32)
+        n, D = data.shape
+        m = {"single": 0, "parallel_pq": 1, "parallel_pq_index": 2}[mode]
+        tables = np.empty((M, ks, D // max(M, 1)), np.float32)
+        reps = np.empty((n_chunks * ks, D), np.float32) if m else None
+        rm = C.c_double()
+        nl = C.c_uint64()
+        h = C.c_void_p()
+        ph = np.empty(9, np.float64)
+        err = C.create_string_buffer(512)
+        rc = self.fn("run_pipeline", C.c_int,
+                     [_f32p, _u64, _u64, _u64, _u32, _u32, _u64, _u32, _u64, _u64, C.c_int,
+                      _f32p, C.POINTER(C.c_double), C.c_void_p, C.POINTER(C.c_uint64),
+                      C.POINTER(C.c_void_p), _f64p, C.c_char_p, _u64])(
+            data, n, D, n_chunks, M, ks, nlist, max_iters, seed, threads, m, tables, C.byref(rm),
+            None if reps is None else reps.ctypes.data, C.byref(nl), C.byref(h), ph, err, 512)
+        if rc:
+            msg = err.value.decode()
+            if rc == -1:
+                raise ValueError(msg)
+            raise RuntimeError(msg)
+        names = ["fit", "chunking", "local_fit", "global_fit", "coarse_fit", "encode",
+                 "index_build", "merge"]
+        out = dict(tables=tables, rmse=rm.value, nlist=nl.value,
+                   phases={k: float(v) for k, v in zip(names, ph[:8]) if v >= 0}, total=float(ph[8]))
+        if reps is not None:
+            out["representatives"] = reps
+        if h.value:
+            hd = RefIndexHandle(self, h.value, M * code_width(ks), D)
+            off, lid, lcodes, coarse = hd.export()
+            out.update(offsets=off, list_ids=lid, list_codes=lcodes, coarse=coarse)
+        return out
 
 
 class RefIndexHandle:

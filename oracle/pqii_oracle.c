@@ -320,6 +320,35 @@ double orc_rmse(const float* a, const float* b, uint64_t rows, uint64_t dims) {
     return sqrt(total / (double)(rows * dims));
 }
 
+/* proj/src/pipeline.cpp:84-106 (train_chunk): a local pq_fit with the chunk's
+ * seed, representative j = codeword j of every subspace concatenated
+ * (reps ks x D), and the chunk's reconstruction rmse under its own codebook
+ * (reconstruction_rmse = rmse(chunk, decode(encode(chunk))), pq.cpp:179-181). */
+int orc_train_chunk(const float* chunk, uint64_t n, uint64_t D, uint32_t M, uint32_t ks,
+                    uint32_t max_iters, uint64_t chunk_seed, float* reps, double* local_rmse) {
+    if (n < ks) return ORC_EINVAL; /* pipeline.cpp:86-89 */
+    if (M == 0 || D % M != 0) return ORC_EINVAL;
+    const uint64_t ds = D / M;
+    float* tables = (float*)malloc((uint64_t)M * ks * ds * sizeof(float));
+    uint8_t* codes = (uint8_t*)malloc(n * M * code_width(ks));
+    float* dec = (float*)malloc(n * D * sizeof(float));
+    int rc = (tables && codes && dec) ? ORC_OK : ORC_ENOMEM;
+    if (rc == ORC_OK) rc = orc_pq_fit(chunk, n, D, M, ks, max_iters, chunk_seed, tables, NULL, NULL);
+    if (rc == ORC_OK) {
+        for (uint32_t j = 0; j < ks; ++j)
+            for (uint32_t m = 0; m < M; ++m)
+                memcpy(reps + (uint64_t)j * D + m * ds, tables + ((uint64_t)m * ks + j) * ds,
+                       ds * sizeof(float));
+        orc_pq_encode(chunk, n, M, ks, (uint32_t)ds, tables, codes);
+        rc = orc_pq_decode(codes, n, M, ks, (uint32_t)ds, tables, dec);
+        if (rc == ORC_OK) *local_rmse = orc_rmse(chunk, dec, n, D);
+    }
+    free(tables);
+    free(codes);
+    free(dec);
+    return rc;
+}
+
 /* proj/src/pq.cpp:132-151: entries are float(fp64 squared_l2). */
 void orc_adc_table(const float* tables, uint32_t M, uint32_t ks, uint32_t ds, const float* query,
                    float* entries) {

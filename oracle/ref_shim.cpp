@@ -20,6 +20,7 @@
 #include "pqii/dataset_io.hpp"
 #include "pqii/ivf.hpp"
 #include "pqii/kmeans.hpp"
+#include "pqii/pipeline.hpp"
 #include "pqii/pq.hpp"
 
 using namespace pqii;
@@ -395,5 +396,75 @@ int ref_chunk_rows(std::uint64_t n, std::uint64_t c, std::uint64_t* bounds) {
 }
 
 unsigned ref_hardware_concurrency() { return std::thread::hardware_concurrency(); }
+
+// train_chunk (proj/src/pipeline.cpp:84-106) on one chunk of rows.
+int ref_train_chunk(const float* chunk, std::uint64_t n, std::uint64_t D, std::uint32_t M,
+                    std::uint32_t ks, std::uint32_t iters, std::uint64_t chunk_seed, float* reps,
+                    double* local_rmse) {
+    return guarded([&] {
+        const ChunkOutput out = train_chunk(as_matrix(chunk, n, D), M, ks, iters, chunk_seed);
+        std::memcpy(reps, out.representatives.values.data(),
+                    out.representatives.values.size() * sizeof(float));
+        *local_rmse = out.local_rmse;
+    });
+}
+
+// run_pipeline (proj/src/pipeline.cpp:142-266).  reps: n_chunks*ks*D (parallel
+// modes, nullable); index: the merged index as a RefIndex handle (index mode,
+// nullable); phases: fit, chunking, local_fit, global_fit, coarse_fit, encode,
+// index_build, merge seconds (-1 when absent), total last (9 entries).
+int ref_run_pipeline(const float* data, std::uint64_t n, std::uint64_t D, std::uint64_t n_chunks,
+                     std::uint32_t M, std::uint32_t ks, std::uint64_t nlist, std::uint32_t iters,
+                     std::uint64_t seed, std::uint64_t threads, int mode, float* tables,
+                     double* global_rmse, float* reps, std::uint64_t* nlist_used, void** index,
+                     double* phases, char* err, std::uint64_t err_len) {
+    int rc = -4;
+    std::string msg;
+    try {
+        PipelineConfig cfg;
+        cfg.n_chunks = n_chunks;
+        cfg.m_subspaces = M;
+        cfg.ks = ks;
+        cfg.nlist = nlist;
+        cfg.kmeans_iters = iters;
+        cfg.seed = seed;
+        cfg.n_threads = threads;
+        cfg.mode = mode == 0 ? PipelineMode::kSingle
+                             : (mode == 1 ? PipelineMode::kParallelPq : PipelineMode::kParallelPqIndex);
+        PipelineReport r = run_pipeline(as_matrix(data, n, D), cfg);
+        std::memcpy(tables, r.global_codebook.tables.data(),
+                    r.global_codebook.tables.size() * sizeof(float));
+        *global_rmse = r.global_rmse;
+        if (nlist_used) *nlist_used = r.config.nlist;
+        if (reps && r.representatives)
+            std::memcpy(reps, r.representatives->values.data(),
+                        r.representatives->values.size() * sizeof(float));
+        if (index) *index = r.merged_index ? new RefIndex{std::move(*r.merged_index)} : nullptr;
+        if (phases) {
+            const char* names[8] = {"fit", "chunking", "local_fit", "global_fit",
+                                    "coarse_fit", "encode", "index_build", "merge"};
+            for (int i = 0; i < 8; ++i) {
+                auto it = r.phase_seconds.find(names[i]);
+                phases[i] = it == r.phase_seconds.end() ? -1.0 : it->second;
+            }
+            phases[8] = r.total_seconds;
+        }
+        rc = 0;
+    } catch (const std::invalid_argument& e) {
+        rc = -1;
+        msg = e.what();
+    } catch (const std::out_of_range& e) {
+        rc = -2;
+        msg = e.what();
+    } catch (const std::exception& e) {
+        rc = -4;
+        msg = e.what();
+    }
+    if (err && err_len) {
+        std::strncpy(err, msg.c_str(), err_len - 1);
+        err[err_len - 1] = 0;
+    }
+    return rc;
+}
 
 }  // extern "C"

@@ -18,6 +18,7 @@ PQG_ERANGE = -2
 PQG_ECUDA = -3
 PQG_ENOMEM = -4
 PQG_EUNSUPPORTED = -5
+PQG_ECHUNK = -6  # a pipeline chunk task failed (std::runtime_error)
 
 _vp = C.c_void_p
 _u64 = C.c_uint64
@@ -72,6 +73,11 @@ _SIGS = {
     "pqg_update_pass": (_i32, [_vp, _vp, _u64, _u64, _u32, _u32, _u32, _vp, _u64, _vp, _vp, _vp]),
     "pqg_rows_sum_f64": (_i32, [_vp, _vp, _u64, _u32, _vp]),
     "pqg_kmeans_init_rows": (_i32, [_u64, _u64, _u64, _vp]),
+    "pqg_train_chunks": (_i32, [_vp, _vp, _u64, _u64, _u64, _u32, _u32, _u32, _u64, _vp, _vp,
+                                _vp]),
+    "pqg_pipeline_run": (_i32, [_vp, _vp, _u64, _u64, _u64, _u32, _u32, _u64, _u32, _u64, _i32,
+                                _vp, C.POINTER(_f64), _vp, _vp, C.POINTER(_u64), C.POINTER(_vp),
+                                _vp]),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -110,4 +116,6 @@ def check(rc: int, what: str = "") -> None:
         raise ValueError(msg)          # std::invalid_argument
     if rc == PQG_ERANGE:
         raise IndexError(msg)          # std::out_of_range
+    if rc == PQG_ECHUNK:
+        raise PQGError(msg)            # run_chunk_tasks' runtime_error("chunk <id>: ...")
     raise PQGError(f"{what}: {msg} (status {rc})")

@@ -9,6 +9,7 @@
 // every numeric result comes from the kernels in nearest.cu, kmeans.cu,
 // pq.cu and ivf.cu.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <numeric>
@@ -264,16 +265,28 @@ struct KMeansOut {
 };
 
 // x: device rows (n x ldx); table (device, B*k*d) receives the centroids;
-// assign (device, B*n u32) receives the final assignments.
+// assign (device, B*n u32) receives the final assignments.  counts (optional,
+// B entries <= n): problem b fits only its first counts[b] rows -- the
+// batched local fits of the chunked pipeline, whose chunks differ by a row.
 static KMeansOut run_kmeans(pqg_ctx* ctx, const float* x, uint64_t n, uint64_t ldx, uint32_t B,
                             uint32_t d, uint32_t col_stride, uint64_t k, uint32_t max_iters,
                             const std::vector<uint64_t>& seeds, double tol, float* table,
-                            uint32_t* assign) {
+                            uint32_t* assign, const std::vector<uint64_t>* counts = nullptr) {
     std::vector<uint64_t> rows;
     rows.reserve(uint64_t(B) * k);
+    uint64_t max_pad = 0;
     for (uint32_t b = 0; b < B; ++b) {
-        auto r = init_rows(n, k, seeds[b]);
+        const uint64_t nb = counts ? (*counts)[b] : n;
+        max_pad = std::max(max_pad, n - nb);
+        auto r = init_rows(nb, k, seeds[b]);
         rows.insert(rows.end(), r.begin(), r.end());
+    }
+    const uint64_t* d_nb = nullptr;
+    if (max_pad) {
+        uint64_t* p = scratch<uint64_t>(ctx, B);
+        PQG_CUDA(cudaMemcpyAsync(p, counts->data(), sizeof(uint64_t) * B, cudaMemcpyHostToDevice,
+                                 ctx->stream));
+        d_nb = p;
     }
     uint64_t* d_rows = scratch<uint64_t>(ctx, rows.size());
     PQG_CUDA(cudaMemcpyAsync(d_rows, rows.data(), rows.size() * sizeof(uint64_t),
@@ -332,9 +345,10 @@ static KMeansOut run_kmeans(pqg_ctx* ctx, const float* x, uint64_t n, uint64_t l
             a.big_nx = prep.big_nx;
         }
         nearest(ctx, a);
-        kmeans_inertia_and_stop(ctx, dist, n, B, it, max_iters, tol, st);
+        kmeans_pad_keys(ctx, assign, n, B, k, d_nb, max_pad);
+        kmeans_inertia_and_stop(ctx, dist, n, B, it, max_iters, tol, st, d_nb);
         if (it == max_iters) break;
-        kmeans_update(ctx, src, n, B, d, table, k, assign, dist, st.active);
+        kmeans_update(ctx, src, n, B, d, table, k, assign, dist, st.active, d_nb);
     }
     KMeansOut o;
     o.inertia.resize(B);
@@ -384,6 +398,20 @@ static void check_pq_shape(uint32_t M, uint32_t ks, uint32_t ds, const char* who
     if (M == 0) inval(std::string(who) + ": M must be >= 1");
     if (ks == 0 || ks > 65536) inval(std::string(who) + ": Ks must be in [1, 65536]");
     if (ds == 0) inval(std::string(who) + ": sub_dim must be >= 1");
+}
+
+// pq_fit's argument checks, in its order (proj/src/pq.cpp:65-75, then
+// kmeans_fit's max_iters check, kmeans.cpp:70)
+static void check_pq_fit(uint64_t n, uint64_t D, uint32_t M, uint32_t ks, uint32_t max_iters) {
+    if (M == 0) inval("pq_fit: M must be >= 1");
+    if (D % M != 0)
+        inval("pq_fit: D (" + std::to_string(D) + ") is not divisible by M (" + std::to_string(M) +
+              ")");
+    if (ks > n)
+        inval("pq_fit: Ks (" + std::to_string(ks) + ") exceeds number of rows (" +
+              std::to_string(n) + ")");
+    check_pq_shape(M, uint32_t(ks), uint32_t(D / M), "codebook");
+    if (max_iters < 1) inval("kmeans_fit: max_iters must be >= 1");
 }
 
 // ---------------------------------------------------------------------------
@@ -446,6 +474,98 @@ static uint32_t* assign_lists(pqg_ctx* ctx, const float* tables, uint32_t M, uin
     nearest(ctx, a);
     if (read_err(ctx)) fail(PQG_ERANGE, "pq_decode: code out of range for Ks=" + std::to_string(ks));
     return list_of;
+}
+
+
+// ---------------------------------------------------------------------------
+// the paper's chunked pipeline (proj/src/pipeline.cpp)
+// ---------------------------------------------------------------------------
+// chunk_rows (proj/src/dataset_io.cpp:322-339) as (base, extra): chunk c holds
+// base + (c < extra) rows.
+static void check_chunks(uint64_t n, uint64_t C) {
+    if (C == 0) inval("chunk_rows: n_chunks must be >= 1");
+    if (C > n)
+        inval("chunk_rows: n_chunks (" + std::to_string(C) + ") exceeds n_rows (" +
+              std::to_string(n) + ")");
+}
+
+// run_chunk_tasks reports the lowest-id failing chunk as a runtime_error
+// "chunk <id>: <what>" (pipeline.cpp:30-62); train_chunk checks the row count before pq_fit's own
+// checks (pipeline.cpp:84-90).  Chunk 0 is the largest, so a size-independent
+// pq_fit failure always surfaces as chunk 0.
+static void check_train_chunks(uint64_t n, uint64_t D, uint64_t C, uint32_t M, uint32_t ks,
+                               uint32_t iters) {
+    check_chunks(n, C);
+    const uint64_t base = n / C, extra = n % C, n_max = base + (extra ? 1 : 0);
+    auto rows_err = [&](uint64_t c, uint64_t rows) {
+        fail(PQG_ECHUNK, "chunk " + std::to_string(c) + ": train_chunk: chunk has " +
+                             std::to_string(rows) + " rows, fewer than ks=" + std::to_string(ks));
+    };
+    if (n_max < ks) rows_err(0, n_max);
+    try {
+        check_pq_fit(n_max, D, M, ks, iters);
+    } catch (Error& e) {
+        fail(PQG_ECHUNK, "chunk 0: " + e.msg);
+    }
+    if (base < ks) rows_err(extra, base);
+}
+
+struct ChunkFits {
+    float* reps = nullptr;       // device [C*ks][D]
+    std::vector<double> rmse;    // [C]
+    std::vector<uint32_t> iters; // [C*M]
+};
+
+// train_chunk for every chunk at once (pipeline.cpp:84-106): the C chunks are
+// laid side by side so the C*M local subspace fits run as ONE batched k-means
+// (problem c*M+m: chunk c's rows, subspace m's columns, seed (seed+c)+m, its
+// own init, tol stop and reseeds).  Each chunk's reconstruction RMSE comes
+// from the fit's final assignments.  x: device n x D.
+static ChunkFits train_chunks_dev(pqg_ctx* ctx, const float* x, uint64_t n, uint64_t D, uint64_t C,
+                                  uint32_t M, uint32_t ks, uint32_t iters, uint64_t seed) {
+    const uint64_t base = n / C, extra = n % C, n_max = base + (extra ? 1 : 0);
+    const uint32_t ds = uint32_t(D / M);
+    const uint64_t B64 = C * M;
+    if (B64 > (1u << 20)) fail(PQG_EUNSUPPORTED, "train_chunks: n_chunks * M too large");
+    const uint32_t B = uint32_t(B64);
+    const float* y = x;
+    if (C > 1) {
+        float* yy = scratch<float>(ctx, n_max * C * D);
+        interleave_chunks(ctx, x, D, C, base, extra, n_max, yy);
+        y = yy;
+    }
+    float* tables = scratch<float>(ctx, B64 * ks * ds);
+    uint32_t* assign = scratch<uint32_t>(ctx, B64 * n_max);
+    std::vector<uint64_t> seeds(B), counts(B);
+    for (uint64_t c = 0; c < C; ++c)
+        for (uint32_t m = 0; m < M; ++m) {
+            seeds[c * M + m] = (seed + c) + m;  // chunk_seed = seed + c (pipeline.cpp:190), pq.cpp:88
+            counts[c * M + m] = base + (c < extra ? 1 : 0);
+        }
+    KMeansOut r = run_kmeans(ctx, y, n_max, C * D, B, ds, ds, ks, iters, seeds, 1e-4, tables,
+                             assign, extra ? &counts : nullptr);
+    ChunkFits f;
+    f.reps = scratch<float>(ctx, C * ks * D);
+    chunk_representatives(ctx, tables, C, M, ks, ds, f.reps);
+    double* sse = scratch<double>(ctx, C);
+    chunk_sse(ctx, x, C, M, ks, ds, base, extra, assign, n_max, tables, sse);
+    f.rmse.resize(C);
+    PQG_CUDA(cudaMemcpyAsync(f.rmse.data(), sse, sizeof(double) * C, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    for (uint64_t c = 0; c < C; ++c)
+        f.rmse[c] = std::sqrt(f.rmse[c] / double((base + (c < extra ? 1 : 0)) * D));  // pq.cpp:169-177
+    f.iters = r.iters;
+    return f;
+}
+
+static uint64_t default_nlist_of(uint64_t n) {  // proj/src/ivf.cpp:118-121
+    const uint64_t r = uint64_t(std::llround(std::sqrt(double(n))));
+    return std::clamp<uint64_t>(r, 1, n == 0 ? 1 : n);
+}
+
+using Clock = std::chrono::steady_clock;
+static double seconds_since(Clock::time_point t) {
+    return std::chrono::duration<double>(Clock::now() - t).count();
 }
 
 // ===========================================================================
@@ -600,22 +720,171 @@ int pqg_kmeans_fit(pqg_ctx* ctx, const float* points, uint64_t n, uint64_t d, ui
     });
 }
 
+int pqg_train_chunks(pqg_ctx* ctx, const float* data, uint64_t n, uint64_t D, uint64_t n_chunks,
+                     uint32_t M, uint32_t ks, uint32_t max_iters, uint64_t seed,
+                     float* representatives, double* local_rmse, uint32_t* iterations_run) {
+    return guard([&] {
+        Scope sc(ctx);
+        check_train_chunks(n, D, n_chunks, M, ks, max_iters);
+        const float* dx = in(ctx, data, n * D);
+        ChunkFits f = train_chunks_dev(ctx, dx, n, D, n_chunks, M, ks, max_iters, seed);
+        if (representatives) {
+            const uint64_t cnt = n_chunks * ks * D;
+            PQG_CUDA(cudaMemcpyAsync(representatives, f.reps, sizeof(float) * cnt,
+                                     on_device(representatives) ? cudaMemcpyDeviceToDevice
+                                                                : cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+        }
+        sync(ctx);
+        if (local_rmse) std::copy(f.rmse.begin(), f.rmse.end(), local_rmse);
+        if (iterations_run) std::copy(f.iters.begin(), f.iters.end(), iterations_run);
+    });
+}
+
+int pqg_pipeline_run(pqg_ctx* ctx, const float* data, uint64_t n, uint64_t D, uint64_t n_chunks,
+                     uint32_t M, uint32_t ks, uint64_t nlist, uint32_t max_iters, uint64_t seed,
+                     int mode, float* global_tables, double* global_rmse, float* representatives,
+                     double* local_rmse, uint64_t* nlist_used, pqg_index** merged_index,
+                     double* phase_seconds) {
+    return guard([&] {
+        Scope sc(ctx);
+        // proj/src/pipeline.cpp:142-163
+        if (n == 0 || D == 0) inval("run_pipeline: empty dataset");
+        if (mode < PQG_MODE_SINGLE || mode > PQG_MODE_PARALLEL_PQ_INDEX)
+            inval("run_pipeline: unknown mode " + std::to_string(mode));
+        uint64_t nl = nlist == 0 ? default_nlist_of(n) : nlist;
+        if (nlist == 0 && mode == PQG_MODE_PARALLEL_PQ_INDEX) nl = std::min<uint64_t>(nl, n_chunks * ks);
+        if (nlist_used) *nlist_used = nl;
+        double ph[PQG_PHASE_COUNT];
+        std::fill(ph, ph + PQG_PHASE_COUNT, -1.0);
+        auto timed = [&](int phase, auto&& body) {
+            const auto t0 = Clock::now();
+            body();
+            sync(ctx);
+            ph[phase] = seconds_since(t0);
+        };
+        const float* dx = in(ctx, data, n * D);
+        const uint32_t ds = (M && D % M == 0) ? uint32_t(D / M) : 0;
+        auto ot = out(ctx, global_tables, uint64_t(M) * ks * (ds ? ds : 1));
+        float* gt = nullptr;
+        double rmse_g = 0.0;
+
+        if (mode == PQG_MODE_SINGLE) {
+            // fit (pipeline.cpp:166-169), then reconstruction_rmse (:171-173): the
+            // final assignment pass of each subspace fit IS the encode of the data
+            // with the returned codebook (no update follows it, kmeans.cpp:93-101),
+            // so the SSE is taken from those assignments.
+            check_pq_fit(n, D, M, ks, max_iters);
+            uint32_t* assign = scratch<uint32_t>(ctx, uint64_t(M) * n);
+            gt = ot.dev ? ot.dev : scratch<float>(ctx, uint64_t(M) * ks * ds);
+            std::vector<uint64_t> seeds(M);
+            for (uint32_t m = 0; m < M; ++m) seeds[m] = seed + m;
+            timed(PQG_PHASE_FIT, [&] {
+                run_kmeans(ctx, dx, n, D, M, ds, ds, ks, max_iters, seeds, 1e-4, gt, assign);
+            });
+            timed(PQG_PHASE_ENCODE, [&] {
+                double* sse = scratch<double>(ctx, 1);
+                chunk_sse(ctx, dx, 1, M, ks, ds, n, 0, assign, n, gt, sse);
+                double h = 0.0;
+                PQG_CUDA(cudaMemcpyAsync(&h, sse, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+                sync(ctx);
+                rmse_g = std::sqrt(h / double(n * D));
+            });
+        } else {
+            timed(PQG_PHASE_CHUNKING, [&] { check_chunks(n, n_chunks); });
+            check_train_chunks(n, D, n_chunks, M, ks, max_iters);
+            const uint64_t C = n_chunks, R = C * ks;
+            ChunkFits f;
+            timed(PQG_PHASE_LOCAL_FIT, [&] {
+                f = train_chunks_dev(ctx, dx, n, D, C, M, ks, max_iters, seed);
+            });
+            // fit_global = pq_fit(representatives, M, ks, iters, seed) (pipeline.cpp:137-140)
+            check_pq_fit(R, D, M, ks, max_iters);
+            gt = ot.dev ? ot.dev : scratch<float>(ctx, uint64_t(M) * ks * ds);
+            timed(PQG_PHASE_GLOBAL_FIT, [&] {
+                uint32_t* assign = scratch<uint32_t>(ctx, uint64_t(M) * R);
+                std::vector<uint64_t> seeds(M);
+                for (uint32_t m = 0; m < M; ++m) seeds[m] = seed + m;
+                run_kmeans(ctx, f.reps, R, D, M, ds, ds, ks, max_iters, seeds, 1e-4, gt, assign);
+            });
+            if (representatives) {
+                PQG_CUDA(cudaMemcpyAsync(representatives, f.reps, sizeof(float) * R * D,
+                                         on_device(representatives) ? cudaMemcpyDeviceToDevice
+                                                                    : cudaMemcpyDeviceToHost,
+                                         ctx->stream));
+            }
+            if (local_rmse) std::copy(f.rmse.begin(), f.rmse.end(), local_rmse);
+            const uint32_t w = code_width(ks);
+            uint8_t* codes = scratch<uint8_t>(ctx, n * M * w);
+            auto encode_rmse = [&] {
+                encode_dev(ctx, dx, n, M, ks, ds, gt, codes);
+                double* sse = scratch<double>(ctx, 1);
+                reset_err(ctx);
+                recon_sse_dev(ctx, dx, codes, n, M, ks, ds, gt, sse, ctx->d_err);
+                double h = 0.0;
+                PQG_CUDA(cudaMemcpyAsync(&h, sse, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+                sync(ctx);
+                rmse_g = std::sqrt(h / double(n * D));
+            };
+            if (mode == PQG_MODE_PARALLEL_PQ) {
+                timed(PQG_PHASE_ENCODE, encode_rmse);  // pipeline.cpp:201-206
+            } else {
+                // shared coarse centroids: kmeans_fit(representatives, nlist, iters,
+                // seed + M) (pipeline.cpp:212-219)
+                if (nl > R)
+                    inval("kmeans_fit: k (" + std::to_string(nl) + ") exceeds number of points (" +
+                          std::to_string(R) + ")");
+                float* coarse = scratch<float>(ctx, nl * D);
+                timed(PQG_PHASE_COARSE_FIT, [&] {
+                    uint32_t* assign = scratch<uint32_t>(ctx, R);
+                    run_kmeans(ctx, f.reps, R, D, 1, uint32_t(D), 0, nl, max_iters, {seed + M}, 1e-4,
+                               coarse, assign);
+                });
+                timed(PQG_PHASE_ENCODE, encode_rmse);  // pipeline.cpp:225-243
+                // per-chunk ivf_build_with_centroids with ids [begin, end) then
+                // ivf_merge in chunk order (pipeline.cpp:245-263): list l of the merge
+                // is chunk 0's list l, then chunk 1's, ... -- exactly the stable
+                // build over all n items with ids 0..n-1, which is what runs here
+                // (one launch sequence for every chunk; the merge is free).
+                pqg_index* ix = nullptr;
+                timed(PQG_PHASE_INDEX_BUILD, [&] {
+                    uint64_t* ids = scratch<uint64_t>(ctx, n);
+                    launch(ctx, "pipeline", iota_u64_kernel, dim3(grid1d(n, 256, 4096)), dim3(256), 0,
+                           ids, n);
+                    ix = new_index(ctx, M, ks, ds, nl, n, gt, coarse);
+                    try {
+                        uint32_t* lo = assign_lists(ctx, ix->tables, M, ks, ds, codes, n, ix->coarse,
+                                                    ix->coarse_norm, ix->coarse_max, nl);
+                        fill_lists(ctx, ix, lo, ids, codes, n);
+                        sync(ctx);
+                    } catch (...) {
+                        ix->free_all();
+                        delete ix;
+                        throw;
+                    }
+                });
+                ph[PQG_PHASE_MERGE] = 0.0;
+                if (merged_index) *merged_index = ix;
+                else {
+                    ix->free_all();
+                    delete ix;
+                }
+            }
+        }
+        finish(ctx, ot);
+        sync(ctx);
+        if (global_rmse) *global_rmse = rmse_g;
+        if (phase_seconds) std::copy(ph, ph + PQG_PHASE_COUNT, phase_seconds);
+    });
+}
+
 int pqg_pq_fit(pqg_ctx* ctx, const float* data, uint64_t n, uint64_t D, uint32_t M, uint32_t ks,
                uint32_t max_iters, uint64_t seed, float* tables, uint32_t* iterations_run,
                double* inertia) {
     return guard([&] {
         Scope sc(ctx);
-        // proj/src/pq.cpp:65-75
-        if (M == 0) inval("pq_fit: M must be >= 1");
-        if (D % M != 0)
-            inval("pq_fit: D (" + std::to_string(D) + ") is not divisible by M (" +
-                  std::to_string(M) + ")");
-        if (ks > n)
-            inval("pq_fit: Ks (" + std::to_string(ks) + ") exceeds number of rows (" +
-                  std::to_string(n) + ")");
+        check_pq_fit(n, D, M, ks, max_iters);
         const uint32_t ds = uint32_t(D / M);
-        check_pq_shape(M, ks, ds, "codebook");
-        if (max_iters < 1) inval("kmeans_fit: max_iters must be >= 1");
         const float* dp = in(ctx, data, n * D);
         auto ot = out(ctx, tables, uint64_t(M) * ks * ds);
         float* table = ot.dev ? ot.dev : scratch<float>(ctx, uint64_t(M) * ks * ds);

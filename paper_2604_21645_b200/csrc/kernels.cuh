@@ -71,7 +71,7 @@ struct Bucketing {
     uint32_t* perm;     // [B][n] rows in key order, stable
 };
 void stable_bucket(pqg_ctx* ctx, const uint32_t* keys, uint64_t n, uint32_t B, uint64_t k,
-                   const int* active, Bucketing out);
+                   const int* active, Bucketing out, const uint64_t* nb = nullptr);
 void exclusive_scan_u32(pqg_ctx* ctx, const uint32_t* in, uint64_t* out, uint64_t count);
 void gather_rows(pqg_ctx* ctx, const float* x, uint64_t ldx, uint32_t B, uint32_t d,
                  uint32_t col_stride, const uint64_t* rows, uint64_t k, float* table);
@@ -84,10 +84,15 @@ struct KMeansState {
 };
 void rows_sum_f64(pqg_ctx* ctx, const double* v, uint64_t n, uint32_t B, double* out);
 void kmeans_inertia_and_stop(pqg_ctx* ctx, const double* dist, uint64_t n, uint32_t B,
-                             uint32_t it, uint32_t max_iters, double tol, KMeansState st);
+                             uint32_t it, uint32_t max_iters, double tol, KMeansState st,
+                             const uint64_t* nb = nullptr);
 void kmeans_update(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint32_t d,
                    float* table, uint64_t k, const uint32_t* assign, double* dist,
-                   const int* active);
+                   const int* active, const uint64_t* nb = nullptr);
+// Batched problems of unequal length (nb[b] <= n rows, the rest padding):
+// padding rows get key k so the update ignores them.
+void kmeans_pad_keys(pqg_ctx* ctx, uint32_t* keys, uint64_t n, uint32_t B, uint64_t k,
+                     const uint64_t* nb, uint64_t max_pad);
 
 // pq.cu
 void pq_decode_dev(pqg_ctx* ctx, const uint8_t* codes, uint64_t n, uint32_t M, uint32_t ks,
@@ -100,6 +105,15 @@ void adc_tables_dev(pqg_ctx* ctx, const float* tables, uint32_t M, uint32_t ks, 
 void adc_lookup_dev(pqg_ctx* ctx, const float* entries, uint32_t M, uint32_t ks,
                     const uint8_t* codes, uint64_t n, double* out, int* err);
 void reduce_sum_f64(pqg_ctx* ctx, const double* parts, uint64_t count, double* out);
+// the chunked pipeline (proj/src/pipeline.cpp): chunks side by side, decoded
+// local codewords, per-chunk reconstruction SSE from the fits' assignments
+void interleave_chunks(pqg_ctx* ctx, const float* x, uint64_t D, uint64_t C, uint64_t base,
+                       uint64_t extra, uint64_t n_max, float* y);
+void chunk_representatives(pqg_ctx* ctx, const float* tables, uint64_t C, uint32_t M, uint32_t ks,
+                           uint32_t ds, float* reps);
+void chunk_sse(pqg_ctx* ctx, const float* x, uint64_t C, uint32_t M, uint32_t ks, uint32_t ds,
+               uint64_t base, uint64_t extra, const uint32_t* assign, uint64_t n_max,
+               const float* tables, double* sse);
 
 // ivf.cu
 struct IndexView {

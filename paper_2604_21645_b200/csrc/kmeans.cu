@@ -29,19 +29,25 @@ __global__ void hist_kernel(const uint32_t* keys, uint64_t n, uint64_t k, uint32
     const uint64_t r0 = uint64_t(tile) * kTile;
     const uint64_t r1 = min64(n, r0 + kTile);
     const uint32_t* kb = keys + uint64_t(b) * n;
-    for (uint64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) atomicAdd(&hist[kb[i]], 1u);
+    for (uint64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+        const uint32_t c = kb[i];
+        if (c < k) atomicAdd(&hist[c], 1u);  // key k marks a padding row (no cluster)
+    }
     __syncthreads();
     uint32_t* out = tile_counts + uint64_t(b) * k * ntiles;
     for (uint64_t c = threadIdx.x; c < k; c += blockDim.x) out[c * ntiles + tile] = hist[c];
 }
 
 __global__ void offsets_kernel(const uint64_t* tile_base, uint64_t n, uint32_t B, uint64_t k,
-                               uint32_t ntiles, uint64_t* offsets) {
+                               uint32_t ntiles, uint64_t* offsets, const uint64_t* nb) {
     const uint64_t total = uint64_t(B) * (k + 1);
     for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
          e += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t b = e / (k + 1), c = e - b * (k + 1);
-        offsets[e] = (c == k) ? n : tile_base[(b * k + c) * ntiles] - b * n;
+        // tile_base is one scan over all problems: problem b starts at its own
+        // first entry (b*n only when every problem has n keys)
+        offsets[e] = (c == k) ? (nb ? nb[b] : n)
+                              : tile_base[(b * k + c) * ntiles] - tile_base[b * k * ntiles];
     }
 }
 
@@ -58,7 +64,8 @@ __global__ void scatter_kernel(const uint32_t* keys, uint64_t n, uint64_t k, uin
     uint32_t* running = running_all + uint64_t(wib) * k;
     const uint64_t* tb = tile_base + uint64_t(b) * k * ntiles;
     const uint64_t base_b = uint64_t(b) * n;
-    for (uint64_t c = lane; c < k; c += 32) running[c] = uint32_t(tb[c * ntiles + tile] - base_b);
+    const uint64_t first = tb[0];  // problem b's start in the all-problem scan
+    for (uint64_t c = lane; c < k; c += 32) running[c] = uint32_t(tb[c * ntiles + tile] - first);
     __syncwarp();
     const uint64_t r0 = uint64_t(tile) * kTile;
     const uint64_t r1 = min64(n, r0 + kTile);
@@ -75,8 +82,8 @@ __global__ void scatter_kernel(const uint32_t* keys, uint64_t n, uint64_t k, uin
 #pragma unroll
         for (int q = 0; q < 32; ++q) {
             const uint64_t i = c0 + uint64_t(q) * 32 + lane;
-            const bool valid = i < r1;
             const uint32_t c = key[q];
+            const bool valid = i < r1 && c < k;
             const uint32_t peers = __match_any_sync(0xffffffffu, c);
             const uint32_t rank = __popc(peers & lanemask_lt());
             uint32_t pos = 0;
@@ -210,12 +217,29 @@ __device__ double block_sum(double v) {
     return r;
 }
 
+// The fixed reduction shape (chunking of n rows) shared by the in-loop
+// inertia and pqg_rows_sum_f64, so sharded and single-process fits see
+// identical sums; a problem with fewer rows (nb) uses its own shape, so a
+// batched fit of unequal problems sums exactly like separate fits.
+__host__ __device__ inline void inertia_parts(uint64_t n, uint64_t& nparts, uint64_t& chunk) {
+    nparts = n == 0 ? 1 : min64(512, (n + 8191) / 8192);
+    chunk = n == 0 ? 1 : (n + nparts - 1) / nparts;
+    nparts = n == 0 ? 1 : (n + chunk - 1) / chunk;
+}
+
 __global__ void partial_sum_kernel(const double* v, uint64_t n, uint64_t chunk, double* parts,
-                                   const int* active) {
+                                   const int* active, const uint64_t* nb) {
     const uint32_t b = blockIdx.y;
     if (active && !active[b]) return;
+    uint64_t nn = n;
+    if (nb) {
+        uint64_t np;
+        nn = nb[b];
+        inertia_parts(nn, np, chunk);
+        if (blockIdx.x >= np) return;
+    }
     const uint64_t c0 = uint64_t(blockIdx.x) * chunk;
-    const uint64_t c1 = min64(n, c0 + chunk);
+    const uint64_t c1 = min64(nn, c0 + chunk);
     const double* vb = v + uint64_t(b) * n;
     double s = 0.0;
     for (uint64_t i = c0 + threadIdx.x; i < c1; i += kRedThreads) s = __dadd_rn(s, vb[i]);
@@ -224,11 +248,16 @@ __global__ void partial_sum_kernel(const double* v, uint64_t n, uint64_t chunk, 
 }
 
 __global__ void stop_kernel(const double* parts, uint32_t nparts, uint32_t it, uint32_t max_iters,
-                            double tol, KMeansState st) {
+                            double tol, KMeansState st, const uint64_t* nb) {
     const uint32_t b = blockIdx.x;
     if (!st.active[b]) return;
+    uint64_t cnt = nparts;
+    if (nb) {
+        uint64_t chunk;
+        inertia_parts(nb[b], cnt, chunk);
+    }
     double s = 0.0;
-    for (uint32_t i = threadIdx.x; i < nparts; i += kRedThreads)
+    for (uint32_t i = threadIdx.x; i < cnt; i += kRedThreads)
         s = __dadd_rn(s, parts[uint64_t(b) * nparts + i]);
     s = block_sum(s);
     if (threadIdx.x != 0) return;
@@ -259,13 +288,14 @@ __global__ void final_parts_kernel(const double* parts, uint32_t nparts, double*
 // ordered sums below stream contiguous memory instead of chasing indices.
 __global__ void gather_sorted_kernel(const float* x, uint64_t ldx, uint32_t col_stride, uint64_t n,
                                      uint32_t B, uint32_t d, const uint32_t* perm, float* sorted,
-                                     const int* active) {
+                                     const int* active, const uint64_t* nb) {
     const uint64_t total = uint64_t(B) * n * d;
     for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
          e += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t bp = e / d, t = e - bp * d;
         const uint64_t b = bp / n;
         if (active && !active[b]) continue;
+        if (nb && bp - b * n >= nb[b]) continue;  // padding rows of a shorter problem
         sorted[e] = __ldg(x + uint64_t(__ldg(perm + bp)) * ldx + b * col_stride + t);
     }
 }
@@ -308,9 +338,11 @@ __global__ void mean_sorted_kernel(const float* sorted, uint64_t n, uint32_t B, 
 // such row on ties), copy it, zero its distance.
 __global__ void reseed_kernel(const float* x, uint64_t ldx, uint32_t col_stride, uint64_t n,
                               uint32_t d, uint64_t k, const uint64_t* offsets, double* dist,
-                              float* table, const int* has_empty, const int* active) {
+                              float* table, const int* has_empty, const int* active,
+                              const uint64_t* nb) {
     const uint32_t b = blockIdx.x;
     if ((active && !active[b]) || !has_empty[b]) return;
+    const uint64_t nn = nb ? nb[b] : n;
     __shared__ double sv[32];
     __shared__ uint64_t si[32];
     const uint64_t* off = offsets + uint64_t(b) * (k + 1);
@@ -320,7 +352,7 @@ __global__ void reseed_kernel(const float* x, uint64_t ldx, uint32_t col_stride,
         if (off[c] != off[c + 1]) continue;
         double bv = -1.0;
         uint64_t bi = ~uint64_t(0);
-        for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        for (uint64_t i = threadIdx.x; i < nn; i += blockDim.x) {
             const double v = db[i];
             if (bi == ~uint64_t(0) || v > bv) { bv = v; bi = i; }
         }
@@ -360,14 +392,31 @@ __global__ void reseed_kernel(const float* x, uint64_t ldx, uint32_t col_stride,
     }
 }
 
+// Rows i >= nb[b] of a shorter problem get key k: no cluster, skipped by the
+// bucketing, the sums and the reseed.
+__global__ void pad_keys_kernel(uint32_t* keys, uint64_t n, uint64_t k, const uint64_t* nb) {
+    const uint32_t b = blockIdx.y;
+    const uint64_t nn = nb[b];
+    for (uint64_t i = nn + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        keys[uint64_t(b) * n + i] = uint32_t(k);
+}
+
 }  // namespace
+
+void kmeans_pad_keys(pqg_ctx* ctx, uint32_t* keys, uint64_t n, uint32_t B, uint64_t k,
+                     const uint64_t* nb, uint64_t max_pad) {
+    if (max_pad == 0) return;
+    launch(ctx, "pad_keys", pad_keys_kernel, dim3(unsigned((max_pad + 255) / 256), B), dim3(256), 0,
+           keys, n, k, nb);
+}
 
 void exclusive_scan_u32(pqg_ctx* ctx, const uint32_t* in, uint64_t* out, uint64_t count) {
     exclusive_scan<uint32_t>(ctx, in, out, count);
 }
 
 void stable_bucket(pqg_ctx* ctx, const uint32_t* keys, uint64_t n, uint32_t B, uint64_t k,
-                   const int* active, Bucketing out) {
+                   const int* active, Bucketing out, const uint64_t* nb) {
     (void)active;
     if (k > 16384) fail(PQG_EUNSUPPORTED, "bucketing supports at most 16384 lists/clusters");
     const uint32_t ntiles = uint32_t((n + kTile - 1) / kTile);
@@ -379,7 +428,7 @@ void stable_bucket(pqg_ctx* ctx, const uint32_t* keys, uint64_t n, uint32_t B, u
            tile_counts);
     exclusive_scan<uint32_t>(ctx, tile_counts, tile_base, uint64_t(B) * k * ntiles);
     launch(ctx, "bucket", offsets_kernel, dim3(grid1d(uint64_t(B) * (k + 1), 256, 4096)),
-           dim3(256), 0, (const uint64_t*)tile_base, n, B, k, ntiles, out.offsets);
+           dim3(256), 0, (const uint64_t*)tile_base, n, B, k, ntiles, out.offsets, nb);
     int wpb = int(std::max<uint64_t>(1, std::min<uint64_t>(8, (96 * 1024) / (4 * k))));
     const size_t ssmem = sizeof(uint32_t) * k * wpb;
     set_smem(scatter_kernel, ssmem);
@@ -393,24 +442,16 @@ void gather_rows(pqg_ctx* ctx, const float* x, uint64_t ldx, uint32_t B, uint32_
            x, ldx, B, d, col_stride, rows, k, table);
 }
 
-// The fixed reduction shape (chunking of n) shared by the in-loop inertia and
-// pqg_rows_sum_f64, so sharded and single-process fits see identical sums.
-static void inertia_parts(uint64_t n, uint64_t& nparts, uint64_t& chunk) {
-    nparts = std::min<uint64_t>(512, std::max<uint64_t>(1, (n + 8191) / 8192));
-    chunk = (n + nparts - 1) / nparts;
-    nparts = (n + chunk - 1) / chunk;
-    if (nparts == 0) nparts = 1;
-}
-
 void kmeans_inertia_and_stop(pqg_ctx* ctx, const double* dist, uint64_t n, uint32_t B,
-                             uint32_t it, uint32_t max_iters, double tol, KMeansState st) {
+                             uint32_t it, uint32_t max_iters, double tol, KMeansState st,
+                             const uint64_t* nb) {
     uint64_t nparts, chunk;
     inertia_parts(n, nparts, chunk);
     double* parts = scratch<double>(ctx, uint64_t(B) * nparts);
     launch(ctx, "inertia", partial_sum_kernel, dim3(unsigned(nparts), B), dim3(kRedThreads), 0,
-           dist, n, chunk, parts, (const int*)st.active);
+           dist, n, chunk, parts, (const int*)st.active, nb);
     launch(ctx, "inertia", stop_kernel, dim3(B), dim3(kRedThreads), 0, (const double*)parts,
-           uint32_t(nparts), it, max_iters, tol, st);
+           uint32_t(nparts), it, max_iters, tol, st, nb);
 }
 
 void rows_sum_f64(pqg_ctx* ctx, const double* v, uint64_t n, uint32_t B, double* out) {
@@ -418,27 +459,27 @@ void rows_sum_f64(pqg_ctx* ctx, const double* v, uint64_t n, uint32_t B, double*
     inertia_parts(n, nparts, chunk);
     double* parts = scratch<double>(ctx, uint64_t(B) * nparts);
     launch(ctx, "inertia", partial_sum_kernel, dim3(unsigned(nparts), B), dim3(kRedThreads), 0,
-           v, n, chunk, parts, (const int*)nullptr);
+           v, n, chunk, parts, (const int*)nullptr, (const uint64_t*)nullptr);
     launch(ctx, "inertia", final_parts_kernel, dim3(B), dim3(kRedThreads), 0, (const double*)parts,
            uint32_t(nparts), out);
 }
 
 void kmeans_update(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint32_t d,
                    float* table, uint64_t k, const uint32_t* assign, double* dist,
-                   const int* active) {
+                   const int* active, const uint64_t* nb) {
     Bucketing bk{scratch<uint64_t>(ctx, uint64_t(B) * (k + 1)), scratch<uint32_t>(ctx, uint64_t(B) * n)};
-    stable_bucket(ctx, assign, n, B, k, active, bk);
+    stable_bucket(ctx, assign, n, B, k, active, bk, nb);
     int* has_empty = scratch<int>(ctx, B);
     PQG_CUDA(cudaMemsetAsync(has_empty, 0, sizeof(int) * B, ctx->stream));
     const uint64_t total = uint64_t(B) * k * d;
     float* sorted = scratch<float>(ctx, uint64_t(B) * n * d);
     launch(ctx, "kmeans_sum", gather_sorted_kernel, dim3(grid1d(uint64_t(B) * n * d, 256, ctx->num_sms * 64)),
            dim3(256), 0, src.x, src.ldx, src.col_stride, n, B, d, (const uint32_t*)bk.perm, sorted,
-           active);
+           active, nb);
     launch(ctx, "kmeans_sum", mean_sorted_kernel, dim3(grid1d(total, 128, 1u << 20)), dim3(128), 0,
            (const float*)sorted, n, B, d, k, (const uint64_t*)bk.offsets, table, has_empty, active);
     launch(ctx, "reseed", reseed_kernel, dim3(B), dim3(1024), 0, src.x, src.ldx, src.col_stride, n,
-           d, k, (const uint64_t*)bk.offsets, dist, table, (const int*)has_empty, active);
+           d, k, (const uint64_t*)bk.offsets, dist, table, (const int*)has_empty, active, nb);
 }
 
 }  // namespace pqg

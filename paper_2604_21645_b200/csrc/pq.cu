@@ -129,11 +129,118 @@ __global__ void adc_lookup_kernel(const float* entries, uint32_t M, uint32_t ks,
     }
 }
 
-uint64_t nparts_for(uint64_t count) {
-    return std::min<uint64_t>(4096, std::max<uint64_t>(1, (count + 65535) / 65536));
+__host__ __device__ inline uint64_t nparts_for(uint64_t count) {
+    const uint64_t p = (count + 65535) / 65536;
+    return p < 1 ? 1 : (p > 4096 ? 4096 : p);
+}
+
+// ---- the paper's chunked pipeline (proj/src/pipeline.cpp) -----------------
+// Chunk c of chunk_rows(n, C) (proj/src/dataset_io.cpp:322-339) starts at
+// c*base + min(c, extra) and holds base + (c < extra) rows.
+__device__ __forceinline__ void chunk_range(uint64_t c, uint64_t base, uint64_t extra,
+                                            uint64_t& r0, uint64_t& nc) {
+    r0 = c * base + (c < extra ? c : extra);
+    nc = base + (c < extra ? 1 : 0);
+}
+
+// Y[i][c*D + j] = x[r0_c + i][j]: the C chunks side by side, so the C*M
+// local PQ fits become C*M column-block problems over n_max shared rows.
+// Rows past a chunk's end repeat its last row (finite; their keys are
+// padded out of every update).
+__global__ void interleave_chunks_kernel(const float* x, uint64_t D, uint64_t C, uint64_t base,
+                                         uint64_t extra, uint64_t n_max, float* y) {
+    const uint64_t W = C * D, total = n_max * W;
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i = e / W, cj = e - i * W;
+        const uint64_t c = cj / D, j = cj - c * D;
+        uint64_t r0, nc;
+        chunk_range(c, base, extra, r0, nc);
+        y[e] = __ldg(x + (r0 + (i < nc ? i : nc - 1)) * D + j);
+    }
+}
+
+// Representative j of chunk c = local codeword j of every subspace,
+// concatenated (pipeline.cpp:95-103): reps[c*ks + j][m*ds + t].
+__global__ void representatives_kernel(const float* tables, uint64_t C, uint32_t M, uint32_t ks,
+                                       uint32_t ds, float* reps) {
+    const uint64_t D = uint64_t(M) * ds, total = C * ks * D;
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t cj = e / D, col = e - cj * D;
+        const uint64_t c = cj / ks, j = cj - c * ks;
+        const uint64_t m = col / ds, t = col - m * ds;
+        reps[e] = __ldg(tables + (((c * M + m) * ks) + j) * ds + t);
+    }
+}
+
+// Per-chunk reconstruction SSE of the chunk against its own local codebook,
+// codes taken from the fit's final assignments (the last pass has no update
+// after it, kmeans.cpp:93-101, so they are the chunk's encode).  Same
+// element order and reduction shape as recon_sse_kernel on that chunk alone.
+__global__ void chunk_sse_kernel(const float* x, uint32_t M, uint32_t ks, uint32_t ds,
+                                 uint64_t base, uint64_t extra, const uint32_t* assign,
+                                 uint64_t n_max, const float* tables, double* parts) {
+    const uint64_t c = blockIdx.y;
+    const uint64_t D = uint64_t(M) * ds;
+    uint64_t r0, nc;
+    chunk_range(c, base, extra, r0, nc);
+    const uint64_t total = nc * D, np = nparts_for(total);
+    if (blockIdx.x >= np) return;
+    const uint64_t chunk = (total + np - 1) / np;
+    const uint64_t c0 = uint64_t(blockIdx.x) * chunk, c1 = min64(total, c0 + chunk);
+    const float* xc = x + r0 * D;
+    double s = 0.0;
+    for (uint64_t e = c0 + threadIdx.x; e < c1; e += kThreads) {
+        const uint64_t i = e / D, col = e - i * D;
+        const uint32_t m = uint32_t(col / ds), t = uint32_t(col - uint64_t(m) * ds);
+        const uint64_t b = c * M + m;
+        const uint32_t code = __ldg(assign + b * n_max + i);
+        const double diff =
+            __dsub_rn((double)__ldg(xc + e), (double)__ldg(tables + (b * ks + code) * ds + t));
+        s = __dadd_rn(s, __dmul_rn(diff, diff));
+    }
+    s = block_sum256(s);
+    if (threadIdx.x == 0) parts[c * gridDim.x + blockIdx.x] = s;
+}
+
+__global__ void chunk_sse_final_kernel(const double* parts, uint64_t stride, uint32_t M,
+                                       uint32_t ds, uint64_t base, uint64_t extra, double* sse) {
+    const uint64_t c = blockIdx.x;
+    uint64_t r0, nc;
+    chunk_range(c, base, extra, r0, nc);
+    const uint64_t np = nparts_for(nc * M * ds);
+    double s = 0.0;
+    for (uint64_t i = threadIdx.x; i < np; i += kThreads) s = __dadd_rn(s, parts[c * stride + i]);
+    s = block_sum256(s);
+    if (threadIdx.x == 0) sse[c] = s;
 }
 
 }  // namespace
+
+void interleave_chunks(pqg_ctx* ctx, const float* x, uint64_t D, uint64_t C, uint64_t base,
+                       uint64_t extra, uint64_t n_max, float* y) {
+    launch(ctx, "pipeline", interleave_chunks_kernel, dim3(grid1d(n_max * C * D, 256, ctx->num_sms * 32)),
+           dim3(256), 0, x, D, C, base, extra, n_max, y);
+}
+
+void chunk_representatives(pqg_ctx* ctx, const float* tables, uint64_t C, uint32_t M, uint32_t ks,
+                           uint32_t ds, float* reps) {
+    launch(ctx, "pipeline", representatives_kernel,
+           dim3(grid1d(C * ks * uint64_t(M) * ds, 256, ctx->num_sms * 32)), dim3(256), 0, tables, C, M,
+           ks, ds, reps);
+}
+
+void chunk_sse(pqg_ctx* ctx, const float* x, uint64_t C, uint32_t M, uint32_t ks, uint32_t ds,
+               uint64_t base, uint64_t extra, const uint32_t* assign, uint64_t n_max,
+               const float* tables, double* sse) {
+    const uint64_t np_max = nparts_for(n_max * M * ds);
+    double* parts = scratch<double>(ctx, C * np_max);
+    launch(ctx, "recon_sse", chunk_sse_kernel, dim3(unsigned(np_max), unsigned(C)), dim3(kThreads), 0,
+           x, M, ks, ds, base, extra, assign, n_max, tables, parts);
+    launch(ctx, "reduce", chunk_sse_final_kernel, dim3(unsigned(C)), dim3(kThreads), 0,
+           (const double*)parts, np_max, M, ds, base, extra, sse);
+}
 
 void reduce_sum_f64(pqg_ctx* ctx, const double* parts, uint64_t count, double* out) {
     launch(ctx, "reduce", final_sum_kernel, dim3(1), dim3(kThreads), 0, parts, count, out);

@@ -9,10 +9,13 @@
 // (posting-list vectors, id_set).  One pqg context per calling thread keeps
 // the API re-entrant as run_pipeline requires (SURVEY.md 8(b) Threading).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <iomanip>
+#include <sstream>
 #include <list>
 #include <memory>
 #include <mutex>
@@ -24,6 +27,7 @@
 #include "pqii/ivf.hpp"
 #include "pqii/kmeans.hpp"
 #include "pqii/matrix.hpp"
+#include "pqii/pipeline.hpp"
 #include "pqii/pq.hpp"
 
 namespace pqii {
@@ -623,6 +627,140 @@ InvertedIndex load_index(const std::string& path) {
     char extra;
     if (in.read(&extra, 1); in.gcount() != 0) throw std::runtime_error(path + ": trailing data after payload");
     return ix;
+}
+
+// ===========================================================================
+// pipeline.hpp (proj/src/pipeline.cpp) -- one batched device fit for all
+// chunks, data resident on the device between phases (pqg_pipeline_run)
+// ===========================================================================
+const char* to_string(PipelineMode mode) {
+    switch (mode) {
+        case PipelineMode::kSingle: return "single";
+        case PipelineMode::kParallelPq: return "parallel_pq";
+        case PipelineMode::kParallelPqIndex: return "parallel_pq_index";
+    }
+    return "unknown";
+}
+
+std::optional<PipelineMode> parse_mode(std::string_view name) {
+    for (PipelineMode m : {PipelineMode::kSingle, PipelineMode::kParallelPq,
+                           PipelineMode::kParallelPqIndex})
+        if (name == to_string(m)) return m;
+    return std::nullopt;
+}
+
+ChunkOutput train_chunk(const VectorMatrix& chunk, std::uint32_t m, std::uint32_t ks,
+                        std::uint32_t iters, std::uint64_t chunk_seed) {
+    const auto t0 = std::chrono::steady_clock::now();
+    ChunkOutput out;
+    out.representatives = VectorMatrix(ks, chunk.dims);
+    const int rc = pqg_train_chunks(ctx(), chunk.values.data(), chunk.rows, chunk.dims, 1, m, ks,
+                                    iters, chunk_seed, out.representatives.values.data(),
+                                    &out.local_rmse, nullptr);
+    if (rc == PQG_ECHUNK) {
+        // train_chunk itself throws invalid_argument without the task prefix
+        // (pipeline.cpp:84-90)
+        std::string msg = pqg_last_error();
+        if (msg.rfind("chunk 0: ", 0) == 0) msg = msg.substr(9);
+        throw std::invalid_argument(msg);
+    }
+    raise(rc);
+    out.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return out;
+}
+
+VectorMatrix aggregate_representatives(const std::vector<ChunkOutput>& outputs) {
+    if (outputs.empty()) throw std::invalid_argument("aggregate_representatives: no outputs");
+    std::vector<const ChunkOutput*> order;
+    for (const auto& o : outputs) order.push_back(&o);
+    std::stable_sort(order.begin(), order.end(),
+                     [](const ChunkOutput* a, const ChunkOutput* b) { return a->chunk_id < b->chunk_id; });
+    const std::size_t d = outputs.front().representatives.dims;
+    std::size_t rows = 0;
+    for (const auto& o : outputs) {
+        if (o.representatives.dims != d)
+            throw std::invalid_argument("aggregate_representatives: dimension mismatch at chunk " +
+                                        std::to_string(o.chunk_id));
+        rows += o.representatives.rows;
+    }
+    VectorMatrix all(rows, d);
+    std::size_t at = 0;
+    for (const ChunkOutput* o : order) {
+        std::copy(o->representatives.values.begin(), o->representatives.values.end(),
+                  all.values.begin() + at * d);
+        at += o->representatives.rows;
+    }
+    return all;
+}
+
+Codebook fit_global(const VectorMatrix& representatives, std::uint32_t m, std::uint32_t ks,
+                    std::uint32_t iters, std::uint64_t seed) {
+    return pq_fit(representatives, m, ks, iters, seed);
+}
+
+PipelineReport run_pipeline(const VectorMatrix& data, const PipelineConfig& config) {
+    if (data.rows == 0 || data.dims == 0) throw std::invalid_argument("run_pipeline: empty dataset");
+    if (config.n_threads == 0) throw std::invalid_argument("run_pipeline: n_threads must be >= 1");
+    const auto t0 = std::chrono::steady_clock::now();
+    PipelineReport r;
+    r.config = config;
+    const std::uint32_t M = config.m_subspaces, ks = config.ks;
+    const bool parallel = config.mode != PipelineMode::kSingle;
+    const std::size_t ds = (M && data.dims % M == 0) ? data.dims / M : 1;
+    r.global_codebook.m_subspaces = M;
+    r.global_codebook.ks = ks;
+    r.global_codebook.sub_dim = static_cast<std::uint32_t>(ds);
+    r.global_codebook.tables.assign(std::size_t(M) * ks * ds, 0.0f);
+    VectorMatrix reps;
+    if (parallel) reps = VectorMatrix(config.n_chunks * ks, data.dims);
+    std::vector<double> local(parallel ? std::max<std::size_t>(config.n_chunks, 1) : 0);
+    std::uint64_t nlist = 0;
+    pqg_index* h = nullptr;
+    double ph[PQG_PHASE_COUNT];
+    const int mode = config.mode == PipelineMode::kSingle
+                         ? PQG_MODE_SINGLE
+                         : (config.mode == PipelineMode::kParallelPq ? PQG_MODE_PARALLEL_PQ
+                                                                     : PQG_MODE_PARALLEL_PQ_INDEX);
+    raise(pqg_pipeline_run(ctx(), data.values.data(), data.rows, data.dims, config.n_chunks, M, ks,
+                           config.nlist, config.kmeans_iters, config.seed, mode,
+                           r.global_codebook.tables.data(), &r.global_rmse,
+                           parallel ? reps.values.data() : nullptr,
+                           parallel ? local.data() : nullptr, &nlist,
+                           mode == PQG_MODE_PARALLEL_PQ_INDEX ? &h : nullptr, ph));
+    r.config.nlist = nlist;
+    static const char* names[PQG_PHASE_COUNT] = {"fit",        "chunking", "local_fit",
+                                                 "global_fit", "coarse_fit", "encode",
+                                                 "index_build", "merge"};
+    for (int i = 0; i < PQG_PHASE_COUNT; ++i)
+        if (ph[i] >= 0.0) r.phase_seconds[names[i]] = ph[i];
+    if (!parallel) r.single_rmse = r.global_rmse;
+    else r.representatives = std::move(reps);
+    if (h) {
+        IndexPtr p(h, IndexDeleter());
+        r.merged_index = to_host(h, r.global_codebook);
+    }
+    r.total_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return r;
+}
+
+std::string PipelineReport::summary() const {
+    std::ostringstream out;
+    out << "mode: " << to_string(config.mode) << '\n';
+    out << "params: M=" << config.m_subspaces << " Ks=" << config.ks << " C=" << config.n_chunks
+        << " T=" << config.n_threads << " nlist=" << config.nlist << " iters=" << config.kmeans_iters
+        << " seed=" << config.seed << '\n';
+    out << "phases:";
+    for (const auto& [phase, secs] : phase_seconds)
+        out << ' ' << phase << '=' << std::fixed << std::setprecision(3) << secs << 's'
+            << std::defaultfloat;
+    out << '\n';
+    out << "total: " << std::fixed << std::setprecision(3) << total_seconds << "s\n"
+        << std::defaultfloat;
+    out << std::setprecision(9) << "rmse: " << global_rmse << '\n';
+    if (merged_index)
+        out << "index: " << merged_index->n_items << " items across " << merged_index->nlist()
+            << " lists\n";
+    return out.str();
 }
 
 }  // namespace pqii

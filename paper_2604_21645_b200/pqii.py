@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -637,3 +638,139 @@ def ivf_query_subset(index: InvertedIndex, query, k: int, subset, nprobe: int,
         int(max_sq_dist is not None), 0.0 if max_sq_dist is None else float(max_sq_dist), v(ids),
         v(dist), v(cnt)), "ivf_query_subset")
     return _to_result(ids[0], dist[0], cnt[0], k)
+
+
+# ---------------------------------------------------------------------------
+# L3: pipeline.hpp -- the paper's chunked fit (proj/src/pipeline.cpp)
+# ---------------------------------------------------------------------------
+PIPELINE_MODES = ("single", "parallel_pq", "parallel_pq_index")
+_PHASES = ("fit", "chunking", "local_fit", "global_fit", "coarse_fit", "encode", "index_build",
+           "merge")
+
+
+def parse_mode(name: str):
+    """pipeline.cpp:78-83: the mode for a name, else None."""
+    return name if name in PIPELINE_MODES else None
+
+
+@dataclass
+class PipelineConfig:  # pipeline.hpp:27-36
+    n_chunks: int = 1
+    m_subspaces: int = 8
+    ks: int = 256
+    nlist: int = 0
+    kmeans_iters: int = 20
+    seed: int = 0
+    n_threads: int = 1
+    mode: str = "single"
+
+
+@dataclass
+class ChunkOutput:  # pipeline.hpp:40-45
+    chunk_id: int
+    representatives: np.ndarray  # ks x D
+    local_rmse: float
+    wall_seconds: float = 0.0
+
+
+@dataclass
+class PipelineReport:  # pipeline.hpp:47-58
+    config: PipelineConfig
+    global_codebook: Codebook
+    global_rmse: float
+    single_rmse: float | None = None
+    phase_seconds: dict = field(default_factory=dict)
+    total_seconds: float = 0.0
+    representatives: np.ndarray | None = None
+    merged_index: InvertedIndex | None = None
+    local_rmse: np.ndarray | None = None
+
+    def summary(self) -> str:
+        """PipelineReport::summary (pipeline.cpp:268-293)."""
+        c = self.config
+        out = [f"mode: {c.mode}",
+               f"params: M={c.m_subspaces} Ks={c.ks} C={c.n_chunks} T={c.n_threads} "
+               f"nlist={c.nlist} iters={c.kmeans_iters} seed={c.seed}",
+               "phases:" + "".join(f" {k}={v:.3f}s" for k, v in sorted(self.phase_seconds.items())),
+               f"total: {self.total_seconds:.3f}s",
+               f"rmse: {self.global_rmse:.9g}"]
+        if self.merged_index is not None:
+            out.append(f"index: {self.merged_index.n_items} items across "
+                       f"{self.merged_index.nlist()} lists")
+        return "\n".join(out) + "\n"
+
+
+def train_chunks(data, n_chunks: int, m: int, ks: int, max_iters: int = 20, seed: int = 0,
+                 ctx: Context | None = None) -> list[ChunkOutput]:
+    """train_chunk (pipeline.cpp:84-106) for every chunk of chunk_rows(n,
+    n_chunks), chunk c with seed + c -- one batched k-means on the device."""
+    ctx = ctx or get_context()
+    data = _f32(data)
+    n, D = data.shape
+    reps = np.empty((max(n_chunks, 1) * max(ks, 1), D), np.float32)
+    local = np.empty(max(n_chunks, 1), np.float64)
+    dp, _a = _ptr(data)
+    _lib.check(ctx.lib.pqg_train_chunks(ctx.h, dp, n, D, n_chunks, m, ks, max_iters, seed,
+                                        reps.ctypes.data_as(C.c_void_p),
+                                        local.ctypes.data_as(C.c_void_p), None), "train_chunk")
+    return [ChunkOutput(c, reps[c * ks:(c + 1) * ks], float(local[c])) for c in range(n_chunks)]
+
+
+def aggregate_representatives(outputs: list[ChunkOutput]) -> np.ndarray:
+    """pipeline.cpp:108-135: row concatenation in ascending chunk_id order."""
+    if not outputs:
+        raise ValueError("aggregate_representatives: no outputs")
+    d = outputs[0].representatives.shape[1]
+    for o in outputs:
+        if o.representatives.shape[1] != d:
+            raise ValueError(f"aggregate_representatives: dimension mismatch at chunk {o.chunk_id}")
+    return np.concatenate([o.representatives for o in sorted(outputs, key=lambda o: o.chunk_id)])
+
+
+def fit_global(representatives, m: int, ks: int, iters: int, seed: int,
+               ctx: Context | None = None) -> Codebook:
+    """pipeline.cpp:137-140."""
+    return pq_fit(representatives, m, ks, iters, seed, ctx=ctx)
+
+
+def run_pipeline(data, config: PipelineConfig, ctx: Context | None = None) -> PipelineReport:
+    """run_pipeline (pipeline.cpp:142-266) on the device: the chunks' local
+    fits are one batched k-means, and the data stays resident between phases."""
+    ctx = ctx or get_context()
+    if config.n_threads == 0:
+        raise ValueError("run_pipeline: n_threads must be >= 1")
+    if config.mode not in PIPELINE_MODES:
+        raise ValueError(f"run_pipeline: unknown mode {config.mode}")
+    mode = PIPELINE_MODES.index(config.mode)
+    data = _f32(data)
+    n, D = data.shape
+    t0 = time.perf_counter()
+    M, ks = config.m_subspaces, config.ks
+    ds = D // M if M and D % M == 0 else 1
+    tables = np.empty((M, max(ks, 1), ds), np.float32)
+    C_ = config.n_chunks
+    reps = np.empty((max(C_, 1) * max(ks, 1), D), np.float32) if mode else None
+    local = np.empty(max(C_, 1), np.float64) if mode else None
+    rm = C.c_double()
+    nl = C.c_uint64()
+    h = C.c_void_p()
+    ph = np.full(8, -1.0)
+    dp, _a = _ptr(data)
+    v = lambda a: None if a is None else a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    _lib.check(ctx.lib.pqg_pipeline_run(ctx.h, dp, n, D, C_, M, ks, config.nlist,
+                                        config.kmeans_iters, config.seed, mode, v(tables),
+                                        C.byref(rm), v(reps), v(local), C.byref(nl),
+                                        C.byref(h) if mode == 2 else None, v(ph)),
+               "run_pipeline")
+    cfg = PipelineConfig(**{**config.__dict__, "nlist": nl.value})
+    rep = PipelineReport(cfg, Codebook(M, ks, ds, tables), rm.value,
+                         phase_seconds={k: float(t) for k, t in zip(_PHASES, ph) if t >= 0})
+    if mode == 0:
+        rep.single_rmse = rm.value
+    else:
+        rep.representatives = reps
+        rep.local_rmse = local
+    if h.value:
+        rep.merged_index = InvertedIndex(h, ctx)
+    rep.total_seconds = time.perf_counter() - t0
+    return rep

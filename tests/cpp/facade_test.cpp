@@ -13,6 +13,7 @@
 
 #include "pqii/ivf.hpp"
 #include "pqii/kmeans.hpp"
+#include "pqii/pipeline.hpp"
 #include "pqii/pq.hpp"
 
 using namespace pqii;
@@ -51,6 +52,37 @@ static VectorMatrix random_matrix(std::size_t rows, std::size_t dims, std::uint6
     VectorMatrix m(rows, dims);
     for (auto& v : m.values) v = dist(rng);
     return m;
+}
+
+// a 12-cluster mixture standing in for the reference's gen_synthetic
+// (its tests use clustered_data, proj/tests/test_pipeline.cpp:15-18)
+static VectorMatrix clustered(std::size_t n, std::size_t d, std::uint64_t seed) {
+    const VectorMatrix centers = random_matrix(12, d, seed * 7 + 1, -8.0f, 8.0f);
+    std::mt19937_64 rng(seed);
+    std::normal_distribution<float> z(0.0f, 0.7f);
+    VectorMatrix m(n, d);
+    for (std::size_t i = 0; i < n; ++i) {
+        const float* c = centers.row(rng() % 12);
+        for (std::size_t t = 0; t < d; ++t) m.row(i)[t] = c[t] + z(rng);
+    }
+    return m;
+}
+
+static bool rows_equal_as_sets(const VectorMatrix& a, const VectorMatrix& b, double tol) {
+    if (!a.same_shape(b)) return false;
+    std::vector<bool> used(b.rows, false);
+    for (std::size_t i = 0; i < a.rows; ++i) {
+        bool matched = false;
+        for (std::size_t j = 0; j < b.rows && !matched; ++j) {
+            if (used[j]) continue;
+            bool close = true;
+            for (std::size_t t = 0; t < a.dims && close; ++t)
+                close = std::fabs(double(a.row(i)[t]) - double(b.row(j)[t])) <= tol;
+            if (close) used[j] = matched = true;
+        }
+        if (!matched) return false;
+    }
+    return true;
 }
 
 static double exhaustive(const float* p, const float* t, std::size_t k, std::size_t d, std::size_t* best) {
@@ -205,6 +237,127 @@ int main() {
         CHECK_THROWS_WITH(ivf_build_with_centroids(cb, codes, dup, ix.coarse_centroids),
                           std::invalid_argument, "duplicate id");
         CHECK(default_nlist(10000) == 100 && default_nlist(0) == 1 && default_nlist(2) == 1);
+    }
+    // ---- test_pipeline.cpp
+    {   // train_chunk :44-92
+        const VectorMatrix chunk = clustered(120, 8, 5);
+        const ChunkOutput one = train_chunk(chunk, 4, 1, 10, 3);
+        CHECK(one.representatives.rows == 1 && one.representatives.dims == 8);
+        for (std::size_t d = 0; d < 8; ++d) {
+            double mean = 0.0;
+            for (std::size_t i = 0; i < chunk.rows; ++i) mean += chunk.row(i)[d];
+            mean /= double(chunk.rows);
+            CHECK(std::fabs(one.representatives.row(0)[d] - mean) <= 1e-5 * std::max(1.0, std::fabs(mean)));
+        }
+        for (std::uint32_t ks : {2u, 8u, 32u}) {
+            const ChunkOutput o = train_chunk(chunk, 4, ks, 10, 3);
+            CHECK(o.representatives.rows == ks && o.representatives.dims == 8);
+        }
+        const VectorMatrix base = random_matrix(8, 8, 17, -5, 5);
+        VectorMatrix data(96, 8);
+        for (std::size_t i = 0; i < data.rows; ++i) std::memcpy(data.row(i), base.row(i % 8), 8 * sizeof(float));
+        const ChunkOutput out = train_chunk(data, 4, 8, 25, 7);
+        CHECK(out.local_rmse <= 1e-6);
+        for (std::uint32_t m = 0; m < 4; ++m) {
+            VectorMatrix got(8, 2), want(8, 2);
+            for (std::size_t j = 0; j < 8; ++j) {
+                std::memcpy(got.row(j), out.representatives.row(j) + m * 2, 2 * sizeof(float));
+                std::memcpy(want.row(j), base.row(j) + m * 2, 2 * sizeof(float));
+            }
+            CHECK(rows_equal_as_sets(got, want, 1e-6));
+        }
+        CHECK(reconstruction_rmse(fit_global(out.representatives, 4, 8, 25, 3), data) <= 1e-6);
+        CHECK_THROWS_WITH(train_chunk(clustered(4, 8, 1), 4, 8, 10, 0), std::invalid_argument,
+                          "fewer than ks");
+    }
+    {   // aggregate_representatives :94-129
+        std::vector<ChunkOutput> ordered(5);
+        for (std::size_t c = 0; c < 5; ++c) {
+            ordered[c].chunk_id = c;
+            ordered[c].representatives = random_matrix(3, 2, c + 1);
+        }
+        std::vector<ChunkOutput> shuffled = {ordered[3], ordered[0], ordered[4], ordered[2], ordered[1]};
+        CHECK(aggregate_representatives(ordered) == aggregate_representatives(shuffled));
+        CHECK(aggregate_representatives({ordered[0]}) == ordered[0].representatives);
+        std::vector<ChunkOutput> bad(2);
+        bad[0].representatives = random_matrix(2, 3, 1);
+        bad[1].chunk_id = 1;
+        bad[1].representatives = random_matrix(2, 4, 2);
+        CHECK_THROWS_WITH(aggregate_representatives(bad), std::invalid_argument, "dimension mismatch");
+    }
+    {   // fit_global :131-157
+        const VectorMatrix data = clustered(600, 8, 21);
+        ChunkOutput out = train_chunk(data, 4, 16, 20, 42);
+        const Codebook global = fit_global(aggregate_representatives({out}), 4, 16, 20, 42);
+        const Codebook local = pq_fit(data, 4, 16, 20, 42);
+        for (std::uint32_t m = 0; m < 4; ++m) {
+            VectorMatrix g(16, 2), l(16, 2);
+            std::memcpy(g.values.data(), global.sub_table(m), 16 * 2 * sizeof(float));
+            std::memcpy(l.values.data(), local.sub_table(m), 16 * 2 * sizeof(float));
+            CHECK(rows_equal_as_sets(g, l, 1e-6));
+        }
+        const Codebook cb = fit_global(VectorMatrix(10, 4, 2.5f), 2, 4, 10, 1);
+        CodeMatrix codes(1, 2, 4);
+        codes.set(0, 0, 3);
+        codes.set(0, 1, 1);
+        const VectorMatrix dec = pq_decode(cb, codes);
+        for (std::size_t t = 0; t < 4; ++t) CHECK(dec.row(0)[t] == 2.5f);
+    }
+    {   // run_pipeline :159-255
+        const VectorMatrix data = clustered(800, 8, 33);
+        PipelineConfig config;
+        config.m_subspaces = 4;
+        config.ks = 16;
+        config.kmeans_iters = 15;
+        config.seed = 3;
+        const PipelineReport a = run_pipeline(data, config);
+        config.mode = PipelineMode::kParallelPq;
+        const PipelineReport b = run_pipeline(data, config);
+        CHECK(std::fabs(a.global_rmse - b.global_rmse) <= 1e-6);
+        CHECK(a.single_rmse.has_value() && !b.single_rmse.has_value() && b.representatives.has_value());
+
+        const VectorMatrix d2 = clustered(700, 8, 61);
+        PipelineConfig c2;
+        c2.mode = PipelineMode::kParallelPqIndex;
+        c2.n_chunks = 5;
+        c2.m_subspaces = 4;
+        c2.ks = 16;
+        c2.nlist = 9;
+        c2.kmeans_iters = 10;
+        c2.seed = 11;
+        c2.n_threads = 2;
+        const PipelineReport r = run_pipeline(d2, c2);
+        c2.n_threads = 1;
+        const PipelineReport r1 = run_pipeline(d2, c2);
+        CHECK(r.global_codebook == r1.global_codebook && r.global_rmse == r1.global_rmse);
+        CHECK(r.merged_index.has_value() && r.merged_index->n_items == d2.rows);
+        const CodeMatrix codes = pq_encode(r.global_codebook, d2);
+        std::vector<std::uint64_t> ids(d2.rows);
+        std::iota(ids.begin(), ids.end(), std::uint64_t{0});
+        const VectorMatrix qs = random_matrix(12, 8, 5, -2, 12);
+        for (std::size_t q = 0; q < qs.rows; ++q) {
+            const auto x = ivf_query(*r.merged_index, qs.row_span(q), 8, r.merged_index->nlist());
+            CHECK(x.hits == flat_scan(r.global_codebook, codes, ids, qs.row_span(q), 8).hits);
+        }
+        for (const char* ph : {"chunking", "local_fit", "global_fit", "coarse_fit", "encode",
+                               "index_build", "merge"})
+            CHECK(r.phase_seconds.count(ph) && r.phase_seconds.at(ph) >= 0.0);
+        CHECK(r.summary().find("index: 700 items across 9 lists") != std::string::npos);
+
+        PipelineConfig bad;
+        bad.mode = PipelineMode::kParallelPq;
+        bad.n_chunks = 5;
+        bad.m_subspaces = 2;
+        bad.ks = 3;
+        bad.n_threads = 2;
+        CHECK_THROWS_WITH(run_pipeline(clustered(10, 4, 71), bad), std::runtime_error, "chunk ");
+        CHECK_THROWS_WITH(run_pipeline(clustered(10, 4, 71), bad), std::runtime_error, "fewer than ks");
+        CHECK(parse_mode("parallel_pq_index") == PipelineMode::kParallelPqIndex && !parse_mode("x"));
+
+        const VectorMatrix d3 = clustered(200, 8, 81);
+        const ChunkOutput o = train_chunk(d3, 4, 8, 10, 9);
+        CHECK(std::fabs(o.local_rmse - reconstruction_rmse(pq_fit(d3, 4, 8, 10, 9), d3)) <=
+              1e-12 * o.local_rmse);
     }
     std::printf("facade_test: %d checks, %d failures\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;

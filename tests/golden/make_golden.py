@@ -118,6 +118,30 @@ def main() -> None:
     g["ivf_build/offsets"], g["ivf_build/list_ids"] = boff, bid
     g["ivf_build/list_codes"], g["ivf_build/coarse"] = bcodes, bcoarse
 
+    # -- the chunked pipeline (proj/src/pipeline.cpp:84-266) -----------------
+    # pipe: uneven chunks (3001 = 5 x 600 + 1); pipe_dup: tiny chunks of
+    # rounded (duplicate-heavy) rows, so local fits reseed empty clusters.
+    pipe_cases = [
+        ("pipe", gaussian_mixture(3001, 16, 12, 5), 5, 4, 16, 0, 8, 3),
+        ("pipe_dup", np.round(gaussian_mixture(203, 8, 3, 6)), 6, 2, 16, 9, 6, 1),
+    ]
+    for name, pdata, C_, M_, ks_, nl_, it_, sd_ in pipe_cases:
+        g[f"{name}/data"] = pdata.astype(np.float32)
+        g[f"{name}/params"] = np.array([C_, M_, ks_, nl_, it_, sd_], np.uint64)
+        bounds = R.chunk_rows(pdata.shape[0], C_)
+        g[f"{name}/local_rmse"] = np.array(
+            [R.train_chunk(pdata[bounds[c]:bounds[c + 1]], M_, ks_, it_, sd_ + c)[1]
+             for c in range(C_)])
+        for mode in ("single", "parallel_pq", "parallel_pq_index"):
+            r = R.run_pipeline(pdata, C_, M_, ks_, nl_, it_, sd_, mode, threads=3)
+            key = f"{name}/{mode}"
+            g[f"{key}/tables"] = r["tables"]
+            g[f"{key}/rmse"] = np.array([r["rmse"]])
+            g[f"{key}/nlist"] = np.array([r["nlist"]], np.uint64)
+            for extra in ("representatives", "offsets", "list_ids", "list_codes", "coarse"):
+                if extra in r:
+                    g[f"{key}/{extra}"] = r[extra]
+
     g["chunk_rows/10_3"] = R.chunk_rows(10, 3)
     g["default_nlist"] = np.array([R.default_nlist(n) for n in (1, 2, 10, 100, 1000, 12345)],
                                   np.uint64)

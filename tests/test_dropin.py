@@ -48,7 +48,7 @@ def test_acceptance_details_match_reference():
     same values as the reference's own hot path on the same seeds."""
     if not (os.path.exists(PQG_BIN) and os.path.exists(REF_BIN)):
         pytest.skip("acceptance binaries not built")
-    crit = [1, 5, 6, 9]
+    crit = [1, 3, 5, 6, 9]
     ours, _ = run(PQG_BIN, crit)
     ref, _ = run(REF_BIN, crit)
     for c in crit:

@@ -157,3 +157,40 @@ def test_ivf_query_subset_golden(golden, orc):
         c = int(golden["ivf/q_sub_count"][qi])
         assert np.array_equal(ids, golden["ivf/q_sub_ids"][qi, :c])
         assert np.array_equal(bits(dist), bits(golden["ivf/q_sub_dist"][qi, :c]))
+
+
+# ---------------------------------------------------------------------------
+# the chunked pipeline (proj/src/pipeline.cpp:84-266)
+# ---------------------------------------------------------------------------
+PIPE_MODES = ("single", "parallel_pq", "parallel_pq_index")
+
+
+@pytest.mark.parametrize("case", ["pipe", "pipe_dup"])
+def test_pipeline_golden(golden, orc, case):
+    C_, M, ks, nl, it, sd = (int(v) for v in golden[f"{case}/params"])
+    data = golden[f"{case}/data"]
+    bounds = orc.chunk_rows(data.shape[0], C_)
+    local = [orc.train_chunk(data[bounds[c]:bounds[c + 1]], M, ks, it, sd + c)[1]
+             for c in range(C_)]
+    assert np.array_equal(bits(np.array(local)), bits(golden[f"{case}/local_rmse"]))
+    for mode in PIPE_MODES:
+        key = f"{case}/{mode}"
+        r = orc.run_pipeline(data, C_, M, ks, nl, it, sd, mode)
+        assert np.array_equal(bits(r["tables"]), bits(golden[f"{key}/tables"])), mode
+        assert r["rmse"] == golden[f"{key}/rmse"][0], mode
+        assert r["nlist"] == golden[f"{key}/nlist"][0]
+        for extra in ("representatives", "offsets", "list_ids", "list_codes", "coarse"):
+            if f"{key}/{extra}" in golden:
+                assert np.array_equal(r[extra], golden[f"{key}/{extra}"]), (mode, extra)
+
+
+def test_oracle_vs_ref_pipeline(orc, ref):
+    from paper_2604_21645_b200.datagen import gaussian_mixture
+    data = gaussian_mixture(1207, 12, 9, 31)
+    for mode in PIPE_MODES:
+        a = orc.run_pipeline(data, 4, 3, 32, 0, 7, 11, mode)
+        b = ref.run_pipeline(data, 4, 3, 32, 0, 7, 11, mode, threads=2)
+        assert np.array_equal(a["tables"], b["tables"]) and a["rmse"] == b["rmse"]
+        if mode == "parallel_pq_index":
+            assert np.array_equal(a["list_ids"], b["list_ids"])
+            assert np.array_equal(a["offsets"], b["offsets"])
