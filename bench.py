@@ -520,8 +520,26 @@ def adc_bench(ctx, lib, L, x, train, args, world, stream, timed):
     ctx.profile(False)
     off = torch.empty(nlist + 1, dtype=torch.int64)
     L.check(lib.pqg_index_export(ctx.h, h, vp(off.data_ptr()), None, None, None, None))
+    # candidates actually scanned: S_q = sum of the probed lists' lengths
+    probes = torch.empty((nq, nprobe), dtype=torch.int32, device="cuda")
+    L.check(lib.pqg_index_probe(ctx.h, h, vp(q.data_ptr()), nq, nprobe, vp(probes.data_ptr())))
+    sizes = (off[1:] - off[:-1]).cuda()
+    cand = int(sizes[probes.long()].sum())
     lib.pqg_index_destroy(h)
+    scan_ms_b = scan_ms / (max(3, args.steps // 2) + 2)
+    peaks, psrc = measured_peaks()
+    code_bytes = cand * M  # algorithmic bytes: the probed lists' code rows, read once
+    ach = code_bytes / (scan_ms_b / 1e3) / 1e9
     return {"queries_per_s": nq / (ms / 1e3), "ms_per_batch": ms, "nq": nq,
+            "candidates_per_query": cand / nq,
+            "roofline_scan": {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"],
+                              "unit": "GB/s", "frac": ach / peaks["hbm_gbs"],
+                              "kernel": "adc_scan_kernel", "kernel_ms": scan_ms_b,
+                              "algorithmic": "S_q*M code bytes per query (S_q measured from the "
+                                             "probe lists) x nq per launch",
+                              "peak_source": psrc,
+                              "note": "the 16 MB of codes are L2-resident across the batch; "
+                                      "the scan is bound by shared-memory LUT gathers"},
             "index_rows": N_ROWS * world, "shards": world,
             "nprobe": nprobe, "k": k, "nlist": nlist, "M": M, "Ks": ks,
             "coarse_kmeans_seconds": coarse_s, "coarse_iters_run": it.value,
