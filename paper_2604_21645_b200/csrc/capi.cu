@@ -178,6 +178,7 @@ struct pqg_index {
     uint64_t* offsets = nullptr;
     uint64_t* ids = nullptr;
     uint8_t* codes = nullptr;
+    mutable TcCache tc;  // decoded candidate operand of the tensor-core search (built lazily)
 
     uint64_t D() const { return uint64_t(M) * ds; }
     uint64_t rb() const { return uint64_t(M) * w; }
@@ -186,6 +187,7 @@ struct pqg_index {
                          offsets, ids, codes, n};
     }
     void free_all() {
+        adc_tc_free(tc);
         for (void* p : {(void*)tables, (void*)coarse, (void*)coarse_norm, (void*)coarse_max,
                         (void*)offsets, (void*)ids, (void*)codes})
             if (p) cudaFree(p);
@@ -566,6 +568,24 @@ static uint64_t default_nlist_of(uint64_t n) {  // proj/src/ivf.cpp:118-121
 using Clock = std::chrono::steady_clock;
 static double seconds_since(Clock::time_point t) {
     return std::chrono::duration<double>(Clock::now() - t).count();
+}
+
+// Search of nq queries with their probe lists: the tensor-core screened scan
+// when it applies (adc_tc.cu), else the LUT scan (ivf.cu).  Both are exact.
+static void search_scan(pqg_ctx* ctx, const pqg_index* ix, const float* dq, uint64_t nq,
+                        const uint32_t* probes, uint64_t nprobe, uint64_t k, int has_max,
+                        double max_sq, uint64_t* oi, double* od, uint32_t* oc,
+                        const uint64_t* subset = nullptr, uint64_t nsub = 0) {
+    const IndexView v = ix->view();
+    if (ix->tc.state >= 0 && adc_tc_supported(v, nq, k, nprobe)) {
+        if (ix->tc.state == 0) ix->tc.state = adc_tc_prepare(ctx, v, ix->tc) ? 1 : -1;
+        if (ix->tc.state == 1) {
+            adc_tc_search(ctx, v, ix->tc, dq, nq, probes, nprobe, k, has_max, max_sq, subset, nsub,
+                          oi, od, oc);
+            return;
+        }
+    }
+    ivf_scan(ctx, v, dq, nq, probes, nprobe, k, has_max, max_sq, oi, od, oc, ctx->d_err, subset, nsub);
 }
 
 // ===========================================================================
@@ -1294,6 +1314,7 @@ int pqg_index_add(pqg_ctx* ctx, pqg_index* ix, const uint8_t* codes, const uint6
         uint64_t* ids_b = scratch<uint64_t>(ctx, n);
         uint8_t* codes_b = scratch<uint8_t>(ctx, n * rb);
         csr_scatter(ctx, bk.perm, n, di, dc, rb, ids_b, codes_b);
+        adc_tc_free(ix->tc);  // the cached decoded operand no longer matches the lists
         concat_into(ctx, ix, ix, off_b, ids_b, codes_b, n);
     });
 }
@@ -1383,8 +1404,7 @@ int pqg_index_search(pqg_ctx* ctx, const pqg_index* ix, const float* queries, ui
         uint32_t* probes = scratch<uint32_t>(ctx, nq * nprobe);
         ivf_probe(ctx, ix->view(), dq, nq, nprobe, probes);
         reset_err(ctx);
-        ivf_scan(ctx, ix->view(), dq, nq, probes, nprobe, k, has_max, max_sq_dist, oi.dev, od.dev,
-                 oc.dev, ctx->d_err);
+        search_scan(ctx, ix, dq, nq, probes, nprobe, k, has_max, max_sq_dist, oi.dev, od.dev, oc.dev);
         finish(ctx, oi);
         finish(ctx, od);
         finish(ctx, oc);
@@ -1422,8 +1442,8 @@ int pqg_index_search_subset(pqg_ctx* ctx, const pqg_index* ix, const float* quer
         uint32_t* probes = scratch<uint32_t>(ctx, nq * nprobe);
         ivf_probe(ctx, ix->view(), dq, nq, nprobe, probes);
         reset_err(ctx);
-        ivf_scan(ctx, ix->view(), dq, nq, probes, nprobe, k, has_max, max_sq_dist, oi.dev, od.dev,
-                 oc.dev, ctx->d_err, dsub, nsub);
+        search_scan(ctx, ix, dq, nq, probes, nprobe, k, has_max, max_sq_dist, oi.dev, od.dev, oc.dev,
+                    dsub, nsub);
         finish(ctx, oi);
         finish(ctx, od);
         finish(ctx, oc);

@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kScanThreads) adc_scan_kernel(
     const float* tables, uint32_t M, uint32_t ks, uint32_t ds, const float* queries,
     const uint64_t* offsets, const uint64_t* ids, const uint8_t* codes, const uint32_t* probes,
     uint64_t nprobe, int k, int has_max, double max_sq, const uint64_t* subset, uint64_t nsub,
-    uint64_t* out_ids, double* out_dists, uint32_t* out_counts, int* err) {
+    uint64_t* out_ids, double* out_dists, uint32_t* out_counts, int* err, const float* luts) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* lut = reinterpret_cast<float*>(smem_raw);  // [M][ks]
     TopK* wl = reinterpret_cast<TopK*>(smem_raw + ((sizeof(float) * M * ks + 15) & ~size_t(15)));
@@ -240,9 +240,14 @@ __global__ void __launch_bounds__(kScanThreads) adc_scan_kernel(
     const uint32_t rb = M * w;
     const uint64_t D = uint64_t(M) * ds;
     const float* qv = queries + q * D;
-    for (uint32_t e = threadIdx.x; e < M * ks; e += blockDim.x) {
-        const uint32_t m = e / ks;
-        lut[e] = __double2float_rn(exact_sq_l2(qv + uint64_t(m) * ds, tables + uint64_t(e) * ds, int(ds)));
+    if (luts) {  // tables already built (adc_tables, identical entries)
+        const float* lq = luts + q * uint64_t(M) * ks;
+        for (uint32_t e = threadIdx.x; e < M * ks; e += blockDim.x) lut[e] = __ldg(lq + e);
+    } else {
+        for (uint32_t e = threadIdx.x; e < M * ks; e += blockDim.x) {
+            const uint32_t m = e / ks;
+            lut[e] = __double2float_rn(exact_sq_l2(qv + uint64_t(m) * ds, tables + uint64_t(e) * ds, int(ds)));
+        }
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -487,7 +492,7 @@ void ivf_probe(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t
 void ivf_scan(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t nq,
               const uint32_t* probes, uint64_t nprobe, uint64_t k, int has_max, double max_sq,
               uint64_t* out_ids, double* out_dists, uint32_t* out_counts, int* err,
-              const uint64_t* subset, uint64_t nsub) {
+              const uint64_t* subset, uint64_t nsub, const float* luts) {
     if (k > 32) fail(PQG_EUNSUPPORTED, "search: k > 32 is not supported by the warp top-k path");
     const size_t lut_bytes = (sizeof(float) * ix.M * ix.ks + 15) & ~size_t(15);
     const size_t smem = lut_bytes + sizeof(TopK) * k * (kScanThreads / 32);
@@ -500,7 +505,8 @@ void ivf_scan(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t 
             launch(ctx, "adc_scan", kern, dim3(unsigned(nc)), dim3(kScanThreads), smem, ix.tables,
                    ix.M, ix.ks, ix.ds, queries + q0 * ix.M * ix.ds, ix.offsets, ix.ids, ix.codes,
                    probes + q0 * nprobe, nprobe, int(k), has_max, max_sq, subset, nsub,
-                   out_ids + q0 * k, out_dists + q0 * k, out_counts + q0, err);
+                   out_ids + q0 * k, out_dists + q0 * k, out_counts + q0, err,
+                   luts ? luts + q0 * uint64_t(ix.M) * ix.ks : nullptr);
         }
     };
     // vector code loads need rb-aligned rows (CSR rows are rb apart from an aligned base)
