@@ -186,6 +186,16 @@ __device__ __forceinline__ void warp_insert(double& my_d, uint64_t& my_id, doubl
     }
 }
 
+// (a0, a1) += (b0, b1) as one packed FADD2 (sm_100): the even and odd
+// subspace chains of the screen sum advance together.
+__device__ __forceinline__ void add_f32x2(float& a0, float& a1, float b0, float b1) {
+    unsigned long long x, y, r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a0), "f"(a1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(y) : "f"(b0), "f"(b1));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(r));
+}
+
 // A code row of RB bytes (RB in {4, 8, 16, 32}) read with vector loads; the
 // codes are extracted from registers (RB == 0: generic byte path).
 template <int RB>
@@ -254,12 +264,16 @@ __global__ void __launch_bounds__(kScanThreads) adc_scan_kernel(
     const double inf = __longlong_as_double(0x7ff0000000000000LL);
     double my_d = inf;
     uint64_t my_id = ~uint64_t(0);
+    // the list's current k-th entry, held by every lane (refreshed after inserts
+    // only): the screen and the insertion test need no shuffles
+    double kd = inf;
+    uint64_t ki = ~uint64_t(0);
     const float shrink = 1.0f - float(M + 2) * kU * 1.05f;
     for (uint64_t p = 0; p < nprobe; ++p) {
         const uint32_t l = probes[q * nprobe + p];
         const uint64_t beg = offsets[l], end = offsets[l + 1];
         for (uint64_t base = beg + uint64_t(wid) * 32; base < end; base += kScanThreads) {
-            const double th = __shfl_sync(0xffffffffu, my_d, k - 1);
+            const double th = kd;
             const uint64_t e = base + lane;
             bool want = false;
             double s64 = 0.0;
@@ -274,16 +288,16 @@ __global__ void __launch_bounds__(kScanThreads) adc_scan_kernel(
                     CodeRow<RB> row;
                     row.load(cr);
                     constexpr int MM = RB / W;
-                    float s_even = 0.f, s_odd = 0.f;  // two chains: half the FADD latency
+                    float s_even = 0.f, s_odd = 0.f;  // two chains, one FADD2 per pair
 #pragma unroll
-                    for (int m = 0; m < MM; ++m) {
-                        uint32_t c = row.template get<W>(m);
+                    for (int m = 0; m < MM; m += 2) {
+                        uint32_t c0 = row.template get<W>(m), c1 = row.template get<W>(m + 1);
                         if (check) {
-                            if (c >= ks) bad = true;
-                            c = min(c, ks - 1);
+                            if (c0 >= ks || c1 >= ks) bad = true;
+                            c0 = min(c0, ks - 1);
+                            c1 = min(c1, ks - 1);
                         }
-                        if (m & 1) s_odd += lut[m * ksc + c];
-                        else s_even += lut[m * ksc + c];
+                        add_f32x2(s_even, s_odd, lut[m * ksc + c0], lut[(m + 1) * ksc + c1]);
                     }
                     s32 = s_even + s_odd;
                     if (!bad) {
@@ -314,15 +328,17 @@ __global__ void __launch_bounds__(kScanThreads) adc_scan_kernel(
                 }
                 if (bad) atomicExch(err, 1);
             }
+            want = want && pair_less(s64, id, kd, ki);
             uint32_t ball = __ballot_sync(0xffffffffu, want);
             while (ball) {
                 const int src = __ffs(ball) - 1;
-                ball &= ball - 1;
                 const double cd = __shfl_sync(0xffffffffu, s64, src);
                 const uint64_t cid = __shfl_sync(0xffffffffu, id, src);
-                const double thd = __shfl_sync(0xffffffffu, my_d, k - 1);
-                const uint64_t thi = __shfl_sync(0xffffffffu, my_id, k - 1);
-                if (pair_less(cd, cid, thd, thi)) warp_insert(my_d, my_id, cd, cid, k, lane);
+                warp_insert(my_d, my_id, cd, cid, k, lane);
+                kd = __shfl_sync(0xffffffffu, my_d, k - 1);
+                ki = __shfl_sync(0xffffffffu, my_id, k - 1);
+                want = want && lane != src && pair_less(s64, id, kd, ki);
+                ball = __ballot_sync(0xffffffffu, want);
             }
         }
     }
