@@ -3,15 +3,14 @@
 // stable scatter) shared with the inverted-index build (K6).
 //
 // Exactness.  The reference accumulates centroid sums in fp64 in row order
-// (kmeans.cpp:103-111).  Floating-point addition is not associative, so a
-// parallel reduction would not reproduce those bits.  Instead the rows are
-// first bucketed by cluster with a STABLE counting sort (members of each
-// cluster in ascending row order), then one thread per (problem, cluster,
-// dimension) adds its members' values in exactly the reference's order.  The
-// mean is float(sum * (1.0 / count)) (:112-118) and empty clusters are
-// reseeded from the pre-update fp64 distances, ascending cluster order,
-// strict '>' argmax (:122-130).  The resulting centroids are bit-identical to
-// the reference's.
+// (kmeans.cpp:103-111).  Floating-point addition is not associative in
+// general, so the rows are first bucketed by cluster with a STABLE counting
+// sort (members of each cluster in ascending row order).  The sums are then
+// taken in parallel where that provably equals the row-order sum (all partial
+// sums exact, see mean_exact_kernel) and in row order otherwise.  The mean is
+// float(sum * (1.0 / count)) (:112-118) and empty clusters are reseeded from
+// the pre-update fp64 distances, ascending cluster order, strict '>' argmax
+// (:122-130).  The resulting centroids are bit-identical to the reference's.
 #include "kernels.cuh"
 
 namespace pqg {
@@ -283,53 +282,106 @@ __global__ void final_parts_kernel(const double* parts, uint32_t nparts, double*
     if (threadIdx.x == 0) out[b] = s;
 }
 
-// ---- ordered fp64 sums -> means (rows gathered into member order first)
-// Rows gathered into member order (problem b's column block only), so the
-// ordered sums below stream contiguous memory instead of chasing indices.
-__global__ void gather_sorted_kernel(const float* x, uint64_t ldx, uint32_t col_stride, uint64_t n,
-                                     uint32_t B, uint32_t d, const uint32_t* perm, float* sorted,
-                                     const int* active, const uint64_t* nb) {
-    const uint64_t total = uint64_t(B) * n * d;
-    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
-         e += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t bp = e / d, t = e - bp * d;
-        const uint64_t b = bp / n;
-        if (active && !active[b]) continue;
-        if (nb && bp - b * n >= nb[b]) continue;  // padding rows of a shorter problem
-        sorted[e] = __ldg(x + uint64_t(__ldg(perm + bp)) * ldx + b * col_stride + t);
-    }
-}
+// Centroid means without a sequential chain.  The reference adds the members'
+// fp32 values into an fp64 sum in row order (kmeans.cpp:103-111).  Every fp32
+// value is an integer multiple of the smallest member's ulp; when the largest
+// magnitude is within 2^(28 - ceil(log2 count)) of that ulp scale, every
+// partial sum of any order fits in fp64's 53-bit significand, so all orders
+// give the same exact sum and the members can be added in parallel.  A
+// (cluster, dim) outside that range (values spanning > ~20 binades, or
+// non-finite) is summed sequentially in row order as the reference does.
+// One CTA per (problem, cluster): threads = (member group, dim), rows read
+// through the stable member permutation (no gathered copy).
+constexpr int kMeanThreads = 256;
+constexpr int kMeanStage = 4096;  // members staged per step of the row-order fallback
 
-// One thread per (problem, cluster, dim): sequential fp64 sum over the
-// cluster's members (ascending row order, contiguous in `sorted`), then
-// float(sum * (1/count)).  Loads are issued 16 ahead of the dependent adds.
-__global__ void mean_sorted_kernel(const float* sorted, uint64_t n, uint32_t B, uint32_t d,
-                                   uint64_t k, const uint64_t* offsets, float* table,
-                                   int* has_empty, const int* active) {
-    const uint64_t total = uint64_t(B) * k * d;
-    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
-         e += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t bc = e / d, t = e - bc * d;
-        const uint64_t b = bc / k, c = bc - b * k;
-        if (active && !active[b]) continue;
-        const uint64_t* off = offsets + b * (k + 1);
-        const uint64_t beg = off[c], end = off[c + 1];
-        if (beg == end) {
-            has_empty[b] = 1;
-            continue;
-        }
-        const float* src = sorted + (b * n) * d + t;
+__global__ void __launch_bounds__(kMeanThreads) mean_exact_kernel(
+    const float* x, uint64_t ldx, uint32_t col_stride, uint64_t n, uint32_t d, uint64_t k,
+    const uint64_t* offsets, const uint32_t* perm, float* table, int* has_empty, const int* active) {
+    __shared__ double ps[kMeanThreads];
+    __shared__ int pmax[kMeanThreads], pmin[kMeanThreads];
+    __shared__ float col[kMeanStage];  // one dim of the members, row order (fallback)
+    __shared__ uint32_t nfail;
+    __shared__ uint32_t failed[kMeanThreads];
+    const uint64_t bc = blockIdx.x;
+    const uint64_t b = bc / k, c = bc - b * k;
+    if (active && !active[b]) return;
+    const uint64_t* off = offsets + b * (k + 1);
+    const uint64_t beg = off[c], end = off[c + 1];
+    if (beg == end) {
+        if (threadIdx.x == 0) has_empty[b] = 1;
+        return;
+    }
+    const uint64_t cnt = end - beg;
+    const uint32_t* pb = perm + b * n;
+    const float* xb = x + b * col_stride;
+    const uint32_t DG = d < kMeanThreads ? d : kMeanThreads;
+    const uint32_t G = kMeanThreads / DG;
+    const uint32_t g = threadIdx.x / DG, tl = threadIdx.x - g * DG;
+    int lg = 0;
+    while ((uint64_t(1) << lg) < cnt) ++lg;
+    const double inv = __ddiv_rn(1.0, (double)cnt);
+    for (uint32_t t0 = 0; t0 < d; t0 += DG) {
+        const uint32_t t = t0 + tl;
         double s = 0.0;
-        uint64_t m = beg;
-        for (; m + 16 <= end; m += 16) {
-            float v[16];
+        int emax = -1, emin = 1 << 30;
+        if (g < G && t < d) {
+            auto acc = [&](float v) {
+                s = __dadd_rn(s, (double)v);
+                const int e = int((__float_as_uint(v) >> 23) & 0xFFu);
+                if (v != 0.f) {
+                    emax = max(emax, e);
+                    emin = min(emin, max(e, 1));
+                }
+            };
+            uint64_t m = beg + g;
+            // four members in flight per thread: the permutation and row loads of
+            // one step are independent of the adds
+            for (; m + 3 * uint64_t(G) < end; m += 4 * uint64_t(G)) {
+                uint32_t r[4];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = __ldg(src + (m + j) * d);
+                for (int u = 0; u < 4; ++u) r[u] = __ldg(pb + m + u * G);
+                float v[4];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) s = __dadd_rn(s, (double)v[j]);
+                for (int u = 0; u < 4; ++u) v[u] = __ldg(xb + uint64_t(r[u]) * ldx + t);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) acc(v[u]);
+            }
+            for (; m < end; m += G) acc(__ldg(xb + uint64_t(__ldg(pb + m)) * ldx + t));
         }
-        for (; m < end; ++m) s = __dadd_rn(s, (double)__ldg(src + m * d));
-        table[e] = __double2float_rn(__dmul_rn(s, __ddiv_rn(1.0, (double)(end - beg))));
+        ps[threadIdx.x] = s;
+        pmax[threadIdx.x] = emax;
+        pmin[threadIdx.x] = emin;
+        if (threadIdx.x == 0) nfail = 0;
+        __syncthreads();
+        if (g == 0 && t < d) {
+            for (uint32_t h = 1; h < G; ++h) {
+                s = __dadd_rn(s, ps[h * DG + tl]);
+                emax = max(emax, pmax[h * DG + tl]);
+                emin = min(emin, pmin[h * DG + tl]);
+            }
+            const bool exact = emax < 0 || (emax < 255 && emax - emin + lg <= 28);
+            if (exact) table[bc * d + t] = __double2float_rn(__dmul_rn(s, inv));  // kmeans.cpp:112-118
+            else failed[atomicAdd(&nfail, 1u)] = t;
+        }
+        __syncthreads();
+        // row-order sums (kmeans.cpp:103-111) for the dims the exactness test
+        // rejects: the block stages the column, one thread adds it in order
+        for (uint32_t fi = 0; fi < nfail; ++fi) {
+            const uint32_t tf = failed[fi];
+            double sf = 0.0;
+            for (uint64_t m0 = beg; m0 < end; m0 += kMeanStage) {
+                const uint64_t m1 = m0 + kMeanStage < end ? m0 + kMeanStage : end;
+                for (uint64_t m = m0 + threadIdx.x; m < m1; m += blockDim.x)
+                    col[m - m0] = __ldg(xb + uint64_t(__ldg(pb + m)) * ldx + tf);
+                __syncthreads();
+                if (threadIdx.x == 0)
+                    for (uint64_t m = m0; m < m1; ++m) sf = __dadd_rn(sf, (double)col[m - m0]);
+                __syncthreads();
+            }
+            if (threadIdx.x == 0) table[bc * d + tf] = __double2float_rn(__dmul_rn(sf, inv));
+        }
+        __syncthreads();
     }
 }
 
@@ -471,13 +523,10 @@ void kmeans_update(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint
     stable_bucket(ctx, assign, n, B, k, active, bk, nb);
     int* has_empty = scratch<int>(ctx, B);
     PQG_CUDA(cudaMemsetAsync(has_empty, 0, sizeof(int) * B, ctx->stream));
-    const uint64_t total = uint64_t(B) * k * d;
-    float* sorted = scratch<float>(ctx, uint64_t(B) * n * d);
-    launch(ctx, "kmeans_sum", gather_sorted_kernel, dim3(grid1d(uint64_t(B) * n * d, 256, ctx->num_sms * 64)),
-           dim3(256), 0, src.x, src.ldx, src.col_stride, n, B, d, (const uint32_t*)bk.perm, sorted,
-           active, nb);
-    launch(ctx, "kmeans_sum", mean_sorted_kernel, dim3(grid1d(total, 128, 1u << 20)), dim3(128), 0,
-           (const float*)sorted, n, B, d, k, (const uint64_t*)bk.offsets, table, has_empty, active);
+    if (uint64_t(B) * k > 0x7FFFFFFFull) fail(PQG_EUNSUPPORTED, "kmeans: too many clusters");
+    launch(ctx, "kmeans_sum", mean_exact_kernel, dim3(unsigned(uint64_t(B) * k)), dim3(kMeanThreads), 0,
+           src.x, src.ldx, src.col_stride, n, d, k, (const uint64_t*)bk.offsets,
+           (const uint32_t*)bk.perm, table, has_empty, active);
     launch(ctx, "reseed", reseed_kernel, dim3(B), dim3(1024), 0, src.x, src.ldx, src.col_stride, n,
            d, k, (const uint64_t*)bk.offsets, dist, table, (const int*)has_empty, active, nb);
 }

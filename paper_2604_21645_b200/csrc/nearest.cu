@@ -25,6 +25,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cstdio>
+
 #include "kernels.cuh"
 
 namespace pqg {
@@ -319,59 +321,65 @@ __global__ void __launch_bounds__(NT, 2) nearest_kernel(NearestArgs a) {
 // value is <= vmin (1+eps)/(1-eps); pass 2 re-scores exactly those in the
 // reference's fp64 arithmetic and takes the (dist, index) minimum -- the
 // result of nearest_in_table (strict '<', lowest index on ties).
-constexpr int kFixWarps = 8;
+constexpr int kFixThreads = 256;
 constexpr int kFixMaxD = 512;
 
-__global__ void __launch_bounds__(32 * kFixWarps) fixup_kernel(NearestArgs a) {
-    __shared__ float xs_all[kFixWarps][kFixMaxD];
+// Exact resolution of the flagged (row, problem) pairs: one CTA per pair, its
+// threads split the k centroids (a single flagged row no longer runs on one
+// warp's latency).  Pass 1: fp32 distances, block minimum; pass 2: every
+// centroid whose fp32 distance is within the fp32 error of that minimum is
+// re-scored in the reference's fp64 arithmetic (kmeans.cpp:11-31), strict '<'
+// with the lowest index on ties.
+__global__ void __launch_bounds__(kFixThreads) fixup_kernel(NearestArgs a) {
+    __shared__ float xs[kFixMaxD];
+    __shared__ float red_f[kFixThreads / 32];
+    __shared__ double red_d[kFixThreads / 32];
+    __shared__ uint32_t red_j[kFixThreads / 32];
     const unsigned long long cnt = *a.flag_count;
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t d = a.d;
     const bool staged = d <= kFixMaxD;
-    float* xs = xs_all[wib];
     const float eps = float(d + 2) * kU * 1.01f;
-    for (uint64_t f = warp; f < cnt; f += nwarps) {
+    for (uint64_t f = blockIdx.x; f < cnt; f += gridDim.x) {
         const uint64_t item = a.flags[f];
         const uint32_t b = uint32_t(item >> 40);
         const uint64_t row = item & ((uint64_t(1) << 40) - 1);
         const float* tab = a.table + (uint64_t)b * a.k * d;
-        if (staged) {
-            __syncwarp();
-            for (uint32_t t = lane; t < d; t += 32) xs[t] = load_x(a.src, row, b, t);
-            __syncwarp();
-        }
+        __syncthreads();  // previous item's reductions are consumed
+        if (staged)
+            for (uint32_t t = threadIdx.x; t < d; t += blockDim.x) xs[t] = load_x(a.src, row, b, t);
+        __syncthreads();
         auto xval = [&](uint32_t t) { return staged ? xs[t] : load_x(a.src, row, b, t); };
-        float vmin = __int_as_float(0x7f800000);
-        for (uint64_t j = lane; j < a.k; j += 32) {
+        auto fdist = [&](uint64_t j) {
             const float* c = tab + j * d;
             float v = 0.f;
             for (uint32_t t = 0; t < d; ++t) {
                 const float df = xval(t) - __ldg(c + t);
                 v = fmaf(df, df, v);
             }
-            vmin = fminf(vmin, v);
-        }
+            return v;
+        };
+        float vmin = __int_as_float(0x7f800000);
+        for (uint64_t j = threadIdx.x; j < a.k; j += blockDim.x) vmin = fminf(vmin, fdist(j));
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, off));
+        if (lane == 0) red_f[wid] = vmin;
+        __syncthreads();
+        vmin = red_f[0];
+        for (int w = 1; w < kFixThreads / 32; ++w) vmin = fminf(vmin, red_f[w]);
         const float thr = vmin * ((1.f + eps) / (1.f - eps)) * (1.f + 4.f * kU) + 1e-37f;
         double best = __longlong_as_double(0x7ff0000000000000LL);
         uint32_t bj = 0xFFFFFFFFu;
-        for (uint64_t j = lane; j < a.k; j += 32) {
-            const float* c = tab + j * d;
-            float v = 0.f;
-            for (uint32_t t = 0; t < d; ++t) {
-                const float df = xval(t) - __ldg(c + t);
-                v = fmaf(df, df, v);
-            }
+        for (uint64_t j = threadIdx.x; j < a.k; j += blockDim.x) {
+            const float v = fdist(j);
             if (!(v <= thr) && !(v != v)) continue;  // NaN candidates go to the exact path
+            const float* c = tab + j * d;
             double acc = 0.0;
             for (uint32_t t = 0; t < d; ++t) {
                 const double diff = __dsub_rn((double)xval(t), (double)__ldg(c + t));
                 acc = __dadd_rn(acc, __dmul_rn(diff, diff));
             }
-            if (acc < best) { best = acc; bj = uint32_t(j); }
+            if (acc < best || (acc == best && uint32_t(j) < bj)) { best = acc; bj = uint32_t(j); }
         }
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) {
@@ -380,6 +388,16 @@ __global__ void __launch_bounds__(32 * kFixWarps) fixup_kernel(NearestArgs a) {
             if (ob < best || (ob == best && oj < bj)) { best = ob; bj = oj; }
         }
         if (lane == 0) {
+            red_d[wid] = best;
+            red_j[wid] = bj;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {  // holds warp 0's result; merge the other warps
+            for (int w = 1; w < kFixThreads / 32; ++w)
+                if (red_d[w] < best || (red_d[w] == best && red_j[w] < bj)) {
+                    best = red_d[w];
+                    bj = red_j[w];
+                }
             if (bj == 0xFFFFFFFFu) {  // every distance NaN: the reference keeps index 0
                 bj = 0;
                 best = exact_dist(a, row, b, tab);
@@ -470,7 +488,14 @@ void nearest(pqg_ctx* ctx, NearestArgs a) {
     if (!force_fp32 && umma_screen_supported(a)) umma_screen(ctx, a);
     else if (!force_fp32 && umma_big_supported(a)) umma_big(ctx, a);
     else dispatch<false>(ctx, a);
-    launch(ctx, "fixup", fixup_kernel, dim3(ctx->num_sms * 4), dim3(32 * kFixWarps), 0, a);
+    launch(ctx, "fixup", fixup_kernel, dim3(ctx->num_sms * 4), dim3(kFixThreads), 0, a);
+    if (std::getenv("PQG_FLAG_STATS")) {  // diagnostics: rows sent to the exact fixup
+        unsigned long long h = 0;
+        PQG_CUDA(cudaMemcpyAsync(&h, a.flag_count, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+        PQG_CUDA(cudaStreamSynchronize(ctx->stream));
+        std::fprintf(stderr, "nearest: n=%llu B=%u k=%llu d=%u flagged=%llu\n", (unsigned long long)a.n,
+                     a.B, (unsigned long long)a.k, a.d, h);
+    }
 }
 
 void distance_matrix(pqg_ctx* ctx, NearestArgs a) {
