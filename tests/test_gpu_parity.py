@@ -102,6 +102,29 @@ def test_kmeans_random_vs_oracle(pq, orc, seed):
     np.testing.assert_allclose(a.inertia_per_iter, b["inertia_per_iter"], rtol=1e-12)
 
 
+@pytest.mark.parametrize("scale", ["wide", "tiny", "mixed_sign"])
+def test_kmeans_sum_order_paths(pq, orc, scale):
+    """Centroid sums: the parallel path is taken only when every partial sum
+    is exact; columns spanning many binades (or huge cancellations) must fall
+    back to the reference's row order and still match bit for bit."""
+    rng = np.random.default_rng(7)
+    pts = orc.random_matrix(4000, 6, 31).astype(np.float32)
+    if scale == "wide":      # values from 1e-30 to 1e4 in the same column
+        pts[:, 0] *= np.float32(10.0) ** rng.integers(-30, 5, size=4000).astype(np.float32)
+    elif scale == "tiny":    # subnormal and tiny magnitudes
+        pts[:, 1] *= np.float32(1e-38)
+        pts[::7, 2] = np.float32(1e-44)
+    else:                    # large +/- pairs that cancel
+        pts[:, 3] += np.where(rng.random(4000) < 0.5, 1e7, -1e7).astype(np.float32)
+    a = pq.kmeans_fit(pts, 37, 15, 3, 0.0)
+    b = orc.kmeans_fit(pts, 37, 15, 3, 0.0)
+    assert np.array_equal(bits(a.centroids), bits(b["centroids"]))
+    assert np.array_equal(a.assignments, b["assignments"])
+    t = pq.pq_fit(pts[:, :6], 3, 16, 8, 5).tables
+    ot, _, _ = orc.pq_fit(pts[:, :6], 3, 16, 8, 5)
+    assert np.array_equal(bits(t), bits(ot))
+
+
 def test_kmeans_validation(pq, orc):
     pts = orc.random_matrix(5, 2, 1)
     with pytest.raises(ValueError):
