@@ -82,6 +82,14 @@ def main():
                                                            ITERS, SEED + M, 1e-4, vp(coarse.data_ptr()),
                                                            None, C.byref(inertia), C.byref(citers), None)))
     out["coarse_fit_iters"] = citers.value
+    if os.environ.get("CFG5_PROFILE"):  # per-kernel-class breakdown of one more coarse fit
+        ctx.profile(True)
+        L.check(lib.pqg_kmeans_fit(ctx.h, vp(train.data_ptr()), n_train, D, NLIST, ITERS, SEED + M, 1e-4,
+                                   vp(coarse.data_ptr()), None, C.byref(inertia), C.byref(citers), None))
+        out["coarse_fit_classes_ms"] = {c: ctx.profile_read(c)[1] for c in (
+            "nearest_big_tc", "big_split", "fixup", "norms", "inertia", "bucket", "scan", "kmeans_sum",
+            "reseed", "gather")}
+        ctx.profile(False)
     codes = torch.empty((args.rows, M), dtype=torch.uint8, device="cuda")
     timed("encode", lambda: L.check(lib.pqg_pq_encode(ctx.h, vp(x.data_ptr()), args.rows, M, KS, D // M,
                                                       vp(tables.data_ptr()), vp(codes.data_ptr()))))
