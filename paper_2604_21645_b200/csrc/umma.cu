@@ -207,30 +207,39 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
     const bool vec4 = ((a.src.ldx | a.src.col_stride) & 3u) == 0 &&
                       (reinterpret_cast<uintptr_t>(a.src.x) & 15u) == 0;
     const uint64_t ntiles = (a.n + kRows - 1) / kRows;
+    // this thread's row of a tile, loaded one tile ahead so the global-load
+    // latency overlaps the current tile's MMA and epilogue
+    auto load_row = [&](uint64_t tl, float (&xx)[DS]) {
+        const uint64_t r = tl * kRows + tid;
+        if (tl < ntiles && r < a.n) {
+            const float* xp = a.src.x + r * a.src.ldx + uint64_t(b) * a.src.col_stride;
+            if (vec4) {
+#pragma unroll
+                for (int t = 0; t < DS; t += 4) {
+                    const float4 v = __ldg(reinterpret_cast<const float4*>(xp + t));
+                    xx[t] = v.x; xx[t + 1] = v.y; xx[t + 2] = v.z; xx[t + 3] = v.w;
+                }
+            } else {
+#pragma unroll
+                for (int t = 0; t < DS; ++t) xx[t] = __ldg(xp + t);
+            }
+        } else {
+#pragma unroll
+            for (int t = 0; t < DS; ++t) xx[t] = 0.f;
+        }
+    };
+    float x_next[DS];
+    load_row(cta, x_next);
     for (uint64_t tile = cta; tile < ntiles; tile += ncta) {
         const uint64_t row = tile * kRows + tid;
         const bool valid = row < a.n;
         // ---- stage A: this thread's row [x, 1, C]
         float x[DS];
         float nx = 0.f;
-        if (valid) {
-            const float* xp = a.src.x + row * a.src.ldx + uint64_t(b) * a.src.col_stride;
-            if (vec4) {
 #pragma unroll
-                for (int t = 0; t < DS; t += 4) {
-                    const float4 v = __ldg(reinterpret_cast<const float4*>(xp + t));
-                    x[t] = v.x; x[t + 1] = v.y; x[t + 2] = v.z; x[t + 3] = v.w;
-                }
-            } else {
+        for (int t = 0; t < DS; ++t) x[t] = x_next[t];
 #pragma unroll
-                for (int t = 0; t < DS; ++t) x[t] = __ldg(xp + t);
-            }
-#pragma unroll
-            for (int t = 0; t < DS; ++t) nx = fmaf(x[t], x[t], nx);
-        } else {
-#pragma unroll
-            for (int t = 0; t < DS; ++t) x[t] = 0.f;
-        }
+        for (int t = 0; t < DS; ++t) nx = fmaf(x[t], x[t], nx);
         const float q = sqrtf(nx) * (1.f + 1e-6f) + cmax;
         const float S = q * q * 1.01f + 1e-6f;  // >= 2|x.c| + ||c||^2 + C
         const float E = tc_error_bound(S, KA);
@@ -267,6 +276,7 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
             }
             mma_commit(&mbar);
         }
+        load_row(tile + ncta, x_next);  // next tile's row, in flight during this epilogue
         mbar_wait(&mbar, phase);
         phase ^= 1;
         fence_after();
