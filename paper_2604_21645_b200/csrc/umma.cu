@@ -165,7 +165,8 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
     const uint32_t cta = blockIdx.x / B, ncta = gridDim.x / B;
     if (a.active && !a.active[b]) return;
     const uint64_t k = a.k;
-    const float* tab = a.table + uint64_t(b) * k * DS;
+    const uint32_t d = a.d;  // actual sub-dimension, zero-padded to DS in the operands
+    const float* tab = a.table + uint64_t(b) * k * d;
     const float cmax = a.cmax[b];
 
     // ---- TMEM allocation (warp 0) and the mbarrier
@@ -184,7 +185,7 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
         const uint32_t j = e / KA, t = e - j * KA;
         float v = 0.f;
         if (j < k) {
-            if (t < DS) v = -2.f * __ldg(tab + uint64_t(j) * DS + t);
+            if (t < d) v = -2.f * __ldg(tab + uint64_t(j) * d + t);
             else if (t == DS) v = __ldg(a.cnorm + uint64_t(b) * k + j);
             else if (t == DS + 1) v = 1.f;
         } else if (t == DS) {
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
     const uint32_t b_hi = smem_u32(Bh), b_lo = smem_u32(Bl);
     uint32_t phase = 0;
 
-    const bool vec4 = ((a.src.ldx | a.src.col_stride) & 3u) == 0 &&
+    const bool vec4 = a.d == uint32_t(DS) && ((a.src.ldx | a.src.col_stride) & 3u) == 0 &&
                       (reinterpret_cast<uintptr_t>(a.src.x) & 15u) == 0;
     const uint64_t ntiles = (a.n + kRows - 1) / kRows;
     // this thread's row of a tile, loaded one tile ahead so the global-load
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
                 }
             } else {
 #pragma unroll
-                for (int t = 0; t < DS; ++t) xx[t] = __ldg(xp + t);
+                for (int t = 0; t < DS; ++t) xx[t] = uint32_t(t) < a.d ? __ldg(xp + t) : 0.f;
             }
         } else {
 #pragma unroll
@@ -334,10 +335,11 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
             if (unique && idx < k) {
                 store_index(a, row, b, idx);
                 if (a.out_dist) {
-                    const float* c = tab + uint64_t(idx) * DS;
+                    const float* c = tab + uint64_t(idx) * d;
                     double acc = 0.0;
 #pragma unroll
                     for (int t = 0; t < DS; ++t) {
+                        if (uint32_t(t) >= d) break;
                         const double diff = __dsub_rn((double)x[t], (double)__ldg(c + t));
                         acc = __dadd_rn(acc, __dmul_rn(diff, diff));
                     }
@@ -384,7 +386,7 @@ __device__ __forceinline__ void load_row(const NearestArgs& a, uint64_t row, uin
             }
         } else {
 #pragma unroll
-            for (int t = 0; t < DS; ++t) r.x[t] = __ldg(xp + t);
+            for (int t = 0; t < DS; ++t) r.x[t] = uint32_t(t) < a.d ? __ldg(xp + t) : 0.f;
         }
     } else {
 #pragma unroll
@@ -414,7 +416,8 @@ __global__ void __launch_bounds__(NW * 32, 1) umma_screen2_kernel(NearestArgs a,
     const uint32_t cta = blockIdx.x / B, ncta = gridDim.x / B;
     if (a.active && !a.active[b]) return;
     const uint64_t k = a.k;
-    const float* tab = a.table + uint64_t(b) * k * DS;
+    const uint32_t d = a.d;  // actual sub-dimension, zero-padded to DS in the operands
+    const float* tab = a.table + uint64_t(b) * k * d;
     const float cmax = a.cmax[b];
     const uint32_t row_l = tid & (kRows - 1);  // row of the tile this thread stages / reads
     const uint32_t half = tid >> 7;             // K part it stages, column part it reduces
@@ -433,7 +436,7 @@ __global__ void __launch_bounds__(NW * 32, 1) umma_screen2_kernel(NearestArgs a,
         const uint32_t j = e / KA, t = e - j * KA;
         float v = 0.f;
         if (j < k) {
-            if (t < DS) v = -2.f * __ldg(tab + uint64_t(j) * DS + t);
+            if (t < d) v = -2.f * __ldg(tab + uint64_t(j) * d + t);
             else if (t == DS) v = __ldg(a.cnorm + uint64_t(b) * k + j);
             else if (t == DS + 1) v = 1.f;
         } else if (t == DS) {
@@ -450,7 +453,7 @@ __global__ void __launch_bounds__(NW * 32, 1) umma_screen2_kernel(NearestArgs a,
     const uint32_t tmem = tmem_base;
     const uint32_t idesc = make_idesc_tf32(kRows, n_pad);
     const uint32_t b_hi = smem_u32(Bh), b_lo = smem_u32(Bl);
-    const bool vec4 = ((a.src.ldx | a.src.col_stride) & 3u) == 0 &&
+    const bool vec4 = a.d == uint32_t(DS) && ((a.src.ldx | a.src.col_stride) & 3u) == 0 &&
                       (reinterpret_cast<uintptr_t>(a.src.x) & 15u) == 0;
     const uint64_t ntiles = (a.n + kRows - 1) / kRows;
     const uint64_t my_tiles = cta < ntiles ? (ntiles - cta + ncta - 1) / ncta : 0;
@@ -599,10 +602,11 @@ __global__ void __launch_bounds__(NW * 32, 1) umma_screen2_kernel(NearestArgs a,
                     store_index(a, row, b, idx);
                     if (a.out_dist) {
                         const float* xp = a.src.x + row * a.src.ldx + uint64_t(b) * a.src.col_stride;
-                        const float* c = tab + uint64_t(idx) * DS;
+                        const float* c = tab + uint64_t(idx) * d;
                         double acc = 0.0;
 #pragma unroll
                         for (int t = 0; t < DS; ++t) {
+                            if (uint32_t(t) >= d) break;
                             const double diff = __dsub_rn((double)__ldg(xp + t), (double)__ldg(c + t));
                             acc = __dadd_rn(acc, __dmul_rn(diff, diff));
                         }
@@ -668,20 +672,21 @@ void launch_umma(pqg_ctx* ctx, const NearestArgs& a) {
 
 }  // namespace
 
+// Any sub-dimension up to 32 (zero-padded to 4/8/16/32 in both operands: the
+// padded products are exactly zero) and any 16 <= k <= 256 (codewords padded to
+// a multiple of 16 never win).
 bool umma_screen_supported(const NearestArgs& a) {
     if (a.src.codes || a.out_mat) return false;
-    if (a.k < 16 || a.k > 256 || a.k % 16 != 0) return false;
-    return a.d == 4 || a.d == 8 || a.d == 16 || a.d == 32;
+    if (a.k < 16 || a.k > 256) return false;
+    return a.d >= 1 && a.d <= 32;
 }
 
 void umma_screen(pqg_ctx* ctx, const NearestArgs& a) {
-    switch (a.d) {
-        case 4: launch_umma<4, 8>(ctx, a); break;
-        case 8: launch_umma<8, 16>(ctx, a); break;
-        case 16: launch_umma<16, 24>(ctx, a); break;
-        case 32: launch_umma<32, 40>(ctx, a); break;
-        default: fail(PQG_EUNSUPPORTED, "umma_screen: unsupported sub-dimension");
-    }
+    if (a.d <= 4) launch_umma<4, 8>(ctx, a);
+    else if (a.d <= 8) launch_umma<8, 16>(ctx, a);
+    else if (a.d <= 16) launch_umma<16, 24>(ctx, a);
+    else if (a.d <= 32) launch_umma<32, 40>(ctx, a);
+    else fail(PQG_EUNSUPPORTED, "umma_screen: unsupported sub-dimension");
 }
 
 }  // namespace pqg
