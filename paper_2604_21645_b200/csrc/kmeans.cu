@@ -385,6 +385,96 @@ __global__ void __launch_bounds__(kMeanThreads) mean_exact_kernel(
     }
 }
 
+
+// The same sums for small sub-dimensions (d <= 32, the PQ fits): one warp per
+// (problem, cluster), lanes = (member group, dim); eight clusters per CTA, so
+// batched fits with many small clusters do not pay one CTA launch each.
+constexpr int kMeanWarpStage = 512;  // members staged per step of the row-order fallback
+
+__global__ void __launch_bounds__(kMeanThreads) mean_exact_warp_kernel(
+    const float* x, uint64_t ldx, uint32_t col_stride, uint64_t n, uint32_t d, uint64_t k,
+    uint64_t nclusters, const uint64_t* offsets, const uint32_t* perm, float* table,
+    int* has_empty, const int* active) {
+    __shared__ float col_all[kMeanThreads / 32][kMeanWarpStage];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    float* col = col_all[wid];
+    const uint64_t bc = uint64_t(blockIdx.x) * (kMeanThreads / 32) + wid;
+    if (bc >= nclusters) return;
+    const uint64_t b = bc / k, c = bc - b * k;
+    if (active && !active[b]) return;
+    const uint64_t* off = offsets + b * (k + 1);
+    const uint64_t beg = off[c], end = off[c + 1];
+    if (beg == end) {
+        if (lane == 0) has_empty[b] = 1;
+        return;
+    }
+    const uint64_t cnt = end - beg;
+    const uint32_t* pb = perm + b * n;
+    const float* xb = x + b * col_stride;
+    const uint32_t G = 32 / d;  // member groups
+    const uint32_t g = uint32_t(lane) / d, t = uint32_t(lane) - g * d;
+    double s = 0.0;
+    int emax = -1, emin = 1 << 30;
+    if (g < G) {
+        auto acc = [&](float v) {
+            s = __dadd_rn(s, (double)v);
+            const int e = int((__float_as_uint(v) >> 23) & 0xFFu);
+            if (v != 0.f) {
+                emax = max(emax, e);
+                emin = min(emin, max(e, 1));
+            }
+        };
+        uint64_t m = beg + g;
+        for (; m + 3 * uint64_t(G) < end; m += 4 * uint64_t(G)) {
+            uint32_t r[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) r[u] = __ldg(pb + m + u * G);
+            float v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = __ldg(xb + uint64_t(r[u]) * ldx + t);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc(v[u]);
+        }
+        for (; m < end; m += G) acc(__ldg(xb + uint64_t(__ldg(pb + m)) * ldx + t));
+    }
+    // combine the member groups of each dim (lanes t, t+d, t+2d, ...): exact
+    // sums, so the combination order does not matter
+    for (uint32_t h = 1; h < G; ++h) {
+        const uint32_t src = h * d + t;
+        const double os = __shfl_sync(0xffffffffu, s, src < 32 ? src : 0);
+        const int oxa = __shfl_sync(0xffffffffu, emax, src < 32 ? src : 0);
+        const int oxi = __shfl_sync(0xffffffffu, emin, src < 32 ? src : 0);
+        if (g == 0) {
+            s = __dadd_rn(s, os);
+            emax = max(emax, oxa);
+            emin = min(emin, oxi);
+        }
+    }
+    int lg = 0;
+    while ((uint64_t(1) << lg) < cnt) ++lg;
+    const double inv = __ddiv_rn(1.0, (double)cnt);
+    const bool mine = g == 0;
+    const bool exact = emax < 0 || (emax < 255 && emax - emin + lg <= 28);
+    if (mine && exact) table[bc * d + t] = __double2float_rn(__dmul_rn(s, inv));  // kmeans.cpp:112-118
+    uint32_t todo = __ballot_sync(0xffffffffu, mine && !exact);
+    while (todo) {  // row-order sums (kmeans.cpp:103-111) of the rejected dims
+        const int src = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const uint32_t tf = uint32_t(src);  // lane src has g == 0, so t == src
+        double sf = 0.0;
+        for (uint64_t m0 = beg; m0 < end; m0 += kMeanWarpStage) {
+            const uint64_t m1 = m0 + kMeanWarpStage < end ? m0 + kMeanWarpStage : end;
+            for (uint64_t m = m0 + lane; m < m1; m += 32)
+                col[m - m0] = __ldg(xb + uint64_t(__ldg(pb + m)) * ldx + tf);
+            __syncwarp();
+            if (lane == 0)
+                for (uint64_t m = m0; m < m1; ++m) sf = __dadd_rn(sf, (double)col[m - m0]);
+            __syncwarp();
+        }
+        if (lane == 0) table[bc * d + tf] = __double2float_rn(__dmul_rn(sf, inv));
+    }
+}
+
 // Empty-cluster repair, proj/src/kmeans.cpp:122-130: for each empty cluster in
 // ascending order take the row with the largest pre-update distance (first
 // such row on ties), copy it, zero its distance.
@@ -524,9 +614,18 @@ void kmeans_update(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint
     int* has_empty = scratch<int>(ctx, B);
     PQG_CUDA(cudaMemsetAsync(has_empty, 0, sizeof(int) * B, ctx->stream));
     if (uint64_t(B) * k > 0x7FFFFFFFull) fail(PQG_EUNSUPPORTED, "kmeans: too many clusters");
-    launch(ctx, "kmeans_sum", mean_exact_kernel, dim3(unsigned(uint64_t(B) * k)), dim3(kMeanThreads), 0,
-           src.x, src.ldx, src.col_stride, n, d, k, (const uint64_t*)bk.offsets,
-           (const uint32_t*)bk.perm, table, has_empty, active);
+    const uint64_t ncl = uint64_t(B) * k;
+    // small clusters (batched chunk fits): a warp each; large ones: a CTA each
+    if (d <= 32 && n <= 128 * k) {
+        const uint64_t blocks = (ncl + kMeanThreads / 32 - 1) / (kMeanThreads / 32);
+        launch(ctx, "kmeans_sum", mean_exact_warp_kernel, dim3(unsigned(blocks)), dim3(kMeanThreads), 0,
+               src.x, src.ldx, src.col_stride, n, d, k, ncl, (const uint64_t*)bk.offsets,
+               (const uint32_t*)bk.perm, table, has_empty, active);
+    } else {
+        launch(ctx, "kmeans_sum", mean_exact_kernel, dim3(unsigned(ncl)), dim3(kMeanThreads), 0,
+               src.x, src.ldx, src.col_stride, n, d, k, (const uint64_t*)bk.offsets,
+               (const uint32_t*)bk.perm, table, has_empty, active);
+    }
     launch(ctx, "reseed", reseed_kernel, dim3(B), dim3(1024), 0, src.x, src.ldx, src.col_stride, n,
            d, k, (const uint64_t*)bk.offsets, dist, table, (const int*)has_empty, active, nb);
 }

@@ -146,7 +146,7 @@ __device__ __forceinline__ float tc_error_bound(float S, int K) {
     return 2.f * (2.f * n_mma + 8.f) * kU * S + 1e-30f;
 }
 
-template <int DS, int KA>
+template <int DS, int KA, bool PAD>
 __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, uint32_t n_pad,
                                                                uint32_t tmem_cols, uint32_t m32) {
     static_assert(KA % 8 == 0 && KA >= DS + 2, "augmented K");
@@ -165,7 +165,8 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
     const uint32_t cta = blockIdx.x / B, ncta = gridDim.x / B;
     if (a.active && !a.active[b]) return;
     const uint64_t k = a.k;
-    const uint32_t d = a.d;  // actual sub-dimension, zero-padded to DS in the operands
+    // actual sub-dimension (compile-time DS unless zero-padded up to DS)
+    const uint32_t d = PAD ? a.d : uint32_t(DS);
     const float* tab = a.table + uint64_t(b) * k * d;
     const float cmax = a.cmax[b];
 
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
                 }
             } else {
 #pragma unroll
-                for (int t = 0; t < DS; ++t) xx[t] = uint32_t(t) < a.d ? __ldg(xp + t) : 0.f;
+                for (int t = 0; t < DS; ++t) xx[t] = (!PAD || uint32_t(t) < a.d) ? __ldg(xp + t) : 0.f;
             }
         } else {
 #pragma unroll
@@ -373,7 +374,7 @@ struct RowRegs {
     float x[DS];
 };
 
-template <int DS>
+template <int DS, bool PAD>
 __device__ __forceinline__ void load_row(const NearestArgs& a, uint64_t row, uint32_t b, bool vec4,
                                          RowRegs<DS>& r) {
     if (row < a.n) {
@@ -386,7 +387,7 @@ __device__ __forceinline__ void load_row(const NearestArgs& a, uint64_t row, uin
             }
         } else {
 #pragma unroll
-            for (int t = 0; t < DS; ++t) r.x[t] = uint32_t(t) < a.d ? __ldg(xp + t) : 0.f;
+            for (int t = 0; t < DS; ++t) r.x[t] = (!PAD || uint32_t(t) < a.d) ? __ldg(xp + t) : 0.f;
         }
     } else {
 #pragma unroll
@@ -394,7 +395,7 @@ __device__ __forceinline__ void load_row(const NearestArgs& a, uint64_t row, uin
     }
 }
 
-template <int DS, int KA, int NW>
+template <int DS, int KA, int NW, bool PAD>
 __global__ void __launch_bounds__(NW * 32, 1) umma_screen2_kernel(NearestArgs a, uint32_t n_pad,
                                                                   uint32_t m32) {
     constexpr int NPART = NW / 4;  // column parts (warp quads) per tile
@@ -416,7 +417,8 @@ __global__ void __launch_bounds__(NW * 32, 1) umma_screen2_kernel(NearestArgs a,
     const uint32_t cta = blockIdx.x / B, ncta = gridDim.x / B;
     if (a.active && !a.active[b]) return;
     const uint64_t k = a.k;
-    const uint32_t d = a.d;  // actual sub-dimension, zero-padded to DS in the operands
+    // actual sub-dimension (compile-time DS unless zero-padded up to DS)
+    const uint32_t d = PAD ? a.d : uint32_t(DS);
     const float* tab = a.table + uint64_t(b) * k * d;
     const float cmax = a.cmax[b];
     const uint32_t row_l = tid & (kRows - 1);  // row of the tile this thread stages / reads
@@ -506,9 +508,9 @@ __global__ void __launch_bounds__(NW * 32, 1) umma_screen2_kernel(NearestArgs a,
 
     RowRegs<DS> xr;
     if (my_tiles > 0) {
-        load_row<DS>(a, tile_of(0) * kRows + row_l, b, vec4, xr);
+        load_row<DS, PAD>(a, tile_of(0) * kRows + row_l, b, vec4, xr);
         stage(0, xr);
-        if (my_tiles > 1) load_row<DS>(a, tile_of(1) * kRows + row_l, b, vec4, xr);
+        if (my_tiles > 1) load_row<DS, PAD>(a, tile_of(1) * kRows + row_l, b, vec4, xr);
         fence_async_smem();
         fence_before();
         __syncthreads();
@@ -522,7 +524,7 @@ __global__ void __launch_bounds__(NW * 32, 1) umma_screen2_kernel(NearestArgs a,
         // stage tile it+1 (rows already in registers), prefetch tile it+2
         if (it + 1 < my_tiles) {
             stage(it + 1, xr);
-            if (it + 2 < my_tiles) load_row<DS>(a, tile_of(it + 2) * kRows + row_l, b, vec4, xr);
+            if (it + 2 < my_tiles) load_row<DS, PAD>(a, tile_of(it + 2) * kRows + row_l, b, vec4, xr);
         }
         fence_async_smem();
         fence_before();
@@ -627,7 +629,7 @@ __global__ void __launch_bounds__(NW * 32, 1) umma_screen2_kernel(NearestArgs a,
     }
 }
 
-template <int DS, int KA>
+template <int DS, int KA, bool PAD>
 void launch_umma2(pqg_ctx* ctx, const NearestArgs& a) {
     const uint32_t n_pad = uint32_t((a.k + 15) / 16 * 16);
     const size_t smem = size_t(2) * n_pad * KA * 4 + size_t(4) * kRows * KA * 4;
@@ -640,11 +642,11 @@ void launch_umma2(pqg_ctx* ctx, const NearestArgs& a) {
         PQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         launch(ctx, "nearest_tc", kern, dim3(unsigned(per_b * a.B)), dim3(nthreads), smem, a, n_pad, 32u);
     };
-    if (nw_env == 8) go(umma_screen2_kernel<DS, KA, 8>, 256);
-    else go(umma_screen2_kernel<DS, KA, 16>, 512);
+    if (nw_env == 8) go(umma_screen2_kernel<DS, KA, 8, PAD>, 256);
+    else go(umma_screen2_kernel<DS, KA, 16, PAD>, 512);
 }
 
-template <int DS, int KA>
+template <int DS, int KA, bool PAD>
 void launch_umma(pqg_ctx* ctx, const NearestArgs& a) {
     // measured (tools/screen_bench.py, r1): the synchronous 2-CTA/SM kernel wins
     // for narrow tables and Ds=16/Ks=256; the pipelined 8-warp kernel otherwise
@@ -654,14 +656,14 @@ void launch_umma(pqg_ctx* ctx, const NearestArgs& a) {
     if (env && env[0] == '1') v1 = true;
     if (env && env[0] == '2') v1 = false;
     if (!v1) {
-        launch_umma2<DS, KA>(ctx, a);
+        launch_umma2<DS, KA, PAD>(ctx, a);
         return;
     }
     const uint32_t n_pad = uint32_t((a.k + 15) / 16 * 16);
     uint32_t cols = 32;
     while (cols < n_pad) cols <<= 1;
     const size_t smem = size_t(2) * n_pad * KA * 4 + size_t(2) * kRows * KA * 4;
-    auto kern = umma_screen_kernel<DS, KA>;
+    auto kern = umma_screen_kernel<DS, KA, PAD>;
     PQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     const uint64_t ntiles = (a.n + kRows - 1) / kRows;
     // persistent: ~2 CTAs per SM in total, each problem gets its share
@@ -682,10 +684,17 @@ bool umma_screen_supported(const NearestArgs& a) {
 }
 
 void umma_screen(pqg_ctx* ctx, const NearestArgs& a) {
-    if (a.d <= 4) launch_umma<4, 8>(ctx, a);
-    else if (a.d <= 8) launch_umma<8, 16>(ctx, a);
-    else if (a.d <= 16) launch_umma<16, 24>(ctx, a);
-    else if (a.d <= 32) launch_umma<32, 40>(ctx, a);
+    switch (a.d) {  // exact widths compile the sub-dimension in; others are zero-padded
+        case 4: launch_umma<4, 8, false>(ctx, a); return;
+        case 8: launch_umma<8, 16, false>(ctx, a); return;
+        case 16: launch_umma<16, 24, false>(ctx, a); return;
+        case 32: launch_umma<32, 40, false>(ctx, a); return;
+        default: break;
+    }
+    if (a.d < 4) launch_umma<4, 8, true>(ctx, a);
+    else if (a.d < 8) launch_umma<8, 16, true>(ctx, a);
+    else if (a.d < 16) launch_umma<16, 24, true>(ctx, a);
+    else if (a.d < 32) launch_umma<32, 40, true>(ctx, a);
     else fail(PQG_EUNSUPPORTED, "umma_screen: unsupported sub-dimension");
 }
 
