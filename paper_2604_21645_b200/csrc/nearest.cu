@@ -304,8 +304,9 @@ __global__ void __launch_bounds__(NT, 2) nearest_kernel(NearestArgs a) {
     const uint32_t v1hi = uint32_t(K >> 32);
     const uint32_t idx = uint32_t(K);
     const float E = rowE[tid];
-    const bool unique = (V2 >= 0x7f800000u) ||
-                        (__uint_as_float(V2) - __uint_as_float(v1hi | 7u) > 2.05f * E);
+    // non-finite E (inf/NaN in the row or table) or best: the exact fixup decides
+            const bool unique = isfinite(E) && v1hi < 0x7f800000u && ((V2 >= 0x7f800000u) ||
+                        (__uint_as_float(V2) - __uint_as_float(v1hi | 7u) > 2.05f * E));
     if (unique) {
         store_index(a, row, b, idx);
         if (a.out_dist) a.out_dist[(uint64_t)b * a.n + row] = exact_dist(a, row, b, tab + (uint64_t)idx * d);
@@ -398,9 +399,13 @@ __global__ void __launch_bounds__(kFixThreads) fixup_kernel(NearestArgs a) {
                     best = red_d[w];
                     bj = red_j[w];
                 }
-            if (bj == 0xFFFFFFFFu) {  // every distance NaN: the reference keeps index 0
+            // nearest_in_table starts from (0, d_0) and only a strictly smaller
+            // distance replaces it (kmeans.cpp:20-31): a NaN d_0 is never replaced
+            // and NaN distances never win
+            const double d0 = exact_dist(a, row, b, tab);
+            if (bj == 0xFFFFFFFFu || d0 != d0) {
                 bj = 0;
-                best = exact_dist(a, row, b, tab);
+                best = d0;
             }
             store_index(a, row, b, bj);
             if (a.out_dist) a.out_dist[(uint64_t)b * a.n + row] = best;

@@ -331,8 +331,9 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
         if (valid) {
             const uint32_t idx = uint32_t(K1);
             const uint32_t v1 = uint32_t(K1 >> 32);
-            const bool unique = (V2 >= 0x7f800000u) ||
-                                (__uint_as_float(V2) - __uint_as_float(v1 | 31u) > 2.05f * E);
+            // non-finite E (inf/NaN in the row or table) or best: the exact fixup decides
+            const bool unique = isfinite(E) && v1 < 0x7f800000u && ((V2 >= 0x7f800000u) ||
+                                (__uint_as_float(V2) - __uint_as_float(v1 | 31u) > 2.05f * E));
             if (unique && idx < k) {
                 store_index(a, row, b, idx);
                 if (a.out_dist) {
@@ -598,8 +599,9 @@ __global__ void __launch_bounds__(NW * 32, 1) umma_screen2_kernel(NearestArgs a,
                 const uint32_t idx = uint32_t(K1);
                 const uint32_t v1 = uint32_t(K1 >> 32);
                 const float E = ebuf[it & 1][row_l];
-                const bool unique = (V2 >= 0x7f800000u) ||
-                                    (__uint_as_float(V2) - __uint_as_float(v1 | 31u) > 2.05f * E);
+                // non-finite E (inf/NaN in the row or table) or best: the exact fixup decides
+            const bool unique = isfinite(E) && v1 < 0x7f800000u && ((V2 >= 0x7f800000u) ||
+                                    (__uint_as_float(V2) - __uint_as_float(v1 | 31u) > 2.05f * E));
                 if (unique && idx < k) {
                     store_index(a, row, b, idx);
                     if (a.out_dist) {

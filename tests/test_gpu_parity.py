@@ -55,6 +55,30 @@ def test_nearest_ties_lowest_index(pq, orc):
     assert np.array_equal(bits(gd), bits(od))
 
 
+@pytest.mark.parametrize("d,k", [(8, 64), (16, 256), (5, 40), (128, 1024)])
+def test_nearest_nonfinite(pq, orc, d, k):
+    """nearest_in_table's NaN rule (kmeans.cpp:20-31): the search starts from
+    (0, d_0) and only a strictly smaller distance replaces it, so a NaN d_0
+    is kept and NaN distances never win."""
+    table = orc.random_matrix(k, d, 11).copy()
+    pts = orc.random_matrix(600, d, 12).copy()
+    table[0, 1] = np.nan          # d_0 is NaN for every point
+    table[3, 0] = np.inf          # inf / NaN distances elsewhere
+    table[5, :] = np.nan
+    pts[7, 2] = np.nan            # every distance NaN for this point
+    pts[9, 0] = np.inf
+    gi, gd = pq.nearest_batch(pts, table)
+    oi, od = orc.nearest_batch(pts, table)
+    assert np.array_equal(gi, oi)
+    assert np.array_equal(bits(gd), bits(od))
+    t2 = table.copy()
+    t2[0] = orc.random_matrix(1, d, 13)[0]   # finite d_0, NaN rows elsewhere
+    gi, gd = pq.nearest_batch(pts, t2)
+    oi, od = orc.nearest_batch(pts, t2)
+    assert np.array_equal(gi, oi)
+    assert np.array_equal(bits(gd), bits(od))
+
+
 def test_nearest_exact_match_and_errors(pq, orc):
     table = orc.random_matrix(16, 8, 31)
     idx, dist = pq.nearest_centroid(table[3], table)
