@@ -366,20 +366,25 @@ __global__ void __launch_bounds__(kMeanThreads) mean_exact_kernel(
         }
         __syncthreads();
         // row-order sums (kmeans.cpp:103-111) for the dims the exactness test
-        // rejects: the block stages the column, one thread adds it in order
-        for (uint32_t fi = 0; fi < nfail; ++fi) {
-            const uint32_t tf = failed[fi];
+        // rejects: the block stages a chunk of members x failing dims, then one
+        // thread per failing dim adds its column in row order (dims in parallel)
+        const uint32_t nf = nfail;
+        if (nf > 0) {
+            const uint64_t mchunk = kMeanStage / nf;
             double sf = 0.0;
-            for (uint64_t m0 = beg; m0 < end; m0 += kMeanStage) {
-                const uint64_t m1 = m0 + kMeanStage < end ? m0 + kMeanStage : end;
-                for (uint64_t m = m0 + threadIdx.x; m < m1; m += blockDim.x)
-                    col[m - m0] = __ldg(xb + uint64_t(__ldg(pb + m)) * ldx + tf);
+            for (uint64_t m0 = beg; m0 < end; m0 += mchunk) {
+                const uint64_t m1 = m0 + mchunk < end ? m0 + mchunk : end;
+                const uint32_t nm = uint32_t(m1 - m0);
+                for (uint32_t e = threadIdx.x; e < nm * nf; e += blockDim.x) {
+                    const uint32_t mi = e / nf, f = e - mi * nf;
+                    col[e] = __ldg(xb + uint64_t(__ldg(pb + m0 + mi)) * ldx + failed[f]);
+                }
                 __syncthreads();
-                if (threadIdx.x == 0)
-                    for (uint64_t m = m0; m < m1; ++m) sf = __dadd_rn(sf, (double)col[m - m0]);
+                if (threadIdx.x < nf)
+                    for (uint32_t mi = 0; mi < nm; ++mi) sf = __dadd_rn(sf, (double)col[mi * nf + threadIdx.x]);
                 __syncthreads();
             }
-            if (threadIdx.x == 0) table[bc * d + tf] = __double2float_rn(__dmul_rn(sf, inv));
+            if (threadIdx.x < nf) table[bc * d + failed[threadIdx.x]] = __double2float_rn(__dmul_rn(sf, inv));
         }
         __syncthreads();
     }
