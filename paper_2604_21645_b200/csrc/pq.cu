@@ -82,27 +82,49 @@ __global__ void sse_kernel(const float* a, const float* b, uint64_t count, uint6
     if (threadIdx.x == 0) parts[blockIdx.x] = s;
 }
 
-// x vs decode(codes) without materialising the decode; rows are read as
-// coalesced runs (consecutive threads -> consecutive elements).
+// Squared error of one (row, subspace) pair: ds elements of x against the
+// codeword, accumulated in fp64 (vector loads when both are 16-byte aligned).
+__device__ __forceinline__ double pair_sse(const float* xp, const float* cw, uint32_t ds, bool vec,
+                                           double s) {
+    if (vec) {
+        for (uint32_t t = 0; t < ds; t += 4) {
+            const float4 a = __ldg(reinterpret_cast<const float4*>(xp + t));
+            const float4 c = __ldg(reinterpret_cast<const float4*>(cw + t));
+            const double d0 = __dsub_rn((double)a.x, (double)c.x), d1 = __dsub_rn((double)a.y, (double)c.y);
+            const double d2 = __dsub_rn((double)a.z, (double)c.z), d3 = __dsub_rn((double)a.w, (double)c.w);
+            s = __dadd_rn(s, __dmul_rn(d0, d0));
+            s = __dadd_rn(s, __dmul_rn(d1, d1));
+            s = __dadd_rn(s, __dmul_rn(d2, d2));
+            s = __dadd_rn(s, __dmul_rn(d3, d3));
+        }
+    } else {
+        for (uint32_t t = 0; t < ds; ++t) {
+            const double diff = __dsub_rn((double)__ldg(xp + t), (double)__ldg(cw + t));
+            s = __dadd_rn(s, __dmul_rn(diff, diff));
+        }
+    }
+    return s;
+}
+
+// x vs decode(codes) without materialising the decode: one (row, subspace)
+// pair per thread step, one code load per pair; block b sums the pairs
+// [b*chunk, (b+1)*chunk) in a fixed order (deterministic).
 __global__ void recon_sse_kernel(const float* x, const uint8_t* codes, uint64_t n, uint32_t M,
                                  uint32_t ks, uint32_t ds, const float* tables, uint64_t chunk,
-                                 double* parts, int* err) {
+                                 double* parts, int* err, bool vec) {
     const uint32_t w = ks <= 256 ? 1 : 2;
-    const uint64_t D = uint64_t(M) * ds, total = n * D;
+    const uint64_t D = uint64_t(M) * ds, total = n * M;
     const uint64_t c0 = uint64_t(blockIdx.x) * chunk, c1 = min64(total, c0 + chunk);
     double s = 0.0;
-    for (uint64_t e = c0 + threadIdx.x; e < c1; e += kThreads) {
-        uint64_t i, col;
-        split_elem(e, D, i, col);
-        const uint32_t m = uint32_t(col) / ds, t = uint32_t(col) - m * ds;
-        uint32_t code = code_at(codes, i, m, M, w);
+    for (uint64_t p = c0 + threadIdx.x; p < c1; p += kThreads) {
+        uint64_t i, m;
+        split_elem(p, M, i, m);
+        uint32_t code = code_at(codes, i, uint32_t(m), M, w);
         if (code >= ks) {
             atomicExch(err, 1);
             code = 0;
         }
-        const double diff =
-            __dsub_rn((double)__ldg(x + e), (double)__ldg(tables + (uint64_t(m) * ks + code) * ds + t));
-        s = __dadd_rn(s, __dmul_rn(diff, diff));
+        s = pair_sse(x + i * D + m * ds, tables + (m * ks + code) * ds, ds, vec, s);
     }
     s = block_sum256(s);
     if (threadIdx.x == 0) parts[blockIdx.x] = s;
@@ -192,30 +214,27 @@ __global__ void representatives_kernel(const float* tables, uint64_t C, uint32_t
 
 // Per-chunk reconstruction SSE of the chunk against its own local codebook,
 // codes taken from the fit's final assignments (the last pass has no update
-// after it, kmeans.cpp:93-101, so they are the chunk's encode).  Same
-// element order and reduction shape as recon_sse_kernel on that chunk alone.
+// after it, kmeans.cpp:93-101, so they are the chunk's encode).  Same pair
+// order and reduction shape as recon_sse_kernel on that chunk alone.
 __global__ void chunk_sse_kernel(const float* x, uint32_t M, uint32_t ks, uint32_t ds,
                                  uint64_t base, uint64_t extra, const uint32_t* assign,
-                                 uint64_t n_max, const float* tables, double* parts) {
+                                 uint64_t n_max, const float* tables, double* parts, bool vec) {
     const uint64_t c = blockIdx.y;
     const uint64_t D = uint64_t(M) * ds;
     uint64_t r0, nc;
     chunk_range(c, base, extra, r0, nc);
-    const uint64_t total = nc * D, np = nparts_for(total);
+    const uint64_t total = nc * M, np = nparts_for(nc * D);
     if (blockIdx.x >= np) return;
     const uint64_t chunk = (total + np - 1) / np;
     const uint64_t c0 = uint64_t(blockIdx.x) * chunk, c1 = min64(total, c0 + chunk);
     const float* xc = x + r0 * D;
     double s = 0.0;
-    for (uint64_t e = c0 + threadIdx.x; e < c1; e += kThreads) {
-        uint64_t i, col;
-        split_elem(e, D, i, col);
-        const uint32_t m = uint32_t(col) / ds, t = uint32_t(col) - m * ds;
+    for (uint64_t p = c0 + threadIdx.x; p < c1; p += kThreads) {
+        uint64_t i, m;
+        split_elem(p, M, i, m);
         const uint64_t b = c * M + m;
         const uint32_t code = __ldg(assign + b * n_max + i);
-        const double diff =
-            __dsub_rn((double)__ldg(xc + e), (double)__ldg(tables + (b * ks + code) * ds + t));
-        s = __dadd_rn(s, __dmul_rn(diff, diff));
+        s = pair_sse(xc + i * D + m * ds, tables + (b * ks + code) * ds, ds, vec, s);
     }
     s = block_sum256(s);
     if (threadIdx.x == 0) parts[c * gridDim.x + blockIdx.x] = s;
@@ -253,8 +272,9 @@ void chunk_sse(pqg_ctx* ctx, const float* x, uint64_t C, uint32_t M, uint32_t ks
                const float* tables, double* sse) {
     const uint64_t np_max = nparts_for(n_max * M * ds);
     double* parts = scratch<double>(ctx, C * np_max);
+    const bool vec = ds % 4 == 0 && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(tables)) & 15u) == 0;
     launch(ctx, "recon_sse", chunk_sse_kernel, dim3(unsigned(np_max), unsigned(C)), dim3(kThreads), 0,
-           x, M, ks, ds, base, extra, assign, n_max, tables, parts);
+           x, M, ks, ds, base, extra, assign, n_max, tables, parts, vec);
     launch(ctx, "reduce", chunk_sse_final_kernel, dim3(unsigned(C)), dim3(kThreads), 0,
            (const double*)parts, np_max, M, ds, base, extra, sse);
 }
@@ -279,12 +299,12 @@ void sq_error_dev(pqg_ctx* ctx, const float* a, const float* b, uint64_t count, 
 
 void recon_sse_dev(pqg_ctx* ctx, const float* x, const uint8_t* codes, uint64_t n, uint32_t M,
                    uint32_t ks, uint32_t ds, const float* tables, double* sse, int* err) {
-    const uint64_t total = n * M * ds;
-    const uint64_t np = nparts_for(total);
-    const uint64_t chunk = (total + np - 1) / np;
+    const uint64_t np = nparts_for(n * M * ds);
+    const uint64_t chunk = (n * M + np - 1) / np;  // (row, subspace) pairs per part
     double* parts = scratch<double>(ctx, np);
+    const bool vec = ds % 4 == 0 && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(tables)) & 15u) == 0;
     launch(ctx, "recon_sse", recon_sse_kernel, dim3(unsigned(np)), dim3(kThreads), 0, x, codes, n, M,
-           ks, ds, tables, chunk, parts, err);
+           ks, ds, tables, chunk, parts, err, vec);
     reduce_sum_f64(ctx, parts, np, sse);
 }
 
