@@ -668,8 +668,13 @@ void launch_umma(pqg_ctx* ctx, const NearestArgs& a) {
     auto kern = umma_screen_kernel<DS, KA, PAD>;
     PQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     const uint64_t ntiles = (a.n + kRows - 1) / kRows;
-    // persistent: ~2 CTAs per SM in total, each problem gets its share
-    uint64_t per_b = std::max<uint64_t>(1, (uint64_t(ctx->num_sms) * 2 + a.B - 1) / a.B);
+    // persistent: CTAs per SM limited by TMEM columns (2 at Ks=256), shared
+    // memory and a cap of 4 (measured: narrow tables gain up to ~1.5x from the
+    // extra CTAs, whose short tiles are latency-bound); PQG_UMMA_CTAS overrides
+    const uint64_t smem_lim = (227u * 1024u) / (smem + 3u * 1024u);
+    uint64_t per_sm = std::max<uint64_t>(1, std::min<uint64_t>(std::min<uint64_t>(4u, 512u / cols), smem_lim));
+    if (const char* ce = std::getenv("PQG_UMMA_CTAS")) per_sm = std::max(1, std::atoi(ce));
+    uint64_t per_b = std::max<uint64_t>(1, (uint64_t(ctx->num_sms) * per_sm + a.B - 1) / a.B);
     per_b = std::min<uint64_t>(per_b, ntiles);
     launch(ctx, "nearest_tc", kern, dim3(unsigned(per_b * a.B)), dim3(kRows), smem, a, n_pad, cols, 32u);
 }
