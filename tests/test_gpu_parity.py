@@ -196,7 +196,9 @@ def test_pq_wide_codes(pq, golden):
 
 
 @pytest.mark.parametrize("M,ks,ds", [(4, 16, 2), (8, 256, 16), (16, 256, 8), (32, 16, 4),
-                                     (4, 64, 32), (3, 7, 5), (2, 1, 3), (12, 256, 8)])
+                                     (4, 64, 32), (3, 7, 5), (2, 1, 3), (12, 256, 8),
+                                     (64, 256, 2), (128, 16, 1), (8, 100, 6), (6, 200, 12),
+                                     (5, 256, 24)])
 def test_pq_encode_vs_oracle(pq, orc, mix, M, ks, ds):
     x = mix(4000, M * ds, 32, seed=M * 100 + ks)
     tables = orc.random_matrix(M * ks, ds, 7 + ks).reshape(M, ks, ds) * 3.0
@@ -209,9 +211,11 @@ def test_pq_encode_vs_oracle(pq, orc, mix, M, ks, ds):
     assert abs(r - ro) <= 1e-12 * max(ro, 1e-30)
 
 
-@pytest.mark.parametrize("M,ks,n,iters", [(8, 256, 20000, 20), (16, 64, 8000, 25), (4, 16, 6000, 25)])
-def test_pq_fit_vs_oracle(pq, orc, mix, M, ks, n, iters):
-    x = mix(n, 64, 64, seed=11 + M)
+@pytest.mark.parametrize("M,ks,n,iters,D", [(8, 256, 20000, 20, 64), (16, 64, 8000, 25, 64),
+                                            (4, 16, 6000, 25, 64), (8, 256, 12000, 15, 48),
+                                            (32, 32, 5000, 12, 64), (6, 100, 7000, 12, 60)])
+def test_pq_fit_vs_oracle(pq, orc, mix, M, ks, n, iters, D):
+    x = mix(n, D, 64, seed=11 + M)
     stats = {}
     cb = pq.pq_fit(x, M, ks, iters, 9, stats=stats)
     t, it, _ = orc.pq_fit(x, M, ks, iters, 9)
