@@ -427,6 +427,13 @@ def run_ours(args, rank, world, local):
         "config": config_block(world),
         "rmse": head_rmse,
         "kmeans_iters_per_s": kmeans_ips,
+        # one iteration = one assignment pass over the sample (2*N*Ks*D flop, the
+        # SURVEY 8(d) K1 count) plus the mean update; FP32 peak as for the encode
+        "kmeans_roofline": {"bound": "fp32",
+                            "achieved": 2.0 * SAMPLE * HEAD_KS * DIMS * kmeans_ips / 1e12,
+                            "peak": fp32_peak, "unit": "TFLOP/s",
+                            "frac": 2.0 * SAMPLE * HEAD_KS * DIMS * kmeans_ips / 1e12 / fp32_peak,
+                            "algorithmic": "2*N*Ks*D flop per iteration, N = sample rows"},
         "kmeans_fit": {"M": HEAD_M, "Ks": HEAD_KS, "sample_rows": SAMPLE, "iters_run": iters_run,
                        "seconds": fit_s},
         "sharded_pq_fit": sharded_fit,
