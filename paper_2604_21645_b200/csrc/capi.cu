@@ -290,6 +290,19 @@ static KMeansOut run_kmeans(pqg_ctx* ctx, const float* x, uint64_t n, uint64_t l
                                  ctx->stream));
         d_nb = p;
     }
+    // Batched fits over rows larger than L2: copy the B column blocks into a
+    // problem-major layout once per fit, so each problem's rows are one dense
+    // region -- the assignment passes and the member gathers of the update
+    // then stay within L2 instead of re-fetching whole rows from HBM for
+    // every problem.
+    if (B > 1 && uint64_t(B) * n * d * sizeof(float) >= (uint64_t(64) << 20)) {
+        if (uint64_t(n) * d > 0xFFFFFFFFull) fail(PQG_EUNSUPPORTED, "kmeans: problem block too large");
+        float* xt = scratch<float>(ctx, uint64_t(B) * n * d);
+        transpose_blocks(ctx, x, n, ldx, B, d, col_stride, xt);
+        x = xt;
+        ldx = d;
+        col_stride = uint32_t(n * d);
+    }
     uint64_t* d_rows = scratch<uint64_t>(ctx, rows.size());
     PQG_CUDA(cudaMemcpyAsync(d_rows, rows.data(), rows.size() * sizeof(uint64_t),
                              cudaMemcpyHostToDevice, ctx->stream));

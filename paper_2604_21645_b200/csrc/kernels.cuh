@@ -73,6 +73,8 @@ struct Bucketing {
 void stable_bucket(pqg_ctx* ctx, const uint32_t* keys, uint64_t n, uint32_t B, uint64_t k,
                    const int* active, Bucketing out, const uint64_t* nb = nullptr);
 void exclusive_scan_u32(pqg_ctx* ctx, const uint32_t* in, uint64_t* out, uint64_t count);
+void transpose_blocks(pqg_ctx* ctx, const float* x, uint64_t n, uint64_t ldx, uint32_t B, uint32_t d,
+                      uint32_t col_stride, float* out);
 void gather_rows(pqg_ctx* ctx, const float* x, uint64_t ldx, uint32_t B, uint32_t d,
                  uint32_t col_stride, const uint64_t* rows, uint64_t k, float* table);
 struct KMeansState {

@@ -583,6 +583,26 @@ void stable_bucket(pqg_ctx* ctx, const uint32_t* keys, uint64_t n, uint32_t B, u
            keys, n, k, ntiles, (const uint64_t*)tile_base, out.perm, wpb);
 }
 
+namespace {
+// out[b][i][t] = x[i*ldx + b*col_stride + t]: reads each row once, coalesced
+__global__ void transpose_blocks_kernel(const float* x, uint64_t n, uint64_t ldx, uint32_t B,
+                                        uint32_t d, uint32_t col_stride, float* out) {
+    const uint64_t per_row = uint64_t(B) * d, total = n * per_row;
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i = e / per_row, r = e - i * per_row;
+        const uint64_t b = r / d, t = r - b * d;
+        out[(b * n + i) * d + t] = __ldg(x + i * ldx + b * col_stride + t);
+    }
+}
+}  // namespace
+
+void transpose_blocks(pqg_ctx* ctx, const float* x, uint64_t n, uint64_t ldx, uint32_t B, uint32_t d,
+                      uint32_t col_stride, float* out) {
+    launch(ctx, "gather", transpose_blocks_kernel, dim3(grid1d(n * B * d, 256, ctx->num_sms * 32)),
+           dim3(256), 0, x, n, ldx, B, d, col_stride, out);
+}
+
 void gather_rows(pqg_ctx* ctx, const float* x, uint64_t ldx, uint32_t B, uint32_t d,
                  uint32_t col_stride, const uint64_t* rows, uint64_t k, float* table) {
     launch(ctx, "gather", gather_kernel, dim3(grid1d(uint64_t(B) * k * d, 256, 8192)), dim3(256), 0,

@@ -223,6 +223,17 @@ def test_pq_fit_vs_oracle(pq, orc, mix, M, ks, n, iters, D):
     assert np.array_equal(bits(cb.tables), bits(t))
 
 
+def test_pq_fit_problem_major_copy(pq, orc, mix):
+    """Batched fits over more than 64 MB of rows run on a problem-major copy
+    of the column blocks (capi.cu run_kmeans); still bit-identical."""
+    x = mix(140_000, 128, 64, seed=5)  # 71.7 MB
+    stats = {}
+    cb = pq.pq_fit(x, 8, 16, 3, 4, stats=stats)
+    t, it, _ = orc.pq_fit(x, 8, 16, 3, 4)
+    assert np.array_equal(stats["iterations_run"], it)
+    assert np.array_equal(bits(cb.tables), bits(t))
+
+
 def test_pq_code_semantics(pq, orc):
     data = orc.random_matrix(40, 8, 23)
     cb = pq.pq_fit(data, 4, 1, 5, 2)  # ks=1 encodes everything to zero
