@@ -148,7 +148,8 @@ __device__ __forceinline__ float tc_error_bound(float S, int K) {
 
 template <int DS, int KA, bool PAD>
 __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, uint32_t n_pad,
-                                                               uint32_t tmem_cols, uint32_t m32) {
+                                                               uint32_t tmem_cols, uint32_t m32,
+                                                               uint32_t n_mma) {
     static_assert(KA % 8 == 0 && KA >= DS + 2, "augmented K");
     constexpr uint32_t SBO = (KA / 4) * 128;  // bytes between 8-row groups
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -201,7 +202,6 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
     __syncthreads();
     fence_after();
     const uint32_t tmem = tmem_base;
-    const uint32_t idesc = make_idesc_tf32(kRows, n_pad);
     const uint32_t a_hi = smem_u32(Ah), a_lo = smem_u32(Al);
     const uint32_t b_hi = smem_u32(Bh), b_lo = smem_u32(Bl);
     uint32_t phase = 0;
@@ -262,60 +262,72 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
         fence_async_smem();
         fence_before();
         __syncthreads();
-        // ---- MMA: D = Ah Bh^T + Ah Bl^T + Al Bh^T over KA/8 k-steps
-        if (tid == 0) {
-            fence_after();
-#pragma unroll
-            for (int s = 0; s < KA / 8; ++s) {
-                const uint32_t ko = s * 256;  // two 16-byte K chunks per k-step
-                const uint64_t dah = make_desc(a_hi + ko, 128, SBO);
-                const uint64_t dal = make_desc(a_lo + ko, 128, SBO);
-                const uint64_t dbh = make_desc(b_hi + ko, 128, SBO);
-                const uint64_t dbl = make_desc(b_lo + ko, 128, SBO);
-                mma_tf32(tmem, dah, dbh, idesc, s > 0);
-                mma_tf32(tmem, dah, dbl, idesc, 1);
-                mma_tf32(tmem, dal, dbh, idesc, 1);
-            }
-            mma_commit(&mbar);
-        }
-        load_row(tile + ncta, x_next);  // next tile's row, in flight during this epilogue
-        mbar_wait(&mbar, phase);
-        phase ^= 1;
-        fence_after();
-        // ---- epilogue: this thread's row, all n_pad columns
-        // keys carry the column within a 32-column chunk in 5 low bits (value
-        // quantum 32 ulp); the chunk of each running best is tracked on
-        // change.  Four independent (best, second) states per thread break the
-        // min/max dependency chain; they are merged at the end.
+        // the accumulator covers n_mma columns: codewords in passes of n_mma
+        // (n_mma < n_pad trades a second MMA round per tile for half the TMEM,
+        // i.e. more resident CTAs per SM); keys carry the column within a
+        // 32-column chunk in 5 low bits (value quantum 32 ulp); the chunk of
+        // each running best is tracked on change.  Four independent (best,
+        // second) states per thread break the min/max dependency chain; they
+        // are merged at the end.
         uint32_t m1[4], m2[4], ch[4];
 #pragma unroll
         for (int s4 = 0; s4 < 4; ++s4) { m1[s4] = 0xFFFFFFFFu; m2[s4] = 0xFFFFFFFFu; ch[s4] = 0; }
         const uint32_t lane_base = (warp * 32u) << 16;
-        for (uint32_t c0 = 0; c0 < n_pad; c0 += 32) {
-            uint32_t r[32];
-            tmem_ld32(tmem + lane_base + c0, r);
-            tmem_wait_ld();
-            if (n_pad - c0 < 32) {  // columns past N are not written by the MMA
-#pragma unroll
-                for (int j = 16; j < 32; ++j) r[j] = 0x7f800000u;
+        for (uint32_t p0 = 0; p0 < n_pad; p0 += n_mma) {
+            const uint32_t w = min(n_mma, n_pad - p0);
+            if (p0 > 0) {  // the previous pass's TMEM reads are complete before the next MMA
+                fence_before();
+                __syncthreads();
             }
-            uint32_t old[4];
+            // ---- MMA: D = Ah Bh^T + Ah Bl^T + Al Bh^T over KA/8 k-steps
+            if (tid == 0) {
+                fence_after();
+                const uint32_t idesc = make_idesc_tf32(kRows, w);
+                const uint32_t boff = (p0 / 8) * SBO;  // codeword rows p0.. of the B stage
 #pragma unroll
-            for (int s4 = 0; s4 < 4; ++s4) old[s4] = m1[s4];
-#pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-#pragma unroll
-                for (int s4 = 0; s4 < 4; ++s4) {
-                    const int jj = j + 2 * s4;
-                    const uint32_t ka = chunk_key(r[jj], uint32_t(jj), m32);
-                    const uint32_t kb = chunk_key(r[jj + 1], uint32_t(jj + 1), m32);
-                    const uint32_t lo = min(ka, kb), hi = max(ka, kb);
-                    m2[s4] = min(min(m2[s4], max(m1[s4], lo)), hi);
-                    m1[s4] = min(m1[s4], lo);
+                for (int s = 0; s < KA / 8; ++s) {
+                    const uint32_t ko = s * 256;  // two 16-byte K chunks per k-step
+                    const uint64_t dah = make_desc(a_hi + ko, 128, SBO);
+                    const uint64_t dal = make_desc(a_lo + ko, 128, SBO);
+                    const uint64_t dbh = make_desc(b_hi + boff + ko, 128, SBO);
+                    const uint64_t dbl = make_desc(b_lo + boff + ko, 128, SBO);
+                    mma_tf32(tmem, dah, dbh, idesc, s > 0);
+                    mma_tf32(tmem, dah, dbl, idesc, 1);
+                    mma_tf32(tmem, dal, dbh, idesc, 1);
                 }
+                mma_commit(&mbar);
             }
+            if (p0 == 0) load_row(tile + ncta, x_next);  // next tile's row, in flight during the epilogue
+            mbar_wait(&mbar, phase);
+            phase ^= 1;
+            fence_after();
+            // ---- epilogue: this thread's row, columns p0 .. p0 + w
+            for (uint32_t c0 = 0; c0 < w; c0 += 32) {
+                uint32_t r[32];
+                tmem_ld32(tmem + lane_base + c0, r);
+                tmem_wait_ld();
+                if (w - c0 < 32) {  // columns past N are not written by the MMA
 #pragma unroll
-            for (int s4 = 0; s4 < 4; ++s4) ch[s4] = (m1[s4] != old[s4]) ? c0 : ch[s4];
+                    for (int j = 16; j < 32; ++j) r[j] = 0x7f800000u;
+                }
+                uint32_t old[4];
+#pragma unroll
+                for (int s4 = 0; s4 < 4; ++s4) old[s4] = m1[s4];
+#pragma unroll
+                for (int j = 0; j < 32; j += 8) {
+#pragma unroll
+                    for (int s4 = 0; s4 < 4; ++s4) {
+                        const int jj = j + 2 * s4;
+                        const uint32_t ka = chunk_key(r[jj], uint32_t(jj), m32);
+                        const uint32_t kb = chunk_key(r[jj + 1], uint32_t(jj + 1), m32);
+                        const uint32_t lo = min(ka, kb), hi = max(ka, kb);
+                        m2[s4] = min(min(m2[s4], max(m1[s4], lo)), hi);
+                        m1[s4] = min(m1[s4], lo);
+                    }
+                }
+#pragma unroll
+                for (int s4 = 0; s4 < 4; ++s4) ch[s4] = (m1[s4] != old[s4]) ? p0 + c0 : ch[s4];
+            }
         }
         // merge the four states: full keys (value bits | global column) for the
         // best, value bits (low 5 cleared) for the runner-up
@@ -650,11 +662,12 @@ void launch_umma2(pqg_ctx* ctx, const NearestArgs& a) {
 
 template <int DS, int KA, bool PAD>
 void launch_umma(pqg_ctx* ctx, const NearestArgs& a) {
-    // measured (tools/screen_bench.py, r1): the synchronous 2-CTA/SM kernel wins
-    // for narrow tables and Ds=16/Ks=256; the pipelined 8-warp kernel otherwise
+    // measured (tools/screen_bench.py, r1): the synchronous multi-CTA/SM kernel
+    // wins for narrow tables, Ds <= 8 (two 128-codeword passes, 4 CTAs/SM) and
+    // Ds=16/Ks=256; the pipelined 8-warp kernel otherwise
     const char* env = std::getenv("PQG_UMMA");
     const uint32_t n_pad_sel = uint32_t((a.k + 15) / 16 * 16);
-    bool v1 = n_pad_sel <= 128 || (DS == 16 && n_pad_sel == 256);
+    bool v1 = n_pad_sel <= 128 || DS <= 8 || (DS == 16 && n_pad_sel == 256);
     if (env && env[0] == '1') v1 = true;
     if (env && env[0] == '2') v1 = false;
     if (!v1) {
@@ -662,21 +675,29 @@ void launch_umma(pqg_ctx* ctx, const NearestArgs& a) {
         return;
     }
     const uint32_t n_pad = uint32_t((a.k + 15) / 16 * 16);
-    uint32_t cols = 32;
-    while (cols < n_pad) cols <<= 1;
     const size_t smem = size_t(2) * n_pad * KA * 4 + size_t(2) * kRows * KA * 4;
+    const uint64_t smem_lim = (227u * 1024u) / (smem + 3u * 1024u);
+    // MMA width: all codewords in one pass, or two passes of 128 when that
+    // halves TMEM and shared memory lets 4 CTAs reside (measured r1,
+    // tools/screen_bench.py at 1M x 128, Ks=256: Ds=8 1.92 -> 1.38 ms, Ds=4
+    // 3.76 -> 3.10 ms against the pipelined kernel; at Ds=16, where only 3 CTAs
+    // fit, the second MMA round costs more than the extra CTA gains: 0.87 -> 1.12)
+    uint32_t n_mma = n_pad;
+    if (n_pad > 128 && smem_lim >= 4) n_mma = 128;
+    if (const char* se = std::getenv("PQG_UMMA_SPLIT")) n_mma = se[0] == '1' && n_pad > 128 ? 128 : n_pad;
+    uint32_t cols = 32;
+    while (cols < n_mma) cols <<= 1;
     auto kern = umma_screen_kernel<DS, KA, PAD>;
     PQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     const uint64_t ntiles = (a.n + kRows - 1) / kRows;
     // persistent: CTAs per SM limited by TMEM columns (2 at Ks=256), shared
     // memory and a cap of 4 (measured: narrow tables gain up to ~1.5x from the
     // extra CTAs, whose short tiles are latency-bound); PQG_UMMA_CTAS overrides
-    const uint64_t smem_lim = (227u * 1024u) / (smem + 3u * 1024u);
     uint64_t per_sm = std::max<uint64_t>(1, std::min<uint64_t>(std::min<uint64_t>(4u, 512u / cols), smem_lim));
     if (const char* ce = std::getenv("PQG_UMMA_CTAS")) per_sm = std::max(1, std::atoi(ce));
     uint64_t per_b = std::max<uint64_t>(1, (uint64_t(ctx->num_sms) * per_sm + a.B - 1) / a.B);
     per_b = std::min<uint64_t>(per_b, ntiles);
-    launch(ctx, "nearest_tc", kern, dim3(unsigned(per_b * a.B)), dim3(kRows), smem, a, n_pad, cols, 32u);
+    launch(ctx, "nearest_tc", kern, dim3(unsigned(per_b * a.B)), dim3(kRows), smem, a, n_pad, cols, 32u, n_mma);
 }
 
 }  // namespace

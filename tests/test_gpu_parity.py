@@ -555,3 +555,19 @@ def test_ivf_query_subset_golden_gpu(pq, gidx, golden):
     with pytest.raises(ValueError, match="not sorted"):
         pq.ivf_query_subset(index, golden["ivf/queries"][0], 10, golden["ivf/subset"][::-1], 6)
     assert pq.ivf_query_subset(index, golden["ivf/queries"][0], 10, [], 6).hits == []
+
+
+@pytest.mark.parametrize("variant", ["v1", "v1split", "v2"])
+@pytest.mark.parametrize("d,k", [(4, 256), (8, 256), (8, 200), (5, 144), (16, 256), (3, 129), (32, 256)])
+def test_umma_screen_variants(pq, orc, mix, monkeypatch, variant, d, k):
+    """Every tcgen05 screen variant (one pass, two 128-codeword passes, the
+    pipelined kernel) returns nearest_in_table's index and distance bits."""
+    monkeypatch.setenv("PQG_SCREEN", "tc")
+    monkeypatch.setenv("PQG_UMMA", "2" if variant == "v2" else "1")
+    monkeypatch.setenv("PQG_UMMA_SPLIT", "1" if variant == "v1split" else "0")
+    pts = mix(5000, d, 32, seed=d * k)
+    table = orc.random_matrix(k, d, 3000 + k) * 2.0
+    gi, gd = pq.nearest_batch(pts, table)
+    oi, od = orc.nearest_batch(pts, table)
+    assert np.array_equal(gi, oi)
+    assert np.array_equal(bits(gd), bits(od))

@@ -35,10 +35,16 @@ def main():
         os.environ["PQG_SCREEN"] = "fp32"
         L.check(lib.pqg_pq_fit(ctx.h, vp(train.data_ptr()), 100_000, D, M, ks, 3, 7, vp(t.data_ptr()), None, None))
         res = {}
-        for mode in ("fp32", "tc1", "tc8", "tc16"):
+        modes = ("fp32", "tc1", "tc1s", "tc8", "tc16", "tcdef")
+        for mode in modes:
+            # tc1: 1-pass v1; tc1s: v1 in two 128-codeword passes; tc8/tc16: the
+            # pipelined kernel with 8/16 warps; tcdef: the library's own choice
             os.environ["PQG_SCREEN"] = "fp32" if mode == "fp32" else "tc"
-            os.environ["PQG_UMMA"] = "1" if mode == "tc1" else "0"
-            os.environ["PQG_UMMA_WARPS"] = "8" if mode == "tc8" else "16"
+            os.environ["PQG_UMMA"] = {"tc1": "1", "tc1s": "1", "tc8": "2", "tc16": "2"}.get(mode, "0")
+            os.environ["PQG_UMMA_WARPS"] = "16" if mode == "tc16" else "8"
+            os.environ["PQG_UMMA_SPLIT"] = "1" if mode == "tc1s" else "0"
+            if mode == "tcdef":
+                del os.environ["PQG_UMMA_SPLIT"]
             codes = torch.empty((N, M), dtype=torch.uint8, device="cuda")
             enc = lambda: L.check(lib.pqg_pq_encode(ctx.h, vp(x.data_ptr()), N, M, ks, D // M,
                                                      vp(t.data_ptr()), vp(codes.data_ptr())))
@@ -60,7 +66,7 @@ def main():
             res[mode] = codes.cpu().numpy()
             print(f"M={M:2d} Ks={ks:3d} {mode:4s}: {ms:7.3f} ms/encode  {N/ms/1e6:8.2f} Mvec/s  "
                   f"screen {k1/max(n1,1):.3f} ms  fixup {k2/max(n2,1):.3f} ms", flush=True)
-        same = all(np.array_equal(res["fp32"], res[m]) for m in ("tc1", "tc8", "tc16"))
+        same = all(np.array_equal(res["fp32"], res[m]) for m in modes[1:])
         ref = orc.pq_encode(xh[sel], t.cpu().numpy())
         ok = np.array_equal(res["tc16"][sel], ref)
         print(f"   codes tc==fp32: {same}  tc==oracle(sample): {ok}", flush=True)
