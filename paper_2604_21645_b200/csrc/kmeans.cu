@@ -12,24 +12,37 @@
 // the pre-update fp64 distances, ascending cluster order, strict '>' argmax
 // (:122-130).  The resulting centroids are bit-identical to the reference's.
 #include "kernels.cuh"
+#include "tc_common.cuh"
 
 namespace pqg {
 
 namespace {
 
-constexpr int kTile = 2048;  // rows per bucketing tile (one warp walks a tile)
+// Bucketing geometry: a tile of T rows per CTA of W warps (each warp walks
+// T/W consecutive rows); W is bounded by the per-warp key counters in shared
+// memory, T by the size of the [k][tiles] count matrix that is scanned.
+struct BucketGeom {
+    uint32_t W, T, ntiles;
+};
+BucketGeom bucket_geom(uint64_t n, uint64_t k) {
+    BucketGeom g;
+    g.W = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(8, (96 * 1024) / (4 * std::max<uint64_t>(k, 1)))));
+    g.T = k <= 1024 ? 1024u : 4096u;  // multiples of 32 * W for every W <= 8
+    g.ntiles = uint32_t((n + g.T - 1) / g.T);
+    return g;
+}
 
-__global__ void hist_kernel(const uint32_t* keys, uint64_t n, uint64_t k, uint32_t ntiles,
+__global__ void hist_kernel(const uint32_t* keys, uint64_t n, uint64_t k, uint32_t ntiles, uint32_t T,
                             uint32_t* tile_counts) {
     extern __shared__ uint32_t hist[];
     const uint32_t tile = blockIdx.x, b = blockIdx.y;
     for (uint64_t c = threadIdx.x; c < k; c += blockDim.x) hist[c] = 0;
     __syncthreads();
-    const uint64_t r0 = uint64_t(tile) * kTile;
-    const uint64_t r1 = min64(n, r0 + kTile);
+    const uint64_t r0 = uint64_t(tile) * T;
+    const uint64_t r1 = min64(n, r0 + T);
     const uint32_t* kb = keys + uint64_t(b) * n;
     for (uint64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-        const uint32_t c = kb[i];
+        const uint32_t c = __ldg(kb + i);
         if (c < k) atomicAdd(&hist[c], 1u);  // key k marks a padding row (no cluster)
     }
     __syncthreads();
@@ -37,60 +50,129 @@ __global__ void hist_kernel(const uint32_t* keys, uint64_t n, uint64_t k, uint32
     for (uint64_t c = threadIdx.x; c < k; c += blockDim.x) out[c * ntiles + tile] = hist[c];
 }
 
-__global__ void offsets_kernel(const uint64_t* tile_base, uint64_t n, uint32_t B, uint64_t k,
-                               uint32_t ntiles, uint64_t* offsets, const uint64_t* nb) {
-    const uint64_t total = uint64_t(B) * (k + 1);
-    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
-         e += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t b = e / (k + 1), c = e - b * (k + 1);
-        // tile_base is one scan over all problems: problem b starts at its own
-        // first entry (b*n only when every problem has n keys)
-        offsets[e] = (c == k) ? (nb ? nb[b] : n)
-                              : tile_base[(b * k + c) * ntiles] - tile_base[b * k * ntiles];
-    }
-}
+// Copy of the bucketed rows: xs[b][pos][0..d) = x row i of problem b, so the
+// sums read each cluster's members as one contiguous, row-ordered block.
+struct RowCopy {
+    const float* x;
+    uint64_t ldx;
+    uint32_t col_stride, d;
+    float* out;      // [B][n][d]
+    bool vec;        // float4 path (d, ldx, col_stride and x 16-byte aligned)
+};
 
-// One warp per (tile, problem): walks its tile in row order 32 rows at a
-// time; __match_any_sync ranks equal keys inside the 32, the per-warp running
-// cursor keeps order across rounds, and tiles start at their scanned base.
-__global__ void scatter_kernel(const uint32_t* keys, uint64_t n, uint64_t k, uint32_t ntiles,
-                               const uint64_t* tile_base, uint32_t* perm, int warps_per_block) {
-    extern __shared__ uint32_t running_all[];
-    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t tile = blockIdx.x * warps_per_block + wib;
-    const uint32_t b = blockIdx.y;
-    if (tile >= ntiles) return;
-    uint32_t* running = running_all + uint64_t(wib) * k;
+// One CTA per (tile, problem), W warps, warp w owning rows [w*T/W, (w+1)*T/W)
+// of the tile.  Pass 1 counts each warp's keys, pass 2 turns the counts into
+// per-warp bases (tile base from the scan + the earlier warps' counts), pass 3
+// re-walks the rows in order: __match_any_sync ranks equal keys within 32
+// rows and the per-warp cursor keeps order across rounds, so members land in
+// ascending row order.  Output: the row permutation or (ROWS) the rows
+// themselves; tile 0 also writes the problem's cluster offsets.  (The
+// minimum-blocks hint keeps ptxas from sinking the row loads of the copy into
+// their stores, which serialises them.)
+template <bool ROWS>
+__global__ void __launch_bounds__(256, 1) scatter_kernel(const uint32_t* keys, uint64_t n, uint64_t k, uint32_t ntiles, uint32_t T,
+                               const uint64_t* tile_base, uint32_t* perm, RowCopy rc, uint64_t* offsets,
+                               const uint64_t* nb) {
+    extern __shared__ uint32_t wc[];  // [W][k]
+    const uint32_t W = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t tile = blockIdx.x, b = blockIdx.y;
     const uint64_t* tb = tile_base + uint64_t(b) * k * ntiles;
-    const uint64_t base_b = uint64_t(b) * n;
     const uint64_t first = tb[0];  // problem b's start in the all-problem scan
-    for (uint64_t c = lane; c < k; c += 32) running[c] = uint32_t(tb[c * ntiles + tile] - first);
-    __syncwarp();
-    const uint64_t r0 = uint64_t(tile) * kTile;
-    const uint64_t r1 = min64(n, r0 + kTile);
-    const uint32_t* kb = keys + base_b;
-    uint32_t* pb = perm + base_b;
-    // keys of the tile prefetched 32 rounds at a time (one register per round)
-    for (uint64_t c0 = r0; c0 < r1; c0 += 32 * 32) {
-        uint32_t key[32];
+    for (uint64_t e = threadIdx.x; e < uint64_t(W) * k; e += blockDim.x) wc[e] = 0;
+    __syncthreads();
+    const uint64_t seg = T / W;
+    const uint64_t wr0 = uint64_t(tile) * T + w * seg;
+    const uint64_t wr1 = min64(n, wr0 + seg);
+    const uint32_t* kb = keys + uint64_t(b) * n;
+    uint32_t* mine = wc + uint64_t(w) * k;
+    // rows go in batches of kRounds x 32: the batch's keys are loaded together
+    constexpr int kRounds = 4;
+    for (uint64_t i0 = wr0; i0 < wr1; i0 += 32 * kRounds) {
+        uint32_t cs[kRounds];
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
-            const uint64_t i = c0 + uint64_t(q) * 32 + lane;
-            key[q] = i < r1 ? __ldg(kb + i) : 0xFFFFFFFFu;
+        for (int r = 0; r < kRounds; ++r) {
+            const uint64_t i = i0 + r * 32 + lane;
+            cs[r] = i < wr1 ? __ldg(kb + i) : 0xFFFFFFFFu;
         }
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
-            const uint64_t i = c0 + uint64_t(q) * 32 + lane;
-            const uint32_t c = key[q];
-            const bool valid = i < r1 && c < k;
+        for (int r = 0; r < kRounds; ++r) {
+            const uint64_t i = i0 + r * 32 + lane;
+            const uint32_t c = cs[r];
+            const uint32_t peers = __match_any_sync(0xffffffffu, c);
+            if (i < wr1 && c < k && (peers & lanemask_lt()) == 0) mine[c] += __popc(peers);
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    for (uint64_t c = threadIdx.x; c < k; c += blockDim.x) {
+        const uint64_t start = tb[c * ntiles] - first;
+        uint64_t base = tb[c * ntiles + tile] - first;
+        for (uint32_t v = 0; v < W; ++v) {
+            const uint32_t t = wc[uint64_t(v) * k + c];
+            wc[uint64_t(v) * k + c] = uint32_t(base);
+            base += t;
+        }
+        if (tile == 0 && offsets) offsets[uint64_t(b) * (k + 1) + c] = start;
+    }
+    if (tile == 0 && offsets && threadIdx.x == 0) offsets[uint64_t(b) * (k + 1) + k] = nb ? nb[b] : n;
+    __syncthreads();
+    for (uint64_t i0 = wr0; i0 < wr1; i0 += 32 * kRounds) {
+        uint32_t cs[kRounds], pos[kRounds];
+        bool valid[kRounds];
+#pragma unroll
+        for (int r = 0; r < kRounds; ++r) {
+            const uint64_t i = i0 + r * 32 + lane;
+            cs[r] = i < wr1 ? __ldg(kb + i) : 0xFFFFFFFFu;
+        }
+#pragma unroll
+        for (int r = 0; r < kRounds; ++r) {
+            const uint64_t i = i0 + r * 32 + lane;
+            const uint32_t c = cs[r];
+            valid[r] = i < wr1 && c < k;
             const uint32_t peers = __match_any_sync(0xffffffffu, c);
             const uint32_t rank = __popc(peers & lanemask_lt());
-            uint32_t pos = 0;
-            if (valid) pos = running[c] + rank;
+            pos[r] = valid[r] ? mine[c] + rank : 0u;
             __syncwarp();
-            if (valid && rank == 0) running[c] += __popc(peers);
+            if (valid[r] && rank == 0) mine[c] += __popc(peers);
             __syncwarp();
-            if (valid) pb[pos] = uint32_t(i);
+        }
+        if (!ROWS) {
+#pragma unroll
+            for (int r = 0; r < kRounds; ++r)
+                if (valid[r]) perm[uint64_t(b) * n + pos[r]] = uint32_t(i0 + r * 32 + lane);
+        } else {
+            // each lane copies its rows: whole 16-byte pieces (full sectors);
+            // the batch's (row, piece) units go eight at a time, all loads
+            // (unpredicated, clamped) issued before the stores
+            const uint32_t Q = rc.vec ? rc.d / 4 : rc.d;
+            const uint32_t U = kRounds * Q;
+            const float* xb = rc.x + uint64_t(b) * rc.col_stride;
+            float* ob = rc.out + uint64_t(b) * n * rc.d;
+            for (uint32_t e0 = 0; e0 < U; e0 += 8) {
+                float4 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint32_t e = min(e0 + u, U - 1);
+                    const uint32_t r = e / Q, t = e - r * Q;
+                    const uint64_t i = min64(i0 + r * 32 + lane, wr1 - 1);
+                    if (rc.vec) v[u] = __ldg(reinterpret_cast<const float4*>(xb + i * rc.ldx) + t);
+                    else v[u].x = __ldg(xb + i * rc.ldx + t);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint32_t e = e0 + u;
+                    if (e >= U) break;
+                    const uint32_t r = e / Q, t = e - r * Q;
+                    bool ok = false;
+                    uint32_t ps = 0;
+#pragma unroll
+                    for (int rr = 0; rr < kRounds; ++rr)
+                        if (uint32_t(rr) == r) { ok = valid[rr]; ps = pos[rr]; }
+                    if (!ok) continue;
+                    if (rc.vec) reinterpret_cast<float4*>(ob + uint64_t(ps) * rc.d)[t] = v[u];
+                    else ob[uint64_t(ps) * rc.d + t] = v[u].x;
+                }
+            }
         }
     }
 }
@@ -295,6 +377,89 @@ __global__ void final_parts_kernel(const double* parts, uint32_t nparts, double*
 constexpr int kMeanThreads = 256;
 constexpr int kMeanStage = 4096;  // members staged per step of the row-order fallback
 
+// Row-order fp64 sum (kmeans.cpp:103-111) of the staged values col[mi*nf+f],
+// mi < nm, continuing from s; every thread of a kMeanThreads block calls it
+// and gets the same result.  The members go in chunks of kMeanThreads: a
+// chunk whose additions are all exact -- every partial sum is a multiple of
+// q = min(ulp(s), ulp of its smallest value) and below 2^lb, lb - log2 q <= 53
+// -- is added as one parallel exact sum; only a chunk that can round is walked
+// sequentially.  (A rejected (cluster, dim) typically holds one tiny value,
+// so one chunk in a thousand-member cluster runs the serial chain.)  s is a
+// normal double here (sums of fp32 values never reach the fp64 subnormals).
+struct SeqScratch {
+    double rsum[2][kMeanThreads / 32];
+    int rmax[2][kMeanThreads / 32], rmin[2][kMeanThreads / 32];
+    double bc;
+};
+__device__ double staged_row_order_sum(double s, const float* col, uint32_t nf, uint32_t f, uint32_t nm,
+                                       SeqScratch& sc, uint32_t& par) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    for (uint32_t c0 = 0; c0 < nm; c0 += kMeanThreads) {
+        const uint32_t mi = c0 + tid;
+        const float v = mi < nm ? col[mi * nf + f] : 0.f;
+        const int eb = int((__float_as_uint(v) >> 23) & 0xFFu);
+        int ehi = v != 0.f ? eb : -1;
+        int elo = v != 0.f ? max(eb, 1) : (1 << 30);
+        double ds = (double)v;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            ds = __dadd_rn(ds, __shfl_xor_sync(0xffffffffu, ds, o));
+            ehi = max(ehi, __shfl_xor_sync(0xffffffffu, ehi, o));
+            elo = min(elo, __shfl_xor_sync(0xffffffffu, elo, o));
+        }
+        if (lane == 0) {
+            sc.rsum[par][w] = ds;
+            sc.rmax[par][w] = ehi;
+            sc.rmin[par][w] = elo;
+        }
+        __syncthreads();
+        double tot = 0.0;
+        ehi = -1;
+        elo = 1 << 30;
+#pragma unroll
+        for (int u = 0; u < kMeanThreads / 32; ++u) {
+            tot = __dadd_rn(tot, sc.rsum[par][u]);
+            ehi = max(ehi, sc.rmax[par][u]);
+            elo = min(elo, sc.rmin[par][u]);
+        }
+        par ^= 1u;
+        bool exact;
+        if (ehi < 0) {
+            exact = true;  // all zeros
+        } else if (ehi == 255 || !isfinite(s)) {
+            exact = false;
+        } else {
+            int lq = elo - 150;  // log2 ulp of the smallest nonzero value
+            int lb = ehi - 118;  // kMeanThreads values below 2^(ehi-126) each
+            if (s != 0.0) {
+                // s = mant * 2^(E-1075): its lowest set bit, not its ulp, bounds
+                // the granularity (a running sum of fp32 values is usually a
+                // multiple of a much coarser power of two than its ulp)
+                const unsigned long long sb = __double_as_longlong(s);
+                const int E = int((sb >> 52) & 0x7FF);
+                const unsigned long long mant = (sb & ((1ull << 52) - 1)) | (1ull << 52);
+                lq = min(lq, E - 1075 + (__ffsll((long long)mant) - 1));
+                lb = max(lb, E - 1022);  // |s| < 2^(E-1022)
+            }
+            exact = lb + 1 - lq <= 53;
+        }
+        if (exact) {
+            s = __dadd_rn(s, tot);
+        } else {
+            if (tid == 0) {
+                const uint32_t me = min(nm - c0, uint32_t(kMeanThreads));
+                double q = s;
+#pragma unroll 8
+                for (uint32_t i = 0; i < me; ++i) q = __dadd_rn(q, (double)col[(c0 + i) * nf + f]);
+                sc.bc = q;
+            }
+            __syncthreads();
+            s = sc.bc;
+        }
+    }
+    return s;
+}
+
 __global__ void __launch_bounds__(kMeanThreads) mean_exact_kernel(
     const float* x, uint64_t ldx, uint32_t col_stride, uint64_t n, uint32_t d, uint64_t k,
     const uint64_t* offsets, const uint32_t* perm, float* table, int* has_empty, const int* active) {
@@ -303,6 +468,8 @@ __global__ void __launch_bounds__(kMeanThreads) mean_exact_kernel(
     __shared__ float col[kMeanStage];  // one dim of the members, row order (fallback)
     __shared__ uint32_t nfail;
     __shared__ uint32_t failed[kMeanThreads];
+    __shared__ SeqScratch sc;
+    __shared__ double sres[kMeanThreads];
     const uint64_t bc = blockIdx.x;
     const uint64_t b = bc / k, c = bc - b * k;
     if (active && !active[b]) return;
@@ -313,7 +480,7 @@ __global__ void __launch_bounds__(kMeanThreads) mean_exact_kernel(
         return;
     }
     const uint64_t cnt = end - beg;
-    const uint32_t* pb = perm + b * n;
+    const uint32_t* pb = perm ? perm + b * n : nullptr;  // null: x is the bucketed copy
     const float* xb = x + b * col_stride;
     const uint32_t DG = d < kMeanThreads ? d : kMeanThreads;
     const uint32_t G = kMeanThreads / DG;
@@ -340,14 +507,14 @@ __global__ void __launch_bounds__(kMeanThreads) mean_exact_kernel(
             for (; m + 3 * uint64_t(G) < end; m += 4 * uint64_t(G)) {
                 uint32_t r[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) r[u] = __ldg(pb + m + u * G);
+                for (int u = 0; u < 4; ++u) r[u] = pb ? __ldg(pb + m + u * G) : uint32_t(m + u * G);
                 float v[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) v[u] = __ldg(xb + uint64_t(r[u]) * ldx + t);
 #pragma unroll
                 for (int u = 0; u < 4; ++u) acc(v[u]);
             }
-            for (; m < end; m += G) acc(__ldg(xb + uint64_t(__ldg(pb + m)) * ldx + t));
+            for (; m < end; m += G) acc(__ldg(xb + uint64_t(pb ? __ldg(pb + m) : uint32_t(m)) * ldx + t));
         }
         ps[threadIdx.x] = s;
         pmax[threadIdx.x] = emax;
@@ -371,25 +538,312 @@ __global__ void __launch_bounds__(kMeanThreads) mean_exact_kernel(
         const uint32_t nf = nfail;
         if (nf > 0) {
             const uint64_t mchunk = kMeanStage / nf;
-            double sf = 0.0;
+            uint32_t par = 0;
+            if (threadIdx.x < nf) sres[threadIdx.x] = 0.0;
             for (uint64_t m0 = beg; m0 < end; m0 += mchunk) {
                 const uint64_t m1 = m0 + mchunk < end ? m0 + mchunk : end;
                 const uint32_t nm = uint32_t(m1 - m0);
                 for (uint32_t e = threadIdx.x; e < nm * nf; e += blockDim.x) {
                     const uint32_t mi = e / nf, f = e - mi * nf;
-                    col[e] = __ldg(xb + uint64_t(__ldg(pb + m0 + mi)) * ldx + failed[f]);
+                    col[e] = __ldg(xb + uint64_t(pb ? __ldg(pb + m0 + mi) : uint32_t(m0 + mi)) * ldx + failed[f]);
                 }
                 __syncthreads();
-                if (threadIdx.x < nf)
-                    for (uint32_t mi = 0; mi < nm; ++mi) sf = __dadd_rn(sf, (double)col[mi * nf + threadIdx.x]);
+                for (uint32_t f = 0; f < nf; ++f) {
+                    const double sf = staged_row_order_sum(sres[f], col, nf, f, nm, sc, par);
+                    __syncthreads();
+                    if (threadIdx.x == 0) sres[f] = sf;
+                }
                 __syncthreads();
             }
-            if (threadIdx.x < nf) table[bc * d + failed[threadIdx.x]] = __double2float_rn(__dmul_rn(sf, inv));
+            if (threadIdx.x < nf)
+                table[bc * d + failed[threadIdx.x]] = __double2float_rn(__dmul_rn(sres[threadIdx.x], inv));
         }
         __syncthreads();
     }
 }
 
+
+// ---- Piece-parallel exact means -------------------------------------------
+// A cluster's members (row order after the stable bucketing) are cut into
+// pieces of R = 8*G rows; one warp per piece accumulates fp64 sums and the
+// exponent range per dim (lane (g, q): float4 column group q of rows g, g+G,
+// ...; eight row loads in flight), writes them as PieceStats, and the warp
+// that completes a cluster's last piece finalizes it: if the whole cluster
+// passes the exactness test the piece sums are added in any order; otherwise
+// the pieces are replayed in row order -- a piece whose additions are
+// provably exact given the running sum is added whole, any other one member
+// by member (the reference's sequential fp64 chain, kmeans.cpp:103-111).
+// Big clusters therefore spread over many warps, and the serial fallback is
+// confined to the pieces that can actually round.
+struct PieceStat {
+    double s;
+    int emax, emin;
+};
+struct PieceGeom {
+    uint32_t DG, G, R, lR;  // lanes per row, row groups, rows per piece, log2 R
+    uint64_t PP;            // piece slots per problem
+};
+__host__ __device__ inline PieceGeom piece_geom(uint32_t d, uint64_t n, uint64_t k) {
+    PieceGeom g;
+    g.DG = d / 4;
+    g.G = 32 / g.DG;
+    g.R = 8 * g.G;
+    g.lR = 0;
+    while ((1u << g.lR) < g.R) ++g.lR;
+    g.PP = (n + g.R - 1) / g.R + k;
+    return g;
+}
+
+// A piece: rows [r0, r0 + rows) of its problem's bucketed order (rows == 0:
+// unused slot).
+struct PieceDesc {
+    uint64_t r0;
+    uint32_t rows, c;
+};
+
+// Per problem: piece counts -> piece_start (exclusive scan), the piece
+// descriptors, the empty-cluster flag.
+__global__ void __launch_bounds__(1024) pieces_setup_kernel(const uint64_t* offsets, uint64_t k, uint32_t R,
+                                                            uint64_t PP, uint32_t* piece_start,
+                                                            PieceDesc* pieces, int* has_empty,
+                                                            const int* active, uint32_t d, double* csum,
+                                                            int* cmax, int* cmin) {
+    __shared__ uint32_t wsum[32];
+    __shared__ int any_empty;
+    const uint32_t b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (tid == 0) any_empty = 0;
+    for (uint64_t e = uint64_t(b) * k * d + tid; e < uint64_t(b + 1) * k * d; e += blockDim.x) {
+        csum[e] = 0.0;
+        cmax[e] = -1;
+        cmin[e] = 1 << 30;
+    }
+    const uint64_t* off = offsets + uint64_t(b) * (k + 1);
+    const uint64_t per = (k + blockDim.x - 1) / blockDim.x;
+    const uint64_t c0 = min64(k, tid * per), c1 = min64(k, c0 + per);
+    uint32_t local = 0;
+    bool empty = false;
+    for (uint64_t c = c0; c < c1; ++c) {
+        const uint64_t cnt = off[c + 1] - off[c];
+        local += uint32_t((cnt + R - 1) / R);
+        empty |= cnt == 0;
+    }
+    uint32_t incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= uint32_t(o)) incl += v;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    if (empty) any_empty = 1;
+    if (w == 0) {
+        const uint32_t nw = blockDim.x >> 5;
+        uint32_t t = lane < nw ? wsum[lane] : 0u, ti = t;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, ti, o);
+            if (lane >= uint32_t(o)) ti += v;
+        }
+        if (lane < nw) wsum[lane] = ti - t;
+    }
+    __syncthreads();
+    uint32_t base = wsum[w] + incl - local;
+    for (uint64_t c = c0; c < c1; ++c) {
+        const uint64_t cnt = off[c + 1] - off[c];
+        const uint32_t np = uint32_t((cnt + R - 1) / R);
+        piece_start[uint64_t(b) * k + c] = base;
+        for (uint32_t i = 0; i < np; ++i) {
+            const uint64_t r0 = off[c] + uint64_t(i) * R;
+            pieces[uint64_t(b) * PP + base + i] = PieceDesc{r0, uint32_t(min64(R, off[c + 1] - r0)), uint32_t(c)};
+        }
+        base += np;
+    }
+    __syncthreads();
+    // the last thread's end is the total: mark the unused slots
+    __shared__ uint32_t total;
+    if (tid == blockDim.x - 1) total = base;
+    __syncthreads();
+    for (uint64_t p = total + tid; p < PP; p += blockDim.x) pieces[uint64_t(b) * PP + p] = PieceDesc{0, 0u, 0u};
+    if (tid == 0) has_empty[b] = (active && !active[b]) ? 0 : any_empty;
+}
+
+// Row m of problem b's bucketed order: the copy (xs) or the permutation.
+struct MemberRows {
+    const float* x;      // copy: [B][n][d]; permutation: the rows
+    uint64_t ldx;
+    uint32_t col_stride;
+    const uint32_t* perm;  // null: x is the bucketed copy
+};
+__device__ __forceinline__ const float* member_row(const MemberRows& mr, uint64_t n, uint32_t d, uint64_t b,
+                                                   uint64_t m) {
+    if (!mr.perm) return mr.x + (b * n + m) * d;
+    return mr.x + uint64_t(__ldg(mr.perm + b * n + m)) * mr.ldx + b * mr.col_stride;
+}
+
+__global__ void __launch_bounds__(kMeanThreads, 4) mean_pieces_kernel(
+    MemberRows mr, uint64_t n, uint32_t d, uint64_t k, uint32_t B, const PieceDesc* pieces, PieceStat* stats,
+    const int* active, double* csum, int* cmax, int* cmin) {
+    const uint32_t lane = threadIdx.x & 31;
+    const PieceGeom pg = piece_geom(d, n, k);
+    const uint64_t wgl = uint64_t(blockIdx.x) * (kMeanThreads / 32) + (threadIdx.x >> 5);
+    if (wgl >= uint64_t(B) * pg.PP) return;
+    const uint64_t b = wgl / pg.PP;
+    if (active && !active[b]) return;
+    const PieceDesc pd = pieces[wgl];
+    if (pd.rows == 0) return;
+    const uint64_t r0 = pd.r0;
+    const uint32_t rows = pd.rows;
+    const uint32_t DG = pg.DG, G = pg.G;
+    const uint32_t g = lane / DG, q = lane - g * DG;
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    int emax[4] = {-1, -1, -1, -1}, emin[4] = {1 << 30, 1 << 30, 1 << 30, 1 << 30};
+    if (g < G) {
+        float4 v[8];
+        if (!mr.perm) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                v[u] = __ldg(reinterpret_cast<const float4*>(mr.x + (b * n + r0 + min(g + u * G, rows - 1)) * d) + q);
+        } else {
+            uint32_t rid[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) rid[u] = __ldg(mr.perm + b * n + r0 + min(g + u * G, rows - 1));
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                v[u] = __ldg(reinterpret_cast<const float4*>(mr.x + uint64_t(rid[u]) * mr.ldx + b * mr.col_stride) + q);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const bool in = g + u * G < rows;  // rows past the end count as zeros: exact, no exponent
+            const float e4[4] = {in ? v[u].x : 0.f, in ? v[u].y : 0.f, in ? v[u].z : 0.f, in ? v[u].w : 0.f};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                s[j] = __dadd_rn(s[j], (double)e4[j]);
+                const int e = int((__float_as_uint(e4[j]) >> 23) & 0xFFu);
+                if (e4[j] != 0.f) {
+                    emax[j] = max(emax[j], e);
+                    emin[j] = min(emin[j], max(e, 1));
+                }
+            }
+        }
+    }
+    for (uint32_t h = 1; h < G; ++h) {  // groups into group 0 (exact: any order)
+        const uint32_t src = h * DG + q;
+        const uint32_t sl = (g == 0 && src < 32) ? src : lane;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const double os = __shfl_sync(0xffffffffu, s[j], sl);
+            const int oa = __shfl_sync(0xffffffffu, emax[j], sl);
+            const int oi = __shfl_sync(0xffffffffu, emin[j], sl);
+            if (g == 0) {
+                s[j] = __dadd_rn(s[j], os);
+                emax[j] = max(emax[j], oa);
+                emin[j] = min(emin[j], oi);
+            }
+        }
+    }
+    // the piece's stats (for a row-order replay) and the cluster totals:
+    // atomic fp64 adds of exact partial sums are exact in any order whenever
+    // the cluster passes the test; the finalize checks that
+    PieceStat* st = stats + wgl * d;
+    if (g == 0) {
+        const uint64_t cb = (b * k + pd.c) * d + q * 4;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            st[q * 4 + j] = PieceStat{s[j], emax[j], emin[j]};
+            atomicAdd(csum + cb + j, s[j]);
+            if (emax[j] >= 0) {
+                atomicMax(cmax + cb + j, emax[j]);
+                atomicMin(cmin + cb + j, emin[j]);
+            }
+        }
+    }
+}
+
+// One warp per cluster: combine its pieces' stats (see above).
+__global__ void __launch_bounds__(kMeanThreads) mean_finalize_kernel(
+    MemberRows mr, uint64_t n, uint32_t d, uint64_t k, uint32_t B, const uint64_t* offsets,
+    const uint32_t* piece_start, const PieceStat* stats, float* table, const int* active, const double* csum,
+    const int* cmax, const int* cmin) {
+    const uint32_t lane = threadIdx.x & 31;
+    const PieceGeom pg = piece_geom(d, n, k);
+    const uint64_t bc = uint64_t(blockIdx.x) * (kMeanThreads / 32) + (threadIdx.x >> 5);
+    if (bc >= uint64_t(B) * k) return;
+    const uint64_t b = bc / k, c = bc - b * k;
+    if (active && !active[b]) return;
+    const uint64_t beg = offsets[b * (k + 1) + c], end = offsets[b * (k + 1) + c + 1];
+    if (beg == end) return;  // empty: the reseed fills it
+    const uint64_t cnt = end - beg;
+    const uint32_t ps = piece_start[bc];
+    const uint32_t np = uint32_t((cnt + pg.R - 1) / pg.R);
+    // ---- finalize cluster c (this warp completed it)
+    int lg = 0;
+    while ((uint64_t(1) << lg) < cnt) ++lg;
+    const double inv = __ddiv_rn(1.0, (double)cnt);
+    const PieceStat* cs = stats + (b * pg.PP + ps) * d;
+    // (1) lane t: the cluster's total and exponent range of dim t
+    uint32_t need = 0;  // bit: dim lane + 32*bit rejected by the exactness test
+    for (uint32_t t = lane, bit = 0; t < d; t += 32, ++bit) {
+        const int ea = cmax[bc * d + t], ei = cmin[bc * d + t];
+        if (ea < 0 || (ea < 255 && ea - ei + lg <= 28))
+            table[bc * d + t] = __double2float_rn(__dmul_rn(csum[bc * d + t], inv));  // any order is exact
+        else
+            need |= 1u << bit;
+    }
+    // (2) rejected dims, one at a time by the whole warp: replay the pieces in
+    // row order; a piece that cannot round given the running sum is added
+    // whole, any other member by member (values loaded together, the chain
+    // walked through shuffles)
+    for (uint32_t bit = 0; 32 * bit < d; ++bit) {
+        for (uint32_t todo = __ballot_sync(0xffffffffu, (need >> bit) & 1u); todo; todo &= todo - 1) {
+            const uint32_t t = 32 * bit + uint32_t(__ffs(todo) - 1);
+            double r = 0.0;
+            for (uint32_t i0 = 0; i0 < np; i0 += 32) {
+                const uint32_t il = min(i0 + lane, np - 1);
+                const PieceStat* e = &cs[uint64_t(il) * d + t];
+                const double ls = __ldcg(&e->s);
+                const int la = __ldcg(&e->emax), lm = __ldcg(&e->emin);
+                const uint32_t cnt_i = min(32u, np - i0);
+                for (uint32_t ii = 0; ii < cnt_i; ++ii) {
+                    const double ss = __shfl_sync(0xffffffffu, ls, ii);
+                    const int a = __shfl_sync(0xffffffffu, la, ii), m = __shfl_sync(0xffffffffu, lm, ii);
+                    bool exact;
+                    if (a < 0) {
+                        exact = true;
+                    } else if (a == 255 || !isfinite(r)) {
+                        exact = false;
+                    } else {
+                        int lq = m - 150, lb = a - 126 + int(pg.lR);
+                        if (r != 0.0) {
+                            const unsigned long long sb = __double_as_longlong(r);
+                            const int E = int((sb >> 52) & 0x7FF);
+                            const unsigned long long mant = (sb & ((1ull << 52) - 1)) | (1ull << 52);
+                            lq = min(lq, E - 1075 + (__ffsll((long long)mant) - 1));
+                            lb = max(lb, E - 1022);
+                        }
+                        exact = lb + 1 - lq <= 53;
+                    }
+                    if (exact) {
+                        r = __dadd_rn(r, ss);
+                        continue;
+                    }
+                    const uint64_t m0 = beg + uint64_t(i0 + ii) * pg.R;
+                    const uint32_t mr_n = uint32_t(min64(pg.R, end - m0));  // <= 256 = 8 x 32
+                    float v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        v[u] = __ldg(member_row(mr, n, d, b, m0 + min(uint32_t(u * 32) + lane, mr_n - 1)) + t);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        if (uint32_t(u * 32) >= mr_n) break;
+                        const uint32_t lim = min(32u, mr_n - u * 32);
+                        for (uint32_t l = 0; l < lim; ++l) r = __dadd_rn(r, (double)__shfl_sync(0xffffffffu, v[u], l));
+                    }
+                }
+            }
+            if (lane == 0) table[(b * k + c) * d + t] = __double2float_rn(__dmul_rn(r, inv));
+        }
+    }
+}
 
 // The same sums for small sub-dimensions (d <= 32, the PQ fits): one warp per
 // (problem, cluster), lanes = (member group, dim); eight clusters per CTA, so
@@ -414,7 +868,7 @@ __global__ void __launch_bounds__(kMeanThreads) mean_exact_warp_kernel(
         return;
     }
     const uint64_t cnt = end - beg;
-    const uint32_t* pb = perm + b * n;
+    const uint32_t* pb = perm ? perm + b * n : nullptr;  // null: x is the bucketed copy
     const float* xb = x + b * col_stride;
     const uint32_t G = 32 / d;  // member groups
     const uint32_t g = uint32_t(lane) / d, t = uint32_t(lane) - g * d;
@@ -433,14 +887,14 @@ __global__ void __launch_bounds__(kMeanThreads) mean_exact_warp_kernel(
         for (; m + 3 * uint64_t(G) < end; m += 4 * uint64_t(G)) {
             uint32_t r[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) r[u] = __ldg(pb + m + u * G);
+            for (int u = 0; u < 4; ++u) r[u] = pb ? __ldg(pb + m + u * G) : uint32_t(m + u * G);
             float v[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) v[u] = __ldg(xb + uint64_t(r[u]) * ldx + t);
 #pragma unroll
             for (int u = 0; u < 4; ++u) acc(v[u]);
         }
-        for (; m < end; m += G) acc(__ldg(xb + uint64_t(__ldg(pb + m)) * ldx + t));
+        for (; m < end; m += G) acc(__ldg(xb + uint64_t(pb ? __ldg(pb + m) : uint32_t(m)) * ldx + t));
     }
     // combine the member groups of each dim (lanes t, t+d, t+2d, ...): exact
     // sums, so the combination order does not matter
@@ -470,7 +924,7 @@ __global__ void __launch_bounds__(kMeanThreads) mean_exact_warp_kernel(
         for (uint64_t m0 = beg; m0 < end; m0 += kMeanWarpStage) {
             const uint64_t m1 = m0 + kMeanWarpStage < end ? m0 + kMeanWarpStage : end;
             for (uint64_t m = m0 + lane; m < m1; m += 32)
-                col[m - m0] = __ldg(xb + uint64_t(__ldg(pb + m)) * ldx + tf);
+                col[m - m0] = __ldg(xb + uint64_t(pb ? __ldg(pb + m) : uint32_t(m)) * ldx + tf);
             __syncwarp();
             if (lane == 0)
                 for (uint64_t m = m0; m < m1; ++m) sf = __dadd_rn(sf, (double)col[m - m0]);
@@ -562,25 +1016,37 @@ void exclusive_scan_u32(pqg_ctx* ctx, const uint32_t* in, uint64_t* out, uint64_
     exclusive_scan<uint32_t>(ctx, in, out, count);
 }
 
+static void bucket_impl(pqg_ctx* ctx, const uint32_t* keys, uint64_t n, uint32_t B, uint64_t k,
+                        Bucketing out, const RowCopy* rows, const uint64_t* nb) {
+    if (k > 16384) fail(PQG_EUNSUPPORTED, "bucketing supports at most 16384 lists/clusters");
+    if (n == 0) {
+        PQG_CUDA(cudaMemsetAsync(out.offsets, 0, sizeof(uint64_t) * B * (k + 1), ctx->stream));
+        return;
+    }
+    const BucketGeom g = bucket_geom(n, k);
+    uint32_t* tile_counts = scratch<uint32_t>(ctx, uint64_t(B) * k * g.ntiles);
+    uint64_t* tile_base = scratch<uint64_t>(ctx, uint64_t(B) * k * g.ntiles);
+    const size_t hsmem = sizeof(uint32_t) * k;
+    set_smem(hist_kernel, hsmem);
+    launch(ctx, "bucket", hist_kernel, dim3(g.ntiles, B), dim3(256), hsmem, keys, n, k, g.ntiles, g.T,
+           tile_counts);
+    exclusive_scan<uint32_t>(ctx, tile_counts, tile_base, uint64_t(B) * k * g.ntiles);
+    const size_t ssmem = sizeof(uint32_t) * k * g.W;
+    if (rows) {
+        set_smem(scatter_kernel<true>, ssmem);
+        launch(ctx, "bucket", scatter_kernel<true>, dim3(g.ntiles, B), dim3(32 * g.W), ssmem, keys, n, k,
+               g.ntiles, g.T, (const uint64_t*)tile_base, (uint32_t*)nullptr, *rows, out.offsets, nb);
+    } else {
+        set_smem(scatter_kernel<false>, ssmem);
+        launch(ctx, "bucket", scatter_kernel<false>, dim3(g.ntiles, B), dim3(32 * g.W), ssmem, keys, n, k,
+               g.ntiles, g.T, (const uint64_t*)tile_base, out.perm, RowCopy{}, out.offsets, nb);
+    }
+}
+
 void stable_bucket(pqg_ctx* ctx, const uint32_t* keys, uint64_t n, uint32_t B, uint64_t k,
                    const int* active, Bucketing out, const uint64_t* nb) {
     (void)active;
-    if (k > 16384) fail(PQG_EUNSUPPORTED, "bucketing supports at most 16384 lists/clusters");
-    const uint32_t ntiles = uint32_t((n + kTile - 1) / kTile);
-    uint32_t* tile_counts = scratch<uint32_t>(ctx, uint64_t(B) * k * ntiles);
-    uint64_t* tile_base = scratch<uint64_t>(ctx, uint64_t(B) * k * ntiles);
-    const size_t hsmem = sizeof(uint32_t) * k;
-    set_smem(hist_kernel, hsmem);
-    launch(ctx, "bucket", hist_kernel, dim3(ntiles, B), dim3(256), hsmem, keys, n, k, ntiles,
-           tile_counts);
-    exclusive_scan<uint32_t>(ctx, tile_counts, tile_base, uint64_t(B) * k * ntiles);
-    launch(ctx, "bucket", offsets_kernel, dim3(grid1d(uint64_t(B) * (k + 1), 256, 4096)),
-           dim3(256), 0, (const uint64_t*)tile_base, n, B, k, ntiles, out.offsets, nb);
-    int wpb = int(std::max<uint64_t>(1, std::min<uint64_t>(8, (96 * 1024) / (4 * k))));
-    const size_t ssmem = sizeof(uint32_t) * k * wpb;
-    set_smem(scatter_kernel, ssmem);
-    launch(ctx, "bucket", scatter_kernel, dim3((ntiles + wpb - 1) / wpb, B), dim3(32 * wpb), ssmem,
-           keys, n, k, ntiles, (const uint64_t*)tile_base, out.perm, wpb);
+    bucket_impl(ctx, keys, n, B, k, out, nullptr, nb);
 }
 
 namespace {
@@ -634,22 +1100,75 @@ void rows_sum_f64(pqg_ctx* ctx, const double* v, uint64_t n, uint32_t B, double*
 void kmeans_update(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint32_t d,
                    float* table, uint64_t k, const uint32_t* assign, double* dist,
                    const int* active, const uint64_t* nb) {
-    Bucketing bk{scratch<uint64_t>(ctx, uint64_t(B) * (k + 1)), scratch<uint32_t>(ctx, uint64_t(B) * n)};
-    stable_bucket(ctx, assign, n, B, k, active, bk, nb);
-    int* has_empty = scratch<int>(ctx, B);
-    PQG_CUDA(cudaMemsetAsync(has_empty, 0, sizeof(int) * B, ctx->stream));
     if (uint64_t(B) * k > 0x7FFFFFFFull) fail(PQG_EUNSUPPORTED, "kmeans: too many clusters");
-    const uint64_t ncl = uint64_t(B) * k;
-    // small clusters (batched chunk fits): a warp each; large ones: a CTA each
-    if (d <= 32 && n <= 128 * k) {
-        const uint64_t blocks = (ncl + kMeanThreads / 32 - 1) / (kMeanThreads / 32);
-        launch(ctx, "kmeans_sum", mean_exact_warp_kernel, dim3(unsigned(blocks)), dim3(kMeanThreads), 0,
-               src.x, src.ldx, src.col_stride, n, d, k, ncl, (const uint64_t*)bk.offsets,
-               (const uint32_t*)bk.perm, table, has_empty, active);
+    // bucket the rows themselves (a stable, cluster-ordered copy), so the sums
+    // stream each cluster's members contiguously instead of gathering rows
+    // through a permutation; the permutation is the fallback for huge blocks
+    bool copy = uint64_t(n) * d <= 0xFFFFFFFFull;
+    if (const char* e = std::getenv("PQG_KM_COPY")) copy = copy && e[0] != '0';
+    Bucketing bk{scratch<uint64_t>(ctx, uint64_t(B) * (k + 1)), nullptr};
+    const float* mx = src.x;
+    uint64_t mldx = src.ldx;
+    uint32_t mcs = src.col_stride;
+    if (copy) {
+        RowCopy rc;
+        rc.x = src.x;
+        rc.ldx = src.ldx;
+        rc.col_stride = src.col_stride;
+        rc.d = d;
+        rc.out = scratch<float>(ctx, uint64_t(B) * n * d);
+        rc.vec = (d % 4) == 0 && (src.ldx % 4) == 0 && (src.col_stride % 4) == 0 &&
+                 (reinterpret_cast<uintptr_t>(src.x) & 15u) == 0;
+        bucket_impl(ctx, assign, n, B, k, bk, &rc, nb);
+        mx = rc.out;
+        mldx = d;
+        mcs = uint32_t(n * d);
     } else {
-        launch(ctx, "kmeans_sum", mean_exact_kernel, dim3(unsigned(ncl)), dim3(kMeanThreads), 0,
-               src.x, src.ldx, src.col_stride, n, d, k, (const uint64_t*)bk.offsets,
-               (const uint32_t*)bk.perm, table, has_empty, active);
+        bk.perm = scratch<uint32_t>(ctx, uint64_t(B) * n);
+        bucket_impl(ctx, assign, n, B, k, bk, nullptr, nb);
+    }
+    int* has_empty = scratch<int>(ctx, B);
+    const uint64_t ncl = uint64_t(B) * k;
+    const char* mean_env = std::getenv("PQG_KM_MEAN");
+    const bool pieces = d % 4 == 0 && d <= 128 && !(mean_env && mean_env[0] != 'p') &&
+                        (copy ? (reinterpret_cast<uintptr_t>(mx) & 15u) == 0
+                              : ((src.ldx | src.col_stride) & 3u) == 0 &&
+                                    (reinterpret_cast<uintptr_t>(src.x) & 15u) == 0);
+    if (pieces) {
+        const PieceGeom pg = piece_geom(d, n, k);
+        if (uint64_t(B) * pg.PP > 0xFFFFFFFFull) fail(PQG_EUNSUPPORTED, "kmeans: too many pieces");
+        uint32_t* piece_start = scratch<uint32_t>(ctx, uint64_t(B) * k);
+        PieceDesc* pieces_d = scratch<PieceDesc>(ctx, uint64_t(B) * pg.PP);
+        PieceStat* stats = scratch<PieceStat>(ctx, uint64_t(B) * pg.PP * d);
+        double* csum = scratch<double>(ctx, ncl * d);
+        int* cmax = scratch<int>(ctx, ncl * d);
+        int* cmin = scratch<int>(ctx, ncl * d);
+        launch(ctx, "kmeans_sum", pieces_setup_kernel, dim3(B), dim3(1024), 0, (const uint64_t*)bk.offsets, k,
+               pg.R, pg.PP, piece_start, pieces_d, has_empty, active, d, csum, cmax, cmin);
+        MemberRows mr;
+        mr.x = mx;
+        mr.ldx = mldx;
+        mr.col_stride = mcs;
+        mr.perm = bk.perm;
+        const uint64_t warps = uint64_t(B) * pg.PP;
+        launch(ctx, "kmeans_sum", mean_pieces_kernel, dim3(unsigned((warps + 7) / 8)), dim3(kMeanThreads), 0, mr,
+               n, d, k, B, (const PieceDesc*)pieces_d, stats, active, csum, cmax, cmin);
+        launch(ctx, "kmeans_sum", mean_finalize_kernel, dim3(unsigned((ncl + 7) / 8)), dim3(kMeanThreads), 0,
+               mr, n, d, k, B, (const uint64_t*)bk.offsets, (const uint32_t*)piece_start,
+               (const PieceStat*)stats, table, active, (const double*)csum, (const int*)cmax, (const int*)cmin);
+    } else {
+        PQG_CUDA(cudaMemsetAsync(has_empty, 0, sizeof(int) * B, ctx->stream));
+        // small clusters (batched chunk fits): a warp each; large ones: a CTA each
+        if (d <= 32 && n <= 128 * k) {
+            const uint64_t blocks = (ncl + kMeanThreads / 32 - 1) / (kMeanThreads / 32);
+            launch(ctx, "kmeans_sum", mean_exact_warp_kernel, dim3(unsigned(blocks)), dim3(kMeanThreads), 0,
+                   mx, mldx, mcs, n, d, k, ncl, (const uint64_t*)bk.offsets, (const uint32_t*)bk.perm, table,
+                   has_empty, active);
+        } else {
+            launch(ctx, "kmeans_sum", mean_exact_kernel, dim3(unsigned(ncl)), dim3(kMeanThreads), 0,
+                   mx, mldx, mcs, n, d, k, (const uint64_t*)bk.offsets, (const uint32_t*)bk.perm, table,
+                   has_empty, active);
+        }
     }
     launch(ctx, "reseed", reseed_kernel, dim3(B), dim3(1024), 0, src.x, src.ldx, src.col_stride, n,
            d, k, (const uint64_t*)bk.offsets, dist, table, (const int*)has_empty, active, nb);

@@ -331,8 +331,10 @@ constexpr int kFixMaxD = 512;
 // centroid whose fp32 distance is within the fp32 error of that minimum is
 // re-scored in the reference's fp64 arithmetic (kmeans.cpp:11-31), strict '<'
 // with the lowest index on ties.
-__global__ void __launch_bounds__(kFixThreads) fixup_kernel(NearestArgs a) {
+__global__ void __launch_bounds__(kFixThreads, 1) fixup_kernel(NearestArgs a, int tstaged) {
     __shared__ float xs[kFixMaxD];
+    extern __shared__ float tsm[];  // tstaged: the problem's table, rows padded to d+1 floats
+    uint32_t staged_b = 0xFFFFFFFFu;
     __shared__ float red_f[kFixThreads / 32];
     __shared__ double red_d[kFixThreads / 32];
     __shared__ uint32_t red_j[kFixThreads / 32];
@@ -349,13 +351,29 @@ __global__ void __launch_bounds__(kFixThreads) fixup_kernel(NearestArgs a) {
         __syncthreads();  // previous item's reductions are consumed
         if (staged)
             for (uint32_t t = threadIdx.x; t < d; t += blockDim.x) xs[t] = load_x(a.src, row, b, t);
+        if (tstaged && b != staged_b) {  // coalesced once per problem, not per distance
+            const uint64_t kd = a.k * d;
+            for (uint64_t e0 = threadIdx.x; e0 < kd; e0 += 8 * blockDim.x) {
+                float v[8];  // eight loads in flight per thread (clamped, unpredicated)
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = __ldg(tab + min64(e0 + u * blockDim.x, kd - 1));
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint64_t e = e0 + u * blockDim.x;
+                    if (e >= kd) break;
+                    const uint64_t j = e / d;
+                    tsm[j * (d + 1) + (e - j * d)] = v[u];
+                }
+            }
+            staged_b = b;
+        }
         __syncthreads();
         auto xval = [&](uint32_t t) { return staged ? xs[t] : load_x(a.src, row, b, t); };
+        auto cval = [&](uint64_t j, uint32_t t) { return tstaged ? tsm[j * (d + 1) + t] : __ldg(tab + j * d + t); };
         auto fdist = [&](uint64_t j) {
-            const float* c = tab + j * d;
             float v = 0.f;
             for (uint32_t t = 0; t < d; ++t) {
-                const float df = xval(t) - __ldg(c + t);
+                const float df = xval(t) - cval(j, t);
                 v = fmaf(df, df, v);
             }
             return v;
@@ -374,10 +392,9 @@ __global__ void __launch_bounds__(kFixThreads) fixup_kernel(NearestArgs a) {
         for (uint64_t j = threadIdx.x; j < a.k; j += blockDim.x) {
             const float v = fdist(j);
             if (!(v <= thr) && !(v != v)) continue;  // NaN candidates go to the exact path
-            const float* c = tab + j * d;
             double acc = 0.0;
             for (uint32_t t = 0; t < d; ++t) {
-                const double diff = __dsub_rn((double)xval(t), (double)__ldg(c + t));
+                const double diff = __dsub_rn((double)xval(t), (double)cval(j, t));
                 acc = __dadd_rn(acc, __dmul_rn(diff, diff));
             }
             if (acc < best || (acc == best && uint32_t(j) < bj)) { best = acc; bj = uint32_t(j); }
@@ -402,7 +419,11 @@ __global__ void __launch_bounds__(kFixThreads) fixup_kernel(NearestArgs a) {
             // nearest_in_table starts from (0, d_0) and only a strictly smaller
             // distance replaces it (kmeans.cpp:20-31): a NaN d_0 is never replaced
             // and NaN distances never win
-            const double d0 = exact_dist(a, row, b, tab);
+            double d0 = 0.0;  // exact_dist to codeword 0, from the staged copies
+            for (uint32_t t = 0; t < d; ++t) {
+                const double diff = __dsub_rn((double)xval(t), (double)cval(0, t));
+                d0 = __dadd_rn(d0, __dmul_rn(diff, diff));
+            }
             if (bj == 0xFFFFFFFFu || d0 != d0) {
                 bj = 0;
                 best = d0;
@@ -493,7 +514,11 @@ void nearest(pqg_ctx* ctx, NearestArgs a) {
     if (!force_fp32 && umma_screen_supported(a)) umma_screen(ctx, a);
     else if (!force_fp32 && umma_big_supported(a)) umma_big(ctx, a);
     else dispatch<false>(ctx, a);
-    launch(ctx, "fixup", fixup_kernel, dim3(ctx->num_sms * 4), dim3(kFixThreads), 0, a);
+    // stage the table in shared memory when it fits (PQ tables: <= 33 KB)
+    const size_t tbytes = size_t(a.k) * (a.d + 1) * sizeof(float);
+    const int tstaged = a.d <= uint32_t(kFixMaxD) && tbytes <= 48 * 1024 ? 1 : 0;
+    launch(ctx, "fixup", fixup_kernel, dim3(ctx->num_sms * 8), dim3(kFixThreads), tstaged ? tbytes : 0, a,
+           tstaged);
     if (std::getenv("PQG_FLAG_STATS")) {  // diagnostics: rows sent to the exact fixup
         unsigned long long h = 0;
         PQG_CUDA(cudaMemcpyAsync(&h, a.flag_count, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));

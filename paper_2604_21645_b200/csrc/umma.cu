@@ -146,6 +146,61 @@ __device__ __forceinline__ float tc_error_bound(float S, int K) {
     return 2.f * (2.f * n_mma + 8.f) * kU * S + 1e-30f;
 }
 
+// B operand rows j = [-2c_j, ||c_j||^2, 1, 0...] split hi/lo (rows j >= k are
+// padding that never wins).  A thread stages whole codewords, two at a time,
+// with their loads issued together (vector loads when the rows are 16-byte
+// aligned): a short fit re-stages every launch, so the staging latency counts.
+template <int DS, int KA, bool PAD>
+__device__ __forceinline__ void stage_codewords(uint8_t* Bh, uint8_t* Bl, const float* tab,
+                                                const float* cnorm, uint64_t k, uint32_t d,
+                                                uint32_t n_pad, uint32_t tid, uint32_t nthreads) {
+    constexpr uint32_t SBO = (KA / 4) * 128;
+    const bool vec = !PAD && (DS % 4) == 0 && (reinterpret_cast<uintptr_t>(tab) & 15u) == 0;
+    for (uint32_t j0 = 0; j0 < n_pad; j0 += 2 * nthreads) {
+        float v[2][KA];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const uint32_t j = j0 + u * nthreads + tid;
+#pragma unroll
+            for (int t = 0; t < KA; ++t) v[u][t] = 0.f;
+            if (j < k) {
+                const float* c = tab + uint64_t(j) * d;
+                if (vec) {
+#pragma unroll
+                    for (int t = 0; t < DS; t += 4) {
+                        const float4 q = __ldg(reinterpret_cast<const float4*>(c + t));
+                        v[u][t] = -2.f * q.x; v[u][t + 1] = -2.f * q.y;
+                        v[u][t + 2] = -2.f * q.z; v[u][t + 3] = -2.f * q.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int t = 0; t < DS; ++t) v[u][t] = (!PAD || uint32_t(t) < d) ? -2.f * __ldg(c + t) : 0.f;
+                }
+                v[u][DS] = __ldg(cnorm + j);
+                v[u][DS + 1] = 1.f;
+            } else {
+                v[u][DS] = 3.0e38f;  // padded codeword: never the minimum
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const uint32_t j = j0 + u * nthreads + tid;
+            if (j >= n_pad) continue;
+#pragma unroll
+            for (int t = 0; t < KA; t += 4) {
+                float h[4], l[4];
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    h[w] = tf32_hi(v[u][t + w]);
+                    l[w] = tf32_hi(v[u][t + w] - h[w]);
+                }
+                *reinterpret_cast<float4*>(Bh + il_off(j, t, SBO)) = make_float4(h[0], h[1], h[2], h[3]);
+                *reinterpret_cast<float4*>(Bl + il_off(j, t, SBO)) = make_float4(l[0], l[1], l[2], l[3]);
+            }
+        }
+    }
+}
+
 template <int DS, int KA, bool PAD>
 __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, uint32_t n_pad,
                                                                uint32_t tmem_cols, uint32_t m32,
@@ -183,20 +238,7 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
     }
 
     // ---- B operand: [-2c, ||c||^2, 1, 0...] split hi/lo, rows j >= k padded
-    for (uint32_t e = tid; e < n_pad * KA; e += kRows) {
-        const uint32_t j = e / KA, t = e - j * KA;
-        float v = 0.f;
-        if (j < k) {
-            if (t < d) v = -2.f * __ldg(tab + uint64_t(j) * d + t);
-            else if (t == DS) v = __ldg(a.cnorm + uint64_t(b) * k + j);
-            else if (t == DS + 1) v = 1.f;
-        } else if (t == DS) {
-            v = 3.0e38f;  // padded codeword: never the minimum
-        }
-        const float h = tf32_hi(v);
-        *reinterpret_cast<float*>(Bh + il_off(j, t, SBO)) = h;
-        *reinterpret_cast<float*>(Bl + il_off(j, t, SBO)) = tf32_hi(v - h);
-    }
+    stage_codewords<DS, KA, PAD>(Bh, Bl, tab, a.cnorm + uint64_t(b) * k, k, d, n_pad, tid, kRows);
     fence_async_smem();
     fence_before();
     __syncthreads();
@@ -447,20 +489,7 @@ __global__ void __launch_bounds__(NW * 32, 1) umma_screen2_kernel(NearestArgs a,
         mbar_init(&mbar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    for (uint32_t e = tid; e < n_pad * KA; e += blockDim.x) {
-        const uint32_t j = e / KA, t = e - j * KA;
-        float v = 0.f;
-        if (j < k) {
-            if (t < d) v = -2.f * __ldg(tab + uint64_t(j) * d + t);
-            else if (t == DS) v = __ldg(a.cnorm + uint64_t(b) * k + j);
-            else if (t == DS + 1) v = 1.f;
-        } else if (t == DS) {
-            v = 3.0e38f;
-        }
-        const float h = tf32_hi(v);
-        *reinterpret_cast<float*>(Bh + il_off(j, t, SBO)) = h;
-        *reinterpret_cast<float*>(Bl + il_off(j, t, SBO)) = tf32_hi(v - h);
-    }
+    stage_codewords<DS, KA, PAD>(Bh, Bl, tab, a.cnorm + uint64_t(b) * k, k, d, n_pad, tid, blockDim.x);
     fence_async_smem();
     fence_before();
     __syncthreads();

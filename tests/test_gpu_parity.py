@@ -149,6 +149,39 @@ def test_kmeans_sum_order_paths(pq, orc, scale):
     assert np.array_equal(bits(t), bits(ot))
 
 
+@pytest.mark.parametrize("copy", ["1", "0"])
+@pytest.mark.parametrize("pattern", ["tiny_sparse", "tiny_dense", "wide", "cancel", "nan"])
+@pytest.mark.parametrize("d", [8, 6, 16])
+def test_kmeans_large_cluster_sums(pq, orc, monkeypatch, d, pattern, copy):
+    """Clusters of thousands of members (one CTA each): the chunked row-order
+    fallback -- exact chunks added in parallel, a chunk that can round walked
+    serially -- must reproduce the reference's sequential fp64 sums bit for
+    bit, through the bucketed row copy and through the permutation."""
+    monkeypatch.setenv("PQG_KM_COPY", copy)
+    rng = np.random.default_rng(d * 100 + len(pattern))
+    n = 20000
+    pts = (orc.random_matrix(n, d, 41 + d) * 10.0).astype(np.float32)
+    if pattern == "tiny_sparse":   # a few tiny values anywhere (one chunk each)
+        pts[rng.choice(n, 12, replace=False), 0] = np.float32(3e-30)
+        pts[rng.choice(n, 5, replace=False), 1] = np.float32(-7e-25)
+    elif pattern == "tiny_dense":  # tiny values in many chunks of a cluster
+        pts[rng.random(n) < 0.01, 1] *= np.float32(1e-20)
+    elif pattern == "wide":        # every magnitude from 1e-20 to 1e5
+        pts[:, 0] *= (np.float32(10.0) ** rng.integers(-20, 6, size=n)).astype(np.float32)
+    elif pattern == "cancel":      # large +/- values that cancel
+        pts[:, d - 1] += np.where(rng.random(n) < 0.5, 1e7, -1e7).astype(np.float32)
+    else:                          # a NaN and an inf coordinate
+        pts[123, 0] = np.nan
+        pts[4567, 1] = np.inf
+    a = pq.kmeans_fit(pts, 8, 6, 3, 0.0)
+    b = orc.kmeans_fit(pts, 8, 6, 3, 0.0)
+    ca, cb = np.asarray(a.centroids), np.asarray(b["centroids"])
+    nan = np.isnan(ca)  # NaN payloads are platform-specific: positions must agree
+    assert np.array_equal(nan, np.isnan(cb))
+    assert np.array_equal(bits(np.where(nan, 0, ca)), bits(np.where(nan, 0, cb)))
+    assert np.array_equal(a.assignments, b["assignments"])
+
+
 def test_kmeans_validation(pq, orc):
     pts = orc.random_matrix(5, 2, 1)
     with pytest.raises(ValueError):
