@@ -336,8 +336,9 @@ static KMeansOut run_kmeans(pqg_ctx* ctx, const float* x, uint64_t n, uint64_t l
     prep.k = k;
     prep.cmax = cmax;
     const bool big = B == 1 && umma_big_prepare_rows(ctx, prep);
+    PQG_CUDA(cudaMemsetAsync(st.iters, 0, sizeof(uint32_t) * B, ctx->stream));
     const auto iter_mark = ctx->arena.mark();
-    for (uint32_t it = 1; it <= max_iters; ++it) {
+    auto body = [&](uint32_t it, bool update) {
         ctx->arena.reset_to(iter_mark);  // per-iteration scratch is reused
         table_norms(ctx, table, B, k, d, cnorm, cmax);
         NearestArgs a;
@@ -362,8 +363,50 @@ static KMeansOut run_kmeans(pqg_ctx* ctx, const float* x, uint64_t n, uint64_t l
         nearest(ctx, a);
         kmeans_pad_keys(ctx, assign, n, B, k, d_nb, max_pad);
         kmeans_inertia_and_stop(ctx, dist, n, B, it, max_iters, tol, st, d_nb);
-        if (it == max_iters) break;
-        kmeans_update(ctx, src, n, B, d, table, k, assign, dist, st.active, d_nb);
+        if (update) kmeans_update(ctx, src, n, B, d, table, k, assign, dist, st.active, d_nb);
+    };
+    // Iterations 2 .. max_iters-1 are identical launch sequences (the pass
+    // number lives on the device, inactive problems are skipped by the
+    // kernels): captured once into a CUDA graph and replayed, so the ~15
+    // small launches of an iteration go to the GPU as one.  Iteration 1 runs
+    // eagerly first (it sizes the scratch the graph then reuses).
+    const char* ge = std::getenv("PQG_KM_GRAPH");
+    const bool use_graph = !ctx->profiling && !(ge && ge[0] == '0') && !std::getenv("PQG_FLAG_STATS") &&
+                           max_iters >= 3;
+    cudaGraphExec_t gexec = nullptr;
+    uint64_t body_launches = 0;
+    try {
+        for (uint32_t it = 1; it <= max_iters; ++it) {
+            const bool last = it == max_iters;
+            if (use_graph && it >= 2 && !last) {
+                if (!gexec) {
+                    const uint64_t l0 = ctx->launches;
+                    PQG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
+                    try {
+                        body(it, true);
+                    } catch (...) {
+                        cudaGraph_t g = nullptr;
+                        cudaStreamEndCapture(ctx->stream, &g);
+                        if (g) cudaGraphDestroy(g);
+                        throw;
+                    }
+                    cudaGraph_t g = nullptr;
+                    PQG_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+                    const cudaError_t ie = cudaGraphInstantiate(&gexec, g, 0);
+                    cudaGraphDestroy(g);
+                    if (ie != cudaSuccess) fail(PQG_ECUDA, std::string("kmeans graph: ") + cudaGetErrorString(ie));
+                    body_launches = ctx->launches - l0;
+                    ctx->launches = l0;
+                }
+                PQG_CUDA(cudaGraphLaunch(gexec, ctx->stream));
+                ctx->launches += body_launches;
+            } else {
+                body(it, !last);
+            }
+        }
+    } catch (...) {
+        if (gexec) cudaGraphExecDestroy(gexec);
+        throw;
     }
     KMeansOut o;
     o.inertia.resize(B);
@@ -374,6 +417,7 @@ static KMeansOut run_kmeans(pqg_ctx* ctx, const float* x, uint64_t n, uint64_t l
     PQG_CUDA(cudaMemcpyAsync(o.per_iter.data(), st.per_iter, sizeof(double) * B * max_iters,
                              cudaMemcpyDeviceToHost, ctx->stream));
     sync(ctx);
+    if (gexec) cudaGraphExecDestroy(gexec);
     return o;
 }
 
