@@ -26,7 +26,10 @@ struct BucketGeom {
 };
 BucketGeom bucket_geom(uint64_t n, uint64_t k) {
     BucketGeom g;
-    g.W = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(8, (96 * 1024) / (4 * std::max<uint64_t>(k, 1)))));
+    // W a power of two (T / W rows per warp must tile T exactly)
+    const uint64_t wmax = std::max<uint64_t>(1, std::min<uint64_t>(8, (96 * 1024) / (4 * std::max<uint64_t>(k, 1))));
+    g.W = 1;
+    while (uint64_t(g.W) * 2 <= wmax) g.W *= 2;
     g.T = k <= 1024 ? 1024u : 4096u;  // multiples of 32 * W for every W <= 8
     g.ntiles = uint32_t((n + g.T - 1) / g.T);
     return g;

@@ -182,6 +182,17 @@ def test_kmeans_large_cluster_sums(pq, orc, monkeypatch, d, pattern, copy):
     assert np.array_equal(a.assignments, b["assignments"])
 
 
+@pytest.mark.parametrize("k", [3100, 4096, 5000])
+def test_kmeans_many_clusters(pq, orc, k):
+    """k > 3072: the bucketing runs fewer warps per tile (per-warp key
+    counters in shared memory); every row must still land in its list."""
+    pts = orc.random_matrix(12000, 4, 77 + k)
+    a = pq.kmeans_fit(pts, k, 3, 5, 0.0)
+    b = orc.kmeans_fit(pts, k, 3, 5, 0.0)
+    assert np.array_equal(bits(a.centroids), bits(b["centroids"]))
+    assert np.array_equal(a.assignments, b["assignments"])
+
+
 def test_kmeans_validation(pq, orc):
     pts = orc.random_matrix(5, 2, 1)
     with pytest.raises(ValueError):
@@ -565,6 +576,20 @@ def test_ivf_large_nlist_both_screens(pq, orc, mix, screen):
         assert np.array_equal(probes[i], orc.probe_order(coarse, q[i], 20))
         ri, rd = orc.ivf_query(cb.tables, coarse, o_off, o_ids, o_codes, q[i], 10, 20)
         assert np.array_equal(gi[i, : gc[i]], ri) and np.array_equal(bits(gd[i, : gc[i]]), bits(rd))
+
+
+def test_ivf_build_nlist_over_3072(pq, orc, mix):
+    """Posting lists with nlist = 4500 (the bucketing's few-warps-per-tile
+    geometry) equal the reference's, list by list and in insertion order."""
+    x = mix(30000, 16, 64, seed=8)
+    cb = pq.pq_fit(x, 4, 16, 4, 2)
+    codes = pq.pq_encode(cb, x)
+    coarse = np.ascontiguousarray(x[::6][:4500])
+    ids = np.arange(30000, dtype=np.uint64) * 3 + 1
+    index = pq.ivf_build_with_centroids(cb, codes, ids, coarse)
+    off, lid, lcodes, _, _ = index.export()
+    o_off, o_ids, o_codes = orc.ivf_build_with_centroids(codes.bytes, ids, cb.tables, coarse)
+    assert np.array_equal(off, o_off) and np.array_equal(lid, o_ids) and np.array_equal(lcodes, o_codes)
 
 
 @pytest.mark.parametrize("M,ks", [(8, 256), (16, 64), (4, 16)])
