@@ -434,16 +434,20 @@ __global__ void __launch_bounds__(kFixThreads, 1) fixup_kernel(NearestArgs a, in
     }
 }
 
-__global__ void norms_kernel(const float* table, uint32_t B, uint64_t k, uint32_t d,
+__global__ void __launch_bounds__(256, 1) norms_kernel(const float* table, uint32_t B, uint64_t k, uint32_t d,
                              float* cnorm, unsigned* cmax_bits) {
     const uint64_t total = uint64_t(B) * k;
     for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
          e += uint64_t(gridDim.x) * blockDim.x) {
         const float* c = table + e * d;
         double s = 0.0;
-        for (uint32_t t = 0; t < d; ++t) {
-            const double v = c[t];
-            s = __dadd_rn(s, __dmul_rn(v, v));
+        for (uint32_t t0 = 0; t0 < d; t0 += 8) {
+            float v[8];  // the row's loads issued together (clamped, unpredicated)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldg(c + min(t0 + u, d - 1));
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (t0 + u < d) s = __dadd_rn(s, __dmul_rn((double)v[u], (double)v[u]));
         }
         cnorm[e] = __double2float_rn(s);
         atomicMax(cmax_bits + e / k, __float_as_uint(__double2float_ru(sqrt(s))));

@@ -724,8 +724,17 @@ void launch_umma(pqg_ctx* ctx, const NearestArgs& a) {
     // extra CTAs, whose short tiles are latency-bound); PQG_UMMA_CTAS overrides
     uint64_t per_sm = std::max<uint64_t>(1, std::min<uint64_t>(std::min<uint64_t>(4u, 512u / cols), smem_lim));
     if (const char* ce = std::getenv("PQG_UMMA_CTAS")) per_sm = std::max(1, std::atoi(ce));
-    uint64_t per_b = std::max<uint64_t>(1, (uint64_t(ctx->num_sms) * per_sm + a.B - 1) / a.B);
-    per_b = std::min<uint64_t>(per_b, ntiles);
+    // CTAs per problem: minimise (waves of CTAs) x (tiles per CTA) -- with
+    // many problems a partial second wave costs a whole extra tile run
+    const uint64_t slots = uint64_t(ctx->num_sms) * per_sm;
+    uint64_t per_b = 1, best = ~0ull;
+    for (uint64_t p = 1; p <= std::min<uint64_t>(ntiles, std::max<uint64_t>(1, (2 * slots + a.B - 1) / a.B)); ++p) {
+        const uint64_t cost = ((p * a.B + slots - 1) / slots) * ((ntiles + p - 1) / p);
+        if (cost < best) {
+            best = cost;
+            per_b = p;
+        }
+    }
     launch(ctx, "nearest_tc", kern, dim3(unsigned(per_b * a.B)), dim3(kRows), smem, a, n_pad, cols, 32u, n_mma);
 }
 
