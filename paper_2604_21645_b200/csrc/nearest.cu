@@ -434,6 +434,92 @@ __global__ void __launch_bounds__(kFixThreads, 1) fixup_kernel(NearestArgs a, in
     }
 }
 
+// Flagged pairs of the PQ subspaces (d = DS in {4, 8, 16, 32}, rows of x and
+// the table 16-byte aligned, no decoded-row source): one warp per pair, the
+// row in registers, lane j scoring codewords j, j+32, ... from the (L1-
+// resident) table with float4 loads; the same fp32 pass / threshold / fp64
+// re-score / (0, d_0) rule as fixup_kernel.  Pairs are taken in flag order,
+// a warp per pair across the whole GPU -- no per-pair block barriers.
+template <int DS>
+__global__ void __launch_bounds__(256) fixup_warp_kernel(NearestArgs a) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    const unsigned long long cnt = *a.flag_count;
+    const uint64_t k = a.k;
+    constexpr float eps = float(DS + 2) * kU * 1.01f;
+    for (uint64_t f = gw; f < cnt; f += nw) {
+        const uint64_t item = __ldcg(a.flags + f);
+        const uint32_t b = uint32_t(item >> 40);
+        const uint64_t row = item & ((uint64_t(1) << 40) - 1);
+        const float* tab = a.table + (uint64_t)b * k * DS;
+        float x[DS];
+        const float4* xp = reinterpret_cast<const float4*>(a.src.x + row * a.src.ldx + (uint64_t)b * a.src.col_stride);
+#pragma unroll
+        for (int t = 0; t < DS; t += 4) {
+            const float4 v = __ldg(xp + t / 4);
+            x[t] = v.x; x[t + 1] = v.y; x[t + 2] = v.z; x[t + 3] = v.w;
+        }
+        auto fdist = [&](uint64_t j) {
+            const float4* c = reinterpret_cast<const float4*>(tab + j * DS);
+            float c4[DS];
+#pragma unroll
+            for (int t = 0; t < DS; t += 4) {
+                const float4 v = __ldg(c + t / 4);
+                c4[t] = v.x; c4[t + 1] = v.y; c4[t + 2] = v.z; c4[t + 3] = v.w;
+            }
+            float v = 0.f;
+#pragma unroll
+            for (int t = 0; t < DS; ++t) {
+                const float df = x[t] - c4[t];
+                v = fmaf(df, df, v);
+            }
+            return v;
+        };
+        float vmin = __int_as_float(0x7f800000);
+        for (uint64_t j = lane; j < k; j += 32) vmin = fminf(vmin, fdist(j));
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
+        const float thr = vmin * ((1.f + eps) / (1.f - eps)) * (1.f + 4.f * kU) + 1e-37f;
+        double best = __longlong_as_double(0x7ff0000000000000LL);
+        uint32_t bj = 0xFFFFFFFFu;
+        for (uint64_t j = lane; j < k; j += 32) {
+            const float v = fdist(j);
+            if (!(v <= thr) && !(v != v)) continue;  // NaN candidates go to the exact path
+            const float* c = tab + j * DS;
+            double acc = 0.0;
+#pragma unroll
+            for (int t = 0; t < DS; ++t) {
+                const double diff = __dsub_rn((double)x[t], (double)__ldg(c + t));
+                acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+            }
+            if (acc < best || (acc == best && uint32_t(j) < bj)) { best = acc; bj = uint32_t(j); }
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const uint32_t oj = __shfl_xor_sync(0xffffffffu, bj, o);
+            if (ob < best || (ob == best && oj < bj)) { best = ob; bj = oj; }
+        }
+        if (lane == 0) {
+            // nearest_in_table starts from (0, d_0), strict '<' (kmeans.cpp:20-31):
+            // a NaN d_0 is never replaced and NaN distances never win
+            double d0 = 0.0;
+#pragma unroll
+            for (int t = 0; t < DS; ++t) {
+                const double diff = __dsub_rn((double)x[t], (double)__ldg(tab + t));
+                d0 = __dadd_rn(d0, __dmul_rn(diff, diff));
+            }
+            if (bj == 0xFFFFFFFFu || d0 != d0) {
+                bj = 0;
+                best = d0;
+            }
+            store_index(a, row, b, bj);
+            if (a.out_dist) a.out_dist[(uint64_t)b * a.n + row] = best;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256, 1) norms_kernel(const float* table, uint32_t B, uint64_t k, uint32_t d,
                              float* cnorm, unsigned* cmax_bits) {
     const uint64_t total = uint64_t(B) * k;
@@ -521,8 +607,17 @@ void nearest(pqg_ctx* ctx, NearestArgs a) {
     // stage the table in shared memory when it fits (PQ tables: <= 33 KB)
     const size_t tbytes = size_t(a.k) * (a.d + 1) * sizeof(float);
     const int tstaged = a.d <= uint32_t(kFixMaxD) && tbytes <= 48 * 1024 ? 1 : 0;
-    launch(ctx, "fixup", fixup_kernel, dim3(ctx->num_sms * 8), dim3(kFixThreads), tstaged ? tbytes : 0, a,
-           tstaged);
+    const bool wvec = !a.src.codes && ((a.src.ldx | a.src.col_stride) & 3u) == 0 &&
+                      (reinterpret_cast<uintptr_t>(a.src.x) & 15u) == 0 &&
+                      (reinterpret_cast<uintptr_t>(a.table) & 15u) == 0;
+    const dim3 wgrid(ctx->num_sms * 16);
+    if (wvec && a.d == 16) launch(ctx, "fixup", fixup_warp_kernel<16>, wgrid, dim3(256), 0, a);
+    else if (wvec && a.d == 8) launch(ctx, "fixup", fixup_warp_kernel<8>, wgrid, dim3(256), 0, a);
+    else if (wvec && a.d == 4) launch(ctx, "fixup", fixup_warp_kernel<4>, wgrid, dim3(256), 0, a);
+    else if (wvec && a.d == 32) launch(ctx, "fixup", fixup_warp_kernel<32>, wgrid, dim3(256), 0, a);
+    else
+        launch(ctx, "fixup", fixup_kernel, dim3(ctx->num_sms * 8), dim3(kFixThreads), tstaged ? tbytes : 0, a,
+               tstaged);
     if (std::getenv("PQG_FLAG_STATS")) {  // diagnostics: rows sent to the exact fixup
         unsigned long long h = 0;
         PQG_CUDA(cudaMemcpyAsync(&h, a.flag_count, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
