@@ -520,6 +520,90 @@ __global__ void __launch_bounds__(256) fixup_warp_kernel(NearestArgs a) {
     }
 }
 
+// Small tables (Ks <= 16 and Ds in {4, 8, 32}: the narrow-codebook encodes
+// and fits): thread per row, the problem's subspaces in one pass, the whole
+// codebook in shared memory read as broadcast float4s.  Same screened value
+// and bound as nearest_kernel's FP32 screen: acc_j = (C_r + ||c_j||^2) +
+// sum_t (-2x_t) c_jt (fma chain), E = 2 (Ds+4) u q^2; a row whose runner-up
+// is within 2.05 E of its best goes to the exact fixup.  Measured r1 (1M x
+// 128, encode): Ks=16 M=4 2.8 -> 3.6, M=16 2.4 -> 2.7, M=32 1.5 -> 2.0 G
+// vectors/s against the tensor-core screen, which re-stages every (row,
+// subspace) as a 128-row MMA tile; slower at Ds=16 and at Ks=64.
+constexpr int kSmallThreads = 128;
+template <int DS>
+__global__ void __launch_bounds__(kSmallThreads) small_table_kernel(NearestArgs a) {
+    extern __shared__ __align__(16) float st[];  // [B][k][DS] then cnorm [B][k]
+    const uint32_t B = a.B;
+    const uint64_t k = a.k;
+    float* cn_s = st + uint64_t(B) * k * DS;
+    for (uint64_t e = threadIdx.x; e < uint64_t(B) * k * DS; e += blockDim.x) st[e] = __ldg(a.table + e);
+    for (uint64_t e = threadIdx.x; e < uint64_t(B) * k; e += blockDim.x) cn_s[e] = __ldg(a.cnorm + e);
+    __syncthreads();
+    constexpr float kE = 2.f * float(DS + 4) * kU;
+    for (uint64_t row = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; row < a.n;
+         row += uint64_t(gridDim.x) * blockDim.x) {
+        for (uint32_t b = 0; b < B; ++b) {
+            if (a.active && !a.active[b]) continue;
+            float x[DS];
+            const float4* xp = reinterpret_cast<const float4*>(a.src.x + row * a.src.ldx + uint64_t(b) * a.src.col_stride);
+#pragma unroll
+            for (int t = 0; t < DS; t += 4) {
+                const float4 v = __ldg(xp + t / 4);
+                x[t] = -2.f * v.x; x[t + 1] = -2.f * v.y; x[t + 2] = -2.f * v.z; x[t + 3] = -2.f * v.w;
+            }
+            float s = 0.f;
+#pragma unroll
+            for (int t = 0; t < DS; ++t) s = fmaf(x[t], x[t], s);
+            const float nx = 0.25f * s;
+            const float q = sqrtf(nx) * (1.f + 1e-6f) + a.cmax[b];
+            const float E = kE * q * q + 1e-30f;
+            const float C = nx * (1.f + 2.f * float(DS + 2) * kU) + 2.f * E;
+            const float* tb = st + uint64_t(b) * k * DS;
+            const float* cnb = cn_s + uint64_t(b) * k;
+            float b1 = __int_as_float(0x7f800000), b2 = b1;
+            uint32_t i1 = 0;
+#pragma unroll 4
+            for (uint32_t j = 0; j < k; ++j) {
+                float acc = cnb[j] + C;
+                const float4* c4 = reinterpret_cast<const float4*>(tb + uint64_t(j) * DS);
+#pragma unroll
+                for (int t = 0; t < DS; t += 4) {
+                    const float4 c = c4[t / 4];
+                    acc = fmaf(x[t], c.x, acc);
+                    acc = fmaf(x[t + 1], c.y, acc);
+                    acc = fmaf(x[t + 2], c.z, acc);
+                    acc = fmaf(x[t + 3], c.w, acc);
+                }
+                if (acc < b1) {  // strict: the lowest column keeps equal values
+                    b2 = b1;
+                    b1 = acc;
+                    i1 = j;
+                } else {
+                    b2 = fminf(b2, acc);
+                }
+            }
+            const bool unique = isfinite(E) && b1 < __int_as_float(0x7f800000) &&
+                                (!(b2 < __int_as_float(0x7f800000)) || b2 - b1 > 2.05f * E);
+            if (unique) {
+                store_index(a, row, b, i1);
+                if (a.out_dist) {  // -0.5 * (-2x) == x exactly
+                    const float* c = tb + uint64_t(i1) * DS;
+                    double acc = 0.0;
+#pragma unroll
+                    for (int t = 0; t < DS; ++t) {
+                        const double diff = __dsub_rn((double)(-0.5f * x[t]), (double)c[t]);
+                        acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+                    }
+                    a.out_dist[uint64_t(b) * a.n + row] = acc;
+                }
+            } else {
+                const unsigned long long slot = atomicAdd(a.flag_count, 1ull);
+                a.flags[slot] = (uint64_t(b) << 40) | row;
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256, 1) norms_kernel(const float* table, uint32_t B, uint64_t k, uint32_t d,
                              float* cnorm, unsigned* cmax_bits) {
     const uint64_t total = uint64_t(B) * k;
@@ -601,7 +685,26 @@ void nearest(pqg_ctx* ctx, NearestArgs a) {
     // screen selection: tcgen05 for PQ subspaces unless PQG_SCREEN=fp32
     const char* mode = std::getenv("PQG_SCREEN");
     const bool force_fp32 = mode && std::strcmp(mode, "fp32") == 0;
-    if (!force_fp32 && umma_screen_supported(a)) umma_screen(ctx, a);
+    // narrow codebooks: the row-wise small-table kernel (PQG_SCREEN=tc keeps
+    // the tensor-core screen)
+    const bool small_tab = !force_fp32 && !(mode && std::strcmp(mode, "tc") == 0) && a.k <= 16 &&
+                           (a.d == 4 || a.d == 8 || a.d == 32) && !a.src.codes && !a.sse_part &&
+                           ((a.src.ldx | a.src.col_stride) & 3u) == 0 &&
+                           (reinterpret_cast<uintptr_t>(a.src.x) & 15u) == 0 &&
+                           (reinterpret_cast<uintptr_t>(a.table) & 15u) == 0 &&
+                           uint64_t(a.B) * a.k * (a.d + 1) * sizeof(float) <= 96 * 1024;
+    if (small_tab) {
+        const size_t smem = size_t(a.B) * a.k * (a.d + 1) * sizeof(float);
+        const unsigned grid = unsigned(std::min<uint64_t>((a.n + kSmallThreads - 1) / kSmallThreads,
+                                                          uint64_t(ctx->num_sms) * 8));
+        auto go = [&](auto kern) {
+            set_smem(kern, smem);
+            launch(ctx, "nearest_small", kern, dim3(grid), dim3(kSmallThreads), smem, a);
+        };
+        if (a.d == 4) go(small_table_kernel<4>);
+        else if (a.d == 8) go(small_table_kernel<8>);
+        else go(small_table_kernel<32>);
+    } else if (!force_fp32 && umma_screen_supported(a)) umma_screen(ctx, a);
     else if (!force_fp32 && umma_big_supported(a)) umma_big(ctx, a);
     else dispatch<false>(ctx, a);
     // stage the table in shared memory when it fits (PQ tables: <= 33 KB)

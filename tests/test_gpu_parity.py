@@ -55,7 +55,7 @@ def test_nearest_ties_lowest_index(pq, orc):
     assert np.array_equal(bits(gd), bits(od))
 
 
-@pytest.mark.parametrize("d,k", [(8, 64), (16, 256), (5, 40), (128, 1024)])
+@pytest.mark.parametrize("d,k", [(8, 64), (16, 256), (5, 40), (128, 1024), (8, 16), (32, 12), (4, 7)])
 def test_nearest_nonfinite(pq, orc, d, k):
     """nearest_in_table's NaN rule (kmeans.cpp:20-31): the search starts from
     (0, d_0) and only a strictly smaller distance replaces it, so a NaN d_0
@@ -239,7 +239,7 @@ def test_pq_wide_codes(pq, golden):
     assert dec.shape == golden["pq_wide/data"].shape
 
 
-@pytest.mark.parametrize("M,ks,ds", [(4, 16, 2), (8, 256, 16), (16, 256, 8), (32, 16, 4),
+@pytest.mark.parametrize("M,ks,ds", [(4, 16, 2), (8, 256, 16), (16, 256, 8), (32, 16, 4), (16, 16, 8), (4, 9, 32),
                                      (4, 64, 32), (3, 7, 5), (2, 1, 3), (12, 256, 8),
                                      (64, 256, 2), (128, 16, 1), (8, 100, 6), (6, 200, 12),
                                      (5, 256, 24)])

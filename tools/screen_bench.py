@@ -35,7 +35,7 @@ def main():
         os.environ["PQG_SCREEN"] = "fp32"
         L.check(lib.pqg_pq_fit(ctx.h, vp(train.data_ptr()), 100_000, D, M, ks, 3, 7, vp(t.data_ptr()), None, None))
         res = {}
-        modes = ("fp32", "tc1", "tc1s", "tc8", "tc16", "tcdef")
+        modes = ("fp32", "tc1", "tc1s", "tc8", "tc16", "tcdef", "auto")
         for mode in modes:
             # tc1: 1-pass v1; tc1s: v1 in two 128-codeword passes; tc8/tc16: the
             # pipelined kernel with 8/16 warps; tcdef: the library's own choice
@@ -43,8 +43,10 @@ def main():
             os.environ["PQG_UMMA"] = {"tc1": "1", "tc1s": "1", "tc8": "2", "tc16": "2"}.get(mode, "0")
             os.environ["PQG_UMMA_WARPS"] = "16" if mode == "tc16" else "8"
             os.environ["PQG_UMMA_SPLIT"] = "1" if mode == "tc1s" else "0"
-            if mode == "tcdef":
+            if mode in ("tcdef", "auto"):
                 del os.environ["PQG_UMMA_SPLIT"]
+            if mode == "auto":  # the library's own choice of screen
+                del os.environ["PQG_SCREEN"]
             codes = torch.empty((N, M), dtype=torch.uint8, device="cuda")
             enc = lambda: L.check(lib.pqg_pq_encode(ctx.h, vp(x.data_ptr()), N, M, ks, D // M,
                                                      vp(t.data_ptr()), vp(codes.data_ptr())))
@@ -61,6 +63,8 @@ def main():
             ms = a.elapsed_time(b) / 10
             kname = "nearest" if mode == "fp32" else "nearest_tc"
             n1, k1 = ctx.profile_read(kname)
+            if mode == "auto" and n1 == 0:
+                n1, k1 = ctx.profile_read("nearest_small")
             n2, k2 = ctx.profile_read("fixup")
             ctx.profile(False)
             res[mode] = codes.cpu().numpy()
