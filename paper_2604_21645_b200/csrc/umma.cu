@@ -116,6 +116,18 @@ __device__ __forceinline__ uint32_t chunk_key(uint32_t r, uint32_t j, uint32_t m
 }
 
 // byte offset of element (row, k) of a K-major interleaved operand
+// After tcgen05.wait::ld: re-define the loaded registers so no consumer is
+// scheduled above the wait (the asm outputs of tcgen05.ld are not ready
+// until then).
+__device__ __forceinline__ void tmem_regs_ready(uint32_t (&r)[32]) {
+    asm volatile(""
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
+                   "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]),
+                   "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]),
+                   "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]),
+                   "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31]));
+}
+
 __device__ __forceinline__ uint32_t il_off(uint32_t row, uint32_t k, uint32_t sbo) {
     return (row >> 3) * sbo + (k >> 2) * 128u + (row & 7u) * 16u + (k & 3u) * 4u;
 }
@@ -201,7 +213,7 @@ __device__ __forceinline__ void stage_codewords(uint8_t* Bh, uint8_t* Bl, const 
     }
 }
 
-template <int DS, int KA, bool PAD>
+template <int DS, int KA, bool PAD, bool DB>
 __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, uint32_t n_pad,
                                                                uint32_t tmem_cols, uint32_t m32,
                                                                uint32_t n_mma) {
@@ -344,10 +356,7 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
             phase ^= 1;
             fence_after();
             // ---- epilogue: this thread's row, columns p0 .. p0 + w
-            for (uint32_t c0 = 0; c0 < w; c0 += 32) {
-                uint32_t r[32];
-                tmem_ld32(tmem + lane_base + c0, r);
-                tmem_wait_ld();
+            auto process = [&](uint32_t (&r)[32], uint32_t c0) {
                 if (w - c0 < 32) {  // columns past N are not written by the MMA
 #pragma unroll
                     for (int j = 16; j < 32; ++j) r[j] = 0x7f800000u;
@@ -369,6 +378,37 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
                 }
 #pragma unroll
                 for (int s4 = 0; s4 < 4; ++s4) ch[s4] = (m1[s4] != old[s4]) ? p0 + c0 : ch[s4];
+            };
+            if constexpr (DB) {
+                // two register buffers: the next 32 columns load from TMEM
+                // while the current ones are reduced (wide tables, where TMEM
+                // already limits the CTAs per SM to two; the extra registers
+                // would cost narrow tables their third and fourth CTA)
+                uint32_t ra[32], rb[32];
+                tmem_ld32(tmem + lane_base, ra);
+                tmem_wait_ld();
+                tmem_regs_ready(ra);
+                for (uint32_t c0 = 0; c0 < w; c0 += 64) {
+                    const bool more = c0 + 32 < w;
+                    if (more) tmem_ld32(tmem + lane_base + c0 + 32, rb);
+                    process(ra, c0);
+                    if (!more) break;
+                    tmem_wait_ld();
+                    tmem_regs_ready(rb);
+                    const bool more2 = c0 + 64 < w;
+                    if (more2) tmem_ld32(tmem + lane_base + c0 + 64, ra);
+                    process(rb, c0 + 32);
+                    if (!more2) break;
+                    tmem_wait_ld();
+                    tmem_regs_ready(ra);
+                }
+            } else {
+                for (uint32_t c0 = 0; c0 < w; c0 += 32) {
+                    uint32_t r[32];
+                    tmem_ld32(tmem + lane_base + c0, r);
+                    tmem_wait_ld();
+                    process(r, c0);
+                }
             }
         }
         // merge the four states: full keys (value bits | global column) for the
@@ -716,7 +756,8 @@ void launch_umma(pqg_ctx* ctx, const NearestArgs& a) {
     if (const char* se = std::getenv("PQG_UMMA_SPLIT")) n_mma = se[0] == '1' && n_pad > 128 ? 128 : n_pad;
     uint32_t cols = 32;
     while (cols < n_mma) cols <<= 1;
-    auto kern = umma_screen_kernel<DS, KA, PAD>;
+    const bool db = n_mma == n_pad && n_pad > 128 && !(std::getenv("PQG_UMMA_DB") && std::getenv("PQG_UMMA_DB")[0] == '0');
+    auto kern = db ? umma_screen_kernel<DS, KA, PAD, true> : umma_screen_kernel<DS, KA, PAD, false>;
     PQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     const uint64_t ntiles = (a.n + kRows - 1) / kRows;
     // persistent: CTAs per SM limited by TMEM columns (2 at Ks=256), shared
