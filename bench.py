@@ -350,7 +350,7 @@ def run_ours(args, rank, world, local):
     probe = C.c_double()
     L.check(lib.pqg_fp32_probe(ctx.h, C.byref(probe)), "fp32_probe")
     fp32_peak = float(probe.value)
-    traffic = ncu_traffic("prof_enc_r1d")
+    traffic = ncu_traffic("prof_enc_r1f")
 
     # ---- e2e through the C ABI with pinned host buffers
     xh = torch.from_numpy(x_host).pin_memory()
