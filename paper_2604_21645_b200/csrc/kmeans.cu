@@ -437,7 +437,6 @@ __device__ double staged_row_order_sum(double s, const float* col, uint32_t nf, 
             exact = false;
         } else {
             int lq = elo - 150;  // log2 ulp of the smallest nonzero value
-            int lb = ehi - 118;  // kMeanThreads values below 2^(ehi-126) each
             if (s != 0.0) {
                 // s = mant * 2^(E-1075): its lowest set bit, not its ulp, bounds
                 // the granularity (a running sum of fp32 values is usually a
@@ -446,9 +445,12 @@ __device__ double staged_row_order_sum(double s, const float* col, uint32_t nf, 
                 const int E = int((sb >> 52) & 0x7FF);
                 const unsigned long long mant = (sb & ((1ull << 52) - 1)) | (1ull << 52);
                 lq = min(lq, E - 1075 + (__ffsll((long long)mant) - 1));
-                lb = max(lb, E - 1022);  // |s| < 2^(E-1022)
             }
-            exact = lb + 1 - lq <= 53;
+            // every partial sum is at most |s| + kMeanThreads values below
+            // 2^(ehi-126) each, rounded up: below 2^lb
+            const double bound = __dadd_ru(fabs(s), ldexp(1.0, ehi - 118));
+            const int lb = int((__double_as_longlong(bound) >> 52) & 0x7FF) - 1022;
+            exact = lb - lq <= 53;
         }
         if (exact) {
             s = __dadd_rn(s, tot);
@@ -614,7 +616,8 @@ __global__ void __launch_bounds__(1024) pieces_setup_kernel(const uint64_t* offs
                                                             uint64_t PP, uint32_t* piece_start,
                                                             PieceDesc* pieces, int* has_empty,
                                                             const int* active, uint32_t d, double* csum,
-                                                            int* cmax, int* cmin) {
+                                                            int* cmax, int* cmin,
+                                                            unsigned long long* work_count) {
     __shared__ uint32_t wsum[32];
     __shared__ int any_empty;
     const uint32_t b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -672,6 +675,7 @@ __global__ void __launch_bounds__(1024) pieces_setup_kernel(const uint64_t* offs
     __syncthreads();
     for (uint64_t p = total + tid; p < PP; p += blockDim.x) pieces[uint64_t(b) * PP + p] = PieceDesc{0, 0u, 0u};
     if (tid == 0) has_empty[b] = (active && !active[b]) ? 0 : any_empty;
+    if (b == 0 && tid == 0) *work_count = 0;
 }
 
 // Row m of problem b's bucketed order: the copy (xs) or the permutation.
@@ -770,9 +774,8 @@ __global__ void __launch_bounds__(kMeanThreads, 4) mean_pieces_kernel(
 __global__ void __launch_bounds__(kMeanThreads) mean_finalize_kernel(
     MemberRows mr, uint64_t n, uint32_t d, uint64_t k, uint32_t B, const uint64_t* offsets,
     const uint32_t* piece_start, const PieceStat* stats, float* table, const int* active, const double* csum,
-    const int* cmax, const int* cmin) {
+    const int* cmax, const int* cmin, unsigned long long* work_count, uint64_t* work) {
     const uint32_t lane = threadIdx.x & 31;
-    const PieceGeom pg = piece_geom(d, n, k);
     const uint64_t bc = uint64_t(blockIdx.x) * (kMeanThreads / 32) + (threadIdx.x >> 5);
     if (bc >= uint64_t(B) * k) return;
     const uint64_t b = bc / k, c = bc - b * k;
@@ -780,13 +783,12 @@ __global__ void __launch_bounds__(kMeanThreads) mean_finalize_kernel(
     const uint64_t beg = offsets[b * (k + 1) + c], end = offsets[b * (k + 1) + c + 1];
     if (beg == end) return;  // empty: the reseed fills it
     const uint64_t cnt = end - beg;
-    const uint32_t ps = piece_start[bc];
-    const uint32_t np = uint32_t((cnt + pg.R - 1) / pg.R);
-    // ---- finalize cluster c (this warp completed it)
+    (void)piece_start;
+    (void)stats;
+    (void)mr;
     int lg = 0;
     while ((uint64_t(1) << lg) < cnt) ++lg;
     const double inv = __ddiv_rn(1.0, (double)cnt);
-    const PieceStat* cs = stats + (b * pg.PP + ps) * d;
     // (1) lane t: the cluster's total and exponent range of dim t
     uint32_t need = 0;  // bit: dim lane + 32*bit rejected by the exactness test
     for (uint32_t t = lane, bit = 0; t < d; t += 32, ++bit) {
@@ -796,59 +798,130 @@ __global__ void __launch_bounds__(kMeanThreads) mean_finalize_kernel(
         else
             need |= 1u << bit;
     }
-    // (2) rejected dims, one at a time by the whole warp: replay the pieces in
-    // row order; a piece that cannot round given the running sum is added
-    // whole, any other member by member (values loaded together, the chain
-    // walked through shuffles)
+    // (2) rejected dims go to the replay worklist (a warp each, below)
     for (uint32_t bit = 0; 32 * bit < d; ++bit) {
-        for (uint32_t todo = __ballot_sync(0xffffffffu, (need >> bit) & 1u); todo; todo &= todo - 1) {
-            const uint32_t t = 32 * bit + uint32_t(__ffs(todo) - 1);
-            double r = 0.0;
-            for (uint32_t i0 = 0; i0 < np; i0 += 32) {
-                const uint32_t il = min(i0 + lane, np - 1);
-                const PieceStat* e = &cs[uint64_t(il) * d + t];
-                const double ls = __ldcg(&e->s);
-                const int la = __ldcg(&e->emax), lm = __ldcg(&e->emin);
-                const uint32_t cnt_i = min(32u, np - i0);
-                for (uint32_t ii = 0; ii < cnt_i; ++ii) {
-                    const double ss = __shfl_sync(0xffffffffu, ls, ii);
-                    const int a = __shfl_sync(0xffffffffu, la, ii), m = __shfl_sync(0xffffffffu, lm, ii);
-                    bool exact;
-                    if (a < 0) {
-                        exact = true;
-                    } else if (a == 255 || !isfinite(r)) {
-                        exact = false;
-                    } else {
-                        int lq = m - 150, lb = a - 126 + int(pg.lR);
-                        if (r != 0.0) {
-                            const unsigned long long sb = __double_as_longlong(r);
-                            const int E = int((sb >> 52) & 0x7FF);
-                            const unsigned long long mant = (sb & ((1ull << 52) - 1)) | (1ull << 52);
-                            lq = min(lq, E - 1075 + (__ffsll((long long)mant) - 1));
-                            lb = max(lb, E - 1022);
-                        }
-                        exact = lb + 1 - lq <= 53;
-                    }
-                    if (exact) {
-                        r = __dadd_rn(r, ss);
-                        continue;
-                    }
-                    const uint64_t m0 = beg + uint64_t(i0 + ii) * pg.R;
-                    const uint32_t mr_n = uint32_t(min64(pg.R, end - m0));  // <= 256 = 8 x 32
+        if ((need >> bit) & 1u) {
+            const unsigned long long slot = atomicAdd(work_count, 1ull);
+            work[slot] = (uint64_t(bc) << 16) | (32 * bit + lane);
+        }
+    }
+}
+
+// Row-order replay of one rejected (cluster, dim) per warp: the pieces in
+// row order, 32 at a time -- a batch whose additions provably cannot round
+// (every partial sum a multiple of 2^lq below 2^(lq+53), lq from the running
+// sum's lowest set bit and the batch's smallest ulp) is added as one sum,
+// otherwise piece by piece: a piece that cannot round is added whole, any
+// other member by member (the reference's chain, kmeans.cpp:103-111).
+__device__ __forceinline__ int lowbit_exp(double r) {  // log2 of r's lowest set bit (r normal, != 0)
+    const unsigned long long sb = __double_as_longlong(r);
+    const int E = int((sb >> 52) & 0x7FF);
+    const unsigned long long mant = (sb & ((1ull << 52) - 1)) | (1ull << 52);
+    return E - 1075 + (__ffsll((long long)mant) - 1);
+}
+__device__ __forceinline__ int mag_exp(double r) {  // |r| < 2^mag_exp
+    return int((__double_as_longlong(r) >> 52) & 0x7FF) - 1022;
+}
+
+__global__ void __launch_bounds__(kMeanThreads) mean_replay_kernel(
+    MemberRows mr, uint64_t n, uint32_t d, uint64_t k, const uint64_t* offsets, const uint32_t* piece_start,
+    const PieceStat* stats, float* table, const unsigned long long* work_count, const uint64_t* work) {
+    __shared__ float wbuf[kMeanThreads / 32][256];  // a piece's members, for the serial chain
+    const uint32_t lane = threadIdx.x & 31;
+    float* buf = wbuf[threadIdx.x >> 5];
+    const PieceGeom pg = piece_geom(d, n, k);
+    const unsigned long long cntw = *work_count;
+    for (uint64_t wi = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; wi < cntw;
+         wi += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        const uint64_t item = work[wi];
+        const uint64_t bc = item >> 16;
+        const uint32_t t = uint32_t(item & 0xFFFFu);
+        const uint64_t b = bc / k, c = bc - b * k;
+        const uint64_t beg = offsets[b * (k + 1) + c], end = offsets[b * (k + 1) + c + 1];
+        const uint64_t cnt = end - beg;
+        const uint32_t np = uint32_t((cnt + pg.R - 1) / pg.R);
+        const PieceStat* cs = stats + (b * pg.PP + piece_start[bc]) * d;
+        double r = 0.0;
+        uint64_t wbeg = 0, wend = 0;  // members cached in buf
+        for (uint32_t i0 = 0; i0 < np; i0 += 32) {
+            const uint32_t nb = min(32u, np - i0);
+            const bool in = lane < nb;
+            const PieceStat* e = &cs[uint64_t(i0 + (in ? lane : 0)) * d + t];
+            const double ls = in ? __ldcg(&e->s) : 0.0;
+            const int la = in ? __ldcg(&e->emax) : -1, lm = in ? __ldcg(&e->emin) : (1 << 30);
+            // batch test
+            int ehi = la, elo = lm;
+            double tot = ls;
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) {
+                ehi = max(ehi, __shfl_xor_sync(0xffffffffu, ehi, o));
+                elo = min(elo, __shfl_xor_sync(0xffffffffu, elo, o));
+                tot = __dadd_rn(tot, __shfl_xor_sync(0xffffffffu, tot, o));
+            }
+            bool batch_exact;
+            if (ehi < 0) {
+                batch_exact = true;
+            } else if (ehi == 255 || !isfinite(r)) {
+                batch_exact = false;
+            } else {
+                // every partial sum is a multiple of 2^lq and at most
+                // |r| + (32 R values below 2^(ehi-126)) < 2^lb
+                int lq = elo - 150;
+                if (r != 0.0) lq = min(lq, lowbit_exp(r));
+                const double bound = __dadd_ru(fabs(r), ldexp(1.0, ehi - 126 + int(pg.lR) + 5));
+                batch_exact = mag_exp(bound) - lq <= 53;
+            }
+            if (batch_exact) {
+                r = __dadd_rn(r, tot);
+                continue;
+            }
+            for (uint32_t ii = 0; ii < nb; ++ii) {
+                const double ss = __shfl_sync(0xffffffffu, ls, ii);
+                const int a = __shfl_sync(0xffffffffu, la, ii), m = __shfl_sync(0xffffffffu, lm, ii);
+                bool exact;
+                if (a < 0) {
+                    exact = true;
+                } else if (a == 255 || !isfinite(r)) {
+                    exact = false;
+                } else {
+                    int lq = m - 150;
+                    if (r != 0.0) lq = min(lq, lowbit_exp(r));
+                    const double bound = __dadd_ru(fabs(r), ldexp(1.0, a - 126 + int(pg.lR)));
+                    exact = mag_exp(bound) - lq <= 53;
+                }
+                if (exact) {
+                    r = __dadd_rn(r, ss);
+                    continue;
+                }
+                // this piece can round: the reference's chain, member by member;
+                // members come through a 256-member window in shared memory
+                // (runs of such pieces share one load round trip)
+                const uint64_t m0 = beg + uint64_t(i0 + ii) * pg.R;
+                const uint32_t mn = uint32_t(min64(pg.R, end - m0));  // <= 256
+                if (m0 < wbeg || m0 + mn > wend) {
+                    wbeg = m0;
+                    wend = min64(end, m0 + 256);
+                    const uint32_t wn = uint32_t(wend - wbeg);
                     float v[8];
 #pragma unroll
                     for (int u = 0; u < 8; ++u)
-                        v[u] = __ldg(member_row(mr, n, d, b, m0 + min(uint32_t(u * 32) + lane, mr_n - 1)) + t);
+                        v[u] = __ldg(member_row(mr, n, d, b, wbeg + min(uint32_t(u * 32) + lane, wn - 1)) + t);
+                    __syncwarp();
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        if (uint32_t(u * 32) >= mr_n) break;
-                        const uint32_t lim = min(32u, mr_n - u * 32);
-                        for (uint32_t l = 0; l < lim; ++l) r = __dadd_rn(r, (double)__shfl_sync(0xffffffffu, v[u], l));
-                    }
+                    for (int u = 0; u < 8; ++u) buf[u * 32 + lane] = v[u];
+                    __syncwarp();
                 }
+                if (lane == 0) {
+                    const float* wv = buf + (m0 - wbeg);
+                    double q = r;
+#pragma unroll 8
+                    for (uint32_t l = 0; l < mn; ++l) q = __dadd_rn(q, (double)wv[l]);
+                    r = q;
+                }
+                r = __shfl_sync(0xffffffffu, r, 0);
             }
-            if (lane == 0) table[(b * k + c) * d + t] = __double2float_rn(__dmul_rn(r, inv));
         }
+        if (lane == 0) table[bc * d + t] = __double2float_rn(__dmul_rn(r, __ddiv_rn(1.0, (double)cnt)));
     }
 }
 
@@ -1151,8 +1224,10 @@ void kmeans_update(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint
         double* csum = scratch<double>(ctx, ncl * d);
         int* cmax = scratch<int>(ctx, ncl * d);
         int* cmin = scratch<int>(ctx, ncl * d);
+        unsigned long long* work_count = scratch<unsigned long long>(ctx, 1);
+        uint64_t* work = scratch<uint64_t>(ctx, ncl * d);
         launch(ctx, "kmeans_sum", pieces_setup_kernel, dim3(B), dim3(1024), 0, (const uint64_t*)bk.offsets, k,
-               pg.R, pg.PP, piece_start, pieces_d, has_empty, active, d, csum, cmax, cmin);
+               pg.R, pg.PP, piece_start, pieces_d, has_empty, active, d, csum, cmax, cmin, work_count);
         MemberRows mr;
         mr.x = mx;
         mr.ldx = mldx;
@@ -1163,7 +1238,11 @@ void kmeans_update(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint
                n, d, k, B, (const PieceDesc*)pieces_d, stats, active, csum, cmax, cmin);
         launch(ctx, "kmeans_sum", mean_finalize_kernel, dim3(unsigned((ncl + 7) / 8)), dim3(kMeanThreads), 0,
                mr, n, d, k, B, (const uint64_t*)bk.offsets, (const uint32_t*)piece_start,
-               (const PieceStat*)stats, table, active, (const double*)csum, (const int*)cmax, (const int*)cmin);
+               (const PieceStat*)stats, table, active, (const double*)csum, (const int*)cmax, (const int*)cmin,
+               work_count, work);
+        launch(ctx, "kmeans_sum", mean_replay_kernel, dim3(ctx->num_sms * 4), dim3(kMeanThreads), 0, mr, n, d, k,
+               (const uint64_t*)bk.offsets, (const uint32_t*)piece_start, (const PieceStat*)stats, table,
+               (const unsigned long long*)work_count, (const uint64_t*)work);
     } else {
         PQG_CUDA(cudaMemsetAsync(has_empty, 0, sizeof(int) * B, ctx->stream));
         // small clusters (batched chunk fits): a warp each; large ones: a CTA each
