@@ -186,6 +186,12 @@ __device__ __forceinline__ void warp_insert(double& my_d, uint64_t& my_id, doubl
     }
 }
 
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+
 // (a0, a1) += (b0, b1) as one packed FADD2 (sm_100): the even and odd
 // subspace chains of the screen sum advance together.
 __device__ __forceinline__ void add_f32x2(float& a0, float& a1, float b0, float b1) {
@@ -254,12 +260,39 @@ __global__ void __launch_bounds__(kScanThreads) adc_scan_kernel(
         const float* lq = luts + q * uint64_t(M) * ks;
         for (uint32_t e = threadIdx.x; e < M * ks; e += blockDim.x) lut[e] = __ldg(lq + e);
     } else {
-        for (uint32_t e = threadIdx.x; e < M * ks; e += blockDim.x) {
-            const uint32_t m = e / ks;
-            lut[e] = __double2float_rn(exact_sq_l2(qv + uint64_t(m) * ds, tables + uint64_t(e) * ds, int(ds)));
+        // adc_table (proj/src/pq.cpp:132-151): the query converted to fp64 once
+        // (shared), then per entry the codeword's conversions and the
+        // reference's dsub / dmul / dadd chain in t order
+        double* qd = reinterpret_cast<double*>(wl + (kScanThreads / 32) * k);
+        for (uint32_t t = threadIdx.x; t < D; t += blockDim.x) qd[t] = (double)qv[t];
+        __syncthreads();
+        for (uint32_t m = 0; m < M; ++m) {
+            const double* qm = qd + m * ds;
+            for (uint32_t j = threadIdx.x; j < ks; j += blockDim.x) {
+                const float* c = tables + (uint64_t(m) * ks + j) * ds;
+                double acc = 0.0;
+                if ((ds & 3u) == 0 && (reinterpret_cast<uintptr_t>(c) & 15u) == 0) {
+                    for (uint32_t t = 0; t < ds; t += 4) {
+                        const float4 u = __ldg(reinterpret_cast<const float4*>(c + t));
+                        const float cc[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) {
+                            const double diff = __dsub_rn(qm[t + v], (double)cc[v]);
+                            acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+                        }
+                    }
+                } else {
+                    for (uint32_t t = 0; t < ds; ++t) {
+                        const double diff = __dsub_rn(qm[t], (double)__ldg(c + t));
+                        acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+                    }
+                }
+                lut[m * ks + j] = __double2float_rn(acc);
+            }
         }
     }
     __syncthreads();
+    const uint32_t lut_s = static_cast<uint32_t>(__cvta_generic_to_shared(lut));
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const double inf = __longlong_as_double(0x7ff0000000000000LL);
     double my_d = inf;
@@ -269,6 +302,16 @@ __global__ void __launch_bounds__(kScanThreads) adc_scan_kernel(
     double kd = inf;
     uint64_t ki = ~uint64_t(0);
     const float shrink = 1.0f - float(M + 2) * kU * 1.05f;
+    // Early exit on partial sums (Ks = 256 byte codes: every code is valid, so
+    // skipping the rest of a row cannot hide a range error).  LUT entries are
+    // >= 0, so a partial sum bounds the full one from below; after each group
+    // of subspaces a lane whose bound already exceeds the list's k-th (or
+    // max_sq) drops out, and the warp stops when no lane is left.  The fp32
+    // test is conservative: partial * shrink_p (rounded) <= the exact partial
+    // sum of the fp32 entries for any h <= M terms, and the k-th is rounded up.
+    constexpr bool kPrune = RB > 0 && W == 1 && KS == 256;
+    const float shrink_p = 1.0f - float(M + 4) * kU * 1.05f;
+    const float max32 = has_max ? __double2float_ru(max_sq) : __int_as_float(0x7f800000);
     for (uint64_t p = 0; p < nprobe; ++p) {
         const uint32_t l = probes[q * nprobe + p];
         const uint64_t beg = offsets[l], end = offsets[l + 1];
@@ -278,7 +321,53 @@ __global__ void __launch_bounds__(kScanThreads) adc_scan_kernel(
             bool want = false;
             double s64 = 0.0;
             uint64_t id = 0;
-            if (e < end) {
+            if constexpr (kPrune) {
+                constexpr int MM = RB;
+                constexpr int GS = MM >= 32 ? 8 : 4;
+                const bool valid = e < end;
+                CodeRow<RB> row;
+                if (valid) row.load(codes + e * RB);
+                else {
+#pragma unroll
+                    for (int i = 0; i < RB / 4; ++i) row.w[i] = 0;
+                }
+                const float lim = fminf(__double2float_ru(th), max32);
+                bool live = valid;
+                float s_even = 0.f, s_odd = 0.f;
+#pragma unroll
+                for (int g = 0; g < MM; g += GS) {
+                    if (g > 0) {
+                        live = live && !((s_even + s_odd) * shrink_p > lim);
+                        if (!__any_sync(0xffffffffu, live)) break;
+                    }
+                    if (live) {
+#pragma unroll
+                        for (int i = g / 4; i < (g + GS) / 4; ++i) {
+                            // the word passes through an opaque move here, so its
+                            // byte extraction is not hoisted above the exit test
+                            uint32_t cw = row.w[i];
+                            asm volatile("" : "+r"(cw));
+                            const uint32_t a0 = lut_s + uint32_t(4 * i) * 1024u;
+                            const float v0 = lds_f32(a0 + ((cw << 2) & 0x3fcu));
+                            const float v1 = lds_f32(a0 + 1024u + ((cw >> 6) & 0x3fcu));
+                            const float v2 = lds_f32(a0 + 2048u + ((cw >> 14) & 0x3fcu));
+                            const float v3 = lds_f32(a0 + 3072u + ((cw >> 22) & 0x3fcu));
+                            add_f32x2(s_even, s_odd, v0, v1);
+                            add_f32x2(s_even, s_odd, v2, v3);
+                        }
+                    }
+                }
+                if (live) {
+                    const double lower = double(s_even + s_odd) * double(shrink);
+                    if (lower <= th && !(has_max && lower > max_sq)) {
+#pragma unroll
+                        for (int m = 0; m < MM; ++m)
+                            s64 = __dadd_rn(s64, (double)lut[m * 256 + row.template get<1>(m)]);
+                        id = ids[e];
+                        want = !(has_max && s64 > max_sq) && member(id);
+                    }
+                }
+            } else if (e < end) {
                 const uint8_t* cr = codes + e * rb;
                 float s32 = 0.f;
                 bool bad = false;
@@ -511,7 +600,8 @@ void ivf_scan(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t 
               const uint64_t* subset, uint64_t nsub, const float* luts) {
     if (k > 32) fail(PQG_EUNSUPPORTED, "search: k > 32 is not supported by the warp top-k path");
     const size_t lut_bytes = (sizeof(float) * ix.M * ix.ks + 15) & ~size_t(15);
-    const size_t smem = lut_bytes + sizeof(TopK) * k * (kScanThreads / 32);
+    const size_t smem = lut_bytes + sizeof(TopK) * k * (kScanThreads / 32) +
+                        sizeof(double) * uint64_t(ix.M) * ix.ds;  // + fp64 query
     if (smem > 220 * 1024) fail(PQG_EUNSUPPORTED, "search: M*ks lookup table exceeds shared memory");
     const uint32_t rb = ix.M * ix.w;
     auto run = [&](auto kern) {
@@ -527,7 +617,9 @@ void ivf_scan(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t 
     };
     // vector code loads need rb-aligned rows (CSR rows are rb apart from an aligned base)
     const bool aligned = (reinterpret_cast<uintptr_t>(ix.codes) % (rb >= 16 ? 16 : rb)) == 0;
-    const bool k256 = ix.ks == 256;
+    // PQG_ADC_PRUNE=0: the Ks = 256 scans without the partial-sum early exit
+    const char* pe = std::getenv("PQG_ADC_PRUNE");
+    const bool k256 = ix.ks == 256 && !(pe && pe[0] == '0');
     if (aligned && ix.w == 1 && rb == 16) k256 ? run(adc_scan_kernel<16, 1, 256>) : run(adc_scan_kernel<16, 1, 0>);
     else if (aligned && ix.w == 1 && rb == 8) k256 ? run(adc_scan_kernel<8, 1, 256>) : run(adc_scan_kernel<8, 1, 0>);
     else if (aligned && ix.w == 1 && rb == 32) k256 ? run(adc_scan_kernel<32, 1, 256>) : run(adc_scan_kernel<32, 1, 0>);
