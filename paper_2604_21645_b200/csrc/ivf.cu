@@ -82,14 +82,29 @@ __global__ void __launch_bounds__(kSelThreads) probe_select_kernel(
             if ((bits & mask) == prefix) atomicAdd(&hist[(bits >> shift) & 255u], 1u);
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t r = s_rank, dg = 0;
-            for (; dg < 256; ++dg) {
-                if (hist[dg] >= r) break;
-                r -= hist[dg];
+        if (threadIdx.x < 32) {  // digit holding rank r: warp scan over 8 bins per lane
+            const uint32_t lane = threadIdx.x;
+            uint32_t h[8], sum = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) { h[i] = hist[lane * 8 + i]; sum += h[i]; }
+            uint32_t incl = sum;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+                if (int(lane) >= off) incl += v;
             }
-            s_rank = r;
-            s_prefix = prefix | (dg << shift);
+            const uint32_t r = s_rank;
+            uint32_t c = incl - sum;
+            if (c < r && r <= incl) {
+                int dg = int(lane) * 8;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    if (c + h[i] >= r) { dg = int(lane) * 8 + i; break; }
+                    c += h[i];
+                }
+                s_rank = r - c;
+                s_prefix = prefix | (uint32_t(dg) << shift);
+            }
         }
         mask |= 255u << shift;
         __syncthreads();
@@ -312,26 +327,31 @@ __global__ void __launch_bounds__(kScanThreads) adc_scan_kernel(
     constexpr bool kPrune = RB > 0 && W == 1 && KS == 256;
     const float shrink_p = 1.0f - float(M + 4) * kU * 1.05f;
     const float max32 = has_max ? __double2float_ru(max_sq) : __int_as_float(0x7f800000);
+    float lim = max32;  // kPrune: min(k-th rounded up, max_sq), refreshed on insertion
     for (uint64_t p = 0; p < nprobe; ++p) {
         const uint32_t l = probes[q * nprobe + p];
         const uint64_t beg = offsets[l], end = offsets[l + 1];
-        for (uint64_t base = beg + uint64_t(wid) * 32; base < end; base += kScanThreads) {
+        // 32-bit offsets within the list (a shard's list is < 2^32 rows)
+        const uint32_t len = uint32_t(end - beg);
+        const uint8_t* lcodes = codes + beg * RB;
+        const uint64_t* lids = ids + beg;
+        for (uint32_t o = uint32_t(wid) * 32; o < len; o += kScanThreads) {
             const double th = kd;
-            const uint64_t e = base + lane;
+            const uint64_t e = beg + o + lane;
             bool want = false;
             double s64 = 0.0;
             uint64_t id = 0;
             if constexpr (kPrune) {
                 constexpr int MM = RB;
                 constexpr int GS = MM >= 32 ? 8 : 4;
-                const bool valid = e < end;
+                const uint32_t oe = o + lane;
+                const bool valid = oe < len;
                 CodeRow<RB> row;
-                if (valid) row.load(codes + e * RB);
+                if (valid) row.load(lcodes + oe * RB);
                 else {
 #pragma unroll
                     for (int i = 0; i < RB / 4; ++i) row.w[i] = 0;
                 }
-                const float lim = fminf(__double2float_ru(th), max32);
                 bool live = valid;
                 float s_even = 0.f, s_odd = 0.f;
 #pragma unroll
@@ -363,7 +383,7 @@ __global__ void __launch_bounds__(kScanThreads) adc_scan_kernel(
 #pragma unroll
                         for (int m = 0; m < MM; ++m)
                             s64 = __dadd_rn(s64, (double)lut[m * 256 + row.template get<1>(m)]);
-                        id = ids[e];
+                        id = lids[oe];
                         want = !(has_max && s64 > max_sq) && member(id);
                     }
                 }
@@ -428,6 +448,7 @@ __global__ void __launch_bounds__(kScanThreads) adc_scan_kernel(
                 ki = __shfl_sync(0xffffffffu, my_id, k - 1);
                 want = want && lane != src && pair_less(s64, id, kd, ki);
                 ball = __ballot_sync(0xffffffffu, want);
+                if constexpr (kPrune) lim = fminf(__double2float_ru(kd), max32);
             }
         }
     }
