@@ -49,77 +49,100 @@ __device__ __forceinline__ float row_x(const RowSrc& s, uint64_t i, uint32_t t) 
 
 
 // ---- operand preparation ---------------------------------------------------
-// One thread per row: A_r = [x_r, 1, C_r, 0...], split hi/lo, interleaved.
-// C_r = ||x_r||^2 (+ 2E margin in matrix mode, whose consumer orders values as
-// unsigned bits); the argmin epilogue compares floats and recomputes E from
-// the stored ||x_r||^2 and the current max ||c||.
-__global__ void split_rows_kernel(RowSrc src, uint64_t n, uint32_t d, uint32_t kchunks,
-                                  const float* cmax_p, int margin, uint8_t* A, float* nxrow) {
-    const float cmax = *cmax_p;
-    for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < (n + kR - 1) / kR * kR;
+// A_r = [x_r, 1, C_r, 0...], split hi/lo, interleaved.  C_r = ||x_r||^2 (+ 2E
+// margin in matrix mode, whose consumer orders values as unsigned bits); the
+// argmin epilogue compares floats and recomputes E from the stored ||x_r||^2
+// and the current max ||c||.  Two passes: the row norms (thread per row, the
+// same sequential fmaf order as before), then one thread per (row, K chunk,
+// 4-element group) with a warp covering 8 rows x 4 groups, so the x reads use
+// whole sectors and every interleaved 128-byte core-matrix line is written by
+// one warp instruction.
+__global__ void row_norms_kernel(RowSrc src, uint64_t n, uint32_t d, float* nxrow) {
+    for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
          r += uint64_t(gridDim.x) * blockDim.x) {
-        const bool valid = r < n;
         float nx = 0.f;
-        if (valid)
-            for (uint32_t t = 0; t < d; ++t) {
-                const float v = row_x(src, r, t);
-                nx = fmaf(v, v, nx);
-            }
+        for (uint32_t t = 0; t < d; ++t) {
+            const float v = row_x(src, r, t);
+            nx = fmaf(v, v, nx);
+        }
+        nxrow[r] = nx;
+    }
+}
+
+// element group g -> (row within the tile, K chunk, group of 4 within the chunk)
+struct SplitIdx {
+    uint64_t tile;
+    uint32_t rl, kc, k4;
+};
+__device__ __forceinline__ SplitIdx split_idx(uint64_t g, uint32_t rows, uint32_t kchunks) {
+    SplitIdx s;
+    const uint32_t lo = uint32_t(g & 7u);
+    s.k4 = uint32_t((g >> 3) & 7u) * 4u;
+    const uint64_t rest = g >> 6;
+    const uint32_t hi = uint32_t(rest % (rows / 8));
+    const uint64_t rest2 = rest / (rows / 8);
+    s.kc = uint32_t(rest2 % kchunks);
+    s.tile = rest2 / kchunks;
+    s.rl = hi * 8 + lo;
+    return s;
+}
+
+__global__ void split_rows_kernel(RowSrc src, uint64_t n, uint32_t d, uint32_t kchunks,
+                                  const float* cmax_p, int margin, uint8_t* A, const float* nxrow) {
+    const float cmax = *cmax_p;
+    const uint64_t total = (n + kR - 1) / kR * kR * kchunks * (kKC / 4);
+    for (uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < total;
+         g += uint64_t(gridDim.x) * blockDim.x) {
+        const SplitIdx ix = split_idx(g, kR, kchunks);
+        const uint64_t r = ix.tile * kR + ix.rl;
+        const bool valid = r < n;
+        const float nx = valid ? nxrow[r] : 0.f;
         const float q = sqrtf(nx) * (1.f + 1e-6f) + cmax;
         const float S = q * q * 1.01f + 1e-6f;
         const float E = big_error_bound(S, kchunks);
         const float C = margin ? nx * (1.f + 2.f * float(d + 2) * kU) + 2.f * E : nx;
-        if (valid) nxrow[r] = nx;
-        const uint64_t tile = r / kR;
-        const uint32_t rl = uint32_t(r % kR);
-        for (uint32_t kc = 0; kc < kchunks; ++kc) {
-            uint8_t* blk = A + (tile * kchunks + kc) * (2 * kAChunk);
-            for (uint32_t k4 = 0; k4 < kKC; k4 += 4) {
-                float h[4], l[4];
+        uint8_t* blk = A + (ix.tile * kchunks + ix.kc) * (2 * kAChunk);
+        float h[4], l[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const uint32_t t = kc * kKC + k4 + u;
-                    float v = 0.f;
-                    if (valid) v = t < d ? row_x(src, r, t) : (t == d ? 1.f : (t == d + 1 ? C : 0.f));
-                    h[u] = tf32_hi(v);
-                    l[u] = tf32_hi(v - h[u]);
-                }
-                *reinterpret_cast<float4*>(blk + il_off(rl, k4)) = make_float4(h[0], h[1], h[2], h[3]);
-                *reinterpret_cast<float4*>(blk + kAChunk + il_off(rl, k4)) = make_float4(l[0], l[1], l[2], l[3]);
-            }
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t t = ix.kc * kKC + ix.k4 + u;
+            float v = 0.f;
+            if (valid) v = t < d ? row_x(src, r, t) : (t == d ? 1.f : (t == d + 1 ? C : 0.f));
+            h[u] = tf32_hi(v);
+            l[u] = tf32_hi(v - h[u]);
         }
+        *reinterpret_cast<float4*>(blk + il_off(ix.rl, ix.k4)) = make_float4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<float4*>(blk + kAChunk + il_off(ix.rl, ix.k4)) = make_float4(l[0], l[1], l[2], l[3]);
     }
 }
 
-// One thread per centroid: B_j = [-2c_j, ||c_j||^2, 1, 0...]; padded rows never win.
+// B_j = [-2c_j, ||c_j||^2, 1, 0...]; padded rows never win.  Same thread
+// layout as split_rows_kernel over 256-row blocks.
 __global__ void split_table_kernel(const float* table, const float* cnorm, uint64_t k, uint32_t d,
                                    uint32_t kchunks, uint64_t k_pad, uint8_t* Bm) {
-    for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < k_pad;
-         j += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t nb = j / kN;
-        const uint32_t jl = uint32_t(j % kN);
-        for (uint32_t kc = 0; kc < kchunks; ++kc) {
-            uint8_t* blk = Bm + (nb * kchunks + kc) * (2 * kBChunk);
-            for (uint32_t k4 = 0; k4 < kKC; k4 += 4) {
-                float h[4], l[4];
+    const uint64_t total = k_pad * kchunks * (kKC / 4);
+    for (uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < total;
+         g += uint64_t(gridDim.x) * blockDim.x) {
+        const SplitIdx ix = split_idx(g, kN, kchunks);
+        const uint64_t j = ix.tile * kN + ix.rl;
+        uint8_t* blk = Bm + (ix.tile * kchunks + ix.kc) * (2 * kBChunk);
+        float h[4], l[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const uint32_t t = kc * kKC + k4 + u;
-                    float v = 0.f;
-                    if (j < k) {
-                        if (t < d) v = -2.f * __ldg(table + j * d + t);
-                        else if (t == d) v = __ldg(cnorm + j);
-                        else if (t == d + 1) v = 1.f;
-                    } else if (t == d) {
-                        v = 3.0e38f;
-                    }
-                    h[u] = tf32_hi(v);
-                    l[u] = tf32_hi(v - h[u]);
-                }
-                *reinterpret_cast<float4*>(blk + il_off(jl, k4)) = make_float4(h[0], h[1], h[2], h[3]);
-                *reinterpret_cast<float4*>(blk + kBChunk + il_off(jl, k4)) = make_float4(l[0], l[1], l[2], l[3]);
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t t = ix.kc * kKC + ix.k4 + u;
+            float v = 0.f;
+            if (j < k) {
+                if (t < d) v = -2.f * __ldg(table + j * d + t);
+                else if (t == d) v = __ldg(cnorm + j);
+                else if (t == d + 1) v = 1.f;
+            } else if (t == d) {
+                v = 3.0e38f;
             }
+            h[u] = tf32_hi(v);
+            l[u] = tf32_hi(v - h[u]);
         }
+        *reinterpret_cast<float4*>(blk + il_off(ix.rl, ix.k4)) = make_float4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<float4*>(blk + kBChunk + il_off(ix.rl, ix.k4)) = make_float4(l[0], l[1], l[2], l[3]);
     }
 }
 
@@ -343,8 +366,10 @@ bool umma_big_prepare_rows(pqg_ctx* ctx, NearestArgs& a) {
     const uint64_t ntiles = (a.n + kR - 1) / kR;
     uint8_t* Am = scratch<uint8_t>(ctx, ntiles * kchunks * 2 * kAChunk);
     float* nx = scratch<float>(ctx, a.n);
-    launch(ctx, "big_split", split_rows_kernel, dim3(grid1d(ntiles * kR, 128, 1u << 20)), dim3(128), 0,
-           a.src, a.n, a.d, kchunks, a.cmax, 0, Am, nx);
+    launch(ctx, "big_split", row_norms_kernel, dim3(grid1d(a.n, 128, 1u << 20)), dim3(128), 0, a.src, a.n,
+           a.d, nx);
+    launch(ctx, "big_split", split_rows_kernel, dim3(grid1d(ntiles * kR * kchunks * (kKC / 4), 256, 1u << 20)),
+           dim3(256), 0, a.src, a.n, a.d, kchunks, a.cmax, 0, Am, (const float*)nx);
     a.big_rows = Am;
     a.big_nx = nx;
     return true;
@@ -355,8 +380,8 @@ void umma_big(pqg_ctx* ctx, const NearestArgs& a0) {
     const uint32_t nblocks = uint32_t((a0.k + kN - 1) / kN);
     const uint64_t k_pad = uint64_t(nblocks) * kN;
     uint8_t* Bm = scratch<uint8_t>(ctx, uint64_t(nblocks) * kchunks * 2 * kBChunk);
-    launch(ctx, "big_split", split_table_kernel, dim3(grid1d(k_pad, 128, 4096)), dim3(128), 0,
-           a0.table, a0.cnorm, a0.k, a0.d, kchunks, k_pad, Bm);
+    launch(ctx, "big_split", split_table_kernel, dim3(grid1d(k_pad * kchunks * (kKC / 4), 256, 1u << 20)),
+           dim3(256), 0, a0.table, a0.cnorm, a0.k, a0.d, kchunks, k_pad, Bm);
     const size_t smem = 2 * size_t(kStage);
     PQG_CUDA(cudaFuncSetAttribute(big_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     PQG_CUDA(cudaFuncSetAttribute(big_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -379,8 +404,11 @@ void umma_big(pqg_ctx* ctx, const NearestArgs& a0) {
         const uint64_t ntiles = (a.n + kR - 1) / kR;
         uint8_t* Am = scratch<uint8_t>(ctx, ntiles * kchunks * 2 * kAChunk);
         float* nx = scratch<float>(ctx, a.n);
-        launch(ctx, "big_split", split_rows_kernel, dim3(grid1d(ntiles * kR, 128, 1u << 20)), dim3(128), 0,
-               a.src, a.n, a.d, kchunks, a.cmax, a.out_mat ? 1 : 0, Am, nx);
+        launch(ctx, "big_split", row_norms_kernel, dim3(grid1d(a.n, 128, 1u << 20)), dim3(128), 0, a.src,
+               a.n, a.d, nx);
+        launch(ctx, "big_split", split_rows_kernel,
+               dim3(grid1d(ntiles * kR * kchunks * (kKC / 4), 256, 1u << 20)), dim3(256), 0, a.src, a.n, a.d,
+               kchunks, a.cmax, a.out_mat ? 1 : 0, Am, (const float*)nx);
         const unsigned grid = unsigned(std::min<uint64_t>(ntiles, uint64_t(ctx->num_sms)));
         if (a.out_mat) {
             a.out_mat += r0 * a.ld_mat;
