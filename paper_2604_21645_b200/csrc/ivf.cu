@@ -30,8 +30,8 @@ __device__ __forceinline__ uint32_t code_at(const uint8_t* p, uint32_t m, uint32
 // ---------------------------------------------------------------------------
 // probe selection
 // ---------------------------------------------------------------------------
-constexpr int kSelThreads = 256;
-constexpr int kCandCap = 1024;
+constexpr int kSelThreads = 64;  // one query per CTA; small CTAs keep ~32 queries in flight per SM
+constexpr int kCandCap = 256;
 
 __device__ __forceinline__ bool pair_less(double a, uint64_t ia, double b, uint64_t ib) {
     return a < b || (a == b && ia < ib);
