@@ -187,6 +187,41 @@ struct TopK {
     uint64_t id;
 };
 
+// Merge the warp's survivor buffer (n <= 32 entries in shared memory) into
+// its sorted list (lane l holds entry l; 32 entries kept, the first k are the
+// top-k): bitonic sort of the buffer across the lanes, then the first stage
+// of a bitonic merge against the list (min of list[l] and buffer[31 - l]
+// keeps the 32 smallest of the union) and five half-cleaner steps.  Order is
+// (dist, id) as in finalize_hits (proj/src/ivf.cpp:51-56).
+__device__ __forceinline__ void warp_merge_buffer(const TopK* buf, uint32_t n, double& my_d, uint64_t& my_id,
+                                               int lane) {
+    double bd = __longlong_as_double(0x7ff0000000000000LL);
+    uint64_t bi = ~uint64_t(0);
+    if (uint32_t(lane) < n) { bd = buf[lane].d; bi = buf[lane].id; }
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const double od = __shfl_xor_sync(0xffffffffu, bd, stride);
+            const uint64_t oi = __shfl_xor_sync(0xffffffffu, bi, stride);
+            const bool take_min = ((lane & stride) == 0) == ((lane & size) == 0 || size == 32);
+            const bool o_less = pair_less(od, oi, bd, bi);
+            if (take_min == o_less && !(od == bd && oi == bi)) { bd = od; bi = oi; }
+        }
+    }
+    const double rd = __shfl_sync(0xffffffffu, bd, 31 - lane);
+    const uint64_t ri = __shfl_sync(0xffffffffu, bi, 31 - lane);
+    if (pair_less(rd, ri, my_d, my_id)) { my_d = rd; my_id = ri; }
+#pragma unroll
+    for (int stride = 16; stride > 0; stride >>= 1) {
+        const double od = __shfl_xor_sync(0xffffffffu, my_d, stride);
+        const uint64_t oi = __shfl_xor_sync(0xffffffffu, my_id, stride);
+        const bool take_min = (lane & stride) == 0;
+        const bool o_less = pair_less(od, oi, my_d, my_id);
+        if (take_min == o_less && !(od == my_d && oi == my_id)) { my_d = od; my_id = oi; }
+    }
+}
+
 // Insert (d, id) into the warp's sorted list (lane l < k holds entry l).
 __device__ __forceinline__ void warp_insert(double& my_d, uint64_t& my_id, double d, uint64_t id,
                                            int k, int lane) {
@@ -328,6 +363,9 @@ __global__ void __launch_bounds__(kScanThreads) adc_scan_kernel(
     const float shrink_p = 1.0f - float(M + 4) * kU * 1.05f;
     const float max32 = has_max ? __double2float_ru(max_sq) : __int_as_float(0x7f800000);
     float lim = max32;  // kPrune: min(k-th rounded up, max_sq), refreshed on insertion
+    // kPrune: per-warp survivor buffer (32 entries) after the fp64 query
+    TopK* buf = reinterpret_cast<TopK*>(reinterpret_cast<double*>(wl + (kScanThreads / 32) * k) + D) + wid * 32;
+    uint32_t bcnt = 0;
     for (uint64_t p = 0; p < nprobe; ++p) {
         const uint32_t l = probes[q * nprobe + p];
         const uint64_t beg = offsets[l], end = offsets[l + 1];
@@ -438,6 +476,26 @@ __global__ void __launch_bounds__(kScanThreads) adc_scan_kernel(
                 if (bad) atomicExch(err, 1);
             }
             want = want && pair_less(s64, id, kd, ki);
+            if constexpr (kPrune) {
+                // survivors are appended to the warp's buffer; a full buffer is
+                // sorted and merged into the list (warp_merge_buffer)
+                uint32_t ball = __ballot_sync(0xffffffffu, want);
+                if (ball) {
+                    if (bcnt + uint32_t(__popc(ball)) > 32u) {
+                        warp_merge_buffer(buf, bcnt, my_d, my_id, lane);
+                        bcnt = 0;
+                        kd = __shfl_sync(0xffffffffu, my_d, k - 1);
+                        ki = __shfl_sync(0xffffffffu, my_id, k - 1);
+                        lim = fminf(__double2float_ru(kd), max32);
+                        want = want && pair_less(s64, id, kd, ki);
+                        ball = __ballot_sync(0xffffffffu, want);
+                    }
+                    if (want) buf[bcnt + __popc(ball & ((1u << lane) - 1u))] = TopK{s64, id};
+                    bcnt += uint32_t(__popc(ball));
+                    __syncwarp();
+                }
+                continue;
+            }
             uint32_t ball = __ballot_sync(0xffffffffu, want);
             while (ball) {
                 const int src = __ffs(ball) - 1;
@@ -451,6 +509,9 @@ __global__ void __launch_bounds__(kScanThreads) adc_scan_kernel(
                 if constexpr (kPrune) lim = fminf(__double2float_ru(kd), max32);
             }
         }
+    }
+    if constexpr (kPrune) {
+        if (bcnt) warp_merge_buffer(buf, bcnt, my_d, my_id, lane);
     }
     // merge the warps' lists through shared memory into warp 0
     if (lane < k) wl[wid * k + lane] = TopK{my_d, my_id};
@@ -622,7 +683,8 @@ void ivf_scan(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t 
     if (k > 32) fail(PQG_EUNSUPPORTED, "search: k > 32 is not supported by the warp top-k path");
     const size_t lut_bytes = (sizeof(float) * ix.M * ix.ks + 15) & ~size_t(15);
     const size_t smem = lut_bytes + sizeof(TopK) * k * (kScanThreads / 32) +
-                        sizeof(double) * uint64_t(ix.M) * ix.ds;  // + fp64 query
+                        sizeof(double) * uint64_t(ix.M) * ix.ds +  // fp64 query
+                        sizeof(TopK) * 32 * (kScanThreads / 32);   // survivor buffers
     if (smem > 220 * 1024) fail(PQG_EUNSUPPORTED, "search: M*ks lookup table exceeds shared memory");
     const uint32_t rb = ix.M * ix.w;
     auto run = [&](auto kern) {

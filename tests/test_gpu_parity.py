@@ -629,3 +629,35 @@ def test_umma_screen_variants(pq, orc, mix, monkeypatch, variant, d, k):
     oi, od = orc.nearest_batch(pts, table)
     assert np.array_equal(gi, oi)
     assert np.array_equal(bits(gd), bits(od))
+
+
+@pytest.mark.parametrize("M", [8, 16, 32])
+@pytest.mark.parametrize("k", [1, 10, 32])
+def test_search_ks256_ties_early_exit(pq, orc, M, k):
+    """Ks = 256 byte codes take the scan's partial-sum early exit and the
+    buffered survivor merge: many identical code rows (distance ties broken by
+    id), the max_sq_dist filter, and a subset, all against the oracle."""
+    rng = np.random.default_rng(M * 100 + k)
+    ds = 4
+    tables = orc.random_matrix(M * 256, ds, 11 + M).reshape(M, 256, ds)
+    base = rng.integers(0, 256, size=(60, M), dtype=np.uint8)
+    n = 6000
+    codes_b = base[rng.integers(0, 60, size=n)]
+    ids = rng.permutation(1_000_000)[:n].astype(np.uint64)
+    cb = pq.Codebook(M, 256, ds, np.ascontiguousarray(tables, np.float32))
+    codes = pq.CodeMatrix(n, M, 256, np.ascontiguousarray(codes_b))
+    coarse = pq.pq_decode(cb, pq.CodeMatrix(10, M, 256, np.ascontiguousarray(base[:10])))
+    index = pq.ivf_build_with_centroids(cb, codes, ids, coarse)
+    o_off, o_ids, o_codes = orc.ivf_build_with_centroids(codes.bytes, ids, cb.tables, coarse)
+    q = orc.random_matrix(24, M * ds, 5 + k)
+    for max_sq in (None, float(M) * 0.9):
+        gi, gd, gc = pq.ivf_query_batch(index, q, k, 4, max_sq_dist=max_sq)
+        for i in range(q.shape[0]):
+            ri, rd = orc.ivf_query(cb.tables, coarse, o_off, o_ids, o_codes, q[i], k, 4, max_sq_dist=max_sq)
+            assert np.array_equal(gi[i, : gc[i]], ri) and np.array_equal(bits(gd[i, : gc[i]]), bits(rd))
+    subset = np.sort(ids[rng.choice(n, n // 3, replace=False)])
+    for i in range(8):
+        r = pq.ivf_query_subset(index, q[i], k, subset, 4)
+        ri, rd = orc.ivf_query_subset(cb.tables, coarse, o_off, o_ids, o_codes, q[i], k, subset, 4)
+        assert [h.id for h in r.hits] == ri.tolist()
+        assert np.array_equal(bits(np.array([h.sq_dist for h in r.hits], np.float64)), bits(rd))
