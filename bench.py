@@ -54,9 +54,9 @@ def dist_setup():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if "RANK" in os.environ:  # launched by torchrun (any world size): NCCL process group
-        # keep stdout to the one JSON line (NCCL prints its version banner otherwise)
-        if not os.environ.get("PQG_KEEP_NCCL_DEBUG"):
-            os.environ["NCCL_DEBUG"] = "WARN"
+        # keep stdout to the one JSON line: NCCL's own log (version banner at
+        # NCCL_DEBUG >= VERSION, INFO lines) goes to stderr
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -185,7 +185,7 @@ def run_reference(args, rank, world):
     import oracle
     from paper_2604_21645_b200.datagen import gaussian_mixture
     if not oracle.ref_available():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libpqii_ref.so not built"}))
+        emit({"impl": "reference", "unavailable": "oracle/_ref/libpqii_ref.so not built"})
         return
     R = oracle.ref_impl()
     threads = max(1, R.hardware_concurrency())
@@ -199,7 +199,7 @@ def run_reference(args, rank, world):
         reference_encode_rate(x, tables, threads, rows)
     dt = (time.perf_counter() - t0) / args.steps
     v = rows / dt
-    print(json.dumps({
+    emit({
         "metric": METRIC, "value": v, "unit": "vectors/s", "impl": "reference", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -208,7 +208,7 @@ def run_reference(args, rank, world):
                          "sample": f"pq_encode of {rows} of the 1M rows per step, M={HEAD_M} Ks={HEAD_KS}, "
                                    f"chunk_rows over {threads} threads (proj/src/pipeline.cpp:226-231)"},
         "e2e": {"value": v, "unit": "vectors/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }))
+    })
 
 
 def reference_codebook(x):
@@ -458,7 +458,7 @@ def run_ours(args, rank, world, local):
         "gpu_launches": int(round(launches_per_step * args.steps)),
         "clocks": clk.summary(),
     }
-    print(json.dumps(out))
+    emit(out)
 
 
 def adc_bench(ctx, lib, L, x, train, args, world, stream, timed):
@@ -559,7 +559,26 @@ def adc_bench(ctx, lib, L, x, train, args, world, stream, timed):
             "max_list": int((off[1:] - off[:-1]).max())}
 
 
+_JSON_FD = None
+
+
+def emit(obj):
+    """The one JSON line, written to the process's original stdout."""
+    line = (json.dumps(obj) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(line.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, line)
+
+
 def main():
+    global _JSON_FD
+    # everything else written to fd 1 (library banners such as NCCL's version
+    # line, printed from C at communicator init) goes to stderr
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
