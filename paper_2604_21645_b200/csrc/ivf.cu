@@ -280,7 +280,7 @@ struct CodeRow {
 };
 
 template <int RB, int W, int KS>
-__global__ void __launch_bounds__(kScanThreads) adc_scan_kernel(
+__global__ void __launch_bounds__(kScanThreads, (RB >= 32 ? 5 : 6)) adc_scan_kernel(
     const float* tables, uint32_t M, uint32_t ks, uint32_t ds, const float* queries,
     const uint64_t* offsets, const uint64_t* ids, const uint8_t* codes, const uint32_t* probes,
     uint64_t nprobe, int k, int has_max, double max_sq, const uint64_t* subset, uint64_t nsub,
