@@ -58,7 +58,11 @@ __device__ void bitonic_sort(double* d, uint32_t* ix, int n) {
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(kSelThreads) probe_select_kernel(
+// PER > 0: the query's screened row is read once into registers (PER values
+// per thread, blockDim * PER >= nlist) and the four digit passes and the band
+// test run on them; PER == 0 re-reads the row from global memory per pass.
+template <int PER>
+__global__ void __launch_bounds__(1024) probe_select_kernel(
     const float* mat, uint64_t ld, const float* row_err, const float* queries, uint64_t D,
     const float* coarse, uint64_t nlist, uint64_t nprobe, uint64_t q0, uint32_t* probes,
     uint32_t* overflow, unsigned* n_overflow) {
@@ -72,12 +76,27 @@ __global__ void __launch_bounds__(kSelThreads) probe_select_kernel(
     const float* v = mat + ql * ld;
     const float E = row_err[ql];
     if (threadIdx.x == 0) { s_prefix = 0; s_rank = uint32_t(nprobe); cnt = 0; }
+    float vals[PER > 0 ? PER : 1];
+    if constexpr (PER > 0) {
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const uint64_t j = threadIdx.x + uint64_t(i) * blockDim.x;
+            vals[i] = j < nlist ? __ldg(v + j) : __int_as_float(0x7f800000);
+        }
+    }
     uint32_t mask = 0;
     for (int shift = 24; shift >= 0; shift -= 8) {
         for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
         __syncthreads();
         const uint32_t prefix = s_prefix;
-        for (uint64_t j = threadIdx.x; j < nlist; j += blockDim.x) {
+        if constexpr (PER > 0) {
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const uint64_t j = threadIdx.x + uint64_t(i) * blockDim.x;
+                const uint32_t bits = __float_as_uint(vals[i]);
+                if (j < nlist && (bits & mask) == prefix) atomicAdd(&hist[(bits >> shift) & 255u], 1u);
+            }
+        } else for (uint64_t j = threadIdx.x; j < nlist; j += blockDim.x) {
             const uint32_t bits = __float_as_uint(v[j]);
             if ((bits & mask) == prefix) atomicAdd(&hist[(bits >> shift) & 255u], 1u);
         }
@@ -111,7 +130,16 @@ __global__ void __launch_bounds__(kSelThreads) probe_select_kernel(
     }
     const float tau = __uint_as_float(s_prefix);
     const float band = tau + 2.05f * E;
-    for (uint64_t j = threadIdx.x; j < nlist; j += blockDim.x) {
+    if constexpr (PER > 0) {
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const uint64_t j = threadIdx.x + uint64_t(i) * blockDim.x;
+            if (j < nlist && vals[i] <= band) {
+                const unsigned p = atomicAdd(&cnt, 1u);
+                if (p < kCandCap) cand[p] = uint32_t(j);
+            }
+        }
+    } else for (uint64_t j = threadIdx.x; j < nlist; j += blockDim.x) {
         if (v[j] <= band) {
             const unsigned p = atomicAdd(&cnt, 1u);
             if (p < kCandCap) cand[p] = uint32_t(j);
@@ -665,9 +693,19 @@ void ivf_probe(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t
         a.ld_mat = ix.nlist;
         a.row_err = rerr;
         distance_matrix(ctx, a);
-        launch(ctx, "probe_select", probe_select_kernel, dim3(unsigned(nc)), dim3(kSelThreads), 0,
-               (const float*)mat, ix.nlist, (const float*)rerr, queries, D, ix.coarse, ix.nlist,
-               nprobe, q0, probes, overflow, n_over);
+        // 16 screened values per thread in registers (nlist <= 16384), else
+        // the row is re-read per pass
+        constexpr int kPer = 16;
+        if (ix.nlist <= uint64_t(kPer) * 1024) {
+            const unsigned th = unsigned(std::max<uint64_t>(kSelThreads, (ix.nlist + kPer * 32 - 1) / (kPer * 32) * 32));
+            launch(ctx, "probe_select", probe_select_kernel<kPer>, dim3(unsigned(nc)), dim3(th), 0,
+                   (const float*)mat, ix.nlist, (const float*)rerr, queries, D, ix.coarse, ix.nlist,
+                   nprobe, q0, probes, overflow, n_over);
+        } else {
+            launch(ctx, "probe_select", probe_select_kernel<0>, dim3(unsigned(nc)), dim3(kSelThreads), 0,
+                   (const float*)mat, ix.nlist, (const float*)rerr, queries, D, ix.coarse, ix.nlist,
+                   nprobe, q0, probes, overflow, n_over);
+        }
     }
     const unsigned fb_blocks = 64;
     double* sd = scratch<double>(ctx, uint64_t(fb_blocks) * ix.nlist);
