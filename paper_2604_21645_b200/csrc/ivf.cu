@@ -32,6 +32,7 @@ __device__ __forceinline__ uint32_t code_at(const uint8_t* p, uint32_t m, uint32
 // ---------------------------------------------------------------------------
 constexpr int kSelThreads = 64;  // one query per CTA; small CTAs keep ~32 queries in flight per SM
 constexpr int kCandCap = 256;
+constexpr int kProbeQD = 512;  // query dims staged in fp64 by the probe select
 
 __device__ __forceinline__ bool pair_less(double a, uint64_t ia, double b, uint64_t ib) {
     return a < b || (a == b && ia < ib);
@@ -154,9 +155,41 @@ __global__ void __launch_bounds__(1024) probe_select_kernel(
     int n2 = 1;
     while (n2 < int(c)) n2 <<= 1;
     const float* qv = queries + q * D;
+    // squared_l2 (proj/src/kmeans.cpp:11-18) per band candidate: the query in
+    // fp64 staged once (shared), each coarse row read 32 coordinates per batch
+    // of independent loads (the load latency, not the dadd chain, bounds it)
+    __shared__ double qd[kProbeQD];
+    const bool staged = D <= uint64_t(kProbeQD) && (D & 3u) == 0 &&
+                        (reinterpret_cast<uintptr_t>(coarse) & 15u) == 0;
+    if (staged)
+        for (uint64_t t = threadIdx.x; t < D; t += blockDim.x) qd[t] = (double)qv[t];
+    __syncthreads();
     for (int t = threadIdx.x; t < n2; t += blockDim.x) {
-        if (t < int(c)) cd[t] = exact_sq_l2(qv, coarse + uint64_t(cand[t]) * D, int(D));
-        else { cd[t] = __longlong_as_double(0x7ff0000000000000LL); cand[t] = 0xFFFFFFFFu; }
+        if (t < int(c)) {
+            const float* row = coarse + uint64_t(cand[t]) * D;
+            if (staged) {
+                double acc = 0.0;
+                for (uint32_t t0 = 0; t0 < uint32_t(D); t0 += 32) {
+                    float cv[32];
+#pragma unroll
+                    for (int u = 0; u < 32; u += 4) {
+                        const float4 f = t0 + u < D ? __ldg(reinterpret_cast<const float4*>(row + t0 + u))
+                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+                        cv[u] = f.x; cv[u + 1] = f.y; cv[u + 2] = f.z; cv[u + 3] = f.w;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) {
+                        if (t0 + u < D) {
+                            const double diff = __dsub_rn(qd[t0 + u], (double)cv[u]);
+                            acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+                        }
+                    }
+                }
+                cd[t] = acc;
+            } else {
+                cd[t] = exact_sq_l2(qv, row, int(D));
+            }
+        } else { cd[t] = __longlong_as_double(0x7ff0000000000000LL); cand[t] = 0xFFFFFFFFu; }
     }
     bitonic_sort(cd, cand, n2);
     for (uint64_t p = threadIdx.x; p < nprobe; p += blockDim.x) probes[q * nprobe + p] = cand[p];
