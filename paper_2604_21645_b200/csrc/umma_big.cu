@@ -277,9 +277,18 @@ __global__ void __launch_bounds__(192, 1) big_kernel(NearestArgs a, const uint8_
                     if constexpr (MAT) {
                         if (row < a.n) {
                             float* o = a.out_mat + row * a.ld_mat + col0;
+                            if (col0 + 32 <= a.k && ((reinterpret_cast<uintptr_t>(o) & 15u) == 0)) {
+                                // the row's 128-byte chunk as eight 16-byte stores
 #pragma unroll
-                            for (int j = 0; j < 32; ++j)
-                                if (col0 + j < a.k) o[j] = __uint_as_float(r[j]);
+                                for (int j = 0; j < 32; j += 4)
+                                    *reinterpret_cast<float4*>(o + j) =
+                                        make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                                    __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < 32; ++j)
+                                    if (col0 + j < a.k) o[j] = __uint_as_float(r[j]);
+                            }
                         }
                     } else {
 #pragma unroll
