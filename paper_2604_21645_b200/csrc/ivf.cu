@@ -377,7 +377,38 @@ __global__ void __launch_bounds__(kScanThreads, (RB >= 32 ? 5 : 6)) adc_scan_ker
         double* qd = reinterpret_cast<double*>(wl + (kScanThreads / 32) * k);
         for (uint32_t t = threadIdx.x; t < D; t += blockDim.x) qd[t] = (double)qv[t];
         __syncthreads();
-        for (uint32_t m = 0; m < M; ++m) {
+        const bool pf = (ds == 8 || ds == 4) && ks <= blockDim.x &&
+                        (reinterpret_cast<uintptr_t>(tables) & 15u) == 0;
+        if (pf) {
+            // Ds <= 8 (one codeword = 1-2 float4): each thread owns codeword j
+            // of every subspace and loads subspace m+1's codeword while it
+            // computes subspace m's entry (the load latency stays hidden)
+            const uint32_t j = threadIdx.x;
+            if (j < ks) {
+                const uint32_t nv = ds / 4;
+                const float4* cp = reinterpret_cast<const float4*>(tables) + uint64_t(j) * nv;
+                const uint64_t mstride = uint64_t(ks) * nv;
+                float4 n0 = __ldg(cp), n1 = nv > 1 ? __ldg(cp + 1) : n0;
+                for (uint32_t m = 0; m < M; ++m) {
+                    const float4 u0 = n0, u1 = n1;
+                    if (m + 1 < M) {
+                        n0 = __ldg(cp + (m + 1) * mstride);
+                        if (nv > 1) n1 = __ldg(cp + (m + 1) * mstride + 1);
+                    }
+                    const float cc[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+                    const double* qm = qd + m * ds;
+                    double acc = 0.0;
+#pragma unroll
+                    for (int v = 0; v < 8; ++v) {
+                        if (uint32_t(v) < ds) {
+                            const double diff = __dsub_rn(qm[v], (double)cc[v]);
+                            acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+                        }
+                    }
+                    lut[m * ks + j] = __double2float_rn(acc);
+                }
+            }
+        } else for (uint32_t m = 0; m < M; ++m) {
             const double* qm = qd + m * ds;
             for (uint32_t j = threadIdx.x; j < ks; j += blockDim.x) {
                 const float* c = tables + (uint64_t(m) * ks + j) * ds;
