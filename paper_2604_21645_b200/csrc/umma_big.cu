@@ -58,14 +58,34 @@ __device__ __forceinline__ float row_x(const RowSrc& s, uint64_t i, uint32_t t) 
 // whole sectors and every interleaved 128-byte core-matrix line is written by
 // one warp instruction.
 __global__ void row_norms_kernel(RowSrc src, uint64_t n, uint32_t d, float* nxrow) {
-    for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
-         r += uint64_t(gridDim.x) * blockDim.x) {
+    // a warp per row, coalesced loads, tree-reduced: ||x||^2 only feeds C_r
+    // and the error bound E_r, whose margins cover any summation order (the
+    // split and the epilogue read the same stored value)
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t w0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    const bool vec = !src.codes && (d & 3u) == 0 && (src.ldx & 3u) == 0 &&
+                     (reinterpret_cast<uintptr_t>(src.x) & 15u) == 0;
+    for (uint64_t r = w0; r < n; r += nw) {
         float nx = 0.f;
-        for (uint32_t t = 0; t < d; ++t) {
-            const float v = row_x(src, r, t);
-            nx = fmaf(v, v, nx);
+        if (vec) {
+            const float4* xp = reinterpret_cast<const float4*>(src.x + r * src.ldx);
+            for (uint32_t t4 = lane; t4 < d / 4; t4 += 32) {
+                const float4 v = __ldg(xp + t4);
+                nx = fmaf(v.x, v.x, nx);
+                nx = fmaf(v.y, v.y, nx);
+                nx = fmaf(v.z, v.z, nx);
+                nx = fmaf(v.w, v.w, nx);
+            }
+        } else {
+            for (uint32_t t = lane; t < d; t += 32) {
+                const float v = row_x(src, r, t);
+                nx = fmaf(v, v, nx);
+            }
         }
-        nxrow[r] = nx;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) nx += __shfl_xor_sync(0xffffffffu, nx, off);
+        if (lane == 0) nxrow[r] = nx;
     }
 }
 
@@ -375,8 +395,8 @@ bool umma_big_prepare_rows(pqg_ctx* ctx, NearestArgs& a) {
     const uint64_t ntiles = (a.n + kR - 1) / kR;
     uint8_t* Am = scratch<uint8_t>(ctx, ntiles * kchunks * 2 * kAChunk);
     float* nx = scratch<float>(ctx, a.n);
-    launch(ctx, "big_split", row_norms_kernel, dim3(grid1d(a.n, 128, 1u << 20)), dim3(128), 0, a.src, a.n,
-           a.d, nx);
+    launch(ctx, "big_split", row_norms_kernel, dim3(grid1d(a.n * 32, 256, 1u << 20)), dim3(256), 0, a.src,
+           a.n, a.d, nx);
     launch(ctx, "big_split", split_rows_kernel, dim3(grid1d(ntiles * kR * kchunks * (kKC / 4), 256, 1u << 20)),
            dim3(256), 0, a.src, a.n, a.d, kchunks, a.cmax, 0, Am, (const float*)nx);
     a.big_rows = Am;
@@ -413,7 +433,7 @@ void umma_big(pqg_ctx* ctx, const NearestArgs& a0) {
         const uint64_t ntiles = (a.n + kR - 1) / kR;
         uint8_t* Am = scratch<uint8_t>(ctx, ntiles * kchunks * 2 * kAChunk);
         float* nx = scratch<float>(ctx, a.n);
-        launch(ctx, "big_split", row_norms_kernel, dim3(grid1d(a.n, 128, 1u << 20)), dim3(128), 0, a.src,
+        launch(ctx, "big_split", row_norms_kernel, dim3(grid1d(a.n * 32, 256, 1u << 20)), dim3(256), 0, a.src,
                a.n, a.d, nx);
         launch(ctx, "big_split", split_rows_kernel,
                dim3(grid1d(ntiles * kR * kchunks * (kKC / 4), 256, 1u << 20)), dim3(256), 0, a.src, a.n, a.d,
