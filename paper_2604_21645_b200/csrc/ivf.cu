@@ -455,6 +455,9 @@ __global__ void __launch_bounds__(kScanThreads, (RB >= 32 ? 5 : 6)) adc_scan_ker
     const float shrink_p = 1.0f - float(M + 4) * kU * 1.05f;
     const float max32 = has_max ? __double2float_ru(max_sq) : __int_as_float(0x7f800000);
     float lim = max32;  // kPrune: min(k-th rounded up, max_sq), refreshed on insertion
+    // the exit test compares the raw fp32 partial sum with lim / shrink_p
+    // rounded up: sum > lim_p implies sum * shrink_p > lim in exact arithmetic
+    float lim_p = __fdiv_ru(lim, shrink_p);
     // kPrune: per-warp survivor buffer (32 entries) after the fp64 query
     TopK* buf = reinterpret_cast<TopK*>(reinterpret_cast<double*>(wl + (kScanThreads / 32) * k) + D) + wid * 32;
     uint32_t bcnt = 0;
@@ -487,7 +490,7 @@ __global__ void __launch_bounds__(kScanThreads, (RB >= 32 ? 5 : 6)) adc_scan_ker
 #pragma unroll
                 for (int g = 0; g < MM; g += GS) {
                     if (g > 0) {
-                        live = live && !((s_even + s_odd) * shrink_p > lim);
+                        live = live && !(s_even + s_odd > lim_p);
                         if (!__any_sync(0xffffffffu, live)) break;
                     }
                     if (live) {
@@ -579,6 +582,7 @@ __global__ void __launch_bounds__(kScanThreads, (RB >= 32 ? 5 : 6)) adc_scan_ker
                         kd = __shfl_sync(0xffffffffu, my_d, k - 1);
                         ki = __shfl_sync(0xffffffffu, my_id, k - 1);
                         lim = fminf(__double2float_ru(kd), max32);
+                        lim_p = __fdiv_ru(lim, shrink_p);
                         want = want && pair_less(s64, id, kd, ki);
                         ball = __ballot_sync(0xffffffffu, want);
                     }
@@ -598,7 +602,10 @@ __global__ void __launch_bounds__(kScanThreads, (RB >= 32 ? 5 : 6)) adc_scan_ker
                 ki = __shfl_sync(0xffffffffu, my_id, k - 1);
                 want = want && lane != src && pair_less(s64, id, kd, ki);
                 ball = __ballot_sync(0xffffffffu, want);
-                if constexpr (kPrune) lim = fminf(__double2float_ru(kd), max32);
+                if constexpr (kPrune) {
+                    lim = fminf(__double2float_ru(kd), max32);
+                    lim_p = __fdiv_ru(lim, shrink_p);
+                }
             }
         }
     }
