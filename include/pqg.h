@@ -48,7 +48,16 @@ void pqg_ctx_destroy(pqg_ctx* ctx);
 /* Run on a caller-owned cudaStream_t (NULL restores the context's own;
  * (void*)1 is cudaStreamLegacy, the default stream of other libraries). */
 int pqg_ctx_set_stream(pqg_ctx* ctx, void* cuda_stream);
+/* (Switching streams makes the new stream wait for the work already queued
+ * on the old one, whose scratch the context reuses.) */
+/* The cudaStream_t the context currently launches on. */
+void* pqg_ctx_stream(pqg_ctx* ctx);
+/* Synchronise the context stream; also reports (PQG_ERANGE) an out-of-range
+ * code found by a search whose outputs all stayed on the device. */
 int pqg_ctx_sync(pqg_ctx* ctx);
+/* Report (PQG_ERANGE, then clear) a pending out-of-range code flagged by a
+ * device-output search (adc_lookup's std::out_of_range, pq.cpp:160-163). */
+int pqg_ctx_check_errors(pqg_ctx* ctx);
 const char* pqg_last_error(void);
 /* Number of kernels this context has launched (bench.py's gpu_launches). */
 uint64_t pqg_ctx_launches(pqg_ctx* ctx);
@@ -83,6 +92,11 @@ int pqg_kmeans_fit(pqg_ctx* ctx, const float* points, uint64_t n, uint64_t d, ui
 int pqg_pq_fit(pqg_ctx* ctx, const float* data, uint64_t n, uint64_t D, uint32_t M,
                uint32_t ks, uint32_t max_iters, uint64_t seed, float* tables,
                uint32_t* iterations_run, double* inertia);
+/* pq_fit plus each subspace's inertia_per_iter (kmeans.hpp:19): M*max_iters
+ * fp64, row m valid for its first iterations_run[m] entries (the rest 0). */
+int pqg_pq_fit_ex(pqg_ctx* ctx, const float* data, uint64_t n, uint64_t D, uint32_t M,
+                  uint32_t ks, uint32_t max_iters, uint64_t seed, float* tables,
+                  uint32_t* iterations_run, double* inertia, double* inertia_per_iter);
 /* pq_encode (pq.cpp:95-111): codes n*M*width. */
 int pqg_pq_encode(pqg_ctx* ctx, const float* data, uint64_t n, uint32_t M, uint32_t ks,
                   uint32_t ds, const float* tables, uint8_t* codes);

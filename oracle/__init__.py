@@ -42,6 +42,27 @@ def code_width(ks: int) -> int:
     return 1 if ks <= 256 else 2
 
 
+def default_threads() -> int:
+    return max(1, os.cpu_count() or 1)
+
+
+def pmap(fn, items, threads: int):
+    """Run fn over items on `threads` Python threads.  ctypes drops the GIL for
+    every call into the checkers, so independent calls (subspace fits, row
+    chunks, queries) run in parallel; results come back in item order."""
+    items = list(items)
+    if threads <= 1 or len(items) <= 1:
+        return [fn(it) for it in items]
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(threads, len(items))) as ex:
+        return list(ex.map(fn, items))
+
+
+def row_chunks(n: int, parts: int):
+    parts = max(1, min(parts, n))
+    return [(n * t // parts, n * (t + 1) // parts) for t in range(parts)]
+
+
 class _Base:
     def __init__(self, path: str, prefix: str):
         if not os.path.exists(path):
@@ -79,17 +100,33 @@ class COracle(_Base):
         b = np.ascontiguousarray(b, np.float32)
         return self.fn("squared_l2", C.c_double, [_f32p, _f32p, _u64])(a, b, a.size)
 
-    def nearest_batch(self, points, table):
+    def nearest_batch(self, points, table, threads=1):
         points = np.ascontiguousarray(points, np.float32)
         table = np.ascontiguousarray(table, np.float32)
         n, d = points.shape
         idx = np.empty(n, np.uint32)
         dist = np.empty(n, np.float64)
-        self.fn("nearest_batch", None, [_f32p, _u64, _u64, _f32p, _u64, _u32p, _f64p])(
-            points, n, d, table, table.shape[0], idx, dist)
+        self.fn("nearest_batch_mt", None,
+                [_f32p, _u64, _u64, _f32p, _u64, _u32p, _f64p, C.c_int])(
+            points, n, d, table, table.shape[0], idx, dist, int(threads))
         return idx, dist
 
-    def kmeans_fit(self, points, k, max_iters=20, seed=0, tol=1e-4):
+    def lloyd_update(self, points, assignments, dists, centroids):
+        """One update step (kmeans.cpp:102-130) from given assignments and
+        fp64 distances: returns (new centroids, dists after the reseeds)."""
+        points = np.ascontiguousarray(points, np.float32)
+        n, d = points.shape
+        cent = np.array(centroids, np.float32, copy=True, order="C")
+        dist = np.array(dists, np.float64, copy=True, order="C")
+        rc = self.fn("lloyd_update", C.c_int, [_f32p, _u64, _u64, _u64, _u32p, _f64p, _f32p])(
+            points, n, d, cent.shape[0], np.ascontiguousarray(assignments, np.uint32), dist, cent)
+        if rc:
+            raise ValueError(f"lloyd_update rc={rc}")
+        return cent, dist
+
+    def kmeans_fit(self, points, k, max_iters=20, seed=0, tol=1e-4, threads=1):
+        """kmeans_fit (kmeans.cpp:61-133); threads > 1 splits the assignment
+        pass's rows only (bit-identical for every thread count)."""
         points = np.ascontiguousarray(points, np.float32)
         n, d = points.shape
         cent = np.empty((k, d), np.float32)
@@ -97,11 +134,11 @@ class COracle(_Base):
         inertia = C.c_double()
         iters = C.c_uint32()
         per = np.zeros(max(1, max_iters), np.float64)
-        rc = self.fn("kmeans_fit", C.c_int,
+        rc = self.fn("kmeans_fit_mt", C.c_int,
                      [_f32p, _u64, _u64, _u64, _u32, _u64, C.c_double, _f32p, _u32p,
-                      C.POINTER(C.c_double), C.POINTER(C.c_uint32), _f64p])(
+                      C.POINTER(C.c_double), C.POINTER(C.c_uint32), _f64p, C.c_int])(
             points, n, d, k, max_iters, seed, tol, cent, assign, C.byref(inertia),
-            C.byref(iters), per)
+            C.byref(iters), per, int(threads))
         if rc:
             raise ValueError(f"kmeans_fit rc={rc}")
         return dict(centroids=cent, assignments=assign, inertia=inertia.value,
@@ -182,6 +219,47 @@ class COracle(_Base):
             codes, n, M, ks, ds, tables, coarse, coarse.shape[0], out)
         if rc:
             raise ValueError(f"ivf_assign rc={rc}")
+        return out
+
+    def ivf_assign_mt(self, codes, tables, coarse, threads):
+        codes = np.ascontiguousarray(codes, np.uint8)
+        parts = pmap(lambda r: self.ivf_assign(codes[r[0]:r[1]], tables, coarse),
+                     row_chunks(codes.shape[0], 4 * threads), threads)
+        return np.concatenate(parts) if parts else np.empty(0, np.uint32)
+
+    def pq_encode_mt(self, data, tables, threads):
+        parts = pmap(lambda r: self.pq_encode(data[r[0]:r[1]], tables),
+                     row_chunks(data.shape[0], 4 * threads), threads)
+        return np.concatenate(parts)
+
+    def ivf_query_mt(self, tables, coarse, offsets, list_ids, list_codes, queries, k, nprobe,
+                     threads, max_sq_dist=None):
+        """ivf_query per query on `threads` threads: (ids nq x k, dists, counts)."""
+        nq = queries.shape[0]
+        ids = np.zeros((nq, k), np.uint64)
+        dist = np.zeros((nq, k), np.float64)
+        cnt = np.zeros(nq, np.uint32)
+        tables = np.ascontiguousarray(tables, np.float32)
+        coarse = np.ascontiguousarray(coarse, np.float32)
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        list_ids = np.ascontiguousarray(list_ids, np.uint64)
+        list_codes = np.ascontiguousarray(list_codes, np.uint8)
+
+        def one(q):
+            i, d = self.ivf_query(tables, coarse, offsets, list_ids, list_codes, queries[q], k,
+                                  nprobe, max_sq_dist)
+            ids[q, : i.size] = i
+            dist[q, : i.size] = d
+            cnt[q] = i.size
+        pmap(one, range(nq), threads)
+        return ids, dist, cnt
+
+    def probe_order_mt(self, coarse, queries, nprobe, threads):
+        out = np.empty((queries.shape[0], nprobe), np.uint32)
+
+        def one(q):
+            out[q] = self.probe_order(coarse, queries[q], nprobe)
+        pmap(one, range(queries.shape[0]), threads)
         return out
 
     def ivf_csr(self, list_of, ids, codes, nlist):
@@ -417,6 +495,48 @@ class RefImpl(_Base):
         self._check(rc, "pq_fit")
         return tables
 
+    def pq_fit_stats(self, data, M, ks, max_iters=20, seed=0, threads=1):
+        """pq_fit (pq.cpp:63-93) = one reference kmeans_fit(slice_m, ks,
+        max_iters, seed + m) per subspace with the default tol, the M fits run
+        on `threads` threads (kmeans_fit is safe for concurrent disjoint fits,
+        kmeans.hpp:40).  Returns (tables, iterations_run[M],
+        inertia_per_iter[M][max_iters] (NaN past iterations_run))."""
+        fits = self.kmeans_fit_many([(np.ascontiguousarray(data[:, m * (data.shape[1] // M):
+                                                                 (m + 1) * (data.shape[1] // M)]),
+                                      ks, max_iters, seed + m) for m in range(M)], threads)
+        return stack_fits(fits, max_iters)
+
+    def kmeans_fit_many(self, problems, threads):
+        """Independent reference kmeans_fit calls (points, k, iters, seed)
+        spread over threads, biggest first."""
+        order = sorted(range(len(problems)),
+                       key=lambda i: -problems[i][0].shape[0] * problems[i][1] * problems[i][0].shape[1])
+        res = pmap(lambda i: self.kmeans_fit(*problems[i]), order, threads)
+        out = [None] * len(problems)
+        for i, r in zip(order, res):
+            out[i] = r
+        return out
+
+    def nearest_batch_mt(self, points, table, threads):
+        parts = pmap(lambda r: self.nearest_batch(points[r[0]:r[1]], table),
+                     row_chunks(points.shape[0], 4 * threads), threads)
+        return np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts])
+
+    def ivf_build_with_centroids_mt(self, codes, ids, tables, coarse, threads):
+        """ivf_build_with_centroids over chunk_rows ranges on threads, the
+        chunk indexes combined by the reference's own ivf_merge in chunk order
+        (list l = chunk 0's then chunk 1's ..., ivf.cpp:203-211) -- the
+        monolithic build (acceptance criterion 5)."""
+        parts = pmap(lambda r: self.ivf_build_with_centroids(codes[r[0]:r[1]], ids[r[0]:r[1]],
+                                                             tables, coarse),
+                     row_chunks(codes.shape[0], threads), threads)
+        while len(parts) > 1:  # pairwise, order preserving
+            nxt = pmap(lambda i: parts[i].merge(parts[i + 1]), range(0, len(parts) - 1, 2), threads)
+            if len(parts) % 2:
+                nxt.append(parts[-1])
+            parts = nxt
+        return parts[0]
+
     def pq_encode(self, data, tables, threads=1):
         data = np.ascontiguousarray(data, np.float32)
         tables = np.ascontiguousarray(tables, np.float32)
@@ -578,6 +698,17 @@ class RefImpl(_Base):
             off, lid, lcodes, coarse = hd.export()
             out.update(offsets=off, list_ids=lid, list_codes=lcodes, coarse=coarse)
         return out
+
+
+def stack_fits(fits, max_iters):
+    """Per-subspace kmeans_fit results -> (tables[M][ks][ds], iters[M],
+    inertia_per_iter[M][max_iters] NaN-padded)."""
+    tables = np.stack([f["centroids"] for f in fits])
+    iters = np.array([f["iterations_run"] for f in fits], np.uint32)
+    per = np.full((len(fits), max_iters), np.nan)
+    for m, f in enumerate(fits):
+        per[m, : f["iterations_run"]] = f["inertia_per_iter"]
+    return tables, iters, per
 
 
 class RefIndexHandle:

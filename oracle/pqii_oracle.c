@@ -20,6 +20,7 @@
  *   (c) the reference's own known-answer tests (test_kmeans.cpp, test_pq.cpp).
  */
 #include <math.h>
+#include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -152,21 +153,103 @@ void orc_nearest_batch(const float* points, uint64_t n, uint64_t d, const float*
 }
 
 /* ------------------------------------------------------------------------ */
+/* Threaded helpers (parity at BASELINE sizes).  Each row's nearest centroid */
+/* is computed exactly as above, independently of the others; the threads   */
+/* only split the row range, and every order-dependent reduction (inertia,   */
+/* sums) stays sequential on the calling thread, so results are bit-identical */
+/* to the single-threaded restatement for any thread count.                  */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    const float* points;
+    const float* table;
+    uint64_t b, e, d, k;
+    uint32_t* index;
+    double* sq_dist;
+} orc_nb_task;
+
+static void* nb_worker(void* p) {
+    const orc_nb_task* t = (const orc_nb_task*)p;
+    orc_nearest_batch(t->points + t->b * t->d, t->e - t->b, t->d, t->table, t->k,
+                      t->index + t->b, t->sq_dist + t->b);
+    return NULL;
+}
+
+void orc_nearest_batch_mt(const float* points, uint64_t n, uint64_t d, const float* table,
+                          uint64_t k, uint32_t* index, double* sq_dist, int threads) {
+    if (threads > 256) threads = 256;
+    if (threads < 2 || n < 2 * (uint64_t)threads) {
+        orc_nearest_batch(points, n, d, table, k, index, sq_dist);
+        return;
+    }
+    pthread_t tid[256];
+    orc_nb_task task[256];
+    for (int t = 0; t < threads; ++t) {
+        task[t] = (orc_nb_task){points, table, n * t / threads, n * (t + 1) / threads, d, k, index,
+                                sq_dist};
+        pthread_create(&tid[t], NULL, nb_worker, &task[t]);
+    }
+    for (int t = 0; t < threads; ++t) pthread_join(tid[t], NULL);
+}
+
+/* The update step of proj/src/kmeans.cpp:102-130 given one pass's
+ * assignments and fp64 distances: fp64 sums in row order, mean =
+ * float(sum * (1/count)) for non-empty clusters, then each empty cluster in
+ * ascending order takes the row of the (strict '>') largest pre-update
+ * distance and zeroes it.  centroids and dists are updated in place; also the
+ * parity checker for one Lloyd step from the GPU's centroids. */
+int orc_lloyd_update(const float* points, uint64_t n, uint64_t d, uint64_t k,
+                     const uint32_t* assignments, double* dists, float* centroids) {
+    double* sums = (double*)calloc(k * d, sizeof(double));
+    uint64_t* counts = (uint64_t*)calloc(k, sizeof(uint64_t));
+    if (!sums || !counts) {
+        free(sums); free(counts);
+        return ORC_ENOMEM;
+    }
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint32_t c = assignments[i];
+        if (c >= k) {
+            free(sums); free(counts);
+            return ORC_ERANGE;
+        }
+        const float* row = points + i * d;
+        double* s = sums + (uint64_t)c * d;
+        for (uint64_t j = 0; j < d; ++j) s[j] += row[j];
+        ++counts[c];
+    }
+    for (uint64_t c = 0; c < k; ++c) {
+        if (counts[c] == 0) continue;
+        const double inv = 1.0 / (double)counts[c];
+        for (uint64_t j = 0; j < d; ++j) centroids[c * d + j] = (float)(sums[c * d + j] * inv);
+    }
+    for (uint64_t c = 0; c < k; ++c) {
+        if (counts[c] != 0) continue;
+        uint64_t far = 0;
+        for (uint64_t i = 1; i < n; ++i)
+            if (dists[i] > dists[far]) far = i;
+        memcpy(centroids + c * d, points + far * d, d * sizeof(float));
+        dists[far] = 0.0;
+    }
+    free(sums);
+    free(counts);
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------ */
 /* Lloyd k-means: proj/src/kmeans.cpp:61-133                                 */
 /* ------------------------------------------------------------------------ */
-int orc_kmeans_fit(const float* points, uint64_t n, uint64_t d, uint64_t k, uint32_t max_iters,
-                   uint64_t seed, double tol, float* centroids, uint32_t* assignments,
-                   double* inertia_out, uint32_t* iterations_run, double* inertia_per_iter) {
+/* threads > 1 splits only the assignment pass's rows (see above). */
+int orc_kmeans_fit_mt(const float* points, uint64_t n, uint64_t d, uint64_t k, uint32_t max_iters,
+                      uint64_t seed, double tol, float* centroids, uint32_t* assignments,
+                      double* inertia_out, uint32_t* iterations_run, double* inertia_per_iter,
+                      int threads) {
     /* validation, :65-71 */
     if (k == 0 || k > n || max_iters < 1 || tol < 0.0) return ORC_EINVAL;
 
     /* init: k distinct rows by partial Fisher-Yates, :73-88 */
     uint64_t* idx = (uint64_t*)malloc(n * sizeof(uint64_t));
     double* dists = (double*)malloc(n * sizeof(double));
-    double* sums = (double*)malloc(k * d * sizeof(double));
-    uint64_t* counts = (uint64_t*)malloc(k * sizeof(uint64_t));
-    if (!idx || !dists || !sums || !counts) {
-        free(idx); free(dists); free(sums); free(counts);
+    if (!idx || !dists) {
+        free(idx); free(dists);
         return ORC_ENOMEM;
     }
     orc_mt64 g;
@@ -179,20 +262,16 @@ int orc_kmeans_fit(const float* points, uint64_t n, uint64_t d, uint64_t k, uint
         idx[j] = t;
     }
     for (uint64_t c = 0; c < k; ++c) memcpy(centroids + c * d, points + idx[c] * d, d * sizeof(float));
+    free(idx);
 
     double inertia = 0.0, prev = 0.0;
     uint32_t it_run = 0;
+    int rc = ORC_OK;
     for (uint32_t it = 1; it <= max_iters; ++it) {
-        /* assign pass, :46-57 */
+        /* assign pass, :46-57; inertia summed sequentially in row order */
+        orc_nearest_batch_mt(points, n, d, centroids, k, assignments, dists, threads);
         inertia = 0.0;
-        for (uint64_t i = 0; i < n; ++i) {
-            uint64_t best;
-            double bd;
-            orc_nearest_in_table(points + i * d, centroids, k, d, &best, &bd);
-            assignments[i] = (uint32_t)best;
-            dists[i] = bd;
-            inertia += bd;
-        }
+        for (uint64_t i = 0; i < n; ++i) inertia += dists[i];
         if (inertia_per_iter) inertia_per_iter[it - 1] = inertia;
         it_run = it;
         /* stop rules, :98-100 */
@@ -200,36 +279,21 @@ int orc_kmeans_fit(const float* points, uint64_t n, uint64_t d, uint64_t k, uint
         if (it > 1 && prev - inertia < tol * floor1) break;
         if (it == max_iters) break;
         prev = inertia;
-
-        /* update: fp64 sums in row order, mean = float(sum * (1/count)), :102-118 */
-        memset(sums, 0, k * d * sizeof(double));
-        memset(counts, 0, k * sizeof(uint64_t));
-        for (uint64_t i = 0; i < n; ++i) {
-            const uint32_t c = assignments[i];
-            const float* row = points + i * d;
-            double* s = sums + (uint64_t)c * d;
-            for (uint64_t j = 0; j < d; ++j) s[j] += row[j];
-            ++counts[c];
-        }
-        for (uint64_t c = 0; c < k; ++c) {
-            if (counts[c] == 0) continue;
-            const double inv = 1.0 / (double)counts[c];
-            for (uint64_t j = 0; j < d; ++j) centroids[c * d + j] = (float)(sums[c * d + j] * inv);
-        }
-        /* empty-cluster reseed on pre-update dists, ascending c, :122-130 */
-        for (uint64_t c = 0; c < k; ++c) {
-            if (counts[c] != 0) continue;
-            uint64_t far = 0;
-            for (uint64_t i = 1; i < n; ++i)
-                if (dists[i] > dists[far]) far = i;
-            memcpy(centroids + c * d, points + far * d, d * sizeof(float));
-            dists[far] = 0.0;
-        }
+        /* update + empty-cluster reseed, :102-130 */
+        rc = orc_lloyd_update(points, n, d, k, assignments, dists, centroids);
+        if (rc) break;
     }
     *inertia_out = inertia;
     *iterations_run = it_run;
-    free(idx); free(dists); free(sums); free(counts);
-    return ORC_OK;
+    free(dists);
+    return rc;
+}
+
+int orc_kmeans_fit(const float* points, uint64_t n, uint64_t d, uint64_t k, uint32_t max_iters,
+                   uint64_t seed, double tol, float* centroids, uint32_t* assignments,
+                   double* inertia_out, uint32_t* iterations_run, double* inertia_per_iter) {
+    return orc_kmeans_fit_mt(points, n, d, k, max_iters, seed, tol, centroids, assignments,
+                             inertia_out, iterations_run, inertia_per_iter, 1);
 }
 
 /* ------------------------------------------------------------------------ */

@@ -32,6 +32,8 @@ _SIGS = {
     "pqg_ctx_destroy": (None, [_vp]),
     "pqg_ctx_set_stream": (_i32, [_vp, _vp]),
     "pqg_ctx_sync": (_i32, [_vp]),
+    "pqg_ctx_stream": (_vp, [_vp]),
+    "pqg_ctx_check_errors": (_i32, [_vp]),
     "pqg_last_error": (C.c_char_p, []),
     "pqg_ctx_launches": (_u64, [_vp]),
     "pqg_profile_enable": (_i32, [_vp, _i32]),
@@ -42,6 +44,7 @@ _SIGS = {
     "pqg_kmeans_fit": (_i32, [_vp, _vp, _u64, _u64, _u64, _u32, _u64, _f64, _vp, _vp,
                               C.POINTER(_f64), C.POINTER(_u32), _vp]),
     "pqg_pq_fit": (_i32, [_vp, _vp, _u64, _u64, _u32, _u32, _u32, _u64, _vp, _vp, _vp]),
+    "pqg_pq_fit_ex": (_i32, [_vp, _vp, _u64, _u64, _u32, _u32, _u32, _u64, _vp, _vp, _vp, _vp]),
     "pqg_pq_encode": (_i32, [_vp, _vp, _u64, _u32, _u32, _u32, _vp, _vp]),
     "pqg_pq_decode": (_i32, [_vp, _vp, _u64, _u32, _u32, _u32, _vp, _vp]),
     "pqg_sq_error": (_i32, [_vp, _vp, _vp, _u64, _vp]),

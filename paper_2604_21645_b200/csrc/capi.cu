@@ -98,7 +98,12 @@ static void finish(pqg_ctx* ctx, const Out<T>& o) {
 
 static void sync(pqg_ctx* ctx) { PQG_CUDA(cudaStreamSynchronize(ctx->stream)); }
 
+// The device error word collects out-of-range code reports.  A call whose
+// outputs all stay on the device does not synchronise to read it: the flag is
+// left pending (err_pending) and reported by the next pqg_ctx_sync /
+// pqg_ctx_check_errors, and later calls do not clear it until then.
 static void reset_err(pqg_ctx* ctx) {
+    if (ctx->err_pending) return;
     PQG_CUDA(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream));
 }
 
@@ -106,6 +111,7 @@ static int read_err(pqg_ctx* ctx) {
     int h = 0;
     PQG_CUDA(cudaMemcpyAsync(&h, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     sync(ctx);
+    ctx->err_pending = false;
     return h;
 }
 
@@ -692,15 +698,41 @@ void pqg_ctx_destroy(pqg_ctx* ctx) {
     for (auto e : ctx->pipe_ev)
         if (e) cudaEventDestroy(e);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->handoff_ev) cudaEventDestroy(ctx->handoff_ev);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
 }
 
 int pqg_ctx_set_stream(pqg_ctx* ctx, void* s) {
-    return guard([&] { ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own_stream; });
+    return guard([&] {
+        cudaStream_t ns = s ? static_cast<cudaStream_t>(s) : ctx->own_stream;
+        if (ns == ctx->stream) return;
+        PQG_CUDA(cudaSetDevice(ctx->device));
+        // Work already queued on the outgoing stream may still use the scratch
+        // arena the next call hands out again: the new stream waits for it.
+        if (!ctx->handoff_ev) PQG_CUDA(cudaEventCreateWithFlags(&ctx->handoff_ev, cudaEventDisableTiming));
+        PQG_CUDA(cudaEventRecord(ctx->handoff_ev, ctx->stream));
+        PQG_CUDA(cudaStreamWaitEvent(ns, ctx->handoff_ev, 0));
+        ctx->stream = ns;
+    });
 }
 
-int pqg_ctx_sync(pqg_ctx* ctx) { return guard([&] { sync(ctx); }); }
+void* pqg_ctx_stream(pqg_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int pqg_ctx_check_errors(pqg_ctx* ctx) {
+    return guard([&] {
+        Scope sc(ctx);
+        if (ctx->err_pending && read_err(ctx)) {
+            PQG_CUDA(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream));
+            fail(PQG_ERANGE, "adc_lookup: code out of range");
+        }
+    });
+}
+
+int pqg_ctx_sync(pqg_ctx* ctx) {
+    const int rc = guard([&] { sync(ctx); });
+    return rc ? rc : pqg_ctx_check_errors(ctx);
+}
 
 uint64_t pqg_ctx_launches(pqg_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
@@ -958,6 +990,13 @@ int pqg_pipeline_run(pqg_ctx* ctx, const float* data, uint64_t n, uint64_t D, ui
 int pqg_pq_fit(pqg_ctx* ctx, const float* data, uint64_t n, uint64_t D, uint32_t M, uint32_t ks,
                uint32_t max_iters, uint64_t seed, float* tables, uint32_t* iterations_run,
                double* inertia) {
+    return pqg_pq_fit_ex(ctx, data, n, D, M, ks, max_iters, seed, tables, iterations_run, inertia,
+                         nullptr);
+}
+
+int pqg_pq_fit_ex(pqg_ctx* ctx, const float* data, uint64_t n, uint64_t D, uint32_t M,
+                  uint32_t ks, uint32_t max_iters, uint64_t seed, float* tables,
+                  uint32_t* iterations_run, double* inertia, double* inertia_per_iter) {
     return guard([&] {
         Scope sc(ctx);
         check_pq_fit(n, D, M, ks, max_iters);
@@ -973,6 +1012,7 @@ int pqg_pq_fit(pqg_ctx* ctx, const float* data, uint64_t n, uint64_t D, uint32_t
         sync(ctx);
         if (iterations_run) std::copy(r.iters.begin(), r.iters.end(), iterations_run);
         if (inertia) std::copy(r.inertia.begin(), r.inertia.end(), inertia);
+        if (inertia_per_iter) std::copy(r.per_iter.begin(), r.per_iter.end(), inertia_per_iter);
     });
 }
 
@@ -1467,6 +1507,8 @@ int pqg_index_search(pqg_ctx* ctx, const pqg_index* ix, const float* queries, ui
         finish(ctx, oc);
         if (oi.host || od.host || oc.host) {
             if (read_err(ctx)) fail(PQG_ERANGE, "adc_lookup: code out of range");
+        } else {
+            ctx->err_pending = true;  // reported by pqg_ctx_sync / pqg_ctx_check_errors
         }
     });
 }
@@ -1506,6 +1548,8 @@ int pqg_index_search_subset(pqg_ctx* ctx, const pqg_index* ix, const float* quer
         finish(ctx, oc);
         if (oi.host || od.host || oc.host) {
             if (read_err(ctx)) fail(PQG_ERANGE, "adc_lookup: code out of range");
+        } else {
+            ctx->err_pending = true;  // reported by pqg_ctx_sync / pqg_ctx_check_errors
         }
     });
 }

@@ -150,6 +150,8 @@ struct pqg_ctx {
     // copy stream + events for host-input pipelines (created on first use)
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t pipe_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t handoff_ev = nullptr;  // pqg_ctx_set_stream: new stream waits for the old
+    bool err_pending = false;          // d_err not yet read (device-output searches)
 };
 
 namespace pqg {

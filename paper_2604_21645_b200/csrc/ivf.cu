@@ -789,7 +789,11 @@ void ivf_scan(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t 
               const uint32_t* probes, uint64_t nprobe, uint64_t k, int has_max, double max_sq,
               uint64_t* out_ids, double* out_dists, uint32_t* out_counts, int* err,
               const uint64_t* subset, uint64_t nsub, const float* luts) {
-    if (k > 32) fail(PQG_EUNSUPPORTED, "search: k > 32 is not supported by the warp top-k path");
+    if (k > 32) {  // beyond the warp top-k: exact scores + segmented sort (topk_large.cu)
+        ivf_scan_large_k(ctx, ix, queries, nq, probes, nprobe, k, has_max, max_sq, out_ids, out_dists,
+                         out_counts, err, subset, nsub, luts);
+        return;
+    }
     const size_t lut_bytes = (sizeof(float) * ix.M * ix.ks + 15) & ~size_t(15);
     const size_t smem = lut_bytes + sizeof(TopK) * k * (kScanThreads / 32) +
                         sizeof(double) * uint64_t(ix.M) * ix.ds +  // fp64 query

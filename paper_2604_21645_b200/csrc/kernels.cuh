@@ -136,6 +136,12 @@ void ivf_scan(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t 
               const uint32_t* probes, uint64_t nprobe, uint64_t k, int has_max, double max_sq,
               uint64_t* out_ids, double* out_dists, uint32_t* out_counts, int* err,
               const uint64_t* subset = nullptr, uint64_t nsub = 0, const float* luts = nullptr);
+// topk_large.cu: the same search for k > 32 (exact scores of every candidate,
+// compacted per query, ordered by (dist, id) with segmented sorts)
+void ivf_scan_large_k(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t nq,
+                      const uint32_t* probes, uint64_t nprobe, uint64_t k, int has_max,
+                      double max_sq, uint64_t* out_ids, double* out_dists, uint32_t* out_counts,
+                      int* err, const uint64_t* subset, uint64_t nsub, const float* luts);
 // adc_tc.cu: tensor-core screened search (decoded candidate operand cached per index)
 struct TcCache {
     uint8_t* Bm = nullptr;        // [block of 256 candidates][K chunk][hi|lo]

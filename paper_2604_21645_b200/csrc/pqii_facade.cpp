@@ -64,16 +64,59 @@ pqg_ctx* ctx() {
 }
 
 // ---------------------------------------------------------------------------
-// device-index cache for repeated queries on the same (unmodified) index
+// device-index cache for repeated queries on the same (unmodified) index.
+// An entry is reused only when the index's CONTENT still matches: a 64-bit
+// digest over every list's ids and code bytes, the list sizes, the coarse
+// centroids and the codebook tables (four independent multiply-xorshift lanes
+// over 8-byte words).  Pointer identity alone is not enough: a freed index's
+// blocks are reused by malloc for the next one of the same shape, and the
+// reference's structs have public fields that callers may edit in place.
 // ---------------------------------------------------------------------------
-using IndexKey = std::tuple<const void*, std::size_t, std::size_t, const void*, const void*,
-                            const void*, const void*, std::size_t>;
+struct Digest {
+    std::uint64_t h[4] = {0x243F6A8885A308D3ull, 0x13198A2E03707344ull, 0xA4093822299F31D0ull,
+                          0x082EFA98EC4E6C89ull};
+    std::uint64_t n = 0;
+    static std::uint64_t mix(std::uint64_t h, std::uint64_t w) {
+        h ^= w;
+        h *= 0x9E3779B97F4A7C15ull;
+        return h ^ (h >> 29);
+    }
+    void bytes(const void* p, std::size_t len) {
+        const auto* c = static_cast<const unsigned char*>(p);
+        std::size_t i = 0;
+        for (; i + 32 <= len; i += 32) {
+            std::uint64_t w[4];
+            std::memcpy(w, c + i, 32);
+            for (int j = 0; j < 4; ++j) h[j] = mix(h[j], w[j]);
+        }
+        std::uint64_t tail = 0;
+        for (int j = 0; i < len; ++i, ++j) {
+            tail |= std::uint64_t(c[i]) << (8 * (j & 7));
+            if ((j & 7) == 7) { h[0] = mix(h[0], tail); tail = 0; }
+        }
+        h[1] = mix(h[1], tail ^ len);
+        n += len;
+    }
+    std::uint64_t value() const {
+        std::uint64_t v = n;
+        for (auto x : h) v = mix(v, x);
+        return v;
+    }
+};
 
-IndexKey key_of(const InvertedIndex& ix) {
-    const void* first = ix.lists.empty() ? nullptr : ix.lists.front().ids.data();
-    const void* last = ix.lists.empty() ? nullptr : ix.lists.back().ids.data();
-    return {ix.lists.data(), ix.lists.size(), ix.n_items, first, last, ix.codebook.tables.data(),
-            ix.coarse_centroids.values.data(), ix.id_set.size()};
+std::uint64_t content_digest(const InvertedIndex& ix) {
+    Digest d;
+    const std::uint64_t hdr[4] = {ix.lists.size(), ix.n_items, ix.codebook.m_subspaces, ix.codebook.ks};
+    d.bytes(hdr, sizeof(hdr));
+    d.bytes(ix.codebook.tables.data(), ix.codebook.tables.size() * sizeof(float));
+    d.bytes(ix.coarse_centroids.values.data(), ix.coarse_centroids.values.size() * sizeof(float));
+    for (const auto& pl : ix.lists) {
+        const std::uint64_t sz = pl.ids.size();
+        d.bytes(&sz, sizeof(sz));
+        d.bytes(pl.ids.data(), pl.ids.size() * sizeof(std::uint64_t));
+        d.bytes(pl.codes.bytes.data(), pl.codes.bytes.size());
+    }
+    return d.value();
 }
 
 struct IndexDeleter {
@@ -82,7 +125,7 @@ struct IndexDeleter {
 using IndexPtr = std::shared_ptr<pqg_index>;
 
 std::mutex g_cache_mu;
-std::list<std::pair<IndexKey, IndexPtr>> g_cache;  // most recent first
+std::list<std::pair<std::uint64_t, IndexPtr>> g_cache;  // (content digest, index), most recent first
 
 IndexPtr upload(const InvertedIndex& ix) {
     const std::size_t nlist = ix.lists.size();
@@ -104,7 +147,7 @@ IndexPtr upload(const InvertedIndex& ix) {
 }
 
 IndexPtr device_index_for(const InvertedIndex& ix) {
-    const IndexKey k = key_of(ix);
+    const std::uint64_t k = content_digest(ix);
     {
         std::lock_guard<std::mutex> g(g_cache_mu);
         for (auto it = g_cache.begin(); it != g_cache.end(); ++it) {
@@ -472,29 +515,14 @@ void ivf_add(InvertedIndex& index, const CodeMatrix& codes, std::span<const std:
 }
 
 InvertedIndex ivf_merge(const InvertedIndex& a, const InvertedIndex& b) {
-    if (!(a.codebook == b.codebook)) throw std::invalid_argument("ivf_merge: codebook mismatch");
-    if (!(a.coarse_centroids == b.coarse_centroids))
-        throw std::invalid_argument("ivf_merge: coarse centroid mismatch");
-    const auto& small = a.id_set.size() <= b.id_set.size() ? a.id_set : b.id_set;
-    const auto& large = a.id_set.size() <= b.id_set.size() ? b.id_set : a.id_set;
-    for (const std::uint64_t id : small)
-        if (large.contains(id)) throw std::invalid_argument("ivf_merge: id collision on id " + std::to_string(id));
-    InvertedIndex out;
-    out.codebook = a.codebook;
-    out.coarse_centroids = a.coarse_centroids;
-    out.lists.resize(a.lists.size());
-    for (std::size_t l = 0; l < a.lists.size(); ++l) {  // list l = a's then b's
-        PostingList& d = out.lists[l];
-        d.ids = a.lists[l].ids;
-        d.ids.insert(d.ids.end(), b.lists[l].ids.begin(), b.lists[l].ids.end());
-        d.codes = a.lists[l].codes;
-        d.codes.bytes.insert(d.codes.bytes.end(), b.lists[l].codes.bytes.begin(), b.lists[l].codes.bytes.end());
-        d.codes.rows += b.lists[l].codes.rows;
-    }
-    out.n_items = a.n_items + b.n_items;
-    out.id_set = a.id_set;
-    out.id_set.insert(b.id_set.begin(), b.id_set.end());
-    return out;
+    // the device merge (pqg_index_merge: codebook / coarse / id-collision
+    // checks, then list l = a's then b's with csr_concat) on the cached
+    // device copies of both operands
+    IndexPtr da = device_index_for(a), db = device_index_for(b);
+    pqg_index* h = nullptr;
+    raise(pqg_index_merge(ctx(), da.get(), db.get(), &h));
+    IndexPtr p(h, IndexDeleter());
+    return to_host(h, a.codebook);
 }
 
 std::vector<QueryResult> ivf_query_batch(const InvertedIndex& index, const VectorMatrix& queries,

@@ -45,3 +45,26 @@ def strided_sample(n_rows: int, n_sample: int, seed: int) -> np.ndarray:
     off = seed % stride
     first = (stride - off) % stride
     return (first + stride * np.arange(n_sample, dtype=np.int64))
+
+
+def device_mixture(rows: int, dims: int, components: int, seed: int, gen_seed: int, out=None,
+                   chunk: int = 1 << 20):
+    """rows x dims float32 drawn on the GPU from the same seeded mixture
+    (mixture_params(dims, components, seed)), rows from a torch CUDA (Philox)
+    generator seeded with gen_seed -- BASELINE configs[4]'s "generated per
+    shard from seed + rank"; also used for configs[3]'s 10M
+    rows.  x = mu_c + sigma_c * z in fp64, stored fp32.  ``out`` (optional) is
+    a preallocated rows x dims CUDA tensor to fill."""
+    import torch
+    means, sigmas = mixture_params(dims, components, seed)
+    mu = torch.from_numpy(means.astype(np.float64)).cuda()
+    sg = torch.from_numpy(sigmas.astype(np.float64)).cuda()
+    g = torch.Generator(device="cuda")
+    g.manual_seed(gen_seed)
+    x = out if out is not None else torch.empty((rows, dims), dtype=torch.float32, device="cuda")
+    for r0 in range(0, rows, chunk):
+        r1 = min(rows, r0 + chunk)
+        comp = torch.randint(0, components, (r1 - r0,), generator=g, device="cuda")
+        z = torch.randn((r1 - r0, dims), generator=g, device="cuda", dtype=torch.float64)
+        x[r0:r1] = (mu[comp] + sg[comp, None] * z).float()
+    return x

@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import threading
 import time
 from dataclasses import dataclass, field
 
@@ -30,19 +31,67 @@ from . import _lib
 # ---------------------------------------------------------------------------
 
 
+_tls = threading.local()  # set by _ptr when a call receives a torch CUDA tensor
+
+
+class _OrderedLib:
+    """libpqg with torch stream ordering: a call that was handed a torch CUDA
+    tensor first makes the context stream wait for torch's current stream
+    (the kernels that produced the inputs), and afterwards makes torch's
+    current stream wait for the context stream (device outputs are complete
+    before torch reads them).  Both are event waits, no host sync."""
+
+    def __init__(self, ctx: "Context", lib):
+        self._ctx = ctx
+        self._lib = lib
+
+    def __getattr__(self, name):
+        f = getattr(self._lib, name)
+        if not name.startswith("pqg_"):
+            return f
+
+        def call(*args):
+            torch_args = getattr(_tls, "torch_cuda", False)
+            _tls.torch_cuda = False
+            if torch_args:
+                self._ctx._fence(into_ctx=True)
+            try:
+                return f(*args)
+            finally:
+                if torch_args:
+                    self._ctx._fence(into_ctx=False)
+        return call
+
+
 class Context:
     """One GPU, one stream, one scratch arena (pqg_ctx)."""
 
     def __init__(self, device: int = 0):
-        self.lib = _lib.load()
+        self._raw = _lib.load()
         h = C.c_void_p()
-        _lib.check(self.lib.pqg_ctx_create(device, C.byref(h)), "ctx_create")
+        _lib.check(self._raw.pqg_ctx_create(device, C.byref(h)), "ctx_create")
         self.h = h
         self.device = device
+        self.lib = _OrderedLib(self, self._raw)
+        self._ext = {}
+
+    def _fence(self, into_ctx: bool):
+        import torch
+        cur = torch.cuda.current_stream(self.device)
+        mine = self._raw.pqg_ctx_stream(self.h) or 0
+        if mine == cur.cuda_stream:
+            return
+        ext = self._ext.get(mine)
+        if ext is None:
+            ext = self._ext[mine] = torch.cuda.ExternalStream(mine, device=self.device)
+        if into_ctx:
+            ext.wait_stream(cur)
+        else:
+            cur.wait_stream(ext)
 
     def close(self):
         if getattr(self, "h", None):
-            self.lib.pqg_ctx_destroy(self.h)
+            self._raw.pqg_ctx_destroy(self.h)
             self.h = None
 
     def __del__(self):
@@ -87,6 +136,8 @@ def _ptr(x):
     if hasattr(x, "data_ptr"):
         if not x.is_contiguous():
             raise ValueError("tensor must be contiguous")
+        if getattr(x, "is_cuda", False):
+            _tls.torch_cuda = True
         return C.c_void_p(x.data_ptr()), x
     a = np.ascontiguousarray(x)
     return C.c_void_p(a.ctypes.data), a
@@ -277,14 +328,20 @@ def pq_fit(data, m: int, ks: int, max_iters: int = 20, seed: int = 0,
     tables = np.empty((m, max(ks, 0), ds), np.float32)
     iters = np.empty(m, np.uint32)
     inert = np.empty(m, np.float64)
+    per = np.zeros((m, max(1, max_iters)), np.float64)
     dp, _a = _ptr(data)
-    _lib.check(ctx.lib.pqg_pq_fit(ctx.h, dp, n, D, m, ks, max_iters, seed,
-                                  tables.ctypes.data_as(C.c_void_p),
-                                  iters.ctypes.data_as(C.c_void_p),
-                                  inert.ctypes.data_as(C.c_void_p)), "pq_fit")
+    _lib.check(ctx.lib.pqg_pq_fit_ex(ctx.h, dp, n, D, m, ks, max_iters, seed,
+                                     tables.ctypes.data_as(C.c_void_p),
+                                     iters.ctypes.data_as(C.c_void_p),
+                                     inert.ctypes.data_as(C.c_void_p),
+                                     per.ctypes.data_as(C.c_void_p) if max_iters > 0 else None),
+               "pq_fit")
     if stats is not None:
         stats["iterations_run"] = iters
         stats["inertia"] = inert
+        for b in range(m):  # kmeans_fit's inertia_per_iter per subspace
+            per[b, iters[b]:] = np.nan
+        stats["inertia_per_iter"] = per
     return Codebook(m, ks, ds, tables)
 
 

@@ -237,6 +237,48 @@ int main() {
         CHECK_THROWS_WITH(ivf_build_with_centroids(cb, codes, dup, ix.coarse_centroids),
                           std::invalid_argument, "duplicate id");
         CHECK(default_nlist(10000) == 100 && default_nlist(0) == 1 && default_nlist(2) == 1);
+        // the device-index cache never serves a stale index: same-shape indexes
+        // built and freed in a loop (malloc reuses their blocks), and a list
+        // edited in place through the public fields
+        for (int rep = 0; rep < 3; ++rep) {
+            const VectorMatrix d2 = random_matrix(2000, 16, 100 + rep, 0, 10);
+            const CodeMatrix c2 = pq_encode(cb, d2);
+            const InvertedIndex i2 = ivf_build_with_centroids(cb, c2, ids, ix.coarse_centroids);
+            const auto r2 = ivf_query(i2, qs.row_span(2), 10, i2.nlist());
+            const auto f2 = flat_scan(cb, c2, ids, qs.row_span(2), 10);
+            CHECK(r2.hits == f2.hits);
+        }
+        {
+            InvertedIndex edit = ivf_build_with_centroids(cb, codes, ids, ix.coarse_centroids);
+            const auto before = ivf_query(edit, qs.row_span(3), 5, edit.nlist());
+            const std::uint64_t top = before.hits[0].id;
+            for (auto& pl : edit.lists)  // move the best hit's code far away
+                for (std::size_t i = 0; i < pl.ids.size(); ++i)
+                    if (pl.ids[i] == top)
+                        for (std::uint32_t m = 0; m < 4; ++m) {
+                            const std::uint32_t c = pl.codes.at(i, m);
+                            pl.codes.set(i, m, (c + 8) % 16);
+                        }
+            const auto after = ivf_query(edit, qs.row_span(3), 5, edit.nlist());
+            CodeMatrix c3(0, 4, 16);
+            std::vector<std::uint64_t> i3;
+            for (const auto& pl : edit.lists)
+                for (std::size_t i = 0; i < pl.ids.size(); ++i) {
+                    c3.append_row_from(pl.codes, i);
+                    i3.push_back(pl.ids[i]);
+                }
+            CHECK(after.hits == flat_scan(cb, c3, i3, qs.row_span(3), 5).hits);
+        }
+        // k > 32 (the CTA-wide path) and k beyond n_items saturating (test_ivf.cpp:255-259)
+        const QueryResult sat = ivf_query(ix, qs.row_span(0), 1000, ix.nlist());
+        CHECK(sat.hits.size() == 1000 && sat.k_requested == 1000);
+        const QueryResult sat2 = ivf_query(mono, qs.row_span(1), 5000, mono.nlist());
+        CHECK(sat2.hits.size() == 2000 && sat2.k_requested == 5000);
+        const QueryResult flat_big = flat_scan(cb, codes, ids, qs.row_span(1), 5000);
+        CHECK(flat_big.hits == sat2.hits);
+        for (std::size_t j = 1; j < sat2.hits.size(); ++j)
+            CHECK(sat2.hits[j - 1].sq_dist < sat2.hits[j].sq_dist ||
+                  (sat2.hits[j - 1].sq_dist == sat2.hits[j].sq_dist && sat2.hits[j - 1].id < sat2.hits[j].id));
     }
     // ---- test_pipeline.cpp
     {   // train_chunk :44-92

@@ -661,3 +661,117 @@ def test_search_ks256_ties_early_exit(pq, orc, M, k):
         ri, rd = orc.ivf_query_subset(cb.tables, coarse, o_off, o_ids, o_codes, q[i], k, subset, 4)
         assert [h.id for h in r.hits] == ri.tolist()
         assert np.array_equal(bits(np.array([h.sq_dist for h in r.hits], np.float64)), bits(rd))
+
+
+# ---------------------------------------------------------------------------
+# k > 32 (topk_large.cu): finalize_hits for any k (proj/src/ivf.cpp:58-68),
+# saturating at the candidate count (proj/tests/test_ivf.cpp:255-259)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("k", [33, 100, 1000, 7000])
+def test_search_large_k(pq, orc, k):
+    rng = np.random.default_rng(k)
+    M, ks, ds, n = 8, 256, 4, 6000
+    tables = orc.random_matrix(M * ks, ds, 31).reshape(M, ks, ds)
+    base = rng.integers(0, ks, size=(80, M), dtype=np.uint8)
+    codes_b = base[rng.integers(0, 80, size=n)]  # duplicate rows: ties broken by id
+    ids = rng.permutation(1_000_000)[:n].astype(np.uint64)
+    cb = pq.Codebook(M, ks, ds, np.ascontiguousarray(tables, np.float32))
+    codes = pq.CodeMatrix(n, M, ks, np.ascontiguousarray(codes_b))
+    coarse = pq.pq_decode(cb, pq.CodeMatrix(10, M, ks, np.ascontiguousarray(base[:10])))
+    index = pq.ivf_build_with_centroids(cb, codes, ids, coarse)
+    o_off, o_ids, o_codes = orc.ivf_build_with_centroids(codes.bytes, ids, cb.tables, coarse)
+    q = orc.random_matrix(12, M * ds, 3 + k)
+    for nprobe in (3, 10):
+        for max_sq in (None, float(M) * 0.8):
+            gi, gd, gc = pq.ivf_query_batch(index, q, k, nprobe, max_sq_dist=max_sq)
+            for i in range(q.shape[0]):
+                ri, rd = orc.ivf_query(cb.tables, coarse, o_off, o_ids, o_codes, q[i], k, nprobe,
+                                       max_sq_dist=max_sq)
+                assert gc[i] == ri.size
+                assert np.array_equal(gi[i, : gc[i]], ri) and np.array_equal(bits(gd[i, : gc[i]]), bits(rd))
+                assert (gi[i, gc[i]:] == 0).all()
+    subset = np.sort(ids[rng.choice(n, n // 4, replace=False)])
+    for i in range(5):
+        r = pq.ivf_query_subset(index, q[i], k, subset, 6)
+        ri, rd = orc.ivf_query_subset(cb.tables, coarse, o_off, o_ids, o_codes, q[i], k, subset, 6)
+        assert [h.id for h in r.hits] == ri.tolist() and r.k_requested == k
+        assert np.array_equal(bits(np.array([h.sq_dist for h in r.hits], np.float64)), bits(rd))
+    fi, fd, fc = pq.flat_scan_batch(cb, codes, ids, q, k)
+    for i in range(q.shape[0]):
+        ri, rd = orc.flat_scan(cb.tables, codes.bytes, ids, q[i], k)
+        assert np.array_equal(fi[i, : fc[i]], ri) and np.array_equal(bits(fd[i, : fc[i]]), bits(rd))
+    # nprobe = nlist == flat_scan for k > 32 as well (test_ivf.cpp:246-253)
+    ai, ad, ac = pq.ivf_query_batch(index, q, k, index.nlist())
+    assert np.array_equal(ac, fc) and np.array_equal(ai, fi) and np.array_equal(bits(ad), bits(fd))
+
+
+def test_search_large_k_saturates_reference_case(pq, ref):
+    """proj/tests/test_ivf.cpp:255-259 on the compiled reference's own index:
+    400 items, k = 1000 at nprobe = nlist -> 400 hits, k_requested 1000."""
+    x = ref.random_matrix(400, 16, 3, 0.0, 10.0)
+    tables = ref.pq_fit(x, 4, 16, 10, 1)
+    codes = ref.pq_encode(x, tables)
+    ids = np.arange(400, dtype=np.uint64) + 7
+    coarse = x[::50].copy()
+    cb = pq.Codebook(4, 16, 4, tables)
+    index = pq.ivf_build_with_centroids(cb, pq.CodeMatrix(400, 4, 16, codes), ids, coarse)
+    q = ref.random_matrix(1, 16, 3)
+    r = pq.ivf_query(index, q[0], 1000, index.nlist())
+    assert len(r.hits) == 400 and r.k_requested == 1000
+    h = ref.ivf_build_with_centroids(codes, ids, tables, coarse)
+    ri, rd, rc = h.query_batch(q, 1000, index.nlist())
+    assert rc[0] == 400
+    assert [x.id for x in r.hits] == ri[0, :400].tolist()
+    assert np.array_equal(bits(np.array([x.sq_dist for x in r.hits])), bits(rd[0, :400]))
+
+
+def test_search_device_outputs_defer_range_error(pq):
+    """An out-of-range code found by a search whose outputs stay on the device
+    is reported by the next pqg_ctx_sync (adc_lookup's out_of_range)."""
+    import ctypes as C
+
+    import torch
+    from paper_2604_21645_b200 import _lib
+    M, ks, ds = 4, 16, 2
+    tables = np.arange(M * ks * ds, dtype=np.float32).reshape(M, ks, ds) / 7
+    codes = np.zeros((64, M), np.uint8)
+    ctx = pq.Context(0)
+    ids = np.arange(64, dtype=np.uint64)
+    coarse = np.zeros((2, M * ds), np.float32)
+    coarse[1] += 100
+    offsets = np.array([0, 64, 64], np.uint64)
+    h = C.c_void_p()
+    v = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    codes[5, 2] = 20  # >= ks
+    _lib.check(ctx.lib.pqg_index_create(ctx.h, v(tables), M, ks, ds, v(coarse), 2, v(offsets), v(ids),
+                                        v(codes), C.byref(h)))
+    q = torch.zeros((3, M * ds), dtype=torch.float32, device="cuda")
+    oi = torch.empty((3, 5), dtype=torch.int64, device="cuda")
+    od = torch.empty((3, 5), dtype=torch.float64, device="cuda")
+    oc = torch.empty((3,), dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    assert ctx.lib.pqg_index_search(ctx.h, h, vp(q), 3, 5, 1, 0, 0.0, vp(oi), vp(od), vp(oc)) == 0
+    assert ctx.lib.pqg_ctx_sync(ctx.h) == _lib.PQG_ERANGE
+    assert ctx.lib.pqg_ctx_sync(ctx.h) == 0  # reported once
+    ctx.lib.pqg_index_destroy(h)
+    ctx.close()
+
+
+def test_torch_inputs_ordered_on_torch_stream(pq, orc, mix):
+    """Device inputs produced on torch's current stream are complete before
+    the library's kernels read them, and device outputs before torch reads
+    them (pqii orders its own stream against torch's with events)."""
+    import torch
+    x = mix(20000, 32, 16, seed=8)
+    cb = pq.pq_fit(x, 4, 64, 6, 2)
+    ref_codes = orc.pq_encode(x, cb.tables)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            xd = torch.zeros((20000, 32), dtype=torch.float32, device="cuda")
+            torch.cuda._sleep(2_000_000)  # keep the stream busy before the data lands
+            xd.copy_(torch.from_numpy(x).cuda(non_blocking=True))
+            codes = pq.pq_encode(cb, xd)
+            assert np.array_equal(codes.bytes, ref_codes)

@@ -194,3 +194,80 @@ def test_oracle_vs_ref_pipeline(orc, ref):
         if mode == "parallel_pq_index":
             assert np.array_equal(a["list_ids"], b["list_ids"])
             assert np.array_equal(a["offsets"], b["offsets"])
+
+
+# ---------------------------------------------------------------------------
+# The threaded checkers used at BASELINE sizes (tests/config_parity.py) are
+# bit-identical to the single-threaded reference for every thread count.
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("threads", [1, 3, 8])
+def test_threaded_kmeans_equals_reference(orc, ref, threads):
+    from paper_2604_21645_b200.datagen import gaussian_mixture
+    x = gaussian_mixture(6000, 24, 16, seed=11)
+    a = orc.kmeans_fit(x, 50, 12, 7, threads=threads)
+    b = ref.kmeans_fit(x, 50, 12, 7)
+    assert np.array_equal(a["centroids"].view(np.uint32), b["centroids"].view(np.uint32))
+    assert np.array_equal(a["assignments"], b["assignments"])
+    assert a["iterations_run"] == b["iterations_run"]
+    assert np.array_equal(a["inertia_per_iter"].view(np.uint64), b["inertia_per_iter"].view(np.uint64))
+
+
+def test_threaded_kmeans_reseed_equals_reference(orc, ref):
+    # identical points force empty clusters and reseeds (test_kmeans.cpp:174-179)
+    x = np.repeat(ref.random_matrix(40, 3, 5), 25, axis=0)
+    a = orc.kmeans_fit(x, 60, 6, 3, threads=4)
+    b = ref.kmeans_fit(x, 60, 6, 3)
+    assert np.array_equal(a["centroids"].view(np.uint32), b["centroids"].view(np.uint32))
+    assert np.array_equal(a["assignments"], b["assignments"])
+
+
+def test_lloyd_update_is_one_reference_step(orc, ref):
+    """fit(t+1)'s centroids == update(fit(t)'s assignment pass) -- the sampled
+    protocol's step check (config_parity.lloyd_step_*)."""
+    from paper_2604_21645_b200.datagen import gaussian_mixture
+    x = gaussian_mixture(5000, 16, 8, seed=3)
+    for t in (1, 2, 4):
+        ft = ref.kmeans_fit(x, 40, t, 9, tol=0.0)
+        ft1 = ref.kmeans_fit(x, 40, t + 1, 9, tol=0.0)
+        idx, dist = ref.nearest_batch(x, ft["centroids"])
+        assert np.array_equal(idx, ft["assignments"])
+        new, _ = orc.lloyd_update(x, idx, dist, ft["centroids"])
+        assert np.array_equal(new.view(np.uint32), ft1["centroids"].view(np.uint32))
+
+
+def test_threaded_reference_entry_points(orc, ref):
+    """pq_fit_stats (subspace fits on threads), nearest_batch_mt, threaded
+    ivf_build (chunk builds + ivf_merge) and threaded queries equal the
+    single-threaded reference calls."""
+    from paper_2604_21645_b200.datagen import gaussian_mixture
+    x = gaussian_mixture(4000, 32, 16, seed=21)
+    tables, iters, per = ref.pq_fit_stats(x, 4, 32, 8, 5, threads=4)
+    assert np.array_equal(tables.view(np.uint32), ref.pq_fit(x, 4, 32, 8, 5).view(np.uint32))
+    for m in range(4):
+        km = ref.kmeans_fit(np.ascontiguousarray(x[:, 8 * m:8 * m + 8]), 32, 8, 5 + m)
+        assert iters[m] == km["iterations_run"]
+        assert np.array_equal(per[m, : iters[m]], km["inertia_per_iter"])
+    i1, d1 = ref.nearest_batch_mt(x, x[:50].copy(), 5)
+    i0, d0 = ref.nearest_batch(x, x[:50].copy())
+    assert np.array_equal(i0, i1) and np.array_equal(d0.view(np.uint64), d1.view(np.uint64))
+    codes = ref.pq_encode(x, tables)
+    assert np.array_equal(codes, ref.pq_encode(x, tables, threads=3))
+    assert np.array_equal(codes, orc.pq_encode_mt(x, tables, 3))
+    ids = np.arange(4000, dtype=np.uint64) * 3 + 1
+    coarse = x[::200].copy()
+    mono = ref.ivf_build_with_centroids(codes, ids, tables, coarse).export()
+    par = ref.ivf_build_with_centroids_mt(codes, ids, tables, coarse, 5).export()
+    for a, b in zip(mono, par):
+        assert np.array_equal(a, b)
+    assert np.array_equal(orc.ivf_assign_mt(codes, tables, coarse, 4),
+                          orc.ivf_assign(codes, tables, coarse))
+    q = gaussian_mixture(30, 32, 16, seed=21, stream=1)
+    h = ref.ivf_build_with_centroids(codes, ids, tables, coarse)
+    ri, rd, rc = h.query_batch(q, 7, 4, threads=4)
+    oi, od, oc = orc.ivf_query_mt(tables, coarse, *mono[:3], q, 7, 4, 3)
+    assert np.array_equal(ri, oi) and np.array_equal(rd.view(np.uint64), od.view(np.uint64))
+    assert np.array_equal(rc, oc)
+    po = orc.probe_order_mt(coarse, q, 5, 3)
+    for j in range(q.shape[0]):
+        assert np.array_equal(po[j], orc.probe_order(coarse, q[j], 5))
