@@ -240,6 +240,59 @@ int pqg_rows_sum_f64(pqg_ctx* ctx, const double* v, uint64_t n, uint32_t B, doub
 /* The k init rows kmeans_fit draws (proj/src/kmeans.cpp:73-85), host-side. */
 int pqg_kmeans_init_rows(uint64_t n, uint64_t k, uint64_t seed, uint64_t* rows);
 
+/* ---- row-sharded k-means, one rank's side -------------
+ * The north-star exchange: per iteration ONE all-reduce (SUM) of the packed
+ * fp64 partials [centroid sums B*k*d | counts B*k | inertia B] and one
+ * all-reduce (MAX) of the u8 exponent ranges [B*k*d | B*k*d]; the caller
+ * (paper_2604_21645_b200/dist.py, torch.distributed / NCCL) owns the
+ * collectives, these calls own the device work.  Ranks hold ascending
+ * contiguous blocks of the global row-ordered sample; the result equals
+ * kmeans_fit (kmeans.cpp:61-133) / pq_fit's per-subspace fits bit for bit:
+ * sums whose global exponent range proves them exact are reduced in any
+ * order, the rest are replayed in global row order from the members the
+ * ranks exchange (pqg_kmshard_pack / _replay), empty clusters are reseeded
+ * from every rank's best candidates (pqg_kmshard_reseed_*).  rows: device,
+ * n x ld; problem b reads columns [b*col_stride, b*col_stride + d); d % 4 ==
+ * 0 and d <= 128 (else PQG_EUNSUPPORTED).  Every call runs on ctx's stream. */
+typedef struct pqg_kmshard pqg_kmshard;
+int pqg_kmshard_create(pqg_ctx* ctx, const float* rows, uint64_t n, uint64_t ld, uint32_t B, uint32_t d,
+                       uint32_t col_stride, uint64_t k, uint32_t max_iters, double tol, pqg_kmshard** out);
+void pqg_kmshard_destroy(pqg_kmshard* h);
+/* element counts of the two packed partial buffers */
+int pqg_kmshard_sizes(const pqg_kmshard* h, uint64_t* n_f64, uint64_t* n_u8);
+/* table_bits (device, B*k*d u32): the bit patterns of the init rows this rank
+ * owns (global row ids init_rows[B*k], host; this rank holds rows
+ * [row0, row0 + n)), zero elsewhere -- an integer all-reduce SUM assembles
+ * the initial centroids (kmeans.cpp:73-88). */
+int pqg_kmshard_init_table(pqg_ctx* ctx, pqg_kmshard* h, const uint64_t* init_rows, uint64_t row0,
+                           uint32_t* table_bits);
+/* assignment pass (kmeans.cpp:46-57) of the local rows against tables
+ * (device B*k*d) and the local partials into f64 / u8 (device) */
+int pqg_kmshard_partials(pqg_ctx* ctx, pqg_kmshard* h, const float* tables, double* f64, uint8_t* u8);
+/* after the all-reduces: stop rule, exact means, the ordered list of
+ * (b, c, t) that need the row-order replay (*n_fail), the largest number of
+ * empty clusters of a continuing problem (*max_empty), *any_active */
+int pqg_kmshard_apply(pqg_ctx* ctx, pqg_kmshard* h, float* tables, const double* f64, const uint8_t* u8,
+                      uint64_t* n_fail, uint32_t* max_empty, int* any_active);
+/* the local members of the n_fail replay columns in local row order: vals
+ * (device, cap floats) and offcnt (device, 2*n_fail u64: offset, count per
+ * column); vals == NULL only reports *n_vals */
+int pqg_kmshard_pack(pqg_ctx* ctx, pqg_kmshard* h, float* vals, uint64_t cap, uint64_t* offcnt,
+                     uint64_t* n_vals);
+/* the reference's chain over every rank's packed members, rank order:
+ * all_vals world x stride floats, all_offcnt world x 2*n_fail */
+int pqg_kmshard_replay(pqg_ctx* ctx, pqg_kmshard* h, float* tables, const double* f64, const float* all_vals,
+                       uint64_t stride, const uint64_t* all_offcnt, uint32_t world);
+/* per problem the E+1 candidate slots (dist, global index, row) of this rank */
+int pqg_kmshard_reseed_candidates(pqg_ctx* ctx, pqg_kmshard* h, uint64_t row0, uint32_t E, double* cand_d,
+                                  uint64_t* cand_i, float* cand_rows);
+int pqg_kmshard_reseed_apply(pqg_ctx* ctx, pqg_kmshard* h, float* tables, const double* f64, uint32_t E,
+                             uint32_t world, const double* all_d, const uint64_t* all_i, const float* all_rows);
+/* iterations_run[B], inertia[B], inertia_per_iter[B*max_iters], the last
+ * pass's local assignments [B*n] (any nullable; host or device) */
+int pqg_kmshard_result(pqg_ctx* ctx, pqg_kmshard* h, uint32_t* iterations_run, double* inertia,
+                       double* inertia_per_iter, uint32_t* assignments);
+
 #ifdef __cplusplus
 }
 #endif

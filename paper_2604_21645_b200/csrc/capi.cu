@@ -12,6 +12,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <memory>
 #include <numeric>
 #include <random>
 #include <string>
@@ -1690,6 +1691,289 @@ int pqg_kmeans_init_rows(uint64_t n, uint64_t k, uint64_t seed, uint64_t* rows) 
         if (k == 0 || k > n) inval("kmeans_fit: k (" + std::to_string(k) + ") exceeds number of points (" + std::to_string(n) + ")");
         const auto r = init_rows(n, k, seed);
         std::copy(r.begin(), r.end(), rows);
+    });
+}
+
+
+// ---------------------------------------------------------------------------
+// row-sharded k-means: one rank's side (kmshard.cu)
+// ---------------------------------------------------------------------------
+}  // extern "C"
+
+struct pqg_kmshard {
+    pqg_ctx* own = nullptr;  // private context: its pinned arena holds the per-fit buffers
+    RowSrc src;
+    uint64_t n = 0, k = 0;
+    uint32_t B = 0, d = 0, max_iters = 0;
+    double tol = 0.0;
+    uint32_t* assign = nullptr;
+    double* dist = nullptr;
+    uint64_t* offsets = nullptr;
+    uint32_t* perm = nullptr;
+    double* csum = nullptr;
+    int* cmax = nullptr;
+    int* cmin = nullptr;
+    uint32_t* flags = nullptr;
+    uint32_t* work = nullptr;
+    uint32_t* empties = nullptr;
+    float* cnorm = nullptr;
+    float* cmaxn = nullptr;
+    uint64_t* init_rows = nullptr;
+    KMeansState st{};
+    uint64_t n_fail = 0;
+    const uint8_t* big_rows = nullptr;
+    const float* big_nx = nullptr;
+    std::pair<size_t, size_t> mark{0, 0};
+    uint64_t nkd() const { return uint64_t(B) * k * d; }
+};
+
+namespace {
+// every step runs on the caller's current stream, in the handle's arena
+struct ShardStep {
+    pqg_kmshard* h;
+    ShardStep(pqg_ctx* ctx, pqg_kmshard* hh) : h(hh) {
+        if (!ctx || !hh) fail(PQG_EINVAL, "kmshard: null handle");
+        PQG_CUDA(cudaSetDevice(h->own->device));
+        h->own->stream = ctx->stream;
+        h->own->arena.reset_to(h->mark);
+    }
+    ~ShardStep() { h->own->arena.reset_to(h->mark); }
+};
+}  // namespace
+
+extern "C" {
+
+int pqg_kmshard_create(pqg_ctx* ctx, const float* rows, uint64_t n, uint64_t ld, uint32_t B, uint32_t d,
+                       uint32_t col_stride, uint64_t k, uint32_t max_iters, double tol, pqg_kmshard** out_h) {
+    return guard([&] {
+        if (!out_h) inval("kmshard: null output");
+        *out_h = nullptr;
+        if (k == 0) inval("kmeans_fit: k must be >= 1");
+        if (max_iters < 1) inval("kmeans_fit: max_iters must be >= 1");
+        if (tol < 0.0) inval("kmeans_fit: tol must be >= 0");
+        if (n == 0 || B == 0 || d == 0) inval("kmshard: empty shard");
+        if (!on_device(rows)) inval("kmshard: rows must be device memory");
+        RowSrc src;
+        src.x = rows;
+        src.ldx = ld;
+        src.col_stride = col_stride;
+        if (!kmeans_partials_supported(src, d) || uint64_t(B) * k * d > 0xFFFFFFFFull || n > 0xFFFFFFFFull)
+            fail(PQG_EUNSUPPORTED, "kmshard: shape not supported by the sharded update (d % 4, d <= 128)");
+        auto h = std::make_unique<pqg_kmshard>();
+        PQG_CUDA(cudaSetDevice(ctx->device));
+        const int rc = pqg_ctx_create(ctx->device, &h->own);
+        if (rc) fail(rc, g_last_error);
+        h->own->stream = ctx->stream;
+        h->own->arena.depth = 1;  // pinned: the buffers below live until destroy
+        pqg_ctx* o = h->own;
+        h->src = src;
+        h->n = n;
+        h->k = k;
+        h->B = B;
+        h->d = d;
+        h->max_iters = max_iters;
+        h->tol = tol;
+        const uint64_t nkd = uint64_t(B) * k * d;
+        h->assign = scratch<uint32_t>(o, uint64_t(B) * n);
+        h->dist = scratch<double>(o, uint64_t(B) * n);
+        h->offsets = scratch<uint64_t>(o, uint64_t(B) * (k + 1));
+        h->perm = scratch<uint32_t>(o, uint64_t(B) * n);
+        h->csum = scratch<double>(o, nkd);
+        h->cmax = scratch<int>(o, nkd);
+        h->cmin = scratch<int>(o, nkd);
+        h->flags = scratch<uint32_t>(o, nkd);
+        h->work = scratch<uint32_t>(o, nkd);
+        h->empties = scratch<uint32_t>(o, B);
+        h->cnorm = scratch<float>(o, uint64_t(B) * k);
+        h->cmaxn = scratch<float>(o, B);
+        h->init_rows = scratch<uint64_t>(o, uint64_t(B) * k);
+        h->st.active = scratch<int>(o, B);
+        h->st.prev = scratch<double>(o, B);
+        h->st.inertia = scratch<double>(o, B);
+        h->st.per_iter = scratch<double>(o, uint64_t(B) * max_iters);
+        h->st.iters = scratch<uint32_t>(o, B);
+        std::vector<int> ones(B, 1);
+        PQG_CUDA(cudaMemcpyAsync(h->st.active, ones.data(), sizeof(int) * B, cudaMemcpyHostToDevice, o->stream));
+        PQG_CUDA(cudaMemsetAsync(h->st.prev, 0, sizeof(double) * B, o->stream));
+        PQG_CUDA(cudaMemsetAsync(h->st.inertia, 0, sizeof(double) * B, o->stream));
+        PQG_CUDA(cudaMemsetAsync(h->st.per_iter, 0, sizeof(double) * B * max_iters, o->stream));
+        PQG_CUDA(cudaMemsetAsync(h->st.iters, 0, sizeof(uint32_t) * B, o->stream));
+        // coarse fits: the row operand split once for the tensor-core screen
+        NearestArgs prep;
+        prep.src = src;
+        prep.n = n;
+        prep.d = d;
+        prep.B = B;
+        prep.k = k;
+        prep.cmax = h->cmaxn;
+        if (B == 1 && umma_big_prepare_rows(o, prep)) {
+            h->big_rows = prep.big_rows;
+            h->big_nx = prep.big_nx;
+        }
+        h->mark = o->arena.mark();
+        PQG_CUDA(cudaStreamSynchronize(o->stream));
+        *out_h = h.release();
+    });
+}
+
+void pqg_kmshard_destroy(pqg_kmshard* h) {
+    if (!h) return;
+    if (h->own) {
+        cudaStreamSynchronize(h->own->stream);
+        h->own->stream = h->own->own_stream;
+        h->own->arena.depth = 0;
+        pqg_ctx_destroy(h->own);
+    }
+    delete h;
+}
+
+int pqg_kmshard_sizes(const pqg_kmshard* h, uint64_t* n_f64, uint64_t* n_u8) {
+    return guard([&] {
+        if (!h) inval("kmshard: null handle");
+        if (n_f64) *n_f64 = h->nkd() + uint64_t(h->B) * h->k + h->B;
+        if (n_u8) *n_u8 = 2 * h->nkd();
+    });
+}
+
+int pqg_kmshard_init_table(pqg_ctx* ctx, pqg_kmshard* h, const uint64_t* init_rows, uint64_t row0,
+                           uint32_t* table_bits) {
+    return guard([&] {
+        ShardStep step(ctx, h);
+        pqg_ctx* o = h->own;
+        PQG_CUDA(cudaMemcpyAsync(h->init_rows, init_rows, sizeof(uint64_t) * h->B * h->k,
+                                 cudaMemcpyHostToDevice, o->stream));
+        shard_init_gather(o, h->src, h->n, h->B, h->d, h->k, h->init_rows, row0, table_bits);
+        PQG_CUDA(cudaStreamSynchronize(o->stream));  // init_rows is the caller's host buffer
+        ctx->launches += 1;
+    });
+}
+
+int pqg_kmshard_partials(pqg_ctx* ctx, pqg_kmshard* h, const float* tables, double* f64, uint8_t* u8) {
+    return guard([&] {
+        ShardStep step(ctx, h);
+        pqg_ctx* o = h->own;
+        const uint64_t l0 = o->launches;
+        table_norms(o, tables, h->B, h->k, h->d, h->cnorm, h->cmaxn);
+        NearestArgs a;
+        a.src = h->src;
+        a.n = h->n;
+        a.d = h->d;
+        a.B = h->B;
+        a.table = tables;
+        a.k = h->k;
+        a.cnorm = h->cnorm;
+        a.cmax = h->cmaxn;
+        a.out_idx = h->assign;
+        a.idx_bytes = 4;
+        a.idx_rs = 1;
+        a.idx_ps = h->n;
+        a.out_dist = h->dist;
+        a.active = h->st.active;
+        a.big_rows = h->big_rows;
+        a.big_nx = h->big_nx;
+        nearest(o, a);
+        kmeans_local_partials(o, h->src, h->n, h->B, h->d, h->k, h->assign, h->st.active, h->offsets,
+                              h->perm, h->csum, h->cmax, h->cmin);
+        shard_pack_partials(o, h->B, h->k, h->d, h->offsets, h->csum, h->cmax, h->cmin, f64, u8);
+        rows_sum_f64(o, h->dist, h->n, h->B, f64 + h->nkd() + uint64_t(h->B) * h->k);
+        ctx->launches += o->launches - l0;
+    });
+}
+
+int pqg_kmshard_apply(pqg_ctx* ctx, pqg_kmshard* h, float* tables, const double* f64, const uint8_t* u8,
+                      uint64_t* n_fail, uint32_t* max_empty, int* any_active) {
+    return guard([&] {
+        ShardStep step(ctx, h);
+        pqg_ctx* o = h->own;
+        const uint64_t l0 = o->launches;
+        kmeans_stop_global(o, f64 + h->nkd() + uint64_t(h->B) * h->k, h->B, h->max_iters, h->tol, h->st);
+        shard_finalize(o, h->B, h->k, h->d, f64, u8, h->st.active, tables, h->flags, h->empties);
+        h->n_fail = shard_compact(o, h->flags, h->nkd(), h->work);  // synchronises
+        std::vector<uint32_t> emp(h->B);
+        std::vector<int> act(h->B);
+        PQG_CUDA(cudaMemcpyAsync(emp.data(), h->empties, sizeof(uint32_t) * h->B, cudaMemcpyDeviceToHost, o->stream));
+        PQG_CUDA(cudaMemcpyAsync(act.data(), h->st.active, sizeof(int) * h->B, cudaMemcpyDeviceToHost, o->stream));
+        PQG_CUDA(cudaStreamSynchronize(o->stream));
+        uint32_t me = 0;
+        int aa = 0;
+        for (uint32_t b = 0; b < h->B; ++b) {
+            if (act[b]) me = std::max(me, emp[b]);
+            aa |= act[b];
+        }
+        if (n_fail) *n_fail = h->n_fail;
+        if (max_empty) *max_empty = me;
+        if (any_active) *any_active = aa;
+        ctx->launches += o->launches - l0;
+    });
+}
+
+int pqg_kmshard_pack(pqg_ctx* ctx, pqg_kmshard* h, float* vals, uint64_t cap, uint64_t* offcnt,
+                     uint64_t* n_vals) {
+    return guard([&] {
+        ShardStep step(ctx, h);
+        pqg_ctx* o = h->own;
+        const uint64_t l0 = o->launches;
+        uint64_t* oc = offcnt ? offcnt : scratch<uint64_t>(o, std::max<uint64_t>(1, 2 * h->n_fail));
+        const uint64_t tot = shard_pack_layout(o, h->work, h->n_fail, h->k, h->d, h->offsets, oc);
+        if (n_vals) *n_vals = tot;
+        if (vals) {
+            if (tot > cap) inval("kmshard_pack: value buffer too small");
+            shard_pack(o, h->src, h->work, h->n_fail, h->k, h->d, h->offsets, h->perm, h->n, oc, vals);
+        }
+        ctx->launches += o->launches - l0;
+    });
+}
+
+int pqg_kmshard_replay(pqg_ctx* ctx, pqg_kmshard* h, float* tables, const double* f64, const float* all_vals,
+                       uint64_t stride, const uint64_t* all_offcnt, uint32_t world) {
+    return guard([&] {
+        ShardStep step(ctx, h);
+        pqg_ctx* o = h->own;
+        const uint64_t l0 = o->launches;
+        shard_replay(o, h->work, h->n_fail, h->k, h->d, h->B, f64, all_vals, stride, all_offcnt, world, tables);
+        ctx->launches += o->launches - l0;
+    });
+}
+
+int pqg_kmshard_reseed_candidates(pqg_ctx* ctx, pqg_kmshard* h, uint64_t row0, uint32_t E, double* cand_d,
+                                  uint64_t* cand_i, float* cand_rows) {
+    return guard([&] {
+        ShardStep step(ctx, h);
+        pqg_ctx* o = h->own;
+        const uint64_t l0 = o->launches;
+        shard_reseed_candidates(o, h->src, h->n, h->B, h->d, h->dist, h->st.active, h->empties, E, row0, cand_d,
+                                cand_i, cand_rows);
+        ctx->launches += o->launches - l0;
+    });
+}
+
+int pqg_kmshard_reseed_apply(pqg_ctx* ctx, pqg_kmshard* h, float* tables, const double* f64, uint32_t E,
+                             uint32_t world, const double* all_d, const uint64_t* all_i, const float* all_rows) {
+    return guard([&] {
+        ShardStep step(ctx, h);
+        pqg_ctx* o = h->own;
+        const uint64_t l0 = o->launches;
+        shard_reseed_apply(o, h->B, h->k, h->d, f64, h->st.active, E, world, all_d, all_i, all_rows, tables);
+        ctx->launches += o->launches - l0;
+    });
+}
+
+int pqg_kmshard_result(pqg_ctx* ctx, pqg_kmshard* h, uint32_t* iterations_run, double* inertia,
+                       double* inertia_per_iter, uint32_t* assignments) {
+    return guard([&] {
+        ShardStep step(ctx, h);
+        pqg_ctx* o = h->own;
+        if (iterations_run)
+            PQG_CUDA(cudaMemcpyAsync(iterations_run, h->st.iters, sizeof(uint32_t) * h->B, cudaMemcpyDefault, o->stream));
+        if (inertia)
+            PQG_CUDA(cudaMemcpyAsync(inertia, h->st.inertia, sizeof(double) * h->B, cudaMemcpyDefault, o->stream));
+        if (inertia_per_iter)
+            PQG_CUDA(cudaMemcpyAsync(inertia_per_iter, h->st.per_iter, sizeof(double) * h->B * h->max_iters,
+                                     cudaMemcpyDefault, o->stream));
+        if (assignments)
+            PQG_CUDA(cudaMemcpyAsync(assignments, h->assign, sizeof(uint32_t) * h->B * h->n, cudaMemcpyDefault,
+                                     o->stream));
+        PQG_CUDA(cudaStreamSynchronize(o->stream));
     });
 }
 

@@ -91,6 +91,36 @@ void kmeans_inertia_and_stop(pqg_ctx* ctx, const double* dist, uint64_t n, uint3
 void kmeans_update(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint32_t d,
                    float* table, uint64_t k, const uint32_t* assign, double* dist,
                    const int* active, const uint64_t* nb = nullptr);
+// Row-sharded fits (kmshard.cu): one rank's bucketing + exact piece sums with
+// exponent ranges, and the stop rule on an already reduced inertia.
+bool kmeans_partials_supported(const RowSrc& src, uint32_t d);
+void kmeans_local_partials(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint32_t d,
+                           uint64_t k, const uint32_t* assign, const int* active, uint64_t* offsets,
+                           uint32_t* perm, double* csum, int* cmax, int* cmin);
+void kmeans_stop_global(pqg_ctx* ctx, const double* inertia, uint32_t B, uint32_t max_iters, double tol,
+                        KMeansState st);
+// kmshard.cu: the exchange-side kernels of pqg_kmshard_*
+void shard_init_gather(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint32_t d, uint64_t k,
+                       const uint64_t* rows, uint64_t row0, uint32_t* bits);
+void shard_pack_partials(pqg_ctx* ctx, uint32_t B, uint64_t k, uint32_t d, const uint64_t* offsets,
+                         const double* csum, const int* cmax, const int* cmin, double* f64, uint8_t* u8);
+void shard_finalize(pqg_ctx* ctx, uint32_t B, uint64_t k, uint32_t d, const double* f64, const uint8_t* u8,
+                    const int* active, float* table, uint32_t* flags, uint32_t* empties);
+uint64_t shard_compact(pqg_ctx* ctx, const uint32_t* flags, uint64_t count, uint32_t* work);
+uint64_t shard_pack_layout(pqg_ctx* ctx, const uint32_t* work, uint64_t n_fail, uint64_t k, uint32_t d,
+                           const uint64_t* offsets, uint64_t* offcnt);
+void shard_pack(pqg_ctx* ctx, const RowSrc& src, const uint32_t* work, uint64_t n_fail, uint64_t k,
+                uint32_t d, const uint64_t* offsets, const uint32_t* perm, uint64_t n, const uint64_t* offcnt,
+                float* vals);
+void shard_replay(pqg_ctx* ctx, const uint32_t* work, uint64_t n_fail, uint64_t k, uint32_t d, uint32_t B,
+                  const double* f64, const float* vals, uint64_t stride, const uint64_t* offcnt,
+                  uint32_t world, float* table);
+void shard_reseed_candidates(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint32_t d,
+                             const double* dist, const int* active, const uint32_t* empties, uint32_t E,
+                             uint64_t row0, double* cand_d, uint64_t* cand_i, float* cand_rows);
+void shard_reseed_apply(pqg_ctx* ctx, uint32_t B, uint64_t k, uint32_t d, const double* f64,
+                        const int* active, uint32_t E, uint32_t world, const double* cand_d,
+                        const uint64_t* cand_i, const float* cand_rows, float* table);
 // Batched problems of unequal length (nb[b] <= n rows, the rest padding):
 // padding rows get key k so the update ignores them.
 void kmeans_pad_keys(pqg_ctx* ctx, uint32_t* keys, uint64_t n, uint32_t B, uint64_t k,

@@ -1261,4 +1261,44 @@ void kmeans_update(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint
            d, k, (const uint64_t*)bk.offsets, dist, table, (const int*)has_empty, active, nb);
 }
 
+// ---- one rank's side of a row-sharded fit (kmshard.cu, pqg_kmshard_*) -----
+// The stable bucketing of the rank's rows by cluster and the exact piece sums
+// with their exponent ranges (csum / cmax / cmin per (problem, cluster,
+// dim)), exactly as kmeans_update computes them before its finalize.
+bool kmeans_partials_supported(const RowSrc& src, uint32_t d) {
+    return d % 4 == 0 && d <= 128 && ((src.ldx | src.col_stride) & 3u) == 0 &&
+           (reinterpret_cast<uintptr_t>(src.x) & 15u) == 0 && !src.codes;
+}
+
+void kmeans_local_partials(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint32_t d,
+                           uint64_t k, const uint32_t* assign, const int* active, uint64_t* offsets,
+                           uint32_t* perm, double* csum, int* cmax, int* cmin) {
+    Bucketing bk{offsets, perm};
+    bucket_impl(ctx, assign, n, B, k, bk, nullptr, nullptr);
+    const PieceGeom pg = piece_geom(d, n, k);
+    if (uint64_t(B) * pg.PP > 0xFFFFFFFFull) fail(PQG_EUNSUPPORTED, "kmeans: too many pieces");
+    uint32_t* piece_start = scratch<uint32_t>(ctx, uint64_t(B) * k);
+    PieceDesc* pieces_d = scratch<PieceDesc>(ctx, uint64_t(B) * pg.PP);
+    PieceStat* stats = scratch<PieceStat>(ctx, uint64_t(B) * pg.PP * d);
+    unsigned long long* work_count = scratch<unsigned long long>(ctx, 1);
+    int* has_empty = scratch<int>(ctx, B);
+    launch(ctx, "kmeans_sum", pieces_setup_kernel, dim3(B), dim3(1024), 0, (const uint64_t*)offsets, k, pg.R,
+           pg.PP, piece_start, pieces_d, has_empty, active, d, csum, cmax, cmin, work_count);
+    MemberRows mr;
+    mr.x = src.x;
+    mr.ldx = src.ldx;
+    mr.col_stride = src.col_stride;
+    mr.perm = perm;
+    const uint64_t warps = uint64_t(B) * pg.PP;
+    launch(ctx, "kmeans_sum", mean_pieces_kernel, dim3(unsigned((warps + 7) / 8)), dim3(kMeanThreads), 0, mr, n,
+           d, k, B, (const PieceDesc*)pieces_d, stats, active, csum, cmax, cmin);
+}
+
+// The stop rule (kmeans.cpp:93-100) on an already reduced per-problem inertia.
+void kmeans_stop_global(pqg_ctx* ctx, const double* inertia, uint32_t B, uint32_t max_iters, double tol,
+                        KMeansState st) {
+    launch(ctx, "inertia", stop_kernel, dim3(B), dim3(kRedThreads), 0, inertia, 1u, 0u, max_iters, tol, st,
+           (const uint64_t*)nullptr);
+}
+
 }  // namespace pqg

@@ -10,11 +10,21 @@ logic is backend-independent, so it is tested on CPU with gloo and an
 oracle-backed backend (tests/test_dist_gloo.py) and on a GPU with NCCL
 (tests/test_dist_gpu.py).
 
-* ``kmeans_fit_sharded`` -- exact: each rank runs the assignment pass on its
-  shard of the training sample, assignments + fp64 distances are
-  all-gathered in global row order, and every rank runs the reference's
-  ordered update (proj/src/kmeans.cpp:102-130) on the replicated sample, so
-  the result is bit-identical to single-process ``kmeans_fit`` / ``pq_fit``.
+* ``kmeans_fit_sharded`` -- the north-star exchange, exact: per iteration
+  each rank assigns its block of the training sample and computes its exact
+  per-(problem, cluster, dim) fp64 sums, exponent ranges, counts and inertia
+  on the device (``pqg_kmshard_partials``); ONE all-reduce SUM of the fp64
+  partials (Ks x D sums + counts + inertia) and one all-reduce MAX of the u8
+  exponent ranges carry the iteration; every rank then finalizes
+  identically (``pqg_kmshard_apply``): sums whose global exponent range
+  proves them exact are the reference's row-order sums
+  (proj/src/kmeans.cpp:103-118), the rare rest are replayed in global row
+  order from the members the ranks all-gather, and empty clusters are
+  reseeded from every rank's best candidates (:122-130).  The result is
+  bit-identical to single-process ``kmeans_fit`` / ``pq_fit``.  Shapes the
+  device partials do not cover (d % 4 != 0, d > 128) use the replicated
+  update: assignments + distances all-gathered, the ordered update on every
+  rank.
 * ``encode_sharded`` -- shard-local encode, global SSE by one all-reduce.
 * ``search_sharded`` -- shard-local index + search, all-gather of the
   per-shard top-k lists, merge by (dist, id): equal to the monolithic
@@ -84,6 +94,22 @@ class Comm:
         self.dist.all_reduce(t, group=self.group)
         return float(t.item())
 
+    def allreduce_(self, t, op="sum"):
+        """In-place all-reduce of a tensor (SUM or MAX)."""
+        rop = self.dist.ReduceOp.SUM if op == "sum" else self.dist.ReduceOp.MAX
+        self.dist.all_reduce(t, op=rop, group=self.group)
+        return t
+
+    def allgather_padded(self, t):
+        """1-D tensors of per-rank lengths -> ([world, stride] padded stack, stride)."""
+        import torch
+        n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+        sizes = [int(v) for v in self.allgather_equal(n).view(-1).tolist()]
+        stride = max(1, max(sizes))
+        pad = torch.zeros(stride, dtype=t.dtype, device=t.device)
+        pad[: t.numel()] = t
+        return self.allgather_equal(pad), stride
+
     def allgather_equal(self, t):
         import torch
         outs = [torch.empty_like(t) for _ in range(self.world)]
@@ -146,6 +172,89 @@ class CudaBackend:
                                               self._p(tables), k, self._p(assign), self._p(dist),
                                               self._p(act)), "update_pass")
 
+    # -- one rank's side of the sharded fit (include/pqg.h pqg_kmshard_*) --
+    def shard_create(self, rows, B, d, col_stride, k, max_iters, tol):
+        """A device handle, or None where the sharded update does not apply."""
+        h = C.c_void_p()
+        n, ld = rows.shape
+        rc = self.lib.pqg_kmshard_create(self.ctx.h, self._p(rows), n, ld, B, d, col_stride, k,
+                                         max_iters, tol, C.byref(h))
+        if rc == self.L.PQG_EUNSUPPORTED:
+            return None
+        self.L.check(rc, "kmshard_create")
+        nf, nu = C.c_uint64(), C.c_uint64()
+        self.L.check(self.lib.pqg_kmshard_sizes(h, C.byref(nf), C.byref(nu)), "kmshard_sizes")
+        return {"h": h, "rows": rows, "B": B, "d": d, "k": k, "n": n, "max_iters": max_iters,
+                "nf": nf.value, "nu": nu.value}
+
+    def shard_destroy(self, s):
+        self.lib.pqg_kmshard_destroy(s["h"])
+
+    def shard_init_table(self, s, init_rows, row0):
+        bits = self.torch.empty((s["B"], s["k"], s["d"]), dtype=self.torch.int32, device=s["rows"].device)
+        init = np.ascontiguousarray(init_rows, np.uint64)
+        self.L.check(self.lib.pqg_kmshard_init_table(self.ctx.h, s["h"], init.ctypes.data_as(C.c_void_p),
+                                                     row0, self._p(bits)), "kmshard_init")
+        return bits
+
+    def shard_partials(self, s, tables):
+        torch = self.torch
+        dev = s["rows"].device
+        f64 = torch.empty(s["nf"], dtype=torch.float64, device=dev)
+        u8 = torch.empty(s["nu"], dtype=torch.uint8, device=dev)
+        self.L.check(self.lib.pqg_kmshard_partials(self.ctx.h, s["h"], self._p(tables), self._p(f64),
+                                                   self._p(u8)), "kmshard_partials")
+        return f64, u8
+
+    def shard_apply(self, s, tables, f64, u8):
+        nf, me, aa = C.c_uint64(), C.c_uint32(), C.c_int()
+        self.L.check(self.lib.pqg_kmshard_apply(self.ctx.h, s["h"], self._p(tables), self._p(f64), self._p(u8),
+                                                C.byref(nf), C.byref(me), C.byref(aa)), "kmshard_apply")
+        return nf.value, me.value, bool(aa.value)
+
+    def shard_pack(self, s, n_fail):
+        torch = self.torch
+        dev = s["rows"].device
+        nv = C.c_uint64()
+        self.L.check(self.lib.pqg_kmshard_pack(self.ctx.h, s["h"], None, 0, None, C.byref(nv)), "kmshard_pack")
+        vals = torch.empty(max(1, nv.value), dtype=torch.float32, device=dev)
+        offcnt = torch.empty(2 * n_fail, dtype=torch.int64, device=dev)
+        self.L.check(self.lib.pqg_kmshard_pack(self.ctx.h, s["h"], self._p(vals), vals.numel(), self._p(offcnt),
+                                               C.byref(nv)), "kmshard_pack")
+        return vals[: nv.value], offcnt
+
+    def shard_replay(self, s, tables, f64, all_vals, stride, all_offcnt, world):
+        self.L.check(self.lib.pqg_kmshard_replay(self.ctx.h, s["h"], self._p(tables), self._p(f64),
+                                                 self._p(all_vals.contiguous()), stride,
+                                                 self._p(all_offcnt.contiguous()), world), "kmshard_replay")
+
+    def shard_reseed_candidates(self, s, row0, E):
+        torch = self.torch
+        dev = s["rows"].device
+        B, d = s["B"], s["d"]
+        cd = torch.empty((B, E + 1), dtype=torch.float64, device=dev)
+        ci = torch.empty((B, E + 1), dtype=torch.int64, device=dev)
+        cr = torch.empty((B, E + 1, d), dtype=torch.float32, device=dev)
+        self.L.check(self.lib.pqg_kmshard_reseed_candidates(self.ctx.h, s["h"], row0, E, self._p(cd), self._p(ci),
+                                                            self._p(cr)), "kmshard_reseed")
+        return cd, ci, cr
+
+    def shard_reseed_apply(self, s, tables, f64, E, world, all_d, all_i, all_r):
+        self.L.check(self.lib.pqg_kmshard_reseed_apply(self.ctx.h, s["h"], self._p(tables), self._p(f64), E, world,
+                                                       self._p(all_d.contiguous()), self._p(all_i.contiguous()),
+                                                       self._p(all_r.contiguous())), "kmshard_reseed")
+
+    def shard_result(self, s):
+        B, mi = s["B"], s["max_iters"]
+        iters = np.empty(B, np.uint32)
+        inertia = np.empty(B, np.float64)
+        per = np.empty((B, mi), np.float64)
+        assign = self.torch.empty((B, s["n"]), dtype=self.torch.int32, device=s["rows"].device)
+        v = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        self.L.check(self.lib.pqg_kmshard_result(self.ctx.h, s["h"], v(iters), v(inertia), v(per),
+                                                 self._p(assign)), "kmshard_result")
+        return iters, inertia, per, assign
+
     def encode_sse(self, rows, tables):
         torch = self.torch
         M, ks, ds = tables.shape
@@ -202,10 +311,11 @@ class ShardedFit:
 
 
 def kmeans_fit_sharded(comm: Comm, backend, local_rows, B: int, d: int, col_stride: int, k: int,
-                       max_iters: int, seeds, tol: float = 1e-4) -> ShardedFit:
+                       max_iters: int, seeds, tol: float = 1e-4, stats: dict | None = None) -> ShardedFit:
     """B batched k-means problems (B = M subspaces for pq_fit, B = 1 for the
     coarse quantizer) over rows sharded by rank; bit-identical to the
-    single-process fit (see module docstring)."""
+    single-process fit (see module docstring).  ``stats`` (optional) receives
+    the exchange volume: bytes all-reduced / all-gathered per iteration."""
     import torch
     dev = local_rows.device
     counts = [int(c) for c in comm.allgather_equal(
@@ -217,6 +327,57 @@ def kmeans_fit_sharded(comm: Comm, backend, local_rows, B: int, d: int, col_stri
         raise ValueError(f"kmeans_fit: k ({k}) exceeds number of points ({n})")
     if max_iters < 1:
         raise ValueError("kmeans_fit: max_iters must be >= 1")
+    if tol < 0:
+        raise ValueError("kmeans_fit: tol must be >= 0")
+    row0 = sum(counts[: comm.rank])
+    s = backend.shard_create(local_rows.contiguous(), B, d, col_stride, k, max_iters, tol) \
+        if hasattr(backend, "shard_create") and min(counts) > 0 else None
+    if s is None:
+        return _kmeans_fit_replicated(comm, backend, local_rows, counts, B, d, col_stride, k, max_iters,
+                                      seeds, tol)
+    st = stats if stats is not None else {}
+    st.update(allreduce_bytes=0, allgather_bytes=0, replay_columns=0, reseeds=0, iterations=0)
+    try:
+        init = np.concatenate([backend.init_rows(n, k, int(seeds[b])) for b in range(B)])
+        bits = backend.shard_init_table(s, init, row0)
+        comm.allreduce_(bits, "sum")  # owners' bit patterns, zeros elsewhere: exact
+        tables = bits.view(torch.float32)
+        for _ in range(max_iters):
+            f64, u8 = backend.shard_partials(s, tables)
+            comm.allreduce_(f64, "sum")
+            comm.allreduce_(u8, "max")
+            st["allreduce_bytes"] += f64.numel() * 8 + u8.numel()
+            st["iterations"] += 1
+            n_fail, max_empty, any_active = backend.shard_apply(s, tables, f64, u8)
+            if n_fail:  # columns whose sum may round: the row-order replay
+                vals, offcnt = backend.shard_pack(s, n_fail)
+                all_vals, stride = comm.allgather_padded(vals)
+                all_oc = comm.allgather_equal(offcnt)
+                backend.shard_replay(s, tables, f64, all_vals, stride, all_oc, comm.world)
+                st["replay_columns"] += n_fail
+                st["allgather_bytes"] += all_vals.numel() * 4 + all_oc.numel() * 8
+            if max_empty:
+                cd, ci, cr = backend.shard_reseed_candidates(s, row0, max_empty)
+                backend.shard_reseed_apply(s, tables, f64, max_empty, comm.world, comm.allgather_equal(cd),
+                                           comm.allgather_equal(ci), comm.allgather_equal(cr))
+                st["reseeds"] += 1
+            if not any_active:
+                break
+        iters, inertia, per, assign = backend.shard_result(s)
+    finally:
+        backend.shard_destroy(s)
+    per_iter = [[float(v) for v in per[b, : iters[b]]] for b in range(B)]
+    return ShardedFit(tables, comm.allgather_cols(assign, counts), inertia, iters, per_iter)
+
+
+def _kmeans_fit_replicated(comm: Comm, backend, local_rows, counts, B, d, col_stride, k, max_iters, seeds,
+                           tol) -> ShardedFit:
+    """The replicated update for shapes the device partials do not cover:
+    assignments + distances all-gathered in global row order, the reference's
+    ordered update (kmeans.cpp:102-130) on every rank."""
+    import torch
+    dev = local_rows.device
+    n = sum(counts)
     full = comm.allgather_rows(local_rows.contiguous(), counts)
     tables = torch.empty((B, k, d), dtype=torch.float32, device=dev)
     for b in range(B):  # init rows: the reference's draws, identical on every rank
