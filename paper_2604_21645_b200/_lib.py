@@ -76,6 +76,17 @@ _SIGS = {
     "pqg_update_pass": (_i32, [_vp, _vp, _u64, _u64, _u32, _u32, _u32, _vp, _u64, _vp, _vp, _vp]),
     "pqg_rows_sum_f64": (_i32, [_vp, _vp, _u64, _u32, _vp]),
     "pqg_kmeans_init_rows": (_i32, [_u64, _u64, _u64, _vp]),
+    "pqg_kmshard_create": (_i32, [_vp, _vp, _u64, _u64, _u32, _u32, _u32, _u64, _u32, _f64, C.POINTER(_vp)]),
+    "pqg_kmshard_destroy": (None, [_vp]),
+    "pqg_kmshard_sizes": (_i32, [_vp, C.POINTER(_u64), C.POINTER(_u64)]),
+    "pqg_kmshard_init_table": (_i32, [_vp, _vp, _vp, _u64, _vp]),
+    "pqg_kmshard_partials": (_i32, [_vp, _vp, _vp, _vp, _vp]),
+    "pqg_kmshard_apply": (_i32, [_vp, _vp, _vp, _vp, _vp, C.POINTER(_u64), C.POINTER(_u32), C.POINTER(_i32)]),
+    "pqg_kmshard_pack": (_i32, [_vp, _vp, _vp, _u64, _vp, C.POINTER(_u64)]),
+    "pqg_kmshard_replay": (_i32, [_vp, _vp, _vp, _vp, _vp, _u64, _vp, _u32]),
+    "pqg_kmshard_reseed_candidates": (_i32, [_vp, _vp, _u64, _u32, _vp, _vp, _vp]),
+    "pqg_kmshard_reseed_apply": (_i32, [_vp, _vp, _vp, _vp, _u32, _u32, _vp, _vp, _vp]),
+    "pqg_kmshard_result": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "pqg_train_chunks": (_i32, [_vp, _vp, _u64, _u64, _u64, _u32, _u32, _u32, _u64, _vp, _vp,
                                 _vp]),
     "pqg_pipeline_run": (_i32, [_vp, _vp, _u64, _u64, _u64, _u32, _u32, _u64, _u32, _u64, _i32,

@@ -123,7 +123,7 @@ class Comm:
 class CudaBackend:
     """Shard-local compute through the C ABI (include/pqg.h) on CUDA tensors."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, private: bool = False):
         import torch
 
         from . import _lib, pqii
@@ -131,7 +131,8 @@ class CudaBackend:
         self.L = _lib
         self.pqii = pqii
         self.device = torch.device("cuda", device)
-        self.ctx = pqii.get_context(device)
+        # private: a context of its own (several backends driven from threads)
+        self.ctx = pqii.Context(device) if private else pqii.get_context(device)
         self.lib = self.ctx.lib
         # libpqg runs on torch's current stream so collectives and kernels order;
         # torch's default stream is the legacy stream (handle 0 -> cudaStreamLegacy)

@@ -60,3 +60,29 @@ def test_sharded_pipeline_world2(tmp_path, orc):
         assert c == len(ri)
         assert np.array_equal(r[0]["s_ids"][qi, :c], ri)
         assert np.array_equal(r[0]["s_d"][qi, :c].view(np.uint64), rd.view(np.uint64))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_kmeans_exchange_paths(tmp_path, orc, world):
+    """The north-star exchange (all-reduce of sums / counts / exponent ranges,
+    all-gathered row-order replay, reseed candidates) on rows that force the
+    replay and the reseed, world 2 and 3 (uneven shards): equal to the
+    single-process reference bit for bit."""
+    import torch.multiprocessing as mp
+
+    from dist_workers import run_rank_stress, stress_data
+    port = free_port()
+    mp.start_processes(run_rank_stress, args=(world, port, str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    r = [np.load(tmp_path / f"stress{i}.npz") for i in range(world)]
+    x = stress_data()
+    ref = orc.kmeans_fit(x, 40, 9, 2, 0.0)
+    for rr in r:
+        assert np.array_equal(rr["km_tables"][0].view(np.uint32), ref["centroids"].view(np.uint32))
+        assert np.array_equal(rr["km_assign"][0], ref["assignments"])
+        assert int(rr["km_iters"][0]) == ref["iterations_run"]
+    assert r[0]["stats"][0] > 0, "the row-order replay path was not exercised"
+    assert r[0]["stats"][1] > 0, "the reseed path was not exercised"
+    t, _, _ = orc.pq_fit(x, 2, 32, 8, 7)
+    for rr in r:
+        assert np.array_equal(rr["pq_tables"].view(np.uint32), t.view(np.uint32))
