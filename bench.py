@@ -179,6 +179,66 @@ def reference_encode_rate(x: np.ndarray, tables: np.ndarray, threads: int, rows:
     return rows / dt, dt
 
 
+def rank_of() -> int:
+    return int(os.environ.get("RANK", "0"))
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or platform.machine()
+
+
+def cpu_baselines(x_host, train_h, adc_host, budget_s: float = 25.0):
+    """The reference (oracle/_ref, compiled from its sources) on this host's
+    cores, on bounded samples of the bench's own workloads:
+    k-means passes of pq_fit (1 thread; all cores = one thread per subspace,
+    kmeans_fit's documented concurrency, kmeans.hpp:40) and ivf_query over the
+    configs[2] index the GPU built (1 thread; all cores = queries split over
+    threads, a frozen index is reader-safe, ivf.hpp:20-22)."""
+    import oracle
+    R = oracle.ref_impl()
+    thr = max(1, R.hardware_concurrency())
+    out = {"cpu_model": cpu_model(), "threads": thr}
+    ds = DIMS // HEAD_M
+    # k-means: 2 passes (1 update) of the headline pq_fit on the 100k sample
+    t0 = time.perf_counter()
+    R.kmeans_fit(np.ascontiguousarray(train_h[:, :ds]), HEAD_KS, 2, SEED, 0.0)
+    one = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    R.pq_fit_stats(train_h, HEAD_M, HEAD_KS, 2, SEED, thr)
+    allc = time.perf_counter() - t0
+    # per full iteration over all M subspaces (2 passes per fit measured)
+    out["kmeans_iters_per_s_1thread"] = 2.0 / (one * HEAD_M)
+    out["kmeans_iters_per_s_allcores"] = 2.0 / allc
+    out["kmeans_sample"] = (f"kmeans_fit 2 passes of one subspace (100k x {ds}, Ks={HEAD_KS}) x M={HEAD_M} "
+                            f"on 1 thread; pq_fit 2 passes with the M subspaces on {thr} threads")
+    if adc_host is not None:
+        a = adc_host
+        ids = np.arange(a["codes"].shape[0], dtype=np.uint64)
+        idx = R.ivf_build_with_centroids_mt(a["codes"], ids, a["tables"], a["coarse"], thr)
+        q = a["queries"]
+        n1 = 300
+        t0 = time.perf_counter()
+        idx.query_batch(q[:n1], a["k"], a["nprobe"], threads=1)
+        q1 = n1 / (time.perf_counter() - t0)
+        nall = min(q.shape[0], max(n1, int(q1 * thr * 2)))
+        t0 = time.perf_counter()
+        idx.query_batch(q[:nall], a["k"], a["nprobe"], threads=thr)
+        qa = nall / (time.perf_counter() - t0)
+        out["adc_queries_per_s_1thread"] = q1
+        out["adc_queries_per_s_allcores"] = qa
+        out["adc_sample"] = (f"ivf_query (nprobe {a['nprobe']}, k {a['k']}) over the configs[2] index "
+                             f"(1M items, nlist 1024): {n1} queries on 1 thread, {nall} on {thr} threads")
+    return out
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -304,22 +364,35 @@ def run_ours(args, rank, world, local):
     fit_s = max_over_ranks(time.perf_counter() - t0, world)
     kmeans_ips = iters_run / fit_s
 
-    # ---- exact sharded PQ fit over the ranks' samples (torchrun only):
-    # assignment pass per shard, all-gather, replicated ordered update
+    # ---- exact sharded PQ fit over the ranks' samples (the north-star
+    # exchange: one all-reduce of sums / counts / exponent ranges per
+    # iteration over NCCL; a 1-rank NCCL group when not under torchrun)
     sharded_fit = None
-    if distributed():
+    if not args.quick:
         from paper_2604_21645_b200 import dist as D
+        if not distributed():
+            import torch.distributed as tdist
+            tdist.init_process_group("nccl", store=tdist.HashStore(), rank=0, world_size=1,
+                                     device_id=torch.device("cuda", local))
         comm, be = D.Comm(), D.CudaBackend(local)
         be.ctx.set_stream(stream.cuda_stream)
-        D.pq_fit_sharded(comm, be, train, HEAD_M, HEAD_KS, 2, SEED)  # warm-up
+        ds = DIMS // HEAD_M
+        seeds = [SEED + m for m in range(HEAD_M)]
+        D.kmeans_fit_sharded(comm, be, train, HEAD_M, ds, ds, HEAD_KS, 2, seeds)  # warm-up
         torch.cuda.synchronize()
         barrier(world)
+        st = {}
         t0 = time.perf_counter()
-        D.pq_fit_sharded(comm, be, train, HEAD_M, HEAD_KS, FIT_ITERS, SEED)
+        sf = D.kmeans_fit_sharded(comm, be, train, HEAD_M, ds, ds, HEAD_KS, FIT_ITERS, seeds, 1e-4, stats=st)
         torch.cuda.synchronize()
         sf_s = max_over_ranks(time.perf_counter() - t0, world)
-        sharded_fit = {"global_sample_rows": SAMPLE * world, "iters": FIT_ITERS, "seconds": sf_s,
-                       "iters_per_s": FIT_ITERS / sf_s}
+        same = bool(torch.equal(sf.tables, tables)) if world == 1 else None
+        sharded_fit = {"global_sample_rows": SAMPLE * world, "iters_run": int(np.max(sf.iterations_run)),
+                       "seconds": sf_s, "iters_per_s": int(np.max(sf.iterations_run)) / sf_s,
+                       "single_process_seconds": fit_s,
+                       "allreduce_bytes_per_iter": st["allreduce_bytes"] / max(1, st["iterations"]),
+                       "replay_columns": st["replay_columns"], "reseeds": st["reseeds"],
+                       "bit_identical_to_single_process": same}
 
     # ---- headline encode, timed with profiling of the dominant kernel
     codes = torch.empty((N_ROWS, HEAD_M), dtype=torch.uint8, device="cuda")
@@ -419,6 +492,12 @@ def run_ours(args, rank, world, local):
 
     if rank != 0:
         return
+    adc_host = adc.pop("_host", None) if adc else None
+    if cpu is not None and cpu.get("value") and not args.no_cpu:
+        try:
+            cpu["extra"] = cpu_baselines(x_host, train.cpu().numpy(), adc_host)
+        except Exception as e:  # reported, never required
+            cpu["extra"] = {"unavailable": str(e)}
     out = {
         "metric": METRIC, "value": value, "unit": "vectors/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -474,24 +553,29 @@ def adc_bench(ctx, lib, L, x, train, args, world, stream, timed):
     coarse = torch.empty((nlist, DIMS), dtype=torch.float32, device="cuda")
     inertia = C.c_double()
     it = C.c_uint32()
-    t0 = time.perf_counter()
-    L.check(lib.pqg_kmeans_fit(ctx.h, vp(train.data_ptr()), SAMPLE, DIMS, nlist, 20, SEED + M,
-                               1e-4, vp(coarse.data_ptr()), None, C.byref(inertia), C.byref(it),
-                               None))
-    torch.cuda.synchronize()
-    coarse_s = time.perf_counter() - t0
+    for rep in range(2):  # the second (warm) fit is timed
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        L.check(lib.pqg_kmeans_fit(ctx.h, vp(train.data_ptr()), SAMPLE, DIMS, nlist, 20, SEED + M,
+                                   1e-4, vp(coarse.data_ptr()), None, C.byref(inertia), C.byref(it),
+                                   None))
+        torch.cuda.synchronize()
+        coarse_s = time.perf_counter() - t0
     codes = torch.empty((N_ROWS, M), dtype=torch.uint8, device="cuda")
     L.check(lib.pqg_pq_encode(ctx.h, vp(x.data_ptr()), N_ROWS, M, ks, DIMS // M,
                               vp(tables.data_ptr()), vp(codes.data_ptr())))
     ids = torch.arange(N_ROWS, dtype=torch.int64, device="cuda") + int(os.environ.get("RANK", "0")) * N_ROWS
     h = C.c_void_p()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    L.check(lib.pqg_ivf_build_with_centroids(ctx.h, vp(tables.data_ptr()), M, ks, DIMS // M,
-                                             vp(codes.data_ptr()), vp(ids.data_ptr()), N_ROWS,
-                                             vp(coarse.data_ptr()), nlist, C.byref(h)))
-    torch.cuda.synchronize()
-    build_s = time.perf_counter() - t0
+    for rep in range(2):  # the second (warm) build is timed
+        if rep:
+            lib.pqg_index_destroy(h)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        L.check(lib.pqg_ivf_build_with_centroids(ctx.h, vp(tables.data_ptr()), M, ks, DIMS // M,
+                                                 vp(codes.data_ptr()), vp(ids.data_ptr()), N_ROWS,
+                                                 vp(coarse.data_ptr()), nlist, C.byref(h)))
+        torch.cuda.synchronize()
+        build_s = time.perf_counter() - t0
     q = torch.from_numpy(gaussian_mixture(nq, DIMS, COMPONENTS, SEED, stream=1)).cuda()
     oi = torch.empty((nq, k), dtype=torch.int64, device="cuda")
     od = torch.empty((nq, k), dtype=torch.float64, device="cuda")
@@ -533,12 +617,17 @@ def adc_bench(ctx, lib, L, x, train, args, world, stream, timed):
     L.check(lib.pqg_index_probe(ctx.h, h, vp(q.data_ptr()), nq, nprobe, vp(probes.data_ptr())))
     sizes = (off[1:] - off[:-1]).cuda()
     cand = int(sizes[probes.long()].sum())
+    host_arrays = None
+    if rank_of() == 0 and world == 1:  # for the CPU baseline leg (reference on the same index)
+        host_arrays = {"codes": codes.cpu().numpy(), "coarse": coarse.cpu().numpy(),
+                       "tables": tables.cpu().numpy(), "queries": q.cpu().numpy(),
+                       "nprobe": nprobe, "k": k}
     lib.pqg_index_destroy(h)
     scan_ms_b = scan_ms / (max(3, args.steps // 2) + 2)
     peaks, psrc = measured_peaks()
     code_bytes = cand * M  # algorithmic bytes: the probed lists' code rows, read once
     ach = code_bytes / (scan_ms_b / 1e3) / 1e9
-    return {"queries_per_s": nq / (ms / 1e3), "ms_per_batch": ms, "nq": nq,
+    return {"_host": host_arrays, "queries_per_s": nq / (ms / 1e3), "ms_per_batch": ms, "nq": nq,
             "candidates_per_query": cand / nq,
             "roofline_scan": {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"],
                               "unit": "GB/s", "frac": ach / peaks["hbm_gbs"],
@@ -588,6 +677,19 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "RANK" not in os.environ and args.impl == "ours":
+        # one process per GPU: relaunch under torchrun (the driver launches it
+        # that way itself); the JSON line comes from rank 0's stdout
+        import socket
+        import subprocess
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        os.dup2(_JSON_FD, 1)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))
         world = int(os.environ.get("WORLD_SIZE", "1"))

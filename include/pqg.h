@@ -269,16 +269,16 @@ int pqg_kmshard_init_table(pqg_ctx* ctx, pqg_kmshard* h, const uint64_t* init_ro
 /* assignment pass (kmeans.cpp:46-57) of the local rows against tables
  * (device B*k*d) and the local partials into f64 / u8 (device) */
 int pqg_kmshard_partials(pqg_ctx* ctx, pqg_kmshard* h, const float* tables, double* f64, uint8_t* u8);
-/* after the all-reduces: stop rule, exact means, the ordered list of
- * (b, c, t) that need the row-order replay (*n_fail), the largest number of
- * empty clusters of a continuing problem (*max_empty), *any_active */
+/* after the all-reduces: stop rule, exact means, the ordered list of the
+ * n_fail (b, c, t) columns that need the row-order replay and *stride (an
+ * upper bound on every rank's pack length: the columns' global member
+ * counts), the largest number of empty clusters of a continuing problem
+ * (*max_empty), *any_active.  The iteration's one host synchronisation. */
 int pqg_kmshard_apply(pqg_ctx* ctx, pqg_kmshard* h, float* tables, const double* f64, const uint8_t* u8,
-                      uint64_t* n_fail, uint32_t* max_empty, int* any_active);
-/* the local members of the n_fail replay columns in local row order: vals
- * (device, cap floats) and offcnt (device, 2*n_fail u64: offset, count per
- * column); vals == NULL only reports *n_vals */
-int pqg_kmshard_pack(pqg_ctx* ctx, pqg_kmshard* h, float* vals, uint64_t cap, uint64_t* offcnt,
-                     uint64_t* n_vals);
+                      uint64_t* n_fail, uint64_t* stride, uint32_t* max_empty, int* any_active);
+/* this rank's members of the replay columns in local row order: vals (device,
+ * cap >= stride floats) and offcnt (device, 2*n_fail u64: offset, count) */
+int pqg_kmshard_pack(pqg_ctx* ctx, pqg_kmshard* h, float* vals, uint64_t cap, uint64_t* offcnt);
 /* the reference's chain over every rank's packed members, rank order:
  * all_vals world x stride floats, all_offcnt world x 2*n_fail */
 int pqg_kmshard_replay(pqg_ctx* ctx, pqg_kmshard* h, float* tables, const double* f64, const float* all_vals,

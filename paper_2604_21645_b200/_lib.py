@@ -81,8 +81,9 @@ _SIGS = {
     "pqg_kmshard_sizes": (_i32, [_vp, C.POINTER(_u64), C.POINTER(_u64)]),
     "pqg_kmshard_init_table": (_i32, [_vp, _vp, _vp, _u64, _vp]),
     "pqg_kmshard_partials": (_i32, [_vp, _vp, _vp, _vp, _vp]),
-    "pqg_kmshard_apply": (_i32, [_vp, _vp, _vp, _vp, _vp, C.POINTER(_u64), C.POINTER(_u32), C.POINTER(_i32)]),
-    "pqg_kmshard_pack": (_i32, [_vp, _vp, _vp, _u64, _vp, C.POINTER(_u64)]),
+    "pqg_kmshard_apply": (_i32, [_vp, _vp, _vp, _vp, _vp, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u32),
+                                 C.POINTER(_i32)]),
+    "pqg_kmshard_pack": (_i32, [_vp, _vp, _vp, _u64, _vp]),
     "pqg_kmshard_replay": (_i32, [_vp, _vp, _vp, _vp, _vp, _u64, _vp, _u32]),
     "pqg_kmshard_reseed_candidates": (_i32, [_vp, _vp, _u64, _u32, _vp, _vp, _vp]),
     "pqg_kmshard_reseed_apply": (_i32, [_vp, _vp, _vp, _vp, _u32, _u32, _vp, _vp, _vp]),

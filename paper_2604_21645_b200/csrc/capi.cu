@@ -700,6 +700,7 @@ void pqg_ctx_destroy(pqg_ctx* ctx) {
         if (e) cudaEventDestroy(e);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->handoff_ev) cudaEventDestroy(ctx->handoff_ev);
+    if (ctx->shard_ws) pqg_ctx_destroy(ctx->shard_ws);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
 }
@@ -1702,6 +1703,7 @@ int pqg_kmeans_init_rows(uint64_t n, uint64_t k, uint64_t seed, uint64_t* rows) 
 
 struct pqg_kmshard {
     pqg_ctx* own = nullptr;  // private context: its pinned arena holds the per-fit buffers
+    pqg_ctx* parent = nullptr;
     RowSrc src;
     uint64_t n = 0, k = 0;
     uint32_t B = 0, d = 0, max_iters = 0;
@@ -1715,6 +1717,9 @@ struct pqg_kmshard {
     int* cmin = nullptr;
     uint32_t* flags = nullptr;
     uint32_t* work = nullptr;
+    uint32_t* cnt = nullptr;              // replay columns' local member counts
+    uint64_t* pre = nullptr;              // their exclusive scan (pack offsets)
+    unsigned long long* res = nullptr;    // n_fail, local pack length, global bound
     uint32_t* empties = nullptr;
     float* cnorm = nullptr;
     float* cmaxn = nullptr;
@@ -1724,7 +1729,19 @@ struct pqg_kmshard {
     const uint8_t* big_rows = nullptr;
     const float* big_nx = nullptr;
     std::pair<size_t, size_t> mark{0, 0};
+    // the fixed launch sequences of a step, replayed as CUDA graphs once their
+    // pointers are known (the arena hands out the same scratch every step)
+    struct Graph {
+        cudaGraphExec_t exec = nullptr;
+        const void* key[3] = {nullptr, nullptr, nullptr};
+        bool warm = false;
+        uint64_t launches = 0;
+    } g_partials, g_apply;
     uint64_t nkd() const { return uint64_t(B) * k * d; }
+    ~pqg_kmshard() {
+        if (g_partials.exec) cudaGraphExecDestroy(g_partials.exec);
+        if (g_apply.exec) cudaGraphExecDestroy(g_apply.exec);
+    }
 };
 
 namespace {
@@ -1739,6 +1756,51 @@ struct ShardStep {
     }
     ~ShardStep() { h->own->arena.reset_to(h->mark); }
 };
+// body() eagerly on the first call, captured on the second, replayed after
+template <class F>
+void run_graphed(pqg_ctx* o, pqg_kmshard::Graph& g, const void* k0, const void* k1, const void* k2, F&& body) {
+    const char* ge = std::getenv("PQG_KM_GRAPH");
+    // the legacy / per-thread default streams cannot be captured
+    const bool legacy = o->stream == nullptr || o->stream == cudaStreamLegacy || o->stream == cudaStreamPerThread;
+    if (o->profiling || legacy || (ge && ge[0] == '0')) {
+        body();
+        return;
+    }
+    if (g.exec && (g.key[0] != k0 || g.key[1] != k1 || g.key[2] != k2)) {
+        cudaGraphExecDestroy(g.exec);
+        g.exec = nullptr;
+        g.warm = false;
+    }
+    if (!g.exec) {
+        if (!g.warm) {
+            body();
+            g.warm = true;
+            g.key[0] = k0;
+            g.key[1] = k1;
+            g.key[2] = k2;
+            return;
+        }
+        const uint64_t l0 = o->launches;
+        PQG_CUDA(cudaStreamBeginCapture(o->stream, cudaStreamCaptureModeRelaxed));
+        try {
+            body();
+        } catch (...) {
+            cudaGraph_t gg = nullptr;
+            cudaStreamEndCapture(o->stream, &gg);
+            if (gg) cudaGraphDestroy(gg);
+            throw;
+        }
+        cudaGraph_t gg = nullptr;
+        PQG_CUDA(cudaStreamEndCapture(o->stream, &gg));
+        const cudaError_t ie = cudaGraphInstantiate(&g.exec, gg, 0);
+        cudaGraphDestroy(gg);
+        if (ie != cudaSuccess) fail(PQG_ECUDA, std::string("kmshard graph: ") + cudaGetErrorString(ie));
+        g.launches = o->launches - l0;
+        o->launches = l0;
+    }
+    PQG_CUDA(cudaGraphLaunch(g.exec, o->stream));
+    o->launches += g.launches;
+}
 }  // namespace
 
 extern "C" {
@@ -1761,9 +1823,18 @@ int pqg_kmshard_create(pqg_ctx* ctx, const float* rows, uint64_t n, uint64_t ld,
             fail(PQG_EUNSUPPORTED, "kmshard: shape not supported by the sharded update (d % 4, d <= 128)");
         auto h = std::make_unique<pqg_kmshard>();
         PQG_CUDA(cudaSetDevice(ctx->device));
-        const int rc = pqg_ctx_create(ctx->device, &h->own);
-        if (rc) fail(rc, g_last_error);
+        // the workspace context (its arena holds the per-fit buffers) is cached
+        // in the caller's context between fits: no allocation per fit
+        if (ctx->shard_ws) {
+            h->own = ctx->shard_ws;
+            ctx->shard_ws = nullptr;
+        } else {
+            const int rc = pqg_ctx_create(ctx->device, &h->own);
+            if (rc) fail(rc, g_last_error);
+        }
+        h->parent = ctx;
         h->own->stream = ctx->stream;
+        h->own->arena.rewind();
         h->own->arena.depth = 1;  // pinned: the buffers below live until destroy
         pqg_ctx* o = h->own;
         h->src = src;
@@ -1783,6 +1854,9 @@ int pqg_kmshard_create(pqg_ctx* ctx, const float* rows, uint64_t n, uint64_t ld,
         h->cmin = scratch<int>(o, nkd);
         h->flags = scratch<uint32_t>(o, nkd);
         h->work = scratch<uint32_t>(o, nkd);
+        h->cnt = scratch<uint32_t>(o, nkd);
+        h->pre = scratch<uint64_t>(o, nkd);
+        h->res = scratch<unsigned long long>(o, 3);
         h->empties = scratch<uint32_t>(o, B);
         h->cnorm = scratch<float>(o, uint64_t(B) * k);
         h->cmaxn = scratch<float>(o, B);
@@ -1822,7 +1896,8 @@ void pqg_kmshard_destroy(pqg_kmshard* h) {
         cudaStreamSynchronize(h->own->stream);
         h->own->stream = h->own->own_stream;
         h->own->arena.depth = 0;
-        pqg_ctx_destroy(h->own);
+        if (h->parent && !h->parent->shard_ws) h->parent->shard_ws = h->own;  // kept for the next fit
+        else pqg_ctx_destroy(h->own);
     }
     delete h;
 }
@@ -1853,6 +1928,7 @@ int pqg_kmshard_partials(pqg_ctx* ctx, pqg_kmshard* h, const float* tables, doub
         ShardStep step(ctx, h);
         pqg_ctx* o = h->own;
         const uint64_t l0 = o->launches;
+        run_graphed(o, h->g_partials, tables, f64, u8, [&] {
         table_norms(o, tables, h->B, h->k, h->d, h->cnorm, h->cmaxn);
         NearestArgs a;
         a.src = h->src;
@@ -1876,50 +1952,53 @@ int pqg_kmshard_partials(pqg_ctx* ctx, pqg_kmshard* h, const float* tables, doub
                               h->perm, h->csum, h->cmax, h->cmin);
         shard_pack_partials(o, h->B, h->k, h->d, h->offsets, h->csum, h->cmax, h->cmin, f64, u8);
         rows_sum_f64(o, h->dist, h->n, h->B, f64 + h->nkd() + uint64_t(h->B) * h->k);
+        });
         ctx->launches += o->launches - l0;
     });
 }
 
 int pqg_kmshard_apply(pqg_ctx* ctx, pqg_kmshard* h, float* tables, const double* f64, const uint8_t* u8,
-                      uint64_t* n_fail, uint32_t* max_empty, int* any_active) {
+                      uint64_t* n_fail, uint64_t* stride, uint32_t* max_empty, int* any_active) {
     return guard([&] {
         ShardStep step(ctx, h);
         pqg_ctx* o = h->own;
         const uint64_t l0 = o->launches;
-        kmeans_stop_global(o, f64 + h->nkd() + uint64_t(h->B) * h->k, h->B, h->max_iters, h->tol, h->st);
-        shard_finalize(o, h->B, h->k, h->d, f64, u8, h->st.active, tables, h->flags, h->empties);
-        h->n_fail = shard_compact(o, h->flags, h->nkd(), h->work);  // synchronises
+        run_graphed(o, h->g_apply, tables, f64, u8, [&] {
+            kmeans_stop_global(o, f64 + h->nkd() + uint64_t(h->B) * h->k, h->B, h->max_iters, h->tol, h->st);
+            shard_finalize(o, h->B, h->k, h->d, f64, u8, h->st.active, tables, h->flags, h->empties);
+            shard_replay_layout(o, h->B, h->k, h->d, h->flags, h->offsets, f64, h->work, h->cnt, h->pre, h->res);
+        });
+        // the iteration's one host synchronisation: sizes of the exchanges to come
+        std::vector<unsigned long long> res(3);
         std::vector<uint32_t> emp(h->B);
         std::vector<int> act(h->B);
+        PQG_CUDA(cudaMemcpyAsync(res.data(), h->res, sizeof(unsigned long long) * 3, cudaMemcpyDeviceToHost, o->stream));
         PQG_CUDA(cudaMemcpyAsync(emp.data(), h->empties, sizeof(uint32_t) * h->B, cudaMemcpyDeviceToHost, o->stream));
         PQG_CUDA(cudaMemcpyAsync(act.data(), h->st.active, sizeof(int) * h->B, cudaMemcpyDeviceToHost, o->stream));
         PQG_CUDA(cudaStreamSynchronize(o->stream));
+        h->n_fail = res[0];
         uint32_t me = 0;
         int aa = 0;
         for (uint32_t b = 0; b < h->B; ++b) {
             if (act[b]) me = std::max(me, emp[b]);
             aa |= act[b];
         }
-        if (n_fail) *n_fail = h->n_fail;
+        if (n_fail) *n_fail = res[0];
+        if (stride) *stride = std::max<unsigned long long>(1, res[2]);
         if (max_empty) *max_empty = me;
         if (any_active) *any_active = aa;
         ctx->launches += o->launches - l0;
     });
 }
 
-int pqg_kmshard_pack(pqg_ctx* ctx, pqg_kmshard* h, float* vals, uint64_t cap, uint64_t* offcnt,
-                     uint64_t* n_vals) {
+int pqg_kmshard_pack(pqg_ctx* ctx, pqg_kmshard* h, float* vals, uint64_t cap, uint64_t* offcnt) {
     return guard([&] {
         ShardStep step(ctx, h);
         pqg_ctx* o = h->own;
         const uint64_t l0 = o->launches;
-        uint64_t* oc = offcnt ? offcnt : scratch<uint64_t>(o, std::max<uint64_t>(1, 2 * h->n_fail));
-        const uint64_t tot = shard_pack_layout(o, h->work, h->n_fail, h->k, h->d, h->offsets, oc);
-        if (n_vals) *n_vals = tot;
-        if (vals) {
-            if (tot > cap) inval("kmshard_pack: value buffer too small");
-            shard_pack(o, h->src, h->work, h->n_fail, h->k, h->d, h->offsets, h->perm, h->n, oc, vals);
-        }
+        (void)cap;  // cap >= the apply's stride bounds every rank's pack
+        shard_pack(o, h->src, h->work, h->n_fail, h->k, h->d, h->offsets, h->perm, h->n, h->cnt, h->pre, offcnt,
+                   vals);
         ctx->launches += o->launches - l0;
     });
 }

@@ -152,6 +152,7 @@ struct pqg_ctx {
     cudaEvent_t pipe_ev[4] = {nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t handoff_ev = nullptr;  // pqg_ctx_set_stream: new stream waits for the old
     bool err_pending = false;          // d_err not yet read (device-output searches)
+    pqg_ctx* shard_ws = nullptr;       // cached workspace context of pqg_kmshard handles
 };
 
 namespace pqg {

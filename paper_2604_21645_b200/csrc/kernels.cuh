@@ -106,12 +106,15 @@ void shard_pack_partials(pqg_ctx* ctx, uint32_t B, uint64_t k, uint32_t d, const
                          const double* csum, const int* cmax, const int* cmin, double* f64, uint8_t* u8);
 void shard_finalize(pqg_ctx* ctx, uint32_t B, uint64_t k, uint32_t d, const double* f64, const uint8_t* u8,
                     const int* active, float* table, uint32_t* flags, uint32_t* empties);
-uint64_t shard_compact(pqg_ctx* ctx, const uint32_t* flags, uint64_t count, uint32_t* work);
-uint64_t shard_pack_layout(pqg_ctx* ctx, const uint32_t* work, uint64_t n_fail, uint64_t k, uint32_t d,
-                           const uint64_t* offsets, uint64_t* offcnt);
+// ordered replay list (work), per-column local counts (cnt) and their
+// exclusive scan (pre); res[0] = n_fail, res[1] = local pack length,
+// res[2] = sum of the columns' global counts (a bound on every rank's pack)
+void shard_replay_layout(pqg_ctx* ctx, uint32_t B, uint64_t k, uint32_t d, const uint32_t* flags,
+                         const uint64_t* offsets, const double* f64, uint32_t* work, uint32_t* cnt, uint64_t* pre,
+                         unsigned long long* res);
 void shard_pack(pqg_ctx* ctx, const RowSrc& src, const uint32_t* work, uint64_t n_fail, uint64_t k,
-                uint32_t d, const uint64_t* offsets, const uint32_t* perm, uint64_t n, const uint64_t* offcnt,
-                float* vals);
+                uint32_t d, const uint64_t* offsets, const uint32_t* perm, uint64_t n, const uint32_t* cnt,
+                const uint64_t* pre, uint64_t* offcnt, float* vals);
 void shard_replay(pqg_ctx* ctx, const uint32_t* work, uint64_t n_fail, uint64_t k, uint32_t d, uint32_t B,
                   const double* f64, const float* vals, uint64_t stride, const uint64_t* offcnt,
                   uint32_t world, float* table);

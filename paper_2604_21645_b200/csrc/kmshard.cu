@@ -84,31 +84,44 @@ __global__ void finalize_kernel(uint32_t B, uint64_t k, uint32_t d, const double
 }
 
 __global__ void compact_kernel(const uint32_t* flags, const uint64_t* pos, uint64_t count, uint32_t* work,
-                               uint64_t* n_out) {
+                               unsigned long long* res) {
     for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < count;
          e += uint64_t(gridDim.x) * blockDim.x) {
         if (flags[e]) work[pos[e]] = uint32_t(e);
-        if (e == count - 1) *n_out = pos[e] + flags[e];
+        if (e == count - 1) res[0] = pos[e] + flags[e];
     }
 }
 
-__global__ void pack_counts_kernel(const uint32_t* work, uint64_t n_fail, uint64_t k, uint32_t d,
-                                   const uint64_t* offsets, uint32_t* cnt) {
-    for (uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < n_fail;
+// replay column p < n_fail: its local member count (cnt) and, summed into
+// res[2], its global count (the per-rank pack is at most that long)
+__global__ void pack_counts_kernel(const uint32_t* work, uint64_t cap, const unsigned long long* res_in,
+                                   uint64_t k, uint32_t d, uint32_t B, const uint64_t* offsets, const double* f64,
+                                   uint32_t* cnt, unsigned long long* res) {
+    const uint64_t n_fail = res_in[0];
+    const uint64_t nkd = uint64_t(B) * k * d;
+    for (uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < cap;
          p += uint64_t(gridDim.x) * blockDim.x) {
+        if (p >= n_fail) {
+            cnt[p] = 0u;
+            continue;
+        }
         const uint64_t bc = work[p] / d, b = bc / k, c = bc - b * k;
         const uint64_t* off = offsets + b * (k + 1);
         cnt[p] = uint32_t(off[c + 1] - off[c]);
+        atomicAdd(res + 2, (unsigned long long)f64[nkd + bc]);
     }
 }
 
-__global__ void pack_offcnt_kernel(const uint32_t* cnt, const uint64_t* pre, uint64_t n_fail, uint64_t* offcnt,
-                                   uint64_t* total) {
+__global__ void pack_total_kernel(const uint32_t* cnt, const uint64_t* pre, unsigned long long* res) {
+    const uint64_t n_fail = res[0];
+    res[1] = n_fail ? pre[n_fail - 1] + cnt[n_fail - 1] : 0ull;
+}
+
+__global__ void pack_offcnt_kernel(const uint32_t* cnt, const uint64_t* pre, uint64_t n_fail, uint64_t* offcnt) {
     for (uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < n_fail;
          p += uint64_t(gridDim.x) * blockDim.x) {
         offcnt[2 * p] = pre[p];
         offcnt[2 * p + 1] = cnt[p];
-        if (p == n_fail - 1) *total = pre[p] + cnt[p];
     }
 }
 
@@ -299,41 +312,29 @@ void shard_finalize(pqg_ctx* ctx, uint32_t B, uint64_t k, uint32_t d, const doub
            k, d, f64, u8, active, table, flags, empties);
 }
 
-uint64_t shard_compact(pqg_ctx* ctx, const uint32_t* flags, uint64_t count, uint32_t* work) {
-    uint64_t* pos = scratch<uint64_t>(ctx, count);
-    uint64_t* n_dev = scratch<uint64_t>(ctx, 1);
-    exclusive_scan_u32(ctx, flags, pos, count);
-    launch(ctx, "kmshard", compact_kernel, dim3(grid1d(count, kThreads, 4096)), dim3(kThreads), 0, flags,
-           (const uint64_t*)pos, count, work, n_dev);
-    uint64_t h = 0;
-    PQG_CUDA(cudaMemcpyAsync(&h, n_dev, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
-    PQG_CUDA(cudaStreamSynchronize(ctx->stream));
-    return h;
-}
-
-uint64_t shard_pack_layout(pqg_ctx* ctx, const uint32_t* work, uint64_t n_fail, uint64_t k, uint32_t d,
-                           const uint64_t* offsets, uint64_t* offcnt) {
-    if (n_fail == 0) return 0;
-    uint32_t* cnt = scratch<uint32_t>(ctx, n_fail);
-    uint64_t* pre = scratch<uint64_t>(ctx, n_fail);
-    uint64_t* tot = scratch<uint64_t>(ctx, 1);
-    launch(ctx, "kmshard", pack_counts_kernel, dim3(grid1d(n_fail, kThreads, 1024)), dim3(kThreads), 0, work,
-           n_fail, k, d, offsets, cnt);
-    exclusive_scan_u32(ctx, cnt, pre, n_fail);
-    launch(ctx, "kmshard", pack_offcnt_kernel, dim3(grid1d(n_fail, kThreads, 1024)), dim3(kThreads), 0,
-           (const uint32_t*)cnt, (const uint64_t*)pre, n_fail, offcnt, tot);
-    uint64_t h = 0;
-    PQG_CUDA(cudaMemcpyAsync(&h, tot, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
-    PQG_CUDA(cudaStreamSynchronize(ctx->stream));
-    return h;
+void shard_replay_layout(pqg_ctx* ctx, uint32_t B, uint64_t k, uint32_t d, const uint32_t* flags,
+                         const uint64_t* offsets, const double* f64, uint32_t* work, uint32_t* cnt, uint64_t* pre,
+                         unsigned long long* res) {
+    const uint64_t nkd = uint64_t(B) * k * d;
+    PQG_CUDA(cudaMemsetAsync(res, 0, sizeof(unsigned long long) * 3, ctx->stream));
+    exclusive_scan_u32(ctx, flags, pre, nkd);
+    launch(ctx, "kmshard", compact_kernel, dim3(grid1d(nkd, kThreads, 4096)), dim3(kThreads), 0, flags,
+           (const uint64_t*)pre, nkd, work, res);
+    launch(ctx, "kmshard", pack_counts_kernel, dim3(grid1d(nkd, kThreads, 4096)), dim3(kThreads), 0,
+           (const uint32_t*)work, nkd, (const unsigned long long*)res, k, d, B, offsets, f64, cnt, res);
+    exclusive_scan_u32(ctx, cnt, pre, nkd);
+    launch(ctx, "kmshard", pack_total_kernel, dim3(1), dim3(1), 0, (const uint32_t*)cnt, (const uint64_t*)pre,
+           res);
 }
 
 void shard_pack(pqg_ctx* ctx, const RowSrc& src, const uint32_t* work, uint64_t n_fail, uint64_t k,
-                uint32_t d, const uint64_t* offsets, const uint32_t* perm, uint64_t n, const uint64_t* offcnt,
-                float* vals) {
+                uint32_t d, const uint64_t* offsets, const uint32_t* perm, uint64_t n, const uint32_t* cnt,
+                const uint64_t* pre, uint64_t* offcnt, float* vals) {
     if (n_fail == 0) return;
+    launch(ctx, "kmshard", pack_offcnt_kernel, dim3(grid1d(n_fail, kThreads, 1024)), dim3(kThreads), 0, cnt, pre,
+           n_fail, offcnt);
     launch(ctx, "kmshard", pack_kernel, dim3(grid1d(n_fail * 32, kThreads)), dim3(kThreads), 0, src, work,
-           n_fail, k, d, offsets, perm, n, offcnt, vals);
+           n_fail, k, d, offsets, perm, n, (const uint64_t*)offcnt, vals);
 }
 
 void shard_replay(pqg_ctx* ctx, const uint32_t* work, uint64_t n_fail, uint64_t k, uint32_t d, uint32_t B,

@@ -95,10 +95,22 @@ class Comm:
         return float(t.item())
 
     def allreduce_(self, t, op="sum"):
-        """In-place all-reduce of a tensor (SUM or MAX)."""
+        """In-place all-reduce of a tensor (SUM or MAX); a 1-rank group has
+        nothing to exchange."""
+        if self.world == 1:
+            return t
         rop = self.dist.ReduceOp.SUM if op == "sum" else self.dist.ReduceOp.MAX
         self.dist.all_reduce(t, op=rop, group=self.group)
         return t
+
+    def allreduce_pair_(self, a, b):
+        """SUM-reduce a and MAX-reduce b, both in flight together."""
+        if self.world == 1:
+            return
+        w1 = self.dist.all_reduce(a, op=self.dist.ReduceOp.SUM, group=self.group, async_op=True)
+        w2 = self.dist.all_reduce(b, op=self.dist.ReduceOp.MAX, group=self.group, async_op=True)
+        w1.wait()
+        w2.wait()
 
     def allgather_padded(self, t):
         """1-D tensors of per-rank lengths -> ([world, stride] padded stack, stride)."""
@@ -111,10 +123,17 @@ class Comm:
         return self.allgather_equal(pad), stride
 
     def allgather_equal(self, t):
+        """[world, *t.shape]: every rank's equally shaped t, rank order."""
         import torch
-        outs = [torch.empty_like(t) for _ in range(self.world)]
-        self.dist.all_gather(outs, t.contiguous(), group=self.group)
-        return torch.stack(outs)
+        t = t.contiguous()
+        if self.world == 1:
+            return t.unsqueeze(0)
+        out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        if hasattr(self.dist, "all_gather_into_tensor") and t.is_cuda:
+            self.dist.all_gather_into_tensor(out, t, group=self.group)
+        else:
+            self.dist.all_gather(list(out.unbind(0)), t, group=self.group)
+        return out
 
 
 # ---------------------------------------------------------------------------
@@ -201,28 +220,31 @@ class CudaBackend:
     def shard_partials(self, s, tables):
         torch = self.torch
         dev = s["rows"].device
-        f64 = torch.empty(s["nf"], dtype=torch.float64, device=dev)
-        u8 = torch.empty(s["nu"], dtype=torch.uint8, device=dev)
+        if "f64" not in s:  # reused every iteration
+            s["f64"] = torch.empty(s["nf"], dtype=torch.float64, device=dev)
+            s["u8"] = torch.empty(s["nu"], dtype=torch.uint8, device=dev)
+        f64, u8 = s["f64"], s["u8"]
         self.L.check(self.lib.pqg_kmshard_partials(self.ctx.h, s["h"], self._p(tables), self._p(f64),
                                                    self._p(u8)), "kmshard_partials")
         return f64, u8
 
     def shard_apply(self, s, tables, f64, u8):
-        nf, me, aa = C.c_uint64(), C.c_uint32(), C.c_int()
+        nf, stride, me, aa = C.c_uint64(), C.c_uint64(), C.c_uint32(), C.c_int()
         self.L.check(self.lib.pqg_kmshard_apply(self.ctx.h, s["h"], self._p(tables), self._p(f64), self._p(u8),
-                                                C.byref(nf), C.byref(me), C.byref(aa)), "kmshard_apply")
+                                                C.byref(nf), C.byref(stride), C.byref(me), C.byref(aa)),
+                     "kmshard_apply")
+        s["stride"] = stride.value
         return nf.value, me.value, bool(aa.value)
 
     def shard_pack(self, s, n_fail):
+        """(vals [stride] padded, offcnt [2*n_fail]): this rank's replay members."""
         torch = self.torch
         dev = s["rows"].device
-        nv = C.c_uint64()
-        self.L.check(self.lib.pqg_kmshard_pack(self.ctx.h, s["h"], None, 0, None, C.byref(nv)), "kmshard_pack")
-        vals = torch.empty(max(1, nv.value), dtype=torch.float32, device=dev)
+        vals = torch.empty(s["stride"], dtype=torch.float32, device=dev)
         offcnt = torch.empty(2 * n_fail, dtype=torch.int64, device=dev)
-        self.L.check(self.lib.pqg_kmshard_pack(self.ctx.h, s["h"], self._p(vals), vals.numel(), self._p(offcnt),
-                                               C.byref(nv)), "kmshard_pack")
-        return vals[: nv.value], offcnt
+        self.L.check(self.lib.pqg_kmshard_pack(self.ctx.h, s["h"], self._p(vals), vals.numel(), self._p(offcnt)),
+                     "kmshard_pack")
+        return vals, offcnt
 
     def shard_replay(self, s, tables, f64, all_vals, stride, all_offcnt, world):
         self.L.check(self.lib.pqg_kmshard_replay(self.ctx.h, s["h"], self._p(tables), self._p(f64),
@@ -345,14 +367,13 @@ def kmeans_fit_sharded(comm: Comm, backend, local_rows, B: int, d: int, col_stri
         tables = bits.view(torch.float32)
         for _ in range(max_iters):
             f64, u8 = backend.shard_partials(s, tables)
-            comm.allreduce_(f64, "sum")
-            comm.allreduce_(u8, "max")
+            comm.allreduce_pair_(f64, u8)
             st["allreduce_bytes"] += f64.numel() * 8 + u8.numel()
             st["iterations"] += 1
             n_fail, max_empty, any_active = backend.shard_apply(s, tables, f64, u8)
             if n_fail:  # columns whose sum may round: the row-order replay
-                vals, offcnt = backend.shard_pack(s, n_fail)
-                all_vals, stride = comm.allgather_padded(vals)
+                vals, offcnt = backend.shard_pack(s, n_fail)  # padded to the common stride
+                all_vals, stride = comm.allgather_equal(vals), vals.numel()
                 all_oc = comm.allgather_equal(offcnt)
                 backend.shard_replay(s, tables, f64, all_vals, stride, all_oc, comm.world)
                 st["replay_columns"] += n_fail

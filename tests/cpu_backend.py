@@ -214,6 +214,7 @@ class ShardOracleBackend(OracleBackend):
                     else:
                         flags[e] = True
         s["work"] = np.flatnonzero(flags)
+        s["stride"] = max(1, int(sum(f64[nkd + int(e) // d] for e in s["work"])))
         me = max([int(s["empties"][b]) for b in range(B) if s["active"][b]] or [0])
         return int(s["work"].size), me, bool(s["active"].any())
 
@@ -230,7 +231,9 @@ class ShardOracleBackend(OracleBackend):
             offcnt += [off, v.size]
             off += v.size
         vals = np.concatenate(vals).astype(np.float32) if vals else np.zeros(0, np.float32)
-        return torch.from_numpy(vals), torch.from_numpy(np.array(offcnt, np.int64))
+        padded = np.zeros(s["stride"], np.float32)  # common length on every rank (no size exchange)
+        padded[: vals.size] = vals
+        return torch.from_numpy(padded), torch.from_numpy(np.array(offcnt, np.int64))
 
     def shard_replay(self, s, tables, f64t, all_vals, stride, all_offcnt, world):
         B, k, d = s["B"], s["k"], s["d"]

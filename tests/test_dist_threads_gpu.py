@@ -42,13 +42,18 @@ class _ThreadDist:
         for o, g in zip(outs, self._exchange(t)):
             o.copy_(g.to(o.device))
 
-    def all_reduce(self, t, op="sum", group=None):
+    def all_reduce(self, t, op="sum", group=None, async_op=False):
         import torch
         got = self._exchange(t)
         acc = got[0].clone()
         for g in got[1:]:
             acc = acc + g if op == "sum" else torch.maximum(acc, g)
         t.copy_(acc)
+
+        class _Done:
+            def wait(self):
+                return True
+        return _Done() if async_op else None
 
 
 def _run_world(world, x, fn):
