@@ -24,6 +24,7 @@
 #include <cfloat>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include <cstdio>
 
@@ -604,6 +605,209 @@ __global__ void __launch_bounds__(kSmallThreads) small_table_kernel(NearestArgs 
     }
 }
 
+// Narrow codebooks, register-resident (Ks <= 64, Ds in {4, 8, 16, 32}): the
+// codebook lives in REGISTERS, split over lanes.  Lane l owns one (subspace
+// s, part g) task -- codewords g*KS/G .. (g+1)*KS/G - 1 of subspace s, at most
+// 128 floats -- for the whole kernel, so the inner loop reads no memory at
+// all: per codeword Ds FMAs on the row's register-resident sub-vector and a
+// running top-2.  A row's M*G tasks are LG consecutive lanes (LG <= 32: a warp
+// covers 32/LG rows per step; LG = 64: two warps share each row), so the
+// x loads of a warp step are whole consecutive rows, fully coalesced; the G
+// lanes of a (row, subspace) merge their top-2 with shuffles and the group's
+// first lane writes the code (consecutive subspaces -> consecutive bytes).
+// Screened value, bound and fixup hand-off are small_table_kernel's.
+constexpr int kNarrowThreads = 256;
+template <int DS, int KS, int G>
+__global__ void __launch_bounds__(kNarrowThreads, (DS <= 4 && KS <= 16) ? 2 : 1) narrow_kernel(NearestArgs a, uint32_t LG, uint32_t RPC,
+                                                                uint32_t WR) {
+    constexpr int KL = KS / G;  // codewords per lane
+    constexpr float kE = 2.f * float(DS + 4) * kU;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t gw = uint64_t(blockIdx.x) * (kNarrowThreads / 32) + (threadIdx.x >> 5);
+    const uint64_t nwarps = uint64_t(gridDim.x) * (kNarrowThreads / 32);
+    uint32_t task, rsub;
+    if (WR == 1) {
+        rsub = lane / LG;
+        task = lane - rsub * LG;
+    } else {
+        rsub = 0;
+        task = uint32_t(gw % WR) * 32 + lane;
+    }
+    const bool lane_on = WR == 1 ? rsub < RPC : task < LG;
+    const uint32_t s = lane_on ? task / G : 0, g = task % G;
+    const bool sub_on = lane_on && !(a.active && !a.active[s]);
+    float cb[KL][DS];
+    float cn[KL];
+#pragma unroll
+    for (int jj = 0; jj < KL; ++jj) {
+        const uint32_t j = g * KL + jj;
+        const bool ok = sub_on && j < a.k;
+        cn[jj] = ok ? __ldg(a.cnorm + uint64_t(s) * a.k + j) : __int_as_float(0x7f800000);
+#pragma unroll
+        for (int t = 0; t < DS; t += 4) {
+            const float4 v = ok ? __ldg(reinterpret_cast<const float4*>(a.table + (uint64_t(s) * a.k + j) * DS) + t / 4)
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+            cb[jj][t] = v.x; cb[jj][t + 1] = v.y; cb[jj][t + 2] = v.z; cb[jj][t + 3] = v.w;
+        }
+    }
+    const float cm = sub_on ? a.cmax[s] : 0.f;
+    const float cm2 = cm * cm;
+    const uint32_t step0 = uint32_t(WR == 1 ? gw : gw / WR);
+    const uint32_t steps = uint32_t(WR == 1 ? nwarps : nwarps / WR);
+    const uint32_t n = uint32_t(a.n);  // < 2^31 (narrow_variant)
+    const uint32_t rstep = steps * RPC;  // rows between a lane's consecutive steps
+    const uint64_t ld4 = a.src.ldx / 4;
+    const uint64_t dptr = uint64_t(rstep) * ld4;
+    // P steps of sub-vectors in flight per lane (a register ring), loads
+    // addressed by a running pointer
+    constexpr int P = DS <= 4 ? 4 : 2;
+    float4 xr[P][DS / 4];
+    uint32_t rr = step0 * RPC + rsub;  // the row of ring slot 0
+    const float4* xp = reinterpret_cast<const float4*>(a.src.x + uint64_t(s) * a.src.col_stride) + uint64_t(rr) * ld4;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        if (sub_on && rr + uint32_t(p) * rstep < n) {
+#pragma unroll
+            for (int t = 0; t < DS / 4; ++t) xr[p][t] = __ldg(xp + uint64_t(p) * dptr + t);
+        }
+    }
+    for (; rr - rsub < n; rr += uint32_t(P) * rstep, xp += uint64_t(P) * dptr) {
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const uint32_t crow = rr + uint32_t(p) * rstep;
+            if (crow - rsub >= n) break;  // warp-uniform
+            const bool cur = sub_on && crow < n;
+            float x[DS];
+#pragma unroll
+            for (int t = 0; t < DS / 4; ++t) {
+                x[4 * t] = -2.f * xr[p][t].x; x[4 * t + 1] = -2.f * xr[p][t].y;
+                x[4 * t + 2] = -2.f * xr[p][t].z; x[4 * t + 3] = -2.f * xr[p][t].w;
+            }
+            if (sub_on && crow + uint32_t(P) * rstep < n) {  // refill the slot P steps ahead
+#pragma unroll
+                for (int t = 0; t < DS / 4; ++t) xr[p][t] = __ldg(xp + uint64_t(p + P) * dptr + t);
+            }
+            float s2 = 0.f;
+#pragma unroll
+            for (int t = 0; t < DS; ++t) s2 = fmaf(x[t], x[t], s2);
+            const float nx = 0.25f * s2;
+            // E = kE q^2 with q = ||x|| + max||c||, bounded without the root:
+            // q^2 <= 2 (||x||^2 + max||c||^2) (the 1e-6 guards nx's rounding)
+            const float E = kE * 2.f * (nx * (1.f + 1e-6f) + cm2) + 1e-30f;
+            const float C = nx * (1.f + 2.f * float(DS + 2) * kU) + 2.f * E;
+            // keys: the (non-negative) screened value's bits with the global
+            // codeword index in the low log2(KS) bits -- the running top-2 is
+            // three integer min/max per codeword, ties resolve to the lower
+            // index, and truncating those bits moves a value by < KS ulps
+            // (added to the margin below)
+            constexpr uint32_t kMask = uint32_t(KS) - 1u;
+            // NS independent top-2 states (codewords jj = ns mod NS), merged
+            // after: the min/max chains of the codewords overlap
+            constexpr int NS = KL >= 4 ? 4 : KL;
+            uint32_t t1[NS], t2[NS];
+#pragma unroll
+            for (int u = 0; u < NS; ++u) t1[u] = t2[u] = 0xFFFFFFFFu;
+#pragma unroll
+            for (int jj = 0; jj < KL; ++jj) {
+                float acc = cn[jj] + C;
+#pragma unroll
+                for (int t = 0; t < DS; ++t) acc = fmaf(x[t], cb[jj][t], acc);
+                const uint32_t key = (__float_as_uint(acc) & ~kMask) | (g * KL + jj);
+                t2[jj % NS] = min(t2[jj % NS], max(t1[jj % NS], key));
+                t1[jj % NS] = min(t1[jj % NS], key);
+            }
+            uint32_t k1 = t1[0], k2 = t2[0];
+#pragma unroll
+            for (int u = 1; u < NS; ++u) {
+                k2 = min(min(k2, t2[u]), max(k1, t1[u]));
+                k1 = min(k1, t1[u]);
+            }
+#pragma unroll
+            for (int o = 1; o < G; o <<= 1) {  // merge the G parts of this (row, subspace)
+                const uint32_t o1 = __shfl_xor_sync(0xffffffffu, k1, o);
+                const uint32_t o2 = __shfl_xor_sync(0xffffffffu, k2, o);
+                k2 = min(min(k2, o2), max(k1, o1));
+                k1 = min(k1, o1);
+            }
+            const uint32_t i1 = k1 & kMask;
+            const float b1 = __uint_as_float(k1 & ~kMask), b2 = __uint_as_float(k2 & ~kMask);
+            if (!cur || g != 0) continue;
+            // b1's true value is below b1 + KS ulp(b1) <= b1 * (1 + KS 2^-23)
+            const bool unique = isfinite(E) && b1 < __int_as_float(0x7f800000) && k1 != 0xFFFFFFFFu &&
+                                (!(b2 < __int_as_float(0x7f800000)) ||
+                                 b2 - b1 > 2.05f * E + b1 * (float(KS) * 2.3841858e-07f));
+            if (unique) {
+                if (a.idx_bytes == 1 && a.idx_ps == 1)
+                    static_cast<uint8_t*>(a.out_idx)[uint64_t(crow) * a.idx_rs + s] = uint8_t(i1);
+                else
+                    store_index(a, crow, s, i1);
+                if (a.out_dist) {  // -0.5 * (-2x) == x exactly
+                    const float* c = a.table + (uint64_t(s) * a.k + i1) * DS;
+                    double accd = 0.0;
+#pragma unroll
+                    for (int t = 0; t < DS; ++t) {
+                        const double diff = __dsub_rn((double)(-0.5f * x[t]), (double)__ldg(c + t));
+                        accd = __dadd_rn(accd, __dmul_rn(diff, diff));
+                    }
+                    a.out_dist[uint64_t(s) * a.n + crow] = accd;
+                }
+            } else {
+                const unsigned long long slot = atomicAdd(a.flag_count, 1ull);
+                a.flags[slot] = (uint64_t(s) << 40) | crow;
+            }
+        }
+    }
+}
+
+template <int DS, int KS>
+void launch_narrow(pqg_ctx* ctx, const NearestArgs& a) {
+    constexpr int G = (KS * DS / 128) > 1 ? KS * DS / 128 : 1;
+    const uint32_t LG = a.B * G;
+    uint32_t RPC = 1, WR = 1;
+    if (LG <= 32) RPC = 32 / LG;
+    else WR = (LG + 31) / 32;
+    const uint64_t units = (a.n + RPC - 1) / RPC * WR;  // warp steps
+    const uint64_t blocks = std::min<uint64_t>((units + 7) / 8, uint64_t(ctx->num_sms) * 16);
+    launch(ctx, "nearest_narrow", narrow_kernel<DS, KS, G>, dim3(unsigned(std::max<uint64_t>(1, blocks))),
+           dim3(kNarrowThreads), 0, a, LG, RPC, WR);
+}
+
+// Which narrow instance applies (0: none).  LG > 32 needs WR | 8 (warps per CTA).
+int narrow_variant(const NearestArgs& a) {
+    const char* e = std::getenv("PQG_NARROW");
+    if (e && e[0] == '0') return 0;
+    if (a.src.codes || a.sse_part || a.out_mat) return 0;
+    if (((a.src.ldx | a.src.col_stride) & 3u) != 0 || (reinterpret_cast<uintptr_t>(a.src.x) & 15u) != 0 ||
+        (reinterpret_cast<uintptr_t>(a.table) & 15u) != 0)
+        return 0;
+    if (!(a.d == 4 || a.d == 8 || a.d == 16 || a.d == 32)) return 0;
+    if (a.n >= (uint64_t(1) << 31)) return 0;
+    const int KS = a.k <= 16 ? 16 : (a.k <= 32 ? 32 : (a.k <= 64 ? 64 : 0));
+    if (!KS) return 0;
+    const int G = std::max(1, KS * int(a.d) / 128);
+    const uint64_t LG = uint64_t(a.B) * G;
+    if (LG > 32 && (LG > 256 || 8 % ((LG + 31) / 32) != 0)) return 0;
+    // measured r2 (1M x 128 encodes, tools/encode_bench.py): the register-
+    // resident kernel wins at Ks <= 16 with Ds <= 8 (M=32: 1.95 -> 2.98,
+    // M=16: 2.64 -> 3.03 G vectors/s); the tcgen05 / small-table screens
+    // stay ahead at Ds >= 16 and at Ks = 64.  PQG_NARROW=1 forces it.
+    if (!(e && e[0] == '1') && (KS > 16 || a.d > 8)) return 0;
+    return KS;
+}
+
+void narrow(pqg_ctx* ctx, const NearestArgs& a, int KS) {
+    auto go = [&](auto ds_tag) {
+        constexpr int DS = decltype(ds_tag)::value;
+        if (KS == 16) launch_narrow<DS, 16>(ctx, a);
+        else if (KS == 32) launch_narrow<DS, 32>(ctx, a);
+        else launch_narrow<DS, 64>(ctx, a);
+    };
+    if (a.d == 4) go(std::integral_constant<int, 4>());
+    else if (a.d == 8) go(std::integral_constant<int, 8>());
+    else if (a.d == 16) go(std::integral_constant<int, 16>());
+    else go(std::integral_constant<int, 32>());
+}
+
 __global__ void __launch_bounds__(256, 1) norms_kernel(const float* table, uint32_t B, uint64_t k, uint32_t d,
                              float* cnorm, unsigned* cmax_bits) {
     const uint64_t total = uint64_t(B) * k;
@@ -693,7 +897,10 @@ void nearest(pqg_ctx* ctx, NearestArgs a) {
                            (reinterpret_cast<uintptr_t>(a.src.x) & 15u) == 0 &&
                            (reinterpret_cast<uintptr_t>(a.table) & 15u) == 0 &&
                            uint64_t(a.B) * a.k * (a.d + 1) * sizeof(float) <= 96 * 1024;
-    if (small_tab) {
+    const int narrow_ks = force_fp32 || (mode && std::strcmp(mode, "tc") == 0) ? 0 : narrow_variant(a);
+    if (narrow_ks) {
+        narrow(ctx, a, narrow_ks);
+    } else if (small_tab) {
         const size_t smem = size_t(a.B) * a.k * (a.d + 1) * sizeof(float);
         const unsigned grid = unsigned(std::min<uint64_t>((a.n + kSmallThreads - 1) / kSmallThreads,
                                                           uint64_t(ctx->num_sms) * 8));

@@ -775,3 +775,29 @@ def test_torch_inputs_ordered_on_torch_stream(pq, orc, mix):
             xd.copy_(torch.from_numpy(x).cuda(non_blocking=True))
             codes = pq.pq_encode(cb, xd)
             assert np.array_equal(codes.bytes, ref_codes)
+
+
+# ---------------------------------------------------------------------------
+# the register-resident narrow-codebook screen (nearest.cu narrow_kernel),
+# forced on for every shape it accepts: encode and k-means fits (which also
+# use its fp64 winner distances) bit-exact against the oracle
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("D,M,ks", [(128, 32, 16), (128, 16, 16), (128, 8, 16), (128, 4, 16), (96, 12, 16),
+                                    (128, 32, 64), (128, 16, 64), (64, 8, 64), (64, 16, 12), (32, 8, 5),
+                                    (128, 32, 32), (96, 24, 16)])
+def test_narrow_screen_parity(pq, orc, mix, monkeypatch, D, M, ks):
+    monkeypatch.setenv("PQG_NARROW", "1")
+    x = mix(6000, D, 24, seed=D + M + ks)
+    st = {}
+    cb = pq.pq_fit(x, M, ks, 6, 3, stats=st)
+    ref_t, ref_it, _ = orc.pq_fit(x, M, ks, 6, 3)
+    assert np.array_equal(bits(cb.tables), bits(ref_t))
+    assert np.array_equal(st["iterations_run"], ref_it)
+    big = mix(40000, D, 24, seed=7)
+    assert np.array_equal(pq.pq_encode(cb, big).bytes, orc.pq_encode_mt(big, ref_t, 8))
+    # exact ties: duplicated codewords must resolve to the lowest index
+    t2 = ref_t.copy()
+    t2[:, ks - ks // 2:] = t2[:, : ks // 2]
+    cb2 = pq.Codebook(M, ks, D // M, np.ascontiguousarray(t2))
+    assert np.array_equal(pq.pq_encode(cb2, big[:5000]).bytes, orc.pq_encode(big[:5000], t2))
