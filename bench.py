@@ -339,12 +339,17 @@ def run_ours(args, rank, world, local):
                                      DIMS // M, vp(tables.data_ptr()), C.byref(sse)), "sse")
         return (sse.value / (N_ROWS * DIMS)) ** 0.5
 
-    def timed(fn, steps, warmup):
+    def timed(fn, steps, warmup, region=None):
         for _ in range(warmup):
             fn()
         torch.cuda.synchronize()
         barrier(world)
         torch.cuda.synchronize()
+        # --profile-region NAME: only this timed region is visible to a
+        # profiler started with `ncu --profile-from-start off`
+        prof = region is not None and region == args.profile_region
+        if prof:
+            torch.cuda.cudart().cudaProfilerStart()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
@@ -352,15 +357,21 @@ def run_ours(args, rank, world, local):
             fn()
         b.record(stream)
         torch.cuda.synchronize()
+        if prof:
+            torch.cuda.cudart().cudaProfilerStop()
         barrier(world)
         return max_over_ranks(a.elapsed_time(b) / steps, world)
 
     # ---- k-means fit at the headline point (iters/s)
     fit(HEAD_M, HEAD_KS)  # warm-up (also JIT of module-level state)
     torch.cuda.synchronize()
+    if args.profile_region == "fit":
+        torch.cuda.cudart().cudaProfilerStart()
     t0 = time.perf_counter()
     tables, iters_run = fit(HEAD_M, HEAD_KS)
     torch.cuda.synchronize()
+    if args.profile_region == "fit":
+        torch.cuda.cudart().cudaProfilerStop()
     fit_s = max_over_ranks(time.perf_counter() - t0, world)
     kmeans_ips = iters_run / fit_s
 
@@ -400,7 +411,7 @@ def run_ours(args, rank, world, local):
     l0 = ctx.launches
     with ClockSampler(local) as clk:
         ctx.profile(True)
-        ms = timed(lambda: encode(tables, HEAD_M, HEAD_KS, codes), args.steps, args.warmup)
+        ms = timed(lambda: encode(tables, HEAD_M, HEAD_KS, codes), args.steps, args.warmup, "encode")
         n_near, near_ms = ctx.profile_read("nearest_tc")
         screen_kernel = "umma_screen (tcgen05 3xTF32, TMEM accumulator)"
         if n_near == 0:
@@ -603,7 +614,7 @@ def adc_bench(ctx, lib, L, x, train, args, world, stream, timed):
                                        world, nq, k, vp(mi.data_ptr()), vp(md.data_ptr()), vp(mc.data_ptr())))
 
     ctx.profile(True)
-    ms = timed(search, max(3, args.steps // 2), 2)
+    ms = timed(search, max(3, args.steps // 2), 2, "adc")
     n_scan, scan_ms = ctx.profile_read("adc_scan")
     n_sel, sel_ms = ctx.profile_read("probe_select")
     n_mat, mat_ms = ctx.profile_read("distance_matrix")
@@ -675,6 +686,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--quick", action="store_true", help="headline only (no sweep / ADC)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--profile-region", default=None, choices=[None, "encode", "adc", "fit"],
+                    help="bracket this timed region with cudaProfilerStart/Stop (ncu --profile-from-start off)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.gpus > 1 and "RANK" not in os.environ and args.impl == "ours":
