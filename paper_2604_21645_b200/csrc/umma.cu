@@ -106,13 +106,103 @@ __device__ __forceinline__ float tf32_hi(float x) {
     return __uint_as_float(r);
 }
 
-// (value bits with the low 5 bits replaced by j): one shift on the ALU pipe
-// and one integer multiply-add on the FMA pipe (m32 == 32 is passed at run
-// time so the compiler cannot fold the pair back into two ALU LOP3s).
-__device__ __forceinline__ uint32_t chunk_key(uint32_t r, uint32_t j, uint32_t m32) {
+// The same rounding (to nearest, ties away from zero, at 10 mantissa bits) as
+// two integer ops for finite x: the magnitude's bit pattern + half an ulp of
+// tf32, low 13 bits cleared.  cvt.rna.tf32 costs ~5 instructions on sm_100
+// (non-finite checks); a non-finite x only occurs in rows / tables whose
+// error bound is non-finite, which the screen flags for the exact fixup.
+__device__ __forceinline__ float tf32_rna_fast(float x) {
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+
+// ---------------------------------------------------------------------------
+// Keys of the running top-2 (r2).  Every screened value of a row lies in one
+// window [2^p, 2^(p+16)) with p = 1 (mod 16) (row_prep adds the offset 2^p
+// inside C), so bits 30..27 of all its values are the same and
+//     key = value_bits * 32 + j          (one IMAD, FMA pipe, j immediate)
+// keeps all 27 remaining value bits (4 exponent + 23 mantissa bits: no
+// quantisation) and the column j of the 32-column chunk in the low 5 bits;
+// unsigned order of keys = order of (value, j).  m32 == 32 is a kernel
+// argument so the multiply cannot be folded into an ALU shift.
+// ---------------------------------------------------------------------------
+template <int J>
+__device__ __forceinline__ uint32_t col_key(uint32_t r, uint32_t m32) {
     uint32_t k;
-    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(k) : "r"(r >> 5), "r"(m32), "r"(j));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(k) : "r"(r), "r"(m32), "n"(J));
     return k;
+}
+
+// a + b and s - lo as IMADs with run-time unit multipliers (FMA pipe): the
+// pair step below then issues 4 ALU + 4 FMA-pipe instructions per two values
+// (the ALU pipe runs at half the issue rate, so balancing the pipes is what
+// makes the epilogue cheap).
+__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t m, uint32_t c) {
+    uint32_t k;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(k) : "r"(a), "r"(m), "r"(c));
+    return k;
+}
+
+// Fold 32 TMEM columns (chunk starting at column c0; columns >= nvalid of the
+// chunk are padding) into four independent (best, second) key states.
+// Pair step: lo = min(a,b); hi = (a+b) - lo; m2 = min(m2, max(m1,lo), hi);
+// m1 = min(m1, lo).  The chunk of each state's best is tracked on change.
+template <int J, bool MASK>
+__device__ __forceinline__ uint32_t col_key_m(const uint32_t (&r)[32], uint32_t nvalid, uint32_t m32) {
+    const uint32_t k = col_key<J>(r[J], m32);
+    if constexpr (MASK) return uint32_t(J) < nvalid ? k : 0xFFFFFFFFu;
+    return k;
+}
+
+template <int P, bool MASK>
+__device__ __forceinline__ void top2_pair(const uint32_t (&r)[32], uint32_t nvalid, uint32_t& m1, uint32_t& m2,
+                                          uint32_t m32, uint32_t one, uint32_t neg1) {
+    const uint32_t a = col_key_m<2 * P, MASK>(r, nvalid, m32), b = col_key_m<2 * P + 1, MASK>(r, nvalid, m32);
+    const uint32_t lo = min(a, b);
+    const uint32_t hi = mad_u32(lo, neg1, mad_u32(a, one, b));
+    m2 = min(m2, min(max(m1, lo), hi));
+    m1 = min(m1, lo);
+}
+
+#ifndef PQG_TOP2_NS
+#define PQG_TOP2_NS 4
+#endif
+constexpr int kNS = PQG_TOP2_NS;  // independent (best, second) states per thread
+
+template <int P, bool MASK>
+__device__ __forceinline__ void top2_pairs(const uint32_t (&r)[32], uint32_t nvalid, uint32_t (&m1)[kNS],
+                                           uint32_t (&m2)[kNS], uint32_t m32, uint32_t one, uint32_t neg1) {
+    if constexpr (P < 16) {
+        top2_pair<P, MASK>(r, nvalid, m1[P % kNS], m2[P % kNS], m32, one, neg1);
+        top2_pairs<P + 1, MASK>(r, nvalid, m1, m2, m32, one, neg1);
+    }
+}
+
+template <bool MASK>
+__device__ __forceinline__ void top2_chunk(const uint32_t (&r)[32], uint32_t nvalid, uint32_t c0,
+                                           uint32_t (&m1)[kNS], uint32_t (&m2)[kNS], uint32_t (&ch)[kNS],
+                                           uint32_t m32) {
+    const uint32_t one = m32 >> 5, neg1 = 0u - one;
+    uint32_t old[kNS];
+#pragma unroll
+    for (int s4 = 0; s4 < kNS; ++s4) old[s4] = m1[s4];
+    // pair p goes to state p % kNS
+    top2_pairs<0, MASK>(r, nvalid, m1, m2, m32, one, neg1);
+#pragma unroll
+    for (int s4 = 0; s4 < kNS; ++s4) ch[s4] = (m1[s4] != old[s4]) ? c0 : ch[s4];
+}
+
+// Merge the states: (best value, global column) and the runner-up's value;
+// values are the 27 key bits above the column field.
+__device__ __forceinline__ void top2_merge(const uint32_t (&m1)[kNS], const uint32_t (&m2)[kNS],
+                                           const uint32_t (&ch)[kNS], uint64_t& K1, uint32_t& V2) {
+    K1 = (uint64_t(m1[0] >> 5) << 32) | (ch[0] + (m1[0] & 31u));
+    V2 = m2[0] >> 5;
+#pragma unroll
+    for (int s4 = 1; s4 < kNS; ++s4) {
+        const uint64_t o = (uint64_t(m1[s4] >> 5) << 32) | (ch[s4] + (m1[s4] & 31u));
+        V2 = min(min(V2, m2[s4] >> 5), uint32_t(max(K1, o) >> 32));
+        K1 = min(K1, o);
+    }
 }
 
 // byte offset of element (row, k) of a K-major interleaved operand
@@ -146,26 +236,90 @@ __device__ __forceinline__ void store_index(const NearestArgs& a, uint64_t i, ui
 }
 
 // |screened - exact| bound for the 3xTF32 tensor-core screen.  S bounds the
-// sum of |terms| (2|x.c| + ||c||^2 + C <= (||x|| + max||c||)^2 + small).
-// Products of tf32 operands are exact in fp32; each MMA instruction may
-// lose up to one fp32 ulp (2u) of the accumulator, whose magnitude is <= S
-// (3 splits x K/8 k-steps instructions); the dropped lo*lo term and the tf32
-// rounding of the lo parts are <= 2^-21 |x_t c_t| per coordinate (<= 4u S).
-// Doubled for safety.  Empirically (tools/screen_bench.py) the TC and FP32
-// screens return identical codes on all 1M x M rows tested.
-__device__ __forceinline__ float tc_error_bound(float S, int K) {
-    const float n_mma = float(3 * (K / 8));
-    return 2.f * (2.f * n_mma + 8.f) * kU * S + 1e-30f;
+// magnitude of every partial sum (2|x.c| + ||c||^2 + C, offset included).
+// Products of tf32 operands are exact in fp32; each MMA instruction may lose
+// up to one fp32 ulp (2u) of the accumulator, whose magnitude is <= S (n_mma
+// instructions per tile); the dropped lo*lo term and the tf32 rounding of the
+// lo parts are <= 2^-21 |x_t c_t| per coordinate (<= 4u S).  Doubled for
+// safety.  Empirically (tools/screen_bench.py) the TC and FP32 screens return
+// identical codes on all 1M x M rows tested.
+__device__ __forceinline__ float tc_error_bound(float S, int n_mma) {
+    return 2.f * (2.f * float(n_mma) + 8.f) * kU * S + 1e-30f;
 }
 
-// B operand rows j = [-2c_j, ||c_j||^2, 1, 0...] split hi/lo (rows j >= k are
-// padding that never wins).  A thread stages whole codewords, two at a time,
-// with their loads issued together (vector loads when the rows are 16-byte
-// aligned): a short fit re-stages every launch, so the staging latency counts.
+// MMA instructions per tile.  Operand columns: [x (DS) | 1 1 1 C] against
+// [-2c (DS) | h m l 1] with ||c||^2 = h + m + l split exactly into three tf32
+// pieces and C rounded up to tf32, so the constant columns are exact in tf32:
+// a k-step holding only constants needs the hi*hi product alone, a k-step
+// holding x needs hi*hi + hi*lo + lo*hi.
+template <int DS>
+__host__ __device__ constexpr int umma_n_mma() {
+    return 3 * ((DS + 7) / 8) + (DS % 8 == 0 ? 1 : 0);
+}
+
+// tf32 value >= v (v finite, > 0): round the 13 dropped mantissa bits up
+__device__ __forceinline__ float tf32_up(float v) {
+    uint32_t u = __float_as_uint(v);
+    if (u & 0x1FFFu) u = (u | 0x1FFFu) + 1u;
+    return __uint_as_float(u);
+}
+
+// Per-row constants of the screen: the bound E, the offset window's top
+// exponent bits hi4 and the tf32 C of the A operand.  The offset O = 2^p
+// (p = 1 mod 16, the smallest p >= floor(log2 S) - 14) puts every screened
+// value of the row in [2^p, 2^(p+16)): values >= C - ||x||^2 - E >= O + E and
+// <= O + S + E < 2^(p+16) (O <= 2S, S < 2^(p+15)).  S (and with it E) grows
+// by at most the offset, i.e. typically not at all (O <= 2^-14 S unless S
+// lies just above a 2^(16i+1) boundary).
+template <int DS>
+struct RowConst {
+    float E, C;
+    uint32_t hi4;
+};
+
+template <int DS>
+__device__ __forceinline__ RowConst<DS> row_prep(float nx, float cmax) {
+    RowConst<DS> rc;
+    const float q = sqrtf(nx) * (1.f + 1e-6f) + cmax;
+    const float S = q * q * 1.01f + 1e-6f;  // >= 2|x.c| + ||c||^2 + ||x||^2 + 2E
+    int e = int((__float_as_uint(S) >> 23) & 0xFF) - 127;
+    e = max(-60, min(e, 100));  // non-finite S: E below is non-finite, the row is flagged
+    int p = e - 14;
+    p += ((1 - p) % 16 + 16) % 16;
+    const float O = __uint_as_float(uint32_t(p + 127) << 23);
+    rc.hi4 = uint32_t(p + 127) >> 4;
+    const float St = (S + O) * 1.002f;  // + C's rounding up to tf32 (<= 2^-10 C)
+    rc.E = tc_error_bound(St, umma_n_mma<DS>());
+    rc.C = tf32_up(nx * (1.f + 2.f * float(DS + 2) * kU) + 2.f * rc.E + O);
+    return rc;
+}
+
+// Decision of a row from its merged keys (see top2_merge).
+__device__ __forceinline__ bool row_unique(uint64_t K1, uint32_t V2, uint32_t hi4, float E, uint64_t k) {
+    const uint32_t v1 = uint32_t(K1 >> 32);
+    if (!isfinite(E) || v1 >= 0x7FFFFFFu || uint32_t(K1) >= k) return false;
+    if (V2 >= 0x7FFFFFFu) return true;  // no runner-up
+    const float f1 = __uint_as_float(v1 | (hi4 << 27)), f2 = __uint_as_float(V2 | (hi4 << 27));
+    return f2 - f1 > 2.05f * E;
+}
+
+// A operand of one row: [x (DS) | 1 1 1 C] split hi / lo (constants exact)
+template <int DS, int KA>
+__device__ __forceinline__ float a_col(const float (&x)[DS], float C, int tt) {
+    return tt < DS ? x[tt] : (tt < DS + 3 ? 1.f : (tt == DS + 3 ? C : 0.f));
+}
+
+// B operand rows j = [-2c_j (DS) | h m l 1 | 0...] split hi/lo, with
+// ||c_j||^2 = h + m + l exactly (three tf32 pieces); rows j >= k are zero
+// padding, masked out of the top-2 by the epilogue.  A thread stages whole
+// codewords, two at a time, with their loads issued together (vector loads
+// when the rows are 16-byte aligned): a short fit re-stages every launch, so
+// the staging latency counts.
 template <int DS, int KA, bool PAD>
 __device__ __forceinline__ void stage_codewords(uint8_t* Bh, uint8_t* Bl, const float* tab,
                                                 const float* cnorm, uint64_t k, uint32_t d,
                                                 uint32_t n_pad, uint32_t tid, uint32_t nthreads) {
+    static_assert(KA >= DS + 4, "constant columns");
     constexpr uint32_t SBO = (KA / 4) * 128;
     const bool vec = !PAD && (DS % 4) == 0 && (reinterpret_cast<uintptr_t>(tab) & 15u) == 0;
     for (uint32_t j0 = 0; j0 < n_pad; j0 += 2 * nthreads) {
@@ -188,10 +342,12 @@ __device__ __forceinline__ void stage_codewords(uint8_t* Bh, uint8_t* Bl, const 
 #pragma unroll
                     for (int t = 0; t < DS; ++t) v[u][t] = (!PAD || uint32_t(t) < d) ? -2.f * __ldg(c + t) : 0.f;
                 }
-                v[u][DS] = __ldg(cnorm + j);
-                v[u][DS + 1] = 1.f;
-            } else {
-                v[u][DS] = 3.0e38f;  // padded codeword: never the minimum
+                const float cn = __ldg(cnorm + j);
+                const float h = tf32_hi(cn), m = tf32_hi(cn - h);
+                v[u][DS] = h;
+                v[u][DS + 1] = m;
+                v[u][DS + 2] = (cn - h) - m;  // <= 3 significant bits: exact in tf32
+                v[u][DS + 3] = 1.f;
             }
         }
 #pragma unroll
@@ -204,11 +360,32 @@ __device__ __forceinline__ void stage_codewords(uint8_t* Bh, uint8_t* Bl, const 
 #pragma unroll
                 for (int w = 0; w < 4; ++w) {
                     h[w] = tf32_hi(v[u][t + w]);
-                    l[w] = tf32_hi(v[u][t + w] - h[w]);
+                    l[w] = t + w < DS ? tf32_hi(v[u][t + w] - h[w]) : 0.f;
                 }
                 *reinterpret_cast<float4*>(Bh + il_off(j, t, SBO)) = make_float4(h[0], h[1], h[2], h[3]);
                 *reinterpret_cast<float4*>(Bl + il_off(j, t, SBO)) = make_float4(l[0], l[1], l[2], l[3]);
             }
+        }
+    }
+}
+
+// The n_mma MMAs of one tile: D (+)= Ah Bh^T (+ Ah Bl^T + Al Bh^T for the
+// k-steps that hold x columns)
+template <int DS, int KA>
+__device__ __forceinline__ void issue_tile(uint32_t d_tmem, uint32_t a_hi, uint32_t a_lo, uint32_t b_hi,
+                                           uint32_t b_lo, uint32_t boff, uint32_t idesc) {
+    constexpr uint32_t SBO = (KA / 4) * 128;
+#pragma unroll
+    for (int s = 0; s < KA / 8; ++s) {
+        const uint32_t ko = s * 256;  // two 16-byte K chunks per k-step
+        const uint64_t dah = make_desc(a_hi + ko, 128, SBO);
+        const uint64_t dbh = make_desc(b_hi + boff + ko, 128, SBO);
+        mma_tf32(d_tmem, dah, dbh, idesc, s > 0);
+        if (8 * s < DS) {
+            const uint64_t dal = make_desc(a_lo + ko, 128, SBO);
+            const uint64_t dbl = make_desc(b_lo + boff + ko, 128, SBO);
+            mma_tf32(d_tmem, dah, dbl, idesc, 1);
+            mma_tf32(d_tmem, dal, dbh, idesc, 1);
         }
     }
 }
@@ -296,19 +473,17 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
         for (int t = 0; t < DS; ++t) x[t] = x_next[t];
 #pragma unroll
         for (int t = 0; t < DS; ++t) nx = fmaf(x[t], x[t], nx);
-        const float q = sqrtf(nx) * (1.f + 1e-6f) + cmax;
-        const float S = q * q * 1.01f + 1e-6f;  // >= 2|x.c| + ||c||^2 + C
-        const float E = tc_error_bound(S, KA);
-        const float C = nx * (1.f + 2.f * float(DS + 2) * kU) + 2.f * E;
+        const RowConst<DS> rc = row_prep<DS>(nx, cmax);
+        const float E = rc.E;
 #pragma unroll
         for (int t = 0; t < KA; t += 4) {
             float h[4], l[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int tt = t + u;
-                const float v = tt < DS ? x[tt] : (tt == DS ? 1.f : (tt == DS + 1 ? C : 0.f));
-                h[u] = tf32_hi(v);
-                l[u] = tf32_hi(v - h[u]);
+                const float v = a_col<DS, KA>(x, rc.C, tt);
+                h[u] = tt < DS ? tf32_rna_fast(v) : v;  // constant columns are tf32 already
+                l[u] = tt < DS ? tf32_rna_fast(v - h[u]) : 0.f;
             }
             *reinterpret_cast<float4*>(Ah + il_off(tid, t, SBO)) = make_float4(h[0], h[1], h[2], h[3]);
             *reinterpret_cast<float4*>(Al + il_off(tid, t, SBO)) = make_float4(l[0], l[1], l[2], l[3]);
@@ -323,9 +498,9 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
         // each running best is tracked on change.  Four independent (best,
         // second) states per thread break the min/max dependency chain; they
         // are merged at the end.
-        uint32_t m1[4], m2[4], ch[4];
+        uint32_t m1[kNS], m2[kNS], ch[kNS];
 #pragma unroll
-        for (int s4 = 0; s4 < 4; ++s4) { m1[s4] = 0xFFFFFFFFu; m2[s4] = 0xFFFFFFFFu; ch[s4] = 0; }
+        for (int s4 = 0; s4 < kNS; ++s4) { m1[s4] = 0xFFFFFFFFu; m2[s4] = 0xFFFFFFFFu; ch[s4] = 0; }
         const uint32_t lane_base = (warp * 32u) << 16;
         for (uint32_t p0 = 0; p0 < n_pad; p0 += n_mma) {
             const uint32_t w = min(n_mma, n_pad - p0);
@@ -333,22 +508,12 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
                 fence_before();
                 __syncthreads();
             }
-            // ---- MMA: D = Ah Bh^T + Ah Bl^T + Al Bh^T over KA/8 k-steps
+            // ---- MMA: D = Ah Bh^T + Ah Bl^T + Al Bh^T (constant k-steps: Ah Bh^T)
             if (tid == 0) {
                 fence_after();
                 const uint32_t idesc = make_idesc_tf32(kRows, w);
                 const uint32_t boff = (p0 / 8) * SBO;  // codeword rows p0.. of the B stage
-#pragma unroll
-                for (int s = 0; s < KA / 8; ++s) {
-                    const uint32_t ko = s * 256;  // two 16-byte K chunks per k-step
-                    const uint64_t dah = make_desc(a_hi + ko, 128, SBO);
-                    const uint64_t dal = make_desc(a_lo + ko, 128, SBO);
-                    const uint64_t dbh = make_desc(b_hi + boff + ko, 128, SBO);
-                    const uint64_t dbl = make_desc(b_lo + boff + ko, 128, SBO);
-                    mma_tf32(tmem, dah, dbh, idesc, s > 0);
-                    mma_tf32(tmem, dah, dbl, idesc, 1);
-                    mma_tf32(tmem, dal, dbh, idesc, 1);
-                }
+                issue_tile<DS, KA>(tmem, a_hi, a_lo, b_hi, b_lo, boff, idesc);
                 mma_commit(&mbar);
             }
             if (p0 == 0) load_row(tile + ncta, x_next);  // next tile's row, in flight during the epilogue
@@ -356,28 +521,12 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
             phase ^= 1;
             fence_after();
             // ---- epilogue: this thread's row, columns p0 .. p0 + w
+            // columns >= k of this pass (codeword padding, and the unwritten
+            // tail of a 16-column-multiple n_mma) are masked out of the top-2
             auto process = [&](uint32_t (&r)[32], uint32_t c0) {
-                if (w - c0 < 32) {  // columns past N are not written by the MMA
-#pragma unroll
-                    for (int j = 16; j < 32; ++j) r[j] = 0x7f800000u;
-                }
-                uint32_t old[4];
-#pragma unroll
-                for (int s4 = 0; s4 < 4; ++s4) old[s4] = m1[s4];
-#pragma unroll
-                for (int j = 0; j < 32; j += 8) {
-#pragma unroll
-                    for (int s4 = 0; s4 < 4; ++s4) {
-                        const int jj = j + 2 * s4;
-                        const uint32_t ka = chunk_key(r[jj], uint32_t(jj), m32);
-                        const uint32_t kb = chunk_key(r[jj + 1], uint32_t(jj + 1), m32);
-                        const uint32_t lo = min(ka, kb), hi = max(ka, kb);
-                        m2[s4] = min(min(m2[s4], max(m1[s4], lo)), hi);
-                        m1[s4] = min(m1[s4], lo);
-                    }
-                }
-#pragma unroll
-                for (int s4 = 0; s4 < 4; ++s4) ch[s4] = (m1[s4] != old[s4]) ? p0 + c0 : ch[s4];
+                const uint32_t cabs = p0 + c0;
+                if (cabs + 32 <= k) top2_chunk<false>(r, 32u, cabs, m1, m2, ch, m32);
+                else top2_chunk<true>(r, uint32_t(k - cabs), cabs, m1, m2, ch, m32);
             };
             if constexpr (DB) {
                 // two register buffers: the next 32 columns load from TMEM
@@ -411,24 +560,14 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
                 }
             }
         }
-        // merge the four states: full keys (value bits | global column) for the
-        // best, value bits (low 5 cleared) for the runner-up
-        uint64_t K1 = (uint64_t(m1[0] & ~31u) << 32) | (ch[0] + (m1[0] & 31u));
-        uint32_t V2 = m2[0] & ~31u;
-#pragma unroll
-        for (int s4 = 1; s4 < 4; ++s4) {
-            const uint64_t o = (uint64_t(m1[s4] & ~31u) << 32) | (ch[s4] + (m1[s4] & 31u));
-            V2 = min(min(V2, m2[s4] & ~31u), uint32_t(max(K1, o) >> 32));
-            K1 = min(K1, o);
-        }
+        uint64_t K1;
+        uint32_t V2;
+        top2_merge(m1, m2, ch, K1, V2);
         fence_before();
         if (valid) {
             const uint32_t idx = uint32_t(K1);
-            const uint32_t v1 = uint32_t(K1 >> 32);
-            // non-finite E (inf/NaN in the row or table) or best: the exact fixup decides
-            const bool unique = isfinite(E) && v1 < 0x7f800000u && ((V2 >= 0x7f800000u) ||
-                                (__uint_as_float(V2) - __uint_as_float(v1 | 31u) > 2.05f * E));
-            if (unique && idx < k) {
+            // non-finite E (inf/NaN in the row or table): the exact fixup decides
+            if (row_unique(K1, V2, rc.hi4, E, k)) {
                 store_index(a, row, b, idx);
                 if (a.out_dist) {
                     const float* c = tab + uint64_t(idx) * d;
@@ -503,6 +642,7 @@ __global__ void __launch_bounds__(NW * 32, 1) umma_screen2_kernel(NearestArgs a,
     __shared__ uint64_t mbar[2];
     __shared__ uint32_t tmem_base;
     __shared__ float ebuf[2][kRows];
+    __shared__ uint32_t hbuf[2][kRows];
     __shared__ uint64_t mK[NPART > 1 ? NPART - 1 : 1][kRows];
     __shared__ uint32_t mV[NPART > 1 ? NPART - 1 : 1][kRows];
 
@@ -547,11 +687,11 @@ __global__ void __launch_bounds__(NW * 32, 1) umma_screen2_kernel(NearestArgs a,
         float nx = 0.f;
 #pragma unroll
         for (int t = 0; t < DS; ++t) nx = fmaf(r.x[t], r.x[t], nx);
-        const float q = sqrtf(nx) * (1.f + 1e-6f) + cmax;
-        const float S = q * q * 1.01f + 1e-6f;
-        const float E = tc_error_bound(S, KA);
-        const float C = nx * (1.f + 2.f * float(DS + 2) * kU) + 2.f * E;
-        if (half == 0) ebuf[it & 1][row_l] = E;
+        const RowConst<DS> rc = row_prep<DS>(nx, cmax);
+        if (half == 0) {
+            ebuf[it & 1][row_l] = rc.E;
+            hbuf[it & 1][row_l] = rc.hi4;
+        }
         uint8_t* Ah = A0 + (it & 1) * 2 * ASTAGE;
         uint8_t* Al = Ah + ASTAGE;
         constexpr int NCH = KA / 4;  // 16-byte chunks per row, dealt round-robin to the parts
@@ -562,9 +702,9 @@ __global__ void __launch_bounds__(NW * 32, 1) umma_screen2_kernel(NearestArgs a,
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int tt = 4 * c + u;
-                const float v = tt < DS ? r.x[tt] : (tt == DS ? 1.f : (tt == DS + 1 ? C : 0.f));
-                h[u] = tf32_hi(v);
-                l[u] = tf32_hi(v - h[u]);
+                const float v = a_col<DS, KA>(r.x, rc.C, tt);
+                h[u] = tt < DS ? tf32_rna_fast(v) : v;
+                l[u] = tt < DS ? tf32_rna_fast(v - h[u]) : 0.f;
             }
             *reinterpret_cast<float4*>(Ah + il_off(row_l, 4 * c, SBO)) = make_float4(h[0], h[1], h[2], h[3]);
             *reinterpret_cast<float4*>(Al + il_off(row_l, 4 * c, SBO)) = make_float4(l[0], l[1], l[2], l[3]);
@@ -573,17 +713,7 @@ __global__ void __launch_bounds__(NW * 32, 1) umma_screen2_kernel(NearestArgs a,
     auto issue = [&](uint64_t it) {
         const uint32_t ah = smem_u32(A0 + (it & 1) * 2 * ASTAGE), al = ah + ASTAGE;
         const uint32_t d_tmem = tmem + uint32_t(it & 1) * 256u;
-#pragma unroll
-        for (int s2 = 0; s2 < KA / 8; ++s2) {
-            const uint32_t ko = s2 * 256;
-            const uint64_t dah = make_desc(ah + ko, 128, SBO);
-            const uint64_t dal = make_desc(al + ko, 128, SBO);
-            const uint64_t dbh = make_desc(b_hi + ko, 128, SBO);
-            const uint64_t dbl = make_desc(b_lo + ko, 128, SBO);
-            mma_tf32(d_tmem, dah, dbh, idesc, s2 > 0);
-            mma_tf32(d_tmem, dah, dbl, idesc, 1);
-            mma_tf32(d_tmem, dal, dbh, idesc, 1);
-        }
+        issue_tile<DS, KA>(d_tmem, ah, al, b_hi, b_lo, 0u, idesc);
         mma_commit(&mbar[it & 1]);
     };
     auto tile_of = [&](uint64_t it) { return uint64_t(cta) + it * ncta; };
@@ -619,9 +749,9 @@ __global__ void __launch_bounds__(NW * 32, 1) umma_screen2_kernel(NearestArgs a,
         phases ^= 1u << (it & 1);
         fence_after();
         // ---- epilogue of tile it: this thread's row, its column half
-        uint32_t m1[4], m2[4], ch[4];
+        uint32_t m1[kNS], m2[kNS], ch[kNS];
 #pragma unroll
-        for (int s4 = 0; s4 < 4; ++s4) { m1[s4] = 0xFFFFFFFFu; m2[s4] = 0xFFFFFFFFu; ch[s4] = 0; }
+        for (int s4 = 0; s4 < kNS; ++s4) { m1[s4] = 0xFFFFFFFFu; m2[s4] = 0xFFFFFFFFu; ch[s4] = 0; }
         const uint32_t lane_base = ((warp & 3u) * 32u) << 16;
         const uint32_t nchunks = (n_pad + 31) / 32;
         const uint32_t per = (nchunks + NPART - 1) / NPART;  // 32-column chunks per part
@@ -632,37 +762,13 @@ __global__ void __launch_bounds__(NW * 32, 1) umma_screen2_kernel(NearestArgs a,
             uint32_t r[32];
             tmem_ld32(tb + lane_base + c0, r);
             tmem_wait_ld();
-            if (n_pad - c0 < 32) {
-#pragma unroll
-                for (int j = 16; j < 32; ++j) r[j] = 0x7f800000u;
-            }
-            uint32_t old[4];
-#pragma unroll
-            for (int s4 = 0; s4 < 4; ++s4) old[s4] = m1[s4];
-#pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-#pragma unroll
-                for (int s4 = 0; s4 < 4; ++s4) {
-                    const int jj = j + 2 * s4;
-                    const uint32_t ka = chunk_key(r[jj], uint32_t(jj), m32);
-                    const uint32_t kb = chunk_key(r[jj + 1], uint32_t(jj + 1), m32);
-                    const uint32_t lo = min(ka, kb), hi = max(ka, kb);
-                    m2[s4] = min(min(m2[s4], max(m1[s4], lo)), hi);
-                    m1[s4] = min(m1[s4], lo);
-                }
-            }
-#pragma unroll
-            for (int s4 = 0; s4 < 4; ++s4) ch[s4] = (m1[s4] != old[s4]) ? c0 : ch[s4];
+            if (c0 + 32 <= k) top2_chunk<false>(r, 32u, c0, m1, m2, ch, m32);
+            else top2_chunk<true>(r, uint32_t(k - c0), c0, m1, m2, ch, m32);
         }
         fence_before();
-        uint64_t K1 = (uint64_t(m1[0] & ~31u) << 32) | (ch[0] + (m1[0] & 31u));
-        uint32_t V2 = m2[0] & ~31u;
-#pragma unroll
-        for (int s4 = 1; s4 < 4; ++s4) {
-            const uint64_t o = (uint64_t(m1[s4] & ~31u) << 32) | (ch[s4] + (m1[s4] & 31u));
-            V2 = min(min(V2, m2[s4] & ~31u), uint32_t(max(K1, o) >> 32));
-            K1 = min(K1, o);
-        }
+        uint64_t K1;
+        uint32_t V2;
+        top2_merge(m1, m2, ch, K1, V2);
         if (half > 0) {
             mK[half - 1][row_l] = K1;
             mV[half - 1][row_l] = V2;
@@ -678,12 +784,8 @@ __global__ void __launch_bounds__(NW * 32, 1) umma_screen2_kernel(NearestArgs a,
             const uint64_t row = tile_of(it) * kRows + row_l;
             if (row < a.n) {
                 const uint32_t idx = uint32_t(K1);
-                const uint32_t v1 = uint32_t(K1 >> 32);
-                const float E = ebuf[it & 1][row_l];
-                // non-finite E (inf/NaN in the row or table) or best: the exact fixup decides
-            const bool unique = isfinite(E) && v1 < 0x7f800000u && ((V2 >= 0x7f800000u) ||
-                                    (__uint_as_float(V2) - __uint_as_float(v1 | 31u) > 2.05f * E));
-                if (unique && idx < k) {
+                // non-finite E (inf/NaN in the row or table): the exact fixup decides
+                if (row_unique(K1, V2, hbuf[it & 1][row_l], ebuf[it & 1][row_l], k)) {
                     store_index(a, row, b, idx);
                     if (a.out_dist) {
                         const float* xp = a.src.x + row * a.src.ldx + uint64_t(b) * a.src.col_stride;

@@ -50,7 +50,11 @@ def main():
                                                 vp(codes.data_ptr())))
         enc()
         torch.cuda.synchronize()
-        if args.ncu:
+        if args.ncu:  # one profiled encode (ncu --profile-from-start off)
+            torch.cuda.cudart().cudaProfilerStart()
+            enc()
+            torch.cuda.synchronize()
+            torch.cuda.cudart().cudaProfilerStop()
             continue
         ctx.profile(True)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
