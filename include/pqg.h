@@ -9,7 +9,7 @@
  * negative status; pqg_last_error() returns the thread's last message.
  * Status mapping to the reference's exceptions:
  *   PQG_EINVAL -> std::invalid_argument   PQG_ERANGE -> std::out_of_range
- *   PQG_ECUDA / PQG_ENOMEM / PQG_EUNSUPPORTED / PQG_ECHUNK -> std::runtime_error
+ *   PQG_ECUDA / PQG_ENOMEM / PQG_EUNSUPPORTED / PQG_ECHUNK / PQG_EIO -> std::runtime_error
  * Message substrings follow the reference ("not divisible", "exceeds",
  * "no items", "duplicate id", "nprobe", ...).
  *
@@ -38,6 +38,7 @@ extern "C" {
 #define PQG_ENOMEM (-4)
 #define PQG_EUNSUPPORTED (-5)
 #define PQG_ECHUNK (-6) /* a pipeline chunk task failed: std::runtime_error("chunk <id>: ...") */
+#define PQG_EIO (-7)    /* file / format error: std::runtime_error with the reference's message */
 
 typedef struct pqg_ctx pqg_ctx;     /* one GPU + stream + scratch arena */
 typedef struct pqg_index pqg_index; /* device-resident inverted index */
@@ -292,6 +293,35 @@ int pqg_kmshard_reseed_apply(pqg_ctx* ctx, pqg_kmshard* h, float* tables, const 
  * pass's local assignments [B*n] (any nullable; host or device) */
 int pqg_kmshard_result(pqg_ctx* ctx, pqg_kmshard* h, uint32_t* iterations_run, double* inertia,
                        double* inertia_per_iter, uint32_t* assignments);
+
+/* ---- on-disk formats ----------------------------------
+ * Byte-identical to the reference's files; load errors carry the reference's
+ * messages ("<format>: bad magic", "truncated read of <what>",
+ * "<path>: unsupported version N", "<path>: duplicate id N",
+ * "<path>: code out of range", "<path>: trailing data after payload", ...) as
+ * PQG_EIO (std::runtime_error), except the codebook-parameter checks
+ * (PQG_EINVAL, std::invalid_argument) the reference raises on the way. */
+
+/* PQII index image (save_index / load_index, ivf.cpp:264-355).  The posting
+ * lists are packed / unpacked by device kernels (formats.cu) straight from /
+ * into the device CSR; ids are checked for duplicates and codes for range on
+ * the device.  serialize: buf (host or device) NULL -> only *size. */
+int pqg_index_serialize(pqg_ctx* ctx, const pqg_index* index, void* buf, uint64_t cap, uint64_t* size);
+int pqg_index_deserialize(pqg_ctx* ctx, const void* buf, uint64_t size, const char* name, pqg_index** out);
+int pqg_index_save(pqg_ctx* ctx, const pqg_index* index, const char* path);
+int pqg_index_load(pqg_ctx* ctx, const char* path, pqg_index** out);
+
+/* PQCM code file (save_codes / load_codes, pq.cpp:221-259): codes host or
+ * device; load validates every code on the device ("code out of range at
+ * row N").  file_info reads only the header (n, M, ks). */
+int pqg_codes_save(pqg_ctx* ctx, const uint8_t* codes, uint64_t n, uint32_t M, uint32_t ks, const char* path);
+int pqg_codes_file_info(const char* path, uint64_t* n, uint32_t* M, uint32_t* ks);
+int pqg_codes_load(pqg_ctx* ctx, const char* path, uint8_t* codes, uint64_t cap_bytes);
+
+/* PQCB codebook file (save_codebook / load_codebook, pq.cpp:183-219). */
+int pqg_codebook_save(pqg_ctx* ctx, const float* tables, uint32_t M, uint32_t ks, uint32_t ds, const char* path);
+int pqg_codebook_file_info(const char* path, uint32_t* M, uint32_t* ks, uint32_t* ds);
+int pqg_codebook_load(pqg_ctx* ctx, const char* path, float* tables, uint64_t cap_floats);
 
 #ifdef __cplusplus
 }

@@ -432,6 +432,15 @@ class RefImpl(_Base):
                 [C.c_void_p, _f32p, _u64, _u64p, _u64, _u64, C.c_int, C.c_double, _u64p, _f64p,
                  _u32p])
         self.fn("hardware_concurrency", C.c_uint, [])
+        self.fn("last_message", C.c_char_p, [])
+        self.fn("save_index", C.c_int, [C.c_void_p, C.c_char_p])
+        self.fn("load_index", C.c_void_p, [C.c_char_p, C.POINTER(C.c_int)])
+        self.fn("save_codes", C.c_int, [_u8p, _u64, _u32, _u32, C.c_char_p])
+        self.fn("load_codes", C.c_int, [C.c_char_p, C.POINTER(_u64), C.POINTER(_u32), C.POINTER(_u32),
+                                        C.c_void_p, _u64])
+        self.fn("save_codebook", C.c_int, [_f32p, _u32, _u32, _u32, C.c_char_p])
+        self.fn("load_codebook", C.c_int, [C.c_char_p, C.POINTER(_u32), C.POINTER(_u32), C.POINTER(_u32),
+                                           C.c_void_p, _u64])
 
     @staticmethod
     def _check(rc, what):
@@ -642,6 +651,51 @@ class RefImpl(_Base):
 
     def default_nlist(self, n):
         return self.fn("default_nlist", _u64, [_u64])(n)
+
+    # -- on-disk formats (the reference's own save_* / load_*) -------------
+    # load_* return (status, message, value): status 0 ok, -1 invalid_argument,
+    # -2 out_of_range, -4 runtime_error; message = the exception's what()
+    def _msg(self):
+        return self.lib.ref_last_message().decode()
+
+    def save_index(self, handle, path):
+        rc = self.lib.ref_save_index(handle.h, path.encode())
+        return rc, self._msg()
+
+    def load_index(self, path, row_bytes, dims):
+        st = C.c_int()
+        h = self.lib.ref_load_index(path.encode(), C.byref(st))
+        if st.value:
+            return st.value, self._msg(), None
+        return 0, "", RefIndexHandle(self, h, row_bytes, dims)
+
+    def save_codes(self, codes, M, ks, path):
+        codes = np.ascontiguousarray(codes, np.uint8)
+        return self.lib.ref_save_codes(codes, codes.shape[0], M, ks, path.encode()), self._msg()
+
+    def load_codes(self, path):
+        n, M, ks = _u64(), _u32(), _u32()
+        rc = self.lib.ref_load_codes(path.encode(), C.byref(n), C.byref(M), C.byref(ks), None, 0)
+        if rc:
+            return rc, self._msg(), None
+        out = np.empty((n.value, M.value * code_width(ks.value)), np.uint8)
+        self.lib.ref_load_codes(path.encode(), C.byref(n), C.byref(M), C.byref(ks), out.ctypes.data, out.nbytes)
+        return 0, "", (out, M.value, ks.value)
+
+    def save_codebook(self, tables, path):
+        tables = np.ascontiguousarray(tables, np.float32)
+        M, ks, ds = tables.shape
+        return self.lib.ref_save_codebook(tables, M, ks, ds, path.encode()), self._msg()
+
+    def load_codebook(self, path):
+        M, ks, ds = _u32(), _u32(), _u32()
+        rc = self.lib.ref_load_codebook(path.encode(), C.byref(M), C.byref(ks), C.byref(ds), None, 0)
+        if rc:
+            return rc, self._msg(), None
+        out = np.empty((M.value, ks.value, ds.value), np.float32)
+        self.lib.ref_load_codebook(path.encode(), C.byref(M), C.byref(ks), C.byref(ds), out.ctypes.data,
+                                   out.size)
+        return 0, "", out
 
     def chunk_rows(self, n, c):
         b = np.empty(c + 1, np.uint64)

@@ -14,6 +14,7 @@
 #include <random>
 #include <span>
 #include <stdexcept>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -465,6 +466,80 @@ int ref_run_pipeline(const float* data, std::uint64_t n, std::uint64_t D, std::u
         err[err_len - 1] = 0;
     }
     return rc;
+}
+
+
+}  // extern "C"
+
+// ---- on-disk formats: the reference's own writers / readers
+// (proj/src/pq.cpp:183-259, ivf.cpp:264-355).  The exception message of a
+// failed call is kept for ref_last_message().
+namespace {
+thread_local std::string g_msg;
+thread_local CodeMatrix g_codes;
+thread_local Codebook g_cb;
+template <class F>
+int guarded_msg(F&& f) {
+    try {
+        f();
+        g_msg.clear();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        g_msg = e.what();
+        return -1;
+    } catch (const std::out_of_range& e) {
+        g_msg = e.what();
+        return -2;
+    } catch (const std::exception& e) {
+        g_msg = e.what();
+        return -4;
+    }
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_message() { return g_msg.c_str(); }
+
+int ref_save_index(void* h, const char* path) {
+    return guarded_msg([&] { save_index(static_cast<RefIndex*>(h)->index, path); });
+}
+
+void* ref_load_index(const char* path, int* status) {
+    RefIndex* h = nullptr;
+    *status = guarded_msg([&] { h = new RefIndex{load_index(path)}; });
+    return h;
+}
+
+int ref_save_codes(const std::uint8_t* codes, std::uint64_t n, std::uint32_t M, std::uint32_t ks, const char* path) {
+    return guarded_msg([&] { save_codes(as_codes(codes, n, M, ks), path); });
+}
+
+// loads into a thread-local CodeMatrix; out (cap bytes) may be null to query the shape
+int ref_load_codes(const char* path, std::uint64_t* n, std::uint32_t* M, std::uint32_t* ks, std::uint8_t* out,
+                   std::uint64_t cap) {
+    return guarded_msg([&] {
+        g_codes = load_codes(path);
+        *n = g_codes.rows;
+        *M = g_codes.m_subspaces;
+        *ks = g_codes.ks;
+        if (out && cap >= g_codes.bytes.size()) std::memcpy(out, g_codes.bytes.data(), g_codes.bytes.size());
+    });
+}
+
+int ref_save_codebook(const float* tables, std::uint32_t M, std::uint32_t ks, std::uint32_t ds, const char* path) {
+    return guarded_msg([&] { save_codebook(as_codebook(tables, M, ks, ds), path); });
+}
+
+int ref_load_codebook(const char* path, std::uint32_t* M, std::uint32_t* ks, std::uint32_t* ds, float* out,
+                      std::uint64_t cap) {
+    return guarded_msg([&] {
+        g_cb = load_codebook(path);
+        *M = g_cb.m_subspaces;
+        *ks = g_cb.ks;
+        *ds = g_cb.sub_dim;
+        if (out && cap >= g_cb.tables.size()) std::memcpy(out, g_cb.tables.data(), g_cb.tables.size() * 4);
+    });
 }
 
 }  // extern "C"

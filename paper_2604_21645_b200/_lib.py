@@ -19,6 +19,7 @@ PQG_ECUDA = -3
 PQG_ENOMEM = -4
 PQG_EUNSUPPORTED = -5
 PQG_ECHUNK = -6  # a pipeline chunk task failed (std::runtime_error)
+PQG_EIO = -7  # file / format error (std::runtime_error, the reference's message)
 
 _vp = C.c_void_p
 _u64 = C.c_uint64
@@ -72,6 +73,16 @@ _SIGS = {
     "pqg_flat_scan": (_i32, [_vp, _vp, _u32, _u32, _u32, _vp, _vp, _u64, _vp, _u64, _u64, _i32,
                              _f64, _vp, _vp, _vp]),
     "pqg_topk_merge": (_i32, [_vp, _vp, _vp, _vp, _u32, _u64, _u64, _vp, _vp, _vp]),
+    "pqg_index_serialize": (_i32, [_vp, _vp, _vp, _u64, C.POINTER(_u64)]),
+    "pqg_index_deserialize": (_i32, [_vp, _vp, _u64, C.c_char_p, C.POINTER(_vp)]),
+    "pqg_index_save": (_i32, [_vp, _vp, C.c_char_p]),
+    "pqg_index_load": (_i32, [_vp, C.c_char_p, C.POINTER(_vp)]),
+    "pqg_codes_save": (_i32, [_vp, _vp, _u64, _u32, _u32, C.c_char_p]),
+    "pqg_codes_file_info": (_i32, [C.c_char_p, C.POINTER(_u64), C.POINTER(_u32), C.POINTER(_u32)]),
+    "pqg_codes_load": (_i32, [_vp, C.c_char_p, _vp, _u64]),
+    "pqg_codebook_save": (_i32, [_vp, _vp, _u32, _u32, _u32, C.c_char_p]),
+    "pqg_codebook_file_info": (_i32, [C.c_char_p, C.POINTER(_u32), C.POINTER(_u32), C.POINTER(_u32)]),
+    "pqg_codebook_load": (_i32, [_vp, C.c_char_p, _vp, _u64]),
     "pqg_assign_pass": (_i32, [_vp, _vp, _u64, _u64, _u32, _u32, _u32, _vp, _u64, _vp, _vp]),
     "pqg_update_pass": (_i32, [_vp, _vp, _u64, _u64, _u32, _u32, _u32, _vp, _u64, _vp, _vp, _vp]),
     "pqg_rows_sum_f64": (_i32, [_vp, _vp, _u64, _u32, _vp]),
@@ -131,6 +142,8 @@ def check(rc: int, what: str = "") -> None:
         raise ValueError(msg)          # std::invalid_argument
     if rc == PQG_ERANGE:
         raise IndexError(msg)          # std::out_of_range
+    if rc == PQG_EIO:
+        raise PQGError(msg)            # the reference's runtime_error (file / format)
     if rc == PQG_ECHUNK:
         raise PQGError(msg)            # run_chunk_tasks' runtime_error("chunk <id>: ...")
     raise PQGError(f"{what}: {msg} (status {rc})")

@@ -12,6 +12,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstring>
+#include <tuple>
 #include <memory>
 #include <numeric>
 #include <random>
@@ -2053,6 +2055,476 @@ int pqg_kmshard_result(pqg_ctx* ctx, pqg_kmshard* h, uint32_t* iterations_run, d
             PQG_CUDA(cudaMemcpyAsync(assignments, h->assign, sizeof(uint32_t) * h->B * h->n, cudaMemcpyDefault,
                                      o->stream));
         PQG_CUDA(cudaStreamSynchronize(o->stream));
+    });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// on-disk formats: PQII / PQCM / PQCB, byte-identical to
+// the reference's writers (proj/src/ivf.cpp:264-355, pq.cpp:183-259).  The
+// posting lists move between the file layout and the device CSR through the
+// pack / unpack kernels of formats.cu; load-time validation (duplicate ids,
+// code range, finite codewords) runs on the device.  Errors carry the
+// reference's messages (io_util.hpp read_bytes / expect_magic) as PQG_EIO.
+// ---------------------------------------------------------------------------
+namespace {
+
+[[noreturn]] void io_fail(const std::string& m) { fail(PQG_EIO, m); }
+
+struct ByteReader {  // proj/src/io_util.hpp:45-87 over a memory image
+    const uint8_t* b;
+    uint64_t size, pos;
+    void need(uint64_t k, const char* what) const {
+        if (size - pos < k) io_fail(std::string("truncated read of ") + what);
+    }
+    uint32_t u32(const char* what) {
+        need(4, what);
+        const uint32_t v = uint32_t(b[pos]) | uint32_t(b[pos + 1]) << 8 | uint32_t(b[pos + 2]) << 16 |
+                           uint32_t(b[pos + 3]) << 24;
+        pos += 4;
+        return v;
+    }
+    uint64_t u64(const char* what) {
+        need(8, what);
+        uint64_t v = 0;
+        for (int i = 7; i >= 0; --i) v = (v << 8) | b[pos + i];
+        pos += 8;
+        return v;
+    }
+    void magic(const char* m, const char* format_name) {
+        need(4, "magic");
+        if (std::memcmp(b + pos, m, 4) != 0) io_fail(std::string(format_name) + ": bad magic");
+        pos += 4;
+    }
+    // k elements of `es` bytes (overflow-safe)
+    const uint8_t* bytes(uint64_t k, uint64_t es, const char* what) {
+        if (es && k > (size - pos) / es) io_fail(std::string("truncated read of ") + what);
+        const uint8_t* p = b + pos;
+        pos += k * es;
+        return p;
+    }
+};
+
+void put32(std::vector<uint8_t>& o, uint32_t v) {
+    for (int i = 0; i < 4; ++i) o.push_back(uint8_t(v >> (8 * i)));
+}
+void put64(std::vector<uint8_t>& o, uint64_t v) {
+    for (int i = 0; i < 8; ++i) o.push_back(uint8_t(v >> (8 * i)));
+}
+
+struct Pinned {  // page-locked host staging for file <-> device transfers
+    uint8_t* p = nullptr;
+    explicit Pinned(uint64_t n) {
+        if (cudaHostAlloc(reinterpret_cast<void**>(&p), std::max<uint64_t>(n, 1), cudaHostAllocDefault) !=
+            cudaSuccess) {
+            cudaGetLastError();
+            fail(PQG_ENOMEM, "pinned host allocation of " + std::to_string(n) + " bytes failed");
+        }
+    }
+    ~Pinned() {
+        if (p) cudaFreeHost(p);
+    }
+};
+
+struct File {
+    FILE* f = nullptr;
+    File(const char* path, const char* mode) : f(std::fopen(path, mode)) {}
+    ~File() {
+        if (f) std::fclose(f);
+    }
+};
+
+// whole file -> pinned host image
+std::unique_ptr<Pinned> read_file(const char* path, uint64_t* size) {
+    File f(path, "rb");
+    if (!f.f) io_fail(std::string("cannot open file: ") + path);
+    std::fseek(f.f, 0, SEEK_END);
+    const long n = std::ftell(f.f);
+    std::fseek(f.f, 0, SEEK_SET);
+    if (n < 0) io_fail(std::string("cannot open file: ") + path);
+    auto buf = std::make_unique<Pinned>(uint64_t(n));
+    if (n && std::fread(buf->p, 1, size_t(n), f.f) != size_t(n)) io_fail(std::string("cannot read file: ") + path);
+    *size = uint64_t(n);
+    return buf;
+}
+
+void write_file(const char* path, const uint8_t* p, uint64_t n) {
+    File f(path, "wb");
+    if (!f.f) io_fail(std::string("cannot open file for writing: ") + path);
+    if (n && std::fwrite(p, 1, size_t(n), f.f) != size_t(n)) io_fail(std::string("write failed: ") + path);
+    if (std::fflush(f.f) != 0) io_fail(std::string("write failed: ") + path);
+}
+
+uint64_t index_header_bytes(const pqg_index* ix) {
+    return 28 + 4 * uint64_t(ix->M) * ix->ks * ix->ds + 4 + 4 * ix->nlist * ix->D();
+}
+
+// PQII header (ivf.cpp:267-281): magic, version, embedded PQCB block, nlist, coarse
+std::vector<uint8_t> index_header(pqg_ctx* ctx, const pqg_index* ix) {
+    std::vector<uint8_t> h;
+    h.reserve(index_header_bytes(ix));
+    h.insert(h.end(), {'P', 'Q', 'I', 'I'});
+    put32(h, 1);
+    h.insert(h.end(), {'P', 'Q', 'C', 'B'});
+    put32(h, 1);
+    put32(h, ix->M);
+    put32(h, ix->ks);
+    put32(h, ix->ds);
+    const uint64_t nt = uint64_t(ix->M) * ix->ks * ix->ds, nc = ix->nlist * ix->D();
+    const size_t at = h.size();
+    h.resize(at + 4 * nt);
+    PQG_CUDA(cudaMemcpyAsync(h.data() + at, ix->tables, 4 * nt, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    put32(h, uint32_t(ix->nlist));
+    const size_t at2 = h.size();
+    h.resize(at2 + 4 * nc);
+    PQG_CUDA(cudaMemcpyAsync(h.data() + at2, ix->coarse, 4 * nc, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    return h;
+}
+
+uint64_t index_image_bytes(const pqg_index* ix) {
+    return index_header_bytes(ix) + 8 * ix->nlist + ix->n * (8 + ix->rb());
+}
+
+void serialize_index(pqg_ctx* ctx, const pqg_index* ix, uint8_t* buf) {
+    const std::vector<uint8_t> hdr = index_header(ctx, ix);
+    const uint64_t sec_bytes = 8 * ix->nlist + ix->n * (8 + ix->rb());
+    const bool dev = on_device(buf);
+    uint8_t* sec = dev ? buf + hdr.size() : scratch<uint8_t>(ctx, sec_bytes);
+    pqii_pack(ctx, ix->offsets, ix->ids, ix->codes, ix->nlist, ix->n, ix->rb(), sec);
+    if (dev) {
+        PQG_CUDA(cudaMemcpyAsync(buf, hdr.data(), hdr.size(), cudaMemcpyHostToDevice, ctx->stream));
+    } else {
+        std::memcpy(buf, hdr.data(), hdr.size());
+        PQG_CUDA(cudaMemcpyAsync(buf + hdr.size(), sec, sec_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    sync(ctx);
+}
+
+// load_index (ivf.cpp:295-355) over a host image: the header and the list
+// headers are walked on the host (one jump per list), the entries are
+// unpacked on the device.  The first error is the one the reference would
+// raise reading front to back: per list, a duplicate id while reading its
+// entries, then a code range error at its end; a truncation stops the walk.
+pqg_index* parse_index(pqg_ctx* ctx, const uint8_t* img, uint64_t size, const std::string& name) {
+    ByteReader r{img, size, 0};
+    r.magic("PQII", "index file");
+    const uint32_t ver = r.u32("version");
+    if (ver != 1) io_fail(name + ": unsupported version " + std::to_string(ver));
+    r.magic("PQCB", "embedded codebook");
+    if (r.u32("codebook version") != 1) io_fail(name + ": unsupported codebook version");
+    const uint32_t M = r.u32("M"), ks = r.u32("Ks"), ds = r.u32("sub_dim");
+    if (M == 0 || ks == 0 || ds == 0) io_fail(name + ": invalid codebook header");
+    if (uint64_t(M) * ks > (uint64_t(1) << 40) / ds) io_fail("truncated read of codebook tables");
+    const uint64_t nt = uint64_t(M) * ks * ds;
+    const float* tables = reinterpret_cast<const float*>(r.bytes(nt, 4, "codebook tables"));
+    const uint32_t nlist = r.u32("nlist");
+    if (nlist == 0) io_fail(name + ": nlist must be >= 1");
+    const uint64_t D = uint64_t(M) * ds;
+    const float* coarse = reinterpret_cast<const float*>(r.bytes(uint64_t(nlist) * D, 4, "coarse centroids"));
+    check_pq_shape(M, ks, 1, "codebook");  // make_lists -> CodeMatrix(0, M, ks) (pq.cpp:35-39)
+    const uint32_t w = code_width(ks);
+    const uint64_t rb = uint64_t(M) * w, es = 8 + rb;
+    // ---- walk the list headers
+    const uint64_t sec0 = r.pos;
+    std::vector<uint64_t> off(1, 0), src;
+    int64_t t_list = -1;
+    uint64_t t_entry = 0;
+    const char* t_what = nullptr;
+    for (uint64_t l = 0; l < nlist; ++l) {
+        if (size - r.pos < 8) {
+            t_list = int64_t(l);
+            t_what = "list length";
+            break;
+        }
+        const uint64_t len = r.u64("list length");
+        const uint64_t avail = (size - r.pos) / es;
+        src.push_back(r.pos - sec0);
+        if (len > avail) {
+            const uint64_t rem = (size - r.pos) - avail * es;
+            t_list = int64_t(l);
+            t_entry = avail;
+            t_what = rem < 8 ? "entry id" : "entry code";
+            off.push_back(off.back() + avail);
+            r.pos += avail * es;
+            break;
+        }
+        off.push_back(off.back() + len);
+        r.pos += len * es;
+    }
+    const uint64_t nl_parsed = off.size() - 1, n = off.back();
+    // ---- device: index object, entries unpacked into its CSR
+    const float* dt = in(ctx, tables, nt);
+    const float* dco = in(ctx, coarse, uint64_t(nlist) * D);
+    pqg_index* ix = new_index(ctx, M, ks, ds, nlist, n, dt, dco);
+    try {
+        const uint64_t sec_bytes = r.pos - sec0;
+        if (nl_parsed) {
+            const uint8_t* dsec = in(ctx, img + sec0, sec_bytes);
+            const uint64_t* dsrc = in(ctx, src.data(), nl_parsed);
+            const uint64_t* doff = in(ctx, off.data(), nl_parsed + 1);
+            pqii_unpack(ctx, dsec, dsrc, doff, nl_parsed, n, rb, ix->ids, ix->codes);
+        }
+        uint64_t h_dup = ~uint64_t(0);
+        unsigned long long h_bad = ~0ull;
+        if (n >= 2) {
+            uint64_t* pos = scratch<uint64_t>(ctx, 1);
+            find_duplicate(ctx, ix->ids, n, pos);
+            PQG_CUDA(cudaMemcpyAsync(&h_dup, pos, sizeof(h_dup), cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        if (n && (w == 2 || ks < 256)) {
+            unsigned long long* bad = scratch<unsigned long long>(ctx, 1);
+            first_bad_code(ctx, ix->codes, n, M, ks, w, bad);
+            PQG_CUDA(cudaMemcpyAsync(&h_bad, bad, sizeof(h_bad), cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        sync(ctx);
+        auto list_of = [&](uint64_t e) {
+            return uint64_t(std::upper_bound(off.begin(), off.end(), e) - off.begin()) - 1;
+        };
+        // event keys (list, phase, entry): entries are read (and id-checked)
+        // in phase 0, the list's codes are range-checked in phase 1
+        struct Ev {
+            uint64_t l, ph, e;
+            int kind;  // 0 dup, 1 range, 2 truncation
+        };
+        std::vector<Ev> ev;
+        if (h_dup != ~uint64_t(0)) {
+            const uint64_t l = list_of(h_dup);
+            ev.push_back({l, 0, h_dup - off[l], 0});
+        }
+        if (h_bad != ~0ull) {
+            const uint64_t l = list_of(h_bad);
+            if (!(t_list >= 0 && l == uint64_t(t_list))) ev.push_back({l, 1, 0, 1});  // a truncated list is never range-checked
+        }
+        if (t_list >= 0) ev.push_back({uint64_t(t_list), 0, t_entry, 2});
+        if (!ev.empty()) {
+            const Ev first = *std::min_element(ev.begin(), ev.end(), [](const Ev& a, const Ev& b) {
+                return std::tie(a.l, a.ph, a.e) < std::tie(b.l, b.ph, b.e);
+            });
+            if (first.kind == 0) {
+                uint64_t id = 0;
+                PQG_CUDA(cudaMemcpy(&id, ix->ids + h_dup, sizeof(id), cudaMemcpyDeviceToHost));
+                io_fail(name + ": duplicate id " + std::to_string(id));
+            }
+            if (first.kind == 1) io_fail(name + ": code out of range");
+            io_fail(std::string("truncated read of ") + t_what);
+        }
+        if (r.pos != size) io_fail(name + ": trailing data after payload");
+        PQG_CUDA(cudaMemcpyAsync(ix->offsets, off.data(), sizeof(uint64_t) * (nlist + 1), cudaMemcpyHostToDevice,
+                                 ctx->stream));
+        sync(ctx);
+    } catch (...) {
+        ix->free_all();
+        delete ix;
+        throw;
+    }
+    return ix;
+}
+
+// PQCM / PQCB headers (pq.cpp:221-232, :183-193)
+struct CodesHdr {
+    uint64_t n;
+    uint32_t M, ks;
+};
+CodesHdr codes_header(ByteReader& r, const std::string& name) {
+    r.magic("PQCM", "code file");
+    const uint32_t ver = r.u32("version");
+    if (ver != 1) io_fail(name + ": unsupported version " + std::to_string(ver));
+    CodesHdr h;
+    h.n = r.u64("row count");
+    h.M = r.u32("M");
+    h.ks = r.u32("Ks");
+    check_pq_shape(h.M, h.ks, 1, "codebook");  // CodeMatrix(n, M, ks) (pq.cpp:35-39)
+    return h;
+}
+struct CbHdr {
+    uint32_t M, ks, ds;
+};
+CbHdr codebook_header(ByteReader& r, const std::string& name) {
+    r.magic("PQCB", "codebook file");
+    const uint32_t ver = r.u32("version");
+    if (ver != 1) io_fail(name + ": unsupported version " + std::to_string(ver));
+    CbHdr h;
+    h.M = r.u32("M");
+    h.ks = r.u32("Ks");
+    h.ds = r.u32("sub_dim");
+    check_pq_shape(h.M, h.ks, h.ds, "codebook");
+    return h;
+}
+
+// the first `cap` bytes of a file (headers only)
+std::vector<uint8_t> read_head(const char* path, uint64_t cap) {
+    File f(path, "rb");
+    if (!f.f) io_fail(std::string("cannot open file: ") + path);
+    std::vector<uint8_t> v(cap);
+    v.resize(std::fread(v.data(), 1, cap, f.f));
+    return v;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pqg_index_serialize(pqg_ctx* ctx, const pqg_index* ix, void* buf, uint64_t cap, uint64_t* size) {
+    return guard([&] {
+        Scope sc(ctx);
+        if (!ix) inval("index serialize: null index");
+        const uint64_t total = index_image_bytes(ix);
+        if (size) *size = total;
+        if (!buf) return;
+        if (cap < total)
+            inval("index serialize: buffer of " + std::to_string(cap) + " bytes, image needs " + std::to_string(total));
+        serialize_index(ctx, ix, static_cast<uint8_t*>(buf));
+    });
+}
+
+int pqg_index_deserialize(pqg_ctx* ctx, const void* buf, uint64_t size, const char* name, pqg_index** out) {
+    return guard([&] {
+        Scope sc(ctx);
+        const std::string nm = name ? name : "index image";
+        const uint8_t* img = static_cast<const uint8_t*>(buf);
+        std::unique_ptr<Pinned> host;
+        if (on_device(buf)) {  // the header walk runs on the host
+            host = std::make_unique<Pinned>(size);
+            PQG_CUDA(cudaMemcpy(host->p, buf, size, cudaMemcpyDeviceToHost));
+            img = host->p;
+        }
+        *out = parse_index(ctx, img, size, nm);
+    });
+}
+
+int pqg_index_save(pqg_ctx* ctx, const pqg_index* ix, const char* path) {
+    return guard([&] {
+        Scope sc(ctx);
+        if (!ix) inval("save_index: null index");
+        const uint64_t total = index_image_bytes(ix);
+        Pinned buf(total);
+        serialize_index(ctx, ix, buf.p);
+        write_file(path, buf.p, total);
+    });
+}
+
+int pqg_index_load(pqg_ctx* ctx, const char* path, pqg_index** out) {
+    return guard([&] {
+        Scope sc(ctx);
+        uint64_t size = 0;
+        auto img = read_file(path, &size);
+        *out = parse_index(ctx, img->p, size, path);
+    });
+}
+
+int pqg_codes_save(pqg_ctx* ctx, const uint8_t* codes, uint64_t n, uint32_t M, uint32_t ks, const char* path) {
+    return guard([&] {
+        Scope sc(ctx);
+        check_pq_shape(M, ks, 1, "codebook");
+        const uint64_t payload = n * M * code_width(ks);
+        std::vector<uint8_t> h;
+        h.insert(h.end(), {'P', 'Q', 'C', 'M'});
+        put32(h, 1);
+        put64(h, n);
+        put32(h, M);
+        put32(h, ks);
+        Pinned buf(h.size() + payload);
+        std::memcpy(buf.p, h.data(), h.size());
+        if (payload) {
+            PQG_CUDA(cudaMemcpyAsync(buf.p + h.size(), codes, payload, cudaMemcpyDefault, ctx->stream));
+            sync(ctx);
+        }
+        write_file(path, buf.p, h.size() + payload);
+    });
+}
+
+int pqg_codes_file_info(const char* path, uint64_t* n, uint32_t* M, uint32_t* ks) {
+    return guard([&] {
+        const std::vector<uint8_t> head = read_head(path, 24);
+        ByteReader r{head.data(), head.size(), 0};
+        const CodesHdr h = codes_header(r, path);
+        if (n) *n = h.n;
+        if (M) *M = h.M;
+        if (ks) *ks = h.ks;
+    });
+}
+
+int pqg_codes_load(pqg_ctx* ctx, const char* path, uint8_t* codes, uint64_t cap_bytes) {
+    return guard([&] {
+        Scope sc(ctx);
+        uint64_t size = 0;
+        auto img = read_file(path, &size);
+        ByteReader r{img->p, size, 0};
+        const CodesHdr h = codes_header(r, path);
+        const uint32_t w = code_width(h.ks);
+        if (h.n > (uint64_t(1) << 48) / (uint64_t(h.M) * w)) io_fail(std::string(path) + ": truncated payload");
+        const uint64_t payload = h.n * h.M * w;
+        if (cap_bytes < payload) inval("load_codes: output buffer of " + std::to_string(cap_bytes) + " bytes < " +
+                                       std::to_string(payload));
+        if (size - r.pos < payload) io_fail(std::string(path) + ": truncated payload");
+        if (!payload) return;
+        const bool dev = on_device(codes);
+        uint8_t* d = dev ? codes : scratch<uint8_t>(ctx, payload);
+        PQG_CUDA(cudaMemcpyAsync(d, img->p + r.pos, payload, cudaMemcpyHostToDevice, ctx->stream));
+        unsigned long long* bad = scratch<unsigned long long>(ctx, 1);
+        unsigned long long hb = ~0ull;
+        first_bad_code(ctx, d, h.n, h.M, h.ks, w, bad);
+        PQG_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost, ctx->stream));
+        if (!dev) std::memcpy(codes, img->p + r.pos, payload);
+        sync(ctx);
+        if (hb != ~0ull) io_fail(std::string(path) + ": code out of range at row " + std::to_string(hb));
+    });
+}
+
+int pqg_codebook_save(pqg_ctx* ctx, const float* tables, uint32_t M, uint32_t ks, uint32_t ds, const char* path) {
+    return guard([&] {
+        Scope sc(ctx);
+        check_pq_shape(M, ks, ds, "codebook");
+        const uint64_t payload = 4 * uint64_t(M) * ks * ds;
+        std::vector<uint8_t> h;
+        h.insert(h.end(), {'P', 'Q', 'C', 'B'});
+        put32(h, 1);
+        put32(h, M);
+        put32(h, ks);
+        put32(h, ds);
+        Pinned buf(h.size() + payload);
+        std::memcpy(buf.p, h.data(), h.size());
+        PQG_CUDA(cudaMemcpyAsync(buf.p + h.size(), tables, payload, cudaMemcpyDefault, ctx->stream));
+        sync(ctx);
+        write_file(path, buf.p, h.size() + payload);
+    });
+}
+
+int pqg_codebook_file_info(const char* path, uint32_t* M, uint32_t* ks, uint32_t* ds) {
+    return guard([&] {
+        const std::vector<uint8_t> head = read_head(path, 20);
+        ByteReader r{head.data(), head.size(), 0};
+        const CbHdr h = codebook_header(r, path);
+        if (M) *M = h.M;
+        if (ks) *ks = h.ks;
+        if (ds) *ds = h.ds;
+    });
+}
+
+int pqg_codebook_load(pqg_ctx* ctx, const char* path, float* tables, uint64_t cap_floats) {
+    return guard([&] {
+        Scope sc(ctx);
+        uint64_t size = 0;
+        auto img = read_file(path, &size);
+        ByteReader r{img->p, size, 0};
+        const CbHdr h = codebook_header(r, path);
+        const uint64_t count = uint64_t(h.M) * h.ks * h.ds;
+        if (cap_floats < count)
+            inval("load_codebook: output buffer of " + std::to_string(cap_floats) + " floats < " + std::to_string(count));
+        if ((size - r.pos) / 4 < count) io_fail(std::string(path) + ": truncated payload");
+        const bool dev = on_device(tables);
+        float* d = dev ? tables : scratch<float>(ctx, count);
+        PQG_CUDA(cudaMemcpyAsync(d, img->p + r.pos, 4 * count, cudaMemcpyHostToDevice, ctx->stream));
+        unsigned long long* bad = scratch<unsigned long long>(ctx, 1);
+        unsigned long long hb = ~0ull;
+        first_nonfinite(ctx, d, count, bad);
+        PQG_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost, ctx->stream));
+        if (!dev) std::memcpy(tables, img->p + r.pos, 4 * count);
+        sync(ctx);
+        if (hb != ~0ull) io_fail(std::string(path) + ": non-finite codeword value");
     });
 }
 

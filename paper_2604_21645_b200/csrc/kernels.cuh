@@ -197,5 +197,13 @@ void find_duplicate(pqg_ctx* ctx, const uint64_t* ids, uint64_t n, uint64_t* fir
 void topk_merge_dev(pqg_ctx* ctx, const uint64_t* ids, const double* dists,
                     const uint32_t* counts, uint32_t shards, uint64_t nq, uint64_t k,
                     uint64_t* out_ids, double* out_dists, uint32_t* out_counts);
+// formats.cu: PQII list section <-> device CSR, load-time validation scans
+void pqii_pack(pqg_ctx* ctx, const uint64_t* off, const uint64_t* ids, const uint8_t* codes, uint64_t nlist,
+               uint64_t n, uint64_t rb, uint8_t* out);
+void pqii_unpack(pqg_ctx* ctx, const uint8_t* sec, const uint64_t* src_off, const uint64_t* off, uint64_t nl,
+                 uint64_t n, uint64_t rb, uint64_t* ids, uint8_t* codes);
+void first_bad_code(pqg_ctx* ctx, const uint8_t* codes, uint64_t n, uint32_t M, uint32_t ks, uint32_t w,
+                    unsigned long long* first);
+void first_nonfinite(pqg_ctx* ctx, const float* v, uint64_t count, unsigned long long* first);
 
 }  // namespace pqg

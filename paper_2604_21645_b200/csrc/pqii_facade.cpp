@@ -220,26 +220,6 @@ QueryResult result_of(const std::uint64_t* ids, const double* d, std::uint32_t c
     return r;
 }
 
-// little-endian scalar IO for the on-disk formats (pq.hpp:90-97, ivf.hpp:88-92)
-template <class T>
-void put(std::ofstream& o, T v) {
-    o.write(reinterpret_cast<const char*>(&v), sizeof(T));
-}
-template <class T>
-T get(std::ifstream& in, const std::string& path, const char* what) {
-    T v{};
-    in.read(reinterpret_cast<char*>(&v), sizeof(T));
-    if (in.gcount() != std::streamsize(sizeof(T)))
-        throw std::runtime_error(path + ": truncated " + what);
-    return v;
-}
-void magic_in(std::ifstream& in, const char* m, const std::string& path, const char* what) {
-    char b[4];
-    in.read(b, 4);
-    if (in.gcount() != 4 || std::memcmp(b, m, 4) != 0)
-        throw std::runtime_error(path + ": bad magic for " + what);
-}
-
 }  // namespace
 
 // ===========================================================================
@@ -390,65 +370,30 @@ double reconstruction_rmse(const Codebook& cb, const VectorMatrix& data) {
     return std::sqrt(sse / double(data.rows * data.dims));
 }
 
+// On-disk formats (pq.cpp:183-259) through the C ABI: byte-identical files,
+// the reference's messages; payload validation runs on the device.
 void save_codebook(const Codebook& cb, const std::string& path) {
-    std::ofstream o(path, std::ios::binary | std::ios::trunc);
-    if (!o) throw std::runtime_error("cannot open file for writing: " + path);
-    o.write("PQCB", 4);
-    put<std::uint32_t>(o, 1);
-    put(o, cb.m_subspaces);
-    put(o, cb.ks);
-    put(o, cb.sub_dim);
-    o.write(reinterpret_cast<const char*>(cb.tables.data()), std::streamsize(cb.tables.size() * 4));
-    if (!o) throw std::runtime_error("write failed: " + path);
+    raise(pqg_codebook_save(ctx(), cb.tables.data(), cb.m_subspaces, cb.ks, cb.sub_dim, path.c_str()));
 }
 
 Codebook load_codebook(const std::string& path) {
-    std::ifstream in(path, std::ios::binary);
-    if (!in) throw std::runtime_error("cannot open file: " + path);
-    magic_in(in, "PQCB", path, "codebook file");
-    const auto ver = get<std::uint32_t>(in, path, "version");
-    if (ver != 1) throw std::runtime_error(path + ": unsupported version " + std::to_string(ver));
     Codebook cb;
-    cb.m_subspaces = get<std::uint32_t>(in, path, "M");
-    cb.ks = get<std::uint32_t>(in, path, "Ks");
-    cb.sub_dim = get<std::uint32_t>(in, path, "sub_dim");
-    check_codebook_params(cb.m_subspaces, cb.ks, cb.sub_dim);
+    raise(pqg_codebook_file_info(path.c_str(), &cb.m_subspaces, &cb.ks, &cb.sub_dim));
     cb.tables.resize(std::size_t(cb.m_subspaces) * cb.ks * cb.sub_dim);
-    in.read(reinterpret_cast<char*>(cb.tables.data()), std::streamsize(cb.tables.size() * 4));
-    if (std::size_t(in.gcount()) != cb.tables.size() * 4) throw std::runtime_error(path + ": truncated payload");
-    for (float v : cb.tables)
-        if (!std::isfinite(v)) throw std::runtime_error(path + ": non-finite codeword value");
+    raise(pqg_codebook_load(ctx(), path.c_str(), cb.tables.data(), cb.tables.size()));
     return cb;
 }
 
 void save_codes(const CodeMatrix& codes, const std::string& path) {
-    std::ofstream o(path, std::ios::binary | std::ios::trunc);
-    if (!o) throw std::runtime_error("cannot open file for writing: " + path);
-    o.write("PQCM", 4);
-    put<std::uint32_t>(o, 1);
-    put<std::uint64_t>(o, codes.rows);
-    put(o, codes.m_subspaces);
-    put(o, codes.ks);
-    o.write(reinterpret_cast<const char*>(codes.bytes.data()), std::streamsize(codes.bytes.size()));
-    if (!o) throw std::runtime_error("write failed: " + path);
+    raise(pqg_codes_save(ctx(), codes.bytes.data(), codes.rows, codes.m_subspaces, codes.ks, path.c_str()));
 }
 
 CodeMatrix load_codes(const std::string& path) {
-    std::ifstream in(path, std::ios::binary);
-    if (!in) throw std::runtime_error("cannot open file: " + path);
-    magic_in(in, "PQCM", path, "code file");
-    const auto ver = get<std::uint32_t>(in, path, "version");
-    if (ver != 1) throw std::runtime_error(path + ": unsupported version " + std::to_string(ver));
-    const auto n = get<std::uint64_t>(in, path, "row count");
-    const auto m = get<std::uint32_t>(in, path, "M");
-    const auto ks = get<std::uint32_t>(in, path, "Ks");
+    std::uint64_t n = 0;
+    std::uint32_t m = 0, ks = 0;
+    raise(pqg_codes_file_info(path.c_str(), &n, &m, &ks));
     CodeMatrix codes(std::size_t(n), m, ks);
-    in.read(reinterpret_cast<char*>(codes.bytes.data()), std::streamsize(codes.bytes.size()));
-    if (std::size_t(in.gcount()) != codes.bytes.size()) throw std::runtime_error(path + ": truncated payload");
-    for (std::size_t i = 0; i < codes.rows; ++i)
-        for (std::uint32_t s = 0; s < m; ++s)
-            if (codes.at(i, s) >= ks)
-                throw std::runtime_error(path + ": code out of range at row " + std::to_string(i));
+    raise(pqg_codes_load(ctx(), path.c_str(), codes.bytes.data(), codes.bytes.size()));
     return codes;
 }
 
@@ -582,79 +527,28 @@ QueryResult flat_scan(const Codebook& cb, const CodeMatrix& codes,
     return result_of(oi.data(), od.data(), cnt, k);
 }
 
+// PQII (ivf.cpp:264-355): the device index (cached upload) is packed into the
+// file image by the device; loading unpacks the lists into a device CSR,
+// checks ids and codes there, and exports the reference's host structure.
 void save_index(const InvertedIndex& index, const std::string& path) {
-    std::ofstream o(path, std::ios::binary | std::ios::trunc);
-    if (!o) throw std::runtime_error("cannot open file for writing: " + path);
-    o.write("PQII", 4);
-    put<std::uint32_t>(o, 1);
-    o.write("PQCB", 4);
-    put<std::uint32_t>(o, 1);
-    put(o, index.codebook.m_subspaces);
-    put(o, index.codebook.ks);
-    put(o, index.codebook.sub_dim);
-    o.write(reinterpret_cast<const char*>(index.codebook.tables.data()),
-            std::streamsize(index.codebook.tables.size() * 4));
-    put<std::uint32_t>(o, std::uint32_t(index.nlist()));
-    o.write(reinterpret_cast<const char*>(index.coarse_centroids.values.data()),
-            std::streamsize(index.coarse_centroids.values.size() * 4));
-    for (const auto& pl : index.lists) {
-        put<std::uint64_t>(o, pl.ids.size());
-        const std::size_t rb = pl.codes.row_bytes();
-        for (std::size_t i = 0; i < pl.ids.size(); ++i) {
-            put<std::uint64_t>(o, pl.ids[i]);
-            o.write(reinterpret_cast<const char*>(pl.codes.bytes.data() + i * rb), std::streamsize(rb));
-        }
-    }
-    if (!o) throw std::runtime_error("write failed: " + path);
+    IndexPtr dev = device_index_for(index);
+    raise(pqg_index_save(ctx(), dev.get(), path.c_str()));
 }
 
 InvertedIndex load_index(const std::string& path) {
-    std::ifstream in(path, std::ios::binary);
-    if (!in) throw std::runtime_error("cannot open file: " + path);
-    magic_in(in, "PQII", path, "index file");
-    if (get<std::uint32_t>(in, path, "version") != 1) throw std::runtime_error(path + ": unsupported version");
-    magic_in(in, "PQCB", path, "embedded codebook");
-    if (get<std::uint32_t>(in, path, "codebook version") != 1)
-        throw std::runtime_error(path + ": unsupported codebook version");
-    InvertedIndex ix;
-    ix.codebook.m_subspaces = get<std::uint32_t>(in, path, "M");
-    ix.codebook.ks = get<std::uint32_t>(in, path, "Ks");
-    ix.codebook.sub_dim = get<std::uint32_t>(in, path, "sub_dim");
-    if (!ix.codebook.m_subspaces || !ix.codebook.ks || !ix.codebook.sub_dim)
-        throw std::runtime_error(path + ": invalid codebook header");
-    ix.codebook.tables.resize(std::size_t(ix.codebook.m_subspaces) * ix.codebook.ks * ix.codebook.sub_dim);
-    in.read(reinterpret_cast<char*>(ix.codebook.tables.data()), std::streamsize(ix.codebook.tables.size() * 4));
-    if (std::size_t(in.gcount()) != ix.codebook.tables.size() * 4) throw std::runtime_error(path + ": truncated codebook tables");
-    const auto nlist = get<std::uint32_t>(in, path, "nlist");
-    if (nlist == 0) throw std::runtime_error(path + ": nlist must be >= 1");
-    ix.coarse_centroids = VectorMatrix(nlist, ix.codebook.dims());
-    in.read(reinterpret_cast<char*>(ix.coarse_centroids.values.data()),
-            std::streamsize(ix.coarse_centroids.values.size() * 4));
-    if (std::size_t(in.gcount()) != ix.coarse_centroids.values.size() * 4)
-        throw std::runtime_error(path + ": truncated coarse centroids");
-    ix.lists.resize(nlist);
-    for (auto& pl : ix.lists) {
-        pl.codes = CodeMatrix(0, ix.codebook.m_subspaces, ix.codebook.ks);
-        const auto len = get<std::uint64_t>(in, path, "list length");
-        const std::size_t rb = pl.codes.row_bytes();
-        pl.ids.resize(len);
-        pl.codes.bytes.resize(len * rb);
-        pl.codes.rows = len;
-        for (std::size_t i = 0; i < len; ++i) {
-            pl.ids[i] = get<std::uint64_t>(in, path, "entry id");
-            in.read(reinterpret_cast<char*>(pl.codes.bytes.data() + i * rb), std::streamsize(rb));
-            if (std::size_t(in.gcount()) != rb) throw std::runtime_error(path + ": truncated entry code");
-            if (!ix.id_set.insert(pl.ids[i]).second)
-                throw std::runtime_error(path + ": duplicate id " + std::to_string(pl.ids[i]));
-        }
-        for (std::size_t i = 0; i < len; ++i)
-            for (std::uint32_t m = 0; m < ix.codebook.m_subspaces; ++m)
-                if (pl.codes.at(i, m) >= ix.codebook.ks) throw std::runtime_error(path + ": code out of range");
-        ix.n_items += len;
-    }
-    char extra;
-    if (in.read(&extra, 1); in.gcount() != 0) throw std::runtime_error(path + ": trailing data after payload");
-    return ix;
+    pqg_index* h = nullptr;
+    raise(pqg_index_load(ctx(), path.c_str(), &h));
+    IndexPtr dev(h, IndexDeleter());
+    std::uint64_t nlist = 0, n = 0;
+    std::uint32_t M = 0, ks = 0, ds = 0;
+    raise(pqg_index_info(h, &nlist, &n, &M, &ks, &ds));
+    Codebook cb;
+    cb.m_subspaces = M;
+    cb.ks = ks;
+    cb.sub_dim = ds;
+    cb.tables.resize(std::size_t(M) * ks * ds);
+    raise(pqg_index_export(ctx(), h, nullptr, nullptr, nullptr, nullptr, cb.tables.data()));
+    return to_host(h, cb);
 }
 
 // ===========================================================================

@@ -853,8 +853,10 @@ void launch_umma(pqg_ctx* ctx, const NearestArgs& a) {
     // tools/screen_bench.py at 1M x 128, Ks=256: Ds=8 1.92 -> 1.38 ms, Ds=4
     // 3.76 -> 3.10 ms against the pipelined kernel; at Ds=16, where only 3 CTAs
     // fit, the second MMA round costs more than the extra CTA gains: 0.87 -> 1.12)
+    // r2 (new epilogue, 7-MMA tiles): the split wins at Ds = 16 too
+    // (M=8 Ks=256 encode 0.69 -> 0.65 ms) and is neutral elsewhere
     uint32_t n_mma = n_pad;
-    if (n_pad > 128 && smem_lim >= 4) n_mma = 128;
+    if (n_pad > 128) n_mma = 128;
     if (const char* se = std::getenv("PQG_UMMA_SPLIT")) n_mma = se[0] == '1' && n_pad > 128 ? 128 : n_pad;
     uint32_t cols = 32;
     while (cols < n_mma) cols <<= 1;

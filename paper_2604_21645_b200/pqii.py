@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import threading
 import time
 from dataclasses import dataclass, field
@@ -583,6 +584,86 @@ def ivf_merge(a: InvertedIndex, b: InvertedIndex) -> InvertedIndex:
     h = C.c_void_p()
     _lib.check(a.ctx.lib.pqg_index_merge(a.ctx.h, a.h, b.h, C.byref(h)), "ivf_merge")
     return InvertedIndex(h, a.ctx)
+
+
+# ---------------------------------------------------------------------------
+# on-disk formats (pq.cpp:183-259, ivf.cpp:264-355): byte-identical files,
+# posting lists packed / unpacked and validated on the device
+# ---------------------------------------------------------------------------
+
+
+def save_index(index: InvertedIndex, path: str) -> None:
+    """save_index (ivf.cpp:264-293)."""
+    _lib.check(index.ctx.lib.pqg_index_save(index.ctx.h, index.h, os.fsencode(path)), "save_index")
+
+
+def load_index(path: str, ctx: Context | None = None) -> InvertedIndex:
+    """load_index (ivf.cpp:295-355): device-resident index straight from the file."""
+    ctx = ctx or get_context()
+    h = C.c_void_p()
+    _lib.check(ctx.lib.pqg_index_load(ctx.h, os.fsencode(path), C.byref(h)), "load_index")
+    return InvertedIndex(h, ctx)
+
+
+def serialize_index(index: InvertedIndex) -> bytes:
+    """The PQII file image of ``index`` in memory."""
+    n = C.c_uint64()
+    _lib.check(index.ctx.lib.pqg_index_serialize(index.ctx.h, index.h, None, 0, C.byref(n)), "serialize")
+    buf = np.empty(n.value, np.uint8)
+    _lib.check(index.ctx.lib.pqg_index_serialize(index.ctx.h, index.h, buf.ctypes.data_as(C.c_void_p), n.value,
+                                                 C.byref(n)), "serialize")
+    return buf.tobytes()
+
+
+def deserialize_index(image, name: str = "index image", ctx: Context | None = None) -> InvertedIndex:
+    """load_index over an in-memory PQII image (bytes, numpy u8 or a CUDA tensor)."""
+    ctx = ctx or get_context()
+    if isinstance(image, (bytes, bytearray)):
+        image = np.frombuffer(image, np.uint8)
+    ip, _keep = _ptr(image)
+    nbytes = int(image.nbytes) if hasattr(image, "nbytes") else int(image.numel() * image.element_size())
+    h = C.c_void_p()
+    _lib.check(ctx.lib.pqg_index_deserialize(ctx.h, ip, nbytes, name.encode(), C.byref(h)), "deserialize")
+    return InvertedIndex(h, ctx)
+
+
+def save_codes(codes: CodeMatrix, path: str, ctx: Context | None = None) -> None:
+    """save_codes (pq.cpp:221-232)."""
+    ctx = ctx or get_context()
+    cp, _k = _ptr(codes.bytes)
+    _lib.check(ctx.lib.pqg_codes_save(ctx.h, cp, codes.rows, codes.m_subspaces, codes.ks, os.fsencode(path)),
+               "save_codes")
+
+
+def load_codes(path: str, ctx: Context | None = None) -> CodeMatrix:
+    """load_codes (pq.cpp:234-259): every code range-checked on the device."""
+    ctx = ctx or get_context()
+    n, M, ks = C.c_uint64(), C.c_uint32(), C.c_uint32()
+    _lib.check(ctx.lib.pqg_codes_file_info(os.fsencode(path), C.byref(n), C.byref(M), C.byref(ks)), "load_codes")
+    out = np.empty((n.value, M.value * code_width(ks.value)), np.uint8)
+    _lib.check(ctx.lib.pqg_codes_load(ctx.h, os.fsencode(path), out.ctypes.data_as(C.c_void_p), out.nbytes),
+               "load_codes")
+    return CodeMatrix(n.value, M.value, ks.value, out)
+
+
+def save_codebook(cb: Codebook, path: str, ctx: Context | None = None) -> None:
+    """save_codebook (pq.cpp:183-194)."""
+    ctx = ctx or get_context()
+    tp, _k = _ptr(_f32(cb.tables))
+    _lib.check(ctx.lib.pqg_codebook_save(ctx.h, tp, cb.m_subspaces, cb.ks, cb.sub_dim, os.fsencode(path)),
+               "save_codebook")
+
+
+def load_codebook(path: str, ctx: Context | None = None) -> Codebook:
+    """load_codebook (pq.cpp:196-219): codewords checked finite on the device."""
+    ctx = ctx or get_context()
+    M, ks, ds = C.c_uint32(), C.c_uint32(), C.c_uint32()
+    _lib.check(ctx.lib.pqg_codebook_file_info(os.fsencode(path), C.byref(M), C.byref(ks), C.byref(ds)),
+               "load_codebook")
+    t = np.empty((M.value, ks.value, ds.value), np.float32)
+    _lib.check(ctx.lib.pqg_codebook_load(ctx.h, os.fsencode(path), t.ctypes.data_as(C.c_void_p), t.size),
+               "load_codebook")
+    return Codebook(M.value, ks.value, ds.value, t)
 
 
 def ivf_query_batch(index: InvertedIndex, queries, k: int, nprobe: int, max_sq_dist=None,

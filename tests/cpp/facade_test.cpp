@@ -2,8 +2,11 @@
 // test_pq.cpp, test_ivf.cpp) restated against the drop-in libpqg_pqii.so
 // through the pqii headers of this repo.  A tiny CHECK harness replaces the
 // absent doctest.  Run by tests/test_facade_cpp.py on a GPU.
+#include <unistd.h>
+
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <random>
@@ -279,6 +282,80 @@ int main() {
         for (std::size_t j = 1; j < sat2.hits.size(); ++j)
             CHECK(sat2.hits[j - 1].sq_dist < sat2.hits[j].sq_dist ||
                   (sat2.hits[j - 1].sq_dist == sat2.hits[j].sq_dist && sat2.hits[j - 1].id < sat2.hits[j].id));
+    }
+    // ---- test_pq.cpp:302-329 "codebook and code files round-trip", and
+    // ---- test_ivf.cpp:357-407 "index serialization round-trips bit-exactly"
+    {
+        const std::string dir = std::string(std::getenv("TMPDIR") ? std::getenv("TMPDIR") : "/tmp") + "/pqg_fmt_" +
+                                std::to_string(::getpid());
+        if (std::system(("mkdir -p " + dir).c_str()) != 0) std::printf("mkdir failed\n");
+        auto read_file = [](const std::string& p) {
+            std::FILE* f = std::fopen(p.c_str(), "rb");
+            std::string out;
+            if (!f) return out;
+            char buf[4096];
+            std::size_t n;
+            while ((n = std::fread(buf, 1, sizeof(buf), f)) > 0) out.append(buf, n);
+            std::fclose(f);
+            return out;
+        };
+        auto write_file = [](const std::string& p, const std::string& b) {
+            std::FILE* f = std::fopen(p.c_str(), "wb");
+            std::fwrite(b.data(), 1, b.size(), f);
+            std::fclose(f);
+        };
+        const VectorMatrix data = random_matrix(64, 8, 3);
+        const Codebook cb = pq_fit(data, 4, 8, 10, 5);
+        save_codebook(cb, dir + "/cb.pqcb");
+        CHECK(load_codebook(dir + "/cb.pqcb") == cb);
+        const CodeMatrix codes = pq_encode(cb, data);
+        save_codes(codes, dir + "/codes.pqcm");
+        CHECK(load_codes(dir + "/codes.pqcm") == codes);
+        save_codebook(load_codebook(dir + "/cb.pqcb"), dir + "/cb2.pqcb");
+        CHECK(read_file(dir + "/cb2.pqcb") == read_file(dir + "/cb.pqcb"));
+        std::string bytes = read_file(dir + "/cb.pqcb");
+        bytes[1] = 'x';
+        write_file(dir + "/bad.pqcb", bytes);
+        CHECK_THROWS_WITH(load_codebook(dir + "/bad.pqcb"), std::runtime_error, "bad magic");
+
+        // byte codes (Ks <= 256): make_fixture(150, 61) shape -- 16-d data, M=4, Ks=16
+        const VectorMatrix d16 = random_matrix(150, 16, 61, -10, 10);
+        const Codebook cb16 = pq_fit(d16, 4, 16, 15, 3);
+        const CodeMatrix c16 = pq_encode(cb16, d16);
+        std::vector<std::uint64_t> ids16(150);
+        std::iota(ids16.begin(), ids16.end(), std::uint64_t{0});
+        const InvertedIndex index = ivf_build(cb16, c16, ids16, 10, 67);
+        save_index(index, dir + "/a.pqii");
+        const InvertedIndex loaded = load_index(dir + "/a.pqii");
+        save_index(loaded, dir + "/b.pqii");
+        CHECK(read_file(dir + "/a.pqii") == read_file(dir + "/b.pqii"));
+        CHECK(loaded.n_items == index.n_items);
+        CHECK(loaded.codebook == index.codebook);
+        CHECK(loaded.coarse_centroids == index.coarse_centroids);
+        CHECK(loaded.id_set.size() == index.id_set.size());
+        const VectorMatrix q = random_matrix(1, 16, 9);
+        CHECK(ivf_query(loaded, q.row_span(0), 5, 10).hits == ivf_query(index, q.row_span(0), 5, 10).hits);
+        // wide codes (Ks > 256)
+        const VectorMatrix dw = random_matrix(600, 8, 71, -10, 10);
+        const Codebook cbw = pq_fit(dw, 2, 300, 8, 3);
+        const CodeMatrix cw = pq_encode(cbw, dw);
+        CHECK(cw.code_width() == 2);
+        std::vector<std::uint64_t> idw(600);
+        std::iota(idw.begin(), idw.end(), std::uint64_t{0});
+        const InvertedIndex iw = ivf_build(cbw, cw, idw, 5, 7);
+        save_index(iw, dir + "/wide.pqii");
+        const InvertedIndex lw = load_index(dir + "/wide.pqii");
+        CHECK(lw.codebook == iw.codebook);
+        for (std::size_t l = 0; l < iw.nlist(); ++l) {
+            CHECK(lw.lists[l].ids == iw.lists[l].ids);
+            CHECK(lw.lists[l].codes == iw.lists[l].codes);
+        }
+        // bad magic
+        std::string ib = read_file(dir + "/a.pqii");
+        ib[0] = 'Z';
+        write_file(dir + "/bad.pqii", ib);
+        CHECK_THROWS_WITH(load_index(dir + "/bad.pqii"), std::runtime_error, "bad magic");
+        if (std::system(("rm -rf " + dir).c_str()) != 0) std::printf("rm failed\n");
     }
     // ---- test_pipeline.cpp
     {   // train_chunk :44-92
