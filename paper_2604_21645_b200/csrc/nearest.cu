@@ -29,6 +29,8 @@
 #include <cstdio>
 
 #include "kernels.cuh"
+#include "tc_common.cuh"
+#include "tmap.cuh"
 
 namespace pqg {
 
@@ -605,22 +607,289 @@ __global__ void __launch_bounds__(kSmallThreads) small_table_kernel(NearestArgs 
     }
 }
 
-// Narrow codebooks, register-resident (Ks <= 64, Ds in {4, 8, 16, 32}): the
-// codebook lives in REGISTERS, split over lanes.  Lane l owns one (subspace
-// s, part g) task -- codewords g*KS/G .. (g+1)*KS/G - 1 of subspace s, at most
-// 128 floats -- for the whole kernel, so the inner loop reads no memory at
-// all: per codeword Ds FMAs on the row's register-resident sub-vector and a
-// running top-2.  A row's M*G tasks are LG consecutive lanes (LG <= 32: a warp
-// covers 32/LG rows per step; LG = 64: two warps share each row), so the
-// x loads of a warp step are whole consecutive rows, fully coalesced; the G
-// lanes of a (row, subspace) merge their top-2 with shuffles and the group's
-// first lane writes the code (consecutive subspaces -> consecutive bytes).
-// Screened value, bound and fixup hand-off are small_table_kernel's.
+// Row-blocked screen for narrow codebooks (r2): Ks <= 32, Ds in {4, 8, 16, 32}.
+// The whole codebook sits in shared memory.  A warp owns 64-row blocks (lane
+// L: rows L and L+32); the rows reach shared memory by 2-D TMA, one box of
+// 64 rows x 32 floats (SG = 32/Ds subspaces) at a time, 128-byte swizzled so
+// a lane reading its row's 16-byte chunks hits distinct bank groups, double-
+// buffered per warp (the next box is in flight while this one is screened:
+// per-subspace 16-byte row slices read straight from HBM left the kernel
+// latency- and L2-bound).  Per codeword pair a lane reads the two codewords
+// once (broadcast LDS.128) for both rows and advances them together with
+// packed FFMA2 (the rows in the two halves, the codeword coordinate as the
+// scalar operand); keys are value_bits * 32 + j (one IMAD, the per-row offset
+// window of the register-resident kernel below), five ALU min/max per
+// codeword pair and row.  Bound and fixup hand-off as in small_table_kernel.
+constexpr int kRowWarps = 4;
+constexpr int kRowRows = 64;  // rows per warp block
+
+template <int DS, int KS, bool PADK>
+__global__ void __launch_bounds__(kRowWarps * 32) row_screen_kernel(NearestArgs a, uint32_t m32,
+                                                                    const __grid_constant__ CUtensorMap xmap) {
+    extern __shared__ __align__(1024) uint8_t smem_rs[];
+    constexpr int KP = KS / 2;
+    constexpr int SG = 32 / DS;          // subspaces per staged box
+    constexpr uint32_t BOX = kRowRows * 128;  // bytes per box
+    constexpr float kE = 2.f * float(DS + 4) * kU;
+    __shared__ uint64_t bars[kRowWarps][2];
+    const uint32_t B = a.B;
+    const uint32_t k = uint32_t(a.k);
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint8_t* xbuf = smem_rs + size_t(warp) * 2 * BOX;                                   // [2][64][128 B]
+    float* st = reinterpret_cast<float*>(smem_rs + size_t(kRowWarps) * 2 * BOX);      // [B][KS][DS]
+    float* cn_s = st + size_t(B) * KS * DS;                                            // [B][KS]
+    for (uint32_t e = threadIdx.x; e < B * KS * DS; e += blockDim.x) {
+        const uint32_t b = e / (KS * DS), r = e - b * (KS * DS), j = r / DS;
+        st[e] = j < k ? __ldg(a.table + (uint64_t(b) * k + j) * DS + (r - j * DS)) : 0.f;
+    }
+    for (uint32_t e = threadIdx.x; e < B * KS; e += blockDim.x) {
+        const uint32_t b = e / KS, j = e - b * KS;
+        cn_s[e] = j < k ? __ldg(a.cnorm + uint64_t(b) * k + j) : 0.f;
+    }
+    if (lane == 0) {
+        tc::bar_init(&bars[warp][0], 1);
+        tc::bar_init(&bars[warp][1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint64_t nblk = (a.n + kRowRows - 1) / kRowRows;
+    const uint32_t ngrp = (B + SG - 1) / SG;
+    const uint64_t w0 = uint64_t(blockIdx.x) * kRowWarps + warp, wstep = uint64_t(gridDim.x) * kRowWarps;
+    // the warp's sequence of (block, group) boxes; box i goes to buffer i & 1
+    auto issue = [&](uint64_t i) {
+        const uint64_t blk = w0 + (i / ngrp) * wstep;
+        if (blk >= nblk) return;
+        const uint32_t g = uint32_t(i % ngrp);
+        uint64_t* bar = &bars[warp][i & 1];
+        tc::bar_expect_tx(bar, BOX);
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+            :: "r"(tc::smem_u32(xbuf + (i & 1) * BOX)), "l"(reinterpret_cast<uint64_t>(&xmap)),
+               "r"(int(g * SG * DS)), "r"(int(blk * kRowRows)), "r"(tc::smem_u32(bar)) : "memory");
+    };
+    if (lane == 0) issue(0);
+    for (uint64_t i = 0;; ++i) {
+        const uint64_t blk = w0 + (i / ngrp) * wstep;
+        if (blk >= nblk) break;
+        const uint32_t g = uint32_t(i % ngrp);
+        if (lane == 0) issue(i + 1);  // its buffer was released by the __syncwarp of box i - 1
+        tc::bar_wait(&bars[warp][i & 1], uint32_t(i >> 1) & 1u);
+        const uint8_t* xb = xbuf + (i & 1) * BOX;
+        const uint64_t row0 = blk * kRowRows + lane, row1 = row0 + 32;
+        const bool on0 = row0 < a.n, on1 = row1 < a.n;
+        for (uint32_t sj = 0; sj < SG; ++sj) {
+            const uint32_t b = g * SG + sj;
+            if (b >= B) break;
+            if (a.active && !a.active[b]) continue;
+            // the two rows' sub-vectors (swizzled chunks c ^ (row & 7)), as -2x pairs
+            float2 xa[DS];
+            float nxa = 0.f, nxb = 0.f;
+#pragma unroll
+            for (int q = 0; q < DS / 4; ++q) {
+                const uint32_t c = sj * (DS / 4) + q;
+                const float4 u = *reinterpret_cast<const float4*>(xb + lane * 128 + ((c ^ (lane & 7)) << 4));
+                const float4 v = *reinterpret_cast<const float4*>(xb + (lane + 32) * 128 + ((c ^ (lane & 7)) << 4));
+                const float uu[4] = {-2.f * u.x, -2.f * u.y, -2.f * u.z, -2.f * u.w};
+                const float vv[4] = {-2.f * v.x, -2.f * v.y, -2.f * v.z, -2.f * v.w};
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    xa[4 * q + w] = make_float2(uu[w], vv[w]);
+                    nxa = fmaf(uu[w], uu[w], nxa);
+                    nxb = fmaf(vv[w], vv[w], nxb);
+                }
+            }
+            const float cm = a.cmax[b];
+            float E[2], Cc[2];
+            uint32_t hi4[2];
+#pragma unroll
+            for (int i2 = 0; i2 < 2; ++i2) {
+                const float nx = 0.25f * (i2 ? nxb : nxa);
+                const float S = 2.f * (nx * (1.f + 1e-6f) + cm * cm) + 1e-6f;
+                int e = int((__float_as_uint(S) >> 23) & 0xFF) - 127;
+                e = max(-60, min(e, 100));
+                const int pw = (e & ~15) + 1;  // smallest p >= e - 14 with p = 1 (mod 16)
+                const float O = __uint_as_float(uint32_t(pw + 127) << 23);
+                hi4[i2] = uint32_t(pw + 127) >> 4;
+                E[i2] = kE * (S + O) * 1.001f + 1e-30f;
+                Cc[i2] = nx * (1.f + 2.f * float(DS + 2) * kU) + 2.f * E[i2] + O;
+            }
+            const float2 C2 = make_float2(Cc[0], Cc[1]);
+            uint32_t m1[2][2], m2[2][2];
+#pragma unroll
+            for (int i2 = 0; i2 < 2; ++i2) m1[i2][0] = m1[i2][1] = m2[i2][0] = m2[i2][1] = 0xFFFFFFFFu;
+            const float* tb = st + size_t(b) * KS * DS;
+            const float* cnb = cn_s + size_t(b) * KS;
+#pragma unroll
+            for (int p = 0; p < KP; ++p) {
+                const float2 cnp = *reinterpret_cast<const float2*>(cnb + 2 * p);
+                float2 a0 = __fadd2_rn(C2, make_float2(cnp.x, cnp.x));
+                float2 a1 = __fadd2_rn(C2, make_float2(cnp.y, cnp.y));
+#pragma unroll
+                for (int t = 0; t < DS; t += 4) {
+                    const float4 c0 = *reinterpret_cast<const float4*>(tb + (2 * p) * DS + t);
+                    const float4 c1 = *reinterpret_cast<const float4*>(tb + (2 * p + 1) * DS + t);
+                    const float v0[4] = {c0.x, c0.y, c0.z, c0.w}, v1[4] = {c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        a0 = __ffma2_rn(xa[t + q], make_float2(v0[q], v0[q]), a0);
+                        a1 = __ffma2_rn(xa[t + q], make_float2(v1[q], v1[q]), a1);
+                    }
+                }
+                const float r0[2] = {a0.x, a0.y}, r1[2] = {a1.x, a1.y};
+#pragma unroll
+                for (int i2 = 0; i2 < 2; ++i2) {
+                    uint32_t ka, kb;
+                    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(ka) : "r"(__float_as_uint(r0[i2])), "r"(m32), "r"(2 * p));
+                    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(kb) : "r"(__float_as_uint(r1[i2])), "r"(m32), "r"(2 * p + 1));
+                    if constexpr (PADK) {
+                        ka = uint32_t(2 * p) < k ? ka : 0xFFFFFFFFu;
+                        kb = uint32_t(2 * p + 1) < k ? kb : 0xFFFFFFFFu;
+                    }
+                    const uint32_t lo = min(ka, kb), hi = max(ka, kb);
+                    m2[i2][p & 1] = min(m2[i2][p & 1], min(max(m1[i2][p & 1], lo), hi));
+                    m1[i2][p & 1] = min(m1[i2][p & 1], lo);
+                }
+            }
+#pragma unroll
+            for (int i2 = 0; i2 < 2; ++i2) {
+                const uint64_t row = i2 ? row1 : row0;
+                if (!(i2 ? on1 : on0)) continue;
+                const uint32_t k1 = min(m1[i2][0], m1[i2][1]);
+                const uint32_t k2 = min(min(m2[i2][0], m2[i2][1]), max(m1[i2][0], m1[i2][1]));
+                const uint32_t i1 = k1 & 31u;
+                bool unique = false;
+                if (isfinite(E[i2]) && k1 != 0xFFFFFFFFu) {
+                    if (k2 == 0xFFFFFFFFu) {
+                        unique = true;
+                    } else {
+                        const float f1 = __uint_as_float((k1 >> 5) | (hi4[i2] << 27));
+                        const float f2 = __uint_as_float((k2 >> 5) | (hi4[i2] << 27));
+                        unique = f2 - f1 > 2.05f * E[i2];
+                    }
+                }
+                if (unique && i1 < k) {
+                    store_index(a, row, b, i1);
+                    if (a.out_dist) {  // -0.5 * (-2x) == x exactly
+                        const float* c = tb + i1 * DS;
+                        double accd = 0.0;
+#pragma unroll
+                        for (int t = 0; t < DS; ++t) {
+                            const float xv = -0.5f * (i2 ? xa[t].y : xa[t].x);
+                            const double diff = __dsub_rn((double)xv, (double)c[t]);
+                            accd = __dadd_rn(accd, __dmul_rn(diff, diff));
+                        }
+                        a.out_dist[uint64_t(b) * a.n + row] = accd;
+                    }
+                } else {
+                    const unsigned long long slot = atomicAdd(a.flag_count, 1ull);
+                    a.flags[slot] = (uint64_t(b) << 40) | row;
+                }
+            }
+        }
+        __syncwarp();  // every lane is done with buffer i & 1 before box i + 2 lands there
+    }
+}
+
+bool row_screen_supported(const NearestArgs& a) {
+    const char* e = std::getenv("PQG_ROWSCREEN");
+    if (e && e[0] == '0') return false;
+    // measured r2 (1M x 128 encodes): the register-resident narrow kernel
+    // keeps Ds = 4 (M=32 Ks=16: 0.32 vs 0.37 ms); this one wins at Ds >= 8
+    // (M=16: 0.26 vs 0.32, M=8: 0.20 vs 0.33 / tcgen05 0.24, M=4: 0.18 vs 0.26)
+    if (a.d == 4 && !(e && e[0] == '1')) return false;
+    if (a.src.codes || a.sse_part || a.out_mat) return false;
+    if (!(a.d == 4 || a.d == 8 || a.d == 16 || a.d == 32) || a.k < 2 || a.k > 32) return false;
+    // the TMA box walks the rows' subspace columns: the standard row layout
+    if (a.src.col_stride != a.d || a.src.ldx != uint64_t(a.B) * a.d || (a.src.ldx * 4) % 16 != 0 ||
+        (reinterpret_cast<uintptr_t>(a.src.x) & 15u) != 0 || a.n >= (uint64_t(1) << 31))
+        return false;
+    const uint64_t KS = a.k <= 16 ? 16 : 32;
+    return uint64_t(a.B) * KS * (a.d + 1) * sizeof(float) + 2ull * kRowWarps * kRowRows * 128 <= 220 * 1024;
+}
+
+void row_screen(pqg_ctx* ctx, const NearestArgs& a) {
+    const uint32_t KS = a.k <= 16 ? 16 : 32;
+    const size_t smem = size_t(2) * kRowWarps * kRowRows * 128 + size_t(a.B) * KS * (a.d + 1) * sizeof(float);
+    CUtensorMap xmap;
+    if (!encode_rows_map(&xmap, a.src.x, a.n, a.src.ldx, kRowRows, 32, CU_TENSOR_MAP_SWIZZLE_128B))
+        fail(PQG_ECUDA, "row_screen: tensor map encoding failed");
+    const uint64_t nblk = (a.n + kRowRows - 1) / kRowRows;
+    const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((nblk + kRowWarps - 1) / kRowWarps,
+                                                                         uint64_t(ctx->num_sms) * 3)));
+    auto go = [&](auto kern) {
+        set_smem(kern, smem);
+        launch(ctx, "nearest_rows", kern, dim3(grid), dim3(kRowWarps * 32), smem, a, 32u, xmap);
+    };
+    const bool pad = a.k != KS;
+    auto pick = [&](auto ds_tag) {
+        constexpr int DS = decltype(ds_tag)::value;
+        if (KS == 16) pad ? go(row_screen_kernel<DS, 16, true>) : go(row_screen_kernel<DS, 16, false>);
+        else pad ? go(row_screen_kernel<DS, 32, true>) : go(row_screen_kernel<DS, 32, false>);
+    };
+    if (a.d == 4) pick(std::integral_constant<int, 4>());
+    else if (a.d == 8) pick(std::integral_constant<int, 8>());
+    else if (a.d == 16) pick(std::integral_constant<int, 16>());
+    else pick(std::integral_constant<int, 32>());
+}
+
+// Narrow sub-vectors, register-resident codebook (r2): Ds in {4, 8, 16},
+// Ks <= 256.  The codebook lives in REGISTERS, split over lanes: lane l owns
+// one (subspace s, part g) task -- codewords g*KL .. (g+1)*KL - 1 of subspace
+// s, KL*Ds <= 128 floats -- for the whole kernel, so the inner loop reads no
+// memory.  A row's M*G tasks are LG consecutive lanes (LG <= 32: a warp covers
+// 32/LG rows per step; LG > 32: LG/32 warps share each row), so the x loads of
+// a warp step are whole consecutive rows, fully coalesced; the G lanes of a
+// (row, subspace) merge their top-2 with shuffles and the group's first lane
+// writes the code (consecutive subspaces -> consecutive bytes).
+//
+// Per codeword pair the lane issues Ds/2... no: Ds packed FFMA2 (two
+// codewords per instruction, __ffma2_rn: the FP32 pipe's two-wide form), one
+// FADD2 for the start value, one IMAD per key and five ALU min/max for the
+// running (best, second): ~(Ds + 6)/2 instructions per (row, codeword) where
+// the r1 kernel needed Ds + 6.  Keys are value_bits * 32 + local index (one
+// IMAD with an immediate): a per-row offset 2^p inside C puts every screened
+// value of the row in [2^p, 2^(p+16)) (p = 1 mod 16; see umma.cu row_prep), so
+// the dropped bits 31..27 are constant and the 27 kept value bits are exact.
+// Screened value and bound: small_table_kernel's acc_j = (C_r + ||c_j||^2) +
+// sum_t (-2x_t) c_jt (fma chain), E = 2 (Ds+4) u S with S >= every partial
+// sum's magnitude (offset included); a row whose runner-up is within 2.05 E of
+// its best goes to the exact fixup.
 constexpr int kNarrowThreads = 256;
-template <int DS, int KS, int G>
-__global__ void __launch_bounds__(kNarrowThreads, (DS <= 4 && KS <= 16) ? 2 : 1) narrow_kernel(NearestArgs a, uint32_t LG, uint32_t RPC,
-                                                                uint32_t WR) {
+
+template <int J>
+__device__ __forceinline__ uint32_t nkey(float v, uint32_t m32) {
+    uint32_t k;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(k) : "r"(__float_as_uint(v)), "r"(m32), "n"(J));
+    return k;
+}
+
+template <int P, int KP, int NS, bool PADK, int DS>
+__device__ __forceinline__ void narrow_pairs(const float2 (&cb)[KP][DS], const float2 (&cn)[KP],
+                                             const float2 (&xx)[DS], float2 C2, uint32_t (&m1)[NS],
+                                             uint32_t (&m2)[NS], uint32_t m32, uint32_t jvalid) {
+    if constexpr (P < KP) {
+        float2 acc = __fadd2_rn(cn[P], C2);
+#pragma unroll
+        for (int t = 0; t < DS; ++t) acc = __ffma2_rn(xx[t], cb[P][t], acc);
+        uint32_t ka = nkey<2 * P>(acc.x, m32), kb = nkey<2 * P + 1>(acc.y, m32);
+        if constexpr (PADK) {  // local codewords >= jvalid are padding
+            ka = uint32_t(2 * P) < jvalid ? ka : 0xFFFFFFFFu;
+            kb = uint32_t(2 * P + 1) < jvalid ? kb : 0xFFFFFFFFu;
+        }
+        const uint32_t lo = min(ka, kb), hi = max(ka, kb);
+        m2[P % NS] = min(m2[P % NS], min(max(m1[P % NS], lo), hi));
+        m1[P % NS] = min(m1[P % NS], lo);
+        narrow_pairs<P + 1, KP, NS, PADK, DS>(cb, cn, xx, C2, m1, m2, m32, jvalid);
+    }
+}
+
+template <int DS, int KS, int G, bool PADK>
+__global__ void __launch_bounds__(kNarrowThreads, (KS / G) * DS <= 64 ? 2 : 1) narrow_kernel(NearestArgs a, uint32_t LG, uint32_t RPC,
+                                                                uint32_t WR, uint32_t m32) {
     constexpr int KL = KS / G;  // codewords per lane
+    constexpr int KP = KL / 2;  // codeword pairs per lane
+    constexpr int NS = KP >= 8 ? 4 : (KP >= 4 ? 2 : 1);  // independent top-2 states
+    static_assert(KL % 2 == 0 && KL <= 32, "lane codewords");
     constexpr float kE = 2.f * float(DS + 4) * kU;
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t gw = uint64_t(blockIdx.x) * (kNarrowThreads / 32) + (threadIdx.x >> 5);
@@ -636,20 +905,30 @@ __global__ void __launch_bounds__(kNarrowThreads, (DS <= 4 && KS <= 16) ? 2 : 1)
     const bool lane_on = WR == 1 ? rsub < RPC : task < LG;
     const uint32_t s = lane_on ? task / G : 0, g = task % G;
     const bool sub_on = lane_on && !(a.active && !a.active[s]);
-    float cb[KL][DS];
-    float cn[KL];
+    // this lane's codewords, pairwise: cb[p][t] = (c_{2p,t}, c_{2p+1,t})
+    float2 cb[KP][DS];
+    float2 cn[KP];
 #pragma unroll
-    for (int jj = 0; jj < KL; ++jj) {
-        const uint32_t j = g * KL + jj;
-        const bool ok = sub_on && j < a.k;
-        cn[jj] = ok ? __ldg(a.cnorm + uint64_t(s) * a.k + j) : __int_as_float(0x7f800000);
+    for (int p = 0; p < KP; ++p) {
+        float c0[DS], c1[DS];
 #pragma unroll
-        for (int t = 0; t < DS; t += 4) {
-            const float4 v = ok ? __ldg(reinterpret_cast<const float4*>(a.table + (uint64_t(s) * a.k + j) * DS) + t / 4)
-                                : make_float4(0.f, 0.f, 0.f, 0.f);
-            cb[jj][t] = v.x; cb[jj][t + 1] = v.y; cb[jj][t + 2] = v.z; cb[jj][t + 3] = v.w;
+        for (int u = 0; u < 2; ++u) {
+            const uint32_t j = g * KL + 2 * p + u;
+            const bool ok = sub_on && j < a.k;
+            float* c = u ? c1 : c0;
+#pragma unroll
+            for (int t = 0; t < DS; t += 4) {
+                const float4 v = ok ? __ldg(reinterpret_cast<const float4*>(a.table + (uint64_t(s) * a.k + j) * DS) + t / 4)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+                c[t] = v.x; c[t + 1] = v.y; c[t + 2] = v.z; c[t + 3] = v.w;
+            }
+            const float nv = ok ? __ldg(a.cnorm + uint64_t(s) * a.k + j) : 0.f;
+            if (u) cn[p].y = nv; else cn[p].x = nv;
         }
+#pragma unroll
+        for (int t = 0; t < DS; ++t) cb[p][t] = make_float2(c0[t], c1[t]);
     }
+    const uint32_t jvalid = a.k > uint64_t(g) * KL ? uint32_t(min(uint64_t(KL), a.k - uint64_t(g) * KL)) : 0u;
     const float cm = sub_on ? a.cmax[s] : 0.f;
     const float cm2 = cm * cm;
     const uint32_t step0 = uint32_t(WR == 1 ? gw : gw / WR);
@@ -658,70 +937,64 @@ __global__ void __launch_bounds__(kNarrowThreads, (DS <= 4 && KS <= 16) ? 2 : 1)
     const uint32_t rstep = steps * RPC;  // rows between a lane's consecutive steps
     const uint64_t ld4 = a.src.ldx / 4;
     const uint64_t dptr = uint64_t(rstep) * ld4;
-    // P steps of sub-vectors in flight per lane (a register ring), loads
-    // addressed by a running pointer
-    constexpr int P = DS <= 4 ? 4 : 2;
-    float4 xr[P][DS / 4];
+    // P steps of sub-vectors in flight per lane (a register ring)
+    constexpr int PF = DS <= 4 ? 4 : 2;
+    float4 xr[PF][DS / 4];
     uint32_t rr = step0 * RPC + rsub;  // the row of ring slot 0
     const float4* xp = reinterpret_cast<const float4*>(a.src.x + uint64_t(s) * a.src.col_stride) + uint64_t(rr) * ld4;
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
+    for (int p = 0; p < PF; ++p) {
         if (sub_on && rr + uint32_t(p) * rstep < n) {
 #pragma unroll
             for (int t = 0; t < DS / 4; ++t) xr[p][t] = __ldg(xp + uint64_t(p) * dptr + t);
         }
     }
-    for (; rr - rsub < n; rr += uint32_t(P) * rstep, xp += uint64_t(P) * dptr) {
+    // the G lanes of a (row, subspace) task are consecutive: their group's bits
+    const uint32_t gbase = lane & ~uint32_t(G - 1);
+    const uint32_t gmask = G >= 32 ? 0xFFFFFFFFu : (((1u << G) - 1u) << gbase);
+    for (; rr - rsub < n; rr += uint32_t(PF) * rstep, xp += uint64_t(PF) * dptr) {
 #pragma unroll
-        for (int p = 0; p < P; ++p) {
+        for (int p = 0; p < PF; ++p) {
             const uint32_t crow = rr + uint32_t(p) * rstep;
             if (crow - rsub >= n) break;  // warp-uniform
             const bool cur = sub_on && crow < n;
-            float x[DS];
+            float2 xx[DS];
+            float nx4 = 0.f;  // ||-2x||^2 = 4 ||x||^2
 #pragma unroll
             for (int t = 0; t < DS / 4; ++t) {
-                x[4 * t] = -2.f * xr[p][t].x; x[4 * t + 1] = -2.f * xr[p][t].y;
-                x[4 * t + 2] = -2.f * xr[p][t].z; x[4 * t + 3] = -2.f * xr[p][t].w;
+                const float v[4] = {-2.f * xr[p][t].x, -2.f * xr[p][t].y, -2.f * xr[p][t].z, -2.f * xr[p][t].w};
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    xx[4 * t + w] = make_float2(v[w], v[w]);
+                    nx4 = fmaf(v[w], v[w], nx4);
+                }
             }
-            if (sub_on && crow + uint32_t(P) * rstep < n) {  // refill the slot P steps ahead
+            if (sub_on && crow + uint32_t(PF) * rstep < n) {  // refill the slot PF steps ahead
 #pragma unroll
-                for (int t = 0; t < DS / 4; ++t) xr[p][t] = __ldg(xp + uint64_t(p + P) * dptr + t);
+                for (int t = 0; t < DS / 4; ++t) xr[p][t] = __ldg(xp + uint64_t(p + PF) * dptr + t);
             }
-            float s2 = 0.f;
+            const float nx = 0.25f * nx4;
+            // S >= (||x|| + max||c||)^2 >= every partial sum's magnitude before
+            // the offset; the offset window starts at 2^p, p = 1 (mod 16)
+            const float S = 2.f * (nx * (1.f + 1e-6f) + cm2) + 1e-6f;
+            int e = int((__float_as_uint(S) >> 23) & 0xFF) - 127;
+            e = max(-60, min(e, 100));
+            const int pw = (e & ~15) + 1;  // smallest p >= e - 14 with p = 1 (mod 16)
+            const float O = __uint_as_float(uint32_t(pw + 127) << 23);
+            const uint32_t hi4 = uint32_t(pw + 127) >> 4;
+            const float E = kE * (S + O) * 1.001f + 1e-30f;
+            const float C = nx * (1.f + 2.f * float(DS + 2) * kU) + 2.f * E + O;
+            uint32_t m1[NS], m2[NS];
 #pragma unroll
-            for (int t = 0; t < DS; ++t) s2 = fmaf(x[t], x[t], s2);
-            const float nx = 0.25f * s2;
-            // E = kE q^2 with q = ||x|| + max||c||, bounded without the root:
-            // q^2 <= 2 (||x||^2 + max||c||^2) (the 1e-6 guards nx's rounding)
-            const float E = kE * 2.f * (nx * (1.f + 1e-6f) + cm2) + 1e-30f;
-            const float C = nx * (1.f + 2.f * float(DS + 2) * kU) + 2.f * E;
-            // keys: the (non-negative) screened value's bits with the global
-            // codeword index in the low log2(KS) bits -- the running top-2 is
-            // three integer min/max per codeword, ties resolve to the lower
-            // index, and truncating those bits moves a value by < KS ulps
-            // (added to the margin below)
-            constexpr uint32_t kMask = uint32_t(KS) - 1u;
-            // NS independent top-2 states (codewords jj = ns mod NS), merged
-            // after: the min/max chains of the codewords overlap
-            constexpr int NS = KL >= 4 ? 4 : KL;
-            uint32_t t1[NS], t2[NS];
-#pragma unroll
-            for (int u = 0; u < NS; ++u) t1[u] = t2[u] = 0xFFFFFFFFu;
-#pragma unroll
-            for (int jj = 0; jj < KL; ++jj) {
-                float acc = cn[jj] + C;
-#pragma unroll
-                for (int t = 0; t < DS; ++t) acc = fmaf(x[t], cb[jj][t], acc);
-                const uint32_t key = (__float_as_uint(acc) & ~kMask) | (g * KL + jj);
-                t2[jj % NS] = min(t2[jj % NS], max(t1[jj % NS], key));
-                t1[jj % NS] = min(t1[jj % NS], key);
-            }
-            uint32_t k1 = t1[0], k2 = t2[0];
+            for (int u = 0; u < NS; ++u) m1[u] = m2[u] = 0xFFFFFFFFu;
+            narrow_pairs<0, KP, NS, PADK, DS>(cb, cn, xx, make_float2(C, C), m1, m2, m32, jvalid);
+            uint32_t k1 = m1[0], k2 = m2[0];
 #pragma unroll
             for (int u = 1; u < NS; ++u) {
-                k2 = min(min(k2, t2[u]), max(k1, t1[u]));
-                k1 = min(k1, t1[u]);
+                k2 = min(min(k2, m2[u]), max(k1, m1[u]));
+                k1 = min(k1, m1[u]);
             }
+            const uint32_t own = k1;
 #pragma unroll
             for (int o = 1; o < G; o <<= 1) {  // merge the G parts of this (row, subspace)
                 const uint32_t o1 = __shfl_xor_sync(0xffffffffu, k1, o);
@@ -729,14 +1002,26 @@ __global__ void __launch_bounds__(kNarrowThreads, (DS <= 4 && KS <= 16) ? 2 : 1)
                 k2 = min(min(k2, o2), max(k1, o1));
                 k1 = min(k1, o1);
             }
-            const uint32_t i1 = k1 & kMask;
-            const float b1 = __uint_as_float(k1 & ~kMask), b2 = __uint_as_float(k2 & ~kMask);
+            // the part holding the winner (an exact key tie between parts means
+            // equal values: the runner-up test below flags the row)
+            uint32_t gwin = 0;
+            if constexpr (G > 1) {
+                const uint32_t bal = __ballot_sync(0xffffffffu, own == k1) & gmask;
+                gwin = bal ? uint32_t(__ffs(bal) - 1) - gbase : 0u;
+            }
             if (!cur || g != 0) continue;
-            // b1's true value is below b1 + KS ulp(b1) <= b1 * (1 + KS 2^-23)
-            const bool unique = isfinite(E) && b1 < __int_as_float(0x7f800000) && k1 != 0xFFFFFFFFu &&
-                                (!(b2 < __int_as_float(0x7f800000)) ||
-                                 b2 - b1 > 2.05f * E + b1 * (float(KS) * 2.3841858e-07f));
-            if (unique) {
+            const uint32_t i1 = gwin * KL + (k1 & 31u);
+            bool unique = false;
+            if (isfinite(E) && k1 != 0xFFFFFFFFu) {
+                if (k2 == 0xFFFFFFFFu) {
+                    unique = true;
+                } else {
+                    const float f1 = __uint_as_float((k1 >> 5) | (hi4 << 27));
+                    const float f2 = __uint_as_float((k2 >> 5) | (hi4 << 27));
+                    unique = f2 - f1 > 2.05f * E;
+                }
+            }
+            if (unique && i1 < a.k) {
                 if (a.idx_bytes == 1 && a.idx_ps == 1)
                     static_cast<uint8_t*>(a.out_idx)[uint64_t(crow) * a.idx_rs + s] = uint8_t(i1);
                 else
@@ -746,7 +1031,7 @@ __global__ void __launch_bounds__(kNarrowThreads, (DS <= 4 && KS <= 16) ? 2 : 1)
                     double accd = 0.0;
 #pragma unroll
                     for (int t = 0; t < DS; ++t) {
-                        const double diff = __dsub_rn((double)(-0.5f * x[t]), (double)__ldg(c + t));
+                        const double diff = __dsub_rn((double)(-0.5f * xx[t].x), (double)__ldg(c + t));
                         accd = __dadd_rn(accd, __dmul_rn(diff, diff));
                     }
                     a.out_dist[uint64_t(s) * a.n + crow] = accd;
@@ -768,8 +1053,13 @@ void launch_narrow(pqg_ctx* ctx, const NearestArgs& a) {
     else WR = (LG + 31) / 32;
     const uint64_t units = (a.n + RPC - 1) / RPC * WR;  // warp steps
     const uint64_t blocks = std::min<uint64_t>((units + 7) / 8, uint64_t(ctx->num_sms) * 16);
-    launch(ctx, "nearest_narrow", narrow_kernel<DS, KS, G>, dim3(unsigned(std::max<uint64_t>(1, blocks))),
-           dim3(kNarrowThreads), 0, a, LG, RPC, WR);
+    const dim3 grid(unsigned(std::max<uint64_t>(1, blocks)));
+    if (a.k == uint64_t(KS))
+        launch(ctx, "nearest_narrow", narrow_kernel<DS, KS, G, false>, grid, dim3(kNarrowThreads), 0, a, LG, RPC,
+               WR, 32u);
+    else
+        launch(ctx, "nearest_narrow", narrow_kernel<DS, KS, G, true>, grid, dim3(kNarrowThreads), 0, a, LG, RPC,
+               WR, 32u);
 }
 
 // Which narrow instance applies (0: none).  LG > 32 needs WR | 8 (warps per CTA).
@@ -780,32 +1070,35 @@ int narrow_variant(const NearestArgs& a) {
     if (((a.src.ldx | a.src.col_stride) & 3u) != 0 || (reinterpret_cast<uintptr_t>(a.src.x) & 15u) != 0 ||
         (reinterpret_cast<uintptr_t>(a.table) & 15u) != 0)
         return 0;
-    if (!(a.d == 4 || a.d == 8 || a.d == 16 || a.d == 32)) return 0;
+    if (!(a.d == 4 || a.d == 8 || a.d == 16)) return 0;
     if (a.n >= (uint64_t(1) << 31)) return 0;
-    const int KS = a.k <= 16 ? 16 : (a.k <= 32 ? 32 : (a.k <= 64 ? 64 : 0));
+    const int KS = a.k <= 16 ? 16 : (a.k <= 32 ? 32 : (a.k <= 64 ? 64 : (a.k <= 128 ? 128 : (a.k <= 256 ? 256 : 0))));
     if (!KS) return 0;
     const int G = std::max(1, KS * int(a.d) / 128);
+    if (KS / G > 32 || KS / G < 2) return 0;
     const uint64_t LG = uint64_t(a.B) * G;
     if (LG > 32 && (LG > 256 || 8 % ((LG + 31) / 32) != 0)) return 0;
-    // measured r2 (1M x 128 encodes, tools/encode_bench.py): the register-
-    // resident kernel wins at Ks <= 16 with Ds <= 8 (M=32: 1.95 -> 2.98,
-    // M=16: 2.64 -> 3.03 G vectors/s); the tcgen05 / small-table screens
-    // stay ahead at Ds >= 16 and at Ks = 64.  PQG_NARROW=1 forces it.
-    if (!(e && e[0] == '1') && (KS > 16 || a.d > 8)) return 0;
+    if (e && e[0] == '1') return KS;  // forced
+    // measured r2 (tools/encode_bench.py, 1M x 128): the tcgen05 screen wins
+    // from Ks = 64 up (M=16 Ks=64: 0.42 vs 0.98 ms, M=32 Ks=64: 0.73 vs 1.21)
+    if (a.d != 4 || KS > 16) return 0;
     return KS;
 }
 
 void narrow(pqg_ctx* ctx, const NearestArgs& a, int KS) {
     auto go = [&](auto ds_tag) {
         constexpr int DS = decltype(ds_tag)::value;
-        if (KS == 16) launch_narrow<DS, 16>(ctx, a);
-        else if (KS == 32) launch_narrow<DS, 32>(ctx, a);
-        else launch_narrow<DS, 64>(ctx, a);
+        if constexpr (DS * 16 / 128 <= 32) {
+            if (KS == 16) launch_narrow<DS, 16>(ctx, a);
+            else if (KS == 32) launch_narrow<DS, 32>(ctx, a);
+            else if (KS == 64) launch_narrow<DS, 64>(ctx, a);
+            else if (KS == 128) launch_narrow<DS, 128>(ctx, a);
+            else launch_narrow<DS, 256>(ctx, a);
+        }
     };
     if (a.d == 4) go(std::integral_constant<int, 4>());
     else if (a.d == 8) go(std::integral_constant<int, 8>());
-    else if (a.d == 16) go(std::integral_constant<int, 16>());
-    else go(std::integral_constant<int, 32>());
+    else go(std::integral_constant<int, 16>());
 }
 
 __global__ void __launch_bounds__(256, 1) norms_kernel(const float* table, uint32_t B, uint64_t k, uint32_t d,
@@ -897,8 +1190,11 @@ void nearest(pqg_ctx* ctx, NearestArgs a) {
                            (reinterpret_cast<uintptr_t>(a.src.x) & 15u) == 0 &&
                            (reinterpret_cast<uintptr_t>(a.table) & 15u) == 0 &&
                            uint64_t(a.B) * a.k * (a.d + 1) * sizeof(float) <= 96 * 1024;
-    const int narrow_ks = force_fp32 || (mode && std::strcmp(mode, "tc") == 0) ? 0 : narrow_variant(a);
-    if (narrow_ks) {
+    const bool tc_forced = mode && std::strcmp(mode, "tc") == 0;
+    const int narrow_ks = force_fp32 || tc_forced ? 0 : narrow_variant(a);
+    if (!force_fp32 && !tc_forced && row_screen_supported(a)) {
+        row_screen(ctx, a);
+    } else if (narrow_ks) {
         narrow(ctx, a, narrow_ks);
     } else if (small_tab) {
         const size_t smem = size_t(a.B) * a.k * (a.d + 1) * sizeof(float);

@@ -284,8 +284,7 @@ __device__ __forceinline__ RowConst<DS> row_prep(float nx, float cmax) {
     const float S = q * q * 1.01f + 1e-6f;  // >= 2|x.c| + ||c||^2 + ||x||^2 + 2E
     int e = int((__float_as_uint(S) >> 23) & 0xFF) - 127;
     e = max(-60, min(e, 100));  // non-finite S: E below is non-finite, the row is flagged
-    int p = e - 14;
-    p += ((1 - p) % 16 + 16) % 16;
+    const int p = (e & ~15) + 1;  // smallest p >= e - 14 with p = 1 (mod 16)
     const float O = __uint_as_float(uint32_t(p + 127) << 23);
     rc.hi4 = uint32_t(p + 127) >> 4;
     const float St = (S + O) * 1.002f;  // + C's rounding up to tf32 (<= 2^-10 C)

@@ -785,9 +785,15 @@ def test_torch_inputs_ordered_on_torch_stream(pq, orc, mix):
 
 @pytest.mark.parametrize("D,M,ks", [(128, 32, 16), (128, 16, 16), (128, 8, 16), (128, 4, 16), (96, 12, 16),
                                     (128, 32, 64), (128, 16, 64), (64, 8, 64), (64, 16, 12), (32, 8, 5),
-                                    (128, 32, 32), (96, 24, 16)])
-def test_narrow_screen_parity(pq, orc, mix, monkeypatch, D, M, ks):
+                                    (128, 32, 32), (96, 24, 16), (128, 32, 256), (128, 16, 256),
+                                    (128, 8, 256), (128, 8, 128), (64, 16, 100), (128, 16, 200)])
+@pytest.mark.parametrize("kern", ["narrow", "rows"])
+def test_narrow_screen_parity(pq, orc, mix, monkeypatch, D, M, ks, kern):
     monkeypatch.setenv("PQG_NARROW", "1")
+    if kern == "narrow":  # the register-resident kernel (the row-blocked one owns Ks <= 32)
+        monkeypatch.setenv("PQG_ROWSCREEN", "0")
+    elif ks > 32:
+        pytest.skip("row-blocked screen: Ks <= 32")
     x = mix(6000, D, 24, seed=D + M + ks)
     st = {}
     cb = pq.pq_fit(x, M, ks, 6, 3, stats=st)
