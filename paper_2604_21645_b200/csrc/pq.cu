@@ -130,6 +130,60 @@ __global__ void recon_sse_kernel(const float* x, const uint8_t* codes, uint64_t 
     if (threadIdx.x == 0) parts[blockIdx.x] = s;
 }
 
+// The same sum for Ds in {4, 8, 16, 32} with aligned rows (r2), software-
+// pipelined: the code of the thread's NEXT pair is loaded one step ahead, so
+// the dependent codeword gather (L2) no longer waits behind the code's HBM
+// latency, and four fp64 partial sums (one per float4 lane) shorten the
+// dependent add chain (ncu r2: the one-pair loop stalled on long scoreboard,
+// 0.57 of HBM).  The order of every addition is fixed by (block, thread,
+// step, lane): the sum is deterministic (within 1e-12 of the reference's
+// sequential sum, like the generic kernel's).
+template <int DS>
+__global__ void __launch_bounds__(kThreads, 4) recon_sse_vec_kernel(const float* x, const uint8_t* codes, uint64_t n,
+                                                                    uint32_t M, uint32_t ks, const float* tables,
+                                                                    uint64_t chunk, double* parts, int* err) {
+    const uint64_t D = uint64_t(M) * DS, total = n * M;
+    const uint64_t c0 = uint64_t(blockIdx.x) * chunk, c1 = min64(total, c0 + chunk);
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    auto code_of = [&](uint64_t p) -> uint32_t {
+        if (p >= c1) return 0u;
+        uint32_t c = ks <= 256 ? uint32_t(__ldg(codes + p)) : uint32_t(__ldg(reinterpret_cast<const uint16_t*>(codes) + p));
+        if (c >= ks) {
+            atomicExch(err, 1);
+            c = 0;
+        }
+        return c;
+    };
+    uint64_t p = c0 + threadIdx.x;
+    uint32_t code = code_of(p);
+    for (; p < c1; p += kThreads) {
+        uint64_t i, m;
+        split_elem(p, M, i, m);
+        const float4* xp = reinterpret_cast<const float4*>(x + i * D + m * DS);
+        const float4* cp = reinterpret_cast<const float4*>(tables + (m * ks + code) * DS);
+        float4 xv[DS / 4], cv[DS / 4];
+#pragma unroll
+        for (int q = 0; q < DS / 4; ++q) {
+            xv[q] = __ldg(xp + q);
+            cv[q] = __ldg(cp + q);
+        }
+        code = code_of(p + kThreads);  // next step's code, in flight during this one
+#pragma unroll
+        for (int q = 0; q < DS / 4; ++q) {
+            const float4 a = xv[q], c = cv[q];
+            const double d0 = __dsub_rn((double)a.x, (double)c.x), d1 = __dsub_rn((double)a.y, (double)c.y);
+            const double d2 = __dsub_rn((double)a.z, (double)c.z), d3 = __dsub_rn((double)a.w, (double)c.w);
+            s0 = __dadd_rn(s0, __dmul_rn(d0, d0));
+            s1 = __dadd_rn(s1, __dmul_rn(d1, d1));
+            s2 = __dadd_rn(s2, __dmul_rn(d2, d2));
+            s3 = __dadd_rn(s3, __dmul_rn(d3, d3));
+        }
+    }
+    double s = __dadd_rn(__dadd_rn(s0, s1), __dadd_rn(s2, s3));
+    s = block_sum256(s);
+    if (threadIdx.x == 0) parts[blockIdx.x] = s;
+}
+
 __global__ void final_sum_kernel(const double* parts, uint64_t count, double* out) {
     double s = 0.0;
     for (uint64_t i = threadIdx.x; i < count; i += kThreads) s = __dadd_rn(s, parts[i]);
@@ -303,8 +357,17 @@ void recon_sse_dev(pqg_ctx* ctx, const float* x, const uint8_t* codes, uint64_t 
     const uint64_t chunk = (n * M + np - 1) / np;  // (row, subspace) pairs per part
     double* parts = scratch<double>(ctx, np);
     const bool vec = ds % 4 == 0 && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(tables)) & 15u) == 0;
-    launch(ctx, "recon_sse", recon_sse_kernel, dim3(unsigned(np)), dim3(kThreads), 0, x, codes, n, M,
-           ks, ds, tables, chunk, parts, err, vec);
+    auto go = [&](auto kern) {
+        launch(ctx, "recon_sse", kern, dim3(unsigned(np)), dim3(kThreads), 0, x, codes, n, M, ks, tables, chunk,
+               parts, err);
+    };
+    // measured r2 (tools/sse_bench.py, 4M rows): the pipelined kernel wins at
+    // Ds <= 8 (D=128 M=16 0.57 -> 0.53 ms), the generic one at Ds = 16
+    if (vec && ds == 4) go(recon_sse_vec_kernel<4>);
+    else if (vec && ds == 8) go(recon_sse_vec_kernel<8>);
+    else
+        launch(ctx, "recon_sse", recon_sse_kernel, dim3(unsigned(np)), dim3(kThreads), 0, x, codes, n, M,
+               ks, ds, tables, chunk, parts, err, vec);
     reduce_sum_f64(ctx, parts, np, sse);
 }
 
