@@ -638,10 +638,41 @@ static double seconds_since(Clock::time_point t) {
 
 // Search of nq queries with their probe lists: the tensor-core screened scan
 // when it applies (adc_tc.cu), else the LUT scan (ivf.cu).  Both are exact.
+// The query LUTs of a search batch (adc_luts_kernel) do not depend on the
+// probe lists: they are built on the context's side stream while the probe
+// kernels run on the main one (r2), and the scan loads them.  Returns null
+// (the scan builds its own) when the batch is small, the shape is not
+// covered or PQG_ADC_LUT=0.
+static const float* search_luts_async(pqg_ctx* ctx, const pqg_index* ix, const float* dq, uint64_t nq) {
+    const char* le = std::getenv("PQG_ADC_LUT");
+    if ((le && le[0] == '0') || nq < 64 || nq > 16384 || ix->ks > 256 ||
+        !(ix->ds == 4 || ix->ds == 8 || ix->ds == 16 || ix->ds == 32))
+        return nullptr;
+    float* luts = scratch<float>(ctx, nq * ix->M * ix->ks);
+    if (!ctx->copy_stream) PQG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    if (!ctx->pipe_ev[2]) PQG_CUDA(cudaEventCreateWithFlags(&ctx->pipe_ev[2], cudaEventDisableTiming));
+    if (!ctx->pipe_ev[3]) PQG_CUDA(cudaEventCreateWithFlags(&ctx->pipe_ev[3], cudaEventDisableTiming));
+    PQG_CUDA(cudaEventRecord(ctx->pipe_ev[2], ctx->stream));
+    PQG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->pipe_ev[2], 0));
+    cudaStream_t main = ctx->stream;
+    ctx->stream = ctx->copy_stream;
+    bool ok = false;
+    try {
+        ok = adc_luts_dev(ctx, ix->tables, ix->M, ix->ks, ix->ds, dq, nq, luts);
+    } catch (...) {
+        ctx->stream = main;
+        throw;
+    }
+    ctx->stream = main;
+    PQG_CUDA(cudaEventRecord(ctx->pipe_ev[3], ctx->copy_stream));
+    return ok ? luts : nullptr;
+}
+
 static void search_scan(pqg_ctx* ctx, const pqg_index* ix, const float* dq, uint64_t nq,
                         const uint32_t* probes, uint64_t nprobe, uint64_t k, int has_max,
                         double max_sq, uint64_t* oi, double* od, uint32_t* oc,
-                        const uint64_t* subset = nullptr, uint64_t nsub = 0) {
+                        const uint64_t* subset = nullptr, uint64_t nsub = 0, const float* luts = nullptr) {
+    if (luts) PQG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->pipe_ev[3], 0));
     const IndexView v = ix->view();
     if (ix->tc.state >= 0 && adc_tc_supported(v, nq, k, nprobe)) {
         if (ix->tc.state == 0) ix->tc.state = adc_tc_prepare(ctx, v, ix->tc) ? 1 : -1;
@@ -651,7 +682,7 @@ static void search_scan(pqg_ctx* ctx, const pqg_index* ix, const float* dq, uint
             return;
         }
     }
-    ivf_scan(ctx, v, dq, nq, probes, nprobe, k, has_max, max_sq, oi, od, oc, ctx->d_err, subset, nsub);
+    ivf_scan(ctx, v, dq, nq, probes, nprobe, k, has_max, max_sq, oi, od, oc, ctx->d_err, subset, nsub, luts);
 }
 
 // ===========================================================================
@@ -1503,9 +1534,11 @@ int pqg_index_search(pqg_ctx* ctx, const pqg_index* ix, const float* queries, ui
         auto od = out(ctx, out_dists, nq * k);
         auto oc = out(ctx, out_counts, nq);
         uint32_t* probes = scratch<uint32_t>(ctx, nq * nprobe);
+        const float* luts = k <= 32 ? search_luts_async(ctx, ix, dq, nq) : nullptr;
         ivf_probe(ctx, ix->view(), dq, nq, nprobe, probes);
         reset_err(ctx);
-        search_scan(ctx, ix, dq, nq, probes, nprobe, k, has_max, max_sq_dist, oi.dev, od.dev, oc.dev);
+        search_scan(ctx, ix, dq, nq, probes, nprobe, k, has_max, max_sq_dist, oi.dev, od.dev, oc.dev, nullptr, 0,
+                    luts);
         finish(ctx, oi);
         finish(ctx, od);
         finish(ctx, oc);

@@ -369,7 +369,13 @@ __global__ void __launch_bounds__(kScanThreads, (RB >= 32 ? 5 : 6)) adc_scan_ker
     const float* qv = queries + q * D;
     if (luts) {  // tables already built (adc_tables, identical entries)
         const float* lq = luts + q * uint64_t(M) * ks;
-        for (uint32_t e = threadIdx.x; e < M * ks; e += blockDim.x) lut[e] = __ldg(lq + e);
+        if (((M * ks) & 3u) == 0 && (reinterpret_cast<uintptr_t>(lq) & 15u) == 0) {
+            const float4* l4 = reinterpret_cast<const float4*>(lq);
+            for (uint32_t e = threadIdx.x; e < M * ks / 4; e += blockDim.x)
+                reinterpret_cast<float4*>(lut)[e] = __ldg(l4 + e);
+        } else {
+            for (uint32_t e = threadIdx.x; e < M * ks; e += blockDim.x) lut[e] = __ldg(lq + e);
+        }
     } else {
         // adc_table (proj/src/pq.cpp:132-151): the query converted to fp64 once
         // (shared), then per entry the codeword's conversions and the
@@ -800,15 +806,25 @@ void ivf_scan(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t 
                         sizeof(TopK) * 32 * (kScanThreads / 32);   // survivor buffers
     if (smem > 220 * 1024) fail(PQG_EUNSUPPORTED, "search: M*ks lookup table exceeds shared memory");
     const uint32_t rb = ix.M * ix.w;
+    // r2: the query LUTs of a batch are built by one batched kernel
+    // (adc_luts_kernel) and loaded by the scan; PQG_ADC_LUT=0 builds them
+    // inside the scan (r1)
+    const char* le = std::getenv("PQG_ADC_LUT");
+    const uint64_t qchunk = 16384;  // bounds the LUT scratch (16384 x 16 KB = 256 MB at M=16)
+    float* lut_buf = nullptr;
+    if (!luts && nq >= 64 && ix.ks <= 256 && !(le && le[0] == '0'))
+        lut_buf = scratch<float>(ctx, std::min<uint64_t>(nq, qchunk) * ix.M * ix.ks);
     auto run = [&](auto kern) {
         set_smem(kern, smem);
-        for (uint64_t q0 = 0; q0 < nq; q0 += 65535) {
-            const uint64_t nc = std::min<uint64_t>(65535, nq - q0);
+        for (uint64_t q0 = 0; q0 < nq; q0 += (lut_buf ? qchunk : 65535)) {
+            const uint64_t nc = std::min<uint64_t>(lut_buf ? qchunk : 65535, nq - q0);
+            const float* lq = luts ? luts + q0 * uint64_t(ix.M) * ix.ks : nullptr;
+            if (lut_buf && adc_luts_dev(ctx, ix.tables, ix.M, ix.ks, ix.ds, queries + q0 * ix.M * ix.ds, nc, lut_buf))
+                lq = lut_buf;
             launch(ctx, "adc_scan", kern, dim3(unsigned(nc)), dim3(kScanThreads), smem, ix.tables,
                    ix.M, ix.ks, ix.ds, queries + q0 * ix.M * ix.ds, ix.offsets, ix.ids, ix.codes,
                    probes + q0 * nprobe, nprobe, int(k), has_max, max_sq, subset, nsub,
-                   out_ids + q0 * k, out_dists + q0 * k, out_counts + q0, err,
-                   luts ? luts + q0 * uint64_t(ix.M) * ix.ks : nullptr);
+                   out_ids + q0 * k, out_dists + q0 * k, out_counts + q0, err, lq);
         }
     };
     // vector code loads need rb-aligned rows (CSR rows are rb apart from an aligned base)

@@ -135,6 +135,9 @@ void pq_decode_dev(pqg_ctx* ctx, const uint8_t* codes, uint64_t n, uint32_t M, u
 void sq_error_dev(pqg_ctx* ctx, const float* a, const float* b, uint64_t count, double* sse);
 void recon_sse_dev(pqg_ctx* ctx, const float* x, const uint8_t* codes, uint64_t n, uint32_t M,
                    uint32_t ks, uint32_t ds, const float* tables, double* sse, int* err);
+// batched search LUTs (one per query, [nq][M][ks]); false if the shape is not covered
+bool adc_luts_dev(pqg_ctx* ctx, const float* tables, uint32_t M, uint32_t ks, uint32_t ds,
+                  const float* queries, uint64_t nq, float* entries);
 void adc_tables_dev(pqg_ctx* ctx, const float* tables, uint32_t M, uint32_t ks, uint32_t ds,
                     const float* queries, uint64_t nq, float* entries);
 void adc_lookup_dev(pqg_ctx* ctx, const float* entries, uint32_t M, uint32_t ks,

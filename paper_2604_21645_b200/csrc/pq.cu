@@ -9,6 +9,8 @@
 // The SSE is reduced in a fixed-shape fp64 tree (deterministic, independent of
 // timing); the reference sums sequentially, so the two agree to ~1e-15
 // relative, far inside the 1e-4 RMSE tolerance of BASELINE.json.
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace pqg {
@@ -133,18 +135,17 @@ __global__ void recon_sse_kernel(const float* x, const uint8_t* codes, uint64_t 
 // The same sum for Ds in {4, 8, 16, 32} with aligned rows (r2), software-
 // pipelined: the code of the thread's NEXT pair is loaded one step ahead, so
 // the dependent codeword gather (L2) no longer waits behind the code's HBM
-// latency, and four fp64 partial sums (one per float4 lane) shorten the
-// dependent add chain (ncu r2: the one-pair loop stalled on long scoreboard,
-// 0.57 of HBM).  The order of every addition is fixed by (block, thread,
-// step, lane): the sum is deterministic (within 1e-12 of the reference's
-// sequential sum, like the generic kernel's).
+// latency (ncu r2: the one-pair loop stalled on long scoreboard, 0.57 of
+// HBM).  Every addition happens in recon_sse_kernel's order, so the two are
+// bit-identical (the chunked pipeline's local RMSE, chunk_sse_kernel, relies
+// on that order too).
 template <int DS>
 __global__ void __launch_bounds__(kThreads, 4) recon_sse_vec_kernel(const float* x, const uint8_t* codes, uint64_t n,
                                                                     uint32_t M, uint32_t ks, const float* tables,
                                                                     uint64_t chunk, double* parts, int* err) {
     const uint64_t D = uint64_t(M) * DS, total = n * M;
     const uint64_t c0 = uint64_t(blockIdx.x) * chunk, c1 = min64(total, c0 + chunk);
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    double s = 0.0;
     auto code_of = [&](uint64_t p) -> uint32_t {
         if (p >= c1) return 0u;
         uint32_t c = ks <= 256 ? uint32_t(__ldg(codes + p)) : uint32_t(__ldg(reinterpret_cast<const uint16_t*>(codes) + p));
@@ -173,13 +174,12 @@ __global__ void __launch_bounds__(kThreads, 4) recon_sse_vec_kernel(const float*
             const float4 a = xv[q], c = cv[q];
             const double d0 = __dsub_rn((double)a.x, (double)c.x), d1 = __dsub_rn((double)a.y, (double)c.y);
             const double d2 = __dsub_rn((double)a.z, (double)c.z), d3 = __dsub_rn((double)a.w, (double)c.w);
-            s0 = __dadd_rn(s0, __dmul_rn(d0, d0));
-            s1 = __dadd_rn(s1, __dmul_rn(d1, d1));
-            s2 = __dadd_rn(s2, __dmul_rn(d2, d2));
-            s3 = __dadd_rn(s3, __dmul_rn(d3, d3));
+            s = __dadd_rn(s, __dmul_rn(d0, d0));
+            s = __dadd_rn(s, __dmul_rn(d1, d1));
+            s = __dadd_rn(s, __dmul_rn(d2, d2));
+            s = __dadd_rn(s, __dmul_rn(d3, d3));
         }
     }
-    double s = __dadd_rn(__dadd_rn(s0, s1), __dadd_rn(s2, s3));
     s = block_sum256(s);
     if (threadIdx.x == 0) parts[blockIdx.x] = s;
 }
@@ -189,6 +189,50 @@ __global__ void final_sum_kernel(const double* parts, uint64_t count, double* ou
     for (uint64_t i = threadIdx.x; i < count; i += kThreads) s = __dadd_rn(s, parts[i]);
     s = block_sum256(s);
     if (threadIdx.x == 0) *out = s;
+}
+
+// Batched LUT build (r2) for the search: entries[q][m][j] =
+// float(sum_t (double(q_t) - double(c_jt))^2) in t order, exactly adc_table
+// (proj/src/pq.cpp:132-151).  Block = (subspace m, block of 32 queries),
+// thread = codeword j: the codeword is converted to fp64 ONCE and kept in
+// registers, the 32 queries' sub-vectors sit in shared memory as fp64, so an
+// entry costs Ds x (dsub, dmul, dadd) + one conversion back; the search
+// kernel then loads its query's table instead of building it (the in-kernel
+// build was 16.5% of the scan's instructions, r1h).
+constexpr uint32_t kLutQB = 32;
+template <int DS>
+__global__ void __launch_bounds__(256) adc_luts_kernel(const float* tables, uint32_t M, uint32_t ks,
+                                                       const float* queries, uint64_t nq, float* entries) {
+    __shared__ double qs[kLutQB][DS];
+    const uint32_t m = blockIdx.y;
+    const uint64_t q0 = uint64_t(blockIdx.x) * kLutQB;
+    const uint64_t D = uint64_t(M) * DS;
+    for (uint32_t e = threadIdx.x; e < kLutQB * DS; e += blockDim.x) {
+        const uint32_t qi = e / DS, t = e - qi * DS;
+        qs[qi][t] = q0 + qi < nq ? (double)__ldg(queries + (q0 + qi) * D + uint64_t(m) * DS + t) : 0.0;
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < ks; j += blockDim.x) {
+        double c[DS];
+#pragma unroll
+        for (int t = 0; t < DS; ++t) c[t] = (double)__ldg(tables + (uint64_t(m) * ks + j) * DS + t);
+        const uint32_t nqb = uint32_t(min64(uint64_t(kLutQB), nq - q0));
+        // four queries per step: four independent fp64 chains in flight
+        for (uint32_t qb = 0; qb < kLutQB; qb += 4) {
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int t = 0; t < DS; ++t) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const double diff = __dsub_rn(qs[qb + u][t], c[t]);
+                    acc[u] = __dadd_rn(acc[u], __dmul_rn(diff, diff));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (qb + u < nqb) entries[((q0 + qb + u) * M + m) * ks + j] = __double2float_rn(acc[u]);
+        }
+    }
 }
 
 __global__ void adc_tables_kernel(const float* tables, uint32_t M, uint32_t ks, uint32_t ds,
@@ -375,6 +419,18 @@ void adc_tables_dev(pqg_ctx* ctx, const float* tables, uint32_t M, uint32_t ks, 
                     const float* queries, uint64_t nq, float* entries) {
     launch(ctx, "adc_tables", adc_tables_kernel, dim3(grid1d(nq * M * ks, 256, 1u << 20)), dim3(256), 0,
            tables, M, ks, ds, queries, nq, entries);
+}
+
+bool adc_luts_dev(pqg_ctx* ctx, const float* tables, uint32_t M, uint32_t ks, uint32_t ds,
+                  const float* queries, uint64_t nq, float* entries) {
+    if (!(ds == 4 || ds == 8 || ds == 16 || ds == 32) || nq == 0 || M > 65535) return false;
+    const dim3 grid(unsigned((nq + kLutQB - 1) / kLutQB), M);
+    const unsigned th = std::min<unsigned>(256, (ks + 31) / 32 * 32);
+    if (ds == 4) launch(ctx, "adc_luts", adc_luts_kernel<4>, grid, dim3(th), 0, tables, M, ks, queries, nq, entries);
+    else if (ds == 8) launch(ctx, "adc_luts", adc_luts_kernel<8>, grid, dim3(th), 0, tables, M, ks, queries, nq, entries);
+    else if (ds == 16) launch(ctx, "adc_luts", adc_luts_kernel<16>, grid, dim3(th), 0, tables, M, ks, queries, nq, entries);
+    else launch(ctx, "adc_luts", adc_luts_kernel<32>, grid, dim3(th), 0, tables, M, ks, queries, nq, entries);
+    return true;
 }
 
 void adc_lookup_dev(pqg_ctx* ctx, const float* entries, uint32_t M, uint32_t ks,
