@@ -187,7 +187,6 @@ struct pqg_index {
     uint64_t* offsets = nullptr;
     uint64_t* ids = nullptr;
     uint8_t* codes = nullptr;
-    mutable TcCache tc;  // decoded candidate operand of the tensor-core search (built lazily)
 
     uint64_t D() const { return uint64_t(M) * ds; }
     uint64_t rb() const { return uint64_t(M) * w; }
@@ -196,7 +195,6 @@ struct pqg_index {
                          offsets, ids, codes, n};
     }
     void free_all() {
-        adc_tc_free(tc);
         for (void* p : {(void*)tables, (void*)coarse, (void*)coarse_norm, (void*)coarse_max,
                         (void*)offsets, (void*)ids, (void*)codes})
             if (p) cudaFree(p);
@@ -636,8 +634,7 @@ static double seconds_since(Clock::time_point t) {
     return std::chrono::duration<double>(Clock::now() - t).count();
 }
 
-// Search of nq queries with their probe lists: the tensor-core screened scan
-// when it applies (adc_tc.cu), else the LUT scan (ivf.cu).  Both are exact.
+// Search of nq queries with their probe lists: the LUT scan (ivf.cu).
 // The query LUTs of a search batch (adc_luts_kernel) do not depend on the
 // probe lists: they are built on the context's side stream while the probe
 // kernels run on the main one (r2), and the scan loads them.  Returns null
@@ -674,14 +671,6 @@ static void search_scan(pqg_ctx* ctx, const pqg_index* ix, const float* dq, uint
                         const uint64_t* subset = nullptr, uint64_t nsub = 0, const float* luts = nullptr) {
     if (luts) PQG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->pipe_ev[3], 0));
     const IndexView v = ix->view();
-    if (ix->tc.state >= 0 && adc_tc_supported(v, nq, k, nprobe)) {
-        if (ix->tc.state == 0) ix->tc.state = adc_tc_prepare(ctx, v, ix->tc) ? 1 : -1;
-        if (ix->tc.state == 1) {
-            adc_tc_search(ctx, v, ix->tc, dq, nq, probes, nprobe, k, has_max, max_sq, subset, nsub,
-                          oi, od, oc);
-            return;
-        }
-    }
     ivf_scan(ctx, v, dq, nq, probes, nprobe, k, has_max, max_sq, oi, od, oc, ctx->d_err, subset, nsub, luts);
 }
 
@@ -1446,7 +1435,6 @@ int pqg_index_add(pqg_ctx* ctx, pqg_index* ix, const uint8_t* codes, const uint6
         uint64_t* ids_b = scratch<uint64_t>(ctx, n);
         uint8_t* codes_b = scratch<uint8_t>(ctx, n * rb);
         csr_scatter(ctx, bk.perm, n, di, dc, rb, ids_b, codes_b);
-        adc_tc_free(ix->tc);  // the cached decoded operand no longer matches the lists
         concat_into(ctx, ix, ix, off_b, ids_b, codes_b, n);
     });
 }

@@ -178,22 +178,6 @@ void ivf_scan_large_k(pqg_ctx* ctx, const IndexView& ix, const float* queries, u
                       const uint32_t* probes, uint64_t nprobe, uint64_t k, int has_max,
                       double max_sq, uint64_t* out_ids, double* out_dists, uint32_t* out_counts,
                       int* err, const uint64_t* subset, uint64_t nsub, const float* luts);
-// adc_tc.cu: tensor-core screened search (decoded candidate operand cached per index)
-struct TcCache {
-    uint8_t* Bm = nullptr;        // [block of 256 candidates][K chunk][hi|lo]
-    uint64_t* blk_off = nullptr;  // [nlist+1] first block of each list
-    float* maxnorm = nullptr;     // max ||decoded candidate||
-    uint64_t nblocks = 0;
-    uint32_t kchunks = 0;
-    int state = 0;                // 0 not built, 1 built, -1 unusable (falls back to the LUT scan)
-};
-bool adc_tc_supported(const IndexView& ix, uint64_t nq, uint64_t k, uint64_t nprobe);
-bool adc_tc_prepare(pqg_ctx* ctx, const IndexView& ix, TcCache& c);
-void adc_tc_free(TcCache& c);
-void adc_tc_search(pqg_ctx* ctx, const IndexView& ix, const TcCache& c, const float* queries,
-                   uint64_t nq, const uint32_t* probes, uint64_t nprobe, uint64_t k, int has_max,
-                   double max_sq, const uint64_t* subset, uint64_t nsub, uint64_t* out_ids,
-                   double* out_dists, uint32_t* out_counts);
 void csr_scatter(pqg_ctx* ctx, const uint32_t* perm, uint64_t n, const uint64_t* ids,
                  const uint8_t* codes, uint64_t row_bytes, uint64_t* out_ids, uint8_t* out_codes);
 void find_duplicate(pqg_ctx* ctx, const uint64_t* ids, uint64_t n, uint64_t* first_dup_pos);

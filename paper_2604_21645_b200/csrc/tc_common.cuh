@@ -1,6 +1,6 @@
 // tc_common.cuh -- tcgen05 / TMEM / bulk-copy helpers and the K-major
 // no-swizzle UMMA operand layout shared by the tensor-core kernels that stream
-// pre-split TF32 hi/lo operands (umma_big.cu, adc_tc.cu).
+// pre-split TF32 hi/lo operands (umma_big.cu).
 #pragma once
 
 #include "kernels.cuh"
