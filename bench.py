@@ -394,13 +394,23 @@ def run_ours(args, rank, world, local):
         barrier(world)
         st = {}
         t0 = time.perf_counter()
-        sf = D.kmeans_fit_sharded(comm, be, train, HEAD_M, ds, ds, HEAD_KS, FIT_ITERS, seeds, 1e-4, stats=st)
+        sf = D.kmeans_fit_sharded(comm, be, train, HEAD_M, ds, ds, HEAD_KS, FIT_ITERS, seeds, 1e-4, stats=st,
+                                  force_exchange=True)
         torch.cuda.synchronize()
         sf_s = max_over_ranks(time.perf_counter() - t0, world)
+        # the default path (a 1-rank group runs the single-process fit)
+        st_def = {}
+        t0 = time.perf_counter()
+        D.kmeans_fit_sharded(comm, be, train, HEAD_M, ds, ds, HEAD_KS, FIT_ITERS, seeds, 1e-4, stats=st_def)
+        torch.cuda.synchronize()
+        sf_def_s = max_over_ranks(time.perf_counter() - t0, world)
         same = bool(torch.equal(sf.tables, tables)) if world == 1 else None
         sharded_fit = {"global_sample_rows": SAMPLE * world, "iters_run": int(np.max(sf.iterations_run)),
                        "seconds": sf_s, "iters_per_s": int(np.max(sf.iterations_run)) / sf_s,
                        "single_process_seconds": fit_s,
+                       "exchange_forced": True,
+                       "default_path_seconds": sf_def_s,
+                       "default_path": st_def.get("path", "exchange"),
                        "allreduce_bytes_per_iter": st["allreduce_bytes"] / max(1, st["iterations"]),
                        "replay_columns": st["replay_columns"], "reseeds": st["reseeds"],
                        "bit_identical_to_single_process": same}

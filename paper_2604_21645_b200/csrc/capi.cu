@@ -378,8 +378,11 @@ static KMeansOut run_kmeans(pqg_ctx* ctx, const float* x, uint64_t n, uint64_t l
     // small launches of an iteration go to the GPU as one.  Iteration 1 runs
     // eagerly first (it sizes the scratch the graph then reuses).
     const char* ge = std::getenv("PQG_KM_GRAPH");
+    // (the legacy / per-thread default streams cannot be captured)
+    const bool capturable = ctx->stream != nullptr && ctx->stream != cudaStreamLegacy &&
+                            ctx->stream != cudaStreamPerThread;
     const bool use_graph = !ctx->profiling && !(ge && ge[0] == '0') && !std::getenv("PQG_FLAG_STATS") &&
-                           max_iters >= 3;
+                           max_iters >= 3 && capturable;
     cudaGraphExec_t gexec = nullptr;
     uint64_t body_launches = 0;
     try {

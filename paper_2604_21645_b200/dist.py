@@ -192,6 +192,32 @@ class CudaBackend:
                                               self._p(tables), k, self._p(assign), self._p(dist),
                                               self._p(act)), "update_pass")
 
+    def fit_local(self, rows, B, d, col_stride, k, max_iters, seeds, tol):
+        """The single-process fit (pqg_kmeans_fit / pqg_pq_fit_ex) of a 1-rank
+        group, or None where its seeds / layout are not those entry points'."""
+        torch = self.torch
+        n, ld = rows.shape
+        iters = np.zeros(B, np.uint32)
+        inertia = np.zeros(B, np.float64)
+        per = np.zeros((B, max_iters), np.float64)
+        v = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        tables = torch.empty((B, k, d), dtype=torch.float32, device=rows.device)
+        if B == 1 and col_stride == 0 and ld == d:
+            assign = torch.empty((1, n), dtype=torch.int32, device=rows.device)
+            it, ine = C.c_uint32(), C.c_double()
+            self.L.check(self.lib.pqg_kmeans_fit(self.ctx.h, self._p(rows), n, d, k, max_iters, int(seeds[0]), tol,
+                                                 self._p(tables), self._p(assign), C.byref(ine), C.byref(it),
+                                                 v(per)), "kmeans_fit")
+            iters[0], inertia[0] = it.value, ine.value
+            return tables, assign, inertia, iters, per
+        if (col_stride == d and ld == B * d and tol == 1e-4 and
+                all(int(seeds[b]) == int(seeds[0]) + b for b in range(B))):
+            self.L.check(self.lib.pqg_pq_fit_ex(self.ctx.h, self._p(rows), n, ld, B, k, max_iters, int(seeds[0]),
+                                                self._p(tables), v(iters), v(inertia), v(per)), "pq_fit")
+            assign, _ = self.assign_pass(rows, B, d, col_stride, tables)  # the final pass's assignments
+            return tables, assign, inertia, iters, per
+        return None
+
     # -- one rank's side of the sharded fit (include/pqg.h pqg_kmshard_*) --
     def shard_create(self, rows, B, d, col_stride, k, max_iters, tol):
         """A device handle, or None where the sharded update does not apply."""
@@ -334,13 +360,27 @@ class ShardedFit:
 
 
 def kmeans_fit_sharded(comm: Comm, backend, local_rows, B: int, d: int, col_stride: int, k: int,
-                       max_iters: int, seeds, tol: float = 1e-4, stats: dict | None = None) -> ShardedFit:
+                       max_iters: int, seeds, tol: float = 1e-4, stats: dict | None = None,
+                       force_exchange: bool = False) -> ShardedFit:
     """B batched k-means problems (B = M subspaces for pq_fit, B = 1 for the
     coarse quantizer) over rows sharded by rank; bit-identical to the
     single-process fit (see module docstring).  ``stats`` (optional) receives
-    the exchange volume: bytes all-reduced / all-gathered per iteration."""
+    the exchange volume: bytes all-reduced / all-gathered per iteration.
+    A 1-rank group has nothing to exchange: it runs the single-process fit
+    (one device-resident graph per iteration, no host round trip) unless
+    ``force_exchange`` (the tests drive the exchange protocol at world 1 too)."""
     import torch
     dev = local_rows.device
+    if comm.world == 1 and not force_exchange and hasattr(backend, "fit_local") and k >= 1 and \
+            k <= local_rows.shape[0] and max_iters >= 1 and tol >= 0:
+        r = backend.fit_local(local_rows.contiguous(), B, d, col_stride, k, max_iters, seeds, tol)
+        if r is not None:
+            tables, assign, inertia, iters, per = r
+            if stats is not None:
+                stats.update(allreduce_bytes=0, allgather_bytes=0, replay_columns=0, reseeds=0,
+                             iterations=int(np.max(iters)), path="1-rank group: single-process fit")
+            per_iter = [[float(v) for v in per[b, : iters[b]]] for b in range(B)]
+            return ShardedFit(tables, assign, inertia, iters, per_iter)
     counts = [int(c) for c in comm.allgather_equal(
         torch.tensor([local_rows.shape[0]], dtype=torch.int64, device=dev)).view(-1).tolist()]
     n = sum(counts)

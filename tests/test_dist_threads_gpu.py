@@ -105,7 +105,8 @@ def test_kmshard_coarse_exchange_paths(orc, world):
     st = [dict() for _ in range(world)]
 
     def fn(comm, be, local):
-        return D.kmeans_fit_sharded(comm, be, local, 1, 8, 0, 40, 9, [2], 0.0, stats=st[comm.rank])
+        return D.kmeans_fit_sharded(comm, be, local, 1, 8, 0, 40, 9, [2], 0.0, stats=st[comm.rank],
+                                    force_exchange=True)
     res = _run_world(world, x, fn)
     ref = orc.kmeans_fit(x, 40, 9, 2, 0.0)
     for r in res:
@@ -137,3 +138,25 @@ def test_kmshard_pq_fit_matches_single_gpu(world):
         assert np.array_equal(np.asarray(r.iterations_run), stats["iterations_run"])
     per_iter = st[0]["allreduce_bytes"] / st[0]["iterations"]
     assert per_iter == 8 * 256 * 64 + 8 * 8 * 256 + 8 * 8 + 2 * 256 * 64
+
+
+@pytest.mark.parametrize("B,d,k", [(1, 8, 40), (8, 8, 256)])
+def test_kmshard_one_rank_delegation(B, d, k):
+    """A 1-rank group runs the single-process fit: same tables, assignments,
+    iterations and inertia as the exchange protocol forced at world 1."""
+    from paper_2604_21645_b200 import dist as D
+    x = _stress() if B == 1 else __import__("paper_2604_21645_b200.datagen", fromlist=["x"]).gaussian_mixture(
+        9001, 64, 32, seed=3)
+    seeds = [2] if B == 1 else [5 + m for m in range(B)]
+    tol = 0.0 if B == 1 else 1e-4
+    st_d, st_f = {}, {}
+    cs = 0 if B == 1 else d
+    rd = _run_world(1, x, lambda comm, be, local: D.kmeans_fit_sharded(comm, be, local, B, d, cs, k, 9, seeds, tol,
+                                                                       stats=st_d))[0]
+    rf = _run_world(1, x, lambda comm, be, local: D.kmeans_fit_sharded(comm, be, local, B, d, cs, k, 9, seeds, tol,
+                                                                       stats=st_f, force_exchange=True))[0]
+    assert st_d.get("path", "").startswith("1-rank") and "path" not in st_f
+    assert np.array_equal(rd.tables.cpu().numpy().view(np.uint32), rf.tables.cpu().numpy().view(np.uint32))
+    assert np.array_equal(rd.assignments.cpu().numpy(), rf.assignments.cpu().numpy())
+    assert np.array_equal(np.asarray(rd.iterations_run), np.asarray(rf.iterations_run))
+    assert rd.inertia_per_iter == rf.inertia_per_iter
