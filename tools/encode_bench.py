@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--points", default="4x16,8x16,16x16,32x16,4x64,8x64,16x64,32x64")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--ncu", action="store_true")
+    ap.add_argument("--rows", type=int, default=1_000_000)
     args = ap.parse_args()
     import torch
 
@@ -33,13 +34,13 @@ def main():
     ctx.set_stream(s.cuda_stream)
     lib = ctx.lib
     vp = C.c_void_p
-    N, D = 1_000_000, 128
+    N, D = args.rows, 128
     xh = gaussian_mixture(N, D, 256, 2604)
     x = torch.from_numpy(xh).cuda()
     train = x.index_select(0, torch.from_numpy(strided_sample(N, 100_000, 2604)).cuda()).contiguous()
     orc = oracle.c_oracle()
     rng = np.random.default_rng(1)
-    sel = np.sort(rng.choice(N, 3000, replace=False))
+    sel = np.sort(rng.choice(N, min(N, 3000), replace=False))
     out = []
     for p in args.points.split(","):
         M, ks = (int(v) for v in p.split("x"))
