@@ -84,13 +84,23 @@ __global__ void sse_kernel(const float* a, const float* b, uint64_t count, uint6
     if (threadIdx.x == 0) parts[blockIdx.x] = s;
 }
 
+// Streamed rows bypass L1 (r2e): the codeword gathers are the kernel's L1
+// working set (M x Ks x Ds fp32, 128 KB at D = 128, Ks = 256) and the rows,
+// read once, would evict it.
+__device__ __forceinline__ float4 ldg_stream(const float4* p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+
 // Squared error of one (row, subspace) pair: ds elements of x against the
 // codeword, accumulated in fp64 (vector loads when both are 16-byte aligned).
 __device__ __forceinline__ double pair_sse(const float* xp, const float* cw, uint32_t ds, bool vec,
                                            double s) {
     if (vec) {
         for (uint32_t t = 0; t < ds; t += 4) {
-            const float4 a = __ldg(reinterpret_cast<const float4*>(xp + t));
+            const float4 a = ldg_stream(reinterpret_cast<const float4*>(xp + t));
             const float4 c = __ldg(reinterpret_cast<const float4*>(cw + t));
             const double d0 = __dsub_rn((double)a.x, (double)c.x), d1 = __dsub_rn((double)a.y, (double)c.y);
             const double d2 = __dsub_rn((double)a.z, (double)c.z), d3 = __dsub_rn((double)a.w, (double)c.w);
@@ -140,7 +150,7 @@ __global__ void recon_sse_kernel(const float* x, const uint8_t* codes, uint64_t 
 // bit-identical (the chunked pipeline's local RMSE, chunk_sse_kernel, relies
 // on that order too).
 template <int DS>
-__global__ void __launch_bounds__(kThreads, 4) recon_sse_vec_kernel(const float* x, const uint8_t* codes, uint64_t n,
+__global__ void __launch_bounds__(kThreads, DS <= 4 ? 8 : 4) recon_sse_vec_kernel(const float* x, const uint8_t* codes, uint64_t n,
                                                                     uint32_t M, uint32_t ks, const float* tables,
                                                                     uint64_t chunk, double* parts, int* err) {
     const uint64_t D = uint64_t(M) * DS, total = n * M;
@@ -165,7 +175,7 @@ __global__ void __launch_bounds__(kThreads, 4) recon_sse_vec_kernel(const float*
         float4 xv[DS / 4], cv[DS / 4];
 #pragma unroll
         for (int q = 0; q < DS / 4; ++q) {
-            xv[q] = __ldg(xp + q);
+            xv[q] = ldg_stream(xp + q);
             cv[q] = __ldg(cp + q);
         }
         code = code_of(p + kThreads);  // next step's code, in flight during this one
