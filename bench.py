@@ -413,6 +413,9 @@ def run_ours(args, rank, world, local):
                        "default_path": st_def.get("path", "exchange"),
                        "allreduce_bytes_per_iter": st["allreduce_bytes"] / max(1, st["iterations"]),
                        "replay_columns": st["replay_columns"], "reseeds": st["reseeds"],
+                       "replay": st.get("replay"),
+                       "chain_bytes_per_iter": st.get("chain_bytes", 0) / max(1, st["iterations"]),
+                       "allgather_bytes_per_iter": st.get("allgather_bytes", 0) / max(1, st["iterations"]),
                        "bit_identical_to_single_process": same}
 
     # ---- headline encode, timed with profiling of the dominant kernel

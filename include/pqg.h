@@ -284,6 +284,14 @@ int pqg_kmshard_pack(pqg_ctx* ctx, pqg_kmshard* h, float* vals, uint64_t cap, ui
  * all_vals world x stride floats, all_offcnt world x 2*n_fail */
 int pqg_kmshard_replay(pqg_ctx* ctx, pqg_kmshard* h, float* tables, const double* f64, const float* all_vals,
                        uint64_t stride, const uint64_t* all_offcnt, uint32_t world);
+/* The chained replay (r2e; no member values cross ranks): run (device,
+ * n_fail fp64) holds each replay column's running row-order sum over the
+ * members of the ranks before this one (zeros on rank 0); _step continues
+ * every chain over this rank's members in local row order (the caller then
+ * hands run to the next rank), _finish writes the means from the last
+ * rank's run (broadcast to every rank). */
+int pqg_kmshard_replay_step(pqg_ctx* ctx, pqg_kmshard* h, double* run);
+int pqg_kmshard_replay_finish(pqg_ctx* ctx, pqg_kmshard* h, float* tables, const double* f64, const double* run);
 /* per problem the E+1 candidate slots (dist, global index, row) of this rank */
 int pqg_kmshard_reseed_candidates(pqg_ctx* ctx, pqg_kmshard* h, uint64_t row0, uint32_t E, double* cand_d,
                                   uint64_t* cand_i, float* cand_rows);

@@ -96,6 +96,8 @@ _SIGS = {
                                  C.POINTER(_i32)]),
     "pqg_kmshard_pack": (_i32, [_vp, _vp, _vp, _u64, _vp]),
     "pqg_kmshard_replay": (_i32, [_vp, _vp, _vp, _vp, _vp, _u64, _vp, _u32]),
+    "pqg_kmshard_replay_step": (_i32, [_vp, _vp, _vp]),
+    "pqg_kmshard_replay_finish": (_i32, [_vp, _vp, _vp, _vp, _vp]),
     "pqg_kmshard_reseed_candidates": (_i32, [_vp, _vp, _u64, _u32, _vp, _vp, _vp]),
     "pqg_kmshard_reseed_apply": (_i32, [_vp, _vp, _vp, _vp, _u32, _u32, _vp, _vp, _vp]),
     "pqg_kmshard_result": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp]),

@@ -321,6 +321,8 @@ static KMeansOut run_kmeans(pqg_ctx* ctx, const float* x, uint64_t n, uint64_t l
     st.inertia = scratch<double>(ctx, B);
     st.per_iter = scratch<double>(ctx, uint64_t(B) * max_iters);
     st.iters = scratch<uint32_t>(ctx, B);
+    st.tickets = scratch<unsigned>(ctx, B);
+    PQG_CUDA(cudaMemsetAsync(st.tickets, 0, sizeof(unsigned) * B, ctx->stream));
     std::vector<int> ones(B, 1);
     PQG_CUDA(cudaMemcpyAsync(st.active, ones.data(), sizeof(int) * B, cudaMemcpyHostToDevice, ctx->stream));
     PQG_CUDA(cudaMemsetAsync(st.prev, 0, sizeof(double) * B, ctx->stream));
@@ -345,9 +347,14 @@ static KMeansOut run_kmeans(pqg_ctx* ctx, const float* x, uint64_t n, uint64_t l
     const bool big = B == 1 && umma_big_prepare_rows(ctx, prep);
     PQG_CUDA(cudaMemsetAsync(st.iters, 0, sizeof(uint32_t) * B, ctx->stream));
     const auto iter_mark = ctx->arena.mark();
+    // small tables (PQ subspaces): the reseed block of each problem computes
+    // the next pass's norms; large ones (coarse fits) keep the wide kernel
+    const bool fuse_norms = uint64_t(k) * d <= 8192;
     auto body = [&](uint32_t it, bool update) {
         ctx->arena.reset_to(iter_mark);  // per-iteration scratch is reused
-        table_norms(ctx, table, B, k, d, cnorm, cmax);
+        // the first pass's norms; later passes get theirs from the previous
+        // update (reseed_kernel computes them once the table is final)
+        if (it == 1 || !fuse_norms) table_norms(ctx, table, B, k, d, cnorm, cmax);
         NearestArgs a;
         a.src = src;
         a.n = n;
@@ -370,7 +377,9 @@ static KMeansOut run_kmeans(pqg_ctx* ctx, const float* x, uint64_t n, uint64_t l
         nearest(ctx, a);
         kmeans_pad_keys(ctx, assign, n, B, k, d_nb, max_pad);
         kmeans_inertia_and_stop(ctx, dist, n, B, it, max_iters, tol, st, d_nb);
-        if (update) kmeans_update(ctx, src, n, B, d, table, k, assign, dist, st.active, d_nb);
+        if (update)
+            kmeans_update(ctx, src, n, B, d, table, k, assign, dist, st.active, d_nb, fuse_norms ? cnorm : nullptr,
+                          cmax);
     };
     // Iterations 2 .. max_iters-1 are identical launch sequences (the pass
     // number lives on the device, inactive problems are skipped by the
@@ -2036,6 +2045,26 @@ int pqg_kmshard_replay(pqg_ctx* ctx, pqg_kmshard* h, float* tables, const double
         pqg_ctx* o = h->own;
         const uint64_t l0 = o->launches;
         shard_replay(o, h->work, h->n_fail, h->k, h->d, h->B, f64, all_vals, stride, all_offcnt, world, tables);
+        ctx->launches += o->launches - l0;
+    });
+}
+
+int pqg_kmshard_replay_step(pqg_ctx* ctx, pqg_kmshard* h, double* run) {
+    return guard([&] {
+        ShardStep step(ctx, h);
+        pqg_ctx* o = h->own;
+        const uint64_t l0 = o->launches;
+        shard_replay_step(o, h->src, h->work, h->n_fail, h->k, h->d, h->offsets, h->perm, h->n, run);
+        ctx->launches += o->launches - l0;
+    });
+}
+
+int pqg_kmshard_replay_finish(pqg_ctx* ctx, pqg_kmshard* h, float* tables, const double* f64, const double* run) {
+    return guard([&] {
+        ShardStep step(ctx, h);
+        pqg_ctx* o = h->own;
+        const uint64_t l0 = o->launches;
+        shard_replay_finish(o, h->work, h->n_fail, h->k, h->d, h->B, f64, run, tables);
         ctx->launches += o->launches - l0;
     });
 }

@@ -83,6 +83,9 @@ struct KMeansState {
     double* inertia;      // [B]
     double* per_iter;     // [B][max_iters]
     uint32_t* iters;      // [B]
+    // [B] zeroed once per fit (r2e): with it the inertia's last partial block
+    // runs the stop rule (one launch per pass instead of two); null: stop_kernel
+    unsigned* tickets = nullptr;
 };
 void rows_sum_f64(pqg_ctx* ctx, const double* v, uint64_t n, uint32_t B, double* out);
 void kmeans_inertia_and_stop(pqg_ctx* ctx, const double* dist, uint64_t n, uint32_t B,
@@ -90,7 +93,8 @@ void kmeans_inertia_and_stop(pqg_ctx* ctx, const double* dist, uint64_t n, uint3
                              const uint64_t* nb = nullptr);
 void kmeans_update(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint32_t d,
                    float* table, uint64_t k, const uint32_t* assign, double* dist,
-                   const int* active, const uint64_t* nb = nullptr);
+                   const int* active, const uint64_t* nb = nullptr, float* cnorm = nullptr,
+                   float* cmax = nullptr);
 // Row-sharded fits (kmshard.cu): one rank's bucketing + exact piece sums with
 // exponent ranges, and the stop rule on an already reduced inertia.
 bool kmeans_partials_supported(const RowSrc& src, uint32_t d);
@@ -115,6 +119,10 @@ void shard_replay_layout(pqg_ctx* ctx, uint32_t B, uint64_t k, uint32_t d, const
 void shard_pack(pqg_ctx* ctx, const RowSrc& src, const uint32_t* work, uint64_t n_fail, uint64_t k,
                 uint32_t d, const uint64_t* offsets, const uint32_t* perm, uint64_t n, const uint32_t* cnt,
                 const uint64_t* pre, uint64_t* offcnt, float* vals);
+void shard_replay_step(pqg_ctx* ctx, const RowSrc& src, const uint32_t* work, uint64_t n_fail, uint64_t k,
+                       uint32_t d, const uint64_t* offsets, const uint32_t* perm, uint64_t n, double* run);
+void shard_replay_finish(pqg_ctx* ctx, const uint32_t* work, uint64_t n_fail, uint64_t k, uint32_t d, uint32_t B,
+                         const double* f64, const double* run, float* table);
 void shard_replay(pqg_ctx* ctx, const uint32_t* work, uint64_t n_fail, uint64_t k, uint32_t d, uint32_t B,
                   const double* f64, const float* vals, uint64_t stride, const uint64_t* offcnt,
                   uint32_t world, float* table);

@@ -35,10 +35,29 @@ BucketGeom bucket_geom(uint64_t n, uint64_t k) {
     return g;
 }
 
+// Accumulators a later kernel of the same update adds into (csum = 0,
+// cmax = -1, cmin = 2^30 per (problem, cluster, dim)): zeroed by the
+// histogram launch, which has the grid for it (r2e: pieces_setup's B CTAs
+// spent ~40% of its 8 us on this).
+struct SumInit {
+    double* csum = nullptr;
+    int* cmax = nullptr;
+    int* cmin = nullptr;
+    uint64_t count = 0;
+};
+
 __global__ void hist_kernel(const uint32_t* keys, uint64_t n, uint64_t k, uint32_t ntiles, uint32_t T,
-                            uint32_t* tile_counts) {
+                            uint32_t* tile_counts, SumInit zi) {
     extern __shared__ uint32_t hist[];
     const uint32_t tile = blockIdx.x, b = blockIdx.y;
+    if (zi.count) {
+        const uint64_t nthr = uint64_t(gridDim.x) * gridDim.y * blockDim.x;
+        for (uint64_t e = (uint64_t(b) * gridDim.x + tile) * blockDim.x + threadIdx.x; e < zi.count; e += nthr) {
+            zi.csum[e] = 0.0;
+            zi.cmax[e] = -1;
+            zi.cmin[e] = 1 << 30;
+        }
+    }
     for (uint64_t c = threadIdx.x; c < k; c += blockDim.x) hist[c] = 0;
     __syncthreads();
     const uint64_t r0 = uint64_t(tile) * T;
@@ -329,6 +348,64 @@ __global__ void partial_sum_kernel(const double* v, uint64_t n, uint64_t chunk, 
     for (uint64_t i = c0 + threadIdx.x; i < c1; i += kRedThreads) s = __dadd_rn(s, vb[i]);
     s = block_sum(s);
     if (threadIdx.x == 0) parts[uint64_t(b) * gridDim.x + blockIdx.x] = s;
+}
+
+// proj/src/kmeans.cpp:93-100 for problem b, every thread of a kRedThreads
+// block calling it (parts read through L2: other blocks wrote them)
+__device__ void stop_rule(const double* parts, uint32_t nparts, uint32_t b, uint32_t max_iters, double tol,
+                          const KMeansState& st, const uint64_t* nb) {
+    const uint32_t itd = st.iters[b] + 1;
+    uint64_t cnt = nparts;
+    if (nb) {
+        uint64_t chunk;
+        inertia_parts(nb[b], cnt, chunk);
+    }
+    double s = 0.0;
+    for (uint32_t i = threadIdx.x; i < cnt; i += kRedThreads)
+        s = __dadd_rn(s, __ldcg(parts + uint64_t(b) * nparts + i));
+    s = block_sum(s);
+    if (threadIdx.x != 0) return;
+    st.inertia[b] = s;
+    if (st.per_iter) st.per_iter[uint64_t(b) * max_iters + (itd - 1)] = s;
+    st.iters[b] = itd;
+    const double prev = st.prev[b];
+    const double floor1 = prev > 1.0 ? prev : 1.0;
+    if ((itd > 1 && prev - s < tol * floor1) || itd == max_iters) {
+        st.active[b] = 0;
+        return;
+    }
+    st.prev[b] = s;
+}
+
+// The inertia's partial sums with the stop rule fused (r2e): the block that
+// completes a problem's parts (ticket) applies the rule; tickets re-armed.
+__global__ void partial_sum_stop_kernel(const double* v, uint64_t n, uint64_t chunk, double* parts,
+                                        const uint64_t* nb, uint32_t max_iters, double tol, KMeansState st) {
+    const uint32_t b = blockIdx.y;
+    if (!st.active[b]) return;
+    uint64_t nn = n, np = gridDim.x;
+    if (nb) {
+        nn = nb[b];
+        inertia_parts(nn, np, chunk);
+        if (blockIdx.x >= np) return;
+    }
+    const uint64_t c0 = uint64_t(blockIdx.x) * chunk;
+    const uint64_t c1 = min64(nn, c0 + chunk);
+    const double* vb = v + uint64_t(b) * n;
+    double s = 0.0;
+    for (uint64_t i = c0 + threadIdx.x; i < c1; i += kRedThreads) s = __dadd_rn(s, vb[i]);
+    s = block_sum(s);
+    __shared__ unsigned last;
+    if (threadIdx.x == 0) {
+        parts[uint64_t(b) * gridDim.x + blockIdx.x] = s;
+        __threadfence();
+        last = atomicAdd(st.tickets + b, 1u) == unsigned(np - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    stop_rule(parts, gridDim.x, b, max_iters, tol, st, nb);
+    if (threadIdx.x == 0) st.tickets[b] = 0u;
 }
 
 __global__ void stop_kernel(const double* parts, uint32_t nparts, uint32_t it, uint32_t max_iters,
@@ -622,11 +699,7 @@ __global__ void __launch_bounds__(1024) pieces_setup_kernel(const uint64_t* offs
     __shared__ int any_empty;
     const uint32_t b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     if (tid == 0) any_empty = 0;
-    for (uint64_t e = uint64_t(b) * k * d + tid; e < uint64_t(b + 1) * k * d; e += blockDim.x) {
-        csum[e] = 0.0;
-        cmax[e] = -1;
-        cmin[e] = 1 << 30;
-    }
+    (void)d; (void)csum; (void)cmax; (void)cmin;  // zeroed by the histogram launch (SumInit)
     const uint64_t* off = offsets + uint64_t(b) * (k + 1);
     const uint64_t per = (k + blockDim.x - 1) / blockDim.x;
     const uint64_t c0 = min64(k, tid * per), c1 = min64(k, c0 + per);
@@ -708,6 +781,11 @@ __global__ void __launch_bounds__(kMeanThreads, 4) mean_pieces_kernel(
     const uint32_t g = lane / DG, q = lane - g * DG;
     double s[4] = {0.0, 0.0, 0.0, 0.0};
     int emax[4] = {-1, -1, -1, -1}, emin[4] = {1 << 30, 1 << 30, 1 << 30, 1 << 30};
+    // r2e: the exponent range from the magnitude bits a = bits << 1 (sign
+    // dropped, biased exponent in bits 31..24): max a, and min (a - 1), which
+    // wraps zeros to 0xFFFFFFFF -- two integer min/max per value instead of
+    // the extract / test / clamp chain (the kernel was ALU-bound, ncu r2e 65%)
+    uint32_t amax[4] = {0u, 0u, 0u, 0u}, amin1[4] = {~0u, ~0u, ~0u, ~0u};
     if (g < G) {
         float4 v[8];
         if (!mr.perm) {
@@ -729,12 +807,15 @@ __global__ void __launch_bounds__(kMeanThreads, 4) mean_pieces_kernel(
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 s[j] = __dadd_rn(s[j], (double)e4[j]);
-                const int e = int((__float_as_uint(e4[j]) >> 23) & 0xFFu);
-                if (e4[j] != 0.f) {
-                    emax[j] = max(emax[j], e);
-                    emin[j] = min(emin[j], max(e, 1));
-                }
+                const uint32_t a2 = __float_as_uint(e4[j]) * 2u;
+                amax[j] = max(amax[j], a2);
+                amin1[j] = min(amin1[j], a2 - 1u);
             }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (amax[j] != 0u) emax[j] = int(amax[j] >> 24);
+            if (amin1[j] != ~0u) emin[j] = max(int((amin1[j] + 1u) >> 24), 1);
         }
     }
     for (uint32_t h = 1; h < G; ++h) {  // groups into group 0 (exact: any order)
@@ -1017,12 +1098,59 @@ __global__ void __launch_bounds__(kMeanThreads) mean_exact_warp_kernel(
 // Empty-cluster repair, proj/src/kmeans.cpp:122-130: for each empty cluster in
 // ascending order take the row with the largest pre-update distance (first
 // such row on ties), copy it, zero its distance.
+__device__ void reseed_problem(const float* x, uint64_t ldx, uint32_t col_stride, uint64_t n,
+                               uint32_t d, uint64_t k, const uint64_t* offsets, double* dist,
+                               float* table, const uint64_t* nb);
+
+// The next pass's centroid norms (cnorm non-null, r2e): norms_kernel's
+// values -- ||c||^2 in fp64 in t order rounded to fp32, and the problem's max
+// ||c|| rounded up -- computed by the problem's reseed block once its table
+// is final, instead of a separate launch at the head of every pass.
+__device__ void problem_norms(const float* table, uint32_t b, uint64_t k, uint32_t d, float* cnorm,
+                              float* cmax) {
+    __shared__ unsigned wmax[32];
+    unsigned mx = 0u;
+    for (uint64_t c = threadIdx.x; c < k; c += blockDim.x) {
+        const float* cp = table + (uint64_t(b) * k + c) * d;
+        double s = 0.0;
+        for (uint32_t t0 = 0; t0 < d; t0 += 8) {
+            float v[8];  // the row's loads issued together (clamped, unpredicated)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = cp[min(t0 + u, d - 1)];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (t0 + u < d) s = __dadd_rn(s, __dmul_rn((double)v[u], (double)v[u]));
+        }
+        cnorm[uint64_t(b) * k + c] = __double2float_rn(s);
+        mx = max(mx, __float_as_uint(__double2float_ru(sqrt(s))));
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (uint32_t w = 1; w < (blockDim.x >> 5); ++w) mx = max(mx, wmax[w]);
+        cmax[b] = __uint_as_float(mx);
+    }
+}
+
 __global__ void reseed_kernel(const float* x, uint64_t ldx, uint32_t col_stride, uint64_t n,
                               uint32_t d, uint64_t k, const uint64_t* offsets, double* dist,
                               float* table, const int* has_empty, const int* active,
-                              const uint64_t* nb) {
+                              const uint64_t* nb, float* cnorm, float* cmax) {
     const uint32_t b = blockIdx.x;
-    if ((active && !active[b]) || !has_empty[b]) return;
+    if (active && !active[b]) return;
+    if (has_empty[b]) reseed_problem(x, ldx, col_stride, n, d, k, offsets, dist, table, nb);
+    if (cnorm) {
+        __syncthreads();
+        problem_norms(table, b, k, d, cnorm, cmax);
+    }
+}
+
+__device__ void reseed_problem(const float* x, uint64_t ldx, uint32_t col_stride, uint64_t n,
+                               uint32_t d, uint64_t k, const uint64_t* offsets, double* dist,
+                               float* table, const uint64_t* nb) {
+    const uint32_t b = blockIdx.x;
     const uint64_t nn = nb ? nb[b] : n;
     __shared__ double sv[32];
     __shared__ uint64_t si[32];
@@ -1097,10 +1225,18 @@ void exclusive_scan_u32(pqg_ctx* ctx, const uint32_t* in, uint64_t* out, uint64_
 }
 
 static void bucket_impl(pqg_ctx* ctx, const uint32_t* keys, uint64_t n, uint32_t B, uint64_t k,
-                        Bucketing out, const RowCopy* rows, const uint64_t* nb) {
+                        Bucketing out, const RowCopy* rows, const uint64_t* nb, SumInit zi = SumInit{}) {
     if (k > 16384) fail(PQG_EUNSUPPORTED, "bucketing supports at most 16384 lists/clusters");
     if (n == 0) {
         PQG_CUDA(cudaMemsetAsync(out.offsets, 0, sizeof(uint64_t) * B * (k + 1), ctx->stream));
+        if (zi.count) {
+            PQG_CUDA(cudaMemsetAsync(zi.csum, 0, sizeof(double) * zi.count, ctx->stream));
+            PQG_CUDA(cudaMemsetAsync(zi.cmax, 0xff, sizeof(int) * zi.count, ctx->stream));
+            std::vector<int> big(zi.count, 1 << 30);
+            PQG_CUDA(cudaMemcpyAsync(zi.cmin, big.data(), sizeof(int) * zi.count, cudaMemcpyHostToDevice,
+                                     ctx->stream));
+            PQG_CUDA(cudaStreamSynchronize(ctx->stream));
+        }
         return;
     }
     const BucketGeom g = bucket_geom(n, k);
@@ -1109,7 +1245,7 @@ static void bucket_impl(pqg_ctx* ctx, const uint32_t* keys, uint64_t n, uint32_t
     const size_t hsmem = sizeof(uint32_t) * k;
     set_smem(hist_kernel, hsmem);
     launch(ctx, "bucket", hist_kernel, dim3(g.ntiles, B), dim3(256), hsmem, keys, n, k, g.ntiles, g.T,
-           tile_counts);
+           tile_counts, zi);
     exclusive_scan<uint32_t>(ctx, tile_counts, tile_base, uint64_t(B) * k * g.ntiles);
     const size_t ssmem = sizeof(uint32_t) * k * g.W;
     if (rows) {
@@ -1161,6 +1297,11 @@ void kmeans_inertia_and_stop(pqg_ctx* ctx, const double* dist, uint64_t n, uint3
     uint64_t nparts, chunk;
     inertia_parts(n, nparts, chunk);
     double* parts = scratch<double>(ctx, uint64_t(B) * nparts);
+    if (st.tickets) {
+        launch(ctx, "inertia", partial_sum_stop_kernel, dim3(unsigned(nparts), B), dim3(kRedThreads), 0,
+               dist, n, chunk, parts, nb, max_iters, tol, st);
+        return;
+    }
     launch(ctx, "inertia", partial_sum_kernel, dim3(unsigned(nparts), B), dim3(kRedThreads), 0,
            dist, n, chunk, parts, (const int*)st.active, nb);
     launch(ctx, "inertia", stop_kernel, dim3(B), dim3(kRedThreads), 0, (const double*)parts,
@@ -1179,7 +1320,7 @@ void rows_sum_f64(pqg_ctx* ctx, const double* v, uint64_t n, uint32_t B, double*
 
 void kmeans_update(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint32_t d,
                    float* table, uint64_t k, const uint32_t* assign, double* dist,
-                   const int* active, const uint64_t* nb) {
+                   const int* active, const uint64_t* nb, float* cnorm, float* cmax) {
     if (uint64_t(B) * k > 0x7FFFFFFFull) fail(PQG_EUNSUPPORTED, "kmeans: too many clusters");
     // Default: the stable permutation, the sums gathering rows through it.
     // PQG_KM_COPY=1 buckets a copy of the rows instead (measured r1 at 100k x
@@ -1188,6 +1329,19 @@ void kmeans_update(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint
     const char* ce = std::getenv("PQG_KM_COPY");
     const bool copy = ce && ce[0] == '1' && uint64_t(n) * d <= 0xFFFFFFFFull;
     Bucketing bk{scratch<uint64_t>(ctx, uint64_t(B) * (k + 1)), nullptr};
+    const uint64_t ncl = uint64_t(B) * k;
+    const char* mean_env = std::getenv("PQG_KM_MEAN");
+    const bool pieces = d % 4 == 0 && d <= 128 && !(mean_env && mean_env[0] != 'p') &&
+                        (copy ? true
+                              : ((src.ldx | src.col_stride) & 3u) == 0 &&
+                                    (reinterpret_cast<uintptr_t>(src.x) & 15u) == 0);
+    SumInit zi;
+    if (pieces) {
+        zi.csum = scratch<double>(ctx, ncl * d);
+        zi.cmax = scratch<int>(ctx, ncl * d);
+        zi.cmin = scratch<int>(ctx, ncl * d);
+        zi.count = ncl * d;
+    }
     const float* mx = src.x;
     uint64_t mldx = src.ldx;
     uint32_t mcs = src.col_stride;
@@ -1200,30 +1354,24 @@ void kmeans_update(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint
         rc.out = scratch<float>(ctx, uint64_t(B) * n * d);
         rc.vec = (d % 4) == 0 && (src.ldx % 4) == 0 && (src.col_stride % 4) == 0 &&
                  (reinterpret_cast<uintptr_t>(src.x) & 15u) == 0;
-        bucket_impl(ctx, assign, n, B, k, bk, &rc, nb);
+        bucket_impl(ctx, assign, n, B, k, bk, &rc, nb, zi);
         mx = rc.out;
         mldx = d;
         mcs = uint32_t(n * d);
     } else {
         bk.perm = scratch<uint32_t>(ctx, uint64_t(B) * n);
-        bucket_impl(ctx, assign, n, B, k, bk, nullptr, nb);
+        bucket_impl(ctx, assign, n, B, k, bk, nullptr, nb, zi);
     }
     int* has_empty = scratch<int>(ctx, B);
-    const uint64_t ncl = uint64_t(B) * k;
-    const char* mean_env = std::getenv("PQG_KM_MEAN");
-    const bool pieces = d % 4 == 0 && d <= 128 && !(mean_env && mean_env[0] != 'p') &&
-                        (copy ? (reinterpret_cast<uintptr_t>(mx) & 15u) == 0
-                              : ((src.ldx | src.col_stride) & 3u) == 0 &&
-                                    (reinterpret_cast<uintptr_t>(src.x) & 15u) == 0);
     if (pieces) {
         const PieceGeom pg = piece_geom(d, n, k);
         if (uint64_t(B) * pg.PP > 0xFFFFFFFFull) fail(PQG_EUNSUPPORTED, "kmeans: too many pieces");
         uint32_t* piece_start = scratch<uint32_t>(ctx, uint64_t(B) * k);
         PieceDesc* pieces_d = scratch<PieceDesc>(ctx, uint64_t(B) * pg.PP);
         PieceStat* stats = scratch<PieceStat>(ctx, uint64_t(B) * pg.PP * d);
-        double* csum = scratch<double>(ctx, ncl * d);
-        int* cmax = scratch<int>(ctx, ncl * d);
-        int* cmin = scratch<int>(ctx, ncl * d);
+        double* csum = zi.csum;
+        int* cmax = zi.cmax;
+        int* cmin = zi.cmin;
         unsigned long long* work_count = scratch<unsigned long long>(ctx, 1);
         uint64_t* work = scratch<uint64_t>(ctx, ncl * d);
         launch(ctx, "kmeans_sum", pieces_setup_kernel, dim3(B), dim3(1024), 0, (const uint64_t*)bk.offsets, k,
@@ -1258,7 +1406,7 @@ void kmeans_update(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint
         }
     }
     launch(ctx, "reseed", reseed_kernel, dim3(B), dim3(1024), 0, src.x, src.ldx, src.col_stride, n,
-           d, k, (const uint64_t*)bk.offsets, dist, table, (const int*)has_empty, active, nb);
+           d, k, (const uint64_t*)bk.offsets, dist, table, (const int*)has_empty, active, nb, cnorm, cmax);
 }
 
 // ---- one rank's side of a row-sharded fit (kmshard.cu, pqg_kmshard_*) -----
@@ -1274,7 +1422,12 @@ void kmeans_local_partials(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t
                            uint64_t k, const uint32_t* assign, const int* active, uint64_t* offsets,
                            uint32_t* perm, double* csum, int* cmax, int* cmin) {
     Bucketing bk{offsets, perm};
-    bucket_impl(ctx, assign, n, B, k, bk, nullptr, nullptr);
+    SumInit zi;
+    zi.csum = csum;
+    zi.cmax = cmax;
+    zi.cmin = cmin;
+    zi.count = uint64_t(B) * k * d;
+    bucket_impl(ctx, assign, n, B, k, bk, nullptr, nullptr, zi);
     const PieceGeom pg = piece_geom(d, n, k);
     if (uint64_t(B) * pg.PP > 0xFFFFFFFFull) fail(PQG_EUNSUPPORTED, "kmeans: too many pieces");
     uint32_t* piece_start = scratch<uint32_t>(ctx, uint64_t(B) * k);

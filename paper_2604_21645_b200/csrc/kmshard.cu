@@ -159,6 +159,78 @@ __global__ void replay_kernel(const uint32_t* work, uint64_t n_fail, uint64_t k,
     }
 }
 
+// Chained replay (r2e): the reference's chain of a replay column runs over
+// rank 0's members, then rank 1's, ...; rank r continues it from the running
+// sums rank r-1 hands over (run[p], one fp64 per column) with its own
+// members in local row order -- no member values cross ranks.  Warp per
+// column, 32 members per step: a step whose additions provably cannot round
+// (every partial sum a multiple of 2^lq and below 2^(lq+53), lq from the
+// running sum's lowest set bit and the step's smallest ulp -- any order gives
+// the same exact sum) is added as one warp sum, otherwise lane 0 walks the
+// 32 members as the reference chains them (kmeans.cpp:103-111).
+__device__ __forceinline__ int lowbit_exp64(double r) {  // log2 of r's lowest set bit (r normal, != 0)
+    const unsigned long long sb = __double_as_longlong(r);
+    const int E = int((sb >> 52) & 0x7FF);
+    const unsigned long long mant = (sb & ((1ull << 52) - 1)) | (1ull << 52);
+    return E - 1075 + (__ffsll((long long)mant) - 1);
+}
+
+__global__ void replay_step_kernel(RowSrc src, const uint32_t* work, uint64_t n_fail, uint64_t k, uint32_t d,
+                                   const uint64_t* offsets, const uint32_t* perm, uint64_t n, double* run) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t p = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (p >= n_fail) return;
+    const uint64_t e = work[p], bc = e / d, t = e - bc * d, b = bc / k, c = bc - b * k;
+    const uint64_t* off = offsets + b * (k + 1);
+    const uint32_t* pb = perm + b * n;
+    const float* xb = src.x + b * src.col_stride + t;
+    double s = run[p];
+    for (uint64_t m0 = off[c]; m0 < off[c + 1]; m0 += 32) {
+        const uint64_t m = m0 + lane;
+        const uint32_t nm = uint32_t(min64(uint64_t(32), off[c + 1] - m0));
+        const float v = m < off[c + 1] ? __ldg(xb + uint64_t(__ldg(pb + m)) * src.ldx) : 0.f;
+        const int eb = int((__float_as_uint(v) >> 23) & 0xFFu);
+        int ehi = v != 0.f ? eb : -1;
+        int elo = v != 0.f ? max(eb, 1) : (1 << 30);
+        double ws = (double)v;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            ws = __dadd_rn(ws, __shfl_xor_sync(0xffffffffu, ws, o));
+            ehi = max(ehi, __shfl_xor_sync(0xffffffffu, ehi, o));
+            elo = min(elo, __shfl_xor_sync(0xffffffffu, elo, o));
+        }
+        bool exact;
+        if (ehi < 0) {
+            exact = true;  // all zeros
+        } else if (ehi == 255 || !isfinite(s)) {
+            exact = false;
+        } else {
+            int lq = elo - 150;  // log2 ulp of the smallest nonzero value
+            if (s != 0.0) lq = min(lq, lowbit_exp64(s));
+            // every partial sum is at most |s| + 32 values below 2^(ehi-126)
+            const double bound = __dadd_ru(fabs(s), ldexp(1.0, ehi - 121));
+            const int lb = int((__double_as_longlong(bound) >> 52) & 0x7FF) - 1022;
+            exact = lb - lq <= 53;
+        }
+        if (exact) {
+            s = __dadd_rn(s, ws);  // ws is exact too (a subset sum)
+        } else {
+            for (uint32_t j = 0; j < nm; ++j) s = __dadd_rn(s, (double)__shfl_sync(0xffffffffu, v, j));
+        }
+    }
+    if (lane == 0) run[p] = s;
+}
+
+__global__ void replay_finish_kernel(const uint32_t* work, uint64_t n_fail, uint64_t k, uint32_t d, uint32_t B,
+                                     const double* f64, const double* run, float* table) {
+    for (uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < n_fail;
+         p += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t e = work[p], bc = e / d;
+        const double cnt = f64[uint64_t(B) * k * d + bc];
+        table[e] = __double2float_rn(__dmul_rn(run[p], __ddiv_rn(1.0, cnt)));
+    }
+}
+
 // block per problem: the rank's E best positive (dist desc, global index asc)
 // candidates, plus its local row 0 in slot E (the merge uses rank 0's = global
 // row 0 once the positive distances run out)
@@ -343,6 +415,20 @@ void shard_replay(pqg_ctx* ctx, const uint32_t* work, uint64_t n_fail, uint64_t 
     if (n_fail == 0) return;
     launch(ctx, "kmshard", replay_kernel, dim3(grid1d(n_fail, 64, 4096)), dim3(64), 0, work, n_fail, k, d, B,
            f64, vals, stride, offcnt, world, table);
+}
+
+void shard_replay_step(pqg_ctx* ctx, const RowSrc& src, const uint32_t* work, uint64_t n_fail, uint64_t k,
+                       uint32_t d, const uint64_t* offsets, const uint32_t* perm, uint64_t n, double* run) {
+    if (n_fail == 0) return;
+    launch(ctx, "kmshard", replay_step_kernel, dim3(grid1d(n_fail * 32, kThreads)), dim3(kThreads), 0, src, work,
+           n_fail, k, d, offsets, perm, n, run);
+}
+
+void shard_replay_finish(pqg_ctx* ctx, const uint32_t* work, uint64_t n_fail, uint64_t k, uint32_t d, uint32_t B,
+                         const double* f64, const double* run, float* table) {
+    if (n_fail == 0) return;
+    launch(ctx, "kmshard", replay_finish_kernel, dim3(grid1d(n_fail, 128, 4096)), dim3(128), 0, work, n_fail, k, d,
+           B, f64, run, table);
 }
 
 void shard_reseed_candidates(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint32_t d,

@@ -122,6 +122,25 @@ class Comm:
         pad[: t.numel()] = t
         return self.allgather_equal(pad), stride
 
+    def _peer(self, r: int) -> int:
+        return r if self.group is None else self.dist.get_global_rank(self.group, r)
+
+    def recv_prev_(self, t):
+        """Rank r > 0 receives t (in place) from rank r - 1."""
+        if self.rank > 0:
+            self.dist.recv(t, src=self._peer(self.rank - 1), group=self.group)
+        return t
+
+    def send_next(self, t):
+        """Rank r < world - 1 sends t to rank r + 1."""
+        if self.rank < self.world - 1:
+            self.dist.send(t.contiguous(), dst=self._peer(self.rank + 1), group=self.group)
+
+    def broadcast_(self, t, src: int):
+        if self.world > 1:
+            self.dist.broadcast(t, src=self._peer(src), group=self.group)
+        return t
+
     def allgather_equal(self, t):
         """[world, *t.shape]: every rank's equally shaped t, rank order."""
         import torch
@@ -277,6 +296,13 @@ class CudaBackend:
                                                  self._p(all_vals.contiguous()), stride,
                                                  self._p(all_offcnt.contiguous()), world), "kmshard_replay")
 
+    def shard_replay_step(self, s, run):
+        self.L.check(self.lib.pqg_kmshard_replay_step(self.ctx.h, s["h"], self._p(run)), "kmshard_replay_step")
+
+    def shard_replay_finish(self, s, tables, f64, run):
+        self.L.check(self.lib.pqg_kmshard_replay_finish(self.ctx.h, s["h"], self._p(tables), self._p(f64),
+                                                        self._p(run)), "kmshard_replay_finish")
+
     def shard_reseed_candidates(self, s, row0, E):
         torch = self.torch
         dev = s["rows"].device
@@ -361,15 +387,23 @@ class ShardedFit:
 
 def kmeans_fit_sharded(comm: Comm, backend, local_rows, B: int, d: int, col_stride: int, k: int,
                        max_iters: int, seeds, tol: float = 1e-4, stats: dict | None = None,
-                       force_exchange: bool = False) -> ShardedFit:
+                       force_exchange: bool = False, replay: str | None = None) -> ShardedFit:
     """B batched k-means problems (B = M subspaces for pq_fit, B = 1 for the
     coarse quantizer) over rows sharded by rank; bit-identical to the
     single-process fit (see module docstring).  ``stats`` (optional) receives
     the exchange volume: bytes all-reduced / all-gathered per iteration.
     A 1-rank group has nothing to exchange: it runs the single-process fit
     (one device-resident graph per iteration, no host round trip) unless
-    ``force_exchange`` (the tests drive the exchange protocol at world 1 too)."""
+    ``force_exchange`` (the tests drive the exchange protocol at world 1 too).
+    ``replay``: "chain" (default; PQG_SHARD_REPLAY overrides) passes the
+    row-order chains of the inexact columns rank to rank; "gather" is the r2
+    protocol that all-gathers every rank's members of those columns."""
+    import os
+
     import torch
+    replay = replay or os.environ.get("PQG_SHARD_REPLAY", "chain")
+    if replay not in ("chain", "gather"):
+        raise ValueError(f"replay must be 'chain' or 'gather', not {replay!r}")
     dev = local_rows.device
     if comm.world == 1 and not force_exchange and hasattr(backend, "fit_local") and k >= 1 and \
             k <= local_rows.shape[0] and max_iters >= 1 and tol >= 0:
@@ -399,7 +433,8 @@ def kmeans_fit_sharded(comm: Comm, backend, local_rows, B: int, d: int, col_stri
         return _kmeans_fit_replicated(comm, backend, local_rows, counts, B, d, col_stride, k, max_iters,
                                       seeds, tol)
     st = stats if stats is not None else {}
-    st.update(allreduce_bytes=0, allgather_bytes=0, replay_columns=0, reseeds=0, iterations=0)
+    st.update(allreduce_bytes=0, allgather_bytes=0, chain_bytes=0, replay_columns=0, reseeds=0, iterations=0,
+              replay=replay)
     try:
         init = np.concatenate([backend.init_rows(n, k, int(seeds[b])) for b in range(B)])
         bits = backend.shard_init_table(s, init, row0)
@@ -411,7 +446,19 @@ def kmeans_fit_sharded(comm: Comm, backend, local_rows, B: int, d: int, col_stri
             st["allreduce_bytes"] += f64.numel() * 8 + u8.numel()
             st["iterations"] += 1
             n_fail, max_empty, any_active = backend.shard_apply(s, tables, f64, u8)
-            if n_fail:  # columns whose sum may round: the row-order replay
+            if n_fail and replay == "chain":
+                # columns whose sum may round: the row-order chain passes rank
+                # to rank (one fp64 per column per hop), then the last rank's
+                # sums are broadcast -- no member values cross ranks
+                run = torch.zeros(n_fail, dtype=torch.float64, device=f64.device)
+                comm.recv_prev_(run)
+                backend.shard_replay_step(s, run)
+                comm.send_next(run)
+                comm.broadcast_(run, comm.world - 1)
+                backend.shard_replay_finish(s, tables, f64, run)
+                st["replay_columns"] += n_fail
+                st["chain_bytes"] += 2 * run.numel() * 8 * (comm.world > 1)
+            elif n_fail:  # r2 protocol: every rank's members all-gathered
                 vals, offcnt = backend.shard_pack(s, n_fail)  # padded to the common stride
                 all_vals, stride = comm.allgather_equal(vals), vals.numel()
                 all_oc = comm.allgather_equal(offcnt)

@@ -249,6 +249,24 @@ class ShardOracleBackend(OracleBackend):
             bc = int(e) // d
             tab.reshape(-1)[e] = np.float32(acc * (1.0 / f64[nkd + bc]))
 
+    def shard_replay_step(self, s, run):
+        k, d = s["k"], s["d"]
+        r = _np(run)
+        for p, e in enumerate(s["work"]):
+            bc, t = divmod(int(e), d)
+            b, c = divmod(bc, k)
+            acc = float(r[p])
+            for v in self._cols(s, b)[np.flatnonzero(s["assign"][b] == c), t].tolist():
+                acc += v  # the reference's chain, kmeans.cpp:103-111, local row order
+            r[p] = acc
+
+    def shard_replay_finish(self, s, tables, f64t, run):
+        B, k, d = s["B"], s["k"], s["d"]
+        f64, tab, r = _np(f64t), _np(tables), _np(run)
+        nkd = B * k * d
+        for p, e in enumerate(s["work"]):
+            tab.reshape(-1)[e] = np.float32(r[p] * (1.0 / f64[nkd + int(e) // d]))
+
     def shard_reseed_candidates(self, s, row0, E):
         B, d = s["B"], s["d"]
         cd = np.full((B, E + 1), -1.0)

@@ -78,7 +78,13 @@ def run_rank_stress(rank, world, port, outdir):
     fit = D.kmeans_fit_sharded(comm, be, local, 1, 8, 0, 40, 9, [2], 0.0, stats=st)
     res["km_tables"], res["km_iters"] = fit.tables.numpy(), fit.iterations_run
     res["km_assign"] = fit.assignments.numpy().view(np.uint32)
-    res["stats"] = np.array([st["replay_columns"], st["reseeds"], st["iterations"]])
+    res["stats"] = np.array([st["replay_columns"], st["reseeds"], st["iterations"], st["chain_bytes"],
+                             st["allgather_bytes"]])
+    # the r2 protocol (members all-gathered) must give the same fit
+    sg = {}
+    fg = D.kmeans_fit_sharded(comm, be, local, 1, 8, 0, 40, 9, [2], 0.0, stats=sg, replay="gather")
+    res["kmg_tables"] = fg.tables.numpy()
+    res["stats_g"] = np.array([sg["replay_columns"], sg["chain_bytes"], sg["allgather_bytes"]])
     res["pq_tables"] = D.pq_fit_sharded(comm, be, local, 2, 32, 8, 7).numpy()
     np.savez(os.path.join(outdir, f"stress{rank}.npz"), **res)
     dist.barrier()

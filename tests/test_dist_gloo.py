@@ -83,6 +83,12 @@ def test_sharded_kmeans_exchange_paths(tmp_path, orc, world):
         assert int(rr["km_iters"][0]) == ref["iterations_run"]
     assert r[0]["stats"][0] > 0, "the row-order replay path was not exercised"
     assert r[0]["stats"][1] > 0, "the reseed path was not exercised"
+    # the chained replay (default) moves one fp64 per column per hop and no
+    # member values; the r2 all-gather protocol gives the identical fit
+    assert r[0]["stats"][3] > 0 and r[0]["stats"][4] == 0
+    assert r[0]["stats_g"][0] == r[0]["stats"][0] and r[0]["stats_g"][1] == 0 and r[0]["stats_g"][2] > 0
+    for rr in r:
+        assert np.array_equal(rr["kmg_tables"][0].view(np.uint32), ref["centroids"].view(np.uint32))
     t, _, _ = orc.pq_fit(x, 2, 32, 8, 7)
     for rr in r:
         assert np.array_equal(rr["pq_tables"].view(np.uint32), t.view(np.uint32))

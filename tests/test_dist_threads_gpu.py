@@ -42,6 +42,21 @@ class _ThreadDist:
         for o, g in zip(outs, self._exchange(t)):
             o.copy_(g.to(o.device))
 
+    def send(self, t, dst, group=None):
+        import torch
+        torch.cuda.current_stream().synchronize()
+        with self.sh["cv"]:
+            self.sh["p2p"][(self.rank, dst)] = t.clone()
+            self.sh["cv"].notify_all()
+
+    def recv(self, t, src, group=None):
+        with self.sh["cv"]:
+            self.sh["cv"].wait_for(lambda: (src, self.rank) in self.sh["p2p"], timeout=120)
+            t.copy_(self.sh["p2p"].pop((src, self.rank)).to(t.device))
+
+    def broadcast(self, t, src, group=None):
+        t.copy_(self._exchange(t)[src].to(t.device))
+
     def all_reduce(self, t, op="sum", group=None, async_op=False):
         import torch
         got = self._exchange(t)
@@ -60,7 +75,7 @@ def _run_world(world, x, fn):
     import torch
 
     from paper_2604_21645_b200 import dist as D
-    shared = {"slots": [None] * world, "bar": threading.Barrier(world)}
+    shared = {"slots": [None] * world, "bar": threading.Barrier(world), "cv": threading.Condition(), "p2p": {}}
     out, errs = [None] * world, []
 
     def body(rank):
@@ -98,15 +113,18 @@ def _stress():
     return stress_data()
 
 
+@pytest.mark.parametrize("replay", ["chain", "gather"])
 @pytest.mark.parametrize("world", [1, 2, 3])
-def test_kmshard_coarse_exchange_paths(orc, world):
+def test_kmshard_coarse_exchange_paths(orc, world, replay):
+    """Both replay protocols -- the chain handed rank to rank (r2e default)
+    and the all-gathered members (r2) -- equal the oracle bit for bit."""
     from paper_2604_21645_b200 import dist as D
     x = _stress()
     st = [dict() for _ in range(world)]
 
     def fn(comm, be, local):
         return D.kmeans_fit_sharded(comm, be, local, 1, 8, 0, 40, 9, [2], 0.0, stats=st[comm.rank],
-                                    force_exchange=True)
+                                    force_exchange=True, replay=replay)
     res = _run_world(world, x, fn)
     ref = orc.kmeans_fit(x, 40, 9, 2, 0.0)
     for r in res:

@@ -36,6 +36,10 @@ def main():
     ap.add_argument("--queries", type=int, default=100_000)
     ap.add_argument("--sample", type=int, default=2_000_000)
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--force-exchange", action="store_true",
+                    help="run the exchange protocol even in a 1-rank group")
+    ap.add_argument("--replay", default="chain", choices=["chain", "gather"],
+                    help="row-order replay protocol of the sharded fits")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -86,15 +90,17 @@ def main():
     D.pq_fit_sharded(comm, be, train, M, KS, 1, SEED)
     D.kmeans_fit_sharded(comm, be, train, 1, Dm, 0, NLIST, 1, [SEED + M], 1e-4)
     st_pq, st_co = {}, {}
+    fx = dict(force_exchange=args.force_exchange, replay=args.replay)
     tables = timed("pq_fit", lambda: D.kmeans_fit_sharded(
-        comm, be, train, M, Dm // M, Dm // M, KS, args.iters, [SEED + m for m in range(M)], 1e-4, stats=st_pq).tables)
+        comm, be, train, M, Dm // M, Dm // M, KS, args.iters, [SEED + m for m in range(M)], 1e-4, stats=st_pq,
+        **fx).tables)
     fit_c = timed("coarse_fit", lambda: D.kmeans_fit_sharded(
-        comm, be, train, 1, Dm, 0, NLIST, args.iters, [SEED + M], 1e-4, stats=st_co))
+        comm, be, train, 1, Dm, 0, NLIST, args.iters, [SEED + M], 1e-4, stats=st_co, **fx))
     coarse = fit_c.tables.view(NLIST, Dm).contiguous()
-    out["pq_fit_exchange"] = {k_: st_pq.get(k_) for k_ in ("allreduce_bytes", "allgather_bytes", "replay_columns",
-                                                            "reseeds", "iterations")}
-    out["coarse_fit_exchange"] = {k_: st_co.get(k_) for k_ in ("allreduce_bytes", "allgather_bytes",
-                                                                "replay_columns", "reseeds", "iterations")}
+    out["pq_fit_exchange"] = {k_: st_pq.get(k_) for k_ in ("allreduce_bytes", "allgather_bytes", "chain_bytes",
+                                                            "replay_columns", "reseeds", "iterations", "replay")}
+    out["coarse_fit_exchange"] = {k_: st_co.get(k_) for k_ in ("allreduce_bytes", "allgather_bytes", "chain_bytes",
+                                                                "replay_columns", "reseeds", "iterations", "replay")}
     out["coarse_iters"] = int(np.max(fit_c.iterations_run))
     codes, rmse = timed("encode_rmse", lambda: D.encode_sharded(comm, be, x, tables))
     out["rmse"] = rmse
