@@ -161,6 +161,12 @@ int pqg_index_merge(pqg_ctx* ctx, const pqg_index* a, const pqg_index* b, pqg_in
 int pqg_index_search(pqg_ctx* ctx, const pqg_index* index, const float* queries, uint64_t nq,
                      uint64_t k, uint64_t nprobe, int has_max, double max_sq_dist,
                      uint64_t* out_ids, double* out_dists, uint32_t* out_counts);
+/* pqg_index_search that also returns each query's probe lists (out_probes:
+ * nq*nprobe u32, host or device; nullable) -- the drop-in uses them to check
+ * only the lists a query read against the caller's host index (r2e). */
+int pqg_index_search_ex(pqg_ctx* ctx, const pqg_index* index, const float* queries, uint64_t nq,
+                        uint64_t k, uint64_t nprobe, int has_max, double max_sq_dist,
+                        uint64_t* out_ids, double* out_dists, uint32_t* out_counts, uint32_t* out_probes);
 /* ivf_query_subset (ivf.cpp:230-245) for nq queries sharing one subset of
  * ids (sorted ascending, unique; PQG_EINVAL "not sorted" otherwise): hits are
  * restricted to the subset before the top-k. */

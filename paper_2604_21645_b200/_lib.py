@@ -67,6 +67,7 @@ _SIGS = {
     "pqg_index_add": (_i32, [_vp, _vp, _vp, _vp, _u64]),
     "pqg_index_merge": (_i32, [_vp, _vp, _vp, C.POINTER(_vp)]),
     "pqg_index_search": (_i32, [_vp, _vp, _vp, _u64, _u64, _u64, _i32, _f64, _vp, _vp, _vp]),
+    "pqg_index_search_ex": (_i32, [_vp, _vp, _vp, _u64, _u64, _u64, _i32, _f64, _vp, _vp, _vp, _vp]),
     "pqg_index_probe": (_i32, [_vp, _vp, _vp, _u64, _u64, _vp]),
     "pqg_index_search_subset": (_i32, [_vp, _vp, _vp, _u64, _u64, _vp, _u64, _u64, _i32, _f64, _vp,
                                        _vp, _vp]),

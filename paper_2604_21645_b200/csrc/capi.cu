@@ -1525,6 +1525,13 @@ int pqg_index_probe(pqg_ctx* ctx, const pqg_index* ix, const float* queries, uin
 int pqg_index_search(pqg_ctx* ctx, const pqg_index* ix, const float* queries, uint64_t nq,
                      uint64_t k, uint64_t nprobe, int has_max, double max_sq_dist,
                      uint64_t* out_ids, double* out_dists, uint32_t* out_counts) {
+    return pqg_index_search_ex(ctx, ix, queries, nq, k, nprobe, has_max, max_sq_dist, out_ids, out_dists,
+                               out_counts, nullptr);
+}
+
+int pqg_index_search_ex(pqg_ctx* ctx, const pqg_index* ix, const float* queries, uint64_t nq,
+                        uint64_t k, uint64_t nprobe, int has_max, double max_sq_dist,
+                        uint64_t* out_ids, double* out_dists, uint32_t* out_counts, uint32_t* out_probes) {
     return guard([&] {
         Scope sc(ctx);
         check_query(ix, k, nprobe);
@@ -1536,6 +1543,9 @@ int pqg_index_search(pqg_ctx* ctx, const pqg_index* ix, const float* queries, ui
         uint32_t* probes = scratch<uint32_t>(ctx, nq * nprobe);
         const float* luts = k <= 32 ? search_luts_async(ctx, ix, dq, nq) : nullptr;
         ivf_probe(ctx, ix->view(), dq, nq, nprobe, probes);
+        if (out_probes)
+            PQG_CUDA(cudaMemcpyAsync(out_probes, probes, sizeof(uint32_t) * nq * nprobe, cudaMemcpyDefault,
+                                     ctx->stream));
         reset_err(ctx);
         search_scan(ctx, ix, dq, nq, probes, nprobe, k, has_max, max_sq_dist, oi.dev, od.dev, oc.dev, nullptr, 0,
                     luts);

@@ -2,6 +2,7 @@
 // test_pq.cpp, test_ivf.cpp) restated against the drop-in libpqg_pqii.so
 // through the pqii headers of this repo.  A tiny CHECK harness replaces the
 // absent doctest.  Run by tests/test_facade_cpp.py on a GPU.
+#include <algorithm>
 #include <unistd.h>
 
 #include <cmath>
@@ -271,6 +272,39 @@ int main() {
                     i3.push_back(pl.ids[i]);
                 }
             CHECK(after.hits == flat_scan(cb, c3, i3, qs.row_span(3), 5).hits);
+            // r2e: a small-nprobe query verifies only the lists it probes --
+            // an in-place edit of a probed list must still be seen: expected =
+            // flat_scan over the items of the two nearest lists (fp64 probe order)
+            const auto q4 = qs.row_span(4);
+            std::vector<std::pair<double, std::size_t>> pd;
+            for (std::size_t l = 0; l < edit.nlist(); ++l) {
+                double acc = 0.0;
+                for (std::size_t t = 0; t < q4.size(); ++t) {
+                    const double df = double(q4[t]) - double(edit.coarse_centroids.row(l)[t]);
+                    acc += df * df;
+                }
+                pd.emplace_back(acc, l);
+            }
+            std::sort(pd.begin(), pd.end());
+            auto probed_flat = [&](std::size_t kk) {
+                CodeMatrix cp(0, 4, 16);
+                std::vector<std::uint64_t> ip;
+                for (int j = 0; j < 2; ++j) {
+                    const PostingList& pl = edit.lists[pd[j].second];
+                    for (std::size_t i = 0; i < pl.ids.size(); ++i) {
+                        cp.append_row_from(pl.codes, i);
+                        ip.push_back(pl.ids[i]);
+                    }
+                }
+                return flat_scan(cb, cp, ip, q4, kk).hits;
+            };
+            const auto b4 = ivf_query(edit, q4, 5, 2);
+            CHECK(b4.hits == probed_flat(5));
+            PostingList& hot = edit.lists[pd[0].second];
+            for (std::size_t i = 0; i < hot.ids.size(); ++i)
+                for (std::uint32_t m = 0; m < 4; ++m) hot.codes.set(i, m, (hot.codes.at(i, m) + 5) % 16);
+            const auto a4 = ivf_query(edit, q4, 5, 2);
+            CHECK(a4.hits == probed_flat(5));
         }
         // k > 32 (the CTA-wide path) and k beyond n_items saturating (test_ivf.cpp:255-259)
         const QueryResult sat = ivf_query(ix, qs.row_span(0), 1000, ix.nlist());
