@@ -405,6 +405,29 @@ def run_ours(args, rank, world, local):
         torch.cuda.synchronize()
         sf_def_s = max_over_ranks(time.perf_counter() - t0, world)
         same = bool(torch.equal(sf.tables, tables)) if world == 1 else None
+        # the same protocol with the loop in C++ and NCCL issued by the library
+        # (pqg_kmeans_fit_sharded, csrc/kmnccl.cu), exchange always run
+        native = None
+        try:
+            nc = D.NcclComm(comm, be)
+            try:
+                D.kmeans_fit_sharded_native(nc, train, HEAD_M, ds, ds, HEAD_KS, 2, seeds)  # warm-up
+                torch.cuda.synchronize()
+                barrier(world)
+                stn = {}
+                t0 = time.perf_counter()
+                sfn = D.kmeans_fit_sharded_native(nc, train, HEAD_M, ds, ds, HEAD_KS, FIT_ITERS, seeds, 1e-4,
+                                                  stats=stn)
+                torch.cuda.synchronize()
+                nat_s = max_over_ranks(time.perf_counter() - t0, world)
+                native = {"seconds": nat_s, "iters_per_s": int(np.max(sfn.iterations_run)) / nat_s,
+                          "host": stn.get("host"), "replay_columns": stn.get("replay_columns"),
+                          "bit_identical_to_single_process":
+                              bool(torch.equal(sfn.tables, tables)) if world == 1 else None}
+            finally:
+                nc.close()
+        except Exception as e:  # NCCL unavailable: reported, not fatal
+            native = {"unavailable": str(e)[:200]}
         sharded_fit = {"global_sample_rows": SAMPLE * world, "iters_run": int(np.max(sf.iterations_run)),
                        "seconds": sf_s, "iters_per_s": int(np.max(sf.iterations_run)) / sf_s,
                        "single_process_seconds": fit_s,
@@ -416,7 +439,8 @@ def run_ours(args, rank, world, local):
                        "replay": st.get("replay"),
                        "chain_bytes_per_iter": st.get("chain_bytes", 0) / max(1, st["iterations"]),
                        "allgather_bytes_per_iter": st.get("allgather_bytes", 0) / max(1, st["iterations"]),
-                       "bit_identical_to_single_process": same}
+                       "bit_identical_to_single_process": same,
+                       "native_host": native}
 
     # ---- headline encode, timed with profiling of the dominant kernel
     codes = torch.empty((N_ROWS, HEAD_M), dtype=torch.uint8, device="cuda")

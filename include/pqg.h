@@ -308,6 +308,28 @@ int pqg_kmshard_reseed_apply(pqg_ctx* ctx, pqg_kmshard* h, float* tables, const 
 int pqg_kmshard_result(pqg_ctx* ctx, pqg_kmshard* h, uint32_t* iterations_run, double* inertia,
                        double* inertia_per_iter, uint32_t* assignments);
 
+/* ---- the native host of the row-sharded fit (kmnccl.cu; r2e) --------------
+ * One rank per GPU with its own NCCL communicator (libnccl.so.2, opened at
+ * run time): pqg_kmeans_fit_sharded runs the whole pqg_kmshard_* protocol
+ * above in C++ -- grouped ncclAllReduce of the partials, the row-order chain
+ * by ncclSend / ncclRecv / ncclBroadcast, ncclAllGather of the reseed
+ * candidates -- on ctx's stream, one host synchronisation per iteration.
+ * rows: this rank's n_local x ld device rows (ranks hold ascending contiguous
+ * blocks of the global row-ordered sample); seeds[B]; tables_out B*k*d (host
+ * or device); iterations_run[B], inertia[B], inertia_per_iter[B*max_iters],
+ * assignments_local[B*n_local] as pqg_kmshard_result (nullable); stats[4]
+ * (nullable): iterations, replay columns, reseeds, all-reduced bytes per
+ * iteration.  Equals kmeans_fit / pq_fit's subspace fits bit for bit. */
+int pqg_nccl_get_unique_id(void* id128);
+int pqg_nccl_comm_init(int device, int world, int rank, const void* id128, void** comm);
+int pqg_nccl_comm_init_all(int ndev, const int* devices, void** comms);
+void pqg_nccl_comm_destroy(void* comm);
+int pqg_kmeans_fit_sharded(pqg_ctx* ctx, void* comm, const float* rows, uint64_t n_local, uint64_t ld,
+                           uint32_t B, uint32_t d, uint32_t col_stride, uint64_t k, uint32_t max_iters,
+                           const uint64_t* seeds, double tol, float* tables_out, uint32_t* iterations_run,
+                           double* inertia, double* inertia_per_iter, uint32_t* assignments_local,
+                           uint64_t* stats);
+
 /* ---- on-disk formats ----------------------------------
  * Byte-identical to the reference's files; load errors carry the reference's
  * messages ("<format>: bad magic", "truncated read of <what>",

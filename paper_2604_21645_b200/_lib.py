@@ -97,6 +97,12 @@ _SIGS = {
                                  C.POINTER(_i32)]),
     "pqg_kmshard_pack": (_i32, [_vp, _vp, _vp, _u64, _vp]),
     "pqg_kmshard_replay": (_i32, [_vp, _vp, _vp, _vp, _vp, _u64, _vp, _u32]),
+    "pqg_nccl_get_unique_id": (_i32, [_vp]),
+    "pqg_nccl_comm_init": (_i32, [C.c_int, C.c_int, C.c_int, _vp, _vp]),
+    "pqg_nccl_comm_init_all": (_i32, [C.c_int, _vp, _vp]),
+    "pqg_nccl_comm_destroy": (None, [_vp]),
+    "pqg_kmeans_fit_sharded": (_i32, [_vp, _vp, _vp, _u64, _u64, _u32, _u32, _u32, _u64, _u32, _vp, _f64, _vp, _vp,
+                                      _vp, _vp, _vp, _vp]),
     "pqg_kmshard_replay_step": (_i32, [_vp, _vp, _vp]),
     "pqg_kmshard_replay_finish": (_i32, [_vp, _vp, _vp, _vp, _vp]),
     "pqg_kmshard_reseed_candidates": (_i32, [_vp, _vp, _u64, _u32, _vp, _vp, _vp]),

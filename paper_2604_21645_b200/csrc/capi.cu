@@ -49,6 +49,11 @@ static int guard(F&& f) {
 
 static void inval(const std::string& m) { fail(PQG_EINVAL, m); }
 
+namespace pqg {
+// the other translation units' C entry points (kmnccl.cu) report through here
+void set_last_error(const std::string& m) { g_last_error = m; }
+}  // namespace pqg
+
 // ---------------------------------------------------------------------------
 // host / device pointer staging
 // ---------------------------------------------------------------------------

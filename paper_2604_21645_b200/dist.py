@@ -479,6 +479,65 @@ def kmeans_fit_sharded(comm: Comm, backend, local_rows, B: int, d: int, col_stri
     return ShardedFit(tables, comm.allgather_cols(assign, counts), inertia, iters, per_iter)
 
 
+class NcclComm:
+    """The library's own NCCL communicator over the ranks of ``comm`` (one
+    per GPU): rank 0 draws the unique id (``pqg_nccl_get_unique_id``), the
+    torch group broadcasts it, every rank joins (``pqg_nccl_comm_init``).
+    Used by :func:`kmeans_fit_sharded_native`, whose iteration loop runs in
+    C++ (csrc/kmnccl.cu) with NCCL on the backend's stream."""
+
+    def __init__(self, comm: Comm, backend):
+        import torch
+        self.backend, self.lib, self.L = backend, backend.lib, backend.L
+        self.rank, self.world = comm.rank, comm.world
+        on_gpu = comm.world > 1 and comm.dist.get_backend(comm.group) == "nccl"
+        uid = torch.zeros(128, dtype=torch.uint8, device=backend.device if on_gpu else "cpu")
+        host = np.zeros(128, np.uint8)
+        if comm.rank == 0:
+            self.L.check(self.lib.pqg_nccl_get_unique_id(host.ctypes.data_as(C.c_void_p)), "nccl_unique_id")
+            uid.copy_(torch.from_numpy(host))
+        comm.broadcast_(uid, 0)
+        host = uid.cpu().numpy().copy()
+        self.h = C.c_void_p()
+        self.L.check(self.lib.pqg_nccl_comm_init(backend.device.index, comm.world, comm.rank,
+                                                 host.ctypes.data_as(C.c_void_p), C.byref(self.h)),
+                     "nccl_comm_init")
+
+    def close(self):
+        if self.h:
+            self.lib.pqg_nccl_comm_destroy(self.h)
+            self.h = C.c_void_p()
+
+
+def kmeans_fit_sharded_native(ncomm: NcclComm, local_rows, B: int, d: int, col_stride: int, k: int,
+                              max_iters: int, seeds, tol: float = 1e-4, stats: dict | None = None) -> ShardedFit:
+    """kmeans_fit_sharded with the iteration loop in C++ (pqg_kmeans_fit_sharded):
+    the same protocol and the same bit-exact result, NCCL collectives issued
+    by the library on the backend's stream.  ``assignments`` are this rank's
+    local rows (the caller gathers them if it needs the global vector)."""
+    import torch
+    be = ncomm.backend
+    rows = local_rows.contiguous()
+    n, ld = rows.shape
+    tables = torch.empty((B, k, d), dtype=torch.float32, device=rows.device)
+    assign = torch.empty((B, n), dtype=torch.int32, device=rows.device)
+    iters = np.zeros(B, np.uint32)
+    inertia = np.zeros(B, np.float64)
+    per = np.zeros((B, max_iters), np.float64)
+    st = np.zeros(4, np.uint64)
+    sd = np.asarray([int(v) for v in seeds], np.uint64)
+    vp = C.c_void_p
+    be.L.check(be.lib.pqg_kmeans_fit_sharded(
+        be.ctx.h, ncomm.h, vp(rows.data_ptr()), n, ld, B, d, col_stride, k, max_iters, sd.ctypes.data_as(vp), tol,
+        vp(tables.data_ptr()), iters.ctypes.data_as(vp), inertia.ctypes.data_as(vp), per.ctypes.data_as(vp),
+        vp(assign.data_ptr()), st.ctypes.data_as(vp)), "kmeans_fit_sharded")
+    if stats is not None:
+        stats.update(iterations=int(st[0]), replay_columns=int(st[1]), reseeds=int(st[2]),
+                     allreduce_bytes=int(st[3]) * int(st[0]), host="C++ (pqg_kmeans_fit_sharded, NCCL)")
+    per_iter = [[float(v) for v in per[b, : iters[b]]] for b in range(B)]
+    return ShardedFit(tables, assign, inertia, iters, per_iter)
+
+
 def _kmeans_fit_replicated(comm: Comm, backend, local_rows, counts, B, d, col_stride, k, max_iters, seeds,
                            tol) -> ShardedFit:
     """The replicated update for shapes the device partials do not cover:
