@@ -743,6 +743,49 @@ __global__ void topk_merge_kernel(const uint64_t* ids, const double* dists, cons
 
 }  // namespace
 
+// r2e: the probe matrix of a few queries (a single ivf_query): thread per
+// (query, list), the reference's fp64 squared_l2 (proj/src/kmeans.cpp:11-18)
+// rounded to fp32, and row_err = 2^-23 * the row's largest value (rounded
+// up) bounds |fp32 - fp64| for the select's band test; a non-finite distance
+// makes the band infinite, so the query takes the exact fallback.
+__global__ void small_probe_matrix_kernel(const float* queries, uint64_t D, const float* coarse, uint64_t nlist,
+                                          uint64_t nq, float* mat, unsigned* row_err_bits) {
+    const uint64_t q = blockIdx.y;
+    const uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= nq || j >= nlist) return;
+    const float* qv = queries + q * D;
+    const float* cv = coarse + j * D;
+    double acc = 0.0;
+    uint64_t t0 = 0;
+    if ((D & 3u) == 0 && ((reinterpret_cast<uintptr_t>(qv) | reinterpret_cast<uintptr_t>(cv)) & 15u) == 0) {
+        for (; t0 + 16 <= D; t0 += 16) {  // sixteen coordinates' loads in flight
+            float4 a[4], c[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                a[u] = __ldg(reinterpret_cast<const float4*>(qv + t0) + u);
+                c[u] = __ldg(reinterpret_cast<const float4*>(cv + t0) + u);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float av[4] = {a[u].x, a[u].y, a[u].z, a[u].w}, cc[4] = {c[u].x, c[u].y, c[u].z, c[u].w};
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const double diff = __dsub_rn((double)av[v], (double)cc[v]);
+                    acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+                }
+            }
+        }
+    }
+    for (; t0 < D; ++t0) {
+        const double diff = __dsub_rn((double)qv[t0], (double)cv[t0]);
+        acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+    }
+    const float f = __double2float_rn(acc);
+    mat[q * nlist + j] = f;
+    const unsigned eb = isfinite(f) ? __float_as_uint(__fmul_ru(f, 1.1920929e-07f)) : 0x7f800000u;
+    atomicMax(row_err_bits + q, eb);
+}
+
 void ivf_probe(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t nq,
                uint64_t nprobe, uint32_t* probes) {
     const uint64_t D = uint64_t(ix.M) * ix.ds;
@@ -769,7 +812,14 @@ void ivf_probe(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t
         a.out_mat = mat;
         a.ld_mat = ix.nlist;
         a.row_err = rerr;
-        distance_matrix(ctx, a);
+        if (nc <= 16) {  // a few queries: one exact kernel (the tensor-core path pays off for batches)
+            PQG_CUDA(cudaMemsetAsync(rerr, 0, sizeof(float) * nc, ctx->stream));
+            launch(ctx, "probe_select", small_probe_matrix_kernel,
+                   dim3(unsigned((ix.nlist + 127) / 128), unsigned(nc)), dim3(128), 0, queries + q0 * D, D,
+                   ix.coarse, ix.nlist, nc, mat, reinterpret_cast<unsigned*>(rerr));
+        } else {
+            distance_matrix(ctx, a);
+        }
         // 16 screened values per thread in registers (nlist <= 16384), else
         // the row is re-read per pass
         constexpr int kPer = 16;
@@ -791,10 +841,40 @@ void ivf_probe(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t
            nprobe, sd, probes);
 }
 
+__global__ void pairs_prep_kernel(const float* queries, uint64_t D, const uint32_t* probes, uint64_t nq,
+                                  uint64_t nprobe, float* qrep, uint32_t* prep) {
+    // pair = p * nq + q: query q's p-th probed list as a one-list query
+    const uint64_t total = nq * nprobe;
+    for (uint64_t pr = blockIdx.x; pr < total; pr += gridDim.x) {
+        const uint64_t p = pr / nq, q = pr - p * nq;
+        for (uint64_t t = threadIdx.x; t < D; t += blockDim.x) qrep[pr * D + t] = queries[q * D + t];
+        if (threadIdx.x == 0) prep[pr] = probes[q * nprobe + p];
+    }
+}
+
 void ivf_scan(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t nq,
               const uint32_t* probes, uint64_t nprobe, uint64_t k, int has_max, double max_sq,
               uint64_t* out_ids, double* out_dists, uint32_t* out_counts, int* err,
               const uint64_t* subset, uint64_t nsub, const float* luts) {
+    // r2e: a few queries would leave all but nq SMs idle -- scan every
+    // (query, probed list) pair in its own CTA (a one-list query) and merge
+    // the per-list top-k by (dist, id) (finalize_hits' order: the k best of
+    // the union are the k best of the per-list k best)
+    const char* se = std::getenv("PQG_ADC_SPLIT");
+    if (k <= 32 && !luts && nprobe > 1 && nprobe <= 64 && nq * nprobe <= uint64_t(4) * ctx->num_sms && nq < 64 &&
+        !(se && se[0] == '0')) {
+        const uint64_t D = uint64_t(ix.M) * ix.ds, np = nq * nprobe;
+        float* qrep = scratch<float>(ctx, np * D);
+        uint32_t* prep = scratch<uint32_t>(ctx, np);
+        uint64_t* ti = scratch<uint64_t>(ctx, np * k);
+        double* td = scratch<double>(ctx, np * k);
+        uint32_t* tc = scratch<uint32_t>(ctx, np);
+        launch(ctx, "adc_scan", pairs_prep_kernel, dim3(unsigned(np)), dim3(128), 0, queries, D, probes, nq, nprobe,
+               qrep, prep);
+        ivf_scan(ctx, ix, qrep, np, prep, 1, k, has_max, max_sq, ti, td, tc, err, subset, nsub, nullptr);
+        topk_merge_dev(ctx, ti, td, tc, uint32_t(nprobe), nq, k, out_ids, out_dists, out_counts);
+        return;
+    }
     if (k > 32) {  // beyond the warp top-k: exact scores + segmented sort (topk_large.cu)
         ivf_scan_large_k(ctx, ix, queries, nq, probes, nprobe, k, has_max, max_sq, out_ids, out_dists,
                          out_counts, err, subset, nsub, luts);
