@@ -992,14 +992,48 @@ __global__ void __launch_bounds__(kMeanThreads) mean_replay_kernel(
                     for (int u = 0; u < 8; ++u) buf[u * 32 + lane] = v[u];
                     __syncwarp();
                 }
-                if (lane == 0) {
-                    const float* wv = buf + (m0 - wbeg);
-                    double q = r;
+                // r2e: in batches of 32 members -- a batch whose additions
+                // provably cannot round given r (the piece test at member
+                // granularity) is added as one warp sum; only the others walk
+                // the chain (ncu r2e at configs[3] scale: the member-by-member
+                // walk of whole pieces was the kernel's tail, 10% occupancy)
+                const float* wv = buf + (m0 - wbeg);
+                for (uint32_t j0 = 0; j0 < mn; j0 += 32) {
+                    const uint32_t nm = min(32u, mn - j0);
+                    const float v = lane < nm ? wv[j0 + lane] : 0.f;
+                    const int eb = int((__float_as_uint(v) >> 23) & 0xFFu);
+                    int bhi = v != 0.f ? eb : -1, blo = v != 0.f ? max(eb, 1) : (1 << 30);
+                    double ws = (double)v;
+#pragma unroll
+                    for (int o = 16; o >= 1; o >>= 1) {
+                        ws = __dadd_rn(ws, __shfl_xor_sync(0xffffffffu, ws, o));
+                        bhi = max(bhi, __shfl_xor_sync(0xffffffffu, bhi, o));
+                        blo = min(blo, __shfl_xor_sync(0xffffffffu, blo, o));
+                    }
+                    bool bex;
+                    if (bhi < 0) {
+                        bex = true;
+                    } else if (bhi == 255 || !isfinite(r)) {
+                        bex = false;
+                    } else {
+                        int lq = blo - 150;
+                        if (r != 0.0) lq = min(lq, lowbit_exp(r));
+                        // 32 values below 2^(bhi-126) each
+                        const double bound = __dadd_ru(fabs(r), ldexp(1.0, bhi - 121));
+                        bex = mag_exp(bound) - lq <= 53;
+                    }
+                    if (bex) {
+                        r = __dadd_rn(r, ws);
+                        continue;
+                    }
+                    if (lane == 0) {
+                        double q = r;
 #pragma unroll 8
-                    for (uint32_t l = 0; l < mn; ++l) q = __dadd_rn(q, (double)wv[l]);
-                    r = q;
+                        for (uint32_t l = 0; l < nm; ++l) q = __dadd_rn(q, (double)wv[j0 + l]);
+                        r = q;
+                    }
+                    r = __shfl_sync(0xffffffffu, r, 0);
                 }
-                r = __shfl_sync(0xffffffffu, r, 0);
             }
         }
         if (lane == 0) table[bc * d + t] = __double2float_rn(__dmul_rn(r, __ddiv_rn(1.0, (double)cnt)));
