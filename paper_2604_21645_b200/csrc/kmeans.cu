@@ -91,7 +91,28 @@ struct RowCopy {
 // themselves; tile 0 also writes the problem's cluster offsets.  (The
 // minimum-blocks hint keeps ptxas from sinking the row loads of the copy into
 // their stores, which serialises them.)
-template <bool ROWS>
+// Lanes holding the same key (valid lanes only): NB > 0 compares the low NB
+// key bits with NB ballots (r2e: ALU votes instead of the MIO-bound MATCH
+// instruction, which throttled the scatter -- ncu: mio_throttle and
+// short_scoreboard stalls); NB == 0 is __match_any_sync.  Invalid lanes get
+// an arbitrary mask and must not use it.
+template <int NB>
+__device__ __forceinline__ uint32_t key_peers(uint32_t c, bool valid) {
+    if constexpr (NB == 0) {
+        return __match_any_sync(0xffffffffu, valid ? c : 0xFFFFFFFFu);
+    } else {
+        uint32_t peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            const bool bit = (c >> i) & 1u;
+            const uint32_t b = __ballot_sync(0xffffffffu, bit);
+            peers &= bit ? b : ~b;
+        }
+        return peers;
+    }
+}
+
+template <bool ROWS, int NB = 0>
 __global__ void __launch_bounds__(256, 1) scatter_kernel(const uint32_t* keys, uint64_t n, uint64_t k, uint32_t ntiles, uint32_t T,
                                const uint64_t* tile_base, uint32_t* perm, RowCopy rc, uint64_t* offsets,
                                const uint64_t* nb) {
@@ -120,8 +141,9 @@ __global__ void __launch_bounds__(256, 1) scatter_kernel(const uint32_t* keys, u
         for (int r = 0; r < kRounds; ++r) {
             const uint64_t i = i0 + r * 32 + lane;
             const uint32_t c = cs[r];
-            const uint32_t peers = __match_any_sync(0xffffffffu, c);
-            if (i < wr1 && c < k && (peers & lanemask_lt()) == 0) mine[c] += __popc(peers);
+            const bool ok = i < wr1 && c < k;
+            const uint32_t peers = key_peers<NB>(c, ok);
+            if (ok && (peers & lanemask_lt()) == 0) mine[c] += __popc(peers);
             __syncwarp();
         }
     }
@@ -151,7 +173,7 @@ __global__ void __launch_bounds__(256, 1) scatter_kernel(const uint32_t* keys, u
             const uint64_t i = i0 + r * 32 + lane;
             const uint32_t c = cs[r];
             valid[r] = i < wr1 && c < k;
-            const uint32_t peers = __match_any_sync(0xffffffffu, c);
+            const uint32_t peers = key_peers<NB>(c, valid[r]);
             const uint32_t rank = __popc(peers & lanemask_lt());
             pos[r] = valid[r] ? mine[c] + rank : 0u;
             __syncwarp();
@@ -1287,8 +1309,10 @@ static void bucket_impl(pqg_ctx* ctx, const uint32_t* keys, uint64_t n, uint32_t
         launch(ctx, "bucket", scatter_kernel<true>, dim3(g.ntiles, B), dim3(32 * g.W), ssmem, keys, n, k,
                g.ntiles, g.T, (const uint64_t*)tile_base, (uint32_t*)nullptr, *rows, out.offsets, nb);
     } else {
-        set_smem(scatter_kernel<false>, ssmem);
-        launch(ctx, "bucket", scatter_kernel<false>, dim3(g.ntiles, B), dim3(32 * g.W), ssmem, keys, n, k,
+        const char* me = std::getenv("PQG_BUCKET_MATCH");
+        auto kern = (k < 512 && !(me && me[0] == '1')) ? scatter_kernel<false, 9> : scatter_kernel<false, 0>;
+        set_smem(kern, ssmem);
+        launch(ctx, "bucket", kern, dim3(g.ntiles, B), dim3(32 * g.W), ssmem, keys, n, k,
                g.ntiles, g.T, (const uint64_t*)tile_base, out.perm, RowCopy{}, out.offsets, nb);
     }
 }
