@@ -1310,7 +1310,14 @@ static void bucket_impl(pqg_ctx* ctx, const uint32_t* keys, uint64_t n, uint32_t
                g.ntiles, g.T, (const uint64_t*)tile_base, (uint32_t*)nullptr, *rows, out.offsets, nb);
     } else {
         const char* me = std::getenv("PQG_BUCKET_MATCH");
-        auto kern = (k < 512 && !(me && me[0] == '1')) ? scatter_kernel<false, 9> : scatter_kernel<false, 0>;
+        // keys 0..k (k = padding), so NB bits must cover k itself
+        auto kern = scatter_kernel<false, 0>;
+        if (!(me && me[0] == '1')) {
+            if (k < 512) kern = scatter_kernel<false, 9>;
+            else if (k < 2048) kern = scatter_kernel<false, 11>;
+            else if (k < 8192) kern = scatter_kernel<false, 13>;
+            else if (k < 32768) kern = scatter_kernel<false, 15>;
+        }
         set_smem(kern, ssmem);
         launch(ctx, "bucket", kern, dim3(g.ntiles, B), dim3(32 * g.W), ssmem, keys, n, k,
                g.ntiles, g.T, (const uint64_t*)tile_base, out.perm, RowCopy{}, out.offsets, nb);

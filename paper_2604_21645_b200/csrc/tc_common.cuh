@@ -10,7 +10,17 @@ namespace tc {
 
 constexpr int kR = 128;             // rows per tile (MMA M)
 constexpr int kN = 256;             // centroids per N block (MMA N)
-constexpr int kKC = 32;             // K elements per chunk
+#ifndef PQG_BIG_KC
+#define PQG_BIG_KC 16
+#endif
+#ifndef PQG_BIG_STAGES
+#define PQG_BIG_STAGES 4
+#endif
+// r2e: 16-element K chunks (48 KB stages) in a 4-deep ring instead of 32 (96
+// KB) x 2: the producer keeps four bulk copies in flight, and the constant
+// columns' chunk is 16 wide (d = 128: 9 chunks = 144 K instead of 160)
+constexpr int kKC = PQG_BIG_KC;     // K elements per chunk
+constexpr int kBigStages = PQG_BIG_STAGES;
 constexpr uint32_t kSBO = (kKC / 4) * 128;  // 1024 B between 8-row groups
 constexpr uint32_t kAChunk = kR * kKC * 4;   // 16 KB per half
 constexpr uint32_t kBChunk = kN * kKC * 4;   // 32 KB per half
@@ -81,7 +91,7 @@ __device__ __forceinline__ uint32_t il_off(uint32_t row, uint32_t k) {  // withi
 // E bound of the 3xTF32 screen (see umma.cu tc_error_bound): 2 ulps of the
 // accumulator magnitude per MMA instruction plus split residuals, doubled.
 __device__ __forceinline__ float big_error_bound(float S, uint32_t kchunks) {
-    const float n_mma = float(3 * 4 * kchunks);
+    const float n_mma = float(3 * (kKC / 8) * kchunks);
     return 2.f * (2.f * n_mma + 8.f) * kU * S + 1e-30f;
 }
 

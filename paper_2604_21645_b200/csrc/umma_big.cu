@@ -97,8 +97,9 @@ struct SplitIdx {
 __device__ __forceinline__ SplitIdx split_idx(uint64_t g, uint32_t rows, uint32_t kchunks) {
     SplitIdx s;
     const uint32_t lo = uint32_t(g & 7u);
-    s.k4 = uint32_t((g >> 3) & 7u) * 4u;
-    const uint64_t rest = g >> 6;
+    constexpr uint32_t KG = kKC / 4;  // groups of 4 K elements per chunk
+    s.k4 = uint32_t((g >> 3) % KG) * 4u;
+    const uint64_t rest = (g >> 3) / KG;
     const uint32_t hi = uint32_t(rest % (rows / 8));
     const uint64_t rest2 = rest / (rows / 8);
     s.kc = uint32_t(rest2 % kchunks);
@@ -195,7 +196,7 @@ __global__ void __launch_bounds__(192, 1) big_kernel(NearestArgs a, const uint8_
                                                      uint64_t row_base) {
     if (a.active && !a.active[0]) return;
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ uint64_t full[2], empty[2], tfull[2], tempty[2];
+    __shared__ uint64_t full[kBigStages], empty[kBigStages], tfull[2], tempty[2];
     __shared__ uint32_t tmem_base;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t ntiles = (a.n + kR - 1) / kR;
@@ -206,9 +207,11 @@ __global__ void __launch_bounds__(192, 1) big_kernel(NearestArgs a, const uint8_
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (threadIdx.x == 32) {
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < kBigStages; ++s) {
             bar_init(&full[s], 1);
             bar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
             bar_init(&tfull[s], 1);
             bar_init(&tempty[s], 4);
         }
@@ -226,7 +229,7 @@ __global__ void __launch_bounds__(192, 1) big_kernel(NearestArgs a, const uint8_
             for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (uint32_t nb = 0; nb < nblocks; ++nb) {
                     for (uint32_t kc = 0; kc < kchunks; ++kc, ++q) {
-                        const uint32_t s = q & 1, ph = (q >> 1) & 1;
+                        const uint32_t s = q % kBigStages, ph = (q / kBigStages) & 1;
                         bar_wait(&empty[s], ph ^ 1);
                         uint8_t* st = smem + s * kStage;
                         bar_expect_tx(&full[s], kStage);
@@ -249,7 +252,7 @@ __global__ void __launch_bounds__(192, 1) big_kernel(NearestArgs a, const uint8_
                     fence_after();
                     const uint32_t d_tmem = tmem + buf * 256u;
                     for (uint32_t kc = 0; kc < kchunks; ++kc, ++q) {
-                        const uint32_t s = q & 1, ph = (q >> 1) & 1;
+                        const uint32_t s = q % kBigStages, ph = (q / kBigStages) & 1;
                         bar_wait(&full[s], ph);
                         fence_after();
                         const uint32_t base = smem_u32(smem + s * kStage);
@@ -411,7 +414,7 @@ void umma_big(pqg_ctx* ctx, const NearestArgs& a0) {
     uint8_t* Bm = scratch<uint8_t>(ctx, uint64_t(nblocks) * kchunks * 2 * kBChunk);
     launch(ctx, "big_split", split_table_kernel, dim3(grid1d(k_pad * kchunks * (kKC / 4), 256, 1u << 20)),
            dim3(256), 0, a0.table, a0.cnorm, a0.k, a0.d, kchunks, k_pad, Bm);
-    const size_t smem = 2 * size_t(kStage);
+    const size_t smem = size_t(kBigStages) * size_t(kStage);
     PQG_CUDA(cudaFuncSetAttribute(big_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     PQG_CUDA(cudaFuncSetAttribute(big_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     if (a0.big_rows) {  // rows prepared by umma_big_prepare_rows (single chunk)
