@@ -131,6 +131,12 @@ __global__ void __launch_bounds__(1024) probe_select_kernel(
     }
     const float tau = __uint_as_float(s_prefix);
     const float band = tau + 2.05f * E;
+    // a non-finite band (the query's distances overflow fp32, or a NaN): the
+    // exact fallback orders every list in fp64 as probe_order does
+    if (!(band < __int_as_float(0x7f800000))) {
+        if (threadIdx.x == 0) overflow[atomicAdd(n_overflow, 1u)] = uint32_t(q);
+        return;
+    }
     if constexpr (PER > 0) {
 #pragma unroll
         for (int i = 0; i < PER; ++i) {

@@ -807,3 +807,29 @@ def test_narrow_screen_parity(pq, orc, mix, monkeypatch, D, M, ks, kern):
     t2[:, ks - ks // 2:] = t2[:, : ks // 2]
     cb2 = pq.Codebook(M, ks, D // M, np.ascontiguousarray(t2))
     assert np.array_equal(pq.pq_encode(cb2, big[:5000]).bytes, orc.pq_encode(big[:5000], t2))
+
+
+@pytest.mark.parametrize("nq", [1, 5, 40])
+def test_probe_d128_small_and_batched_vs_oracle(pq, orc, nq):
+    """probe_order (proj/src/ivf.cpp:91-101) at d=128, nlist 300: the exact
+    small-batch probe (<= 16 queries, r2e) and the tensor-core batch path,
+    plus a query whose distances all overflow to inf (every list ties: the
+    lowest indices win, through the exact fallback)."""
+    from paper_2604_21645_b200.datagen import gaussian_mixture
+    x = gaussian_mixture(3000, 128, 24, seed=41)
+    cb = pq.pq_fit(x, 16, 16, 4, 3)
+    codes = pq.pq_encode(cb, x)
+    coarse = np.ascontiguousarray(x[::10][:300])
+    index = pq.ivf_build_with_centroids(cb, codes, np.arange(3000, dtype=np.uint64), coarse)
+    qs = gaussian_mixture(nq, 128, 24, seed=41, stream=3)
+    if nq > 1:
+        qs[nq - 1, 7] = np.float32(1e30)  # squared distances overflow: all inf
+    probes = pq.ivf_probe(index, qs, 9)
+    for q in range(nq):
+        assert np.array_equal(probes[q], orc.probe_order(coarse, qs[q], 9)), q
+    # and the searches on top of them (split scan for < 64 queries)
+    gi, gd, gc = pq.ivf_query_batch(index, qs, 7, 9)
+    off, lid, lcodes, _, _ = index.export()
+    for q in range(nq):  # the overflowing query too: every candidate at inf, ids ascending
+        ri, rd = orc.ivf_query(cb.tables, coarse, off, lid, lcodes, qs[q], 7, 9)
+        assert np.array_equal(gi[q, : gc[q]], ri) and np.array_equal(gd[q, : gc[q]], rd), q
