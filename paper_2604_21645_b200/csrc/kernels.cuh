@@ -91,6 +91,9 @@ void rows_sum_f64(pqg_ctx* ctx, const double* v, uint64_t n, uint32_t B, double*
 void kmeans_inertia_and_stop(pqg_ctx* ctx, const double* dist, uint64_t n, uint32_t B,
                              uint32_t it, uint32_t max_iters, double tol, KMeansState st,
                              const uint64_t* nb = nullptr);
+// table_norms for small (PQ) tables: a block per problem (kmeans.cu)
+void table_norms_small(pqg_ctx* ctx, const float* table, uint32_t B, uint64_t k, uint32_t d, float* cnorm,
+                       float* cmax);
 void kmeans_update(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint32_t d,
                    float* table, uint64_t k, const uint32_t* assign, double* dist,
                    const int* active, const uint64_t* nb = nullptr, float* cnorm = nullptr,

@@ -1163,6 +1163,16 @@ __device__ void reseed_problem(const float* x, uint64_t ldx, uint32_t col_stride
 // ||c|| rounded up -- computed by the problem's reseed block once its table
 // is final, instead of a separate launch at the head of every pass.
 __device__ void problem_norms(const float* table, uint32_t b, uint64_t k, uint32_t d, float* cnorm,
+                              float* cmax);
+
+// table_norms for small tables (r2e): a block per problem, no memset and no
+// atomics (the PQ encode and fit heads; the wide kernel stays for coarse tables)
+__global__ void __launch_bounds__(256) norms_block_kernel(const float* table, uint64_t k, uint32_t d, float* cnorm,
+                                                          float* cmax) {
+    problem_norms(table, blockIdx.x, k, d, cnorm, cmax);
+}
+
+__device__ void problem_norms(const float* table, uint32_t b, uint64_t k, uint32_t d, float* cnorm,
                               float* cmax) {
     __shared__ unsigned wmax[32];
     unsigned mx = 0u;
@@ -1381,6 +1391,11 @@ void rows_sum_f64(pqg_ctx* ctx, const double* v, uint64_t n, uint32_t B, double*
            v, n, chunk, parts, (const int*)nullptr, (const uint64_t*)nullptr);
     launch(ctx, "inertia", final_parts_kernel, dim3(B), dim3(kRedThreads), 0, (const double*)parts,
            uint32_t(nparts), out);
+}
+
+void table_norms_small(pqg_ctx* ctx, const float* table, uint32_t B, uint64_t k, uint32_t d, float* cnorm,
+                       float* cmax) {
+    launch(ctx, "norms", norms_block_kernel, dim3(B), dim3(256), 0, table, k, d, cnorm, cmax);
 }
 
 void kmeans_update(pqg_ctx* ctx, const RowSrc& src, uint64_t n, uint32_t B, uint32_t d,

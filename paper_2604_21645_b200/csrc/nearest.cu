@@ -1165,6 +1165,10 @@ void dispatch(pqg_ctx* ctx, const NearestArgs& a) {
 
 void table_norms(pqg_ctx* ctx, const float* table, uint32_t B, uint64_t k, uint32_t d,
                  float* cnorm, float* cmax) {
+    if (k * d <= 8192 && k <= 4096) {  // PQ codebooks: one block per subspace
+        table_norms_small(ctx, table, B, k, d, cnorm, cmax);
+        return;
+    }
     PQG_CUDA(cudaMemsetAsync(cmax, 0, sizeof(float) * B, ctx->stream));
     launch(ctx, "norms", norms_kernel, dim3(grid1d(uint64_t(B) * k, 256, 4096)), dim3(256), 0,
            table, B, k, d, cnorm, reinterpret_cast<unsigned*>(cmax));
