@@ -71,9 +71,18 @@ class _Base:
         self.p = prefix
 
     def fn(self, name, restype, argtypes):
-        f = getattr(self.lib, self.p + name)
-        f.restype = restype
-        f.argtypes = argtypes
+        # one prototype-bound callable per (name, signature): the CDLL's own
+        # function objects are shared, and re-setting their argtypes while a
+        # checker thread is inside a call raced (test_config3_full)
+        key = (name, restype, tuple(argtypes))
+        cache = self.__dict__.setdefault("_fn_cache", {})
+        f = cache.get(key)
+        if f is None:
+            shared = getattr(self.lib, self.p + name)
+            shared.restype = restype  # direct self.lib.<name> callers keep working
+            shared.argtypes = argtypes
+            f = C.CFUNCTYPE(restype, *argtypes)(C.cast(shared, C.c_void_p).value)
+            cache[key] = f
         return f
 
 

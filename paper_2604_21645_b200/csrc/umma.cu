@@ -389,7 +389,10 @@ __device__ __forceinline__ void issue_tile(uint32_t d_tmem, uint32_t a_hi, uint3
     }
 }
 
-template <int DS, int KA, bool PAD, bool DB>
+// KD: the pass wants the winners' fp64 distances (k-means; a.out_dist set),
+// computed under the next tile's MMAs -- a separate instance, so the encode's
+// kernel keeps its registers (and CTAs per SM)
+template <int DS, int KA, bool PAD, bool DB, bool KD = false>
 __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, uint32_t n_pad,
                                                                uint32_t tmem_cols, uint32_t m32,
                                                                uint32_t n_mma) {
@@ -462,6 +465,38 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
     };
     float x_next[DS];
     load_row(cta, x_next);
+    // r2e: the winner's fp64 distance (k-means passes) is computed while the
+    // NEXT tile's MMAs run, off the CTA's critical path (in the epilogue it
+    // cost ~18 us of a 97 us 100k-row pass): the row, its codeword and x wait
+    // in registers for one tile
+    float x_pend[DS];
+    uint32_t idx_pend = 0xFFFFFFFFu;
+    uint64_t row_pend = 0;
+    auto flush_dist = [&]() {
+        if constexpr (!KD) return;
+        if (idx_pend == 0xFFFFFFFFu) return;
+        const float* c = tab + uint64_t(idx_pend) * d;
+        float cv[DS];
+        if (!PAD && (DS % 4) == 0 && (reinterpret_cast<uintptr_t>(tab) & 15u) == 0) {
+#pragma unroll
+            for (int t = 0; t < DS; t += 4) {
+                const float4 q = __ldg(reinterpret_cast<const float4*>(c + t));
+                cv[t] = q.x; cv[t + 1] = q.y; cv[t + 2] = q.z; cv[t + 3] = q.w;
+            }
+        } else {
+#pragma unroll
+            for (int t = 0; t < DS; ++t) cv[t] = uint32_t(t) < d ? __ldg(c + t) : 0.f;
+        }
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t < DS; ++t) {
+            if (uint32_t(t) >= d) break;
+            const double diff = __dsub_rn((double)x_pend[t], (double)cv[t]);
+            acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+        }
+        a.out_dist[uint64_t(b) * a.n + row_pend] = acc;
+        idx_pend = 0xFFFFFFFFu;
+    };
     for (uint64_t tile = cta; tile < ntiles; tile += ncta) {
         const uint64_t row = tile * kRows + tid;
         const bool valid = row < a.n;
@@ -515,7 +550,10 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
                 issue_tile<DS, KA>(tmem, a_hi, a_lo, b_hi, b_lo, boff, idesc);
                 mma_commit(&mbar);
             }
-            if (p0 == 0) load_row(tile + ncta, x_next);  // next tile's row, in flight during the epilogue
+            if (p0 == 0) {
+                load_row(tile + ncta, x_next);  // next tile's row, in flight during the epilogue
+                flush_dist();                   // the previous tile's winner, under this tile's MMAs
+            }
             mbar_wait(&mbar, phase);
             phase ^= 1;
             fence_after();
@@ -568,16 +606,11 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
             // non-finite E (inf/NaN in the row or table): the exact fixup decides
             if (row_unique(K1, V2, rc.hi4, E, k)) {
                 store_index(a, row, b, idx);
-                if (a.out_dist) {
-                    const float* c = tab + uint64_t(idx) * d;
-                    double acc = 0.0;
+                if (KD && a.out_dist) {  // computed under the next tile's MMAs (flush_dist)
 #pragma unroll
-                    for (int t = 0; t < DS; ++t) {
-                        if (uint32_t(t) >= d) break;
-                        const double diff = __dsub_rn((double)x[t], (double)__ldg(c + t));
-                        acc = __dadd_rn(acc, __dmul_rn(diff, diff));
-                    }
-                    a.out_dist[uint64_t(b) * a.n + row] = acc;
+                    for (int t = 0; t < DS; ++t) x_pend[t] = x[t];
+                    idx_pend = idx;
+                    row_pend = row;
                 }
             } else {
                 const unsigned long long slot = atomicAdd(a.flag_count, 1ull);
@@ -586,6 +619,7 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
         }
         __syncthreads();  // TMEM and the A stage are reused by the next tile
     }
+    flush_dist();  // the last tile's winner
     fence_before();
     __syncthreads();
     if (warp == 0) {
@@ -861,6 +895,7 @@ void launch_umma(pqg_ctx* ctx, const NearestArgs& a) {
     while (cols < n_mma) cols <<= 1;
     const bool db = n_mma == n_pad && n_pad > 128 && !(std::getenv("PQG_UMMA_DB") && std::getenv("PQG_UMMA_DB")[0] == '0');
     auto kern = db ? umma_screen_kernel<DS, KA, PAD, true> : umma_screen_kernel<DS, KA, PAD, false>;
+    if (a.out_dist) kern = db ? umma_screen_kernel<DS, KA, PAD, true, true> : umma_screen_kernel<DS, KA, PAD, false, true>;
     PQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     const uint64_t ntiles = (a.n + kRows - 1) / kRows;
     // persistent: CTAs per SM limited by TMEM columns (2 at Ks=256), shared
