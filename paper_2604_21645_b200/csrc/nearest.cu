@@ -479,15 +479,38 @@ __global__ void __launch_bounds__(256) fixup_warp_kernel(NearestArgs a) {
             }
             return v;
         };
+        // r2e: k <= 256 (PQ codebooks) -- a lane's eight codewords scored with
+        // all their loads in flight and kept in registers for the second pass
+        // (the per-pair chain of dependent L2 round trips was the kernel)
+        constexpr int kPer = 8;
+        float vr[kPer];
+        const bool small = k <= uint64_t(32 * kPer);
         float vmin = __int_as_float(0x7f800000);
-        for (uint64_t j = lane; j < k; j += 32) vmin = fminf(vmin, fdist(j));
+        if (small) {
+#pragma unroll
+            for (int i = 0; i < kPer; ++i) {
+                const uint64_t j = lane + 32u * i;
+                vr[i] = j < k ? fdist(j) : __int_as_float(0x7f800000);
+            }
+#pragma unroll
+            for (int i = 0; i < kPer; ++i) vmin = fminf(vmin, vr[i]);
+        } else {
+            for (uint64_t j = lane; j < k; j += 32) vmin = fminf(vmin, fdist(j));
+        }
 #pragma unroll
         for (int o = 16; o >= 1; o >>= 1) vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
         const float thr = vmin * ((1.f + eps) / (1.f - eps)) * (1.f + 4.f * kU) + 1e-37f;
         double best = __longlong_as_double(0x7ff0000000000000LL);
         uint32_t bj = 0xFFFFFFFFu;
-        for (uint64_t j = lane; j < k; j += 32) {
-            const float v = fdist(j);
+        for (uint64_t j = lane, i = 0; j < k; j += 32, ++i) {
+            float v = 0.f;
+            if (small) {
+#pragma unroll
+                for (int u = 0; u < kPer; ++u)
+                    if (uint64_t(u) == i) v = vr[u];
+            } else {
+                v = fdist(j);
+            }
             if (!(v <= thr) && !(v != v)) continue;  // NaN candidates go to the exact path
             const float* c = tab + j * DS;
             double acc = 0.0;
