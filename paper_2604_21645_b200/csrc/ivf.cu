@@ -15,6 +15,8 @@
 // candidate is re-scored in fp64 -- the same float entries added in m order,
 // exactly adc_lookup -- only if s32 could beat the warp's current k-th hit.
 #include <cfloat>
+#include <cstdlib>
+#include <cstring>
 
 #include "kernels.cuh"
 
@@ -199,6 +201,223 @@ __global__ void __launch_bounds__(1024) probe_select_kernel(
     }
     bitonic_sort(cd, cand, n2);
     for (uint64_t p = threadIdx.x; p < nprobe; p += blockDim.x) probes[q * nprobe + p] = cand[p];
+}
+
+// ---------------------------------------------------------------------------
+// r2h: warp per query (nlist <= 1024, nprobe <= 32), no block barriers.  The
+// CTA-wide radix select above spends ~6k warp instructions per query (four
+// digit passes with shared-atomic histograms, barrier-stalled: ncu
+// r2f_probe_select).  Here:
+//   1. each lane keeps its <= 32 screened keys in registers (column lane+32i);
+//      the nprobe-th smallest LANE MINIMUM (warp bitonic sort of 32 minima)
+//      is an upper bound U of tau, the nprobe-th smallest key (>= nprobe keys
+//      are <= U: those minima);
+//   2. the keys <= U (typically ~nprobe + a few) are compacted into shared
+//      memory and tau is the candidate whose rank bracket holds nprobe -- the
+//      same key the radix select finds; if more than kWCand keys are <= U
+//      (heavy duplicates) tau comes from a bitwise bisection over the
+//      registers instead;
+//   3. band, overflow rule, fp64 re-score (squared_l2, kmeans.cpp:11-18) and
+//      the (dist, index) order are those of probe_select_kernel.
+// ---------------------------------------------------------------------------
+constexpr int kWarpSelWarps = 8;
+constexpr int kWCand = 128;
+
+// ascending warp bitonic sort of one u32 per lane
+__device__ __forceinline__ uint32_t warp_sort_u32(uint32_t v, uint32_t lane) {
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const uint32_t o = __shfl_xor_sync(0xffffffffu, v, stride);
+            const bool up = (lane & size) == 0 || size == 32;
+            const bool low = (lane & stride) == 0;
+            v = (low == up) ? min(v, o) : max(v, o);
+        }
+    }
+    return v;
+}
+
+// ascending warp bitonic sort of one (dist, index) pair per lane
+__device__ __forceinline__ void warp_sort_pair(double& d, uint32_t& ix, uint32_t lane) {
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const double od = __shfl_xor_sync(0xffffffffu, d, stride);
+            const uint32_t oi = __shfl_xor_sync(0xffffffffu, ix, stride);
+            const bool up = (lane & size) == 0 || size == 32;
+            const bool low = (lane & stride) == 0;
+            // the lower lane of a pair keeps the smaller (ascending block) or larger
+            const bool o_less = pair_less(od, oi, d, ix);
+            const bool take = (low == up) ? o_less : pair_less(d, ix, od, oi);
+            if (take) { d = od; ix = oi; }
+        }
+    }
+}
+
+// warp-local bitonic sort in shared memory (n a power of two <= 2 * kCandCap)
+__device__ void warp_bitonic_sort(double* d, uint32_t* ix, int n, uint32_t lane) {
+    for (int size = 2; size <= n; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            __syncwarp();
+            for (int t = int(lane); t < n / 2; t += 32) {
+                const int lo = 2 * t - (t & (stride - 1));
+                const int hi = lo + stride;
+                const bool up = ((lo & size) == 0);
+                const bool sw = up ? pair_less(d[hi], ix[hi], d[lo], ix[lo])
+                                   : pair_less(d[lo], ix[lo], d[hi], ix[hi]);
+                if (sw) {
+                    const double td = d[lo]; d[lo] = d[hi]; d[hi] = td;
+                    const uint32_t ti = ix[lo]; ix[lo] = ix[hi]; ix[hi] = ti;
+                }
+            }
+        }
+    }
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(kWarpSelWarps * 32) probe_select_warp_kernel(
+    const float* mat, uint64_t ld, const float* row_err, const float* queries, uint64_t D,
+    const float* coarse, uint64_t nlist, uint64_t nprobe, uint64_t nq, uint64_t q0, uint32_t* probes,
+    uint32_t* overflow, unsigned* n_overflow) {
+    __shared__ uint32_t s_cand[kWarpSelWarps][kCandCap];
+    __shared__ double s_cd[kWarpSelWarps][kCandCap];
+    const uint32_t lane = threadIdx.x & 31u, wq = threadIdx.x >> 5;
+    const uint64_t ql = uint64_t(blockIdx.x) * kWarpSelWarps + wq;
+    if (ql >= nq) return;
+    const uint64_t q = q0 + ql;
+    uint32_t* cand = s_cand[wq];
+    double* cd = s_cd[wq];
+    const float* v = mat + ql * ld;
+    const float E = row_err[ql];
+    const uint32_t r = uint32_t(nprobe);
+    constexpr uint32_t kPad = 0xFFFFFFFFu;  // above every real key (NaN keys included)
+    uint32_t key[32];
+    uint32_t lmin = kPad;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        const uint64_t j = lane + 32u * uint32_t(i);
+        key[i] = j < nlist ? __float_as_uint(__ldg(v + j)) : kPad;
+        lmin = min(lmin, key[i]);
+    }
+    // 1. U = the r-th smallest lane minimum (r <= 32 <= lanes holding a real key, or r <= nlist)
+    const uint32_t U = __shfl_sync(0xffffffffu, warp_sort_u32(lmin, lane), int(r - 1));
+    // 2. tau = the r-th smallest key, among the keys <= U
+    uint32_t nle = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) nle += (key[i] != kPad && key[i] <= U) ? 1u : 0u;
+    uint32_t incl = nle;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= uint32_t(off)) incl += o;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    uint32_t tau;
+    if (total <= uint32_t(kWCand)) {
+        uint32_t p = incl - nle;
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+            if (key[i] != kPad && key[i] <= U) cand[p++] = key[i];
+        __syncwarp();
+        uint32_t found = 0, mine = 0;
+        for (uint32_t c = lane; c < total; c += 32) {
+            const uint32_t x = cand[c];
+            uint32_t lt = 0, le = 0;
+            for (uint32_t t = 0; t < total; ++t) {
+                const uint32_t y = cand[t];
+                lt += y < x ? 1u : 0u;
+                le += y <= x ? 1u : 0u;
+            }
+            if (lt < r && r <= le) { found = 1; mine = x; }
+        }
+        const uint32_t who = __ballot_sync(0xffffffffu, found);
+        // no bracket holds r (fewer than r real keys): the exact fallback decides
+        tau = who ? __shfl_sync(0xffffffffu, mine, __ffs(who) - 1) : 0xFFFFFFFFu;
+        __syncwarp();
+    } else {
+        // bisection: the smallest t with #{keys <= t} >= r
+        uint32_t ans = 0;
+        for (int b = 31; b >= 0; --b) {
+            const uint32_t t = ans | ((1u << b) - 1u);
+            uint32_t c = 0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) c += (key[i] != kPad && key[i] <= t) ? 1u : 0u;
+            c = __reduce_add_sync(0xffffffffu, c);
+            if (c < r) ans |= 1u << b;
+        }
+        tau = ans;
+    }
+    // 3. the band of probe_select_kernel
+    const float band = __uint_as_float(tau) + 2.05f * E;
+    if (!(band < __int_as_float(0x7f800000))) {
+        if (lane == 0) overflow[atomicAdd(n_overflow, 1u)] = uint32_t(q);
+        return;
+    }
+    uint32_t nb = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) nb += (key[i] != kPad && __uint_as_float(key[i]) <= band) ? 1u : 0u;
+    incl = nb;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= uint32_t(off)) incl += o;
+    }
+    const uint32_t c = __shfl_sync(0xffffffffu, incl, 31);
+    if (c > uint32_t(kCandCap)) {
+        if (lane == 0) overflow[atomicAdd(n_overflow, 1u)] = uint32_t(q);
+        return;
+    }
+    const float* qv = queries + q * D;
+    const bool vec = (D & 3u) == 0 && (reinterpret_cast<uintptr_t>(coarse) & 15u) == 0 &&
+                     (reinterpret_cast<uintptr_t>(qv) & 15u) == 0;
+    auto rescore = [&](uint32_t j) -> double {
+        const float* row = coarse + uint64_t(j) * D;
+        if (!vec) return exact_sq_l2(qv, row, int(D));
+        double acc = 0.0;
+        for (uint64_t t = 0; t < D; t += 4) {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(row + t));
+            const float4 g = __ldg(reinterpret_cast<const float4*>(qv + t));
+            const float cv[4] = {f.x, f.y, f.z, f.w}, xv[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const double diff = __dsub_rn((double)xv[u], (double)cv[u]);
+                acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+            }
+        }
+        return acc;
+    };
+    if (c <= 32u) {
+        // one band member per lane (columns compacted through shared memory:
+        // a lane may hold several), then a register sort of (dist, index)
+        uint32_t p = incl - nb, myj = 0xFFFFFFFFu;
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+            if (key[i] != kPad && __uint_as_float(key[i]) <= band) cand[p++] = lane + 32u * uint32_t(i);
+        __syncwarp();
+        double d = __longlong_as_double(0x7ff0000000000000LL);
+        if (lane < c) {
+            myj = cand[lane];
+            d = rescore(myj);
+        }
+        warp_sort_pair(d, myj, lane);
+        if (lane < r) probes[q * nprobe + lane] = myj;
+        return;
+    }
+    uint32_t p = incl - nb;
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+        if (key[i] != kPad && __uint_as_float(key[i]) <= band) cand[p++] = lane + 32u * uint32_t(i);
+    int n2 = 1;
+    while (n2 < int(c)) n2 <<= 1;
+    __syncwarp();
+    for (int t = int(lane); t < n2; t += 32) {
+        if (t < int(c)) cd[t] = rescore(cand[t]);
+        else { cd[t] = __longlong_as_double(0x7ff0000000000000LL); cand[t] = 0xFFFFFFFFu; }
+    }
+    warp_bitonic_sort(cd, cand, n2, lane);
+    for (uint64_t pp = lane; pp < nprobe; pp += 32) probes[q * nprobe + pp] = cand[pp];
 }
 
 // Rare fallback (more than kCandCap lists inside the screen band, e.g. many
@@ -829,7 +1048,14 @@ void ivf_probe(pqg_ctx* ctx, const IndexView& ix, const float* queries, uint64_t
         // 16 screened values per thread in registers (nlist <= 16384), else
         // the row is re-read per pass
         constexpr int kPer = 16;
-        if (ix.nlist <= uint64_t(kPer) * 1024) {
+        const char* sel_env = std::getenv("PQG_PROBE_SEL");
+        const bool warp_sel = !(sel_env && std::strcmp(sel_env, "cta") == 0);
+        if (warp_sel && ix.nlist <= 1024 && nprobe <= 32) {
+            launch(ctx, "probe_select", probe_select_warp_kernel,
+                   dim3(unsigned((nc + kWarpSelWarps - 1) / kWarpSelWarps)), dim3(kWarpSelWarps * 32), 0,
+                   (const float*)mat, ix.nlist, (const float*)rerr, queries, D, ix.coarse, ix.nlist, nprobe,
+                   nc, q0, probes, overflow, n_over);
+        } else if (ix.nlist <= uint64_t(kPer) * 1024) {
             const unsigned th = unsigned(std::max<uint64_t>(kSelThreads, (ix.nlist + kPer * 32 - 1) / (kPer * 32) * 32));
             launch(ctx, "probe_select", probe_select_kernel<kPer>, dim3(unsigned(nc)), dim3(th), 0,
                    (const float*)mat, ix.nlist, (const float*)rerr, queries, D, ix.coarse, ix.nlist,

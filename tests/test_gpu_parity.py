@@ -833,3 +833,41 @@ def test_probe_d128_small_and_batched_vs_oracle(pq, orc, nq):
     for q in range(nq):  # the overflowing query too: every candidate at inf, ids ascending
         ri, rd = orc.ivf_query(cb.tables, coarse, off, lid, lcodes, qs[q], 7, 9)
         assert np.array_equal(gi[q, : gc[q]], ri) and np.array_equal(gd[q, : gc[q]], rd), q
+
+
+@pytest.mark.parametrize("layout", ["mixture", "clustered_lanes", "duplicates"])
+def test_probe_select_warp_nlist1024_vs_oracle(pq, orc, layout):
+    """r2h warp-per-query probe select (nlist <= 1024, nprobe <= 32) against
+    probe_order (proj/src/ivf.cpp:91-101) and the CTA radix select
+    (PQG_PROBE_SEL=cta) at d=128, nlist 1024.  'clustered_lanes' puts the near
+    lists in columns j % 32 < 10, so more than 128 keys lie below the lane-minimum
+    bound and tau comes from the bisection; 'duplicates' repeats one centroid
+    300 times (a band of > 256 lists: the exact fallback)."""
+    import os
+    from paper_2604_21645_b200.datagen import gaussian_mixture
+    rng = np.random.default_rng(7)
+    x = gaussian_mixture(4096, 128, 32, seed=43)
+    cb = pq.pq_fit(x, 16, 16, 3, 3)
+    codes = pq.pq_encode(cb, x)
+    qs = gaussian_mixture(48, 128, 32, seed=43, stream=5)
+    coarse = np.ascontiguousarray(x[::4][:1024]).copy()
+    if layout == "clustered_lanes":
+        near = np.array([j for j in range(1024) if j % 32 < 10])
+        coarse = (rng.standard_normal((1024, 128)) * 30 + 100).astype(np.float32)
+        coarse[near] = qs[0] + (rng.standard_normal((near.size, 128)) * 0.05).astype(np.float32)
+    elif layout == "duplicates":
+        coarse[100:400] = coarse[99]
+        qs[1] = coarse[99]
+    coarse = np.ascontiguousarray(coarse, dtype=np.float32)
+    index = pq.ivf_build_with_centroids(cb, codes, np.arange(4096, dtype=np.uint64), coarse)
+    for nprobe in (1, 16, 32):
+        got = pq.ivf_probe(index, qs, nprobe)
+        os.environ["PQG_PROBE_SEL"] = "cta"
+        try:
+            cta = pq.ivf_probe(index, qs, nprobe)
+        finally:
+            del os.environ["PQG_PROBE_SEL"]
+        assert np.array_equal(got, cta), nprobe
+        for q in range(0, 48, 3):
+            assert np.array_equal(got[q], orc.probe_order(coarse, qs[q], nprobe)), (nprobe, q)
+        assert np.array_equal(got[1], orc.probe_order(coarse, qs[1], nprobe)), nprobe
