@@ -22,6 +22,7 @@
 // SBO = (K/4)*128 B apart.  Descriptor / instruction-descriptor bit layouts
 // follow the sm_100 UMMA definitions (CUTLASS cute/arch/mma_sm100_desc.hpp).
 #include <cstdlib>
+#include <type_traits>
 
 #include "kernels.cuh"
 
@@ -189,6 +190,47 @@ __device__ __forceinline__ void top2_chunk(const uint32_t (&r)[32], uint32_t nva
     top2_pairs<0, MASK>(r, nvalid, m1, m2, m32, one, neg1);
 #pragma unroll
     for (int s4 = 0; s4 < kNS; ++s4) ch[s4] = (m1[s4] != old[s4]) ? c0 : ch[s4];
+}
+
+// r2h fast path (full 64- or 128-column passes, k % 64 == 0): the chunk loop of
+// a pass is unrolled and a key's 5 low bits carry (chunk within the pass,
+// pair within the state, column within the pair) instead of the column within
+// the chunk -- state s sees pairs p = 4q + s, i.e. columns 8q + 2s + b of a
+// chunk, so J = 8*chunk + 2q + b with s implicit.  The per-chunk tracking of
+// each best's chunk (ISETP + MOV + SEL per state per chunk, plus the loop
+// control: ~24 of ~156 instructions per chunk, ncu r2h source counters)
+// becomes one check per state per pass.
+template <int CC, int P>
+__device__ __forceinline__ void top2_pairs_fast(const uint32_t (&r)[32], uint32_t (&m1)[kNS], uint32_t (&m2)[kNS],
+                                                uint32_t m32, uint32_t one, uint32_t neg1) {
+    static_assert(kNS == 4, "the fast key layout assumes four states");
+    if constexpr (P < 16) {
+        constexpr int J = CC * 8 + 2 * (P / 4);
+        const uint32_t a = col_key<J>(r[2 * P], m32), b = col_key<J + 1>(r[2 * P + 1], m32);
+        const uint32_t lo = min(a, b);
+        const uint32_t hi = mad_u32(lo, neg1, mad_u32(a, one, b));
+        m2[P % 4] = min(m2[P % 4], min(max(m1[P % 4], lo), hi));
+        m1[P % 4] = min(m1[P % 4], lo);
+        top2_pairs_fast<CC, P + 1>(r, m1, m2, m32, one, neg1);
+    }
+}
+
+// column (within its pass) of state s's key
+__device__ __forceinline__ uint32_t fast_col(uint32_t key, uint32_t s) {
+    const uint32_t J = key & 31u;
+    return (J >> 3) * 32u + ((J >> 1) & 3u) * 8u + 2u * s + (J & 1u);
+}
+
+__device__ __forceinline__ void top2_merge_fast(const uint32_t (&m1)[kNS], const uint32_t (&m2)[kNS],
+                                                const uint32_t (&pch)[kNS], uint64_t& K1, uint32_t& V2) {
+    K1 = (uint64_t(m1[0] >> 5) << 32) | (pch[0] + fast_col(m1[0], 0));
+    V2 = m2[0] >> 5;
+#pragma unroll
+    for (int s4 = 1; s4 < kNS; ++s4) {
+        const uint64_t o = (uint64_t(m1[s4] >> 5) << 32) | (pch[s4] + fast_col(m1[s4], s4));
+        V2 = min(min(V2, m2[s4] >> 5), uint32_t(max(K1, o) >> 32));
+        K1 = min(K1, o);
+    }
 }
 
 // Merge the states: (best value, global column) and the runner-up's value;
@@ -395,7 +437,7 @@ __device__ __forceinline__ void issue_tile(uint32_t d_tmem, uint32_t a_hi, uint3
 template <int DS, int KA, bool PAD, bool DB, bool KD = false>
 __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, uint32_t n_pad,
                                                                uint32_t tmem_cols, uint32_t m32,
-                                                               uint32_t n_mma) {
+                                                               uint32_t n_mma, uint32_t allow_fast) {
     static_assert(KA % 8 == 0 && KA >= DS + 2, "augmented K");
     constexpr uint32_t SBO = (KA / 4) * 128;  // bytes between 8-row groups
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -536,6 +578,9 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
 #pragma unroll
         for (int s4 = 0; s4 < kNS; ++s4) { m1[s4] = 0xFFFFFFFFu; m2[s4] = 0xFFFFFFFFu; ch[s4] = 0; }
         const uint32_t lane_base = (warp * 32u) << 16;
+        // r2h: full 64/128-column passes take the unrolled fast path (ch[] then
+        // holds each state's pass base; see top2_pairs_fast)
+        const bool fast = !DB && allow_fast && (k % 64) == 0 && (n_mma == 64 || n_mma == 128);
         for (uint32_t p0 = 0; p0 < n_pad; p0 += n_mma) {
             const uint32_t w = min(n_mma, n_pad - p0);
             if (p0 > 0) {  // the previous pass's TMEM reads are complete before the next MMA
@@ -565,7 +610,28 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
                 if (cabs + 32 <= k) top2_chunk<false>(r, 32u, cabs, m1, m2, ch, m32);
                 else top2_chunk<true>(r, uint32_t(k - cabs), cabs, m1, m2, ch, m32);
             };
-            if constexpr (DB) {
+            if (!DB && fast) {
+                const uint32_t one = m32 >> 5, neg1 = 0u - one;
+                uint32_t old[kNS];
+#pragma unroll
+                for (int s4 = 0; s4 < kNS; ++s4) old[s4] = m1[s4];
+                auto chunk = [&](auto cc_tag) {
+                    constexpr int CC = decltype(cc_tag)::value;
+                    uint32_t r[32];
+                    tmem_ld32(tmem + lane_base + uint32_t(CC * 32), r);
+                    tmem_wait_ld();
+                    tmem_regs_ready(r);
+                    top2_pairs_fast<CC, 0>(r, m1, m2, m32, one, neg1);
+                };
+                chunk(std::integral_constant<int, 0>{});
+                chunk(std::integral_constant<int, 1>{});
+                if (w == 128) {
+                    chunk(std::integral_constant<int, 2>{});
+                    chunk(std::integral_constant<int, 3>{});
+                }
+#pragma unroll
+                for (int s4 = 0; s4 < kNS; ++s4) ch[s4] = (m1[s4] != old[s4]) ? p0 : ch[s4];
+            } else if constexpr (DB) {
                 // two register buffers: the next 32 columns load from TMEM
                 // while the current ones are reduced (wide tables, where TMEM
                 // already limits the CTAs per SM to two; the extra registers
@@ -599,7 +665,8 @@ __global__ void __launch_bounds__(kRows, 1) umma_screen_kernel(NearestArgs a, ui
         }
         uint64_t K1;
         uint32_t V2;
-        top2_merge(m1, m2, ch, K1, V2);
+        if (fast) top2_merge_fast(m1, m2, ch, K1, V2);
+        else top2_merge(m1, m2, ch, K1, V2);
         fence_before();
         if (valid) {
             const uint32_t idx = uint32_t(K1);
@@ -914,7 +981,11 @@ void launch_umma(pqg_ctx* ctx, const NearestArgs& a) {
             per_b = p;
         }
     }
-    launch(ctx, "nearest_tc", kern, dim3(unsigned(per_b * a.B)), dim3(kRows), smem, a, n_pad, cols, 32u, n_mma);
+    // r2h unrolled fast epilogue (A/B switch PQG_UMMA_FAST=0)
+    const char* fe = std::getenv("PQG_UMMA_FAST");
+    const uint32_t allow_fast = (fe && fe[0] == '0') ? 0u : 1u;
+    launch(ctx, "nearest_tc", kern, dim3(unsigned(per_b * a.B)), dim3(kRows), smem, a, n_pad, cols, 32u, n_mma,
+           allow_fast);
 }
 
 }  // namespace
