@@ -471,7 +471,7 @@ def run_ours(args, rank, world, local):
     probe = C.c_double()
     L.check(lib.pqg_fp32_probe(ctx.h, C.byref(probe)), "fp32_probe")
     fp32_peak = float(probe.value)
-    traffic = ncu_traffic("prof_enc_r2")
+    traffic = ncu_traffic("prof_enc_r2h")
     tc_bf16 = float(peaks.get("bf16_tflops", 1590.0))
     psrc_tc = src
     tc_peak = tc_bf16 / 2.0 / 3.0
